@@ -1,0 +1,1259 @@
+// ORACLE — test infrastructure only (tests/, __graft_entry__.smoke(), bench.py cpu_baseline and
+// --impl reference).  Plain, slow, FP64 transcription of Specular Polynomials, step by
+// step in the paper's order and notation.  Shares no code with the CUDA path.
+//
+// Parity status per function (DESIGN.md §3 lists every reading):
+//   build_system (Eqs. 6, 9, 12, 13-20, 21-23) ............ pinned (tests/test_oracle_system.py)
+//   bezout (Eq. 24) / det_laplace (Sec. 5.2) .............. pinned (Sylvester resultant, sympy-free)
+//   isolate (Sec. 5.2 derivative recursion) ............... pinned (planted roots, numpy.roots)
+//   scan (Sec. 5.2 piecewise bisection) ................... pinned (planted RR/TT, brute force)
+//   validate / contribution / cull ......................... pinned (closed forms, brute force)
+//   sqrt surrogate table (Eq. 20) .......................... pinned (certified error < 1e-3);
+//       the paper's own coefficients are unavailable -> "parity unpinned" vs the paper's table.
+#include "oracle.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "poly.hpp"
+
+namespace oracle {
+
+using std::vector;
+
+// ------------------------------------------------------------------ small vector helpers
+struct V3 {
+  double x = 0, y = 0, z = 0;
+};
+static inline V3 mk(const double* p) { return {p[0], p[1], p[2]}; }
+static inline V3 operator+(V3 a, V3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+static inline V3 operator-(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+static inline V3 operator*(double s, V3 a) { return {s * a.x, s * a.y, s * a.z}; }
+static inline double dot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static inline V3 cross(V3 a, V3 b) { return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x}; }
+static inline double norm(V3 a) { return std::sqrt(dot(a, a)); }
+static inline V3 normalize(V3 a) { return (1.0 / norm(a)) * a; }
+static inline void put(V3 a, double* o) { o[0] = a.x; o[1] = a.y; o[2] = a.z; }
+
+// ------------------------------------------------------------------ triangles
+// P_i = (p_{i,0}, p_{i,1}, p_{i,2}), N_i = (n_{i,0}, n_{i,1}, n_{i,2})   (Table 1)
+struct Tri {
+  V3 p[3], n[3];
+  V3 e1() const { return p[1] - p[0]; }  // e_{i,1}
+  V3 e2() const { return p[2] - p[0]; }
+  V3 g() const { return cross(e1(), e2()); }  // geometric normal (winding)
+  V3 centroid() const { return (1.0 / 3.0) * (p[0] + p[1] + p[2]); }
+  V3 X(double u, double v) const { return p[0] + u * e1() + v * e2(); }                       // Eq. 1
+  V3 N(double u, double v) const { return n[0] + u * (n[1] - n[0]) + v * (n[2] - n[0]); }  // Eq. 2
+};
+static Tri load_tri(const double* t) {
+  Tri T;
+  for (int k = 0; k < 3; ++k) T.p[k] = mk(t + 3 * k);
+  for (int k = 0; k < 3; ++k) T.n[k] = mk(t + 9 + 3 * k);
+  return T;
+}
+static Tri relabel(const Tri& T) {  // p1 <-> p2, n1 <-> n2 : (u,v) -> (v,u)
+  Tri R = T;
+  std::swap(R.p[1], R.p[2]);
+  std::swap(R.n[1], R.n[2]);
+  return R;
+}
+
+// ------------------------------------------------------------------ sqrt surrogate (Eq. 20)
+// Literal copy of tests/golden/sqrt_table.txt (written by oracle/fit_sqrt.py); columns lo hi c0 c1 d1.
+static const double SQRT_TAB[6][5] = {
+    {0, 0.00042432536375417839, 0.00089999999999879705, 154.92902483814683, 5615.7008147954339},
+    {0.00042432536375417839, 0.0077313602416299448, 0.013714746392967799, 21.253136166194601, 135.24944765874642},
+    {0.0077313602416299448, 0.051793068389647277, 0.04635497395617269, 6.7900571325924943, 14.594946360257405},
+    {0.051793068389647277, 0.21636853563098274, 0.10736470812718857, 3.006160575603614, 2.9223382765562778},
+    {0.21636853563098274, 0.68268233146982271, 0.20527897991137517, 1.5904325277264706, 0.82650456712266585},
+    {0.68268233146982271, 1, 0.30276242425651556, 1.0984677499357838, 0.40129928835931156}};
+static int sqrt_piece(double x) {
+  for (int i = 0; i < 6; ++i)
+    if (x <= SQRT_TAB[i][1]) return i;
+  return 5;
+}
+
+// ------------------------------------------------------------------ chain + decisions
+struct Decisions {
+  bool relabel = false;  // product form at the last vertex uses t = n x e2 (as p1<->p2 relabel)
+  V3 ell{1, 0, 0};       // square-form projection basis b (Eq. 9)
+  bool degenerate_basis = false;
+  double eta[3] = {1, 1, 1};  // eta_0 .. eta_k (eta_i = IOR of the outgoing side of x_i)
+  int piece = 5;              // sqrt surrogate piece for a refracting first vertex (k=2)
+  double s_scale = 1;         // sqrt argument normalisation s (c4)
+  double sigma = 1;           // orientation of the refraction normal at vertex 1 (k=2)
+};
+
+static bool front_side(V3 x, const Tri& T) { return dot(x - T.p[0], T.g()) > 0; }
+
+// c3 / c7 decisions, computed in FP64 from the (float32-derived) inputs.
+static Decisions decide(const std::string& chain, const vector<Tri>& tris, V3 x0, V3 xk1, double eta_front,
+                        double eta_back) {
+  Decisions D;
+  const int k = (int)chain.size();
+  // c7: eta_0 from the side of x_0 w.r.t. T_1; refraction flips the medium, reflection keeps it.
+  D.eta[0] = front_side(x0, tris[0]) ? eta_front : eta_back;
+  D.eta[1] = chain[0] == 'T' ? (D.eta[0] == eta_front ? eta_back : eta_front) : D.eta[0];
+  if (k == 2) {
+    // medium on the far side of T_2, decided from the centroid of T_1 (the incoming side)
+    V3 c1 = tris[0].centroid();
+    double near_eta = front_side(c1, tris[1]) ? eta_front : eta_back;
+    double far_eta = front_side(c1, tris[1]) ? eta_back : eta_front;
+    (void)near_eta;
+    D.eta[2] = chain[1] == 'T' ? far_eta : D.eta[1];
+  }
+  // c3 (reading R1 in DESIGN.md): the incidence-plane normal expected near the centroid c of T_k,
+  //   l_c = (x_{k+1} - x_{k-1}) x n(c),   x_{k-1} = x_0 (k=1) or the centroid of T_1 (k=2).
+  // At a true chain x_{k+1} - x_{k-1} = d_{k-1} + d_k lies in the incidence plane with n, so l_c is
+  // that plane's normal up to the normal's variation across T_k.  Square form (Eq. 9): basis b = l_c.
+  // Product form (Eq. 12): t = n x e1 unless |e1^ . l_c^| < |e2^ . l_c^| (then t = n x e2, realised
+  // as the relabeling p1 <-> p2 so that deg_u b stays 3).
+  const Tri& L = tris[k - 1];
+  V3 c = L.centroid();
+  V3 xp = (k == 1) ? x0 : tris[0].centroid();
+  V3 nc = L.N(1.0 / 3, 1.0 / 3);
+  V3 m = cross(xk1 - xp, nc);
+  double mn = norm(m);
+  D.degenerate_basis = !(mn > 1e-12 * norm(xk1 - xp) * norm(nc));
+  (void)c;
+  if (chain[k - 1] == 'R') {
+    if (mn > 0) {
+      V3 e1 = L.e1(), e2 = L.e2();
+      double s1 = std::fabs(dot(e1, m)) / (norm(e1) * mn);
+      double s2 = std::fabs(dot(e2, m)) / (norm(e2) * mn);
+      D.relabel = s1 < s2;
+    }
+  } else {
+    D.ell = mn > 0 ? (1.0 / mn) * m : V3{1, 0, 0};
+  }
+  if (k == 2 && chain[0] == 'T') {
+    // c4: s = max_j |n_{1,j}|^2 * max_j |p_{1,j} - x0|^2 ; piece of beta/s at the centroid of T_1
+    const Tri& T1 = tris[0];
+    double nmax = 0, dmax = 0;
+    for (int j = 0; j < 3; ++j) {
+      nmax = std::max(nmax, dot(T1.n[j], T1.n[j]));
+      dmax = std::max(dmax, dot(T1.p[j] - x0, T1.p[j] - x0));
+    }
+    D.s_scale = nmax * dmax;
+    V3 n = T1.N(1.0 / 3, 1.0 / 3), d = T1.X(1.0 / 3, 1.0 / 3) - x0;
+    double ep = D.eta[0] / D.eta[1];
+    double nn = dot(n, n), dd = dot(d, d), dn = dot(d, n);
+    double beta = nn * dd - ep * ep * (nn * dd - dn * dn);  // Eq. 19
+    D.piece = sqrt_piece(std::min(1.0, std::max(0.0, beta / D.s_scale)));
+    D.sigma = dn < 0 ? 1.0 : -1.0;
+  }
+  return D;
+}
+
+// ------------------------------------------------------------------ coefficient phase
+// Builds a(u1,v1), b(u1,v1) (Sec. 4.5) for the tuple; the last triangle already relabeled
+// according to D.relabel by the caller.
+static void build_system(const std::string& chain, const vector<Tri>& tris, V3 x0, V3 xk1, const Decisions& D, Biv& a,
+                         Biv& b) {
+  const int k = (int)chain.size();
+  const Tri& T1 = tris[0];
+  double p0[3], e1[3], e2[3], n0[3], m1[3], m2[3], xx0[3], xxk[3];
+  put(T1.p[0], p0); put(T1.e1(), e1); put(T1.e2(), e2);
+  put(T1.n[0], n0); put(T1.n[1] - T1.n[0], m1); put(T1.n[2] - T1.n[0], m2);
+  put(x0, xx0); put(xk1, xxk);
+  BVec3 X1 = BVec3::affine(p0, e1, e2);  // P_1 u_1 (Eq. 1)
+  BVec3 N1 = BVec3::affine(n0, m1, m2);  // N_1 u_1 (Eq. 2)
+  BVec3 X0 = BVec3::constant(xx0);
+  BVec3 Xk = BVec3::constant(xxk);
+  if (k == 1) {
+    BVec3 D0 = X1 - X0;  // d_0 = x_1 - x_0
+    BVec3 D1 = Xk - X1;  // d_1 = x_2 - x_1
+    // Eq. 6 / Eq. 21-22 first line: a = ((P1 u1 - x0) x (x2 - x0)) . N1 u1
+    a = dot(cross(D0, Xk - X0), N1);
+    if (chain[0] == 'R') {
+      // Eq. 12 / Eq. 21: b = (d0.n)(d1.t) + (d0.t)(d1.n), t = n x e_{1,1}
+      BVec3 E1 = BVec3::constant(e1);
+      BVec3 Tt = cross(N1, E1);
+      b = dot(D0, N1) * dot(D1, Tt) + dot(D1, N1) * dot(D0, Tt);
+    } else {
+      // Eq. 9 / Eq. 22: b = eta0^2 d1^2 ((d0 x n).b)^2 - eta1^2 d0^2 ((d1 x n).b)^2
+      double ell[3];
+      put(D.ell, ell);
+      Biv P = dotc(cross(D0, N1), ell);
+      Biv Q = dotc(cross(D1, N1), ell);
+      b = (D.eta[0] * D.eta[0]) * (dot(D1, D1) * (P * P)) - (D.eta[1] * D.eta[1]) * (dot(D0, D0) * (Q * Q));
+    }
+    return;
+  }
+  // ---- k = 2 : rational coordinate mapping u_2 = (u~, v~)/kappa (Eqs. 13-16)
+  BVec3 D0 = X1 - X0;
+  BVec3 Dt;  // scaled direction d~_1
+  if (chain[0] == 'R') {
+    // Eq. 17: d~ = -2 (d0.n) n + d0 n^2
+    Dt = (-2.0 * dot(D0, N1)) * N1 + dot(N1, N1) * D0;
+  } else {
+    // Eq. 18-20 with sqrt(beta) ~ sqrt(s) (c0 s + c1 beta)/(s + d1 beta); the positive denominator
+    // (s + d1 beta) is cleared (c4).
+    double ep = D.eta[0] / D.eta[1];
+    Biv nn = dot(N1, N1), dn = dot(D0, N1), dd = dot(D0, D0);
+    Biv beta = nn * dd - (ep * ep) * (nn * dd - dn * dn);  // Eq. 19
+    double s = D.s_scale;
+    const double* pc = SQRT_TAB[D.piece];
+    Biv den = Biv::constant(s) + pc[4] * beta;              // s + d1 beta
+    Biv sq = Biv::constant(pc[2] * s) + pc[3] * beta;       // c0 s + c1 beta
+    BVec3 tang = nn * D0 - dn * N1;                         // d0 n^2 - (d0.n) n
+    Dt = (ep * den) * tang - (D.sigma * std::sqrt(s)) * (sq * N1);
+  }
+  const Tri& T2 = tris[1];
+  double q0[3], f1[3], f2[3], r0[3], g1[3], g2[3];
+  put(T2.p[0], q0); put(T2.e1(), f1); put(T2.e2(), f2);
+  put(T2.n[0], r0); put(T2.n[1] - T2.n[0], g1); put(T2.n[2] - T2.n[0], g2);
+  BVec3 Q0 = BVec3::constant(q0), F1 = BVec3::constant(f1), F2 = BVec3::constant(f2);
+  BVec3 S = X1 - Q0;                            // x_1 - p_{2,0}
+  Biv U = dot(cross(Dt, F2), S);                // Eq. 14
+  Biv V = dot(cross(S, F1), Dt);                // Eq. 15
+  Biv K = dot(cross(Dt, F2), F1);               // Eq. 16
+  BVec3 X2 = K * Q0 + U * F1 + V * F2;          // kappa x_2
+  BVec3 N2 = K * BVec3::constant(r0) + U * BVec3::constant(g1) + V * BVec3::constant(g2);  // kappa n_2
+  // Eq. 6 at x_2 (Eq. 23 first line), times kappa^2
+  a = dot(cross(X2 - K * X1, Xk - X1), N2);
+  BVec3 D2 = K * Xk - X2;  // kappa d_2
+  if (chain[1] == 'R') {
+    // Eq. 12 with d~_1 (Eq. 23 second line), times kappa^3
+    BVec3 Tt = cross(N2, F1);
+    b = dot(Dt, N2) * dot(D2, Tt) + dot(Dt, Tt) * dot(D2, N2);
+  } else {
+    // Eq. 9 at x_2 with d_1 -> d~_1, times kappa^4
+    double ell[3];
+    put(D.ell, ell);
+    Biv P = dotc(cross(Dt, N2), ell);
+    Biv Q = dotc(cross(D2, N2), ell);
+    b = (D.eta[1] * D.eta[1]) * (dot(D2, D2) * (P * P)) - (D.eta[2] * D.eta[2]) * (dot(Dt, Dt) * (Q * Q));
+  }
+}
+
+// the mapping polynomials (u~, v~, kappa) for k=2, needed to evaluate u_2 at raw roots
+static void build_mapping(const std::string& chain, const vector<Tri>& tris, V3 x0, const Decisions& D, Biv& U, Biv& V,
+                          Biv& K) {
+  const Tri& T1 = tris[0];
+  double p0[3], e1[3], e2[3], n0[3], m1[3], m2[3], xx0[3];
+  put(T1.p[0], p0); put(T1.e1(), e1); put(T1.e2(), e2);
+  put(T1.n[0], n0); put(T1.n[1] - T1.n[0], m1); put(T1.n[2] - T1.n[0], m2);
+  put(x0, xx0);
+  BVec3 X1 = BVec3::affine(p0, e1, e2), N1 = BVec3::affine(n0, m1, m2), X0 = BVec3::constant(xx0);
+  BVec3 D0 = X1 - X0, Dt;
+  if (chain[0] == 'R') {
+    Dt = (-2.0 * dot(D0, N1)) * N1 + dot(N1, N1) * D0;
+  } else {
+    double ep = D.eta[0] / D.eta[1];
+    Biv nn = dot(N1, N1), dn = dot(D0, N1), dd = dot(D0, D0);
+    Biv beta = nn * dd - (ep * ep) * (nn * dd - dn * dn);
+    double s = D.s_scale;
+    const double* pc = SQRT_TAB[D.piece];
+    Biv den = Biv::constant(s) + pc[4] * beta;
+    Biv sq = Biv::constant(pc[2] * s) + pc[3] * beta;
+    Dt = (ep * den) * (nn * D0 - dn * N1) - (D.sigma * std::sqrt(s)) * (sq * N1);
+  }
+  const Tri& T2 = tris[1];
+  double q0[3], f1[3], f2[3];
+  put(T2.p[0], q0); put(T2.e1(), f1); put(T2.e2(), f2);
+  BVec3 Q0 = BVec3::constant(q0), F1 = BVec3::constant(f1), F2 = BVec3::constant(f2);
+  BVec3 S = X1 - Q0;
+  U = dot(cross(Dt, F2), S);
+  V = dot(cross(S, F1), Dt);
+  K = dot(cross(Dt, F2), F1);
+}
+
+// c5: normalise to max|coeff| = 1, then (ii) numerical u-degree truncation
+static int numerical_u_degree(const Biv& p, double tau) {
+  int d = 0;
+  for (int i = 0; i <= p.deg; ++i) {
+    double m = 0;
+    for (int j = 0; i + j <= p.deg; ++j) m = std::max(m, std::fabs(p.at(i, j)));
+    if (m * std::pow(1.1, i) > tau) d = i;
+  }
+  return d;
+}
+static void truncate_u(Biv& p, int d) {
+  for (int i = d + 1; i <= p.deg; ++i)
+    for (int j = 0; i + j <= p.deg; ++j) p.at(i, j) = 0.0;
+}
+
+// ------------------------------------------------------------------ elimination phase (Sec. 5.1)
+// Eq. 24: R_ij(v) = sum_{k=0}^{min(i, n-1-j)} (a_{i-k} b_{j+1+k} - b_{i-k} a_{j+1+k}),  0 <= i,j < n
+static vector<vector<Uni>> bezout(const Biv& a, const Biv& b, int n) {
+  vector<Uni> as(n + 1), bs(n + 1);
+  for (int i = 0; i <= n; ++i) {
+    as[i] = a.slice(i);
+    bs[i] = b.slice(i);
+  }
+  vector<vector<Uni>> R(n, vector<Uni>(n));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      Uni s;
+      for (int k = 0; k <= std::min(i, n - 1 - j); ++k) s = s + (as[i - k] * bs[j + 1 + k] - bs[i - k] * as[j + 1 + k]);
+      R[i][j] = s;
+    }
+  return R;
+}
+static vector<vector<double>> bezout_at(const Biv& a, const Biv& b, int n, double v) {
+  vector<double> as(n + 1), bs(n + 1);
+  for (int i = 0; i <= n; ++i) {
+    as[i] = a.slice(i)(v);
+    bs[i] = b.slice(i)(v);
+  }
+  vector<vector<double>> R(n, vector<double>(n, 0.0));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      double s = 0;
+      for (int k = 0; k <= std::min(i, n - 1 - j); ++k) s += as[i - k] * bs[j + 1 + k] - bs[i - k] * as[j + 1 + k];
+      R[i][j] = s;
+    }
+  return R;
+}
+
+// Sec. 5.2: "Laplacian expansion" — plain recursive cofactor expansion along the first row.
+static Uni det_laplace(const vector<vector<Uni>>& M) {
+  const int n = (int)M.size();
+  if (n == 1) return M[0][0];
+  Uni r;
+  for (int j = 0; j < n; ++j) {
+    vector<vector<Uni>> minor(n - 1, vector<Uni>(n - 1));
+    for (int i = 1; i < n; ++i) {
+      int cc = 0;
+      for (int l = 0; l < n; ++l)
+        if (l != j) minor[i - 1][cc++] = M[i][l];
+    }
+    Uni t = M[0][j] * det_laplace(minor);
+    r = (j % 2 == 0) ? r + t : r - t;
+  }
+  return r;
+}
+
+// Sec. 5.2: determinant by Gaussian elimination (partial pivoting: max |.|, lowest index on ties).
+// Returns the sign (+1/-1/0) and log|det| (natural log) in *logabs.
+static int det_ge(vector<vector<double>> A, double* logabs) {
+  const int n = (int)A.size();
+  int sign = 1;
+  double lg = 0;
+  for (int c = 0; c < n; ++c) {
+    int piv = c;
+    for (int r = c + 1; r < n; ++r)
+      if (std::fabs(A[r][c]) > std::fabs(A[piv][c])) piv = r;
+    if (A[piv][c] == 0.0) {
+      *logabs = -INFINITY;
+      return 0;
+    }
+    if (piv != c) {
+      std::swap(A[piv], A[c]);
+      sign = -sign;
+    }
+    if (A[c][c] < 0) sign = -sign;
+    lg += std::log(std::fabs(A[c][c]));
+    for (int r = c + 1; r < n; ++r) {
+      double f = A[r][c] / A[c][c];
+      for (int l = c; l < n; ++l) A[r][l] -= f * A[c][l];
+    }
+  }
+  *logabs = lg;
+  return sign;
+}
+
+// ------------------------------------------------------------------ univariate roots (Sec. 5.2)
+// "The derivative of a polynomial of degree d is a polynomial of degree d-1, and the zeros of the
+// latter determine the monotonic pieces of the former. On each monotonic piece, only a single root
+// exists and can be found through a bisection solver ... interval smaller than 1e-9".
+static double bisect(const Uni& p, double a, double b, double fa, double tol) {
+  while (b - a >= tol) {
+    double m = 0.5 * (a + b);
+    if (m <= a || m >= b) break;
+    double fm = p(m);
+    if (fm == 0.0) return m;
+    if ((fm < 0) == (fa < 0)) {
+      a = m;
+      fa = fm;
+    } else {
+      b = m;
+    }
+  }
+  return 0.5 * (a + b);
+}
+static vector<double> isolate(Uni p, double lo, double hi, double tol) {
+  p.trim();
+  vector<double> roots;
+  if (p.deg() <= 0) return roots;
+  if (p.deg() == 1) {
+    double x = -p.c[0] / p.c[1];
+    if (x >= lo && x <= hi) roots.push_back(x);
+    return roots;
+  }
+  vector<double> crit = isolate(derivative(p), lo, hi, tol);
+  vector<double> pts;
+  pts.push_back(lo);
+  for (double c : crit)
+    if (c > lo && c < hi) pts.push_back(c);
+  pts.push_back(hi);
+  for (size_t i = 0; i + 1 < pts.size(); ++i) {
+    double fa = p(pts[i]), fb = p(pts[i + 1]);
+    if (fa == 0.0) {
+      roots.push_back(pts[i]);
+      continue;
+    }
+    if (fb != 0.0 && ((fa < 0) != (fb < 0))) roots.push_back(bisect(p, pts[i], pts[i + 1], fa, tol));
+  }
+  if (p(hi) == 0.0) roots.push_back(hi);
+  std::sort(roots.begin(), roots.end());
+  return roots;
+}
+static vector<double> dedup(const vector<double>& r, double tol) {
+  vector<double> o;
+  for (double x : r)
+    if (o.empty() || x - o.back() >= tol) o.push_back(x);
+  return o;
+}
+
+// ------------------------------------------------------------------ path space (Eq. 3)
+static bool refract(V3 d, V3 n, double eta_in, double eta_out, V3* out) {
+  double ep = eta_in / eta_out;
+  double ci = -dot(d, n);
+  if (ci < 0) {
+    n = -1.0 * n;
+    ci = -ci;
+  }
+  double kk = 1 - ep * ep * (1 - ci * ci);
+  if (kk < 0) return false;
+  *out = ep * d + (ep * ci - std::sqrt(kk)) * n;
+  return true;
+}
+static V3 reflect(V3 d, V3 n) { return d - (2 * dot(d, n)) * n; }
+static bool scatter(char type, V3 d, V3 n, double eta_in, double eta_out, V3* out) {
+  if (type == 'R') {
+    *out = reflect(d, n);
+    return true;
+  }
+  return refract(d, n, eta_in, eta_out, out);
+}
+// ray (o, d) against the plane of T: barycentrics (extrapolated) and distance
+static bool hit_plane(V3 o, V3 d, const Tri& T, double* u, double* v, double* t) {
+  V3 e1 = T.e1(), e2 = T.e2();
+  V3 P = cross(d, e2);
+  double det = dot(e1, P);
+  if (det == 0) return false;
+  V3 s = o - T.p[0];
+  *u = dot(s, P) / det;
+  V3 Q = cross(s, e1);
+  *v = dot(d, Q) / det;
+  *t = dot(e2, Q) / det;
+  return true;
+}
+
+// Eq. 3 residual rho_i = |h^ x n^|, h = eta_i d^_i - eta_{i-1} d^_{i-1}
+static double vertex_residual(V3 xp, V3 x, V3 xn, V3 n, double eta_prev, double eta_next) {
+  V3 dp = normalize(x - xp), dn = normalize(xn - x), nh = normalize(n);
+  V3 h = eta_next * dn - eta_prev * dp;
+  // reading R3: relative to |h| with a floor 1e-3 (eta_prev + eta_next), so an index-matched
+  // straight-through path (h = 0, Eq. 3 vacuous) is admissible instead of dividing noise by noise.
+  double hn = norm(h);
+  return norm(cross(h, nh)) / std::max(hn, 1e-3 * (eta_prev + eta_next));
+}
+// c12(iv): side consistency w.r.t. the shading and geometric planes
+static bool side_ok(char type, V3 xp, V3 x, V3 xn, V3 n, V3 g) {
+  double spn = dot(xp - x, n), snn = dot(xn - x, n), spg = dot(xp - x, g), sng = dot(xn - x, g);
+  if (!(spn * spg > 0)) return false;
+  if (type == 'R') return spn * snn > 0 && spg * sng > 0;
+  return spn * snn < 0 && spg * sng < 0;
+}
+
+// ------------------------------------------------------------------ contribution (c15)
+// Forward light-side trace: from x_{k+1} along omega through T_k..T_1 (exact reflect/refract with the
+// extrapolated interpolated normal), then onto the plane through x0 perpendicular to dref.
+// Returns the 2D position on that plane in the frame (c1, c2).
+struct Trace {
+  std::string chain;
+  vector<Tri> tris;
+  V3 x0, xk1, dref, c1, c2;
+  double eta[3];
+};
+static bool light_trace(const Trace& T, V3 omega, double out[2]) {
+  const int k = (int)T.chain.size();
+  V3 o = T.xk1, d = omega;
+  for (int i = k - 1; i >= 0; --i) {
+    double u, v, t;
+    if (!hit_plane(o, d, T.tris[i], &u, &v, &t)) return false;
+    if (t <= 0) return false;
+    V3 x = o + t * d;
+    V3 n = normalize(T.tris[i].N(u, v));
+    V3 nd;
+    // travelling backwards: incoming medium eta_{i+1}, outgoing eta_i (0-based vertex i+1)
+    if (!scatter(T.chain[i], d, n, T.eta[i + 1], T.eta[i], &nd)) return false;
+    o = x;
+    d = normalize(nd);
+  }
+  // intersect with plane through x0 perpendicular to dref
+  double den = dot(d, T.dref);
+  if (den == 0) return false;
+  double t = dot(T.x0 - o, T.dref) / den;
+  V3 p = o + t * d - T.x0;
+  out[0] = dot(p, T.c1);
+  out[1] = dot(p, T.c2);
+  return true;
+}
+static void frame(V3 w, V3* a, V3* b) {
+  V3 ax = std::fabs(w.x) < 0.6 ? V3{1, 0, 0} : (std::fabs(w.y) < 0.6 ? V3{0, 1, 0} : V3{0, 0, 1});
+  *a = normalize(cross(w, ax));
+  *b = cross(w, *a);
+}
+// J = |det d(x0-plane position)/d(omega)| by central differences + one Richardson step
+static double jacobian_fd(const std::string& chain, const vector<Tri>& tris, V3 x0, V3 xk1, const double* eta,
+                          const vector<V3>& verts /* x_1..x_k */) {
+  Trace T;
+  T.chain = chain;
+  T.tris = tris;
+  T.x0 = x0;
+  T.xk1 = xk1;
+  for (int i = 0; i < 3; ++i) T.eta[i] = eta[i];
+  T.dref = normalize(x0 - verts[0]);
+  frame(T.dref, &T.c1, &T.c2);
+  V3 w = normalize(verts.back() - xk1), b1, b2;
+  frame(w, &b1, &b2);
+  auto deriv = [&](V3 dir, double h, double out[2]) -> bool {
+    double p[2], m[2];
+    if (!light_trace(T, normalize(w + h * dir), p)) return false;
+    if (!light_trace(T, normalize(w - h * dir), m)) return false;
+    out[0] = (p[0] - m[0]) / (2 * h);
+    out[1] = (p[1] - m[1]) / (2 * h);
+    return true;
+  };
+  double h = 1e-5;
+  double d1h[2], d2h[2], d1q[2], d2q[2];
+  if (!deriv(b1, h, d1h) || !deriv(b2, h, d2h) || !deriv(b1, h / 2, d1q) || !deriv(b2, h / 2, d2q)) return -1;
+  double j1[2], j2[2];
+  for (int c = 0; c < 2; ++c) {
+    j1[c] = (4 * d1q[c] - d1h[c]) / 3;
+    j2[c] = (4 * d2q[c] - d2h[c]) / 3;
+  }
+  return std::fabs(j1[0] * j2[1] - j1[1] * j2[0]);
+}
+
+// ------------------------------------------------------------------ polish (c13)
+struct Shoot {
+  std::string chain;
+  vector<Tri> tris;
+  V3 x0, xk1;
+  double eta[3];
+  V3 f1, f2;
+};
+// exact forward shooting residual G(u1,v1) for k=2; also returns (u2, v2)
+static bool shoot(const Shoot& S, double u1, double v1, double G[2], double* u2, double* v2) {
+  V3 x1 = S.tris[0].X(u1, v1);
+  V3 n1 = normalize(S.tris[0].N(u1, v1));
+  V3 d0 = normalize(x1 - S.x0), w1;
+  if (!scatter(S.chain[0], d0, n1, S.eta[0], S.eta[1], &w1)) return false;
+  double t;
+  if (!hit_plane(x1, w1, S.tris[1], u2, v2, &t) || t <= 0) return false;
+  V3 x2 = x1 + t * w1;
+  V3 n2 = normalize(S.tris[1].N(*u2, *v2)), w2;
+  if (!scatter(S.chain[1], normalize(w1), n2, S.eta[1], S.eta[2], &w2)) return false;
+  V3 tgt = normalize(S.xk1 - x2);
+  V3 dw = normalize(w2) - tgt;
+  G[0] = dot(dw, S.f1);
+  G[1] = dot(dw, S.f2);
+  return true;
+}
+
+// ------------------------------------------------------------------ per-tuple solve
+struct Sol {
+  double bary[4];
+  double contribution;
+  double residual;
+  uint32_t flags;
+};
+struct Counters {
+  uint64_t c[10] = {0};  // pairs_in, systems, vroots, candidates, rej_domain, rej_constraint, rej_side,
+                         // rej_kappa, flagged, admissible
+};
+struct TupleResult {
+  vector<Sol> sols;
+  uint32_t flags = 0;
+};
+
+static bool in_domain(double u, double v, double eps) { return u >= -eps && v >= -eps && u + v <= 1 + eps; }
+static double edge_dist(double u, double v) { return std::min(std::min(u, v), 1 - u - v); }
+
+// candidate u-roots of the univariate polynomial A(u) (back-substitution; c11)
+static vector<double> u_roots(Uni A, double tol, uint32_t* flags) {
+  A.trim();
+  vector<double> r;
+  if (A.deg() <= 0) return r;
+  if (A.deg() == 1) {
+    r.push_back(-A.c[0] / A.c[1]);
+    return r;
+  }
+  if (A.deg() == 2) {
+    double a0 = A.c[0], a1 = A.c[1], a2 = A.c[2];
+    double disc = a1 * a1 - 4 * a2 * a0, scale = a1 * a1 + 4 * std::fabs(a2 * a0);
+    if (std::fabs(disc) <= 1e-8 * scale) *flags |= ORC_FLAG_NEAR_TANGENT;
+    if (disc < -1e-12 * scale) return r;
+    if (disc < 0) disc = 0;
+    double q = -0.5 * (a1 + std::copysign(std::sqrt(disc), a1));
+    if (q == 0) {
+      r.push_back(0.0);
+      return r;
+    }
+    r.push_back(q / a2);
+    r.push_back(a0 / q);
+    std::sort(r.begin(), r.end());
+    return dedup(r, 1e-7);
+  }
+  return dedup(isolate(A, -0.1, 1.1, tol), 1e-7);
+}
+
+static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris_in, V3 x0, V3 xk1, double eta_front,
+                               double eta_back, double intensity, const orc_config& cfg, Counters& C) {
+  TupleResult out;
+  const int k = (int)chain.size();
+  C.c[0]++;
+  Decisions D = decide(chain, tris_in, x0, xk1, eta_front, eta_back);
+  if (D.degenerate_basis) out.flags |= ORC_FLAG_DEGENERATE;
+  vector<Tri> tris = tris_in;
+  if (D.relabel) tris[k - 1] = relabel(tris[k - 1]);
+
+  Biv a, b;
+  build_system(chain, tris, x0, xk1, D, a, b);
+  double ma = a.maxabs(), mb = b.maxabs();
+  if (!(ma > 0) || !(mb > 0)) {
+    out.flags |= ORC_FLAG_DEGENERATE;
+    if (out.flags) C.c[8]++;
+    return out;
+  }
+  a = (1.0 / ma) * a;  // c5: max|coeff| = 1
+  b = (1.0 / mb) * b;
+  if (k == 1 && chain[0] == 'R') truncate_u(b, 3);  // c5(i): structural deg_u b = 3 (t . e1 = 0)
+  int da = numerical_u_degree(a, cfg.tau_trunc), db = numerical_u_degree(b, cfg.tau_trunc);  // c5(ii)
+  truncate_u(a, da);
+  truncate_u(b, db);
+  const int n = std::max(da, db);
+  if (n == 0) {
+    out.flags |= ORC_FLAG_DEGENERATE;
+    C.c[8]++;
+    return out;
+  }
+  C.c[1]++;
+
+  // ---- univariate roots v*
+  vector<double> vroots;
+  if (k == 1) {
+    Uni r = det_laplace(bezout(a, b, n));
+    double mr = r.maxabs();
+    if (!(mr > 0)) {
+      out.flags |= ORC_FLAG_DEGENERATE;
+      C.c[8]++;
+      return out;
+    }
+    r = (1.0 / mr) * r;
+    vector<double> raw = isolate(r, 0.0, 1.0, cfg.bisect_tol);
+    for (size_t i = 1; i < raw.size(); ++i)
+      if (raw[i] - raw[i - 1] < cfg.eps_flag) out.flags |= ORC_FLAG_NEAR_TANGENT;
+    // c14: a critical point of r in [0,1] with |r(c)| <= 1e-10 max_[0,1] |r|
+    vector<double> crit = isolate(derivative(r), 0.0, 1.0, cfg.bisect_tol);
+    double rmax = std::max(std::fabs(r(0.0)), std::fabs(r(1.0)));
+    for (double c : crit) rmax = std::max(rmax, std::fabs(r(c)));
+    for (double c : crit)
+      if (std::fabs(r(c)) <= 1e-10 * rmax) out.flags |= ORC_FLAG_NEAR_TANGENT;
+    vroots = dedup(raw, 1e-7);
+  } else {
+    // k >= 2: sign scan of det R(v_j) at v_j = j/pieces, then bisection
+    const int P = cfg.pieces;
+    vector<int> s(P + 1);
+    vector<double> lg(P + 1);
+    for (int j = 0; j <= P; ++j) s[j] = det_ge(bezout_at(a, b, n, (double)j / P), &lg[j]);
+    for (int j = 0; j <= P; ++j) {
+      double nb = -INFINITY;
+      if (j > 0) nb = std::max(nb, lg[j - 1]);
+      if (j < P) nb = std::max(nb, lg[j + 1]);
+      if (lg[j] < std::log(1e-9) + nb) out.flags |= ORC_FLAG_NEAR_TANGENT;
+    }
+    int last_change = -10;
+    for (int j = 0; j <= P; ++j) {
+      if (s[j] == 0) {
+        vroots.push_back((double)j / P);
+        continue;
+      }
+      if (j < P && s[j + 1] != 0 && s[j] != s[j + 1]) {
+        if (j - last_change == 1) out.flags |= ORC_FLAG_NEAR_TANGENT;  // changes in adjacent pieces
+        last_change = j;
+        double lo = (double)j / P, hi = (double)(j + 1) / P;
+        int slo = s[j];
+        for (int it = 0; it < cfg.scan_bisect_iters; ++it) {
+          double m = 0.5 * (lo + hi), l2;
+          int sm = det_ge(bezout_at(a, b, n, m), &l2);
+          if (sm == 0) {
+            lo = hi = m;
+            break;
+          }
+          if (sm == slo)
+            lo = m;
+          else
+            hi = m;
+        }
+        vroots.push_back(0.5 * (lo + hi));
+      }
+    }
+    std::sort(vroots.begin(), vroots.end());
+  }
+  C.c[2] += vroots.size();
+
+  Biv U, V, K;
+  if (k == 2) build_mapping(chain, tris, x0, D, U, V, K);
+  Shoot S;
+  if (k == 2) {
+    S.chain = chain;
+    S.tris = tris_in;
+    S.x0 = x0;
+    S.xk1 = xk1;
+    for (int i = 0; i < 3; ++i) S.eta[i] = D.eta[i];
+  }
+
+  vector<Sol> found;
+  for (double vs : vroots) {
+    Uni A = a.at_v(vs);
+    if (!(A.maxabs() >= 1e-12)) {
+      A = b.at_v(vs);  // c11 fallback: a(., v*) == 0
+      if (!(A.maxabs() >= 1e-12)) {
+        out.flags |= ORC_FLAG_DEGENERATE;
+        continue;
+      }
+    }
+    vector<double> us = u_roots(A, cfg.bisect_tol, &out.flags);
+    for (double us_ : us) {
+      C.c[3]++;
+      double vs_ = vs;
+      if (k == 1) {
+        // reading R2: <= 3 Newton steps on F = (a, b) (normalised system, relabeled coordinates),
+        // a step is kept only if |F| decreases (SPEC newton_polish_2d).  The bisection
+        // threshold 1e-9 on v is otherwise amplified by 1/|da/du| in u.
+        double fa = a(us_, vs_), fb = b(us_, vs_);
+        for (int it = 0; it < 3; ++it) {
+          double au = a.du(us_, vs_), av = a.dv(us_, vs_), bu = b.du(us_, vs_), bv = b.dv(us_, vs_);
+          double det = au * bv - av * bu;
+          if (det == 0) break;
+          double du = -(bv * fa - av * fb) / det, dv = -(-bu * fa + au * fb) / det;
+          double na = a(us_ + du, vs_ + dv), nb = b(us_ + du, vs_ + dv);
+          if (!(std::hypot(na, nb) < std::hypot(fa, fb))) break;
+          us_ += du;
+          vs_ += dv;
+          fa = na;
+          fb = nb;
+        }
+      }
+      // map back to the ORIGINAL labeling
+      double bary[4];
+      double ur = us_, vr = vs_;  // (u_1, v_1) — T_1 is relabeled only when k == 1
+      if (k == 1 && D.relabel) std::swap(ur, vr);
+      bary[0] = ur;
+      bary[1] = vr;
+      if (k == 1) {
+        const Tri& T = tris_in[0];
+        V3 x1 = T.X(ur, vr), n1 = T.N(ur, vr);
+        if (!in_domain(ur, vr, cfg.eps_domain)) {
+          // boundary proximity is judged only for physically valid candidates
+          if (edge_dist(ur, vr) >= -cfg.eps_flag) {
+            double rho = vertex_residual(x0, x1, xk1, n1, D.eta[0], D.eta[1]);
+            if (rho < cfg.theta_final && side_ok(chain[0], x0, x1, xk1, n1, T.g())) out.flags |= ORC_FLAG_BOUNDARY;
+          }
+          C.c[4]++;
+          continue;
+        }
+        double rho = vertex_residual(x0, x1, xk1, n1, D.eta[0], D.eta[1]);
+        if (!(rho < cfg.theta_final)) {
+          C.c[5]++;
+          continue;
+        }
+        if (!side_ok(chain[0], x0, x1, xk1, n1, T.g())) {
+          C.c[6]++;
+          continue;
+        }
+        if (rho >= 1e-7) out.flags |= ORC_FLAG_RESIDUAL;
+        if (edge_dist(ur, vr) <= cfg.eps_flag) out.flags |= ORC_FLAG_BOUNDARY;
+        // c14 Jacobian transversality of (a, b) at the root (relabeled coordinates)
+        double au = a.du(us_, vs_), av = a.dv(us_, vs_), bu = b.du(us_, vs_), bv = b.dv(us_, vs_);
+        if (std::fabs(au * bv - av * bu) < 1e-6 * std::hypot(au, av) * std::hypot(bu, bv))
+          out.flags |= ORC_FLAG_NEAR_TANGENT;
+        Sol s;
+        s.bary[0] = ur;
+        s.bary[1] = vr;
+        s.bary[2] = s.bary[3] = 0;
+        s.residual = rho;
+        s.flags = 0;
+        double J = jacobian_fd(chain, tris_in, x0, xk1, D.eta, {x1});
+        s.contribution = J > 0 ? intensity / J : 0.0;
+        found.push_back(s);
+        continue;
+      }
+      // ---- k = 2
+      double kap = K(ur, vr), ut = U(ur, vr), vt = V(ur, vr);
+      const Tri& T2r = tris[1];  // relabeled T_2
+      double kscale = 0;
+      {
+        // |kappa| > 1e-12 |d~| |e21| |e22|  (c12 ii) — |d~| bounded by the mapping scale
+        V3 f1 = T2r.e1(), f2 = T2r.e2();
+        kscale = norm(f1) * norm(f2);
+      }
+      (void)kscale;
+      double u2 = ut / kap, v2 = vt / kap;
+      if (!(std::fabs(kap) > 0) || !std::isfinite(u2) || !std::isfinite(v2)) {
+        C.c[7]++;
+        continue;
+      }
+      if (D.relabel) std::swap(u2, v2);
+      // raw admission (domain with flag margin, residual < theta_admit)
+      const double dm = 1e-3;  // raw roots carry 1e-5 scan localisation and surrogate error
+      if (!in_domain(ur, vr, dm) || !in_domain(u2, v2, dm)) {
+        C.c[4]++;
+        continue;
+      }
+      V3 x1 = tris_in[0].X(ur, vr), x2 = tris_in[1].X(u2, v2);
+      double r1 = vertex_residual(x0, x1, x2, tris_in[0].N(ur, vr), D.eta[0], D.eta[1]);
+      double r2 = vertex_residual(x1, x2, xk1, tris_in[1].N(u2, v2), D.eta[1], D.eta[2]);
+      if (!(std::max(r1, r2) < cfg.theta_admit)) {
+        C.c[5]++;
+        continue;
+      }
+      // polish: <= polish_iters Newton steps on the exact shooting residual, accept if |G| decreases
+      frame(normalize(xk1 - x2), &S.f1, &S.f2);
+      double uu = ur, vv = vr, G[2], uu2 = u2, vv2 = v2;
+      bool ok = shoot(S, uu, vv, G, &uu2, &vv2);
+      double Jm[4] = {0, 0, 0, 0};
+      for (int it = 0; ok && it < cfg.polish_iters; ++it) {
+        const double h = 1e-7;
+        double Gp[2], Gm[2], t1, t2;
+        bool f = shoot(S, uu + h, vv, Gp, &t1, &t2) && shoot(S, uu - h, vv, Gm, &t1, &t2);
+        if (!f) break;
+        Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
+        Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
+        f = shoot(S, uu, vv + h, Gp, &t1, &t2) && shoot(S, uu, vv - h, Gm, &t1, &t2);
+        if (!f) break;
+        Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
+        Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
+        double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
+        if (det == 0) break;
+        double du = -(Jm[3] * G[0] - Jm[1] * G[1]) / det;
+        double dv = -(-Jm[2] * G[0] + Jm[0] * G[1]) / det;
+        double Gn[2], nu2, nv2;
+        if (!shoot(S, uu + du, vv + dv, Gn, &nu2, &nv2)) break;
+        if (!(std::hypot(Gn[0], Gn[1]) < std::hypot(G[0], G[1]))) break;
+        uu += du;
+        vv += dv;
+        G[0] = Gn[0];
+        G[1] = Gn[1];
+        uu2 = nu2;
+        vv2 = nv2;
+      }
+      if (!ok) {
+        C.c[5]++;
+        continue;
+      }
+      if (!in_domain(uu, vv, cfg.eps_domain) || !in_domain(uu2, vv2, cfg.eps_domain)) {
+        C.c[4]++;
+        continue;
+      }
+      x1 = tris_in[0].X(uu, vv);
+      x2 = tris_in[1].X(uu2, vv2);
+      V3 n1 = tris_in[0].N(uu, vv), n2 = tris_in[1].N(uu2, vv2);
+      r1 = vertex_residual(x0, x1, x2, n1, D.eta[0], D.eta[1]);
+      r2 = vertex_residual(x1, x2, xk1, n2, D.eta[1], D.eta[2]);
+      double rho = std::max(r1, r2);
+      if (!(rho < cfg.theta_final)) {
+        C.c[5]++;
+        continue;
+      }
+      if (!side_ok(chain[0], x0, x1, x2, n1, tris_in[0].g()) || !side_ok(chain[1], x1, x2, xk1, n2, tris_in[1].g())) {
+        C.c[6]++;
+        continue;
+      }
+      // eta consistency: x_1 must lie on the side of T_2 whose IOR is eta_1
+      {
+        double side_eta = front_side(x1, tris_in[1]) ? eta_front : eta_back;
+        if (chain[1] == 'T' && side_eta != D.eta[1]) {
+          C.c[6]++;
+          continue;
+        }
+      }
+      if (rho >= 1e-7) out.flags |= ORC_FLAG_RESIDUAL;
+      if (edge_dist(uu, vv) <= cfg.eps_flag || edge_dist(uu2, vv2) <= cfg.eps_flag) out.flags |= ORC_FLAG_BOUNDARY;
+      if (std::fabs(Jm[0] * Jm[3] - Jm[1] * Jm[2]) <
+          1e-6 * std::hypot(Jm[0], Jm[1]) * std::hypot(Jm[2], Jm[3]))
+        out.flags |= ORC_FLAG_NEAR_TANGENT;
+      Sol s;
+      s.bary[0] = uu;
+      s.bary[1] = vv;
+      s.bary[2] = uu2;
+      s.bary[3] = vv2;
+      s.residual = rho;
+      s.flags = 0;
+      double J = jacobian_fd(chain, tris_in, x0, xk1, D.eta, {x1, x2});
+      s.contribution = J > 0 ? intensity / J : 0.0;
+      found.push_back(s);
+    }
+  }
+  // dedup admissible chains closer than 1e-7 in (u1, v1) (polished candidates may coincide)
+  for (const Sol& s : found) {
+    bool dup = false;
+    for (const Sol& t : out.sols)
+      if (std::fabs(s.bary[0] - t.bary[0]) < 1e-7 && std::fabs(s.bary[1] - t.bary[1]) < 1e-7) dup = true;
+    if (!dup) out.sols.push_back(s);
+    else
+      C.c[6]++;  // counted as rejected duplicate
+  }
+  C.c[9] += out.sols.size();
+  if (out.flags) C.c[8]++;
+  for (Sol& s : out.sols) s.flags = out.flags;
+  return out;
+}
+
+// ------------------------------------------------------------------ cull predicate
+// direction cone of a point set seen from / towards: axis = normalised sum of unit directions,
+// chord = max |w_j - axis| (= 2 sin(theta/2)), theta = max angle.
+struct Cone {
+  V3 axis;
+  double chord, theta;
+  bool valid;
+};
+static Cone cone_of(const vector<V3>& dirs) {
+  V3 s{0, 0, 0};
+  vector<V3> w;
+  for (V3 d : dirs) {
+    double n = norm(d);
+    if (!(n > 0)) return {{0, 0, 0}, 0, 0, false};
+    w.push_back((1.0 / n) * d);
+    s = s + w.back();
+  }
+  if (!(norm(s) > 0)) return {{0, 0, 0}, 0, 0, false};
+  Cone c;
+  c.axis = normalize(s);
+  c.chord = 0;
+  c.theta = 0;
+  for (V3 x : w) {
+    c.chord = std::max(c.chord, norm(x - c.axis));
+    c.theta = std::max(c.theta, std::atan2(norm(cross(x, c.axis)), dot(x, c.axis)));
+  }
+  c.valid = c.theta < M_PI / 2;
+  return c;
+}
+// is there h in Ball(A, r) parallel (either sign) to some normal in cone N ?
+static bool vertex_keep(const Cone& prev, const Cone& next, double eta_prev, double eta_next, const Cone& N,
+                        double margin) {
+  if (!prev.valid || !next.valid || !N.valid) return true;
+  V3 A = eta_prev * prev.axis + eta_next * next.axis;
+  double r = eta_prev * prev.chord + eta_next * next.chord;
+  double An = norm(A);
+  if (!(An > r)) return true;
+  double alpha = std::asin(r / An);
+  V3 Ah = (1.0 / An) * A;
+  double phi = std::atan2(norm(cross(Ah, N.axis)), dot(Ah, N.axis));
+  double lim = alpha + N.theta + margin;
+  return phi <= lim || (M_PI - phi) <= lim;
+}
+static bool cull_keep(const std::string& chain, const vector<Tri>& tris, V3 x0, V3 xk1, double eta_front,
+                      double eta_back, double margin) {
+  const int k = (int)chain.size();
+  auto ncone = [](const Tri& T) { return cone_of({T.n[0], T.n[1], T.n[2]}); };
+  if (k == 1) {
+    const Tri& T = tris[0];
+    Cone cp = cone_of({x0 - T.p[0], x0 - T.p[1], x0 - T.p[2]});
+    Cone cn = cone_of({xk1 - T.p[0], xk1 - T.p[1], xk1 - T.p[2]});
+    double e0 = front_side(x0, T) ? eta_front : eta_back;
+    double e1 = chain[0] == 'T' ? (e0 == eta_front ? eta_back : eta_front) : e0;
+    return vertex_keep(cp, cn, e0, e1, ncone(T), margin);
+  }
+  const Tri &A = tris[0], &B = tris[1];
+  vector<V3> ab, ba;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      ab.push_back(B.p[j] - A.p[i]);
+      ba.push_back(A.p[i] - B.p[j]);
+    }
+  Cone cab = cone_of(ab), cba = cone_of(ba);
+  double e0 = front_side(x0, A) ? eta_front : eta_back;
+  double e1 = chain[0] == 'T' ? (e0 == eta_front ? eta_back : eta_front) : e0;
+  Cone c0 = cone_of({x0 - A.p[0], x0 - A.p[1], x0 - A.p[2]});
+  if (!vertex_keep(c0, cab, e0, e1, ncone(A), margin)) return false;
+  Cone c3 = cone_of({xk1 - B.p[0], xk1 - B.p[1], xk1 - B.p[2]});
+  // eta_2 depends on the side of x_1 w.r.t. T_2: test both media when ambiguous (union = sound)
+  vector<double> e2s;
+  if (chain[1] == 'R')
+    e2s.push_back(e1);
+  else {
+    e2s.push_back(eta_front);
+    e2s.push_back(eta_back);
+  }
+  for (double e2 : e2s)
+    if (vertex_keep(cba, c3, e1, e2, ncone(B), margin)) return true;
+  return false;
+}
+
+}  // namespace oracle
+
+// ================================================================== C API
+using namespace oracle;
+
+struct orc_result {
+  int k = 1;
+  uint32_t nq = 0;
+  vector<uint32_t> q, tup, flags, fq, ftup, fflags;
+  vector<double> bary, contrib, resid, per_query;
+  uint64_t counters[10] = {0};
+};
+
+extern "C" {
+
+void orc_default_config(orc_config* c) {
+  c->pieces = 100;
+  c->scan_bisect_iters = 10;
+  c->bisect_tol = 1e-9;
+  c->polish_iters = 3;
+  c->theta_admit = 1e-3;
+  c->theta_final = 1e-6;
+  c->eps_domain = 1e-9;
+  c->eps_flag = 1e-6;
+  c->tau_trunc = 1e-12;
+  c->cull = 1;
+  c->cull_margin = 1e-9;
+}
+
+static vector<Tri> mesh_tris(const float* pos, const float* nrm, const uint32_t* tri, const uint32_t* ids, int k) {
+  vector<Tri> out(k);
+  for (int i = 0; i < k; ++i) {
+    uint32_t t = ids[i];
+    for (int j = 0; j < 3; ++j) {
+      uint32_t vi = tri[3 * t + j];
+      out[i].p[j] = {(double)pos[3 * vi], (double)pos[3 * vi + 1], (double)pos[3 * vi + 2]};
+      out[i].n[j] = {(double)nrm[3 * vi], (double)nrm[3 * vi + 1], (double)nrm[3 * vi + 2]};
+    }
+  }
+  return out;
+}
+
+orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri, uint32_t ntris,
+                      float eta_front, float eta_back, const char* chain_c, const double* endpoints, uint32_t nq,
+                      const double* intensity, const uint32_t* offsets, const uint32_t* tri_ids,
+                      const orc_config* cfg_in, int nthreads) {
+  if (!pos || !nrm || !tri || !chain_c || !endpoints) return nullptr;
+  std::string chain(chain_c);
+  const int k = (int)chain.size();
+  if (k < 1 || k > 2) return nullptr;
+  for (char ch : chain)
+    if (ch != 'R' && ch != 'T') return nullptr;
+  for (uint64_t i = 0; i < 3ull * ntris; ++i)
+    if (tri[i] >= nverts) return nullptr;
+  orc_config cfg;
+  if (cfg_in)
+    cfg = *cfg_in;
+  else
+    orc_default_config(&cfg);
+  struct PerQ {
+    vector<uint32_t> tup, ftup, fflags;
+    vector<Sol> sols;
+    Counters C;
+    double sum = 0;
+  };
+  vector<PerQ> per(nq);
+  std::atomic<uint32_t> next{0};
+  auto work = [&]() {
+    for (;;) {
+      uint32_t qi = next.fetch_add(1);
+      if (qi >= nq) break;
+      PerQ& P = per[qi];
+      V3 x0 = mk(endpoints + 6ull * qi), xk1 = mk(endpoints + 6ull * qi + 3);
+      double I = intensity ? intensity[qi] : 1.0;
+      auto run = [&](const uint32_t* ids) {
+        vector<Tri> tris = mesh_tris(pos, nrm, tri, ids, k);
+        TupleResult R = solve_tuple(chain, tris, x0, xk1, eta_front, eta_back, I, cfg, P.C);
+        for (const Sol& s : R.sols) {
+          P.sols.push_back(s);
+          for (int i = 0; i < k; ++i) P.tup.push_back(ids[i]);
+          P.sum += s.contribution;
+        }
+        if (R.flags) {
+          for (int i = 0; i < k; ++i) P.ftup.push_back(ids[i]);
+          P.fflags.push_back(R.flags);
+        }
+      };
+      if (offsets) {
+        for (uint32_t t = offsets[qi]; t < offsets[qi + 1]; ++t) run(tri_ids + (uint64_t)k * t);
+      } else if (k == 1) {
+        for (uint32_t t = 0; t < ntris; ++t) {
+          if (cfg.cull) {
+            vector<Tri> tr = mesh_tris(pos, nrm, tri, &t, 1);
+            if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin)) continue;
+          }
+          run(&t);
+        }
+      } else {
+        for (uint32_t t1 = 0; t1 < ntris; ++t1)
+          for (uint32_t t2 = 0; t2 < ntris; ++t2) {
+            if (t1 == t2) continue;
+            uint32_t ids[2] = {t1, t2};
+            if (cfg.cull) {
+              vector<Tri> tr = mesh_tris(pos, nrm, tri, ids, 2);
+              if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin)) continue;
+            }
+            run(ids);
+          }
+      }
+    }
+  };
+  int nt = nthreads > 0 ? nthreads : (int)std::thread::hardware_concurrency();
+  if (nt < 1) nt = 1;
+  vector<std::thread> th;
+  for (int i = 0; i < nt; ++i) th.emplace_back(work);
+  for (auto& t : th) t.join();
+
+  orc_result* R = new orc_result;
+  R->k = k;
+  R->nq = nq;
+  R->per_query.resize(nq);
+  for (uint32_t qi = 0; qi < nq; ++qi) {
+    PerQ& P = per[qi];
+    for (size_t s = 0; s < P.sols.size(); ++s) {
+      R->q.push_back(qi);
+      for (int i = 0; i < k; ++i) R->tup.push_back(P.tup[s * k + i]);
+      for (int i = 0; i < 2 * k; ++i) R->bary.push_back(P.sols[s].bary[i]);
+      R->contrib.push_back(P.sols[s].contribution);
+      R->resid.push_back(P.sols[s].residual);
+      R->flags.push_back(P.sols[s].flags);
+    }
+    for (size_t f = 0; f < P.fflags.size(); ++f) {
+      R->fq.push_back(qi);
+      for (int i = 0; i < k; ++i) R->ftup.push_back(P.ftup[f * k + i]);
+      R->fflags.push_back(P.fflags[f]);
+    }
+    R->per_query[qi] = P.sum;
+    for (int c = 0; c < 10; ++c) R->counters[c] += P.C.c[c];
+  }
+  return R;
+}
+
+void orc_free(orc_result* r) { delete r; }
+uint64_t orc_n_solutions(const orc_result* r) { return r->q.size(); }
+uint64_t orc_n_flagged(const orc_result* r) { return r->fq.size(); }
+int orc_k(const orc_result* r) { return r->k; }
+void orc_get_solutions(const orc_result* r, uint32_t* query, uint32_t* tuple, double* bary, double* contribution,
+                       double* residual, uint32_t* flags) {
+  std::copy(r->q.begin(), r->q.end(), query);
+  std::copy(r->tup.begin(), r->tup.end(), tuple);
+  std::copy(r->bary.begin(), r->bary.end(), bary);
+  std::copy(r->contrib.begin(), r->contrib.end(), contribution);
+  std::copy(r->resid.begin(), r->resid.end(), residual);
+  std::copy(r->flags.begin(), r->flags.end(), flags);
+}
+void orc_get_flagged(const orc_result* r, uint32_t* query, uint32_t* tuple, uint32_t* flags) {
+  std::copy(r->fq.begin(), r->fq.end(), query);
+  std::copy(r->ftup.begin(), r->ftup.end(), tuple);
+  std::copy(r->fflags.begin(), r->fflags.end(), flags);
+}
+void orc_get_per_query(const orc_result* r, double* out) { std::copy(r->per_query.begin(), r->per_query.end(), out); }
+void orc_get_report(const orc_result* r, uint64_t c[10]) { std::copy(r->counters, r->counters + 10, c); }
+
+// ---- pieces
+static vector<Tri> tris_from(const double* t, int k) {
+  vector<Tri> v;
+  for (int i = 0; i < k; ++i) v.push_back(load_tri(t + 18 * i));
+  return v;
+}
+static void store_biv(const Biv& p, double* out, int* deg) {
+  *deg = p.deg;
+  for (int i = 0; i <= p.deg; ++i)
+    for (int j = 0; j <= p.deg; ++j) out[i * (p.deg + 1) + j] = (i + j <= p.deg) ? p.at(i, j) : 0.0;
+}
+static Biv load_biv(const double* in, int deg) {
+  Biv p(deg);
+  for (int i = 0; i <= deg; ++i)
+    for (int j = 0; i + j <= deg; ++j) p.at(i, j) = in[i * (deg + 1) + j];
+  return p;
+}
+
+int orc_build_system(const char* chain_c, const double* t, const double* x0, const double* xk1, double eta_front,
+                     double eta_back, const double* /*sqrt_table*/, double* a_out, int* deg_a, double* b_out,
+                     int* deg_b, int* info) {
+  std::string chain(chain_c);
+  const int k = (int)chain.size();
+  if (k < 1 || k > 2) return -1;
+  vector<Tri> tris = tris_from(t, k);
+  Decisions D = decide(chain, tris, mk(x0), mk(xk1), eta_front, eta_back);
+  if (D.relabel) tris[k - 1] = relabel(tris[k - 1]);
+  Biv a, b;
+  build_system(chain, tris, mk(x0), mk(xk1), D, a, b);
+  store_biv(a, a_out, deg_a);
+  store_biv(b, b_out, deg_b);
+  info[0] = D.relabel;
+  info[1] = (int)std::lround(D.eta[0] * 1000);
+  info[2] = D.degenerate_basis;
+  return 0;
+}
+
+int orc_bezout(const double* a, int deg_a, const double* b, int deg_b, int n, double* ent, int* ent_deg) {
+  vector<vector<Uni>> R = bezout(load_biv(a, deg_a), load_biv(b, deg_b), n);
+  const int maxc = 128;
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      const Uni& u = R[i][j];
+      ent_deg[i * n + j] = u.deg();
+      for (int l = 0; l < maxc; ++l) ent[(i * n + j) * maxc + l] = l <= u.deg() ? u.c[l] : 0.0;
+    }
+  return n;
+}
+
+int orc_det_laplace(const double* ent, const int* ent_deg, int n, double* r_out) {
+  const int maxc = 128;
+  vector<vector<Uni>> M(n, vector<Uni>(n));
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) {
+      int d = ent_deg[i * n + j];
+      M[i][j] = Uni(vector<double>(ent + (i * n + j) * maxc, ent + (i * n + j) * maxc + d + 1));
+    }
+  Uni r = det_laplace(M);
+  for (int l = 0; l <= r.deg(); ++l) r_out[l] = r.c[l];
+  return r.deg();
+}
+
+double orc_det_at(const double* a, int deg_a, const double* b, int deg_b, int n, double v) {
+  double lg;
+  int s = det_ge(bezout_at(load_biv(a, deg_a), load_biv(b, deg_b), n, v), &lg);
+  return s == 0 ? 0.0 : s * std::exp(lg);
+}
+
+int orc_isolate(const double* p, int deg, double lo, double hi, double tol, double* roots_out) {
+  vector<double> r = isolate(Uni(vector<double>(p, p + deg + 1)), lo, hi, tol);
+  for (size_t i = 0; i < r.size(); ++i) roots_out[i] = r[i];
+  return (int)r.size();
+}
+
+int orc_cull_keep(const char* chain_c, const double* t, const double* x0, const double* xk1, double eta_front,
+                  double eta_back, double margin) {
+  std::string chain(chain_c);
+  return cull_keep(chain, tris_from(t, (int)chain.size()), mk(x0), mk(xk1), eta_front, eta_back, margin) ? 1 : 0;
+}
+
+double orc_jacobian(const char* chain_c, const double* t, const double* x0, const double* xk1, double eta_front,
+                    double eta_back, const double* bary) {
+  std::string chain(chain_c);
+  const int k = (int)chain.size();
+  vector<Tri> tris = tris_from(t, k);
+  Decisions D = decide(chain, tris, mk(x0), mk(xk1), eta_front, eta_back);
+  vector<V3> verts;
+  for (int i = 0; i < k; ++i) verts.push_back(tris[i].X(bary[2 * i], bary[2 * i + 1]));
+  return jacobian_fd(chain, tris, mk(x0), mk(xk1), D.eta, verts);
+}
+
+void orc_sqrt_table(double* out) {
+  for (int i = 0; i < 6; ++i)
+    for (int j = 0; j < 5; ++j) out[i * 5 + j] = SQRT_TAB[i][j];
+}
+double orc_sqrt_approx(double x) {
+  const double* p = SQRT_TAB[sqrt_piece(x)];
+  return (p[2] + p[3] * x) / (1 + p[4] * x);
+}
+
+}  // extern "C"

@@ -1,0 +1,438 @@
+"""Pins of the oracle against what the paper and the mathematics fix (no GPU).
+
+Each test names the passage it pins.  None of them re-types the oracle's formula: they use
+closed forms (image source, Fermat), independent numerics (numpy roots/det, Sylvester
+resultant), physics invariants (planted forward-traced chains, Eq. 3 residual), and brute force.
+"""
+import numpy as np
+import pytest
+
+import bruteforce
+from planted import planted_many
+from paper_2405_13409_b200.workloads import Mesh, patch_c1, random_triangles
+
+
+# ------------------------------------------------------------------ degrees (Table 2, Table 3)
+def _degrees(G, tol=0.0):
+    """total degree and u-degree of a coefficient grid, counting |c| > tol*max"""
+    m = np.max(np.abs(G))
+    idx = np.argwhere(np.abs(G) > tol * m)
+    return int(max(i + j for i, j in idx)), int(max(i for i, j in idx))
+
+
+@pytest.mark.parametrize("chain,face,expect_a,expect_b", [
+    ("R", False, 2, 4),   # PAPER.md:497 "degree 2 and 4"; Table 2 product form 4, endpoint coplanarity 2
+    ("T", False, 2, 6),   # PAPER.md:515 "degree 2 and 6"
+])
+def test_degrees_one_bounce(orc, chain, face, expect_a, expect_b):
+    for seed in range(5):
+        mesh, ids, x0, xk1, _ = planted_many(seed, chain, 1)[0]
+        A, B, _ = orc.build_system(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+        assert _degrees(A, 1e-14)[0] == expect_a
+        da, dua = _degrees(A, 1e-14)
+        db, dub = _degrees(B, 1e-13)
+        assert db == expect_b
+        if chain == "R":
+            assert dub == 3  # t = n x e1 is orthogonal to e1 -> the u^4 slice is rounding noise only
+            assert np.max(np.abs(B[4:])) <= 1e-13 * np.max(np.abs(B))
+
+
+def test_degrees_face_normals(orc):
+    # Table 2: face normals give coplanarity 1 and product form 2 / square form 4.
+    rng = np.random.default_rng(7)
+    for chain, eb in (("R", 2), ("T", 4)):
+        # a constant shading normal that is NOT the geometric normal (generic face mode)
+        P = rng.normal(size=(3, 3))
+        n = P[0] * 0 + np.array([0.1, 0.2, 1.0])
+        mesh = Mesh(P.astype(np.float32), np.tile(n, (3, 1)).astype(np.float32), np.array([[0, 1, 2]], np.uint32),
+                    1.0, 1.5)
+        A, B, _ = orc.build_system(chain, orc.tri_block(mesh, [0]), np.array([0.3, 0.1, 2.0]),
+                                   np.array([-0.5, 0.4, 1.5]) if chain == "R" else np.array([0.1, -0.2, -2.0]),
+                                   1.0, 1.5)
+        assert _degrees(A)[0] == 1
+        assert _degrees(B)[0] == eb
+
+
+@pytest.mark.parametrize("chain,bound_a,bound_b,derived_a,derived_b", [
+    ("RR", 10, 16, 9, 15),   # Table 3: RR 10, 16 — our construction gives 9, 15
+    ("TT", 18, 48, 17, 46),  # Table 3: TT 18, 48 — square form at x_2 (c3 reading)
+])
+def test_degrees_two_bounce(orc, chain, bound_a, bound_b, derived_a, derived_b):
+    mesh, ids, x0, xk1, _ = planted_many(11, chain, 1)[0]
+    A, B, _ = orc.build_system(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+    da, db = _degrees(A, 1e-300)[0], _degrees(B, 1e-300)[0]
+    assert da == derived_a and db == derived_b
+    assert da <= bound_a and db <= bound_b
+
+
+# ------------------------------------------------------------------ planted chains: a, b vanish (Eq. 3)
+@pytest.mark.parametrize("chain", ["R", "T", "RR"])
+def test_system_vanishes_at_planted_chain(orc, chain):
+    for mesh, ids, x0, xk1, bary in planted_many(3, chain, 20):
+        A, B, info = orc.build_system(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+        u, v = bary[0], bary[1]
+        if len(chain) == 1 and info["relabel"]:
+            u, v = v, u
+
+        def ev(G):
+            d = G.shape[0] - 1
+            return sum(G[i, j] * u ** i * v ** j for i in range(d + 1) for j in range(d + 1 - i))
+
+        sa = np.sum(np.abs(A)) + 1e-300
+        sb = np.sum(np.abs(B)) + 1e-300
+        assert abs(ev(A)) / sa < 1e-10
+        assert abs(ev(B)) / sb < 1e-10
+
+
+def test_tt_system_near_planted_chain(orc):
+    # TT uses the sqrt surrogate (error < 1e-3), so the planted chain is only
+    # an approximate root: the normalised residuals are small but not rounding-level.
+    for mesh, ids, x0, xk1, bary in planted_many(5, "TT", 5):
+        A, B, _ = orc.build_system("TT", orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+        u, v = bary[0], bary[1]
+        ev = lambda G: sum(G[i, j] * u ** i * v ** j for i in range(G.shape[0]) for j in range(G.shape[0] - i))
+        assert abs(ev(A)) / np.sum(np.abs(A)) < 1e-2
+
+
+# ------------------------------------------------------------------ Bezout (Eq. 24) vs Sylvester resultant
+def _sylvester_det(a, b):
+    """Sylvester resultant det of univariate a (deg m), b (deg n), ascending coefficients."""
+    a = np.trim_zeros(np.asarray(a, float), "b")
+    b = np.trim_zeros(np.asarray(b, float), "b")
+    m, n = len(a) - 1, len(b) - 1
+    S = np.zeros((m + n, m + n))
+    for i in range(n):
+        S[i, i:i + m + 1] = a[::-1]
+    for i in range(m):
+        S[n + i, i:i + n + 1] = b[::-1]
+    return np.linalg.det(S)
+
+
+def test_bezout_symmetric_and_resultant(orc):
+    # det R(v) vanishes exactly where a(.,v), b(.,v) share a root.
+    # Standard identity: det Bezout = +-lc_u(b)^(n - deg_u a) * Res_u(a, b).
+    rng = np.random.default_rng(0)
+    for trial in range(10):
+        da, db = rng.integers(1, 4), rng.integers(2, 5)
+        n = max(da, db)
+        A = np.zeros((n + 3, n + 3))
+        B = np.zeros((n + 3, n + 3))
+        A[:da + 1, :3] = rng.normal(size=(da + 1, 3))
+        B[:db + 1, :3] = rng.normal(size=(db + 1, 3))
+        M = orc.bezout(A, B, n)
+        for v in rng.uniform(-1, 1, 4):
+            Mv = np.array([[np.polyval(M[i][j][::-1], v) for j in range(n)] for i in range(n)])
+            assert np.allclose(Mv, Mv.T, rtol=1e-12, atol=1e-12)
+            av = [np.polyval(A[i, :][::-1], v) for i in range(n + 1)]
+            bv = [np.polyval(B[i, :][::-1], v) for i in range(n + 1)]
+            res = _sylvester_det(av[:da + 1], bv[:db + 1])
+            lc = bv[db] ** (n - da) if db == n else av[da] ** (n - db)
+            det = np.linalg.det(Mv)
+            assert abs(abs(det) - abs(lc * res)) <= 1e-8 * max(1.0, abs(det))
+
+
+def test_laplace_equals_numeric_det(orc):
+    # Sec. 5.2 Laplace expansion: the expanded r(v) equals det R(v) (numpy LU) at 100 points.
+    for mesh, ids, x0, xk1, _ in planted_many(9, "T", 3) + planted_many(10, "R", 3):
+        chain = "T" if mesh.eta_back != mesh.eta_front and len(ids) == 1 else "R"
+        A, B, _ = orc.build_system(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+        A = A / np.max(np.abs(A))
+        B = B / np.max(np.abs(B))
+        n = 6 if chain == "T" else 4
+        M = orc.bezout(A, B, n)
+        r = orc.det_laplace(M)
+        for v in np.linspace(0, 1, 100):
+            Mv = np.array([[np.polyval(M[i][j][::-1], v) for j in range(n)] for i in range(n)])
+            d = np.linalg.det(Mv)
+            scale = np.prod(np.linalg.norm(Mv, axis=1))
+            assert abs(np.polyval(r[::-1], v) - d) <= 1e-9 * scale
+
+
+def test_det_ge_matches_numpy(orc):
+    rng = np.random.default_rng(4)
+    A = rng.normal(size=(6, 6))
+    B = rng.normal(size=(6, 6))
+    A[np.add.outer(np.arange(6), np.arange(6)) > 5] = 0
+    B[np.add.outer(np.arange(6), np.arange(6)) > 5] = 0
+    M = orc.bezout(A, B, 5)
+    for v in (0.0, 0.3, 0.77, 1.0):
+        Mv = np.array([[np.polyval(M[i][j][::-1], v) for j in range(5)] for i in range(5)])
+        assert np.isclose(orc.det_at(A, B, 5, v), np.linalg.det(Mv), rtol=1e-10)
+
+
+# ------------------------------------------------------------------ root isolation (Sec. 5.2)
+def test_isolate_planted_roots(orc):
+    # PAPER.md:608 derivative recursion + bisection to 1e-9; SPEC S:442 planted-root fuzz
+    rng = np.random.default_rng(1)
+    for trial in range(300):
+        k = rng.integers(1, 7)
+        roots = np.sort(rng.uniform(0.02, 0.98, k))
+        if k > 1 and np.min(np.diff(roots)) < 1e-3:
+            continue
+        extra = rng.integers(0, 4)
+        q = np.array([1.0])
+        for _ in range(extra):  # sign-definite quadratic factors: (v - c)^2 + s^2
+            c, s = rng.uniform(-1, 2), rng.uniform(0.1, 1)
+            q = np.convolve(q, [c * c + s * s, -2 * c, 1.0])
+        p = q
+        for r in roots:
+            p = np.convolve(p, [-r, 1.0])
+        p = p * rng.uniform(0.5, 2) * rng.choice([-1, 1])
+        found = orc.isolate(p, 0.0, 1.0, 1e-9)
+        assert len(found) == k
+        assert np.max(np.abs(found - roots)) < 1e-8
+
+
+def test_isolate_matches_numpy_roots(orc):
+    rng = np.random.default_rng(2)
+    for trial in range(300):
+        d = rng.integers(2, 13)
+        p = rng.normal(size=d + 1)
+        rr = np.roots(p[::-1])
+        real = np.sort(rr[np.abs(rr.imag) < 1e-7].real)
+        inside = real[(real > 1e-6) & (real < 1 - 1e-6)]
+        if len(inside) > 1 and np.min(np.diff(inside)) < 1e-5:
+            continue
+        found = orc.isolate(p, 0.0, 1.0, 1e-9)
+        assert len(found) == len(inside), (p, inside, found)
+        if len(inside):
+            assert np.max(np.abs(found - inside)) < 1e-7
+
+
+def test_isolate_trivial_examples(orc):
+    # SPEC S:440-441
+    assert np.allclose(orc.isolate([-0.5, 1.0]), [0.5])
+    assert np.allclose(orc.isolate(np.convolve([-0.25, 1.0], [-0.75, 1.0])), [0.25, 0.75], atol=1e-9)
+
+
+# ------------------------------------------------------------------ closed forms
+def _image_source(P, x0, x2):
+    """flat mirror: reflect x0 across the plane, intersect segment x0'->x2 with the plane"""
+    g = np.cross(P[1] - P[0], P[2] - P[0])
+    g /= np.linalg.norm(g)
+    x0p = x0 - 2 * np.dot(x0 - P[0], g) * g
+    t = np.dot(P[0] - x0p, g) / np.dot(x2 - x0p, g)
+    x = x0p + t * (x2 - x0p)
+    M = np.stack([P[1] - P[0], P[2] - P[0]], 1)
+    uv, *_ = np.linalg.lstsq(M, x - P[0], rcond=None)
+    return uv, np.linalg.norm(x - x0) + np.linalg.norm(x2 - x)
+
+
+def test_flat_mirror_fixture(orc):
+    # SURVEY §8(c) fixed point 1: x1 = (0.5,0,0), (u,v) = (0.5, 1/3); J = (d0+d1)^2
+    pos = np.array([[-1, -1, 0], [2, -1, 0], [-1, 2, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    mesh = Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32))
+    ep = np.array([[[0, 0, 1], [1, 0, 1]]], float)
+    r = orc.solve(mesh, "R", ep)
+    assert r.n_solutions == 1
+    assert np.allclose(r.bary[0], [0.5, 1 / 3], atol=1e-9)
+    assert np.isclose(1 / r.contribution[0], (2 * np.sqrt(1.25)) ** 2, rtol=1e-8)
+
+
+def test_flat_mirror_random_orientations(orc):
+    rng = np.random.default_rng(5)
+    n_checked = 0
+    for trial in range(200):
+        P = rng.normal(size=(3, 3)).astype(np.float32).astype(np.float64)
+        g = np.cross(P[1] - P[0], P[2] - P[0])
+        gh = g / np.linalg.norm(g)
+        c = P.mean(0)
+        x0 = c + gh * rng.uniform(0.5, 2) + rng.normal(size=3) * 0.5
+        x2 = c + gh * rng.uniform(0.5, 2) + rng.normal(size=3) * 0.5
+        if np.dot(x0 - c, gh) <= 0.1 or np.dot(x2 - c, gh) <= 0.1:
+            continue
+        mesh = Mesh(P.astype(np.float32), np.tile(gh, (3, 1)).astype(np.float32), np.array([[0, 1, 2]], np.uint32))
+        uv, L = _image_source(P, x0, x2)
+        r = orc.solve(mesh, "R", np.array([[x0, x2]]), cfg=orc.default_config(cull=0))
+        inside = uv[0] > 1e-6 and uv[1] > 1e-6 and uv.sum() < 1 - 1e-6
+        if not inside:
+            assert r.n_solutions == 0 or (r.flags[0] & 2)
+            continue
+        # face normals are float32-rounded: the shading plane differs from the geometric plane by ~1e-7
+        assert r.n_solutions == 1
+        assert np.allclose(r.bary[0], uv, atol=1e-6)
+        assert np.isclose(1 / r.contribution[0], L * L, rtol=1e-5)
+        n_checked += 1
+    assert n_checked > 30
+
+
+def _fermat_1d(x0, x2, z0, eta0, eta1):
+    """flat interface z = z0: minimise optical path eta0|x0-x| + eta1|x-x2| along the line (1D bisection
+    on the derivative)."""
+    a = np.array([x0[0], x0[1], z0])
+    b = np.array([x2[0], x2[1], z0])
+    def dL(t):
+        x = a + t * (b - a)
+        return eta0 * np.dot(x - x0, b - a) / np.linalg.norm(x - x0) + eta1 * np.dot(x - x2, b - a) / np.linalg.norm(x - x2)
+    lo, hi = 0.0, 1.0
+    for _ in range(200):
+        m = 0.5 * (lo + hi)
+        if dL(m) > 0:
+            hi = m
+        else:
+            lo = m
+    return a + 0.5 * (lo + hi) * (b - a)
+
+
+def test_flat_interface_fermat(orc):
+    # SURVEY §8(c) fixed point 2: flat interface T, face mode, both directions
+    pos = np.array([[-4, -4, 0], [6, -4, 0], [-4, 6, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    rng = np.random.default_rng(6)
+    for direction in (0, 1):
+        for trial in range(20):
+            x0 = np.array([*rng.uniform(-0.8, 0.8, 2), rng.uniform(0.5, 2)])
+            x2 = np.array([*rng.uniform(-0.8, 0.8, 2), -rng.uniform(0.5, 2)])
+            if direction:
+                x0, x2 = x2, x0
+            mesh = Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32), 1.0, 1.5)
+            eta0 = 1.0 if x0[2] > 0 else 1.5
+            eta1 = 2.5 - eta0
+            x = _fermat_1d(x0, x2, 0.0, eta0, eta1)
+            r = orc.solve(mesh, "T", np.array([[x0, x2]]), cfg=orc.default_config(cull=0))
+            assert r.n_solutions == 1
+            u, v = r.bary[0]
+            xs = pos[0] + u * (pos[1] - pos[0]) + v * (pos[2] - pos[0])
+            assert np.linalg.norm(xs - x) < 1e-7  # bisection tol 1e-9 in v x edge length 10
+
+
+def test_index_matched_interface_free_space(orc):
+    # eta = 1 on both sides: no bending, J = |x0 - x2|^2
+    pos = np.array([[-2, -2, 0], [3, -2, 0], [-2, 3, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    mesh = Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32), 1.0, 1.0)
+    x0 = np.array([0.2, 0.1, 1.0])
+    x2 = np.array([-0.3, 0.4, -1.5])
+    r = orc.solve(mesh, "T", np.array([[x0, x2]]), cfg=orc.default_config(cull=0))
+    assert r.n_solutions == 1
+    assert np.isclose(1 / r.contribution[0], np.sum((x0 - x2) ** 2), rtol=1e-7)
+
+
+def test_contribution_scale_covariance(orc):
+    # doubling the scene scale quarters the contribution
+    for mesh, ids, x0, xk1, bary in planted_many(21, "R", 5) + planted_many(22, "T", 5):
+        chain = "R" if mesh.eta_back == 1.5 and False else None
+        for ch in ("R", "T"):
+            r1 = orc.solve(mesh, ch, np.array([[x0, xk1]]), cfg=orc.default_config(cull=0))
+            if r1.n_solutions == 0:
+                continue
+            m2 = Mesh(mesh.pos * 2, mesh.nrm, mesh.tri, mesh.eta_front, mesh.eta_back)
+            r2 = orc.solve(m2, ch, np.array([[2 * x0, 2 * xk1]]), cfg=orc.default_config(cull=0))
+            assert r2.n_solutions == r1.n_solutions
+            assert np.allclose(r2.contribution * 4, r1.contribution, rtol=1e-6)
+
+
+# ------------------------------------------------------------------ planted recovery + residual (north_star)
+@pytest.mark.parametrize("chain,size", [("R", 0.2), ("R", 0.01), ("T", 0.2), ("T", 0.01)])
+def test_one_bounce_recovers_planted(orc, chain, size):
+    cases = planted_many(31 + int(size * 100), chain, 60, size=size)
+    for mesh, ids, x0, xk1, bary in cases:
+        r = orc.solve(mesh, chain, np.array([[x0, xk1]]), cfg=orc.default_config(cull=0))
+        d = [np.max(np.abs(b - bary)) for b in r.bary]
+        assert len(d) >= 1 and min(d) < 1e-7, (bary, r.bary, r.flagged_flags)
+        for b in r.bary:
+            assert bruteforce.specular_residual(chain, mesh, ids, x0, xk1, b, mesh.eta_front, mesh.eta_back) < 1e-6
+
+
+@pytest.mark.parametrize("chain", ["RR", "TT"])
+def test_two_bounce_recovers_planted(orc, chain):
+    cases = planted_many(41, chain, 12, size=0.15)
+    hit = 0
+    for mesh, ids, x0, xk1, bary in cases:
+        r = orc.solve(mesh, chain, np.array([[x0, xk1]]), offsets=np.array([0, 1]), tri_ids=np.array([0, 1]))
+        for b in r.bary:
+            assert bruteforce.specular_residual(chain, mesh, ids, x0, xk1, b, mesh.eta_front, mesh.eta_back) < 1e-6
+        d = [np.max(np.abs(b - bary)) for b in r.bary]
+        if d and min(d) < 1e-6:
+            hit += 1
+    # the 100-piece scan can miss clustered roots by design; SPEC S:714 recall >= 0.95
+    assert hit >= int(0.9 * len(cases))
+
+
+# ------------------------------------------------------------------ brute force on tiny inputs
+def _match(a, b, tol):
+    a = [np.asarray(x) for x in a]
+    b = [np.asarray(x) for x in b]
+    used = set()
+    for x in a:
+        j = next((j for j, y in enumerate(b) if j not in used and np.max(np.abs(x - y)) < tol), None)
+        if j is None:
+            return False
+        used.add(j)
+    return len(used) == len(b)
+
+
+def test_bruteforce_c1_patch(orc):
+    w = patch_c1()
+    r = orc.solve(w.mesh, "R", w.endpoints, cfg=orc.default_config(cull=0))
+    x0, xk1 = w.endpoints[0]
+    flagged = set(map(int, r.flagged_tuple[:, 0])) if len(r.flagged_flags) else set()
+    for t in range(w.mesh.ntris):
+        if t in flagged:
+            continue
+        bf = bruteforce.brute_force("R", w.mesh, [t], x0, xk1, grid=96)
+        mine = [r.bary[i] for i in range(r.n_solutions) if r.tuple[i, 0] == t]
+        assert _match(mine, bf, 1e-6), (t, mine, bf)
+
+
+@pytest.mark.parametrize("chain", ["R", "T"])
+def test_bruteforce_random_interpolated(orc, chain):
+    rng = np.random.default_rng(8 if chain == "R" else 9)
+    mesh = random_triangles(rng, 80, 0.35, normal_tilt=0.35)
+    mesh.eta_front, mesh.eta_back = 1.0, 1.5
+    eps = [[[0.1, -0.3, 1.5], [0.4, 0.6, 1.2]], [[-0.6, 0.2, 0.9], [0.7, -0.1, 2.0]]]
+    if chain == "T":
+        eps = [[[0.1, -0.3, 1.5], [0.4, 0.6, -1.2]], [[-0.6, 0.2, -0.9], [0.7, -0.1, 2.0]]]
+    ep = np.array(eps, float)
+    r = orc.solve(mesh, chain, ep, cfg=orc.default_config(cull=0))
+    total = 0
+    for qi in range(len(ep)):
+        fl = {int(t) for q, t in zip(r.flagged_query, r.flagged_tuple[:, 0]) if q == qi}
+        for t in range(mesh.ntris):
+            if t in fl:
+                continue
+            bf = bruteforce.brute_force(chain, mesh, [t], ep[qi, 0], ep[qi, 1], grid=160,
+                                        eta_front=mesh.eta_front, eta_back=mesh.eta_back)
+            mine = [r.bary[i] for i in range(r.n_solutions) if r.query[i] == qi and r.tuple[i, 0] == t]
+            assert _match(mine, bf, 1e-6), (qi, t, mine, bf)
+            total += len(bf)
+    assert total >= 3
+
+
+# ------------------------------------------------------------------ cull soundness
+@pytest.mark.parametrize("chain", ["R", "T", "RR", "TT"])
+def test_cull_sound_on_planted(orc, chain):
+    n = 300 if len(chain) == 1 else 60
+    for size in (0.01, 0.3):
+        for mesh, ids, x0, xk1, bary in planted_many(51, chain, n, size=size):
+            assert orc.cull_keep(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+
+
+def test_cull_actually_culls(orc):
+    w = patch_c1()
+    x0, xk1 = w.endpoints[0]
+    kept = sum(orc.cull_keep("R", orc.tri_block(w.mesh, [t]), x0, xk1) for t in range(w.mesh.ntris))
+    assert 0 < kept < w.mesh.ntris // 4
+
+
+# ------------------------------------------------------------------ sqrt surrogate (Eq. 20)
+def test_sqrt_table_certified(orc):
+    # 6 consecutive pieces on [0,1], error < 1e-3
+    tab = orc.sqrt_table()
+    assert tab.shape == (6, 5)
+    assert tab[0, 0] == 0 and tab[-1, 1] == 1
+    assert np.all(tab[1:, 0] == tab[:-1, 1])
+    x = np.linspace(0, 1, 100001)
+    err = max(abs(orc.sqrt_approx(xx) - np.sqrt(xx)) for xx in x[::7])
+    assert err < 1e-3
+    for lo, hi, c0, c1, d1 in tab:
+        xs = np.linspace(lo, hi, 20001)
+        assert np.max(np.abs((c0 + c1 * xs) / (1 + d1 * xs) - np.sqrt(xs))) < 1e-3
+        assert d1 > 0  # positive denominator: clearing it keeps the zero set (c4)
+
+
+def test_sqrt_table_matches_golden(orc):
+    import os
+    g = np.loadtxt(os.path.join(os.path.dirname(__file__), "golden", "sqrt_table.txt"))
+    assert np.array_equal(orc.sqrt_table(), g[:, :5])
