@@ -1,0 +1,299 @@
+#!/usr/bin/env python
+"""Benchmark of the Specular Polynomials hot path on B200 (driver contract: one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): C2 "glints" — 256x256 light samples (queries) x 100,352-triangle
+normal-mapped bumpy plane, one-bounce reflection (R), cull pre-pass + fused solve + deterministic
+compaction.  One step = one spoly_solve over all 65,536 queries with inputs resident in HBM.
+
+Multi-GPU (torchrun): the path shards by query; every rank solves its own full C2 frame (different light
+stratification seed) -> weak scaling; NCCL only all-reduces the counters and gathers per-query sums.
+
+--impl reference: the CPU oracle (plain FP64 C++ transcription of the paper) timed on the host cores on a
+bounded sample of the same workload (the reference arm for this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "admissible specular paths/sec and query-tuple solves/sec at 1/2/4/8 B200"
+UNIT = "paths/s"
+
+# ---------------------------------------------------------------- algorithmic FLOP model
+# Minimal-form FP64 FLOPs of the one-bounce reflection solve (FMA = 2 FLOPs), counted from the kernel's
+# formulas: per pair (decision + build a,b + normalise + 3x3 Bezout + Laplace), per FMA term of the
+# univariate root-finding evaluations (counter n_eval_terms), per candidate (back-substitution, one (a,b)
+# evaluation, Eq. 3 validation), per admissible chain (analytic ray-differential Jacobian).
+FLOP_PER_PAIR_R = 880
+FLOP_PER_EVAL_TERM = 2
+FLOP_PER_CANDIDATE_R = 270
+FLOP_PER_ADMISSIBLE_R = 290
+
+
+def flop_model_R(rep):
+    return (rep["n_pairs_in"] * FLOP_PER_PAIR_R + rep["n_eval_terms"] * FLOP_PER_EVAL_TERM +
+            rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
+
+
+# FP64 ALU peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz;
+# 64 FP64 FMA lanes per SM per clock)
+def fp64_peak(sm_mhz=1965.0, nsm=148):
+    return nsm * 64 * 2 * sm_mhz * 1e6
+
+
+class ClockSampler:
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+
+    def __enter__(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+            self.f.close()
+
+    def summary(self):
+        try:
+            rows = [l.strip().split(",") for l in open(self.path) if l.strip()]
+        except Exception:
+            return None
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for r in rows:
+            for i, nm in enumerate(names):
+                if len(r) > 4 + i and "Active" in r[4 + i] and "Not" not in r[4 + i]:
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def oracle_baseline(w, nsample, nthreads=0):
+    """The oracle as it stands on a bounded, strided sample of the workload's queries."""
+    import oracle
+    oracle.build()
+    idx = np.linspace(0, w.nqueries - 1, nsample).astype(np.int64)
+    sub = w.subset(idx)
+    t0 = time.perf_counter()
+    r = oracle.solve(sub.mesh, w.chain, sub.endpoints, intensity=sub.intensity, nthreads=nthreads)
+    dt = time.perf_counter() - t0
+    cores = nthreads if nthreads > 0 else (os.cpu_count() or 1)
+    return {"value": r.n_solutions / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{nsample} of {w.nqueries} queries (strided), full mesh, oracle cull + solve; "
+                      f"{r.n_solutions} paths, {r.report['pairs_in']} pairs in {dt:.2f} s",
+            "solves_per_s": r.report["pairs_in"] / dt, "seconds": dt}
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the oracle on the host cores (rank 0 only)."""
+    if rank != 0:
+        return
+    from paper_2405_13409_b200 import workloads as W
+    w = W.glints_c2()
+    times, paths, pairs = [], 0, 0
+    for s in range(args.warmup + args.steps):
+        b = oracle_baseline(w, args.ref_sample)
+        if s >= args.warmup:
+            times.append(b["seconds"])
+            paths += b["value"] * b["seconds"]
+            pairs += b["solves_per_s"] * b["seconds"]
+    tot = sum(times)
+    val = paths / tot
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "query_tuple_solves_per_s": pairs / tot,
+            "config": {"workload": "C2 glints: 65,536 light samples x 100,352-tri bumpy plane, R (sampled "
+                                   f"{args.ref_sample} queries per step)", "chain": "R"},
+            "cpu_baseline": {"value": val, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+                             "sample": f"{args.ref_sample} strided queries of C2 per step"},
+            "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--res", type=int, default=256, help="C2 light-sample grid (256 -> 65,536 queries)")
+    ap.add_argument("--cpu-sample", type=int, default=48)
+    ap.add_argument("--ref-sample", type=int, default=24)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2405_13409_b200 import spoly
+    from paper_2405_13409_b200 import workloads as W
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    w = W.glints_c2(res=args.res, seed_strata=2 + rank)  # weak scaling: one full frame per rank
+    stream = torch.cuda.current_stream(dev)
+    ctx = spoly.Context(local, stream=stream)
+    ctx.upload_mesh(w.mesh)
+    ep = torch.as_tensor(w.endpoints, dtype=torch.float64, device=dev)
+    inten = torch.as_tensor(w.intensity, dtype=torch.float64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(max(args.warmup, 3)):
+        r = ctx.solve("R", ep, inten)
+    barrier()
+
+    step_ms, solve_ms, reports = [], [], []
+    with ClockSampler(local) as clk:
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)  # L2 flush between timed iterations (untimed)
+            barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            r = ctx.solve("R", ep, inten)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            step_ms.append(e0.elapsed_time(e1))
+            solve_ms.append(r.report["ms_solve"])
+            reports.append(dict(r.report, n_solutions=r.n_solutions))
+    clocks = clk.summary()
+    total_ms = float(sum(step_ms))
+    n_paths = sum(x["n_solutions"] for x in reports)
+    n_pairs = sum(x["n_pairs_in"] for x in reports)
+    launches = sum(x["n_launches"] for x in reports)
+
+    # ---- end to end through the public API with host buffers (H2D endpoints + intensity, D2H per-query)
+    e2e = None
+    if not args.no_e2e:
+        ep_h = np.ascontiguousarray(w.endpoints)
+        it_h = np.ascontiguousarray(w.intensity)
+        pq, _ = ctx.solve_host("R", ep_h, it_h)
+        e2e_t, e2e_paths = 0.0, 0
+        for s in range(args.steps):
+            flush.fill_(s & 0xFF)
+            barrier()
+            t0 = time.perf_counter()
+            pq, rr = ctx.solve_host("R", ep_h, it_h)
+            torch.cuda.synchronize(dev)
+            e2e_t += time.perf_counter() - t0
+            e2e_paths += rr.n_solutions
+        e2e = [e2e_paths, e2e_t]
+
+    # ---- cross-rank aggregation (NCCL): counters sum, time max; per-query sums gathered to every rank
+    if world > 1:
+        t = torch.tensor([total_ms, e2e[1] if e2e else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        c = torch.tensor([n_paths, n_pairs, launches, e2e[0] if e2e else 0], dtype=torch.float64, device=dev)
+        dist.all_reduce(c, op=dist.ReduceOp.SUM)
+        total_ms, e2e_max = float(t[0]), float(t[1])
+        n_paths, n_pairs, launches = int(c[0]), int(c[1]), int(c[2])
+        if e2e:
+            e2e = [int(c[3]), e2e_max]
+        gathered = [torch.empty_like(r.per_query) for _ in range(world)]
+        dist.all_gather(gathered, r.per_query.contiguous())
+
+    # ---- roofline of the dominant kernel (solve), from its own launch's CUDA-event time
+    rep = reports[-1]
+    flops = flop_model_R(rep)
+    solve_s = statistics.mean(solve_ms) / 1e3
+    achieved = flops / solve_s
+    peak = fp64_peak()
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "solve_traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get("bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_baseline(w, args.cpu_sample)
+        cpu.pop("seconds", None)
+
+    line = {
+        "metric": METRIC, "value": n_paths / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "query_tuple_solves_per_s": n_pairs / (total_ms / 1e3),
+        "config": {"workload": "C2 glints: %d light samples x %d-tri normal-mapped bumpy plane, one-bounce R, "
+                               "cull pre-pass + fused FP64 solve + deterministic compaction" % (w.nqueries, w.mesh.ntris),
+                   "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": "R",
+                   "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
+        "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
+        "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": solve_s * 1e3,
+                     "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
+        "roofline": {"bound": "alu", "kernel": "k_solve_R_list", "achieved": achieved / 1e12, "peak": peak / 1e12,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                     "flop_per_launch": flops,
+                     "peak_note": "FP64: 148 SMs x 64 FMA/clk x 2 x 1965 MHz (unit counts x clocks.max.sm)"},
+        "clocks": clocks,
+        "gpu_launches": launches,
+    }
+    if e2e:
+        line["e2e"] = {"value": e2e[0] / e2e[1], "unit": UNIT, "h2d_bytes_per_step": int(w.endpoints.nbytes +
+                                                                                         w.intensity.nbytes),
+                       "d2h_bytes_per_step": int(8 * w.nqueries)}
+    if cpu:
+        line["cpu_baseline"] = cpu
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,160 @@
+/* spoly.h — C ABI of the B200-native Specular Polynomials hot path (libspoly.so).
+ *
+ * Problem (Sec. 3.1): given two separators x_0, x_{k+1} (a "query") and a tuple
+ * of k specular triangles T_1..T_k (positions P_i, shading normals N_i, Eqs. 1-2),
+ * return ALL admissible specular chains x_1..x_k satisfying h_i x n_i = 0 (Eq. 3), and, when
+ * several connect the same separators, the sum of their contributions.
+ *
+ * Method on the device (all sm_100a kernels, FP64 where the tolerance needs it):
+ *   cull (replaces the Wang20 pruning PAPER.md:680)  ->  coefficient phase (Eqs. 6, 9, 12, 13-20;
+ *   Sec. 5.3)  ->  elimination phase (hidden-variable Bezout resultant, Eq. 24)  ->  univariate
+ *   roots (Laplace expansion + derivative-recursion root isolation for k=1, PAPER.md:604-608;
+ *   determinant-sign bisection over 100 pieces for k=2)  ->  path phase
+ *   (back-substitution, validation, contribution)  ->  deterministic compaction.
+ *
+ * Conventions
+ *  - Every call returns spoly_status; no exception crosses the ABI.  Errors are sticky only for the
+ *    call that reports them.
+ *  - Pointers documented "device" are CUDA device pointers valid on the ctx's device (e.g. a torch
+ *    CUDA tensor's data_ptr()); pointers documented "host" are ordinary host memory.
+ *  - The ctx owns every output buffer; they stay valid until the next spoly_solve* on the same ctx
+ *    or spoly_destroy.
+ *  - All work is enqueued on the ctx's stream; spoly_solve returns after the stream has completed
+ *    (it synchronises once to read the solution count), so outputs are ready on return.
+ *  - Per-tuple degeneracies (near-tangent roots, boundary roots, degenerate systems) are FLAGS on
+ *    the tuple, never errors.
+ */
+#ifndef SPOLY_H
+#define SPOLY_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  SPOLY_OK = 0,
+  SPOLY_ERR_INVALID_ARG = 1,       /* NULL pointer, bounces != strlen(chain), bad sizes        */
+  SPOLY_ERR_BAD_MESH = 2,          /* index out of range or degenerate triangle (|e1xe2| tiny) */
+  SPOLY_ERR_UNSUPPORTED_CHAIN = 3, /* chain not in {"R","T","RR","TT","RT","TR"}              */
+  SPOLY_ERR_OOM = 4,               /* device allocation failed                                 */
+  SPOLY_ERR_CAPACITY = 5,          /* max_solutions too small even after one regrow            */
+  SPOLY_ERR_CUDA = 6               /* any other CUDA runtime error (message: spoly_last_error) */
+} spoly_status;
+
+/* tuple flags: excluded from exact-count parity, reported per tuple */
+#define SPOLY_FLAG_NEAR_TANGENT 1u /* root pair closer than eps_flag, tiny critical value, or
+                                      non-transversal (a,b) intersection                        */
+#define SPOLY_FLAG_BOUNDARY 2u     /* a valid chain within eps_flag of a triangle edge           */
+#define SPOLY_FLAG_RESIDUAL 4u     /* accepted chain with residual in [1e-7, theta_final)        */
+#define SPOLY_FLAG_DEGENERATE 8u   /* a or b identically zero, u-free system, degenerate basis   */
+
+typedef struct spoly_ctx spoly_ctx;
+
+typedef struct {
+  int pieces;            /* k>=2 determinant scan pieces; 100                 */
+  int scan_bisect_iters; /* k>=2 bisections per sign-changing piece; 10       */
+  double bisect_tol;     /* k=1 root bracket threshold; 1e-9                  */
+  int polish_iters;      /* Newton steps on the exact shooting residual (k=2); 3             */
+  double theta_admit;    /* raw-root residual gate before polish (k=2); 1e-3                 */
+  double theta_final;    /* final Eq. 3 residual gate; 1e-6 (north_star)                     */
+  double eps_domain;     /* barycentric slack of the inside test; 1e-9                       */
+  double eps_flag;       /* near-tangent / boundary flag distance; 1e-6                      */
+  double tau_trunc;      /* numerical u-degree truncation threshold; 1e-12       */
+  int cull;              /* 1: run the cull pre-pass when no tuple list is given             */
+  int deterministic;     /* 1: sort solutions by (query, tuple, root) -> bit-identical output */
+  float cull_margin;     /* angular slack (rad) of the FP32 cull; 1e-4                       */
+  uint64_t max_solutions;/* initial solution-buffer capacity (regrown once on overflow)      */
+  uint64_t max_pairs;    /* work-list chunk size in (query, tuple) pairs                      */
+} spoly_config;
+
+/* Fills cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
+spoly_status spoly_default_config(spoly_config* cfg);
+
+/* Creates a context on CUDA device `cuda_device`.  cfg NULL -> defaults.  cuda_stream: a
+ * cudaStream_t to enqueue on (NULL -> the ctx creates and owns a non-blocking stream).
+ * On success *out owns device memory until spoly_destroy. */
+spoly_status spoly_create(int cuda_device, const spoly_config* cfg, void* cuda_stream, spoly_ctx** out);
+void spoly_destroy(spoly_ctx* ctx);
+/* Human-readable message of the last failing call on this ctx (static storage of the ctx). */
+const char* spoly_last_error(const spoly_ctx* ctx);
+
+/* Uploads a triangle mesh (HOST pointers, copied): pos/nrm are nverts x 3 float32 (positions and
+ * per-vertex shading normals; normals need not be unit, Eq. 2 interpolates them un-normalised),
+ * tri is ntris x 3 uint32 vertex indices; the winding defines the geometric normal e1 x e2 whose
+ * side has index of refraction eta_front (the other side eta_back).  Builds the per-triangle FP32
+ * records, the spatial (Morton) cluster hierarchy and the cluster bounds used by the cull.
+ * Replaces any previously uploaded mesh; *mesh_id receives its id (always 0 in this version). */
+spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts,
+                               const uint32_t* tri, uint32_t ntris, float eta_front, float eta_back,
+                               uint32_t* mesh_id);
+
+/* Optional explicit tuple list (device pointers): CSR offsets[nqueries+1] into tri_ids, which holds
+ * k uint32 triangle ids per tuple (ORIGINAL mesh indices). */
+typedef struct {
+  const uint32_t* offsets;
+  const uint32_t* tri_ids;
+} spoly_tuple_list;
+
+typedef struct {
+  /* telescoping counters */
+  uint64_t n_pairs_in, n_systems, n_vroots, n_candidates, n_rej_domain, n_rej_constraint, n_rej_side,
+      n_rej_kappa, n_flagged, n_admissible;
+  float ms_cull, ms_solve, ms_reduce; /* CUDA-event times of the phases of the last solve       */
+  uint32_t n_launches;                /* kernels this library launched in the last solve        */
+  uint64_t n_eval_terms;              /* FMA terms of the univariate root-finding evaluations
+                                         (input of the algorithmic FLOP model)     */
+  uint64_t required_solutions;        /* set with SPOLY_ERR_CAPACITY                            */
+} spoly_report;
+
+typedef struct {
+  uint64_t n_solutions; /* admissible chains                                                */
+  uint64_t n_flagged;   /* tuples carrying a flag                                           */
+  int k;                /* bounces                                                          */
+  /* device pointers owned by the ctx, sorted by (query, tuple position, root) when
+   * deterministic=1 */
+  const uint32_t* query;        /* [n_solutions]                                            */
+  const uint32_t* tuple;        /* [n_solutions * k] original triangle ids                  */
+  const double* bary;           /* [n_solutions * 2k] (u_1, v_1[, u_2, v_2]), Eq. 1          */
+  const double* contribution;   /* [n_solutions] I / J (geometric point-light factor, c15)  */
+  const float* residual;        /* [n_solutions] max_i |h_i^ x n_i^| (Eq. 3)                */
+  const uint32_t* flags;        /* [n_solutions] flags of the solution's tuple              */
+  const uint32_t* flagged_query;/* [n_flagged]                                              */
+  const uint32_t* flagged_tuple;/* [n_flagged * k]                                          */
+  const uint32_t* flagged_flags;/* [n_flagged]                                              */
+  const double* per_query;      /* [nqueries] sum of contributions           */
+  spoly_report report;
+} spoly_result;
+
+/* Solves every (query, tuple) pair.  chain: "R", "T", "RR" or "TT" (Heckbert notation,
+ * PAPER.md:479); bounces must equal strlen(chain).  endpoints: DEVICE, nqueries x 2 x 3 float64
+ * (x_0 then x_{k+1}).  light_intensity: DEVICE, nqueries float64, or NULL (= 1).  tuples: DEVICE
+ * CSR list, or NULL -> the cull pre-pass enumerates candidate tuples itself (cfg.cull=1) or all
+ * tuples (cfg.cull=0).  out: filled with ctx-owned device pointers. */
+spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces,
+                         const double* endpoints, uint32_t nqueries, const double* light_intensity,
+                         const spoly_tuple_list* tuples, spoly_result* out);
+
+/* Same as spoly_solve but from/to HOST memory: copies endpoints/intensity host->device (through
+ * ctx-owned pinned staging), solves, and copies the per-query contribution sums (nqueries float64)
+ * back into per_query_host.  out (optional) receives the device-side result as spoly_solve. */
+spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces,
+                              const double* endpoints_host, uint32_t nqueries,
+                              const double* light_intensity_host, double* per_query_host,
+                              spoly_result* out);
+
+/* Device pointers of the (query, tuple) work list of the LAST solve (cull output or the given list),
+ * query-major: pair_query[n_pairs], pair_tuple[n_pairs * k] (original ids).  Only the last chunk
+ * is retained when the solve was chunked (*n_pairs then counts that chunk). */
+spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pair_query,
+                                 const uint32_t** pair_tuple, uint64_t* n_pairs);
+
+/* FMA-throughput microbenchmark on the ctx's device (roofline denominator): independent FMA
+ * chains on every SM for about `seconds`.  fp64=1: double, 0: float.  Returns FLOP/s. */
+spoly_status spoly_bench_fma(spoly_ctx* ctx, int fp64, double seconds, double* flops_per_s);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPOLY_H */

@@ -731,14 +731,18 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
       double vs_ = vs;
       if (k == 1) {
         // reading R2: <= 3 Newton steps on F = (a, b) (normalised system, relabeled coordinates),
-        // a step is kept only if |F| decreases (SPEC newton_polish_2d).  The bisection
-        // threshold 1e-9 on v is otherwise amplified by 1/|da/du| in u.
+        // a step is kept only if |F| decreases and the candidate stays within 1e-3 (max-norm) of where
+        // back-substitution put it: a refinement of a located root, never a search (SPEC
+        // newton_polish_2d).  The bisection threshold 1e-9 on v is
+        // otherwise amplified by 1/|da/du| in u.
+        const double u_start = us_, v_start = vs_;
         double fa = a(us_, vs_), fb = b(us_, vs_);
         for (int it = 0; it < 3; ++it) {
           double au = a.du(us_, vs_), av = a.dv(us_, vs_), bu = b.du(us_, vs_), bv = b.dv(us_, vs_);
           double det = au * bv - av * bu;
           if (det == 0) break;
           double du = -(bv * fa - av * fb) / det, dv = -(-bu * fa + au * fb) / det;
+          if (!(std::max(std::fabs(us_ + du - u_start), std::fabs(vs_ + dv - v_start)) <= 1e-3)) break;
           double na = a(us_ + du, vs_ + dv), nb = b(us_ + du, vs_ + dv);
           if (!(std::hypot(na, nb) < std::hypot(fa, fb))) break;
           us_ += du;

@@ -1,0 +1,567 @@
+// C-ABI of libspoly.so (include/spoly.h): context, mesh upload, solve orchestration on one stream.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <cub/cub.cuh>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+using namespace spoly;
+
+namespace {
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  cudaError_t ensure(size_t n) {
+    if (n <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(n, 1);
+    cudaError_t e = cudaMalloc(&p, want * sizeof(T));
+    if (e == cudaSuccess) cap = want;
+    return e;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+};
+
+}  // namespace
+
+struct spoly_ctx {
+  int device = 0;
+  int nsm = 148;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  spoly_config cfg;
+  std::string err;
+  // mesh
+  bool has_mesh = false;
+  DeviceMesh M;
+  DBuf<TriRec> d_tris;
+  DBuf<float4> d_tricone;
+  DBuf<uint32_t> d_orig, d_perm;
+  DBuf<ClusterRec> d_cl;
+  // work list
+  DBuf<uint64_t> d_counts;
+  DBuf<unsigned long long> d_offsets;
+  DBuf<uint32_t> d_pq, d_pt, d_pt_orig;
+  uint64_t npairs = 0;
+  // raw sink
+  DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2;
+  DBuf<uint32_t> d_query, d_tuple, d_flags, d_fquery, d_ftuple, d_fflags, d_perm_in, d_perm_out, d_fperm_in,
+      d_fperm_out;
+  DBuf<double> d_bary, d_contrib;
+  DBuf<float> d_resid;
+  // sorted output
+  DBuf<uint32_t> o_query, o_tuple, o_flags, o_fquery, o_ftuple, o_fflags;
+  DBuf<double> o_bary, o_contrib, o_per_query;
+  DBuf<float> o_resid;
+  DBuf<unsigned char> d_temp;
+  // host staging
+  DBuf<double> d_ep, d_int;
+  double* h_pinned = nullptr;
+  size_t h_pinned_cap = 0;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t launches = 0;
+};
+
+#define CK(call)                                                                  \
+  do {                                                                            \
+    cudaError_t e_ = (call);                                                      \
+    if (e_ != cudaSuccess) {                                                      \
+      ctx->err = std::string(#call) + ": " + cudaGetErrorString(e_);              \
+      return e_ == cudaErrorMemoryAllocation ? SPOLY_ERR_OOM : SPOLY_ERR_CUDA;    \
+    }                                                                             \
+  } while (0)
+
+static spoly_status fail(spoly_ctx* ctx, spoly_status s, const char* msg) {
+  if (ctx) ctx->err = msg;
+  return s;
+}
+
+extern "C" {
+
+spoly_status spoly_default_config(spoly_config* c) {
+  if (!c) return SPOLY_ERR_INVALID_ARG;
+  c->pieces = 100;
+  c->scan_bisect_iters = 10;
+  c->bisect_tol = 1e-9;
+  c->polish_iters = 3;
+  c->theta_admit = 1e-3;
+  c->theta_final = 1e-6;
+  c->eps_domain = 1e-9;
+  c->eps_flag = 1e-6;
+  c->tau_trunc = 1e-12;
+  c->cull = 1;
+  c->deterministic = 1;
+  c->cull_margin = 1e-4f;
+  c->max_solutions = 1ull << 22;
+  c->max_pairs = 1ull << 32;
+  return SPOLY_OK;
+}
+
+spoly_status spoly_create(int dev, const spoly_config* cfg, void* stream, spoly_ctx** out) {
+  if (!out) return SPOLY_ERR_INVALID_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || dev < 0 || dev >= ndev) return SPOLY_ERR_CUDA;
+  spoly_ctx* ctx = new spoly_ctx;
+  ctx->device = dev;
+  if (cfg)
+    ctx->cfg = *cfg;
+  else
+    spoly_default_config(&ctx->cfg);
+  if (cudaSetDevice(dev) != cudaSuccess) {
+    delete ctx;
+    return SPOLY_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&ctx->nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (stream) {
+    ctx->st = (cudaStream_t)stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking) != cudaSuccess) {
+      delete ctx;
+      return SPOLY_ERR_CUDA;
+    }
+    ctx->own_stream = true;
+  }
+  for (auto& e : ctx->ev) cudaEventCreate(&e);
+  *out = ctx;
+  return SPOLY_OK;
+}
+
+void spoly_destroy(spoly_ctx* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->st);
+  ctx->d_tris.release(); ctx->d_tricone.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
+  ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
+  ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
+  ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_query.release(); ctx->d_tuple.release();
+  ctx->d_flags.release(); ctx->d_fquery.release(); ctx->d_ftuple.release(); ctx->d_fflags.release();
+  ctx->d_perm_in.release(); ctx->d_perm_out.release(); ctx->d_fperm_in.release(); ctx->d_fperm_out.release();
+  ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
+  ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
+  ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
+  ctx->o_per_query.release(); ctx->o_resid.release(); ctx->d_temp.release(); ctx->d_ep.release(); ctx->d_int.release();
+  if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+  for (auto& e : ctx->ev)
+    if (e) cudaEventDestroy(e);
+  if (ctx->own_stream) cudaStreamDestroy(ctx->st);
+  delete ctx;
+}
+
+const char* spoly_last_error(const spoly_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
+
+spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri,
+                               uint32_t ntris, float eta_front, float eta_back, uint32_t* mesh_id) {
+  if (!ctx || !pos || !nrm || !tri || ntris == 0 || nverts == 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null mesh");
+  if (!(eta_front > 0) || !(eta_back > 0)) return fail(ctx, SPOLY_ERR_INVALID_ARG, "eta must be > 0");
+  CK(cudaSetDevice(ctx->device));
+  // host-side validation + Morton order of the centroids (one-time scene setup)
+  double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (uint64_t i = 0; i < 3ull * ntris; ++i)
+    if (tri[i] >= nverts) return fail(ctx, SPOLY_ERR_BAD_MESH, "triangle index out of range");
+  for (uint32_t v = 0; v < nverts; ++v)
+    for (int c = 0; c < 3; ++c) {
+      double x = pos[3ull * v + c];
+      if (!std::isfinite(x) || !std::isfinite((double)nrm[3ull * v + c]))
+        return fail(ctx, SPOLY_ERR_BAD_MESH, "non-finite vertex");
+      lo[c] = std::min(lo[c], x);
+      hi[c] = std::max(hi[c], x);
+    }
+  const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
+                       (hi[2] - lo[2]) * (hi[2] - lo[2]);
+  std::vector<uint64_t> key(ntris);
+  for (uint32_t t = 0; t < ntris; ++t) {
+    double P[3][3];
+    for (int j = 0; j < 3; ++j)
+      for (int c = 0; c < 3; ++c) P[j][c] = pos[3ull * tri[3ull * t + j] + c];
+    double e1[3], e2[3];
+    for (int c = 0; c < 3; ++c) {
+      e1[c] = P[1][c] - P[0][c];
+      e2[c] = P[2][c] - P[0][c];
+    }
+    double g[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
+    if (!(std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]) > 1e-12 * diag2))
+      return fail(ctx, SPOLY_ERR_BAD_MESH, "degenerate triangle");
+    uint32_t code = 0;
+    uint32_t ix[3];
+    for (int c = 0; c < 3; ++c) {
+      double m = (P[0][c] + P[1][c] + P[2][c]) / 3.0;
+      double s = hi[c] > lo[c] ? (m - lo[c]) / (hi[c] - lo[c]) : 0.0;
+      ix[c] = (uint32_t)std::min(1023.0, std::max(0.0, s * 1024.0));
+    }
+    for (int b = 9; b >= 0; --b)
+      for (int c = 0; c < 3; ++c) code = (code << 1) | ((ix[c] >> b) & 1u);
+    key[t] = ((uint64_t)code << 32) | t;
+  }
+  std::sort(key.begin(), key.end());
+  std::vector<uint32_t> order(ntris);
+  for (uint32_t i = 0; i < ntris; ++i) order[i] = (uint32_t)(key[i] & 0xffffffffu);
+
+  float *dpos = nullptr, *dnrm = nullptr;
+  uint32_t *dtri = nullptr, *dorder = nullptr;
+  CK(cudaMalloc(&dpos, sizeof(float) * 3ull * nverts));
+  CK(cudaMalloc(&dnrm, sizeof(float) * 3ull * nverts));
+  CK(cudaMalloc(&dtri, sizeof(uint32_t) * 3ull * ntris));
+  CK(cudaMalloc(&dorder, sizeof(uint32_t) * ntris));
+  CK(cudaMemcpyAsync(dpos, pos, sizeof(float) * 3ull * nverts, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dnrm, nrm, sizeof(float) * 3ull * nverts, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dtri, tri, sizeof(uint32_t) * 3ull * ntris, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dorder, order.data(), sizeof(uint32_t) * ntris, cudaMemcpyHostToDevice, ctx->st));
+  const uint32_t ncl = (ntris + kClusterSize - 1) / kClusterSize;
+  CK(ctx->d_tris.ensure(ntris));
+  CK(ctx->d_tricone.ensure(ntris));
+  CK(ctx->d_orig.ensure(ntris));
+  CK(ctx->d_perm.ensure(ntris));
+  CK(ctx->d_cl.ensure(ncl));
+  launch_build_tris(dpos, dnrm, dtri, dorder, ntris, ctx->d_tris.p, ctx->d_tricone.p, ctx->d_orig.p, ctx->d_perm.p,
+                    ctx->st);
+  launch_build_clusters(ctx->d_tris.p, ctx->d_tricone.p, ntris, ctx->d_cl.p, ctx->st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(dpos);
+  cudaFree(dnrm);
+  cudaFree(dtri);
+  cudaFree(dorder);
+  ctx->M.ntris = ntris;
+  ctx->M.nclusters = ncl;
+  ctx->M.eta_front = eta_front;
+  ctx->M.eta_back = eta_back;
+  ctx->M.tris = ctx->d_tris.p;
+  ctx->M.tricone = ctx->d_tricone.p;
+  ctx->M.orig_id = ctx->d_orig.p;
+  ctx->M.perm_of = ctx->d_perm.p;
+  ctx->M.clusters = ctx->d_cl.p;
+  ctx->has_mesh = true;
+  if (mesh_id) *mesh_id = 0;
+  return SPOLY_OK;
+}
+
+static SolSink raw_sink(spoly_ctx* ctx) {
+  SolSink S;
+  S.count = ctx->d_count.p;
+  S.capacity = ctx->d_key.cap;
+  S.key = ctx->d_key.p;
+  S.query = ctx->d_query.p;
+  S.tuple = ctx->d_tuple.p;
+  S.bary = ctx->d_bary.p;
+  S.contrib = ctx->d_contrib.p;
+  S.resid = ctx->d_resid.p;
+  S.flags = ctx->d_flags.p;
+  S.fcount = ctx->d_count.p + 1;
+  S.fcapacity = ctx->d_fkey.cap;
+  S.fkey = ctx->d_fkey.p;
+  S.fquery = ctx->d_fquery.p;
+  S.ftuple = ctx->d_ftuple.p;
+  S.fflags = ctx->d_fflags.p;
+  S.counters = ctx->d_counters.p;
+  return S;
+}
+
+static spoly_status ensure_sink(spoly_ctx* ctx, uint64_t nsol, uint64_t nflag, int k) {
+  CK(ctx->d_key.ensure(nsol));
+  CK(ctx->d_query.ensure(nsol));
+  CK(ctx->d_tuple.ensure(nsol * k));
+  CK(ctx->d_bary.ensure(nsol * 2 * k));
+  CK(ctx->d_contrib.ensure(nsol));
+  CK(ctx->d_resid.ensure(nsol));
+  CK(ctx->d_flags.ensure(nsol));
+  CK(ctx->d_fkey.ensure(nflag));
+  CK(ctx->d_fquery.ensure(nflag));
+  CK(ctx->d_ftuple.ensure(nflag * k));
+  CK(ctx->d_fflags.ensure(nflag));
+  // keep all arrays at equal capacity so S.capacity bounds every write
+  uint64_t cap = std::min({ctx->d_key.cap, ctx->d_query.cap, ctx->d_contrib.cap, ctx->d_resid.cap, ctx->d_flags.cap,
+                           ctx->d_tuple.cap / k, ctx->d_bary.cap / (2 * k)});
+  uint64_t fcap = std::min({ctx->d_fkey.cap, ctx->d_fquery.cap, ctx->d_fflags.cap, ctx->d_ftuple.cap / k});
+  ctx->d_key.cap = cap;
+  ctx->d_fkey.cap = fcap;
+  return SPOLY_OK;
+}
+
+static int bits_for(uint64_t n) {
+  int b = 1;
+  while (b < 64 && (1ull << b) <= n) ++b;
+  return b;
+}
+
+spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces, const double* endpoints,
+                         uint32_t nq, const double* inten, const spoly_tuple_list* tuples, spoly_result* out) {
+  if (!ctx || !chain || !out) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
+  const int k = (int)strlen(chain);
+  if (bounces != k || k < 1) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bounces != strlen(chain)");
+  if (strcmp(chain, "R") != 0) return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
+  if (!ctx->has_mesh || mesh_id != 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no such mesh");
+  if (nq && !endpoints) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null endpoints");
+  CK(cudaSetDevice(ctx->device));
+  cudaStream_t st = ctx->st;
+  ctx->launches = 0;
+  memset(out, 0, sizeof(*out));
+  out->k = k;
+  CK(ctx->d_count.ensure(2));
+  CK(ctx->d_counters.ensure(C_NUM));
+  CK(ctx->o_per_query.ensure(nq));
+  CK(cudaEventRecord(ctx->ev[0], st));
+
+  // ---------------- work list
+  uint64_t npairs = 0;
+  if (tuples) {
+    if (!tuples->offsets || !tuples->tri_ids) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null tuple list");
+    uint32_t tot = 0;
+    CK(cudaMemcpyAsync(&tot, tuples->offsets + nq, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    npairs = tot;
+    CK(ctx->d_pq.ensure(npairs));
+    CK(ctx->d_pt.ensure(npairs * k));
+    launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    ctx->launches++;
+  } else if (ctx->cfg.cull) {
+    CK(ctx->d_counts.ensure(nq));
+    CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
+    CullParams cp;
+    cp.margin = ctx->cfg.cull_margin;
+    cp.refract = chain[0] == 'T';
+    cp.eta_front = ctx->M.eta_front;
+    cp.eta_back = ctx->M.eta_back;
+    CK(cudaMemsetAsync(ctx->d_counts.p, 0, sizeof(uint64_t) * nq, st));
+    launch_cull_k1(0, endpoints, nq, ctx->M, cp, reinterpret_cast<uint32_t*>(ctx->d_counts.p), nullptr, nullptr,
+                   nullptr, ctx->nsm, st);
+    ctx->launches++;
+    // counts were written as u32 into a u64-sized buffer: widen by scanning the u32 view
+    const uint32_t* c32 = reinterpret_cast<const uint32_t*>(ctx->d_counts.p);
+    size_t tbytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
+    CK(ctx->d_temp.ensure(tbytes));
+    CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
+    CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nq, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    npairs = tot;
+    CK(ctx->d_pq.ensure(npairs));
+    CK(ctx->d_pt.ensure(npairs * k));
+    launch_cull_k1(1, endpoints, nq, ctx->M, cp, nullptr, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    ctx->launches++;
+  } else {
+    npairs = (uint64_t)nq * ctx->M.ntris;
+    CK(ctx->d_pq.ensure(npairs));
+    CK(ctx->d_pt.ensure(npairs * k));
+    launch_all_pairs_k1(nq, ctx->M.ntris, ctx->d_pq.p, ctx->d_pt.p, st);
+    ctx->launches++;
+  }
+  ctx->npairs = npairs;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[1], st));
+
+  // ---------------- solve (regrow the sink once on overflow)
+  SolveParams prm;
+  prm.bisect_tol = ctx->cfg.bisect_tol;
+  prm.theta_admit = ctx->cfg.theta_admit;
+  prm.theta_final = ctx->cfg.theta_final;
+  prm.eps_domain = ctx->cfg.eps_domain;
+  prm.eps_flag = ctx->cfg.eps_flag;
+  prm.tau_trunc = ctx->cfg.tau_trunc;
+  prm.pieces = ctx->cfg.pieces;
+  prm.scan_bisect_iters = ctx->cfg.scan_bisect_iters;
+  prm.polish_iters = ctx->cfg.polish_iters;
+  prm.eta_front = ctx->M.eta_front;
+  prm.eta_back = ctx->M.eta_back;
+  spoly_status s = ensure_sink(ctx, std::max<uint64_t>(ctx->d_key.cap, ctx->cfg.max_solutions),
+                               std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
+  if (s != SPOLY_OK) return s;
+  unsigned long long cnt[2] = {0, 0};
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    CK(cudaMemsetAsync(ctx->d_count.p, 0, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_counters.p, 0, C_NUM * sizeof(unsigned long long), st));
+    SolSink S = raw_sink(ctx);
+    launch_solve_R_list(ctx->d_pq.p, ctx->d_pt.p, npairs, 0, ctx->M, endpoints, inten, prm, S, ctx->nsm, st);
+    ctx->launches++;
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (cnt[0] <= S.capacity && cnt[1] <= S.fcapacity) break;
+    if (attempt == 1) {
+      out->report.required_solutions = cnt[0];
+      return fail(ctx, SPOLY_ERR_CAPACITY, "solution buffer overflow after regrow");
+    }
+    s = ensure_sink(ctx, (uint64_t)(cnt[0] * 1.25) + 1024, (uint64_t)(cnt[1] * 1.25) + 1024, k);
+    if (s != SPOLY_OK) return s;
+  }
+  CK(cudaEventRecord(ctx->ev[2], st));
+
+  // ---------------- deterministic order + per-query sums
+  const uint64_t n = cnt[0], nf = cnt[1];
+  CK(ctx->o_query.ensure(n));
+  CK(ctx->o_tuple.ensure(n * k));
+  CK(ctx->o_bary.ensure(n * 2 * k));
+  CK(ctx->o_contrib.ensure(n));
+  CK(ctx->o_resid.ensure(n));
+  CK(ctx->o_flags.ensure(n));
+  CK(ctx->o_fquery.ensure(nf));
+  CK(ctx->o_ftuple.ensure(nf * k));
+  CK(ctx->o_fflags.ensure(nf));
+  CK(ctx->d_key2.ensure(n));
+  CK(ctx->d_perm_in.ensure(n));
+  CK(ctx->d_perm_out.ensure(n));
+  CK(ctx->d_fkey2.ensure(nf));
+  CK(ctx->d_fperm_in.ensure(nf));
+  CK(ctx->d_fperm_out.ensure(nf));
+  SolSink in = raw_sink(ctx), o;
+  memset(&o, 0, sizeof(o));
+  o.query = ctx->o_query.p;
+  o.tuple = ctx->o_tuple.p;
+  o.bary = ctx->o_bary.p;
+  o.contrib = ctx->o_contrib.p;
+  o.resid = ctx->o_resid.p;
+  o.flags = ctx->o_flags.p;
+  o.fquery = ctx->o_fquery.p;
+  o.ftuple = ctx->o_ftuple.p;
+  o.fflags = ctx->o_fflags.p;
+  const int end_bit = std::min(64, 6 + bits_for(npairs));
+  if (n) {
+    launch_iota(ctx->d_perm_in.p, n, st);
+    ctx->launches++;
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p, ctx->d_perm_out.p,
+                                       (int64_t)n, 0, end_bit, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p,
+                                       ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
+    launch_gather_solutions(ctx->d_perm_out.p, n, k, in, o, st);
+    ctx->launches++;
+  }
+  if (nf) {
+    launch_iota(ctx->d_fperm_in.p, nf, st);
+    ctx->launches++;
+    size_t tb = 0;
+    const int fbits = std::min(64, bits_for(npairs));
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fperm_in.p,
+                                       ctx->d_fperm_out.p, (int64_t)nf, 0, fbits, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fperm_in.p,
+                                       ctx->d_fperm_out.p, (int64_t)nf, 0, fbits, st));
+    launch_gather_flagged(ctx->d_fperm_out.p, nf, k, in, o, st);
+    ctx->launches++;
+  }
+  launch_per_query_sorted(ctx->o_query.p, ctx->o_contrib.p, n, nq, ctx->o_per_query.p, st);
+  ctx->launches++;
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(ctx->ev[3], st));
+  unsigned long long counters[C_NUM];
+  CK(cudaMemcpyAsync(counters, ctx->d_counters.p, sizeof(counters), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+
+  out->n_solutions = n;
+  out->n_flagged = nf;
+  out->query = ctx->o_query.p;
+  out->tuple = ctx->o_tuple.p;
+  out->bary = ctx->o_bary.p;
+  out->contribution = ctx->o_contrib.p;
+  out->residual = ctx->o_resid.p;
+  out->flags = ctx->o_flags.p;
+  out->flagged_query = ctx->o_fquery.p;
+  out->flagged_tuple = ctx->o_ftuple.p;
+  out->flagged_flags = ctx->o_fflags.p;
+  out->per_query = ctx->o_per_query.p;
+  spoly_report& R = out->report;
+  R.n_pairs_in = counters[C_PAIRS];
+  R.n_systems = counters[C_SYSTEMS];
+  R.n_vroots = counters[C_VROOTS];
+  R.n_candidates = counters[C_CANDIDATES];
+  R.n_rej_domain = counters[C_REJ_DOMAIN];
+  R.n_rej_constraint = counters[C_REJ_CONSTRAINT];
+  R.n_rej_side = counters[C_REJ_SIDE];
+  R.n_rej_kappa = counters[C_REJ_KAPPA];
+  R.n_flagged = counters[C_FLAGGED];
+  R.n_admissible = counters[C_ADMISSIBLE];
+  cudaEventElapsedTime(&R.ms_cull, ctx->ev[0], ctx->ev[1]);
+  cudaEventElapsedTime(&R.ms_solve, ctx->ev[1], ctx->ev[2]);
+  cudaEventElapsedTime(&R.ms_reduce, ctx->ev[2], ctx->ev[3]);
+  R.n_launches = ctx->launches;
+  R.n_eval_terms = counters[C_EVAL_TERMS];
+  return SPOLY_OK;
+}
+
+spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces,
+                              const double* ep_host, uint32_t nq, const double* int_host, double* per_query_host,
+                              spoly_result* out) {
+  if (!ctx || !ep_host || !per_query_host) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
+  CK(cudaSetDevice(ctx->device));
+  const size_t need = 7ull * nq;
+  if (ctx->h_pinned_cap < need) {
+    if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
+    ctx->h_pinned = nullptr;
+    CK(cudaMallocHost(&ctx->h_pinned, need * sizeof(double)));
+    ctx->h_pinned_cap = need;
+  }
+  CK(ctx->d_ep.ensure(6ull * nq));
+  memcpy(ctx->h_pinned, ep_host, sizeof(double) * 6ull * nq);
+  CK(cudaMemcpyAsync(ctx->d_ep.p, ctx->h_pinned, sizeof(double) * 6ull * nq, cudaMemcpyHostToDevice, ctx->st));
+  const double* dint = nullptr;
+  if (int_host) {
+    CK(ctx->d_int.ensure(nq));
+    memcpy(ctx->h_pinned + 6ull * nq, int_host, sizeof(double) * nq);
+    CK(cudaMemcpyAsync(ctx->d_int.p, ctx->h_pinned + 6ull * nq, sizeof(double) * nq, cudaMemcpyHostToDevice, ctx->st));
+    dint = ctx->d_int.p;
+  }
+  spoly_result tmp;
+  spoly_result* r = out ? out : &tmp;
+  spoly_status s = spoly_solve(ctx, mesh_id, chain, bounces, ctx->d_ep.p, nq, dint, nullptr, r);
+  if (s != SPOLY_OK) return s;
+  CK(cudaMemcpyAsync(ctx->h_pinned, r->per_query, sizeof(double) * nq, cudaMemcpyDeviceToHost, ctx->st));
+  CK(cudaStreamSynchronize(ctx->st));
+  memcpy(per_query_host, ctx->h_pinned, sizeof(double) * nq);
+  return SPOLY_OK;
+}
+
+spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pq, const uint32_t** pt, uint64_t* n) {
+  if (!ctx || !pq || !pt || !n) return SPOLY_ERR_INVALID_ARG;
+  spoly_ctx* c = const_cast<spoly_ctx*>(ctx);
+  if (c->d_pt_orig.ensure(std::max<uint64_t>(c->npairs, 1)) != cudaSuccess) return SPOLY_ERR_OOM;
+  launch_map_ids(c->d_pt.p, c->npairs, c->M.orig_id, c->d_pt_orig.p, c->st);
+  if (cudaStreamSynchronize(c->st) != cudaSuccess) return SPOLY_ERR_CUDA;
+  *pq = c->d_pq.p;
+  *pt = c->d_pt_orig.p;
+  *n = c->npairs;
+  return SPOLY_OK;
+}
+
+spoly_status spoly_bench_fma(spoly_ctx* ctx, int fp64, double seconds, double* flops) {
+  if (!ctx || !flops) return SPOLY_ERR_INVALID_ARG;
+  CK(cudaSetDevice(ctx->device));
+  double* sink = nullptr;
+  CK(cudaMalloc(&sink, sizeof(double)));
+  int blocks, threads, fpt;
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  int iters = 256;
+  float ms = 0;
+  for (int rep = 0; rep < 8; ++rep) {
+    cudaEventRecord(a, ctx->st);
+    launch_fma_peak(fp64, iters, sink, ctx->nsm, ctx->st, &blocks, &threads, &fpt);
+    cudaEventRecord(b, ctx->st);
+    CK(cudaEventSynchronize(b));
+    cudaEventElapsedTime(&ms, a, b);
+    if (ms > 1000.0 * seconds * 0.5) break;
+    iters = (int)std::min(1e9, iters * std::max(2.0, 1000.0 * seconds / std::max(ms, 0.01f)));
+  }
+  *flops = (double)blocks * threads * fpt * (double)iters / (ms * 1e-3);
+  cudaEventDestroy(a);
+  cudaEventDestroy(b);
+  cudaFree(sink);
+  return SPOLY_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,107 @@
+// Shared device-side definitions of the CUDA path (libspoly.so).  Nothing here is shared with the
+// oracle: the oracle is a separate plain-C++ program used only by the tests.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/spoly.h"
+
+namespace spoly {
+
+// ----------------------------------------------------------------------------- FP64 3-vectors
+struct d3 {
+  double x, y, z;
+};
+__host__ __device__ __forceinline__ d3 mk3(double x, double y, double z) { return {x, y, z}; }
+__host__ __device__ __forceinline__ d3 operator+(d3 a, d3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__host__ __device__ __forceinline__ d3 operator-(d3 a, d3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__host__ __device__ __forceinline__ d3 operator*(double s, d3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__host__ __device__ __forceinline__ double dot(d3 a, d3 b) { return fma(a.x, b.x, fma(a.y, b.y, a.z * b.z)); }
+__host__ __device__ __forceinline__ d3 cross(d3 a, d3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+__host__ __device__ __forceinline__ double norm(d3 a) { return sqrt(dot(a, a)); }
+__host__ __device__ __forceinline__ d3 normalize(d3 a) { return (1.0 / norm(a)) * a; }
+
+// ----------------------------------------------------------------------------- FP32 3-vectors
+struct f3 {
+  float x, y, z;
+};
+__device__ __forceinline__ f3 operator+(f3 a, f3 b) { return {a.x + b.x, a.y + b.y, a.z + b.z}; }
+__device__ __forceinline__ f3 operator-(f3 a, f3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+__device__ __forceinline__ f3 operator*(float s, f3 a) { return {s * a.x, s * a.y, s * a.z}; }
+__device__ __forceinline__ float dotf(f3 a, f3 b) { return fmaf(a.x, b.x, fmaf(a.y, b.y, a.z * b.z)); }
+__device__ __forceinline__ f3 crossf(f3 a, f3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+// ----------------------------------------------------------------------------- mesh records
+// Per-triangle solve record: the float32 input vertices and vertex normals of P_i, N_i
+// (PAPER.md:186), de-indexed, 5 x float4 = 80 B, triangles stored in Morton (cluster) order.
+//   r0 = (p0.x p0.y p0.z p1.x)  r1 = (p1.y p1.z p2.x p2.y)  r2 = (p2.z n0.x n0.y n0.z)
+//   r3 = (n1.x n1.y n1.z n2.x)  r4 = (n2.y n2.z orig_id(bits) 0)
+struct TriRec {
+  float4 r[5];
+};
+// Per-cluster cull bounds (FP32): bounding sphere (c, rho) and normal cone (axis, cos, sin of the
+// half angle); valid = cone half angle < 90 deg.
+struct ClusterRec {
+  float4 sphere;  // c.xyz, rho
+  float4 cone;    // axis.xyz, theta (radians; >= pi/2 means "no bound")
+};
+constexpr int kClusterSize = 64;
+
+struct DeviceMesh {
+  uint32_t ntris = 0;
+  uint32_t nclusters = 0;
+  float eta_front = 1, eta_back = 1;
+  TriRec* tris = nullptr;       // [ntris], Morton order
+  float4* tricone = nullptr;    // [ntris] normal cone axis.xyz, theta
+  uint32_t* orig_id = nullptr;  // [ntris] Morton position -> original id
+  uint32_t* perm_of = nullptr;  // [ntris] original id -> Morton position
+  ClusterRec* clusters = nullptr;
+};
+
+__device__ __forceinline__ void load_tri(const TriRec* __restrict__ T, uint32_t i, d3 p[3], d3 n[3]) {
+  const float4* r = T[i].r;
+  float4 a = __ldg(r + 0), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+  p[0] = mk3(a.x, a.y, a.z);
+  p[1] = mk3(a.w, b.x, b.y);
+  p[2] = mk3(b.z, b.w, c.x);
+  n[0] = mk3(c.y, c.z, c.w);
+  n[1] = mk3(d.x, d.y, d.z);
+  n[2] = mk3(d.w, e.x, e.y);
+}
+
+// ----------------------------------------------------------------------------- solve parameters
+struct SolveParams {
+  double bisect_tol, theta_admit, theta_final, eps_domain, eps_flag, tau_trunc;
+  int pieces, scan_bisect_iters, polish_iters;
+  double eta_front, eta_back;
+};
+
+// solution sink (ctx-owned, appended with warp-aggregated atomics)
+struct SolSink {
+  unsigned long long* count;  // [1]
+  uint64_t capacity;
+  unsigned long long* key;    // (pair index << 6) | slot
+  uint32_t* query;
+  uint32_t* tuple;  // k per solution (original ids)
+  double* bary;     // 2k per solution
+  double* contrib;
+  float* resid;
+  uint32_t* flags;
+  // flagged tuples
+  unsigned long long* fcount;
+  uint64_t fcapacity;
+  unsigned long long* fkey;
+  uint32_t* fquery;
+  uint32_t* ftuple;
+  uint32_t* fflags;
+  unsigned long long* counters;  // [C_NUM]
+};
+
+enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,
+       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_NUM };
+
+}  // namespace spoly

@@ -1,0 +1,91 @@
+// Deterministic compaction: sort the appended solutions by their key
+// (pair index << 6 | root slot), gather the records into that order, then sum the contributions
+// per query in a fixed order ("we sum the contributions from all of them").
+#include <cub/cub.cuh>
+
+#include "kernels.cuh"
+
+namespace spoly {
+
+__global__ void k_iota(uint32_t* v, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    v[i] = (uint32_t)i;
+}
+void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st) {
+  if (n) k_iota<<<1024, 256, 0, st>>>(v, n);
+}
+
+__global__ void k_map_ids(const uint32_t* __restrict__ tpos, uint64_t n, const uint32_t* __restrict__ orig,
+                          uint32_t* out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = orig[tpos[i]];
+}
+void launch_map_ids(const uint32_t* tpos, uint64_t n, const uint32_t* orig_id, uint32_t* out, cudaStream_t st) {
+  if (n) k_map_ids<<<1024, 256, 0, st>>>(tpos, n, orig_id, out);
+}
+
+__global__ void k_gather_solutions(const uint32_t* __restrict__ perm, uint64_t n, int k, SolSink in, SolSink out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = perm[i];
+    out.query[i] = in.query[s];
+    for (int j = 0; j < k; ++j) out.tuple[(uint64_t)k * i + j] = in.tuple[(uint64_t)k * s + j];
+    for (int j = 0; j < 2 * k; ++j) out.bary[(uint64_t)2 * k * i + j] = in.bary[(uint64_t)2 * k * s + j];
+    out.contrib[i] = in.contrib[s];
+    out.resid[i] = in.resid[s];
+    out.flags[i] = in.flags[s];
+  }
+}
+void launch_gather_solutions(const uint32_t* perm, uint64_t n, int k, const SolSink& in, const SolSink& out,
+                             cudaStream_t st) {
+  if (n) k_gather_solutions<<<2048, 256, 0, st>>>(perm, n, k, in, out);
+}
+
+__global__ void k_gather_flagged(const uint32_t* __restrict__ perm, uint64_t n, int k, SolSink in, SolSink out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = perm[i];
+    out.fquery[i] = in.fquery[s];
+    for (int j = 0; j < k; ++j) out.ftuple[(uint64_t)k * i + j] = in.ftuple[(uint64_t)k * s + j];
+    out.fflags[i] = in.fflags[s];
+  }
+}
+void launch_gather_flagged(const uint32_t* perm, uint64_t n, int k, const SolSink& in, const SolSink& out,
+                           cudaStream_t st) {
+  if (n) k_gather_flagged<<<256, 256, 0, st>>>(perm, n, k, in, out);
+}
+
+// one warp per query: binary-search its range in the query-sorted solution list, then a fixed-order
+// sum (lane-strided partial sums + fixed xor tree) -> bit-reproducible per-query totals.
+__global__ void k_per_query_sorted(const uint32_t* __restrict__ query, const double* __restrict__ contrib, uint64_t n,
+                                   uint32_t nq, double* per_query) {
+  const int lane = threadIdx.x & 31;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  for (uint64_t q = gw; q < nq; q += nw) {
+    uint64_t lo = 0, hi = n;
+    while (lo < hi) {
+      uint64_t m = (lo + hi) >> 1;
+      if (query[m] < q) lo = m + 1; else hi = m;
+    }
+    uint64_t b = lo;
+    hi = n;
+    while (lo < hi) {
+      uint64_t m = (lo + hi) >> 1;
+      if (query[m] <= q) lo = m + 1; else hi = m;
+    }
+    const uint64_t e = lo;
+    double s = 0.0;
+    for (uint64_t i = b + lane; i < e; i += 32) s += contrib[i];
+#pragma unroll
+    for (int off = 16; off; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off);
+    if (lane == 0) per_query[q] = s;
+  }
+}
+void launch_per_query_sorted(const uint32_t* query, const double* contrib, uint64_t n, uint32_t nq, double* per_query,
+                             cudaStream_t st) {
+  if (!nq) return;
+  uint64_t blocks = ((uint64_t)nq * 32 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  k_per_query_sorted<<<(int)blocks, 256, 0, st>>>(query, contrib, n, nq, per_query);
+}
+
+}  // namespace spoly

@@ -1,0 +1,246 @@
+"""Thin ctypes binding of libspoly.so with the names of include/spoly.h.
+
+Argument marshalling only: every step of the hot path runs in the CUDA kernels behind the C-ABI.
+Device inputs are torch CUDA tensors (their data_ptr()); device outputs are returned as zero-copy
+torch views of the ctx-owned buffers (valid until the next solve / destroy; clone() to keep).
+There is no CPU fallback: importing on a machine without the built library raises.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libspoly.so")
+
+SPOLY_OK = 0
+STATUS = {0: "SPOLY_OK", 1: "SPOLY_ERR_INVALID_ARG", 2: "SPOLY_ERR_BAD_MESH", 3: "SPOLY_ERR_UNSUPPORTED_CHAIN",
+          4: "SPOLY_ERR_OOM", 5: "SPOLY_ERR_CAPACITY", 6: "SPOLY_ERR_CUDA"}
+FLAG_NEAR_TANGENT, FLAG_BOUNDARY, FLAG_RESIDUAL, FLAG_DEGENERATE = 1, 2, 4, 8
+
+EXPORTS = ["spoly_default_config", "spoly_create", "spoly_destroy", "spoly_last_error", "spoly_upload_mesh",
+           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma"]
+
+
+class SpolyError(RuntimeError):
+    pass
+
+
+class spoly_config(ctypes.Structure):
+    _fields_ = [("pieces", ctypes.c_int), ("scan_bisect_iters", ctypes.c_int), ("bisect_tol", ctypes.c_double),
+                ("polish_iters", ctypes.c_int), ("theta_admit", ctypes.c_double), ("theta_final", ctypes.c_double),
+                ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
+                ("cull", ctypes.c_int), ("deterministic", ctypes.c_int), ("cull_margin", ctypes.c_float),
+                ("max_solutions", ctypes.c_uint64), ("max_pairs", ctypes.c_uint64)]
+
+
+class spoly_tuple_list(ctypes.Structure):
+    _fields_ = [("offsets", ctypes.c_void_p), ("tri_ids", ctypes.c_void_p)]
+
+
+REPORT_FIELDS = ["n_pairs_in", "n_systems", "n_vroots", "n_candidates", "n_rej_domain", "n_rej_constraint",
+                 "n_rej_side", "n_rej_kappa", "n_flagged", "n_admissible"]
+
+
+class spoly_report(ctypes.Structure):
+    _fields_ = [(f, ctypes.c_uint64) for f in REPORT_FIELDS] + [
+        ("ms_cull", ctypes.c_float), ("ms_solve", ctypes.c_float), ("ms_reduce", ctypes.c_float),
+        ("n_launches", ctypes.c_uint32), ("n_eval_terms", ctypes.c_uint64), ("required_solutions", ctypes.c_uint64)]
+
+
+class spoly_result(ctypes.Structure):
+    _fields_ = [("n_solutions", ctypes.c_uint64), ("n_flagged", ctypes.c_uint64), ("k", ctypes.c_int),
+                ("query", ctypes.c_void_p), ("tuple", ctypes.c_void_p), ("bary", ctypes.c_void_p),
+                ("contribution", ctypes.c_void_p), ("residual", ctypes.c_void_p), ("flags", ctypes.c_void_p),
+                ("flagged_query", ctypes.c_void_p), ("flagged_tuple", ctypes.c_void_p),
+                ("flagged_flags", ctypes.c_void_p), ("per_query", ctypes.c_void_p), ("report", spoly_report)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libspoly.so (must have been built by build.py / __graft_entry__.build())."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise SpolyError(f"{LIB_PATH} is missing: run `python -m paper_2405_13409_b200.build` "
+                             "(there is no CPU fallback)")
+        L = ctypes.CDLL(LIB_PATH)
+        P, I, U32, U64, D = ctypes.c_void_p, ctypes.c_int, ctypes.c_uint32, ctypes.c_uint64, ctypes.c_double
+        L.spoly_default_config.argtypes = [P]
+        L.spoly_create.argtypes = [I, P, P, P]
+        L.spoly_destroy.argtypes = [P]
+        L.spoly_destroy.restype = None
+        L.spoly_last_error.argtypes = [P]
+        L.spoly_last_error.restype = ctypes.c_char_p
+        L.spoly_upload_mesh.argtypes = [P, P, P, U32, P, U32, ctypes.c_float, ctypes.c_float, P]
+        L.spoly_solve.argtypes = [P, U32, ctypes.c_char_p, I, P, U32, P, P, P]
+        L.spoly_solve_host.argtypes = [P, U32, ctypes.c_char_p, I, P, U32, P, P, P]
+        L.spoly_last_worklist.argtypes = [P, P, P, P]
+        L.spoly_bench_fma.argtypes = [P, I, D, P]
+        _lib = L
+    return _lib
+
+
+def default_config(**kw) -> spoly_config:
+    c = spoly_config()
+    lib().spoly_default_config(ctypes.byref(c))
+    for k, v in kw.items():
+        setattr(c, k, v)
+    return c
+
+
+class _CudaArray:
+    """__cuda_array_interface__ shim for zero-copy torch views of ctx-owned device memory."""
+
+    def __init__(self, ptr, shape, typestr):
+        self.__cuda_array_interface__ = {"data": (int(ptr or 0), False), "shape": tuple(shape), "typestr": typestr,
+                                         "version": 3, "strides": None}
+
+
+def _view(ptr, shape, typestr, device):
+    import torch
+    n = int(np.prod(shape)) if len(shape) else 1
+    dt = {"<u4": torch.int32, "<f8": torch.float64, "<f4": torch.float32}[typestr]
+    if n == 0 or not ptr:
+        return torch.zeros(shape, dtype=dt, device=device)
+    return torch.as_tensor(_CudaArray(ptr, shape, typestr), device=device)
+
+
+@dataclass
+class Result:
+    """Device-side result (torch views).  query/tuple/flags are int32 views of uint32 data."""
+    n_solutions: int
+    n_flagged: int
+    k: int
+    query: object
+    tuple: object
+    bary: object
+    contribution: object
+    residual: object
+    flags: object
+    flagged_query: object
+    flagged_tuple: object
+    flagged_flags: object
+    per_query: object
+    report: dict
+
+    def to_numpy(self):
+        out = {}
+        for f in ("query", "tuple", "bary", "contribution", "residual", "flags", "flagged_query", "flagged_tuple",
+                  "flagged_flags", "per_query"):
+            a = getattr(self, f).cpu().numpy()
+            if a.dtype == np.int32:
+                a = a.view(np.uint32)
+            out[f] = a
+        return out
+
+
+class Context:
+    """RAII wrapper of spoly_ctx (one per device / process)."""
+
+    def __init__(self, device: int = 0, config: spoly_config = None, stream=None):
+        self._L = lib()
+        self.device = device
+        h = ctypes.c_void_p()
+        st = None
+        if stream is not None:
+            st = ctypes.c_void_p(int(stream.cuda_stream if hasattr(stream, "cuda_stream") else stream))
+        rc = self._L.spoly_create(device, ctypes.byref(config) if config is not None else None, st, ctypes.byref(h))
+        if rc != SPOLY_OK:
+            raise SpolyError(f"spoly_create: {STATUS.get(rc, rc)}")
+        self._h = h
+        self.k = None
+        self.nq = 0
+
+    def _check(self, rc, what):
+        if rc != SPOLY_OK:
+            msg = self._L.spoly_last_error(self._h)
+            raise SpolyError(f"{what}: {STATUS.get(rc, rc)}: {msg.decode() if msg else ''}")
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._L.spoly_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    def upload_mesh(self, mesh) -> int:
+        pos = np.ascontiguousarray(mesh.pos, dtype=np.float32)
+        nrm = np.ascontiguousarray(mesh.nrm, dtype=np.float32)
+        tri = np.ascontiguousarray(mesh.tri, dtype=np.uint32)
+        mid = ctypes.c_uint32()
+        rc = self._L.spoly_upload_mesh(self._h, pos.ctypes.data, nrm.ctypes.data, pos.shape[0], tri.ctypes.data,
+                                       tri.shape[0], float(mesh.eta_front), float(mesh.eta_back), ctypes.byref(mid))
+        self._check(rc, "spoly_upload_mesh")
+        return mid.value
+
+    def _wrap(self, r: spoly_result, nq: int):
+        dev = f"cuda:{self.device}"
+        n, m, k = int(r.n_solutions), int(r.n_flagged), int(r.k)
+        rep = {f: int(getattr(r.report, f)) for f in REPORT_FIELDS}
+        rep.update(ms_cull=r.report.ms_cull, ms_solve=r.report.ms_solve, ms_reduce=r.report.ms_reduce,
+                   n_launches=int(r.report.n_launches), n_eval_terms=int(r.report.n_eval_terms))
+        return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
+                      _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
+                      _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),
+                      _view(r.flagged_query, (m,), "<u4", dev), _view(r.flagged_tuple, (m, k), "<u4", dev),
+                      _view(r.flagged_flags, (m,), "<u4", dev), _view(r.per_query, (nq,), "<f8", dev), rep)
+
+    def solve(self, chain: str, endpoints, intensity=None, offsets=None, tri_ids=None, mesh_id: int = 0) -> Result:
+        """endpoints: CUDA float64 tensor (Q,2,3); intensity: CUDA float64 (Q,) or None;
+        offsets/tri_ids: CUDA int32/uint32 CSR tuple list or None (cull pre-pass)."""
+        import torch
+        assert endpoints.is_cuda and endpoints.dtype == torch.float64 and endpoints.is_contiguous()
+        nq = int(endpoints.shape[0])
+        tl = None
+        if offsets is not None:
+            tl = spoly_tuple_list(offsets.data_ptr(), tri_ids.data_ptr())
+        r = spoly_result()
+        rc = self._L.spoly_solve(self._h, mesh_id, chain.encode(), len(chain), endpoints.data_ptr(), nq,
+                                 intensity.data_ptr() if intensity is not None else None,
+                                 ctypes.byref(tl) if tl is not None else None, ctypes.byref(r))
+        self._check(rc, "spoly_solve")
+        return self._wrap(r, nq)
+
+    def solve_host(self, chain: str, endpoints: np.ndarray, intensity: np.ndarray = None, mesh_id: int = 0):
+        """Host in, host out: returns (per_query numpy (Q,), Result device views)."""
+        ep = np.ascontiguousarray(endpoints, dtype=np.float64)
+        nq = ep.shape[0]
+        it = None if intensity is None else np.ascontiguousarray(intensity, dtype=np.float64)
+        pq = np.zeros(nq, np.float64)
+        r = spoly_result()
+        rc = self._L.spoly_solve_host(self._h, mesh_id, chain.encode(), len(chain), ep.ctypes.data, nq,
+                                      it.ctypes.data if it is not None else None, pq.ctypes.data, ctypes.byref(r))
+        self._check(rc, "spoly_solve_host")
+        return pq, self._wrap(r, nq)
+
+    def last_worklist(self):
+        """(pair_query, pair_tuple) of the last solve as int32 torch views (original triangle ids)."""
+        pq = ctypes.c_void_p()
+        pt = ctypes.c_void_p()
+        n = ctypes.c_uint64()
+        rc = self._L.spoly_last_worklist(self._h, ctypes.byref(pq), ctypes.byref(pt), ctypes.byref(n))
+        self._check(rc, "spoly_last_worklist")
+        dev = f"cuda:{self.device}"
+        return _view(pq.value, (n.value,), "<u4", dev), _view(pt.value, (n.value,), "<u4", dev)
+
+    def bench_fma(self, fp64: bool = True, seconds: float = 1.0) -> float:
+        f = ctypes.c_double()
+        rc = self._L.spoly_bench_fma(self._h, 1 if fp64 else 0, seconds, ctypes.byref(f))
+        self._check(rc, "spoly_bench_fma")
+        return f.value

@@ -1,0 +1,59 @@
+"""The C-ABI library builds for sm_100a, loads here (no GPU) and exports every symbol include/*.h declares."""
+import glob
+import os
+import re
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_symbols():
+    syms = set()
+    for h in glob.glob(os.path.join(ROOT, "include", "*.h")):
+        txt = open(h).read()
+        txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+        for m in re.finditer(r"\b(spoly_\w+)\s*\(", txt):
+            syms.add(m.group(1))
+    return syms
+
+
+def test_header_declares_the_boundary():
+    s = declared_symbols()
+    for f in ("spoly_create", "spoly_upload_mesh", "spoly_solve", "spoly_destroy"):
+        assert f in s
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2405_13409_b200 import build, spoly
+    lib = build.build()
+    out = subprocess.check_output(["nm", "-D", "--defined-only", lib]).decode()
+    exported = set(re.findall(r"\bT (spoly_\w+)", out))
+    missing = declared_symbols() - exported
+    assert not missing, missing
+    L = spoly.lib()
+    for s in declared_symbols():
+        getattr(L, s)
+    assert set(spoly.EXPORTS) <= declared_symbols()
+
+
+def test_library_is_sm100a():
+    from paper_2405_13409_b200 import build
+    lib = build.build()
+    out = subprocess.check_output(["/usr/local/cuda/bin/cuobjdump", "--list-elf", lib]).decode()
+    assert "sm_100a" in out
+
+
+def test_config_defaults_match_paper():
+    from paper_2405_13409_b200 import spoly
+    c = spoly.default_config()
+    assert c.pieces == 100 and c.scan_bisect_iters == 10
+    assert c.bisect_tol == 1e-9
+
+
+def test_no_oracle_import_in_product():
+    for f in glob.glob(os.path.join(ROOT, "paper_2405_13409_b200", "**", "*"), recursive=True):
+        if f.endswith((".py", ".cu", ".cuh", ".h")):
+            txt = open(f).read()
+            assert "import oracle" not in txt and "oracle/" not in txt.replace("oracle/ ", ""), f

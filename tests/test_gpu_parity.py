@@ -1,0 +1,141 @@
+"""GPU (CUDA path through the C-ABI) vs oracle parity — needs a B200.
+
+Inputs are the seeded synthetic workloads; the oracle is the plain FP64 CPU transcription.
+"""
+import numpy as np
+import pytest
+
+import parity
+from paper_2405_13409_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    return torch
+
+
+@pytest.fixture(scope="module")
+def sp(torch_cuda):
+    from paper_2405_13409_b200 import spoly
+    spoly.lib()
+    return spoly
+
+
+def _gpu_solve(sp, torch, mesh, chain, ep, cfg=None, offsets=None, tri_ids=None, intensity=None):
+    ctx = sp.Context(0, cfg)
+    ctx.upload_mesh(mesh)
+    e = torch.as_tensor(np.ascontiguousarray(ep), dtype=torch.float64, device="cuda")
+    it = None if intensity is None else torch.as_tensor(intensity, dtype=torch.float64, device="cuda")
+    off = None if offsets is None else torch.as_tensor(offsets.astype(np.int32), device="cuda")
+    ids = None if tri_ids is None else torch.as_tensor(tri_ids.astype(np.int32), device="cuda")
+    r = ctx.solve(chain, e, it, off, ids)
+    out = r.to_numpy()
+    out["report"] = r.report
+    wl = ctx.last_worklist()
+    out["worklist"] = (wl[0].cpu().numpy().view(np.uint32), wl[1].cpu().numpy().view(np.uint32))
+    ctx.close()
+    return out
+
+
+def test_c1_patch_parity(orc, sp, torch_cuda):
+    w = W.patch_c1()
+    ro = orc.solve(w.mesh, "R", w.endpoints, cfg=orc.default_config(cull=0))
+    g = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints, cfg=sp.default_config(cull=0))
+    st = parity.compare(ro, g, w.nqueries)
+    assert g["report"]["n_pairs_in"] == w.mesh.ntris
+    assert st["compared_solutions"] >= 1
+    # culled run finds the same chains
+    gc = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
+    parity.compare(ro, gc, w.nqueries)
+
+
+def test_random_interpolated_R(orc, sp, torch_cuda):
+    rng = np.random.default_rng(12)
+    mesh = W.random_triangles(rng, 300, 0.3, normal_tilt=0.3)
+    Q = 24
+    ep = np.zeros((Q, 2, 3))
+    ep[:, 0] = rng.uniform(-1, 1, (Q, 3)) * [1, 1, 0.3] + [0, 0, 1.5]
+    ep[:, 1] = rng.uniform(-1, 1, (Q, 3)) * [1, 1, 0.3] + [0, 0, 1.8]
+    inten = rng.uniform(0.5, 2.0, Q)
+    ro = orc.solve(mesh, "R", ep, intensity=inten, cfg=orc.default_config(cull=0))
+    g = _gpu_solve(sp, torch_cuda, mesh, "R", ep, cfg=sp.default_config(cull=0), intensity=inten)
+    st = parity.compare(ro, g, Q)
+    assert st["compared_solutions"] > 50, st
+    # with the cull on both sides
+    ro2 = orc.solve(mesh, "R", ep, intensity=inten)
+    g2 = _gpu_solve(sp, torch_cuda, mesh, "R", ep, intensity=inten)
+    parity.compare(ro2, g2, Q)
+    assert g2["report"]["n_pairs_in"] >= ro2.report["pairs_in"]  # FP32 cull at most more permissive
+
+
+def test_explicit_tuple_list_and_edges(orc, sp, torch_cuda):
+    w = W.patch_c1()
+    ep = np.repeat(w.endpoints, 3, axis=0)
+    ep[1, 1] += [0.05, -0.02, 0.0]
+    # ragged CSR: 0 tuples for query 2
+    ids = np.arange(0, 256, 3, dtype=np.uint32)
+    offsets = np.array([0, len(ids), 2 * len(ids), 2 * len(ids)], np.uint32)
+    tri_ids = np.concatenate([ids, ids])
+    ro = orc.solve(w.mesh, "R", ep, offsets=offsets, tri_ids=tri_ids)
+    g = _gpu_solve(sp, torch_cuda, w.mesh, "R", ep, offsets=offsets, tri_ids=tri_ids)
+    parity.compare(ro, g, 3)
+    assert g["per_query"][2] == 0.0
+    assert g["report"]["n_pairs_in"] == 2 * len(ids)
+
+
+def test_empty_and_errors(sp, torch_cuda):
+    torch = torch_cuda
+    w = W.patch_c1()
+    ctx = sp.Context(0)
+    ctx.upload_mesh(w.mesh)
+    r = ctx.solve("R", torch.zeros((0, 2, 3), dtype=torch.float64, device="cuda"))
+    assert r.n_solutions == 0
+    with pytest.raises(sp.SpolyError):
+        ctx.solve("Q", torch.zeros((1, 2, 3), dtype=torch.float64, device="cuda"))
+    bad = W.Mesh(np.zeros((3, 3), np.float32), np.tile([0, 0, 1], (3, 1)).astype(np.float32),
+                 np.array([[0, 1, 2]], np.uint32))
+    with pytest.raises(sp.SpolyError):
+        ctx.upload_mesh(bad)
+    ctx.close()
+
+
+def test_c2_subset_parity(orc, sp, torch_cuda):
+    """C2 glints mesh (100,352 tris), 24 light samples: cull + solve vs the oracle's own cull + solve."""
+    w = W.glints_c2(res=256)
+    sub = w.subset(np.arange(0, 65536, 65536 // 24)[:24])
+    ro = orc.solve(sub.mesh, "R", sub.endpoints)
+    g = _gpu_solve(sp, torch_cuda, sub.mesh, "R", sub.endpoints)
+    st = parity.compare(ro, g, sub.nqueries)
+    assert st["compared_solutions"] > 1000, st
+    assert st["flagged_tuples"] <= 0.01 * g["report"]["n_pairs_in"], st
+
+
+def test_c2_full_size_sampled(orc, sp, torch_cuda):
+    """Full C2 (65,536 queries) in the bench launch configuration; sampled queries re-solved by the oracle."""
+    w = W.glints_c2(res=256)
+    g = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
+    rng = np.random.default_rng(99)
+    qs = np.sort(rng.choice(w.nqueries, 6, replace=False))
+    sub = w.subset(qs)
+    ro = orc.solve(sub.mesh, "R", sub.endpoints)
+    # restrict the GPU result to the sampled queries, renumbered 0..5
+    sel = np.isin(g["query"], qs)
+    remap = {int(q): i for i, q in enumerate(qs)}
+    gs = {"query": np.array([remap[int(q)] for q in g["query"][sel]], np.uint32), "tuple": g["tuple"][sel],
+          "bary": g["bary"][sel], "per_query": g["per_query"][qs]}
+    fsel = np.isin(g["flagged_query"], qs)
+    gs["flagged_query"] = np.array([remap[int(q)] for q in g["flagged_query"][fsel]], np.uint32)
+    gs["flagged_tuple"] = g["flagged_tuple"][fsel]
+    gs["contribution"] = g["contribution"][sel]
+    st = parity.compare(ro, gs, len(qs))
+    assert st["compared_solutions"] > 100
+    # properties at full size: every returned vertex inside the triangle and specular (Eq. 3)
+    assert np.all(g["residual"] < 1e-6)
+    b = g["bary"]
+    assert np.all(b[:, 0] >= -1e-9) and np.all(b[:, 1] >= -1e-9) and np.all(b.sum(1) <= 1 + 1e-9)
+    assert abs(g["per_query"].sum() - g["contribution"].sum()) <= 1e-9 * abs(g["contribution"].sum())
