@@ -47,19 +47,19 @@ struct spoly_ctx {
   bool has_mesh = false;
   DeviceMesh M;
   DBuf<TriRec> d_tris;
-  DBuf<float4> d_tricone;
+  DBuf<TriCull> d_tcull;
   DBuf<uint32_t> d_orig, d_perm;
-  DBuf<ClusterRec> d_cl;
+  DBuf<ClusterRec> d_cl, d_sub;
+  DBuf<uint32_t> d_bits;
   // work list
   DBuf<uint64_t> d_counts;
   DBuf<unsigned long long> d_offsets;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig;
   uint64_t npairs = 0;
-  // raw sink
-  DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2;
-  DBuf<uint32_t> d_query, d_tuple, d_flags, d_fquery, d_ftuple, d_fflags, d_perm_in, d_perm_out, d_fperm_in,
-      d_fperm_out;
-  DBuf<double> d_bary, d_contrib;
+  // raw sink + job list
+  DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
+  DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
+  DBuf<double> d_bary, d_contrib, d_jr;
   DBuf<float> d_resid;
   // sorted output
   DBuf<uint32_t> o_query, o_tuple, o_flags, o_fquery, o_ftuple, o_fflags;
@@ -143,12 +143,13 @@ void spoly_destroy(spoly_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
-  ctx->d_tris.release(); ctx->d_tricone.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
+  ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
+  ctx->d_sub.release(); ctx->d_bits.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
-  ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_query.release(); ctx->d_tuple.release();
-  ctx->d_flags.release(); ctx->d_fquery.release(); ctx->d_ftuple.release(); ctx->d_fflags.release();
-  ctx->d_perm_in.release(); ctx->d_perm_out.release(); ctx->d_fperm_in.release(); ctx->d_fperm_out.release();
+  ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
+  ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
+  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
   ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
@@ -219,15 +220,16 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   CK(cudaMemcpyAsync(dnrm, nrm, sizeof(float) * 3ull * nverts, cudaMemcpyHostToDevice, ctx->st));
   CK(cudaMemcpyAsync(dtri, tri, sizeof(uint32_t) * 3ull * ntris, cudaMemcpyHostToDevice, ctx->st));
   CK(cudaMemcpyAsync(dorder, order.data(), sizeof(uint32_t) * ntris, cudaMemcpyHostToDevice, ctx->st));
-  const uint32_t ncl = (ntris + kClusterSize - 1) / kClusterSize;
+  const uint32_t ncl = (ntris + kClusterSize - 1) / kClusterSize, nsub = (ntris + kSubSize - 1) / kSubSize;
   CK(ctx->d_tris.ensure(ntris));
-  CK(ctx->d_tricone.ensure(ntris));
+  CK(ctx->d_tcull.ensure(ntris));
   CK(ctx->d_orig.ensure(ntris));
   CK(ctx->d_perm.ensure(ntris));
   CK(ctx->d_cl.ensure(ncl));
-  launch_build_tris(dpos, dnrm, dtri, dorder, ntris, ctx->d_tris.p, ctx->d_tricone.p, ctx->d_orig.p, ctx->d_perm.p,
-                    ctx->st);
-  launch_build_clusters(ctx->d_tris.p, ctx->d_tricone.p, ntris, ctx->d_cl.p, ctx->st);
+  CK(ctx->d_sub.ensure(nsub));
+  launch_build_tris(dpos, dnrm, dtri, dorder, ntris, ctx->cfg.cull_margin, ctx->d_tris.p, ctx->d_tcull.p,
+                    ctx->d_orig.p, ctx->d_perm.p, ctx->st);
+  launch_build_clusters(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, ctx->d_cl.p, ctx->d_sub.p, ctx->st);
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->st));
   cudaFree(dpos);
@@ -239,7 +241,8 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   ctx->M.eta_front = eta_front;
   ctx->M.eta_back = eta_back;
   ctx->M.tris = ctx->d_tris.p;
-  ctx->M.tricone = ctx->d_tricone.p;
+  ctx->M.tcull = ctx->d_tcull.p;
+  ctx->M.sub = ctx->d_sub.p;
   ctx->M.orig_id = ctx->d_orig.p;
   ctx->M.perm_of = ctx->d_perm.p;
   ctx->M.clusters = ctx->d_cl.p;
@@ -253,17 +256,11 @@ static SolSink raw_sink(spoly_ctx* ctx) {
   S.count = ctx->d_count.p;
   S.capacity = ctx->d_key.cap;
   S.key = ctx->d_key.p;
-  S.query = ctx->d_query.p;
-  S.tuple = ctx->d_tuple.p;
   S.bary = ctx->d_bary.p;
   S.contrib = ctx->d_contrib.p;
   S.resid = ctx->d_resid.p;
-  S.flags = ctx->d_flags.p;
-  S.fcount = ctx->d_count.p + 1;
   S.fcapacity = ctx->d_fkey.cap;
   S.fkey = ctx->d_fkey.p;
-  S.fquery = ctx->d_fquery.p;
-  S.ftuple = ctx->d_ftuple.p;
   S.fflags = ctx->d_fflags.p;
   S.counters = ctx->d_counters.p;
   return S;
@@ -271,24 +268,20 @@ static SolSink raw_sink(spoly_ctx* ctx) {
 
 static spoly_status ensure_sink(spoly_ctx* ctx, uint64_t nsol, uint64_t nflag, int k) {
   CK(ctx->d_key.ensure(nsol));
-  CK(ctx->d_query.ensure(nsol));
-  CK(ctx->d_tuple.ensure(nsol * k));
   CK(ctx->d_bary.ensure(nsol * 2 * k));
   CK(ctx->d_contrib.ensure(nsol));
   CK(ctx->d_resid.ensure(nsol));
-  CK(ctx->d_flags.ensure(nsol));
   CK(ctx->d_fkey.ensure(nflag));
-  CK(ctx->d_fquery.ensure(nflag));
-  CK(ctx->d_ftuple.ensure(nflag * k));
   CK(ctx->d_fflags.ensure(nflag));
   // keep all arrays at equal capacity so S.capacity bounds every write
-  uint64_t cap = std::min({ctx->d_key.cap, ctx->d_query.cap, ctx->d_contrib.cap, ctx->d_resid.cap, ctx->d_flags.cap,
-                           ctx->d_tuple.cap / k, ctx->d_bary.cap / (2 * k)});
-  uint64_t fcap = std::min({ctx->d_fkey.cap, ctx->d_fquery.cap, ctx->d_fflags.cap, ctx->d_ftuple.cap / k});
-  ctx->d_key.cap = cap;
-  ctx->d_fkey.cap = fcap;
+  ctx->d_key.cap = std::min({ctx->d_key.cap, ctx->d_contrib.cap, ctx->d_resid.cap, ctx->d_bary.cap / (2 * k)});
+  ctx->d_fkey.cap = std::min(ctx->d_fkey.cap, ctx->d_fflags.cap);
   return SPOLY_OK;
 }
+
+struct BitOr {
+  __host__ __device__ uint32_t operator()(uint32_t a, uint32_t b) const { return a | b; }
+};
 
 static int bits_for(uint64_t n) {
   int b = 1;
@@ -327,19 +320,14 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else if (ctx->cfg.cull) {
+    const uint32_t words = 2 * ctx->M.nclusters;
     CK(ctx->d_counts.ensure(nq));
     CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
-    CullParams cp;
-    cp.margin = ctx->cfg.cull_margin;
-    cp.refract = chain[0] == 'T';
-    cp.eta_front = ctx->M.eta_front;
-    cp.eta_back = ctx->M.eta_back;
-    CK(cudaMemsetAsync(ctx->d_counts.p, 0, sizeof(uint64_t) * nq, st));
-    launch_cull_k1(0, endpoints, nq, ctx->M, cp, reinterpret_cast<uint32_t*>(ctx->d_counts.p), nullptr, nullptr,
-                   nullptr, ctx->nsm, st);
+    CK(ctx->d_bits.ensure((uint64_t)nq * words));
+    CK(cudaMemsetAsync(ctx->d_bits.p, 0, sizeof(uint32_t) * (uint64_t)nq * words, st));
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+    launch_cull_bits(endpoints, nq, ctx->M, chain[0] == 'T', ctx->d_bits.p, words, c32, ctx->nsm, st);
     ctx->launches++;
-    // counts were written as u32 into a u64-sized buffer: widen by scanning the u32 view
-    const uint32_t* c32 = reinterpret_cast<const uint32_t*>(ctx->d_counts.p);
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
     CK(ctx->d_temp.ensure(tbytes));
@@ -351,7 +339,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     npairs = tot;
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
-    launch_cull_k1(1, endpoints, nq, ctx->M, cp, nullptr, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    launch_expand_bits(ctx->d_bits.p, words, nq, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else {
     npairs = (uint64_t)nq * ctx->M.ntris;
@@ -380,13 +368,23 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   spoly_status s = ensure_sink(ctx, std::max<uint64_t>(ctx->d_key.cap, ctx->cfg.max_solutions),
                                std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
   if (s != SPOLY_OK) return s;
-  unsigned long long cnt[2] = {0, 0};
+  CK(ctx->d_count.ensure(3));
+  CK(ctx->d_jpair.ensure(npairs));
+  CK(ctx->d_jmeta.ensure(npairs));
+  CK(ctx->d_jr.ensure(npairs * 10));
+  unsigned long long cnt[3] = {0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
-    CK(cudaMemsetAsync(ctx->d_count.p, 0, 2 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_count.p, 0, 3 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(ctx->d_counters.p, 0, C_NUM * sizeof(unsigned long long), st));
     SolSink S = raw_sink(ctx);
-    launch_solve_R_list(ctx->d_pq.p, ctx->d_pt.p, npairs, 0, ctx->M, endpoints, inten, prm, S, ctx->nsm, st);
-    ctx->launches++;
+    JobSink J;
+    J.count = ctx->d_count.p + 2;
+    J.capacity = std::min(ctx->d_jpair.cap, ctx->d_jr.cap / 10);
+    J.pair = ctx->d_jpair.p;
+    J.meta = ctx->d_jmeta.p;
+    J.r = ctx->d_jr.p;
+    launch_solve_R(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J, ctx->nsm, st);
+    ctx->launches += 2;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -401,34 +399,60 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(cudaEventRecord(ctx->ev[2], st));
 
   // ---------------- deterministic order + per-query sums
-  const uint64_t n = cnt[0], nf = cnt[1];
+  const uint64_t n = cnt[0], nf_raw = cnt[1];
   CK(ctx->o_query.ensure(n));
   CK(ctx->o_tuple.ensure(n * k));
   CK(ctx->o_bary.ensure(n * 2 * k));
   CK(ctx->o_contrib.ensure(n));
   CK(ctx->o_resid.ensure(n));
   CK(ctx->o_flags.ensure(n));
-  CK(ctx->o_fquery.ensure(nf));
-  CK(ctx->o_ftuple.ensure(nf * k));
-  CK(ctx->o_fflags.ensure(nf));
   CK(ctx->d_key2.ensure(n));
   CK(ctx->d_perm_in.ensure(n));
   CK(ctx->d_perm_out.ensure(n));
-  CK(ctx->d_fkey2.ensure(nf));
-  CK(ctx->d_fperm_in.ensure(nf));
-  CK(ctx->d_fperm_out.ensure(nf));
-  SolSink in = raw_sink(ctx), o;
+  CK(ctx->d_fkey2.ensure(nf_raw));
+  CK(ctx->d_fflags2.ensure(nf_raw));
+  CK(ctx->d_upair.ensure(nf_raw));
+  CK(ctx->d_uflags.ensure(nf_raw));
+  CK(ctx->d_nruns.ensure(1));
+  SolSink in = raw_sink(ctx);
+  OutArrays o;
   memset(&o, 0, sizeof(o));
   o.query = ctx->o_query.p;
   o.tuple = ctx->o_tuple.p;
+  o.flags = ctx->o_flags.p;
   o.bary = ctx->o_bary.p;
   o.contrib = ctx->o_contrib.p;
   o.resid = ctx->o_resid.p;
-  o.flags = ctx->o_flags.p;
-  o.fquery = ctx->o_fquery.p;
-  o.ftuple = ctx->o_ftuple.p;
-  o.fflags = ctx->o_fflags.p;
   const int end_bit = std::min(64, 6 + bits_for(npairs));
+  const int fbits = std::min(64, bits_for(npairs));
+  // flags: sort the per-pair records, OR-reduce by pair
+  uint64_t nf = 0;
+  if (nf_raw) {
+    size_t tb = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fflags.p, ctx->d_fflags2.p,
+                                       (int64_t)nf_raw, 0, fbits, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fflags.p,
+                                       ctx->d_fflags2.p, (int64_t)nf_raw, 0, fbits, st));
+    tb = 0;
+    CK(cub::DeviceReduce::ReduceByKey(nullptr, tb, ctx->d_fkey2.p, ctx->d_upair.p, ctx->d_fflags2.p, ctx->d_uflags.p,
+                                      ctx->d_nruns.p, BitOr(), (int64_t)nf_raw, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceReduce::ReduceByKey(ctx->d_temp.p, tb, ctx->d_fkey2.p, ctx->d_upair.p, ctx->d_fflags2.p,
+                                      ctx->d_uflags.p, ctx->d_nruns.p, BitOr(), (int64_t)nf_raw, st));
+    unsigned long long nr = 0;
+    CK(cudaMemcpyAsync(&nr, ctx->d_nruns.p, sizeof(nr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    nf = nr;
+    CK(ctx->o_fquery.ensure(nf));
+    CK(ctx->o_ftuple.ensure(nf * k));
+    CK(ctx->o_fflags.ensure(nf));
+    o.fquery = ctx->o_fquery.p;
+    o.ftuple = ctx->o_ftuple.p;
+    o.fflags = ctx->o_fflags.p;
+    launch_gather_flagged(ctx->d_upair.p, ctx->d_uflags.p, nf, k, ctx->d_pq.p, ctx->d_pt.p, ctx->M.orig_id, o, st);
+    ctx->launches++;
+  }
   if (n) {
     launch_iota(ctx->d_perm_in.p, n, st);
     ctx->launches++;
@@ -438,21 +462,10 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(ctx->d_temp.ensure(tb));
     CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p,
                                        ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
-    launch_gather_solutions(ctx->d_perm_out.p, n, k, in, o, st);
-    ctx->launches++;
-  }
-  if (nf) {
-    launch_iota(ctx->d_fperm_in.p, nf, st);
-    ctx->launches++;
-    size_t tb = 0;
-    const int fbits = std::min(64, bits_for(npairs));
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fperm_in.p,
-                                       ctx->d_fperm_out.p, (int64_t)nf, 0, fbits, st));
-    CK(ctx->d_temp.ensure(tb));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_fkey.p, ctx->d_fkey2.p, ctx->d_fperm_in.p,
-                                       ctx->d_fperm_out.p, (int64_t)nf, 0, fbits, st));
-    launch_gather_flagged(ctx->d_fperm_out.p, nf, k, in, o, st);
-    ctx->launches++;
+    launch_gather_solutions(ctx->d_perm_out.p, ctx->d_key2.p, n, k, in, ctx->d_pq.p, ctx->d_pt.p, ctx->M.orig_id, o,
+                            st);
+    launch_solution_flags(ctx->d_key2.p, n, ctx->d_upair.p, ctx->d_uflags.p, nf, o.flags, st);
+    ctx->launches += 2;
   }
   launch_per_query_sorted(ctx->o_query.p, ctx->o_contrib.p, n, nq, ctx->o_per_query.p, st);
   ctx->launches++;
@@ -483,7 +496,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_rej_constraint = counters[C_REJ_CONSTRAINT];
   R.n_rej_side = counters[C_REJ_SIDE];
   R.n_rej_kappa = counters[C_REJ_KAPPA];
-  R.n_flagged = counters[C_FLAGGED];
+  R.n_flagged = nf;
   R.n_admissible = counters[C_ADMISSIBLE];
   cudaEventElapsedTime(&R.ms_cull, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&R.ms_solve, ctx->ev[1], ctx->ev[2]);

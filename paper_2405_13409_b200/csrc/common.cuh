@@ -21,7 +21,7 @@ __host__ __device__ __forceinline__ d3 cross(d3 a, d3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 __host__ __device__ __forceinline__ double norm(d3 a) { return sqrt(dot(a, a)); }
-__host__ __device__ __forceinline__ d3 normalize(d3 a) { return (1.0 / norm(a)) * a; }
+__host__ __device__ __forceinline__ d3 normalize(d3 a) { return rsqrt(dot(a, a)) * a; }
 
 // ----------------------------------------------------------------------------- FP32 3-vectors
 struct f3 {
@@ -43,23 +43,30 @@ __device__ __forceinline__ f3 crossf(f3 a, f3 b) {
 struct TriRec {
   float4 r[5];
 };
-// Per-cluster cull bounds (FP32): bounding sphere (c, rho) and normal cone (axis, cos, sin of the
-// half angle); valid = cone half angle < 90 deg.
+// Cull nodes (FP32).  Bounding sphere (c, rho) and normal cone (axis, sin(beta)) where beta is the cone
+// half angle of the (normalised) vertex normals plus the cull margin; sin(beta) = 1 means "no bound".
 struct ClusterRec {
   float4 sphere;  // c.xyz, rho
-  float4 cone;    // axis.xyz, theta (radians; >= pi/2 means "no bound")
+  float4 cone;    // axis.xyz, sin(beta)
 };
-constexpr int kClusterSize = 64;
+struct TriCull {
+  float4 sphere;  // centroid, rho
+  float4 cone;    // axis.xyz, sin(beta)
+  float4 plane;   // geometric normal g = e1 x e2 (unnormalised), g . p0
+};
+constexpr int kClusterSize = 64;  // level-1 cull cluster (Morton-consecutive triangles)
+constexpr int kSubSize = 8;       // level-2 sub-cluster
 
 struct DeviceMesh {
   uint32_t ntris = 0;
   uint32_t nclusters = 0;
   float eta_front = 1, eta_back = 1;
-  TriRec* tris = nullptr;       // [ntris], Morton order
-  float4* tricone = nullptr;    // [ntris] normal cone axis.xyz, theta
-  uint32_t* orig_id = nullptr;  // [ntris] Morton position -> original id
-  uint32_t* perm_of = nullptr;  // [ntris] original id -> Morton position
-  ClusterRec* clusters = nullptr;
+  TriRec* tris = nullptr;         // [ntris], Morton order
+  TriCull* tcull = nullptr;       // [ntris]
+  uint32_t* orig_id = nullptr;    // [ntris] Morton position -> original id
+  uint32_t* perm_of = nullptr;    // [ntris] original id -> Morton position
+  ClusterRec* clusters = nullptr; // [ceil(ntris/64)]
+  ClusterRec* sub = nullptr;      // [ceil(ntris/8)]
 };
 
 __device__ __forceinline__ void load_tri(const TriRec* __restrict__ T, uint32_t i, d3 p[3], d3 n[3]) {
@@ -80,25 +87,27 @@ struct SolveParams {
   double eta_front, eta_back;
 };
 
-// solution sink (ctx-owned, appended with warp-aggregated atomics)
+// solution sink (ctx-owned, appended with warp-aggregated atomics).  Records carry only the sort key
+// (pair index << 6 | root slot); query and triangle ids are recovered from the work list at gather time.
 struct SolSink {
-  unsigned long long* count;  // [1]
+  unsigned long long* count;  // [0] solutions, [1] flag records
   uint64_t capacity;
-  unsigned long long* key;    // (pair index << 6) | slot
-  uint32_t* query;
-  uint32_t* tuple;  // k per solution (original ids)
-  double* bary;     // 2k per solution
+  unsigned long long* key;
+  double* bary;  // 2k per solution
   double* contrib;
   float* resid;
-  uint32_t* flags;
-  // flagged tuples
-  unsigned long long* fcount;
   uint64_t fcapacity;
-  unsigned long long* fkey;
-  uint32_t* fquery;
-  uint32_t* ftuple;
+  unsigned long long* fkey;  // pair index (a pair may emit several flag records; OR-reduced later)
   uint32_t* fflags;
   unsigned long long* counters;  // [C_NUM]
+};
+// dense job list between the two solve phases
+struct JobSink {
+  unsigned long long* count;
+  uint64_t capacity;
+  uint32_t* pair;
+  uint32_t* meta;  // kfree | deg << 8
+  double* r;       // 10 per job
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,

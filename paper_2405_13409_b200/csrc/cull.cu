@@ -1,159 +1,204 @@
 // Culling pre-pass (replaces the Wang20 pruning of PAPER.md:680).
 //
-// Predicate (sound): any admissible x_1 on T has a generalised half vector
-//   h = eta_prev w_prev + eta_next w_next  parallel to +-n(x_1)            (Eq. 3)
-// where w_prev / w_next are the unit directions from x_1 to x_0 / x_2.  Each direction set is bounded
-// by a cone (axis a, chord c = 2 sin(theta/2)); h then lies in the ball B(A, r), A = sum eta a,
-// r = sum eta c, i.e. in the cone (A^, asin(r/|A|)) when |A| > r.  The tuple is culled when that cone
-// misses both the normal cone and its negation by more than `margin`.  Cluster level: bounding
-// sphere + cluster normal cone; triangle level: exact vertex-direction cones + the triangle's normal
-// cone.  FP32 with a margin: at most more permissive than the FP64 oracle predicate.
+// Predicate (sound): any admissible x_1 on a node (triangle, or cluster of triangles) has a generalised
+// half vector h = eta_prev w_prev + eta_next w_next parallel to +-n(x_1)  (Eq. 3), with w_prev / w_next
+// the unit directions from x_1 to x_0 / x_2.  Each direction set is bounded through the node's bounding
+// sphere (c, rho): axis (x - c)^, chord <= s (1 + s^2), s = rho / |x - c|.  Then h lies in the ball
+// B(A, r), A = sum eta axis, r = sum eta chord, i.e. in the cone (A^, alpha), sin alpha = r/|A|.  The node
+// is culled when |A x N| > |A| sin(alpha + beta) with beta the node's normal-cone half angle plus the
+// FP32 margin (folded in at upload), i.e. when the h-cone misses both +N and -N cones.  FP32 with a
+// margin: at most more permissive than the FP64 oracle predicate.
 //
-// One warp per query (grid-stride).  pass 0 counts survivors per query; pass 1 rewrites the same
-// decisions into the query-major work list at the scanned offsets (deterministic order: Morton
-// position ascending).
+// Hierarchy: 64-triangle clusters -> 8-triangle sub-clusters -> triangles (all in Morton order).  One
+// warp per query; survivors are OR-ed into a per-query bitmask row (one bit per Morton position), so
+// the work list that `k_expand_bits` emits is query-major and Morton-ordered (deterministic) whatever
+// order the tests ran in.
 #include "kernels.cuh"
 
 namespace spoly {
 
-struct DirCone {
-  f3 a;
-  float chord;
-  bool ok;
-};
-
-__device__ __forceinline__ f3 nrmz(f3 v) {
-  float l = rsqrtf(dotf(v, v));
-  return l * v;
-}
-
-// cone of the directions from the three vertices to x
-__device__ __forceinline__ DirCone tri_dir_cone(f3 x, f3 p0, f3 p1, f3 p2) {
-  f3 w0 = nrmz(x - p0), w1 = nrmz(x - p1), w2 = nrmz(x - p2);
-  f3 s = w0 + w1 + w2;
-  f3 a = nrmz(s);
-  DirCone c;
-  c.a = a;
-  f3 d0 = w0 - a, d1 = w1 - a, d2 = w2 - a;
-  c.chord = sqrtf(fmaxf(dotf(d0, d0), fmaxf(dotf(d1, d1), dotf(d2, d2))));
-  // all directions within 90 deg of the axis (chord < sqrt 2) -> the cone bounds their spherical hull
-  c.ok = dotf(w0, a) > 1e-3f && dotf(w1, a) > 1e-3f && dotf(w2, a) > 1e-3f;
-  return c;
-}
-
-// cone of the directions from a sphere (c, rho) to x
-__device__ __forceinline__ DirCone sphere_dir_cone(f3 x, f3 c, float rho) {
-  f3 d = x - c;
-  float l2 = dotf(d, d);
-  DirCone r;
-  r.a = rsqrtf(l2) * d;
-  float s2 = rho * rho / l2;  // sin^2 theta
-  r.ok = s2 < 0.98f;
-  float ct = sqrtf(fmaxf(1.f - s2, 0.f));
-  r.chord = sqrtf(2.f * s2 / (1.f + ct));  // 2 sin(theta/2)
-  return r;
-}
-
-// keep test against the normal cone (axis nax, half angle nth), both orientations
-__device__ __forceinline__ bool cone_keep(const DirCone& p, const DirCone& q, float ep, float en, f3 nax, float nth,
-                                          float margin) {
-  if (!p.ok || !q.ok || nth >= 1.5707f) return true;
-  f3 A = ep * p.a + en * q.a;
-  float r = ep * p.chord + en * q.chord;
-  float An = sqrtf(dotf(A, A));
-  if (!(An > r * 1.0001f + 1e-6f)) return true;
-  float alpha = asinf(fminf(r / An, 1.f));
-  float beta = alpha + nth + margin;
-  if (beta >= 1.5707f) return true;
-  f3 cr = crossf(A, nax);
-  float phi = atan2f(sqrtf(dotf(cr, cr)), dotf(A, nax));
-  return phi <= beta || (3.14159265f - phi) <= beta;
-}
-
 __device__ __forceinline__ f3 ld3(float4 a) { return {a.x, a.y, a.z}; }
 
-__global__ void __launch_bounds__(256) k_cull_k1(int pass, const double* __restrict__ ep, uint32_t nq,
-                                                 const TriRec* __restrict__ tris, const float4* __restrict__ tricone,
-                                                 const ClusterRec* __restrict__ cl, uint32_t ntris, uint32_t ncl,
-                                                 CullParams cp, uint32_t* counts,
-                                                 const unsigned long long* __restrict__ offsets,
-                                                 uint32_t* pair_query, uint32_t* pair_tpos) {
+// direction bound from a sphere to x: writes axis and chord, returns false when no bound (s^2 > 1/4)
+__device__ __forceinline__ bool sphere_dir(f3 x, float4 s, f3& a, float& chord) {
+  f3 d = {x.x - s.x, x.y - s.y, x.z - s.z};
+  const float l2 = dotf(d, d);
+  const float inv = rsqrtf(l2);
+  const float sn = s.w * inv;
+  const float s2 = sn * sn;
+  a = inv * d;
+  chord = sn * (1.f + s2);  // >= 2 sin(asin(sn)/2) for s2 <= 1/4
+  return s2 <= 0.25f;
+}
+
+// keep test of one node given the two direction bounds and the IOR pair
+__device__ __forceinline__ bool node_keep(f3 ap, float cp, f3 an, float cn, float ep, float en, float4 nc) {
+  const f3 A = ep * ap + en * an;
+  const float r = ep * cp + en * cn;
+  const float A2 = dotf(A, A);
+  if (!(A2 > r * r * 1.0001f + 1e-12f)) return true;
+  const float sb = nc.w, cb = sqrtf(fmaxf(1.f - sb * sb, 0.f));
+  const float q = sqrtf(A2 - r * r);             // |A| cos(alpha)
+  if (!(q * cb - r * sb > 0.f)) return true;      // alpha + beta >= 90 deg: no bound
+  const f3 X = crossf(A, ld3(nc));
+  const float rhs = r * cb + q * sb;              // |A| sin(alpha + beta)
+  return !(dotf(X, X) > rhs * rhs);
+}
+
+template <bool REFRACT>
+__device__ __forceinline__ bool test_cluster(f3 x0, f3 x2, const ClusterRec& C, float ef, float eb) {
+  f3 ap, an;
+  float cp, cn;
+  if (!sphere_dir(x0, C.sphere, ap, cp) || !sphere_dir(x2, C.sphere, an, cn)) return true;
+  if (!REFRACT) return node_keep(ap, cp, an, cn, 1.f, 1.f, C.cone);
+  return node_keep(ap, cp, an, cn, ef, eb, C.cone) || node_keep(ap, cp, an, cn, eb, ef, C.cone);
+}
+
+template <bool REFRACT>
+__device__ __forceinline__ bool test_tri(f3 x0, f3 x2, const TriCull& T, float ef, float eb) {
+  f3 ap, an;
+  float cp, cn;
+  if (!sphere_dir(x0, T.sphere, ap, cp) || !sphere_dir(x2, T.sphere, an, cn)) return true;
+  if (!REFRACT) return node_keep(ap, cp, an, cn, 1.f, 1.f, T.cone);
+  // eta_0 from the side of x_0 w.r.t. the triangle plane (c7); within float noise of the plane: both
+  const float sd = dotf(ld3(T.plane), x0) - T.plane.w;
+  const float gl = sqrtf(dotf(ld3(T.plane), ld3(T.plane)));
+  const bool front = sd > 0.f;
+  bool k = front ? node_keep(ap, cp, an, cn, ef, eb, T.cone) : node_keep(ap, cp, an, cn, eb, ef, T.cone);
+  if (!k && fabsf(sd) <= 1e-4f * gl * (fabsf(x0.x) + fabsf(x0.y) + fabsf(x0.z) + 1.f))
+    k = front ? node_keep(ap, cp, an, cn, eb, ef, T.cone) : node_keep(ap, cp, an, cn, ef, eb, T.cone);
+  return k;
+}
+
+template <bool REFRACT>
+__global__ void __launch_bounds__(256) k_cull_bits(const double* __restrict__ ep, uint32_t nq,
+                                                   const ClusterRec* __restrict__ l1, const ClusterRec* __restrict__ l2,
+                                                   const TriCull* __restrict__ tc, uint32_t ntris, uint32_t nl1,
+                                                   float ef, float eb, uint32_t* __restrict__ bits, uint32_t words,
+                                                   uint32_t* __restrict__ counts) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nl2 = (ntris + 7) >> 3;
   for (uint32_t q = gw; q < nq; q += nw) {
     const double* e = ep + 6ull * q;
     const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
     const f3 x2 = {(float)e[3], (float)e[4], (float)e[5]};
+    uint32_t* row = bits + (uint64_t)q * words;
     uint32_t count = 0;
-    unsigned long long wpos = pass ? offsets[q] : 0ull;
-    for (uint32_t cb = 0; cb < ncl; cb += 32) {
-      const uint32_t c = cb + lane;
-      bool keep = false;
-      if (c < ncl) {
-        const ClusterRec R = cl[c];
-        const f3 cc = ld3(R.sphere);
-        DirCone dp = sphere_dir_cone(x0, cc, R.sphere.w), dn = sphere_dir_cone(x2, cc, R.sphere.w);
-        const f3 nax = ld3(R.cone);
-        if (cp.refract)
-          keep = cone_keep(dp, dn, cp.eta_front, cp.eta_back, nax, R.cone.w, cp.margin) ||
-                 cone_keep(dp, dn, cp.eta_back, cp.eta_front, nax, R.cone.w, cp.margin);
-        else
-          keep = cone_keep(dp, dn, 1.f, 1.f, nax, R.cone.w, cp.margin);
-      }
-      unsigned cmask = __ballot_sync(0xffffffffu, keep);
-      while (cmask) {
-        const int b = __ffs(cmask) - 1;
-        cmask &= cmask - 1;
-        const uint32_t cid = cb + b;
+    for (uint32_t base = 0; base < nl1; base += 32) {
+      const uint32_t c = base + lane;
+      const bool k1 = c < nl1 && test_cluster<REFRACT>(x0, x2, l1[c], ef, eb);
+      uint32_t m1 = __ballot_sync(0xffffffffu, k1);
+      while (m1) {
+        // up to 4 surviving 64-clusters per round: 32 lanes test their 8 sub-clusters each
+        uint32_t sel[4];
+        int nsel = 0;
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {
-          const uint32_t t = cid * kClusterSize + half * 32 + lane;
-          bool k = false;
-          if (t < ntris) {
-            const float4* r = tris[t].r;
-            float4 a = __ldg(r), bb = __ldg(r + 1), c2 = __ldg(r + 2);
-            f3 p0 = {a.x, a.y, a.z}, p1 = {a.w, bb.x, bb.y}, p2 = {bb.z, bb.w, c2.x};
-            float4 nc = __ldg(tricone + t);
-            DirCone dp = tri_dir_cone(x0, p0, p1, p2), dn = tri_dir_cone(x2, p0, p1, p2);
-            float e0 = 1.f, e1 = 1.f;
-            if (cp.refract) {
-              f3 g = crossf(p1 - p0, p2 - p0);
-              bool front = dotf(x0 - p0, g) > 0.f;
-              e0 = front ? cp.eta_front : cp.eta_back;
-              e1 = front ? cp.eta_back : cp.eta_front;
-              // a side decision within float noise of the plane: test both media
-              float dd = dotf(x0 - p0, g), gl = sqrtf(dotf(g, g)), xl = sqrtf(dotf(x0 - p0, x0 - p0));
-              if (fabsf(dd) <= 1e-4f * gl * xl)
-                k = cone_keep(dp, dn, e1, e0, ld3(nc), nc.w, cp.margin);
+        for (int i = 0; i < 4; ++i) {
+          if (m1) {
+            sel[i] = base + __ffs(m1) - 1;
+            m1 &= m1 - 1;
+            nsel = i + 1;
+          } else {
+            sel[i] = 0;
+          }
+        }
+        const int which = lane >> 3, sub = lane & 7;
+        const uint32_t sc = sel[which] * 8 + sub;
+        const bool k2 = which < nsel && sc < nl2 && test_cluster<REFRACT>(x0, x2, l2[sc], ef, eb);
+        uint32_t m2 = __ballot_sync(0xffffffffu, k2);
+        uint32_t word = 0;  // lane i < 2*nsel owns bits [32*(i&1), 32*(i&1)+32) of cluster sel[i>>1]
+        while (m2) {
+          int pick[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (m2) {
+              pick[i] = __ffs(m2) - 1;
+              m2 &= m2 - 1;
+            } else {
+              pick[i] = -1;
             }
-            k = k || cone_keep(dp, dn, e0, e1, ld3(nc), nc.w, cp.margin);
           }
-          const unsigned m = __ballot_sync(0xffffffffu, k);
-          if (pass && k) {
-            const unsigned long long pos = wpos + __popc(m & ((1u << lane) - 1u));
-            pair_query[pos] = q;
-            pair_tpos[pos] = t;
+          const int j = lane >> 3, t = lane & 7;
+          bool k3 = false;
+          if (pick[j] >= 0) {
+            const uint32_t tri = sel[pick[j] >> 3] * 64 + (pick[j] & 7) * 8 + t;
+            if (tri < ntris) k3 = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb);
           }
-          wpos += __popc(m);
-          count += __popc(m);
+          const uint32_t m3 = __ballot_sync(0xffffffffu, k3);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            if (pick[i] >= 0) {
+              const int cl = pick[i] >> 3, sb = pick[i] & 7;
+              const uint32_t b8 = (m3 >> (8 * i)) & 0xFFu;
+              if (lane == 2 * cl + (sb >> 2)) word |= b8 << (8 * (sb & 3));
+            }
+          }
+        }
+        if (lane < 2 * nsel && word) {
+          row[sel[lane >> 1] * 2 + (lane & 1)] = word;
+          count += __popc(word);
         }
       }
     }
-    if (!pass && lane == 0) counts[q] = count;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) count += __shfl_xor_sync(0xffffffffu, count, off);
+    if (lane == 0) counts[q] = count;
   }
 }
 
-void launch_cull_k1(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, const CullParams& cp,
-                    uint32_t* counts, const unsigned long long* offsets, uint32_t* pair_query, uint32_t* pair_tpos,
-                    int nsm, cudaStream_t st) {
+void launch_cull_bits(const double* ep, uint32_t nq, const DeviceMesh& M, int refract, uint32_t* bits, uint32_t words,
+                      uint32_t* counts, int nsm, cudaStream_t st) {
   if (!nq) return;
   const int threads = 256;
   uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
   uint64_t cap = (uint64_t)nsm * 8;
   int blocks = (int)(want < cap ? want : cap);
-  k_cull_k1<<<blocks, threads, 0, st>>>(pass, ep, nq, M.tris, M.tricone, M.clusters, M.ntris, M.nclusters, cp, counts,
-                                        offsets, pair_query, pair_tpos);
+  if (refract)
+    k_cull_bits<true><<<blocks, threads, 0, st>>>(ep, nq, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
+                                                   M.eta_front, M.eta_back, bits, words, counts);
+  else
+    k_cull_bits<false><<<blocks, threads, 0, st>>>(ep, nq, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
+                                                    M.eta_front, M.eta_back, bits, words, counts);
+}
+
+// bitmask rows -> query-major work list at the scanned offsets; one warp per query
+__global__ void k_expand_bits(const uint32_t* __restrict__ bits, uint32_t words, uint32_t nq,
+                              const unsigned long long* __restrict__ offsets, uint32_t* pq, uint32_t* pt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t q = gw; q < nq; q += nw) {
+    const uint32_t* row = bits + (uint64_t)q * words;
+    unsigned long long pos = offsets[q];
+    for (uint32_t w0 = 0; w0 < words; w0 += 32) {
+      const uint32_t wi = w0 + lane;
+      uint32_t word = wi < words ? row[wi] : 0u;
+      const uint32_t c = __popc(word);
+      uint32_t incl = c;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+        if (lane >= off) incl += t;
+      }
+      unsigned long long p = pos + incl - c;
+      while (word) {
+        const int b = __ffs(word) - 1;
+        word &= word - 1;
+        pq[p] = q;
+        pt[p] = wi * 32 + b;
+        ++p;
+      }
+      pos += __shfl_sync(0xffffffffu, incl, 31);
+    }
+  }
+}
+
+void launch_expand_bits(const uint32_t* bits, uint32_t words, uint32_t nq, const unsigned long long* offsets,
+                        uint32_t* pq, uint32_t* pt, int nsm, cudaStream_t st) {
+  if (!nq) return;
+  k_expand_bits<<<nsm * 16, 256, 0, st>>>(bits, words, nq, offsets, pq, pt);
 }
 
 // no cull: every (query, triangle) pair, query-major, Morton order

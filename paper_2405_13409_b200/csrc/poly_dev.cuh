@@ -164,6 +164,16 @@ static __constant__ double c_falling[16][16] = {
     {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 87178291200.0, 1307674368000.0},
     {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1307674368000.0}};
 
+// reciprocal good to ~1e-14 relative: FP32 MUFU seed + two FP64 Newton refinements (the Newton step
+// of the root solver only needs an accurate-enough quotient; the bracket guarantees convergence)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r = (double)__frcp_rn((float)x);
+  if (!(fabs(r) < 1e300) || r == 0.0) return 1.0 / x;  // float over/underflow: exact path
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
+  return r;
+}
+
 // p^(k)(x) and p^(k+1)(x) from the per-level coefficient registers g (p^(k) basis) and h (p^(k+1))
 template <int N>
 __device__ __forceinline__ double level_eval(const double* g, const double* h, int k, int deg, double x, double* dval) {
@@ -192,7 +202,7 @@ __device__ __forceinline__ double solve_piece(const double* g, const double* h, 
       lo = x;
     else
       hi = x;
-    double xn = x - f / fp;
+    double xn = x - f * fast_rcp(fp);
     if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
     if (fabs(xn - x) <= 1e-15 || hi - lo <= 1e-15) {
       *its = it + 1;
@@ -204,8 +214,12 @@ __device__ __forceinline__ double solve_piece(const double* g, const double* h, 
   return x;
 }
 
+// kstart: a derivative level known to have no root in (lo, hi) (so p^(kstart-1) is monotone there and
+// the recursion starts at level kstart-1 with no critical points); kstart < 0 or >= deg-1 runs the plain
+// recursion from the linear level deg-1.
 template <int N>
-__device__ void isolate_roots(const double* c, int deg, double lo, double hi, double eps_close, RootSet<N>& R) {
+__device__ void isolate_roots(const double* c, int deg, double lo, double hi, double eps_close, RootSet<N>& R,
+                              int kstart = -1) {
   R.terms = 0;
   R.n = 0;
   R.min_crit_ratio = 1.0;
@@ -213,7 +227,7 @@ __device__ void isolate_roots(const double* c, int deg, double lo, double hi, do
   if (deg <= 0) return;
   double prev[N];
   int nprev = 0;
-  {
+  if (kstart < 0 || kstart >= deg - 1) {
     // level deg-1: p^(deg-1)(x) = c_{deg-1} (deg-1)! + c_deg deg! x   (linear: closed form)
     double a0 = 0.0, a1 = 0.0;
 #pragma unroll
@@ -227,8 +241,9 @@ __device__ void isolate_roots(const double* c, int deg, double lo, double hi, do
       return;
     }
     if (x > lo && x < hi) prev[nprev++] = x;
+    kstart = deg - 1;
   }
-  for (int k = deg - 2; k >= 0; --k) {
+  for (int k = kstart - 1; k >= 0; --k) {
     double g[N], h[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {

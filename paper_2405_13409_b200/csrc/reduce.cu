@@ -1,8 +1,7 @@
 // Deterministic compaction: sort the appended solutions by their key
-// (pair index << 6 | root slot), gather the records into that order, then sum the contributions
-// per query in a fixed order ("we sum the contributions from all of them").
-#include <cub/cub.cuh>
-
+// (pair index << 6 | root slot), gather the records into that order (query / triangle ids from the work
+// list), OR-reduce the per-pair flag records, then sum the contributions per query in a fixed order
+// ("we sum the contributions from all of them").
 #include "kernels.cuh"
 
 namespace spoly {
@@ -24,33 +23,58 @@ void launch_map_ids(const uint32_t* tpos, uint64_t n, const uint32_t* orig_id, u
   if (n) k_map_ids<<<1024, 256, 0, st>>>(tpos, n, orig_id, out);
 }
 
-__global__ void k_gather_solutions(const uint32_t* __restrict__ perm, uint64_t n, int k, SolSink in, SolSink out) {
+__global__ void k_gather_solutions(const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ skey,
+                                   uint64_t n, int k, SolSink in, const uint32_t* __restrict__ pq,
+                                   const uint32_t* __restrict__ pt, const uint32_t* __restrict__ orig, OutArrays out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = perm[i];
-    out.query[i] = in.query[s];
-    for (int j = 0; j < k; ++j) out.tuple[(uint64_t)k * i + j] = in.tuple[(uint64_t)k * s + j];
+    const uint64_t pair = skey[i] >> 6;
+    out.query[i] = pq[pair];
+    for (int j = 0; j < k; ++j) out.tuple[(uint64_t)k * i + j] = orig[pt[(uint64_t)k * pair + j]];
     for (int j = 0; j < 2 * k; ++j) out.bary[(uint64_t)2 * k * i + j] = in.bary[(uint64_t)2 * k * s + j];
     out.contrib[i] = in.contrib[s];
     out.resid[i] = in.resid[s];
-    out.flags[i] = in.flags[s];
   }
 }
-void launch_gather_solutions(const uint32_t* perm, uint64_t n, int k, const SolSink& in, const SolSink& out,
-                             cudaStream_t st) {
-  if (n) k_gather_solutions<<<2048, 256, 0, st>>>(perm, n, k, in, out);
+void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, uint64_t n, int k,
+                             const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
+                             const OutArrays& out, cudaStream_t st) {
+  if (n) k_gather_solutions<<<2048, 256, 0, st>>>(perm, skey, n, k, in, pq, pt, orig_id, out);
 }
 
-__global__ void k_gather_flagged(const uint32_t* __restrict__ perm, uint64_t n, int k, SolSink in, SolSink out) {
+__global__ void k_gather_flagged(const unsigned long long* __restrict__ upair, const uint32_t* __restrict__ uflags,
+                                 uint64_t n, int k, const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                 const uint32_t* __restrict__ orig, OutArrays out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t s = perm[i];
-    out.fquery[i] = in.fquery[s];
-    for (int j = 0; j < k; ++j) out.ftuple[(uint64_t)k * i + j] = in.ftuple[(uint64_t)k * s + j];
-    out.fflags[i] = in.fflags[s];
+    const uint64_t pair = upair[i];
+    out.fquery[i] = pq[pair];
+    for (int j = 0; j < k; ++j) out.ftuple[(uint64_t)k * i + j] = orig[pt[(uint64_t)k * pair + j]];
+    out.fflags[i] = uflags[i];
   }
 }
-void launch_gather_flagged(const uint32_t* perm, uint64_t n, int k, const SolSink& in, const SolSink& out,
+void launch_gather_flagged(const unsigned long long* upair, const uint32_t* uflags, uint64_t n, int k,
+                           const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id, const OutArrays& out,
                            cudaStream_t st) {
-  if (n) k_gather_flagged<<<256, 256, 0, st>>>(perm, n, k, in, out);
+  if (n) k_gather_flagged<<<256, 256, 0, st>>>(upair, uflags, n, k, pq, pt, orig_id, out);
+}
+
+// every solution carries its tuple's (OR-reduced) flags: binary search of its pair in the sorted list
+__global__ void k_solution_flags(const unsigned long long* __restrict__ skey, uint64_t n,
+                                 const unsigned long long* __restrict__ upair, const uint32_t* __restrict__ uflags,
+                                 uint64_t nf, uint32_t* flags) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long pair = skey[i] >> 6;
+    uint64_t lo = 0, hi = nf;
+    while (lo < hi) {
+      const uint64_t m = (lo + hi) >> 1;
+      if (upair[m] < pair) lo = m + 1; else hi = m;
+    }
+    flags[i] = (lo < nf && upair[lo] == pair) ? uflags[lo] : 0u;
+  }
+}
+void launch_solution_flags(const unsigned long long* skey, uint64_t n, const unsigned long long* upair,
+                           const uint32_t* uflags, uint64_t nf, uint32_t* flags, cudaStream_t st) {
+  if (n) k_solution_flags<<<2048, 256, 0, st>>>(skey, n, upair, uflags, nf, flags);
 }
 
 // one warp per query: binary-search its range in the query-sorted solution list, then a fixed-order
@@ -66,7 +90,7 @@ __global__ void k_per_query_sorted(const uint32_t* __restrict__ query, const dou
       uint64_t m = (lo + hi) >> 1;
       if (query[m] < q) lo = m + 1; else hi = m;
     }
-    uint64_t b = lo;
+    const uint64_t b = lo;
     hi = n;
     while (lo < hi) {
       uint64_t m = (lo + hi) >> 1;

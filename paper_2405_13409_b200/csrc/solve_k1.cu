@@ -1,112 +1,212 @@
-// One-bounce fused solve kernels (chain "R" now; "T" shares the path phase).
+// One-bounce reflection solve ("R", Eq. 21), split into two kernels so that every lane has work:
+//
+//   k_r_phase1 (one thread per (query, triangle) pair, uniform control flow):
+//       decision (reading R1) -> coefficient phase (Eq. 6 a, Eq. 12 b) -> normalise + truncate (c5)
+//       -> elimination phase (Eq. 24 Bezout, Laplace expansion) -> r(v) normalised
+//       -> Bernstein root-exclusion level; pairs whose r may have a root in [0,1] are appended to a
+//       dense job list (warp-aggregated).
+//   k_r_phase2 (one thread per job):
+//       univariate roots (derivative recursion) -> back-substitution
+//       -> (a,b) refinement (reading R2) -> Eq. 3 validation, sides, flags -> contribution (c15)
+//       -> warp-aggregated emission.  The coefficient phase is recomputed from the geometry (same code,
+//       bit-identical) instead of being stored.
 #include "kernels.cuh"
 #include "solve_k1.cuh"
 
 namespace spoly {
 
-// ---------------------------------------------------------------------------------------------
-// Solve one (query, triangle) pair of a one-bounce reflection chain (Eq. 21).  All decisions follow
-// the readings in DESIGN.md §3 (t choice, truncation, flags) so that the oracle takes the same ones.
-__device__ void solve_pair_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
-                             const SolveParams& prm, PairOut& out, uint32_t* cnt) {
-  out.nsol = 0;
-  out.flags = 0;
-  cnt[C_PAIRS]++;
-  // ---- decision (reading R1): incidence-plane normal l_c = (x2 - x0) x n(centroid)
-  d3 nc = (1.0 / 3.0) * (N_in[0] + N_in[1] + N_in[2]);
-  d3 lc = cross(x2 - x0, nc);
+struct SystemR {
+  double A[9], B[25];
+  bool relabel;
+  uint32_t flags;
+  int n;
+};
+
+// decision + coefficient phase + normalisation/truncation; false when the system is degenerate
+__device__ __forceinline__ bool build_system_R(d3 x0, d3 x2, const d3 P_in[3], const d3 N_in[3],
+                                               const SolveParams& prm, SystemR& S) {
+  S.flags = 0;
+  // reading R1: incidence-plane normal l_c = (x2 - x0) x n(centroid); t = n x e1 unless e2 is further
+  // out of the incidence plane (then the relabeling p1 <-> p2)
+  const d3 nc = (1.0 / 3.0) * (N_in[0] + N_in[1] + N_in[2]);
+  const d3 lc = cross(x2 - x0, nc);
   const double ln = norm(lc);
-  if (!(ln > 1e-12 * norm(x2 - x0) * norm(nc))) out.flags |= SPOLY_FLAG_DEGENERATE;
-  d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
-  bool relabel = false;
+  if (!(ln > 1e-12 * norm(x2 - x0) * norm(nc))) S.flags |= SPOLY_FLAG_DEGENERATE;
+  const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
+  S.relabel = false;
   if (ln > 0) {
-    double s1 = fabs(dot(e1o, lc)) / (norm(e1o) * ln), s2 = fabs(dot(e2o, lc)) / (norm(e2o) * ln);
-    relabel = s1 < s2;
+    const double s1 = fabs(dot(e1o, lc)) / (norm(e1o) * ln), s2 = fabs(dot(e2o, lc)) / (norm(e2o) * ln);
+    S.relabel = s1 < s2;
   }
-  const d3 p0 = P_in[0], p1 = relabel ? P_in[2] : P_in[1], p2 = relabel ? P_in[1] : P_in[2];
-  const d3 n0 = N_in[0], n1 = relabel ? N_in[2] : N_in[1], n2 = relabel ? N_in[1] : N_in[2];
+  const d3 p0 = P_in[0], p1 = S.relabel ? P_in[2] : P_in[1], p2 = S.relabel ? P_in[1] : P_in[2];
+  const d3 n0 = N_in[0], n1 = S.relabel ? N_in[2] : N_in[1], n2 = S.relabel ? N_in[1] : N_in[2];
   const d3 e1 = p1 - p0, e2 = p2 - p0, m1 = n1 - n0, m2 = n2 - n0;
   const d3 q = p0 - x0, w = x2 - x0;
-
-  // ---- coefficient phase
-  double A[9], B[25];
-  build_a(q, w, e1, e2, n0, m1, m2, A);
-  build_b_R(q, w, e1, e2, n0, m1, m2, B);
-  const double ma = bmaxabs<2, 3>(A), mb = bmaxabs<4, 5>(B);
+  build_a(q, w, e1, e2, n0, m1, m2, S.A);
+  build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
+  const double ma = bmaxabs<2, 3>(S.A), mb = bmaxabs<4, 5>(S.B);
   if (!(ma > 0) || !(mb > 0)) {
-    out.flags |= SPOLY_FLAG_DEGENERATE;
-    cnt[C_FLAGGED]++;
-    return;
+    S.flags |= SPOLY_FLAG_DEGENERATE;
+    return false;
   }
-  bscale<2, 3>(A, 1.0 / ma);
-  bscale<4, 5>(B, 1.0 / mb);
-  const int da = bnum_udeg<2, 3>(A, prm.tau_trunc), db = bnum_udeg<4, 5>(B, prm.tau_trunc);
-  btrunc_u<2, 3>(A, da);
-  btrunc_u<4, 5>(B, db);
-  const int n = max(da, db);
-  if (n == 0) {
-    out.flags |= SPOLY_FLAG_DEGENERATE;
-    cnt[C_FLAGGED]++;
-    return;
+  bscale<2, 3>(S.A, 1.0 / ma);
+  bscale<4, 5>(S.B, 1.0 / mb);
+  const int da = bnum_udeg<2, 3>(S.A, prm.tau_trunc), db = bnum_udeg<4, 5>(S.B, prm.tau_trunc);
+  btrunc_u<2, 3>(S.A, da);
+  btrunc_u<4, 5>(S.B, db);
+  S.n = max(da, db);
+  if (S.n == 0) {
+    S.flags |= SPOLY_FLAG_DEGENERATE;
+    return false;
   }
-  cnt[C_SYSTEMS]++;
+  return true;
+}
 
-  // ---- elimination phase: r(v) = det R(v), Laplace expansion (deg <= 9)
-  double r[10];
-  det_R(A, B, n, r);
-  double mr = 0.0;
+// ---------------------------------------------------------------------------------------------
+// warp-aggregated appends (all 32 lanes must call)
+__device__ __forceinline__ unsigned long long warp_alloc(unsigned long long* counter, uint32_t n, uint32_t* excl) {
+  const int lane = threadIdx.x & 31;
+  uint32_t incl = n;
 #pragma unroll
-  for (int i = 0; i < 10; ++i) mr = fmax(mr, fabs(r[i]));
-  if (!(mr > 0)) {
-    out.flags |= SPOLY_FLAG_DEGENERATE;
-    cnt[C_FLAGGED]++;
-    return;
+  for (int off = 1; off < 32; off <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
+    if (lane >= off) incl += t;
   }
-  int deg = 0;
-  const double inv = 1.0 / mr;
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  unsigned long long base = 0;
+  if (total) {
+    if (lane == 31) base = atomicAdd(counter, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+  }
+  *excl = incl - n;
+  return base;
+}
+
+__device__ __forceinline__ void emit_flag(bool has, uint32_t flags, uint64_t pair, const SolSink& S) {
+  uint32_t ex;
+  const unsigned long long base = warp_alloc(S.count + 1, has ? 1u : 0u, &ex);
+  if (has && base + ex < S.fcapacity) {
+    S.fkey[base + ex] = pair;
+    S.fflags[base + ex] = flags;
+  }
+}
+
+__device__ __forceinline__ void flush_counters(const SolSink& S, const uint32_t* cnt) {
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int i = 0; i < 10; ++i) {
-    r[i] *= inv;
-    if (r[i] != 0.0) deg = i;
+  for (int i = 0; i < C_NUM; ++i) {
+    uint32_t v = cnt[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if (lane == 0 && v) atomicAdd(S.counters + i, (unsigned long long)v);
   }
+}
 
-  // ---- univariate roots on [0,1]
-  RootSet<10> R;
-  isolate_roots<10>(r, deg, 0.0, 1.0, prm.eps_flag, R);
-  cnt[C_EVAL_TERMS] += R.terms;
-  if (R.flags & 1) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
-  if (R.min_crit_ratio <= 1e-10) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
-  // dedup (1e-7) as the oracle
-  double vr[10];
-  int nv = 0;
-  for (int i = 0; i < R.n; ++i)
-    if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
-  cnt[C_VROOTS] += nv;
+__device__ __forceinline__ void load_pair(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                          const TriRec* __restrict__ tris, const double* __restrict__ ep, uint64_t i,
+                                          d3 P[3], d3 N[3], d3& x0, d3& x2, uint32_t& q) {
+  q = __ldg(pq + i);
+  load_tri(tris, __ldg(pt + i), P, N);
+  const double* e = ep + 6ull * q;
+  x0 = mk3(__ldg(e), __ldg(e + 1), __ldg(e + 2));
+  x2 = mk3(__ldg(e + 3), __ldg(e + 4), __ldg(e + 5));
+}
 
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_r_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                  uint64_t npairs, const TriRec* __restrict__ tris,
+                                                  const double* __restrict__ ep, SolveParams prm, SolSink S,
+                                                  JobSink J) {
+  uint32_t cnt[C_NUM];
+#pragma unroll
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = gw * 32; base < npairs; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const bool active = i < npairs;
+    bool job = false;
+    uint32_t flags = 0, meta = 0;
+    double r[10];
+    if (active) {
+      d3 P[3], N[3], x0, x2;
+      uint32_t q;
+      load_pair(pq, pt, tris, ep, i, P, N, x0, x2, q);
+      cnt[C_PAIRS]++;
+      SystemR Sys;
+      const bool ok = build_system_R(x0, x2, P, N, prm, Sys);
+      flags = Sys.flags;
+      if (ok) {
+        cnt[C_SYSTEMS]++;
+        det_R(Sys.A, Sys.B, Sys.n, r);
+        double mr = 0.0;
+#pragma unroll
+        for (int t = 0; t < 10; ++t) mr = fmax(mr, fabs(r[t]));
+        if (!(mr > 0)) {
+          flags |= SPOLY_FLAG_DEGENERATE;
+        } else {
+          int deg = 0;
+          const double inv = 1.0 / mr;
+#pragma unroll
+          for (int t = 0; t < 10; ++t) {
+            r[t] *= inv;
+            if (r[t] != 0.0) deg = t;
+          }
+          cnt[C_EVAL_TERMS] += 55 + 23;  // Bernstein transform + forward differences
+          const int kfree = bernstein_root_free_level(r);
+          if (kfree > 0 && deg > 0) {
+            job = true;
+            meta = (uint32_t)kfree | ((uint32_t)deg << 8);
+          }
+        }
+      }
+    }
+    emit_flag(active && flags != 0, flags, i, S);
+    uint32_t ex;
+    const unsigned long long jb = warp_alloc(J.count, job ? 1u : 0u, &ex);
+    if (job && jb + ex < J.capacity) {
+      const unsigned long long p = jb + ex;
+      J.pair[p] = (uint32_t)i;
+      J.meta[p] = meta;
+#pragma unroll
+      for (int t = 0; t < 10; ++t) J.r[p * 10 + t] = r[t];
+    }
+  }
+  flush_counters(S, cnt);
+}
+
+// ---------------------------------------------------------------------------------------------
+__device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
+                             const SolveParams& prm, const SystemR& Sys, const double* vr, int nv, PairOut& out,
+                             uint32_t* cnt) {
+  const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
   const d3 g_geo = cross(e1o, e2o);
-  // ---- path phase
+  const double* A = Sys.A;
+  const double* B = Sys.B;
   for (int iv = 0; iv < nv; ++iv) {
     const double vs = vr[iv];
     double al[3];
     bslices_at<2, 3>(A, vs, al);
     double ua[4];
     int nu = 0;
-    double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+    const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
     if (amax >= 1e-12) {
       // quadratic / linear in u (stable formula, disc clamp; reading R4)
       if (al[2] != 0.0) {
         const double a0 = al[0], a1 = al[1], a2 = al[2];
-        double disc = a1 * a1 - 4.0 * a2 * a0, sc = a1 * a1 + 4.0 * fabs(a2 * a0);
+        double disc = a1 * a1 - 4.0 * a2 * a0;
+        const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
         if (fabs(disc) <= 1e-8 * sc) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
         if (!(disc < -1e-12 * sc)) {
           if (disc < 0) disc = 0;
-          double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+          const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
           if (qq == 0.0) {
             ua[nu++] = 0.0;
           } else {
             double r1 = qq / a2, r2 = a0 / qq;
             if (r1 > r2) {
-              double t = r1;
+              const double t = r1;
               r1 = r2;
               r2 = t;
             }
@@ -132,11 +232,8 @@ __device__ void solve_pair_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
         out.flags |= SPOLY_FLAG_DEGENERATE;
         continue;
       }
-      double bc[5];
-#pragma unroll
-      for (int i = 0; i < 5; ++i) bc[i] = bl[i];
       RootSet<5> Rb;
-      isolate_roots<5>(bc, bd, -0.1, 1.1, 1e-7, Rb);
+      isolate_roots<5>(bl, bd, -0.1, 1.1, 1e-7, Rb);
       for (int i = 0; i < Rb.n && nu < 4; ++i)
         if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) ua[nu++] = Rb.x[i];
     }
@@ -149,20 +246,21 @@ __device__ void solve_pair_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       beval<2, 3>(A, us, vv, &fa, &fau, &fav);
       beval<4, 5>(B, us, vv, &fb, &fbu, &fbv);
       for (int it = 0; it < 3; ++it) {
-        double det = fau * fbv - fav * fbu;
+        const double det = fau * fbv - fav * fbu;
         if (det == 0.0) break;
-        double du = -(fbv * fa - fav * fb) / det, dv = -(-fbu * fa + fau * fb) / det;
+        const double idet = 1.0 / det;
+        const double du = -(fbv * fa - fav * fb) * idet, dv = -(-fbu * fa + fau * fb) * idet;
         if (!(fmax(fabs(us + du - ua[iu]), fabs(vv + dv - vs)) <= 1e-3)) break;
         double na, nau, nav, nb, nbu, nbv;
         beval<2, 3>(A, us + du, vv + dv, &na, &nau, &nav);
         beval<4, 5>(B, us + du, vv + dv, &nb, &nbu, &nbv);
-        if (!(hypot(na, nb) < hypot(fa, fb))) break;
+        if (!(na * na + nb * nb < fa * fa + fb * fb)) break;
         us += du;
         vv += dv;
         fa = na; fau = nau; fav = nav;
         fb = nb; fbu = nbu; fbv = nbv;
       }
-      const double ur = relabel ? vv : us, vr_ = relabel ? us : vv;  // original labeling
+      const double ur = Sys.relabel ? vv : us, vr_ = Sys.relabel ? us : vv;  // original labeling
       const d3 x1 = P_in[0] + ur * e1o + vr_ * e2o;
       const d3 nx = N_in[0] + ur * (N_in[1] - N_in[0]) + vr_ * (N_in[2] - N_in[0]);
       const double ed = fmin(fmin(ur, vr_), 1.0 - ur - vr_);
@@ -185,8 +283,7 @@ __device__ void solve_pair_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       if (rho >= 1e-7) out.flags |= SPOLY_FLAG_RESIDUAL;
       if (ed <= prm.eps_flag) out.flags |= SPOLY_FLAG_BOUNDARY;
       if (fabs(fau * fbv - fav * fbu) < 1e-6 * hypot(fau, fav) * hypot(fbu, fbv)) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
-      // dedup against accepted chains (1e-7)
-      bool dup = false;
+      bool dup = false;  // dedup against accepted chains (1e-7)
       for (int s = 0; s < out.nsol; ++s)
         if (fabs(out.u[s] - ur) < 1e-7 && fabs(out.v[s] - vr_) < 1e-7) dup = true;
       if (dup) {
@@ -205,116 +302,80 @@ __device__ void solve_pair_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       }
     }
   }
-  if (out.flags) cnt[C_FLAGGED]++;
 }
 
-// ---------------------------------------------------------------------------------------------
-// warp-aggregated emission of the pair results (all 32 lanes must call)
-__device__ __forceinline__ void emit_k1(const PairOut& o, bool active, uint32_t q, uint32_t orig, uint64_t pair_idx,
-                                        const SolSink& S) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t n = active ? (uint32_t)o.nsol : 0u;
-  uint32_t incl = n;
-#pragma unroll
-  for (int off = 1; off < 32; off <<= 1) {
-    uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
-    if (lane >= off) incl += t;
-  }
-  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-  if (total) {
-    unsigned long long base = 0;
-    if (lane == 31) base = atomicAdd(S.count, (unsigned long long)total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    unsigned long long pos = base + incl - n;
-    for (uint32_t s = 0; s < n; ++s, ++pos) {
-      if (pos < S.capacity) {
-        S.key[pos] = ((unsigned long long)pair_idx << 6) | o.slot[s];
-        S.query[pos] = q;
-        S.tuple[pos] = orig;
-        S.bary[2 * pos] = o.u[s];
-        S.bary[2 * pos + 1] = o.v[s];
-        S.contrib[pos] = o.contrib[s];
-        S.resid[pos] = o.resid[s];
-        S.flags[pos] = o.flags;
-      }
-    }
-  }
-  const bool fl = active && o.flags != 0;
-  const unsigned bal = __ballot_sync(0xffffffffu, fl);
-  if (bal) {
-    unsigned long long fbase = 0;
-    const int leader = __ffs(bal) - 1;
-    if (lane == leader) fbase = atomicAdd(S.fcount, (unsigned long long)__popc(bal));
-    fbase = __shfl_sync(0xffffffffu, fbase, leader);
-    if (fl) {
-      unsigned long long pos = fbase + __popc(bal & ((1u << lane) - 1u));
-      if (pos < S.fcapacity) {
-        S.fkey[pos] = pair_idx;
-        S.fquery[pos] = q;
-        S.ftuple[pos] = orig;
-        S.fflags[pos] = o.flags;
-      }
-    }
-  }
-}
-
-__device__ __forceinline__ void flush_counters(const SolSink& S, const uint32_t* cnt) {
-  const int lane = threadIdx.x & 31;
-#pragma unroll
-  for (int i = 0; i < C_NUM; ++i) {
-    uint32_t v = cnt[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0 && v) atomicAdd(S.counters + i, (unsigned long long)v);
-  }
-}
-
-// Flat work list: pair i = (pair_query[i], pair_tpos[i]) with tpos a Morton position; all lanes of a
-// warp iterate the same number of times so the emission stays warp-synchronous.
-__global__ void __launch_bounds__(128) k_solve_R_list(const uint32_t* __restrict__ pair_query,
-                                                      const uint32_t* __restrict__ pair_tpos, uint64_t npairs,
-                                                      uint64_t pair_base, const TriRec* __restrict__ tris,
-                                                      const uint32_t* __restrict__ orig_id,
-                                                      const double* __restrict__ ep, const double* __restrict__ inten,
-                                                      SolveParams prm, SolSink S) {
+__global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                  const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                                  const double* __restrict__ inten, SolveParams prm, SolSink S,
+                                                  const unsigned long long* __restrict__ njobs_p,
+                                                  const uint32_t* __restrict__ jpair, const uint32_t* __restrict__ jmeta,
+                                                  const double* __restrict__ jr) {
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t njobs = *njobs_p;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
-  for (uint64_t base = gw * 32; base < npairs; base += nw * 32) {
-    const uint64_t i = base + lane;
-    const bool active = i < npairs;
+  for (uint64_t base = gw * 32; base < njobs; base += nw * 32) {
+    const uint64_t j = base + lane;
+    const bool active = j < njobs;
     PairOut o;
     o.nsol = 0;
     o.flags = 0;
-    uint32_t q = 0, orig = 0;
+    uint32_t pair = 0;
     if (active) {
-      q = __ldg(pair_query + i);
-      const uint32_t tp = __ldg(pair_tpos + i);
-      orig = __ldg(orig_id + tp);
-      d3 P[3], N[3];
-      load_tri(tris, tp, P, N);
-      const double* e = ep + 6ull * q;
-      d3 x0 = mk3(__ldg(e), __ldg(e + 1), __ldg(e + 2)), x2 = mk3(__ldg(e + 3), __ldg(e + 4), __ldg(e + 5));
-      const double I = inten ? __ldg(inten + q) : 1.0;
-      solve_pair_R(x0, x2, I, P, N, prm, o, cnt);
+      pair = __ldg(jpair + j);
+      const uint32_t meta = __ldg(jmeta + j);
+      double r[10];
+#pragma unroll
+      for (int t = 0; t < 10; ++t) r[t] = __ldg(jr + j * 10 + t);
+      RootSet<10> R;
+      isolate_roots<10>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+      cnt[C_EVAL_TERMS] += R.terms;
+      if (R.flags & 1) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
+      if (R.min_crit_ratio <= 1e-10) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
+      double vr[10];
+      int nv = 0;
+      for (int i = 0; i < R.n; ++i)
+        if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
+      cnt[C_VROOTS] += nv;
+      if (nv > 0) {
+        d3 P[3], N[3], x0, x2;
+        uint32_t q;
+        load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
+        SystemR Sys;
+        build_system_R(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (already known non-degenerate)
+        const double I = inten ? __ldg(inten + q) : 1.0;
+        path_phase_R(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
+      }
     }
-    emit_k1(o, active, q, orig, pair_base + i, S);
+    emit_flag(active && o.flags != 0, o.flags, pair, S);
+    uint32_t ex;
+    const unsigned long long b = warp_alloc(S.count, active ? (uint32_t)o.nsol : 0u, &ex);
+    for (int s = 0; s < o.nsol; ++s) {
+      const unsigned long long p = b + ex + s;
+      if (p < S.capacity) {
+        S.key[p] = ((unsigned long long)pair << 6) | o.slot[s];
+        S.bary[2 * p] = o.u[s];
+        S.bary[2 * p + 1] = o.v[s];
+        S.contrib[p] = o.contrib[s];
+        S.resid[p] = o.resid[s];
+      }
+    }
   }
   flush_counters(S, cnt);
 }
 
-void launch_solve_R_list(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, uint64_t pair_base,
-                         const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
-                         const SolSink& S, int nsm, cudaStream_t st) {
+void launch_solve_R(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M, const double* ep,
+                    const double* inten, const SolveParams& prm, const SolSink& S, const JobSink& J, int nsm,
+                    cudaStream_t st) {
   if (npairs == 0) return;
   const int threads = 128;
-  uint64_t want = (npairs + threads - 1) / threads;
-  uint64_t cap = (uint64_t)nsm * 16;  // persistent-ish grid: 16 CTAs of 4 warps per SM
-  int blocks = (int)(want < cap ? want : cap);
-  k_solve_R_list<<<blocks, threads, 0, st>>>(pq, pt, npairs, pair_base, M.tris, M.orig_id, ep, inten, prm, S);
+  const uint64_t cap = (uint64_t)nsm * 16;
+  const uint64_t want1 = (npairs + threads - 1) / threads;
+  k_r_phase1<<<(int)(want1 < cap ? want1 : cap), threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
+  k_r_phase2<<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.pair, J.meta, J.r);
 }
 
 }  // namespace spoly

@@ -12,7 +12,52 @@
 
 namespace spoly {
 
+// monomial -> degree-9 Bernstein basis on [0,1]: b_k = sum_{i<=k} C(k,i)/C(9,i) c_i
+static __constant__ double c_bern9[10][10] = {
+    {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.1111111111111111, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.2222222222222222, 0.027777777777777776, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.3333333333333333, 0.08333333333333333, 0.011904761904761904, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.4444444444444444, 0.16666666666666666, 0.047619047619047616, 0.007936507936507936, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.5555555555555556, 0.2777777777777778, 0.11904761904761904, 0.03968253968253968, 0.007936507936507936, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.6666666666666666, 0.4166666666666667, 0.23809523809523808, 0.11904761904761904, 0.047619047619047616, 0.011904761904761904, 0.0, 0.0, 0.0},
+    {1.0, 0.7777777777777778, 0.5833333333333334, 0.4166666666666667, 0.2777777777777778, 0.16666666666666666, 0.08333333333333333, 0.027777777777777776, 0.0, 0.0},
+    {1.0, 0.8888888888888888, 0.7777777777777778, 0.6666666666666666, 0.5555555555555556, 0.4444444444444444, 0.3333333333333333, 0.2222222222222222, 0.1111111111111111, 0.0},
+    {1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0}};
+
 constexpr int kMaxSolPerPair = 8;
+
+// Bernstein exclusion (exact, no effect on the root set): the degree-9 Bernstein coefficients b of r on
+// [0,1] bound r there (convex hull property), and the k-th derivative of r has the Bernstein coefficients
+// 9!/(9-k)! * (k-th forward differences of b).  When the k-th differences all have one strict sign,
+// r^(k) has no root in [0,1]; the derivative recursion can then start at level k-1 with
+// no critical points, because every higher level only serves to locate the roots of r^(k).
+// Returns the smallest such k (0: r itself has no root in [0,1]; 10: none found).
+__device__ __forceinline__ int bernstein_root_free_level(const double* r) {
+  double b[10];
+#pragma unroll
+  for (int k = 0; k < 10; ++k) {
+    double acc = 0.0;
+#pragma unroll
+    for (int i = 0; i <= k; ++i) acc = fma(c_bern9[k][i], r[i], acc);
+    b[k] = acc;
+  }
+  int level = 10;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    bool pos = true, neg = true;
+#pragma unroll
+    for (int i = 0; i < 10 - k; ++i) {
+      pos = pos && (b[i] > 0.0);
+      neg = neg && (b[i] < 0.0);
+    }
+    if ((pos || neg) && level == 10) level = k;
+    // next differences
+#pragma unroll
+    for (int i = 0; i < 9 - k; ++i) b[i] = b[i + 1] - b[i];
+  }
+  return level;
+}
 
 struct PairOut {
   int nsol;
