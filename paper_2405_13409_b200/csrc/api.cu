@@ -368,13 +368,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   spoly_status s = ensure_sink(ctx, std::max<uint64_t>(ctx->d_key.cap, ctx->cfg.max_solutions),
                                std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
   if (s != SPOLY_OK) return s;
-  CK(ctx->d_count.ensure(3));
+  CK(ctx->d_count.ensure(4));
   CK(ctx->d_jpair.ensure(npairs));
   CK(ctx->d_jmeta.ensure(npairs));
   CK(ctx->d_jr.ensure(npairs * 10));
-  unsigned long long cnt[3] = {0, 0, 0};
+  unsigned long long cnt[4] = {0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
-    CK(cudaMemsetAsync(ctx->d_count.p, 0, 3 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_count.p, 0, 4 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(ctx->d_counters.p, 0, C_NUM * sizeof(unsigned long long), st));
     SolSink S = raw_sink(ctx);
     JobSink J;
@@ -388,6 +388,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+    if (cnt[2] + cnt[3] > J.capacity) return fail(ctx, SPOLY_ERR_CUDA, "job list overflow");
     if (cnt[0] <= S.capacity && cnt[1] <= S.fcapacity) break;
     if (attempt == 1) {
       out->report.required_solutions = cnt[0];

@@ -169,8 +169,7 @@ static __constant__ double c_falling[16][16] = {
 __device__ __forceinline__ double fast_rcp(double x) {
   double r = (double)__frcp_rn((float)x);
   if (!(fabs(r) < 1e300) || r == 0.0) return 1.0 / x;  // float over/underflow: exact path
-  r = r * fma(-x, r, 2.0);
-  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);  // one refinement: ~1e-14 relative, plenty for a Newton quotient
   return r;
 }
 
@@ -189,11 +188,14 @@ __device__ __forceinline__ double level_eval(const double* g, const double* h, i
 
 template <int N>
 __device__ __forceinline__ double solve_piece(const double* g, const double* h, int k, int deg, double lo, double hi,
-                                              double flo, int* its) {
-  double x = 0.5 * (lo + hi);
+                                              double flo, double fhi, int* its) {
+  // secant start inside the bracket, then Newton safeguarded by bisection; |step| <= 1e-12 stops
+  // (quadratic convergence: the error after such a step is far below 1e-15)
+  double x = lo - flo * (hi - lo) / (fhi - flo);
+  if (!(x > lo && x < hi)) x = 0.5 * (lo + hi);
   for (int it = 0; it < 100; ++it) {
     double fp;
-    double f = level_eval<N>(g, h, k, deg, x, &fp);
+    const double f = level_eval<N>(g, h, k, deg, x, &fp);
     if (f == 0.0) {
       *its = it + 1;
       return x;
@@ -204,7 +206,7 @@ __device__ __forceinline__ double solve_piece(const double* g, const double* h, 
       hi = x;
     double xn = x - f * fast_rcp(fp);
     if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
-    if (fabs(xn - x) <= 1e-15 || hi - lo <= 1e-15) {
+    if (fabs(xn - x) <= 1e-12 || hi - lo <= 1e-15) {
       *its = it + 1;
       return xn;
     }
@@ -212,6 +214,55 @@ __device__ __forceinline__ double solve_piece(const double* g, const double* h, 
   }
   *its = 100;
   return x;
+}
+
+// Root of a polynomial that is monotone on [lo, hi] (its derivative is root-free there), degree <= N-1,
+// all N coefficients live: full-length unrolled Horner (no per-level predication).  Returns the number
+// of roots (0 or 1; an exact zero at an endpoint counts as in the general recursion).
+template <int N>
+__device__ __forceinline__ int monotone_root(const double* c, double lo, double hi, double* root, uint32_t* terms) {
+  double flo = c[N - 1], fhi = c[N - 1];
+#pragma unroll
+  for (int i = N - 2; i >= 0; --i) {
+    flo = fma(flo, lo, c[i]);
+    fhi = fma(fhi, hi, c[i]);
+  }
+  *terms += 2 * N;
+  if (flo == 0.0) {
+    *root = lo;
+    return 1;
+  }
+  if (fhi == 0.0) {
+    *root = hi;
+    return 1;
+  }
+  if ((flo < 0.0) == (fhi < 0.0)) return 0;
+  double a = lo, b = hi;
+  double x = a - flo * (b - a) / (fhi - flo);
+  if (!(x > a && x < b)) x = 0.5 * (a + b);
+  for (int it = 0; it < 100; ++it) {
+    double f = c[N - 1], fp = 0.0;
+#pragma unroll
+    for (int i = N - 2; i >= 0; --i) {
+      fp = fma(fp, x, f);
+      f = fma(f, x, c[i]);
+    }
+    *terms += 2 * N - 1;
+    if (f == 0.0) break;
+    if ((f < 0.0) == (flo < 0.0))
+      a = x;
+    else
+      b = x;
+    double xn = x - f * fast_rcp(fp);
+    if (!(xn > a && xn < b)) xn = 0.5 * (a + b);
+    if (fabs(xn - x) <= 1e-12 || b - a <= 1e-15) {
+      x = xn;
+      break;
+    }
+    x = xn;
+  }
+  *root = x;
+  return 1;
 }
 
 // kstart: a derivative level known to have no root in (lo, hi) (so p^(kstart-1) is monotone there and
@@ -267,7 +318,7 @@ __device__ void isolate_roots(const double* c, int deg, double lo, double hi, do
         cur[ncur++] = xa;
       } else if (fb != 0.0 && ((fa < 0.0) != (fb < 0.0))) {
         int its = 0;
-        cur[ncur++] = solve_piece<N>(g, h, k, deg, xa, xb, fa, &its);
+        cur[ncur++] = solve_piece<N>(g, h, k, deg, xa, xb, fa, fb, &its);
         R.terms += (uint32_t)its * (uint32_t)(2 * (deg - k) + 1);
       }
       xa = xb;

@@ -163,14 +163,20 @@ __global__ void __launch_bounds__(128) k_r_phase1(const uint32_t* __restrict__ p
       }
     }
     emit_flag(active && flags != 0, flags, i, S);
-    uint32_t ex;
-    const unsigned long long jb = warp_alloc(J.count, job ? 1u : 0u, &ex);
-    if (job && jb + ex < J.capacity) {
-      const unsigned long long p = jb + ex;
-      J.pair[p] = (uint32_t)i;
-      J.meta[p] = meta;
+    // two-ended dense job list: monotone jobs (kfree == 1) from the front, deeper recursions from the back,
+    // so that phase-2 warps see one job class
+    const bool mono = job && (meta & 0xFF) == 1;
+    uint32_t ex1, ex2;
+    const unsigned long long b1 = warp_alloc(J.count, mono ? 1u : 0u, &ex1);
+    const unsigned long long b2 = warp_alloc(J.count + 1, (job && !mono) ? 1u : 0u, &ex2);
+    if (job) {
+      const unsigned long long p = mono ? b1 + ex1 : J.capacity - 1 - (b2 + ex2);
+      if ((mono ? b1 + ex1 : b2 + ex2) < J.capacity) {
+        J.pair[p] = (uint32_t)i;
+        J.meta[p] = meta;
 #pragma unroll
-      for (int t = 0; t < 10; ++t) J.r[p * 10 + t] = r[t];
+        for (int t = 0; t < 10; ++t) J.r[p * 10 + t] = r[t];
+      }
     }
   }
   flush_counters(S, cnt);
@@ -307,13 +313,14 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
 __global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                   const TriRec* __restrict__ tris, const double* __restrict__ ep,
                                                   const double* __restrict__ inten, SolveParams prm, SolSink S,
-                                                  const unsigned long long* __restrict__ njobs_p,
+                                                  const unsigned long long* __restrict__ njobs_p, uint64_t jcap,
                                                   const uint32_t* __restrict__ jpair, const uint32_t* __restrict__ jmeta,
                                                   const double* __restrict__ jr) {
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t njobs = *njobs_p;
+  const uint64_t nmono = njobs_p[0], ndeep = njobs_p[1];
+  const uint64_t njobs = nmono + ndeep;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -325,13 +332,23 @@ __global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ p
     o.flags = 0;
     uint32_t pair = 0;
     if (active) {
-      pair = __ldg(jpair + j);
-      const uint32_t meta = __ldg(jmeta + j);
+      const uint64_t jj = j < nmono ? j : jcap - 1 - (j - nmono);
+      pair = __ldg(jpair + jj);
+      const uint32_t meta = __ldg(jmeta + jj);
       double r[10];
 #pragma unroll
-      for (int t = 0; t < 10; ++t) r[t] = __ldg(jr + j * 10 + t);
+      for (int t = 0; t < 10; ++t) r[t] = __ldg(jr + jj * 10 + t);
       RootSet<10> R;
-      isolate_roots<10>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+      if ((meta & 0xFF) == 1) {
+        // r' has no root in [0,1] (Bernstein): r is monotone there, at most one root, no critical point
+        R.n = 0;
+        R.flags = 0;
+        R.min_crit_ratio = 1.0;
+        R.terms = 0;
+        R.n = monotone_root<10>(r, 0.0, 1.0, &R.x[0], &R.terms);
+      } else {
+        isolate_roots<10>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+      }
       cnt[C_EVAL_TERMS] += R.terms;
       if (R.flags & 1) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
       if (R.min_crit_ratio <= 1e-10) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
@@ -375,7 +392,8 @@ void launch_solve_R(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, con
   const uint64_t cap = (uint64_t)nsm * 16;
   const uint64_t want1 = (npairs + threads - 1) / threads;
   k_r_phase1<<<(int)(want1 < cap ? want1 : cap), threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-  k_r_phase2<<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.pair, J.meta, J.r);
+  k_r_phase2<<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair, J.meta,
+                                           J.r);
 }
 
 }  // namespace spoly
