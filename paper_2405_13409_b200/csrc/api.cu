@@ -294,7 +294,8 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   if (!ctx || !chain || !out) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
   const int k = (int)strlen(chain);
   if (bounces != k || k < 1) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bounces != strlen(chain)");
-  if (strcmp(chain, "R") != 0) return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
+  if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0)
+    return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
   if (!ctx->has_mesh || mesh_id != 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no such mesh");
   if (nq && !endpoints) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null endpoints");
   CK(cudaSetDevice(ctx->device));
@@ -371,7 +372,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(ctx->d_count.ensure(4));
   CK(ctx->d_jpair.ensure(npairs));
   CK(ctx->d_jmeta.ensure(npairs));
-  CK(ctx->d_jr.ensure(npairs * 10));
+  CK(ctx->d_jr.ensure(npairs * kJobStride));
   unsigned long long cnt[4] = {0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     CK(cudaMemsetAsync(ctx->d_count.p, 0, 4 * sizeof(unsigned long long), st));
@@ -379,11 +380,12 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     SolSink S = raw_sink(ctx);
     JobSink J;
     J.count = ctx->d_count.p + 2;
-    J.capacity = std::min(ctx->d_jpair.cap, ctx->d_jr.cap / 10);
+    J.capacity = std::min(ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride);
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
-    launch_solve_R(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J, ctx->nsm, st);
+    launch_solve_k1(chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J, ctx->nsm,
+                    st);
     ctx->launches += 2;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));

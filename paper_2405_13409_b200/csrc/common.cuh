@@ -101,13 +101,14 @@ struct SolSink {
   uint32_t* fflags;
   unsigned long long* counters;  // [C_NUM]
 };
+constexpr int kJobStride = 13;  // doubles per job (r(v) up to degree 12)
 // dense job list between the two solve phases
 struct JobSink {
   unsigned long long* count;
   uint64_t capacity;
   uint32_t* pair;
   uint32_t* meta;  // kfree | deg << 8
-  double* r;       // 10 per job
+  double* r;       // kJobStride per job
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,

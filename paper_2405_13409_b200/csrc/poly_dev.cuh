@@ -164,12 +164,14 @@ static __constant__ double c_falling[16][16] = {
     {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 87178291200.0, 1307674368000.0},
     {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 1307674368000.0}};
 
-// reciprocal good to ~1e-14 relative: FP32 MUFU seed + two FP64 Newton refinements (the Newton step
-// of the root solver only needs an accurate-enough quotient; the bracket guarantees convergence)
+// reciprocal good to ~1e-15 relative: MUFU.RCP64H seed (rcp.approx.ftz.f64) + two FP64 Newton
+// refinements.  The Newton step of the root solver only needs an accurate-enough quotient (the bracket
+// guarantees convergence), so the correctly rounded DDIV sequence is not needed.
 __device__ __forceinline__ double fast_rcp(double x) {
-  double r = (double)__frcp_rn((float)x);
-  if (!(fabs(r) < 1e300) || r == 0.0) return 1.0 / x;  // float over/underflow: exact path
-  r = r * fma(-x, r, 2.0);  // one refinement: ~1e-14 relative, plenty for a Newton quotient
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = r * fma(-x, r, 2.0);
+  r = r * fma(-x, r, 2.0);
   return r;
 }
 

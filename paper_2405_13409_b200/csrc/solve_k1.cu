@@ -1,11 +1,12 @@
-// One-bounce reflection solve ("R", Eq. 21), split into two kernels so that every lane has work:
+// One-bounce solve, reflection "R" (Eq. 21) and refraction "T" (Eq. 22), split into two kernels so that
+// every lane has work:
 //
-//   k_r_phase1 (one thread per (query, triangle) pair, uniform control flow):
-//       decision (reading R1) -> coefficient phase (Eq. 6 a, Eq. 12 b) -> normalise + truncate (c5)
-//       -> elimination phase (Eq. 24 Bezout, Laplace expansion) -> r(v) normalised
-//       -> Bernstein root-exclusion level; pairs whose r may have a root in [0,1] are appended to a
-//       dense job list (warp-aggregated).
-//   k_r_phase2 (one thread per job):
+//   k1_phase1 (one thread per (query, triangle) pair, uniform control flow):
+//       decisions (readings R1, c7) -> coefficient phase (Eq. 6 a; Eq. 12 b for R, Eq. 9 b for T)
+//       -> normalise + truncate (c5) -> elimination phase: r(v) (R: Eq. 24 Bezout + Laplace expansion,
+//       PAPER.md:607; T: Res_u(a,b) by pseudo-remainder, reading R5) -> r normalised -> Bernstein
+//       root-free level; pairs whose r may have a root in [0,1] are appended to a dense job list.
+//   k1_phase2 (one thread per job):
 //       univariate roots (derivative recursion) -> back-substitution
 //       -> (a,b) refinement (reading R2) -> Eq. 3 validation, sides, flags -> contribution (c15)
 //       -> warp-aggregated emission.  The coefficient phase is recomputed from the geometry (same code,
@@ -15,51 +16,79 @@
 
 namespace spoly {
 
-struct SystemR {
-  double A[9], B[25];
+template <bool TC>
+struct Sys1 {
+  static constexpr int DB = TC ? 6 : 4;   // total degree of b (Table 2: square form 6, product form 4)
+  static constexpr int NR = TC ? 13 : 10; // coefficients of r(v): degree 12 (T), 9 (R)
+  double A[9], B[(DB + 1) * (DB + 1)];
+  double eta0, eta1;
   bool relabel;
   uint32_t flags;
-  int n;
+  int da, db, n;
 };
 
-// decision + coefficient phase + normalisation/truncation; false when the system is degenerate
-__device__ __forceinline__ bool build_system_R(d3 x0, d3 x2, const d3 P_in[3], const d3 N_in[3],
-                                               const SolveParams& prm, SystemR& S) {
+// decisions + coefficient phase + normalisation/truncation; false when the system is degenerate
+template <bool TC>
+__device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], const d3 N_in[3],
+                                             const SolveParams& prm, Sys1<TC>& S) {
+  constexpr int DB = Sys1<TC>::DB;
   S.flags = 0;
-  // reading R1: incidence-plane normal l_c = (x2 - x0) x n(centroid); t = n x e1 unless e2 is further
-  // out of the incidence plane (then the relabeling p1 <-> p2)
+  // reading R1: incidence-plane normal l_c = (x2 - x0) x n(centroid)
   const d3 nc = (1.0 / 3.0) * (N_in[0] + N_in[1] + N_in[2]);
   const d3 lc = cross(x2 - x0, nc);
   const double ln = norm(lc);
   if (!(ln > 1e-12 * norm(x2 - x0) * norm(nc))) S.flags |= SPOLY_FLAG_DEGENERATE;
   const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
   S.relabel = false;
-  if (ln > 0) {
-    const double s1 = fabs(dot(e1o, lc)) / (norm(e1o) * ln), s2 = fabs(dot(e2o, lc)) / (norm(e2o) * ln);
-    S.relabel = s1 < s2;
+  S.eta0 = S.eta1 = 1.0;
+  if (!TC) {
+    // product form: t = n x e1 unless e2 is further out of the incidence plane (relabel p1 <-> p2)
+    if (ln > 0) {
+      const double s1 = fabs(dot(e1o, lc)) / (norm(e1o) * ln), s2 = fabs(dot(e2o, lc)) / (norm(e2o) * ln);
+      S.relabel = s1 < s2;
+    }
+  } else {
+    // c7: eta_0 from the side of x_0 w.r.t. the triangle's geometric plane; refraction flips the medium
+    const bool front = dot(x0 - P_in[0], cross(e1o, e2o)) > 0;
+    S.eta0 = front ? prm.eta_front : prm.eta_back;
+    S.eta1 = front ? prm.eta_back : prm.eta_front;
   }
   const d3 p0 = P_in[0], p1 = S.relabel ? P_in[2] : P_in[1], p2 = S.relabel ? P_in[1] : P_in[2];
   const d3 n0 = N_in[0], n1 = S.relabel ? N_in[2] : N_in[1], n2 = S.relabel ? N_in[1] : N_in[2];
   const d3 e1 = p1 - p0, e2 = p2 - p0, m1 = n1 - n0, m2 = n2 - n0;
   const d3 q = p0 - x0, w = x2 - x0;
   build_a(q, w, e1, e2, n0, m1, m2, S.A);
-  build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
-  const double ma = bmaxabs<2, 3>(S.A), mb = bmaxabs<4, 5>(S.B);
+  if (TC) {
+    const d3 l = ln > 0 ? (1.0 / ln) * lc : mk3(1, 0, 0);
+    build_b_T(q, w, e1, e2, n0, m1, m2, l, S.eta0, S.eta1, S.B);
+  } else {
+    build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
+  }
+  const double ma = bmaxabs<2, 3>(S.A), mb = bmaxabs<DB, DB + 1>(S.B);
   if (!(ma > 0) || !(mb > 0)) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
   }
   bscale<2, 3>(S.A, 1.0 / ma);
-  bscale<4, 5>(S.B, 1.0 / mb);
-  const int da = bnum_udeg<2, 3>(S.A, prm.tau_trunc), db = bnum_udeg<4, 5>(S.B, prm.tau_trunc);
-  btrunc_u<2, 3>(S.A, da);
-  btrunc_u<4, 5>(S.B, db);
-  S.n = max(da, db);
+  bscale<DB, DB + 1>(S.B, 1.0 / mb);
+  S.da = bnum_udeg<2, 3>(S.A, prm.tau_trunc);
+  S.db = bnum_udeg<DB, DB + 1>(S.B, prm.tau_trunc);
+  btrunc_u<2, 3>(S.A, S.da);
+  btrunc_u<DB, DB + 1>(S.B, S.db);
+  S.n = max(S.da, S.db);
   if (S.n == 0) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
   }
   return true;
+}
+
+template <bool TC>
+__device__ __forceinline__ void eliminate(const Sys1<TC>& S, double* r) {
+  if (TC)
+    resultant_T(S.A, S.B, S.da, S.db, r);
+  else
+    det_R(S.A, S.B, S.n, r);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -113,10 +142,12 @@ __device__ __forceinline__ void load_pair(const uint32_t* __restrict__ pq, const
 }
 
 // ---------------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k_r_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                                  uint64_t npairs, const TriRec* __restrict__ tris,
-                                                  const double* __restrict__ ep, SolveParams prm, SolSink S,
-                                                  JobSink J) {
+template <bool TC>
+__global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                    uint64_t npairs, const TriRec* __restrict__ tris,
+                                                    const double* __restrict__ ep, SolveParams prm, SolSink S,
+                                                    JobSink J) {
+  constexpr int NR = Sys1<TC>::NR;
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
@@ -128,33 +159,33 @@ __global__ void __launch_bounds__(128) k_r_phase1(const uint32_t* __restrict__ p
     const bool active = i < npairs;
     bool job = false;
     uint32_t flags = 0, meta = 0;
-    double r[10];
+    double r[NR];
     if (active) {
       d3 P[3], N[3], x0, x2;
       uint32_t q;
       load_pair(pq, pt, tris, ep, i, P, N, x0, x2, q);
       cnt[C_PAIRS]++;
-      SystemR Sys;
-      const bool ok = build_system_R(x0, x2, P, N, prm, Sys);
+      Sys1<TC> Sys;
+      const bool ok = build_system<TC>(x0, x2, P, N, prm, Sys);
       flags = Sys.flags;
       if (ok) {
         cnt[C_SYSTEMS]++;
-        det_R(Sys.A, Sys.B, Sys.n, r);
+        eliminate<TC>(Sys, r);
         double mr = 0.0;
 #pragma unroll
-        for (int t = 0; t < 10; ++t) mr = fmax(mr, fabs(r[t]));
+        for (int t = 0; t < NR; ++t) mr = fmax(mr, fabs(r[t]));
         if (!(mr > 0)) {
           flags |= SPOLY_FLAG_DEGENERATE;
         } else {
           int deg = 0;
           const double inv = 1.0 / mr;
 #pragma unroll
-          for (int t = 0; t < 10; ++t) {
+          for (int t = 0; t < NR; ++t) {
             r[t] *= inv;
             if (r[t] != 0.0) deg = t;
           }
-          cnt[C_EVAL_TERMS] += 55 + 23;  // Bernstein transform + forward differences
-          const int kfree = bernstein_root_free_level(r);
+          cnt[C_EVAL_TERMS] += NR * (NR + 1) / 2 + NR * (NR - 1) / 4;  // Bernstein + differences
+          const int kfree = bernstein_root_free_level<NR>(r);
           if (kfree > 0 && deg > 0) {
             job = true;
             meta = (uint32_t)kfree | ((uint32_t)deg << 8);
@@ -169,23 +200,23 @@ __global__ void __launch_bounds__(128) k_r_phase1(const uint32_t* __restrict__ p
     uint32_t ex1, ex2;
     const unsigned long long b1 = warp_alloc(J.count, mono ? 1u : 0u, &ex1);
     const unsigned long long b2 = warp_alloc(J.count + 1, (job && !mono) ? 1u : 0u, &ex2);
-    if (job) {
+    if (job && (mono ? b1 + ex1 : b2 + ex2) < J.capacity) {
       const unsigned long long p = mono ? b1 + ex1 : J.capacity - 1 - (b2 + ex2);
-      if ((mono ? b1 + ex1 : b2 + ex2) < J.capacity) {
-        J.pair[p] = (uint32_t)i;
-        J.meta[p] = meta;
+      J.pair[p] = (uint32_t)i;
+      J.meta[p] = meta;
 #pragma unroll
-        for (int t = 0; t < 10; ++t) J.r[p * 10 + t] = r[t];
-      }
+      for (int t = 0; t < NR; ++t) J.r[p * kJobStride + t] = r[t];
     }
   }
   flush_counters(S, cnt);
 }
 
 // ---------------------------------------------------------------------------------------------
-__device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
-                             const SolveParams& prm, const SystemR& Sys, const double* vr, int nv, PairOut& out,
-                             uint32_t* cnt) {
+template <bool TC>
+__device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
+                           const SolveParams& prm, const Sys1<TC>& Sys, const double* vr, int nv, PairOut& out,
+                           uint32_t* cnt) {
+  constexpr int DB = Sys1<TC>::DB;
   const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
   const d3 g_geo = cross(e1o, e2o);
   const double* A = Sys.A;
@@ -225,12 +256,12 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       }
     } else {
       // fallback (c11): a(., v*) == 0 -> roots of b(., v*) on [-0.1, 1.1]
-      double bl[5];
-      bslices_at<4, 5>(B, vs, bl);
+      double bl[DB + 1];
+      bslices_at<DB, DB + 1>(B, vs, bl);
       double bmax = 0.0;
       int bd = 0;
 #pragma unroll
-      for (int i = 0; i < 5; ++i) {
+      for (int i = 0; i <= DB; ++i) {
         bmax = fmax(bmax, fabs(bl[i]));
         if (bl[i] != 0.0) bd = i;
       }
@@ -238,8 +269,8 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
         out.flags |= SPOLY_FLAG_DEGENERATE;
         continue;
       }
-      RootSet<5> Rb;
-      isolate_roots<5>(bl, bd, -0.1, 1.1, 1e-7, Rb);
+      RootSet<DB + 1> Rb;
+      isolate_roots<DB + 1>(bl, bd, -0.1, 1.1, 1e-7, Rb);
       for (int i = 0; i < Rb.n && nu < 4; ++i)
         if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) ua[nu++] = Rb.x[i];
     }
@@ -250,7 +281,7 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       // stays within 1e-3 of its back-substituted position (local refinement, never a search)
       double fa, fau, fav, fb, fbu, fbv;
       beval<2, 3>(A, us, vv, &fa, &fau, &fav);
-      beval<4, 5>(B, us, vv, &fb, &fbu, &fbv);
+      beval<DB, DB + 1>(B, us, vv, &fb, &fbu, &fbv);
       for (int it = 0; it < 3; ++it) {
         const double det = fau * fbv - fav * fbu;
         if (det == 0.0) break;
@@ -259,7 +290,7 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
         if (!(fmax(fabs(us + du - ua[iu]), fabs(vv + dv - vs)) <= 1e-3)) break;
         double na, nau, nav, nb, nbu, nbv;
         beval<2, 3>(A, us + du, vv + dv, &na, &nau, &nav);
-        beval<4, 5>(B, us + du, vv + dv, &nb, &nbu, &nbv);
+        beval<DB, DB + 1>(B, us + du, vv + dv, &nb, &nbu, &nbv);
         if (!(na * na + nb * nb < fa * fa + fb * fb)) break;
         us += du;
         vv += dv;
@@ -271,9 +302,9 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
       const d3 nx = N_in[0] + ur * (N_in[1] - N_in[0]) + vr_ * (N_in[2] - N_in[0]);
       const double ed = fmin(fmin(ur, vr_), 1.0 - ur - vr_);
       const bool inside = ur >= -prm.eps_domain && vr_ >= -prm.eps_domain && ur + vr_ <= 1.0 + prm.eps_domain;
-      const double rho = vertex_residual(x0, x1, x2, nx, 1.0, 1.0);
+      const double rho = vertex_residual(x0, x1, x2, nx, Sys.eta0, Sys.eta1);
       if (!inside) {
-        if (ed >= -prm.eps_flag && rho < prm.theta_final && side_ok(false, x0, x1, x2, nx, g_geo))
+        if (ed >= -prm.eps_flag && rho < prm.theta_final && side_ok(TC, x0, x1, x2, nx, g_geo))
           out.flags |= SPOLY_FLAG_BOUNDARY;
         cnt[C_REJ_DOMAIN]++;
         continue;
@@ -282,7 +313,7 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
         cnt[C_REJ_CONSTRAINT]++;
         continue;
       }
-      if (!side_ok(false, x0, x1, x2, nx, g_geo)) {
+      if (!side_ok(TC, x0, x1, x2, nx, g_geo)) {
         cnt[C_REJ_SIDE]++;
         continue;
       }
@@ -297,7 +328,9 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
         continue;
       }
       if (out.nsol < kMaxSolPerPair) {
-        const double J = jacobian_k1(false, x0, x2, x1, e1o, e2o, N_in[1] - N_in[0], N_in[2] - N_in[0], nx, 1.0, 1.0);
+        // light-side trace: incoming medium eta_1 (light side), outgoing eta_0
+        const double J = jacobian_k1(TC, x0, x2, x1, e1o, e2o, N_in[1] - N_in[0], N_in[2] - N_in[0], nx, Sys.eta1,
+                                     Sys.eta0);
         const int s = out.nsol++;
         out.u[s] = ur;
         out.v[s] = vr_;
@@ -310,12 +343,14 @@ __device__ void path_phase_R(d3 x0, d3 x2, double intensity, const d3 P_in[3], c
   }
 }
 
-__global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                                  const TriRec* __restrict__ tris, const double* __restrict__ ep,
-                                                  const double* __restrict__ inten, SolveParams prm, SolSink S,
-                                                  const unsigned long long* __restrict__ njobs_p, uint64_t jcap,
-                                                  const uint32_t* __restrict__ jpair, const uint32_t* __restrict__ jmeta,
-                                                  const double* __restrict__ jr) {
+template <bool TC>
+__global__ void __launch_bounds__(128) k1_phase2(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                 const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                                 const double* __restrict__ inten, SolveParams prm, SolSink S,
+                                                 const unsigned long long* __restrict__ njobs_p, uint64_t jcap,
+                                                 const uint32_t* __restrict__ jpair, const uint32_t* __restrict__ jmeta,
+                                                 const double* __restrict__ jr) {
+  constexpr int NR = Sys1<TC>::NR;
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
@@ -335,24 +370,23 @@ __global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ p
       const uint64_t jj = j < nmono ? j : jcap - 1 - (j - nmono);
       pair = __ldg(jpair + jj);
       const uint32_t meta = __ldg(jmeta + jj);
-      double r[10];
+      double r[NR];
 #pragma unroll
-      for (int t = 0; t < 10; ++t) r[t] = __ldg(jr + jj * 10 + t);
-      RootSet<10> R;
+      for (int t = 0; t < NR; ++t) r[t] = __ldg(jr + jj * kJobStride + t);
+      RootSet<NR> R;
       if ((meta & 0xFF) == 1) {
         // r' has no root in [0,1] (Bernstein): r is monotone there, at most one root, no critical point
-        R.n = 0;
         R.flags = 0;
         R.min_crit_ratio = 1.0;
         R.terms = 0;
-        R.n = monotone_root<10>(r, 0.0, 1.0, &R.x[0], &R.terms);
+        R.n = monotone_root<NR>(r, 0.0, 1.0, &R.x[0], &R.terms);
       } else {
-        isolate_roots<10>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+        isolate_roots<NR>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
       }
       cnt[C_EVAL_TERMS] += R.terms;
       if (R.flags & 1) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
       if (R.min_crit_ratio <= 1e-10) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
-      double vr[10];
+      double vr[NR];
       int nv = 0;
       for (int i = 0; i < R.n; ++i)
         if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
@@ -361,10 +395,10 @@ __global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ p
         d3 P[3], N[3], x0, x2;
         uint32_t q;
         load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
-        SystemR Sys;
-        build_system_R(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (already known non-degenerate)
+        Sys1<TC> Sys;
+        build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
         const double I = inten ? __ldg(inten + q) : 1.0;
-        path_phase_R(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
+        path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
       }
     }
     emit_flag(active && o.flags != 0, o.flags, pair, S);
@@ -384,16 +418,23 @@ __global__ void __launch_bounds__(128) k_r_phase2(const uint32_t* __restrict__ p
   flush_counters(S, cnt);
 }
 
-void launch_solve_R(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M, const double* ep,
-                    const double* inten, const SolveParams& prm, const SolSink& S, const JobSink& J, int nsm,
-                    cudaStream_t st) {
+void launch_solve_k1(int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
+                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S,
+                     const JobSink& J, int nsm, cudaStream_t st) {
   if (npairs == 0) return;
   const int threads = 128;
   const uint64_t cap = (uint64_t)nsm * 16;
   const uint64_t want1 = (npairs + threads - 1) / threads;
-  k_r_phase1<<<(int)(want1 < cap ? want1 : cap), threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-  k_r_phase2<<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair, J.meta,
-                                           J.r);
+  const int g1 = (int)(want1 < cap ? want1 : cap);
+  if (refract) {
+    k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
+    k1_phase2<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
+                                                   J.meta, J.r);
+  } else {
+    k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
+    k1_phase2<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
+                                                    J.meta, J.r);
+  }
 }
 
 }  // namespace spoly

@@ -27,36 +27,160 @@ static __constant__ double c_bern9[10][10] = {
 
 constexpr int kMaxSolPerPair = 8;
 
-// Bernstein exclusion (exact, no effect on the root set): the degree-9 Bernstein coefficients b of r on
+// monomial -> degree-12 Bernstein basis on [0,1]
+static __constant__ double c_bern12[13][13] = {
+    {1.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.08333333333333333, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.16666666666666666, 0.015151515151515152, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.25, 0.045454545454545456, 0.004545454545454545, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.3333333333333333, 0.09090909090909091, 0.01818181818181818, 0.00202020202020202, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.4166666666666667, 0.15151515151515152, 0.045454545454545456, 0.010101010101010102, 0.0012626262626262627, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.5, 0.22727272727272727, 0.09090909090909091, 0.030303030303030304, 0.007575757575757576, 0.0010822510822510823, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.5833333333333334, 0.3181818181818182, 0.1590909090909091, 0.0707070707070707, 0.026515151515151516, 0.007575757575757576, 0.0012626262626262627, 0.0, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.6666666666666666, 0.42424242424242425, 0.2545454545454545, 0.1414141414141414, 0.0707070707070707, 0.030303030303030304, 0.010101010101010102, 0.00202020202020202, 0.0, 0.0, 0.0, 0.0},
+    {1.0, 0.75, 0.5454545454545454, 0.38181818181818183, 0.2545454545454545, 0.1590909090909091, 0.09090909090909091, 0.045454545454545456, 0.01818181818181818, 0.004545454545454545, 0.0, 0.0, 0.0},
+    {1.0, 0.8333333333333334, 0.6818181818181818, 0.5454545454545454, 0.42424242424242425, 0.3181818181818182, 0.22727272727272727, 0.15151515151515152, 0.09090909090909091, 0.045454545454545456, 0.015151515151515152, 0.0, 0.0},
+    {1.0, 0.9166666666666666, 0.8333333333333334, 0.75, 0.6666666666666666, 0.5833333333333334, 0.5, 0.4166666666666667, 0.3333333333333333, 0.25, 0.16666666666666666, 0.08333333333333333, 0.0},
+    {1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0, 1.0}};
+
+// Bernstein exclusion (exact, no effect on the root set): the degree-D Bernstein coefficients b of r on
 // [0,1] bound r there (convex hull property), and the k-th derivative of r has the Bernstein coefficients
-// 9!/(9-k)! * (k-th forward differences of b).  When the k-th differences all have one strict sign,
+// D!/(D-k)! * (k-th forward differences of b).  When the k-th differences all have one strict sign,
 // r^(k) has no root in [0,1]; the derivative recursion can then start at level k-1 with
 // no critical points, because every higher level only serves to locate the roots of r^(k).
-// Returns the smallest such k (0: r itself has no root in [0,1]; 10: none found).
+// Returns the smallest such k (0: r itself has no root in [0,1]; N: none found).  N = D + 1.
+template <int N>
 __device__ __forceinline__ int bernstein_root_free_level(const double* r) {
-  double b[10];
+  double b[N];
 #pragma unroll
-  for (int k = 0; k < 10; ++k) {
+  for (int k = 0; k < N; ++k) {
     double acc = 0.0;
 #pragma unroll
-    for (int i = 0; i <= k; ++i) acc = fma(c_bern9[k][i], r[i], acc);
+    for (int i = 0; i <= k; ++i) acc = fma(N == 10 ? c_bern9[k][i] : c_bern12[k][i], r[i], acc);
     b[k] = acc;
   }
-  int level = 10;
+  int level = N;
 #pragma unroll
-  for (int k = 0; k < 9; ++k) {
+  for (int k = 0; k < N - 1; ++k) {
     bool pos = true, neg = true;
 #pragma unroll
-    for (int i = 0; i < 10 - k; ++i) {
+    for (int i = 0; i < N - k; ++i) {
       pos = pos && (b[i] > 0.0);
       neg = neg && (b[i] < 0.0);
     }
-    if ((pos || neg) && level == 10) level = k;
-    // next differences
+    if ((pos || neg) && level == N) level = k;
 #pragma unroll
-    for (int i = 0; i < 9 - k; ++i) b[i] = b[i + 1] - b[i];
+    for (int i = 0; i < N - 1 - k; ++i) b[i] = b[i + 1] - b[i];
   }
   return level;
+}
+
+// T: r(v) = Res_u(a, b) up to a constant, by pseudo-division of b by a (a's u^2 coefficient a_2 is a
+// constant because a has total degree 2).  Exact identity with the Bezout determinant of Eq. 24:
+// det R(v) = +-lc_u(b)^(n - deg_u a) Res_u(a, b); the lc_u(b) roots it drops never carry a common root
+// of (a, b), so the admissible chains are the same (reading R5).
+__device__ __forceinline__ void resultant_T(const double* A /*3x3*/, const double* B /*7x7*/, int da, int db,
+                                            double* r /*13*/) {
+#pragma unroll
+  for (int t = 0; t < 13; ++t) r[t] = 0.0;
+  double a0[3] = {A[0], A[1], A[2]}, a1[2] = {A[3], A[4]};
+  const double a2 = A[6];
+  if (db == 0) {  // b u-free: its roots in v, then u from a
+#pragma unroll
+    for (int t = 0; t < 7; ++t) r[t] = B[t];
+    return;
+  }
+  if (da == 0) {  // a u-free: det = +-a0^n b_n^n -> roots of a0 (b_n roots never admissible)
+#pragma unroll
+    for (int t = 0; t < 3; ++t) r[t] = a0[t];
+    return;
+  }
+  double c[7][7];
+#pragma unroll
+  for (int j = 0; j < 7; ++j)
+#pragma unroll
+    for (int t = 0; t < 7; ++t) c[j][t] = (j + t <= 6) ? B[j * 7 + t] : 0.0;
+  if (da == 1) {
+    // Res(a, b) = sum_j b_j (-a0)^j a1^(db-j), Horner in (-a0) with running powers of a1
+    double t_[13], p[13];  // accumulated polynomial, a1 power
+#pragma unroll
+    for (int t = 0; t < 13; ++t) t_[t] = p[t] = 0.0;
+    p[0] = 1.0;
+#pragma unroll
+    for (int j = 6; j >= 0; --j) {
+      if (j > db) continue;
+      if (j == db) {
+#pragma unroll
+        for (int t = 0; t < 7; ++t) t_[t] = c[j][t];
+      } else {
+        // p <- p * a1
+        double np[13];
+#pragma unroll
+        for (int t = 0; t < 13; ++t) np[t] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 12; ++t) {
+          np[t] = fma(p[t], a1[0], np[t]);
+          np[t + 1] = fma(p[t], a1[1], np[t + 1]);
+        }
+        // t <- t * (-a0) + c_j * p
+        double nt[13];
+#pragma unroll
+        for (int t = 0; t < 13; ++t) nt[t] = 0.0;
+#pragma unroll
+        for (int t = 0; t < 11; ++t)
+#pragma unroll
+          for (int s = 0; s < 3; ++s) nt[t + s] = fma(-t_[t], a0[s], nt[t + s]);
+#pragma unroll
+        for (int t = 0; t < 7; ++t)
+#pragma unroll
+          for (int s = 0; s < 13; ++s)
+            if (t + s < 13) nt[t + s] = fma(c[j][t], np[s], nt[t + s]);
+#pragma unroll
+        for (int t = 0; t < 13; ++t) {
+          t_[t] = nt[t];
+          p[t] = np[t];
+        }
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 13; ++t) r[t] = t_[t];
+    return;
+  }
+  // da == 2: pseudo-remainder of b by a (degree <= 1 in u)
+#pragma unroll
+  for (int j = 6; j >= 2; --j) {
+    if (j > db) continue;
+    double lead[7];
+#pragma unroll
+    for (int t = 0; t < 7; ++t) lead[t] = c[j][t];
+#pragma unroll
+    for (int i = 0; i < j; ++i)
+#pragma unroll
+      for (int t = 0; t < 7; ++t) c[i][t] *= a2;
+#pragma unroll
+    for (int t = 0; t < 6; ++t) {
+      c[j - 1][t] = fma(-lead[t], a1[0], c[j - 1][t]);
+      c[j - 1][t + 1] = fma(-lead[t], a1[1], c[j - 1][t + 1]);
+    }
+#pragma unroll
+    for (int t = 0; t < 5; ++t)
+#pragma unroll
+      for (int s = 0; s < 3; ++s) c[j - 2][t + s] = fma(-lead[t], a0[s], c[j - 2][t + s]);
+  }
+  // Res(a, rho1 u + rho0) = a2 rho0^2 - a1 rho0 rho1 + a0 rho1^2
+  const double* rho0 = c[0];
+  const double* rho1 = c[1];
+#pragma unroll
+  for (int t = 0; t < 7; ++t)
+#pragma unroll
+    for (int s = 0; s < 7; ++s) {
+      r[t + s] = fma(a2 * rho0[t], rho0[s], r[t + s]);
+      r[t + s] = fma(a0[0] * rho1[t], rho1[s], r[t + s]);
+      if (t + s + 1 < 13) r[t + s + 1] = fma(a0[1] * rho1[t], rho1[s], r[t + s + 1]);
+      if (t + s + 2 < 13) r[t + s + 2] = fma(a0[2] * rho1[t], rho1[s], r[t + s + 2]);
+      r[t + s] = fma(-a1[0] * rho0[t], rho1[s], r[t + s]);
+      if (t + s + 1 < 13) r[t + s + 1] = fma(-a1[1] * rho0[t], rho1[s], r[t + s + 1]);
+    }
 }
 
 struct PairOut {

@@ -139,3 +139,47 @@ def test_c2_full_size_sampled(orc, sp, torch_cuda):
     b = g["bary"]
     assert np.all(b[:, 0] >= -1e-9) and np.all(b[:, 1] >= -1e-9) and np.all(b.sum(1) <= 1 + 1e-9)
     assert abs(g["per_query"].sum() - g["contribution"].sum()) <= 1e-9 * abs(g["contribution"].sum())
+
+
+# ---------------------------------------------------------------- one-bounce refraction (T, Eq. 22)
+def test_random_interpolated_T(orc, sp, torch_cuda):
+    rng = np.random.default_rng(13)
+    mesh = W.random_triangles(rng, 300, 0.3, normal_tilt=0.3)
+    mesh.eta_front, mesh.eta_back = 1.0, 1.5
+    Q = 24
+    ep = np.zeros((Q, 2, 3))
+    ep[:, 0] = rng.uniform(-1, 1, (Q, 3)) * [1, 1, 0.3] + [0, 0, 1.5]
+    ep[:, 1] = rng.uniform(-1, 1, (Q, 3)) * [1, 1, 0.3] + [0, 0, -1.8]
+    ep[Q // 2:] = ep[Q // 2:, ::-1]  # half the queries from below (both media orders)
+    ro = orc.solve(mesh, "T", ep, cfg=orc.default_config(cull=0))
+    g = _gpu_solve(sp, torch_cuda, mesh, "T", ep, cfg=sp.default_config(cull=0))
+    st = parity.compare(ro, g, Q)
+    assert st["compared_solutions"] > 30, st
+    ro2 = orc.solve(mesh, "T", ep)
+    g2 = _gpu_solve(sp, torch_cuda, mesh, "T", ep)
+    parity.compare(ro2, g2, Q)
+
+
+def test_flat_interface_T(orc, sp, torch_cuda):
+    pos = np.array([[-4, -4, 0], [6, -4, 0], [-4, 6, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    mesh = W.Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32), 1.0, 1.33)
+    rng = np.random.default_rng(3)
+    ep = np.zeros((32, 2, 3))
+    ep[:, 0] = np.c_[rng.uniform(-0.8, 0.8, (32, 2)), rng.uniform(0.5, 2, 32)]
+    ep[:, 1] = np.c_[rng.uniform(-0.8, 0.8, (32, 2)), -rng.uniform(0.5, 2, 32)]
+    ro = orc.solve(mesh, "T", ep, cfg=orc.default_config(cull=0))
+    g = _gpu_solve(sp, torch_cuda, mesh, "T", ep, cfg=sp.default_config(cull=0))
+    parity.compare(ro, g, 32)
+    assert g["query"].shape[0] == 32  # exactly one refraction path per query
+
+
+def test_c3_pool_subset_parity(orc, sp, torch_cuda):
+    """C3 pool (199,712-tri water surface), 48 floor receivers: cull + solve vs the oracle's cull + solve."""
+    w = W.pool_c3(res=512)
+    sub = w.subset(np.linspace(0, w.nqueries - 1, 48).astype(np.int64))
+    ro = orc.solve(sub.mesh, "T", sub.endpoints)
+    g = _gpu_solve(sp, torch_cuda, sub.mesh, "T", sub.endpoints)
+    st = parity.compare(ro, g, sub.nqueries)
+    assert st["compared_solutions"] >= 20, st
+    assert np.all(g["residual"] < 1e-6)
