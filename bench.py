@@ -30,19 +30,26 @@ METRIC = "admissible specular paths/sec and query-tuple solves/sec at 1/2/4/8 B2
 UNIT = "paths/s"
 
 # ---------------------------------------------------------------- algorithmic FLOP model
-# Minimal-form FP64 FLOPs of the one-bounce reflection solve (FMA = 2 FLOPs), counted from the kernel's
-# formulas: per pair (decision + build a,b + normalise + 3x3 Bezout + Laplace), per FMA term of the
-# univariate root-finding evaluations (counter n_eval_terms), per candidate (back-substitution, one (a,b)
-# evaluation, Eq. 3 validation), per admissible chain (analytic ray-differential Jacobian).
-FLOP_PER_PAIR_R = 880
+# Minimal-form FP64 FLOPs of the one-bounce reflection solve (FMA = 2, add/mul/div/sqrt = 1), counted
+# from the kernel formulas (DESIGN.md §5 table):
+#   phase 1, per pair: decision 75 + setup 18 + a 75 + b 268 + normalise 22 + truncation 10 + Bezout 128
+#                      + Laplace 316 + normalise r 11 + Bernstein level 155                  = 1078
+#   phase 2: 2 per FMA term of the root-finding evaluations (counter n_eval_terms)
+#            + 468 per coefficient-phase rebuild (counter n_rebuilds)
+#            + 430 per candidate (back-substitution 25, one (a,b) Newton step 277, Eq. 3 + sides 130)
+#            + 250 per admissible chain (analytic ray-differential Jacobian)
+FLOP_PHASE1_PER_PAIR_R = 1078
 FLOP_PER_EVAL_TERM = 2
-FLOP_PER_CANDIDATE_R = 270
-FLOP_PER_ADMISSIBLE_R = 290
+FLOP_PER_REBUILD_R = 468
+FLOP_PER_CANDIDATE_R = 430
+FLOP_PER_ADMISSIBLE_R = 250
 
 
 def flop_model_R(rep):
-    return (rep["n_pairs_in"] * FLOP_PER_PAIR_R + rep["n_eval_terms"] * FLOP_PER_EVAL_TERM +
-            rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
+    p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_R
+    p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_R +
+          rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
+    return p1, p2
 
 
 # FP64 ALU peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz;
@@ -149,8 +156,8 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--res", type=int, default=256, help="C2 light-sample grid (256 -> 65,536 queries)")
-    ap.add_argument("--cpu-sample", type=int, default=48)
-    ap.add_argument("--ref-sample", type=int, default=24)
+    ap.add_argument("--cpu-sample", type=int, default=256)
+    ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -241,19 +248,23 @@ def main():
         gathered = [torch.empty_like(r.per_query) for _ in range(world)]
         dist.all_gather(gathered, r.per_query.contiguous())
 
-    # ---- roofline of the dominant kernel (solve), from its own launch's CUDA-event time
+    # ---- roofline of the dominant kernel, from its own launch's CUDA-event time (recorded by the library on
+    # the launching stream around each solve kernel, averaged over the timed steps)
     rep = reports[-1]
-    flops = flop_model_R(rep)
-    solve_s = statistics.mean(solve_ms) / 1e3
-    achieved = flops / solve_s
+    f1, f2 = flop_model_R(rep)
+    t1 = statistics.mean(x["ms_phase1"] for x in reports) / 1e3
+    t2 = statistics.mean(x["ms_phase2"] for x in reports) / 1e3
     peak = fp64_peak()
+    dom = ("k1_phase2<R>", f2, t2) if t2 >= t1 else ("k1_phase1<R>", f1, t1)
+    achieved = dom[1] / dom[2]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "solve_traffic.json")
     if os.path.exists(tp):
         try:
-            traffic = json.load(open(tp)).get("bytes_per_launch")
+            traffic = json.load(open(tp)).get(dom[0], {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    measured_fp64 = ctx.bench_fma(True, 0.5) if rank == 0 else None
 
     if rank != 0:
         if world > 1:
@@ -277,10 +288,13 @@ def main():
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": solve_s * 1e3,
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
-        "roofline": {"bound": "alu", "kernel": "k_solve_R_list", "achieved": achieved / 1e12, "peak": peak / 1e12,
-                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                     "flop_per_launch": flops,
-                     "peak_note": "FP64: 148 SMs x 64 FMA/clk x 2 x 1965 MHz (unit counts x clocks.max.sm)"},
+        "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,
+                     "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "flop_per_launch": dom[1],
+                     "peak_note": "FP64: 148 SMs x 64 FMA/clk x 2 x 1965 MHz (unit counts x clocks.max.sm)",
+                     "measured_fp64_fma_tflops": measured_fp64 / 1e12 if measured_fp64 else None,
+                     "phases": {"k1_phase1<R>": {"ms": t1 * 1e3, "tflops": f1 / t1 / 1e12, "frac": f1 / t1 / peak},
+                                "k1_phase2<R>": {"ms": t2 * 1e3, "tflops": f2 / t2 / 1e12, "frac": f2 / t2 / peak},
+                                "solve_total": {"ms": (t1 + t2) * 1e3, "frac": (f1 + f2) / (t1 + t2) / peak}}},
         "clocks": clocks,
         "gpu_launches": launches,
     }

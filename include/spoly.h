@@ -106,6 +106,9 @@ typedef struct {
   uint64_t n_eval_terms;              /* FMA terms of the univariate root-finding evaluations
                                          (input of the algorithmic FLOP model)     */
   uint64_t required_solutions;        /* set with SPOLY_ERR_CAPACITY                            */
+  float ms_phase1, ms_phase2;         /* CUDA-event times of the two solve kernels (phase 2 incl.
+                                         the count read-back)                                    */
+  uint64_t n_rebuilds;                /* phase-2 coefficient-phase recomputations (FLOP model)   */
 } spoly_report;
 
 typedef struct {

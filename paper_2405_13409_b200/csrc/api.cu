@@ -70,7 +70,7 @@ struct spoly_ctx {
   DBuf<double> d_ep, d_int;
   double* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint32_t launches = 0;
 };
 
@@ -384,8 +384,12 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
-    launch_solve_k1(chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J, ctx->nsm,
-                    st);
+    CK(cudaEventRecord(ctx->ev[4], st));
+    launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
+                    ctx->nsm, st);
+    CK(cudaEventRecord(ctx->ev[5], st));
+    launch_solve_k1(2, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
+                    ctx->nsm, st);
     ctx->launches += 2;
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
@@ -504,6 +508,12 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   cudaEventElapsedTime(&R.ms_cull, ctx->ev[0], ctx->ev[1]);
   cudaEventElapsedTime(&R.ms_solve, ctx->ev[1], ctx->ev[2]);
   cudaEventElapsedTime(&R.ms_reduce, ctx->ev[2], ctx->ev[3]);
+  R.ms_phase1 = R.ms_phase2 = 0.f;
+  if (npairs) {
+    cudaEventElapsedTime(&R.ms_phase1, ctx->ev[4], ctx->ev[5]);
+    cudaEventElapsedTime(&R.ms_phase2, ctx->ev[5], ctx->ev[2]);
+  }
+  R.n_rebuilds = counters[C_REBUILDS];
   R.n_launches = ctx->launches;
   R.n_eval_terms = counters[C_EVAL_TERMS];
   return SPOLY_OK;

@@ -21,9 +21,9 @@ void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32
                         uint32_t* pair_query, uint32_t* pair_tpos, int nsm, cudaStream_t st);
 
 // solve_k1.cu
-void launch_solve_k1(int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S,
-                     const JobSink& J, int nsm, cudaStream_t st);
+void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs,
+                     const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
+                     const SolSink& S, const JobSink& J, int nsm, cudaStream_t st);
 
 // reduce.cu
 struct OutArrays {

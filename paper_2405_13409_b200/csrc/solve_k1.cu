@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(128) k1_phase2(const uint32_t* __restrict__ pq
         load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
         Sys1<TC> Sys;
         build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
+        cnt[C_REBUILDS]++;
         const double I = inten ? __ldg(inten + q) : 1.0;
         path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
       }
@@ -418,22 +419,26 @@ __global__ void __launch_bounds__(128) k1_phase2(const uint32_t* __restrict__ pq
   flush_counters(S, cnt);
 }
 
-void launch_solve_k1(int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S,
-                     const JobSink& J, int nsm, cudaStream_t st) {
+void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs,
+                     const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
+                     const SolSink& S, const JobSink& J, int nsm, cudaStream_t st) {
   if (npairs == 0) return;
   const int threads = 128;
   const uint64_t cap = (uint64_t)nsm * 16;
   const uint64_t want1 = (npairs + threads - 1) / threads;
   const int g1 = (int)(want1 < cap ? want1 : cap);
-  if (refract) {
-    k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-    k1_phase2<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
-                                                   J.meta, J.r);
+  if (phase == 1) {
+    if (refract)
+      k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
+    else
+      k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
   } else {
-    k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-    k1_phase2<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
-                                                    J.meta, J.r);
+    if (refract)
+      k1_phase2<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
+                                                     J.meta, J.r);
+    else
+      k1_phase2<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
+                                                      J.meta, J.r);
   }
 }
 
