@@ -286,7 +286,7 @@ def main():
                    "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": "R",
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
-        "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": solve_s * 1e3,
+        "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "flop_per_launch": dom[1],
