@@ -294,8 +294,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   if (!ctx || !chain || !out) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
   const int k = (int)strlen(chain);
   if (bounces != k || k < 1) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bounces != strlen(chain)");
-  if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0)
+  if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0 && strcmp(chain, "RR") != 0 && strcmp(chain, "TT") != 0)
     return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
+  if (k == 2 && !tuples && ctx->cfg.cull)
+    return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN,
+                "two-bounce cull pre-pass not in this build: pass a tuple list or set cfg.cull = 0");
   if (!ctx->has_mesh || mesh_id != 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no such mesh");
   if (nq && !endpoints) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null endpoints");
   CK(cudaSetDevice(ctx->device));
@@ -343,10 +346,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_expand_bits(ctx->d_bits.p, words, nq, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else {
-    npairs = (uint64_t)nq * ctx->M.ntris;
+    npairs = k == 1 ? (uint64_t)nq * ctx->M.ntris : (uint64_t)nq * ctx->M.ntris * (ctx->M.ntris - 1);
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
-    launch_all_pairs_k1(nq, ctx->M.ntris, ctx->d_pq.p, ctx->d_pt.p, st);
+    if (k == 1)
+      launch_all_pairs_k1(nq, ctx->M.ntris, ctx->d_pq.p, ctx->d_pt.p, st);
+    else
+      launch_all_pairs_k2(nq, ctx->M.ntris, ctx->d_pq.p, ctx->d_pt.p, st);
     ctx->launches++;
   }
   ctx->npairs = npairs;
@@ -370,9 +376,9 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
                                std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
   if (s != SPOLY_OK) return s;
   CK(ctx->d_count.ensure(4));
-  CK(ctx->d_jpair.ensure(npairs));
-  CK(ctx->d_jmeta.ensure(npairs));
-  CK(ctx->d_jr.ensure(npairs * kJobStride));
+  CK(ctx->d_jpair.ensure(k == 1 ? npairs : 1));
+  CK(ctx->d_jmeta.ensure(k == 1 ? npairs : 1));
+  CK(ctx->d_jr.ensure(k == 1 ? npairs * kJobStride : kJobStride));
   unsigned long long cnt[4] = {0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     CK(cudaMemsetAsync(ctx->d_count.p, 0, 4 * sizeof(unsigned long long), st));
@@ -385,12 +391,19 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
     CK(cudaEventRecord(ctx->ev[4], st));
-    launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
-                    ctx->nsm, st);
-    CK(cudaEventRecord(ctx->ev[5], st));
-    launch_solve_k1(2, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
-                    ctx->nsm, st);
-    ctx->launches += 2;
+    if (k == 1) {
+      launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
+                      ctx->nsm, st);
+      CK(cudaEventRecord(ctx->ev[5], st));
+      launch_solve_k1(2, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
+                      ctx->nsm, st);
+      ctx->launches += 2;
+    } else {
+      CK(cudaEventRecord(ctx->ev[5], st));
+      launch_solve_k2(chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, ctx->nsm,
+                      st);
+      ctx->launches += 1;
+    }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(cnt, ctx->d_count.p, sizeof(cnt), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

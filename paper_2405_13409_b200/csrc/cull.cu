@@ -213,6 +213,24 @@ void launch_all_pairs_k1(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint
   k_all_pairs<<<1024, 256, 0, st>>>(nq, ntris, pair_query, pair_tpos);
 }
 
+// no cull, k = 2: every ordered pair of distinct triangles per query (tiny meshes / tests)
+__global__ void k_all_pairs2(uint32_t nq, uint32_t ntris, uint32_t* pq, uint32_t* pt) {
+  const uint64_t per = (uint64_t)ntris * (ntris - 1);
+  const uint64_t n = (uint64_t)nq * per;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t q = i / per, r = i % per;
+    const uint32_t a = (uint32_t)(r / (ntris - 1));
+    uint32_t b = (uint32_t)(r % (ntris - 1));
+    if (b >= a) ++b;
+    pq[i] = (uint32_t)q;
+    pt[2 * i] = a;
+    pt[2 * i + 1] = b;
+  }
+}
+void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st) {
+  if (ntris >= 2) k_all_pairs2<<<1024, 256, 0, st>>>(nq, ntris, pair_query, pair_tpos);
+}
+
 // explicit CSR tuple list (original ids) -> work list (Morton positions); one warp per query
 __global__ void k_expand_list(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ids, uint32_t nq, int k,
                               const uint32_t* __restrict__ perm_of, uint32_t* pq, uint32_t* pt) {

@@ -183,3 +183,47 @@ def test_c3_pool_subset_parity(orc, sp, torch_cuda):
     st = parity.compare(ro, g, sub.nqueries)
     assert st["compared_solutions"] >= 20, st
     assert np.all(g["residual"] < 1e-6)
+
+
+# ---------------------------------------------------------------- two bounces (RR, TT; 100-piece scan)
+def _planted_batch(chain, n, seed, size=0.15):
+    from planted import planted_many
+    cases = planted_many(seed, chain, n, size=size)
+    pos, nrm, tri, eps = [], [], [], []
+    for i, (m, ids, x0, xk1, bary) in enumerate(cases):
+        pos.append(m.pos)
+        nrm.append(m.nrm)
+        tri.append(m.tri + 6 * i)
+        eps.append([x0, xk1])
+    mesh = W.Mesh(np.concatenate(pos), np.concatenate(nrm), np.concatenate(tri).astype(np.uint32),
+                  cases[0][0].eta_front, cases[0][0].eta_back)
+    ep = np.array(eps, float)
+    rng = np.random.default_rng(seed + 1)
+    offsets = [0]
+    ids = []
+    for i in range(len(cases)):
+        tl = [(2 * i, 2 * i + 1)]
+        for _ in range(2):  # decoy pairs from other configurations
+            j, l = rng.integers(0, len(cases), 2)
+            tl.append((2 * int(j), 2 * int(l) + 1))
+        for a, b in tl:
+            ids += [a, b]
+        offsets.append(offsets[-1] + len(tl))
+    return mesh, ep, np.array(offsets, np.uint32), np.array(ids, np.uint32), [c[4] for c in cases]
+
+
+@pytest.mark.parametrize("chain", ["RR", "TT"])
+def test_two_bounce_planted_parity(orc, sp, torch_cuda, chain):
+    mesh, ep, off, ids, truth = _planted_batch(chain, 16 if chain == "RR" else 8, 61)
+    ro = orc.solve(mesh, chain, ep, offsets=off, tri_ids=ids)
+    g = _gpu_solve(sp, torch_cuda, mesh, chain, ep, offsets=off, tri_ids=ids)
+    st = parity.compare(ro, g, len(ep), tol_bary=1e-4)
+    assert st["compared_solutions"] >= len(ep) // 2, st
+    assert np.all(g["residual"] < 1e-6)
+    # the planted chain is recovered on the GPU for most queries (100-piece scan misses are by design)
+    hit = 0
+    for qi, b in enumerate(truth):
+        sel = g["query"] == qi
+        if any(np.max(np.abs(x - b)) < 1e-6 for x in g["bary"][sel]):
+            hit += 1
+    assert hit >= int(0.85 * len(truth)), (hit, len(truth))
