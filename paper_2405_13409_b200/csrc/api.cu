@@ -294,7 +294,8 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   if (!ctx || !chain || !out) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
   const int k = (int)strlen(chain);
   if (bounces != k || k < 1) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bounces != strlen(chain)");
-  if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0 && strcmp(chain, "RR") != 0 && strcmp(chain, "TT") != 0)
+  if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0 && strcmp(chain, "RR") != 0 && strcmp(chain, "TT") != 0 &&
+      strcmp(chain, "RT") != 0 && strcmp(chain, "TR") != 0)
     return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
   if (k == 2 && !tuples && ctx->cfg.cull)
     return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN,
@@ -400,7 +401,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       ctx->launches += 2;
     } else {
       CK(cudaEventRecord(ctx->ev[5], st));
-      launch_solve_k2(chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, ctx->nsm,
+      launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, ctx->nsm,
                       st);
       ctx->launches += 1;
     }

@@ -26,7 +26,7 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
                      const SolSink& S, const JobSink& J, int nsm, cudaStream_t st);
 
 // solve_k2.cu
-void launch_solve_k2(int tt, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
+void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
                      const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, int nsm,
                      cudaStream_t st);
 void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);

