@@ -972,6 +972,25 @@ static bool cull_keep(const std::string& chain, const vector<Tri>& tris, V3 x0, 
     return vertex_keep(cp, cn, e0, e1, ncone(T), margin);
   }
   const Tri &A = tris[0], &B = tris[1];
+  // side filter (reading R10 / R14): a valid chain has x_2 on x_0's side of T_1's plane for a reflection at
+  // x_1 (the opposite side for a refraction), and x_1 on x_3's side of T_2's plane for a reflection at x_2
+  // (opposite for a refraction).  Keep the pair when some vertex of the other triangle is strictly on the
+  // required side by more than 1e-6 of the triangle scale (grazing chains are not admissible).
+  {
+    auto side_keep = [](const Tri& P, V3 xref, bool refract, const Tri& Oth) {
+      V3 g = P.g();
+      double gl = norm(g), sc = std::max(norm(P.e1()), norm(P.e2()));
+      double sref = dot(xref - P.p[0], g);
+      double want = refract ? -1.0 : 1.0;
+      if (sref == 0) return true;
+      double sg = sref > 0 ? want : -want;
+      for (int j = 0; j < 3; ++j)
+        if (sg * dot(Oth.p[j] - P.p[0], g) > 1e-6 * gl * sc) return true;
+      return false;
+    };
+    if (!side_keep(A, x0, chain[0] == 'T', B)) return false;
+    if (!side_keep(B, xk1, chain[1] == 'T', A)) return false;
+  }
   vector<V3> ab, ba;
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) {

@@ -56,6 +56,7 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_offsets;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig;
   uint64_t npairs = 0;
+  int last_k = 1;
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
@@ -297,9 +298,6 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   if (strcmp(chain, "R") != 0 && strcmp(chain, "T") != 0 && strcmp(chain, "RR") != 0 && strcmp(chain, "TT") != 0 &&
       strcmp(chain, "RT") != 0 && strcmp(chain, "TR") != 0)
     return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "chain not supported by this build");
-  if (k == 2 && !tuples && ctx->cfg.cull)
-    return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN,
-                "two-bounce cull pre-pass not in this build: pass a tuple list or set cfg.cull = 0");
   if (!ctx->has_mesh || mesh_id != 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no such mesh");
   if (nq && !endpoints) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null endpoints");
   CK(cudaSetDevice(ctx->device));
@@ -323,6 +321,27 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
     launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    ctx->launches++;
+  } else if (ctx->cfg.cull && k == 2) {
+    CK(ctx->d_counts.ensure(nq));
+    CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+    launch_cull_pairs(0, endpoints, nq, ctx->M, chain[0] == 'T', chain[1] == 'T', c32, nullptr, nullptr, nullptr,
+                      ctx->nsm, st);
+    ctx->launches++;
+    size_t tbytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
+    CK(ctx->d_temp.ensure(tbytes));
+    CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
+    CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nq, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    npairs = tot;
+    CK(ctx->d_pq.ensure(npairs));
+    CK(ctx->d_pt.ensure(npairs * k));
+    launch_cull_pairs(1, endpoints, nq, ctx->M, chain[0] == 'T', chain[1] == 'T', nullptr, ctx->d_offsets.p,
+                      ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else if (ctx->cfg.cull) {
     const uint32_t words = 2 * ctx->M.nclusters;
@@ -357,6 +376,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     ctx->launches++;
   }
   ctx->npairs = npairs;
+  ctx->last_k = k;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[1], st));
 
@@ -568,8 +588,8 @@ spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chai
 spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pq, const uint32_t** pt, uint64_t* n) {
   if (!ctx || !pq || !pt || !n) return SPOLY_ERR_INVALID_ARG;
   spoly_ctx* c = const_cast<spoly_ctx*>(ctx);
-  if (c->d_pt_orig.ensure(std::max<uint64_t>(c->npairs, 1)) != cudaSuccess) return SPOLY_ERR_OOM;
-  launch_map_ids(c->d_pt.p, c->npairs, c->M.orig_id, c->d_pt_orig.p, c->st);
+  if (c->d_pt_orig.ensure(std::max<uint64_t>(c->npairs * c->last_k, 1)) != cudaSuccess) return SPOLY_ERR_OOM;
+  launch_map_ids(c->d_pt.p, c->npairs * c->last_k, c->M.orig_id, c->d_pt_orig.p, c->st);
   if (cudaStreamSynchronize(c->st) != cudaSuccess) return SPOLY_ERR_CUDA;
   *pq = c->d_pq.p;
   *pt = c->d_pt_orig.p;

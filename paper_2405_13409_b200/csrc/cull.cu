@@ -251,3 +251,165 @@ void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32
 }
 
 }  // namespace spoly
+
+namespace spoly {
+
+// ------------------------------------------------------------------ two-bounce pair cull
+// Node pair (A, B): the directions from any point of A to any point of B lie in the cone with axis
+// (cB - cA)^ and sin(theta) = (rhoA + rhoB) / |cB - cA| (Minkowski difference of the two spheres).
+// Vertex 1 at A: h1 = eta0 w(x1->x0) + eta1 w(x1->x2) parallel to +-n(A); vertex 2 at B:
+// h2 = eta1 w(x2->x1) + eta2 w(x2->x3) parallel to +-n(B).  The pair is kept if both hold for one of the
+// IOR assignments consistent with the chain (reading R9 enumerated: RR (1,1,1); RT (f,f,b),(b,b,f);
+// TR (f,b,b),(b,f,f); TT (f,b,f),(b,f,b)).
+__device__ __forceinline__ bool pair_dir(float4 sa, float4 sb, f3& a, float& chord) {
+  f3 d = {sb.x - sa.x, sb.y - sa.y, sb.z - sa.z};
+  const float l2 = dotf(d, d);
+  const float inv = rsqrtf(l2);
+  const float sn = (sa.w + sb.w) * inv;
+  const float s2 = sn * sn;
+  a = inv * d;
+  chord = sn * (1.f + s2);
+  return s2 <= 0.25f && l2 > 0.f;
+}
+
+__device__ __forceinline__ bool pair_keep(f3 x0, f3 x3, float4 sA, float4 nA, float4 sB, float4 nB, int v1t, int v2t,
+                                          float ef, float eb) {
+  f3 a0, a3, aAB;
+  float c0, c3, cAB;
+  if (!sphere_dir(x0, sA, a0, c0) || !sphere_dir(x3, sB, a3, c3) || !pair_dir(sA, sB, aAB, cAB)) return true;
+  const f3 aBA = {-aAB.x, -aAB.y, -aAB.z};
+  float e[2][3];
+  int ncombo = 0;
+  if (!v1t && !v2t) {
+    e[0][0] = e[0][1] = e[0][2] = 1.f;
+    ncombo = 1;
+  } else {
+    // combo 0 starts in the front medium, combo 1 in the back medium
+    for (int c = 0; c < 2; ++c) {
+      const float s = c == 0 ? ef : eb, o = c == 0 ? eb : ef;
+      e[c][0] = s;
+      e[c][1] = v1t ? o : s;
+      e[c][2] = v2t ? (e[c][1] == s ? o : s) : e[c][1];
+    }
+    ncombo = 2;
+  }
+  for (int c = 0; c < ncombo; ++c)
+    if (node_keep(a0, c0, aAB, cAB, e[c][0], e[c][1], nA) && node_keep(aBA, cAB, a3, c3, e[c][1], e[c][2], nB))
+      return true;
+  return false;
+}
+
+// side filter (readings R10, R14): the other triangle needs a vertex strictly on the required side of
+// this triangle's plane (x_0's / x_3's side for a reflection, the opposite side for a refraction), by more
+// than 1e-6 of the triangle scale; FP32 with the tolerance halved is at most more permissive.
+__device__ __forceinline__ bool side_keep(const TriRec* __restrict__ tris, uint32_t tp, f3 xref, int refract,
+                                          uint32_t to) {
+  const float4* r = tris[tp].r;
+  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+  const f3 p0 = {a.x, a.y, a.z}, p1 = {a.w, b.x, b.y}, p2 = {b.z, b.w, c.x};
+  const f3 e1 = p1 - p0, e2 = p2 - p0;
+  const f3 g = crossf(e1, e2);
+  const float gl = sqrtf(dotf(g, g)), sc = sqrtf(fmaxf(dotf(e1, e1), dotf(e2, e2)));
+  const float sref = dotf(xref - p0, g);
+  if (sref == 0.f) return true;
+  const float sg = (sref > 0.f) == (refract == 0) ? 1.f : -1.f;
+  const float4* o = tris[to].r;
+  const float4 oa = __ldg(o), ob = __ldg(o + 1), oc = __ldg(o + 2);
+  const f3 q0 = {oa.x, oa.y, oa.z}, q1 = {oa.w, ob.x, ob.y}, q2 = {ob.z, ob.w, oc.x};
+  const float tol = 0.5e-6f * gl * sc;
+  return sg * dotf(q0 - p0, g) > tol || sg * dotf(q1 - p0, g) > tol || sg * dotf(q2 - p0, g) > tol;
+}
+
+// one warp per query; pass 0 counts, pass 1 writes (same traversal order -> deterministic list)
+__global__ void __launch_bounds__(256) k_cull_pairs(int pass, const double* __restrict__ ep, uint32_t nq,
+                                                    const TriRec* __restrict__ tris,
+                                                    const ClusterRec* __restrict__ l1,
+                                                    const ClusterRec* __restrict__ l2,
+                                                    const TriCull* __restrict__ tc, uint32_t ntris, uint32_t nl1,
+                                                    int v1t, int v2t, float ef, float eb, uint32_t* counts,
+                                                    const unsigned long long* __restrict__ offsets,
+                                                    uint32_t* __restrict__ pq, uint32_t* __restrict__ pt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t nl2 = (ntris + 7) >> 3;
+  const uint64_t npair1 = (uint64_t)nl1 * nl1;
+  for (uint32_t q = gw; q < nq; q += nw) {
+    const double* e = ep + 6ull * q;
+    const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
+    const f3 x3 = {(float)e[3], (float)e[4], (float)e[5]};
+    uint32_t count = 0;
+    unsigned long long wpos = pass ? offsets[q] : 0ull;
+    for (uint64_t b1 = 0; b1 < npair1; b1 += 32) {
+      const uint64_t p1 = b1 + lane;
+      bool k1 = false;
+      if (p1 < npair1) {
+        const ClusterRec A = l1[p1 / nl1], B = l1[p1 % nl1];
+        k1 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb);
+      }
+      uint32_t m1 = __ballot_sync(0xffffffffu, k1);
+      while (m1) {
+        const uint64_t cp = b1 + __ffs(m1) - 1;
+        m1 &= m1 - 1;
+        const uint32_t ca = (uint32_t)(cp / nl1), cb = (uint32_t)(cp % nl1);
+        // 64 sub-cluster pairs: 2 per lane
+        uint32_t m2[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int sp = h * 32 + lane;
+          const uint32_t sa = ca * 8 + (sp >> 3), sb = cb * 8 + (sp & 7);
+          bool k2 = false;
+          if (sa < nl2 && sb < nl2) {
+            const ClusterRec A = l2[sa], B = l2[sb];
+            k2 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb);
+          }
+          m2[h] = __ballot_sync(0xffffffffu, k2);
+        }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          while (m2[h]) {
+            const int sp = h * 32 + __ffs(m2[h]) - 1;
+            m2[h] &= m2[h] - 1;
+            const uint32_t sa = ca * 8 + (sp >> 3), sb = cb * 8 + (sp & 7);
+            // 64 triangle pairs: 2 per lane, fixed order
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const int tp = g * 32 + lane;
+              const uint32_t ta = sa * 8 + (tp >> 3), tb = sb * 8 + (tp & 7);
+              bool k3 = false;
+              if (ta < ntris && tb < ntris && ta != tb) {
+                const TriCull A = tc[ta], B = tc[tb];
+                k3 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb) &&
+                     side_keep(tris, ta, x0, v1t, tb) && side_keep(tris, tb, x3, v2t, ta);
+              }
+              const unsigned m3 = __ballot_sync(0xffffffffu, k3);
+              if (pass && k3) {
+                const unsigned long long pos = wpos + __popc(m3 & ((1u << lane) - 1u));
+                pq[pos] = q;
+                pt[2 * pos] = ta;
+                pt[2 * pos + 1] = tb;
+              }
+              wpos += __popc(m3);
+              count += __popc(m3);
+            }
+          }
+        }
+      }
+    }
+    if (!pass && lane == 0) counts[q] = count;
+  }
+}
+
+void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, int v1t, int v2t,
+                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
+                       cudaStream_t st) {
+  if (!nq) return;
+  const int threads = 256;
+  uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
+  uint64_t cap = (uint64_t)nsm * 8;
+  int blocks = (int)(want < cap ? want : cap);
+  k_cull_pairs<<<blocks, threads, 0, st>>>(pass, ep, nq, M.tris, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters, v1t, v2t,
+                                           M.eta_front, M.eta_back, counts, offsets, pq, pt);
+}
+
+}  // namespace spoly

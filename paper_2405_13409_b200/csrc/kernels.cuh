@@ -29,6 +29,9 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
 void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
                      const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, int nsm,
                      cudaStream_t st);
+void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, int v1t, int v2t,
+                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
+                       cudaStream_t st);
 void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 
 // reduce.cu

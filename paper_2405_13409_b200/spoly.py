@@ -217,6 +217,7 @@ class Context:
                                  intensity.data_ptr() if intensity is not None else None,
                                  ctypes.byref(tl) if tl is not None else None, ctypes.byref(r))
         self._check(rc, "spoly_solve")
+        self.k = len(chain)
         return self._wrap(r, nq)
 
     def solve_host(self, chain: str, endpoints: np.ndarray, intensity: np.ndarray = None, mesh_id: int = 0):
@@ -239,7 +240,8 @@ class Context:
         rc = self._L.spoly_last_worklist(self._h, ctypes.byref(pq), ctypes.byref(pt), ctypes.byref(n))
         self._check(rc, "spoly_last_worklist")
         dev = f"cuda:{self.device}"
-        return _view(pq.value, (n.value,), "<u4", dev), _view(pt.value, (n.value,), "<u4", dev)
+        k = self.k or 1
+        return _view(pq.value, (n.value,), "<u4", dev), _view(pt.value, (n.value, k), "<u4", dev)
 
     def bench_fma(self, fp64: bool = True, seconds: float = 1.0) -> float:
         f = ctypes.c_double()

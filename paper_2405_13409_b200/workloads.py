@@ -267,6 +267,40 @@ def shell_c5(res: int = 1024, level: int = 3) -> Workload:
     return Workload("shell", "TT", mesh, ep, np.ones(Q), {"config": "C5", "res": res})
 
 
+def mirrors_rr(res: int = 64, quads: int = 128, seed: int = 5) -> Workload:
+    """C5 RR variant: two facing bumpy mirror panels 1 m apart (x = -0.5 facing +x,
+    x = +0.5 facing -x; y, z in [-0.5, 0.5]; quads x quads each), point light between them at
+    (0, 0.2, 0), receivers on the wall y = -1.5 over x, z in [-1, 1]."""
+    rng = np.random.default_rng(seed)
+    k, phi = _waves(rng, 16, 0.05, 0.5)
+    A = 0.2 / np.linalg.norm(k, axis=1) / 4.0
+    _, grad = _wave_fields(A, k, phi)
+    base = grid_mesh(quads + 1, quads + 1, -0.5, 0.5, -0.5, 0.5, lambda X, Y: np.zeros_like(X), grad)
+    # panel A: (x, y) grid -> world (x=-0.5, y=X, z=Y), normal (nz, nx, ny) facing +x
+    def place(m, sign):
+        P = m.pos.astype(np.float64)
+        N = m.nrm.astype(np.float64)
+        pos = np.stack([np.full(len(P), -0.5 * sign), P[:, 0], P[:, 1]], 1)
+        nrm = np.stack([sign * N[:, 2], N[:, 0], N[:, 1]], 1)
+        tri = m.tri.copy()
+        # winding: geometric normal must face the other panel (+x for A, -x for B)
+        p = pos[tri]
+        g = np.cross(p[:, 1] - p[:, 0], p[:, 2] - p[:, 0])
+        flip = g[:, 0] * sign < 0
+        tri[flip] = tri[flip][:, [0, 2, 1]]
+        return Mesh(pos.astype(np.float32), nrm.astype(np.float32), tri.astype(np.uint32))
+    mesh = merge(place(base, 1.0), place(base, -1.0))
+    xs = -1.0 + (np.arange(res) + 0.5) * (2.0 / res)
+    X, Z = np.meshgrid(xs, xs, indexing="xy")
+    Q = res * res
+    ep = np.zeros((Q, 2, 3))
+    ep[:, 0, 0] = X.ravel()
+    ep[:, 0, 1] = -1.5
+    ep[:, 0, 2] = Z.ravel()
+    ep[:, 1] = (0.0, 0.2, 0.0)
+    return Workload("mirrors", "RR", mesh, ep, np.ones(Q), {"config": "C5-RR", "res": res})
+
+
 def random_triangles(rng, n: int, size: float, center=(0.0, 0.0, 0.0), spread: float = 1.0,
                      normal_tilt: float = 0.2, face: bool = False) -> Mesh:
     """Independent random triangles (for parity fuzzing): roughly facing +z, random vertex-normal tilt."""
@@ -296,4 +330,5 @@ CONFIGS = {
     "C3": pool_c3,
     "C4": sphere_c4,
     "C5": shell_c5,
+    "C5RR": mirrors_rr,
 }

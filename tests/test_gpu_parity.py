@@ -37,7 +37,7 @@ def _gpu_solve(sp, torch, mesh, chain, ep, cfg=None, offsets=None, tri_ids=None,
     out = r.to_numpy()
     out["report"] = r.report
     wl = ctx.last_worklist()
-    out["worklist"] = (wl[0].cpu().numpy().view(np.uint32), wl[1].cpu().numpy().view(np.uint32))
+    out["worklist"] = (wl[0].cpu().numpy().view(np.uint32), wl[1].cpu().numpy().view(np.uint32).reshape(-1, len(chain)))
     ctx.close()
     return out
 
@@ -227,3 +227,35 @@ def test_two_bounce_planted_parity(orc, sp, torch_cuda, chain):
         if any(np.max(np.abs(x - b)) < 1e-6 for x in g["bary"][sel]):
             hit += 1
     assert hit >= int(0.85 * len(truth)), (hit, len(truth))
+
+
+@pytest.mark.parametrize("chain", ["RR", "TT"])
+def test_two_bounce_cull_sound_on_planted(orc, sp, torch_cuda, chain):
+    """GPU pair cull (no tuple list) keeps every planted pair and the solve recovers the planted chains."""
+    mesh, ep, off, ids, truth = _planted_batch(chain, 12, 71)
+    g = _gpu_solve(sp, torch_cuda, mesh, chain, ep)
+    pq, pt = g["worklist"]
+    for qi in range(len(ep)):
+        assert np.any((pq == qi) & (pt[:, 0] == 2 * qi) & (pt[:, 1] == 2 * qi + 1)), qi
+    ro = orc.solve(mesh, chain, ep)  # the oracle's own cull
+    parity.compare(ro, g, len(ep), tol_bary=1e-4)
+
+
+def test_rr_mirrors_parity(orc, sp, torch_cuda):
+    """C5 RR variant (two facing bumpy mirrors): GPU pair cull + solve vs the oracle's cull + solve."""
+    w = W.mirrors_rr(res=8, quads=16)
+    sub = w.subset(np.arange(0, 64, 8))
+    ro = orc.solve(sub.mesh, "RR", sub.endpoints)
+    g = _gpu_solve(sp, torch_cuda, sub.mesh, "RR", sub.endpoints)
+    st = parity.compare(ro, g, sub.nqueries, tol_bary=1e-4)
+    assert st["compared_solutions"] >= 10, st
+    assert g["report"]["n_pairs_in"] >= ro.report["pairs_in"]
+
+
+def test_tt_sphere_parity(orc, sp, torch_cuda):
+    """C4-shaped dielectric icosphere (level 2, 320 tris), TT through it: GPU cull + solve vs the oracle."""
+    w = W.sphere_c4(res=4, level=2)
+    sub = w.subset([5, 6])
+    ro = orc.solve(sub.mesh, "TT", sub.endpoints)
+    g = _gpu_solve(sp, torch_cuda, sub.mesh, "TT", sub.endpoints)
+    parity.compare(ro, g, sub.nqueries, tol_bary=1e-4)
