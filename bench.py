@@ -45,11 +45,33 @@ FLOP_PER_CANDIDATE_R = 430
 FLOP_PER_ADMISSIBLE_R = 250
 
 
+# one-bounce refraction (T), same accounting: phase 1 per pair: decision 60 + setup 18 + a 75 + b (square
+# form, Eq. 9) 656 + normalise/truncate 55 + resultant by pseudo-remainder 998 + Bernstein (degree 12) 260
+# = 2122; rebuild 864; candidate 755 (b has 28 coefficients); admissible 300 (refraction Jacobian).
+FLOP_PHASE1_PER_PAIR_T = 2122
+FLOP_PER_REBUILD_T = 864
+FLOP_PER_CANDIDATE_T = 755
+FLOP_PER_ADMISSIBLE_T = 300
+
+
 def flop_model_R(rep):
     p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_R
     p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_R +
           rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
     return p1, p2
+
+
+def flop_model(chain, rep):
+    """(phase-1 FLOPs, phase-2 FLOPs) per solve; for two bounces phase 1 is empty and phase 2 is the
+    single two-bounce kernel, whose algorithmic kFLOP the kernel counts itself (alg_kflop)."""
+    if chain == "R":
+        return flop_model_R(rep)
+    if chain == "T":
+        p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_T
+        p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_T +
+              rep["n_candidates"] * FLOP_PER_CANDIDATE_T + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_T)
+        return p1, p2
+    return 0.0, rep["alg_kflop"] * 1e3
 
 
 # FP64 ALU peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz;
@@ -155,7 +177,9 @@ def main():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--res", type=int, default=256, help="C2 light-sample grid (256 -> 65,536 queries)")
+    ap.add_argument("--res", type=int, default=None, help="query grid side (default: the config's own)")
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5", "C5RR"],
+                    help="workload (BASELINE.json configs; C2 is the driver's bench line)")
     ap.add_argument("--cpu-sample", type=int, default=256)
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -181,7 +205,12 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
-    w = W.glints_c2(res=args.res, seed_strata=2 + rank)  # weak scaling: one full frame per rank
+    if args.config == "C2":
+        w = W.glints_c2(res=args.res or 256, seed_strata=2 + rank)  # weak scaling: one full frame per rank
+    else:
+        kw = {} if args.res is None else {"res": args.res}
+        w = W.CONFIGS[args.config](**kw)
+    chain = w.chain
     stream = torch.cuda.current_stream(dev)
     ctx = spoly.Context(local, stream=stream)
     ctx.upload_mesh(w.mesh)
@@ -195,7 +224,7 @@ def main():
         torch.cuda.synchronize(dev)
 
     for _ in range(max(args.warmup, 3)):
-        r = ctx.solve("R", ep, inten)
+        r = ctx.solve(chain, ep, inten)
     barrier()
 
     step_ms, solve_ms, reports = [], [], []
@@ -206,7 +235,7 @@ def main():
             e0 = torch.cuda.Event(enable_timing=True)
             e1 = torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-            r = ctx.solve("R", ep, inten)
+            r = ctx.solve(chain, ep, inten)
             e1.record(stream)
             torch.cuda.synchronize(dev)
             step_ms.append(e0.elapsed_time(e1))
@@ -223,13 +252,13 @@ def main():
     if not args.no_e2e:
         ep_h = np.ascontiguousarray(w.endpoints)
         it_h = np.ascontiguousarray(w.intensity)
-        pq, _ = ctx.solve_host("R", ep_h, it_h)
+        pq, _ = ctx.solve_host(chain, ep_h, it_h)
         e2e_t, e2e_paths = 0.0, 0
         for s in range(args.steps):
             flush.fill_(s & 0xFF)
             barrier()
             t0 = time.perf_counter()
-            pq, rr = ctx.solve_host("R", ep_h, it_h)
+            pq, rr = ctx.solve_host(chain, ep_h, it_h)
             torch.cuda.synchronize(dev)
             e2e_t += time.perf_counter() - t0
             e2e_paths += rr.n_solutions
@@ -251,11 +280,12 @@ def main():
     # ---- roofline of the dominant kernel, from its own launch's CUDA-event time (recorded by the library on
     # the launching stream around each solve kernel, averaged over the timed steps)
     rep = reports[-1]
-    f1, f2 = flop_model_R(rep)
+    f1, f2 = flop_model(chain, rep)
     t1 = statistics.mean(x["ms_phase1"] for x in reports) / 1e3
     t2 = statistics.mean(x["ms_phase2"] for x in reports) / 1e3
     peak = fp64_peak()
-    dom = ("k1_phase2<R>", f2, t2) if t2 >= t1 else ("k1_phase1<R>", f1, t1)
+    k1n, k2n = (f"k1_phase1<{chain}>", f"k1_phase2<{chain}>") if len(chain) == 1 else ("-", f"k2_solve<{chain}>")
+    dom = (k2n, f2, t2) if t2 >= t1 else (k1n, f1, t1)
     achieved = dom[1] / dom[2]
     traffic = None
     tp = os.path.join(ROOT, "profiles", "solve_traffic.json")
@@ -273,7 +303,7 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(w, args.cpu_sample)
+        cpu = oracle_baseline(w, min(args.cpu_sample, w.nqueries) if len(chain) == 1 else min(4, w.nqueries))
         cpu.pop("seconds", None)
 
     line = {
@@ -281,9 +311,11 @@ def main():
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "query_tuple_solves_per_s": n_pairs / (total_ms / 1e3),
-        "config": {"workload": "C2 glints: %d light samples x %d-tri normal-mapped bumpy plane, one-bounce R, "
-                               "cull pre-pass + fused FP64 solve + deterministic compaction" % (w.nqueries, w.mesh.ntris),
-                   "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": "R",
+        "config": {"workload": ("C2 glints: %d light samples x %d-tri normal-mapped bumpy plane, one-bounce R, "
+                                "cull pre-pass + fused FP64 solve + deterministic compaction" % (w.nqueries, w.mesh.ntris))
+                   if args.config == "C2" else "%s %s: %d queries x %d tris, chain %s, cull + solve + compaction" % (
+                       args.config, w.name, w.nqueries, w.mesh.ntris, chain),
+                   "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": chain,
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
@@ -292,8 +324,9 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "flop_per_launch": dom[1],
                      "peak_note": "FP64: 148 SMs x 64 FMA/clk x 2 x 1965 MHz (unit counts x clocks.max.sm)",
                      "measured_fp64_fma_tflops": measured_fp64 / 1e12 if measured_fp64 else None,
-                     "phases": {"k1_phase1<R>": {"ms": t1 * 1e3, "tflops": f1 / t1 / 1e12, "frac": f1 / t1 / peak},
-                                "k1_phase2<R>": {"ms": t2 * 1e3, "tflops": f2 / t2 / 1e12, "frac": f2 / t2 / peak},
+                     "phases": {k1n: {"ms": t1 * 1e3, "tflops": f1 / t1 / 1e12 if t1 > 0 else None,
+                                      "frac": f1 / t1 / peak if t1 > 0 else None},
+                                k2n: {"ms": t2 * 1e3, "tflops": f2 / t2 / 1e12, "frac": f2 / t2 / peak},
                                 "solve_total": {"ms": (t1 + t2) * 1e3, "frac": (f1 + f2) / (t1 + t2) / peak}}},
         "clocks": clocks,
         "gpu_launches": launches,

@@ -109,6 +109,8 @@ typedef struct {
   float ms_phase1, ms_phase2;         /* CUDA-event times of the two solve kernels (phase 2 incl.
                                          the count read-back)                                    */
   uint64_t n_rebuilds;                /* phase-2 coefficient-phase recomputations (FLOP model)   */
+  uint64_t alg_kflop;                 /* two-bounce kernel: algorithmic kFLOP (coefficient phase +
+                                         determinant evaluations)                   */
 } spoly_report;
 
 typedef struct {

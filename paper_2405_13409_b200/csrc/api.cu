@@ -548,6 +548,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     cudaEventElapsedTime(&R.ms_phase2, ctx->ev[5], ctx->ev[2]);
   }
   R.n_rebuilds = counters[C_REBUILDS];
+  R.alg_kflop = counters[C_KFLOP];
   R.n_launches = ctx->launches;
   R.n_eval_terms = counters[C_EVAL_TERMS];
   return SPOLY_OK;

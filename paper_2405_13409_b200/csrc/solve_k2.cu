@@ -621,6 +621,16 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
       C.eta[2] = Sys.eta2;
       if (ok) {
         cnt[C_SYSTEMS]++;
+        // algorithmic FLOPs (kFLOP units): coefficient phase (dense products of the Eq. 13-23 chain,
+        // counted in DESIGN.md §5: RR 17k, RT 40k, TR 150k, TT 400k) + per determinant evaluation:
+        // slices 2 (sum of the a_i, b_i lengths, i <= n) + Chionh 3 n^2 + GE (2/3) n^3
+        const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
+        double slice_terms = 0;
+        for (int i = 0; i <= Sys.n; ++i)
+          slice_terms += (i <= Sys.da ? Sy::DA - i + 1 : 0) + (i <= Sys.db ? Sy::DB - i + 1 : 0);
+        const double nn = (double)Sys.n;
+        const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
+        double kflop_acc = build_f;
         // ---- 100-piece determinant-sign scan
         double M[MAXN * MAXN];
         const int P = prm.pieces;
@@ -631,10 +641,14 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
         int s_cur;
         double lg_cur;
         s_cur = det_sign_at<V1T, V2T>(Sys, 0.0, &lg_cur, M);
+        kflop_acc += eval_f;
         for (int j = 0; j <= P; ++j) {
           int s_next = 0;
           double lg_next = -INFINITY;
-          if (j < P) s_next = det_sign_at<V1T, V2T>(Sys, (double)(j + 1) / P, &lg_next, M);
+          if (j < P) {
+            s_next = det_sign_at<V1T, V2T>(Sys, (double)(j + 1) / P, &lg_next, M);
+            kflop_acc += eval_f;
+          }
           // near-tangent: |det(v_j)| < 1e-9 max(neighbours)
           const double nb = fmax(lg_prev, lg_next);
           if (lg_cur < log(1e-9) + nb) flags |= SPOLY_FLAG_NEAR_TANGENT;
@@ -648,6 +662,7 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
               const double m = 0.5 * (lo + hi);
               double l2;
               const int sm = det_sign_at<V1T, V2T>(Sys, m, &l2, M);
+              kflop_acc += eval_f;
               if (sm == 0) {
                 lo = hi = m;
                 break;
@@ -667,6 +682,7 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
         }
         (void)s_prev;
         (void)lg_prev2;
+        cnt[C_KFLOP] += (uint32_t)(kflop_acc * 1e-3);
         cnt[C_VROOTS] += nv;
         // ---- path phase
         constexpr int NA = Sy::DB + 1;
