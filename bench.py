@@ -318,6 +318,8 @@ def main():
                    "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": chain,
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
+        "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
+                                                 "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds")},
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,

@@ -111,6 +111,7 @@ typedef struct {
   uint64_t n_rebuilds;                /* phase-2 coefficient-phase recomputations (FLOP model)   */
   uint64_t alg_kflop;                 /* two-bounce kernel: algorithmic kFLOP (coefficient phase +
                                          determinant evaluations)                   */
+  uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce phase-2 jobs: monotone r / deeper recursion   */
 } spoly_report;
 
 typedef struct {

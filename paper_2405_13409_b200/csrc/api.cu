@@ -50,7 +50,9 @@ struct spoly_ctx {
   DBuf<TriCull> d_tcull;
   DBuf<uint32_t> d_orig, d_perm;
   DBuf<ClusterRec> d_cl, d_sub;
-  DBuf<uint32_t> d_bits;
+  DBuf<uint32_t> d_tlist, d_tcount, d_qkeys, d_qorder;
+  DBuf<float> d_qbounds;
+  uint32_t tile_cap = 4096, tile_used_cap = 4096;
   // work list
   DBuf<uint64_t> d_counts;
   DBuf<unsigned long long> d_offsets;
@@ -145,7 +147,8 @@ void spoly_destroy(spoly_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
   ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
-  ctx->d_sub.release(); ctx->d_bits.release();
+  ctx->d_sub.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
+  ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
@@ -344,13 +347,45 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
                       ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else if (ctx->cfg.cull) {
-    const uint32_t words = 2 * ctx->M.nclusters;
+    // query order (Morton of the endpoints), tile cull, per-query cull on the tile survivors
+    const uint32_t ntiles = (nq + 31) / 32;
+    CK(ctx->d_qbounds.ensure(12));
+    CK(ctx->d_qkeys.ensure(2ull * nq));
+    CK(ctx->d_qorder.ensure(2ull * nq));
+    launch_query_order(endpoints, nq, ctx->d_qbounds.p, ctx->d_qkeys.p, ctx->d_qorder.p, st);
+    ctx->launches += 2;
+    {
+      size_t tb = 0;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
+                                         ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
+      CK(ctx->d_temp.ensure(tb));
+      CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
+                                         ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
+    }
+    const uint32_t* order = ctx->d_qorder.p + nq;
+    CK(ctx->d_tcount.ensure(ntiles + 1));
+    for (int attempt = 0; attempt < 2; ++attempt) {
+      const uint32_t cap = std::max<uint32_t>(64, std::min<uint32_t>(ctx->tile_cap, ctx->M.ntris));
+      CK(ctx->d_tlist.ensure((uint64_t)ntiles * cap));
+      CK(cudaMemsetAsync(ctx->d_tcount.p + ntiles, 0, sizeof(uint32_t), st));
+      launch_tile_cull(endpoints, nq, order, ctx->M, chain[0] == 'T', cap, ctx->d_tlist.p, ctx->d_tcount.p,
+                       reinterpret_cast<unsigned int*>(ctx->d_tcount.p + ntiles), ctx->nsm, st);
+      ctx->launches++;
+      uint32_t mx = 0;
+      CK(cudaMemcpyAsync(&mx, ctx->d_tcount.p + ntiles, sizeof(mx), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (mx <= cap) {
+        ctx->tile_used_cap = cap;
+        break;
+      }
+      ctx->tile_cap = mx + mx / 8 + 64;  // regrow and redo (kept for later solves)
+    }
+    const uint32_t cap = ctx->tile_used_cap;
     CK(ctx->d_counts.ensure(nq));
     CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
-    CK(ctx->d_bits.ensure((uint64_t)nq * words));
-    CK(cudaMemsetAsync(ctx->d_bits.p, 0, sizeof(uint32_t) * (uint64_t)nq * words, st));
     uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
-    launch_cull_bits(endpoints, nq, ctx->M, chain[0] == 'T', ctx->d_bits.p, words, c32, ctx->nsm, st);
+    launch_query_cull(0, endpoints, nq, order, ctx->M, chain[0] == 'T', cap, ctx->d_tlist.p, ctx->d_tcount.p, c32,
+                      nullptr, nullptr, nullptr, ctx->nsm, st);
     ctx->launches++;
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
@@ -363,7 +398,8 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     npairs = tot;
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
-    launch_expand_bits(ctx->d_bits.p, words, nq, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    launch_query_cull(1, endpoints, nq, order, ctx->M, chain[0] == 'T', cap, ctx->d_tlist.p, ctx->d_tcount.p,
+                      nullptr, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else {
     npairs = k == 1 ? (uint64_t)nq * ctx->M.ntris : (uint64_t)nq * ctx->M.ntris * (ctx->M.ntris - 1);
@@ -549,6 +585,8 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   }
   R.n_rebuilds = counters[C_REBUILDS];
   R.alg_kflop = counters[C_KFLOP];
+  R.n_jobs_mono = cnt[2];
+  R.n_jobs_deep = cnt[3];
   R.n_launches = ctx->launches;
   R.n_eval_terms = counters[C_EVAL_TERMS];
   return SPOLY_OK;

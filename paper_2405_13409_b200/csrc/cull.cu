@@ -9,10 +9,9 @@
 // FP32 margin (folded in at upload), i.e. when the h-cone misses both +N and -N cones.  FP32 with a
 // margin: at most more permissive than the FP64 oracle predicate.
 //
-// Hierarchy: 64-triangle clusters -> 8-triangle sub-clusters -> triangles (all in Morton order).  One
-// warp per query; survivors are OR-ed into a per-query bitmask row (one bit per Morton position), so
-// the work list that `k_expand_bits` emits is query-major and Morton-ordered (deterministic) whatever
-// order the tests ran in.
+// Hierarchy: 64-triangle clusters -> 8-triangle sub-clusters -> triangles (all in Morton order), first
+// per tile of 32 Morton-sorted queries (tile endpoint spheres), then per query on the tile's survivors;
+// the work list is query-major and Morton-ordered (deterministic).
 #include "kernels.cuh"
 
 namespace spoly {
@@ -70,135 +69,266 @@ __device__ __forceinline__ bool test_tri(f3 x0, f3 x2, const TriCull& T, float e
   return k;
 }
 
+// ------------------------------------------------------------------ query-coherent tiles
+// Queries are sorted by a Morton code of their endpoints; each tile of 32 consecutive sorted queries is
+// culled once against the tile's endpoint bounding spheres (the direction sets from a node to a sphere of
+// endpoints are bounded by axis (c_x - c)^, sin(theta) = (rho + rho_x)/|c_x - c|), then each query is
+// tested exactly against its tile's surviving triangles only.
+
+__global__ void k_endpoint_bounds(const double* __restrict__ ep, uint32_t nq, float* bounds /* 12: min6, max6 */) {
+  __shared__ float smin[6][256], smax[6][256];
+  float lo[6], hi[6];
+  for (int c = 0; c < 6; ++c) {
+    lo[c] = INFINITY;
+    hi[c] = -INFINITY;
+  }
+  for (uint32_t q = threadIdx.x; q < nq; q += blockDim.x)
+    for (int c = 0; c < 6; ++c) {
+      const float v = (float)ep[6ull * q + c];
+      lo[c] = fminf(lo[c], v);
+      hi[c] = fmaxf(hi[c], v);
+    }
+  for (int c = 0; c < 6; ++c) {
+    smin[c][threadIdx.x] = lo[c];
+    smax[c][threadIdx.x] = hi[c];
+  }
+  __syncthreads();
+  for (int s = blockDim.x / 2; s > 0; s >>= 1) {
+    if (threadIdx.x < s)
+      for (int c = 0; c < 6; ++c) {
+        smin[c][threadIdx.x] = fminf(smin[c][threadIdx.x], smin[c][threadIdx.x + s]);
+        smax[c][threadIdx.x] = fmaxf(smax[c][threadIdx.x], smax[c][threadIdx.x + s]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) {
+    bounds[threadIdx.x] = smin[threadIdx.x][0];
+    bounds[6 + threadIdx.x] = smax[threadIdx.x][0];
+  }
+}
+
+// 30-bit key: 5 bits per endpoint coordinate, interleaved (x0.x x0.y x0.z x2.x x2.y x2.z)
+__global__ void k_query_keys(const double* __restrict__ ep, uint32_t nq, const float* __restrict__ bounds,
+                             uint32_t* keys, uint32_t* idx) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nq) return;
+  uint32_t b[6];
+  for (int c = 0; c < 6; ++c) {
+    const float lo = bounds[c], hi = bounds[6 + c];
+    const float s = hi > lo ? ((float)ep[6ull * q + c] - lo) / (hi - lo) : 0.f;
+    b[c] = (uint32_t)fminf(31.f, fmaxf(0.f, s * 32.f));
+  }
+  uint32_t key = 0;
+  for (int bit = 4; bit >= 0; --bit)
+    for (int c = 0; c < 6; ++c) key = (key << 1) | ((b[c] >> bit) & 1u);
+  keys[q] = key;
+  idx[q] = q;
+}
+
+void launch_query_order(const double* ep, uint32_t nq, float* bounds, uint32_t* keys, uint32_t* idx,
+                        cudaStream_t st) {
+  if (!nq) return;
+  k_endpoint_bounds<<<1, 256, 0, st>>>(ep, nq, bounds);
+  k_query_keys<<<(nq + 255) / 256, 256, 0, st>>>(ep, nq, bounds, keys, idx);
+}
+
+// direction bound from a node sphere to a sphere of endpoints (c_x, rho_x)
+__device__ __forceinline__ bool sphere_dir2(f3 x, float rx, float4 s, f3& a, float& chord) {
+  f3 d = {x.x - s.x, x.y - s.y, x.z - s.z};
+  const float l2 = dotf(d, d);
+  const float inv = rsqrtf(l2);
+  const float sn = (s.w + rx) * inv;
+  const float s2 = sn * sn;
+  a = inv * d;
+  chord = sn * (1.f + s2);
+  return s2 <= 0.25f;
+}
+
 template <bool REFRACT>
-__global__ void __launch_bounds__(256) k_cull_bits(const double* __restrict__ ep, uint32_t nq,
-                                                   const ClusterRec* __restrict__ l1, const ClusterRec* __restrict__ l2,
-                                                   const TriCull* __restrict__ tc, uint32_t ntris, uint32_t nl1,
-                                                   float ef, float eb, uint32_t* __restrict__ bits, uint32_t words,
-                                                   uint32_t* __restrict__ counts) {
+__device__ __forceinline__ bool tile_node_keep(f3 x0, float r0, f3 x2, float r2, float4 sphere, float4 cone, float ef,
+                                               float eb) {
+  f3 ap, an;
+  float cp, cn;
+  if (!sphere_dir2(x0, r0, sphere, ap, cp) || !sphere_dir2(x2, r2, sphere, an, cn)) return true;
+  if (!REFRACT) return node_keep(ap, cp, an, cn, 1.f, 1.f, cone);
+  return node_keep(ap, cp, an, cn, ef, eb, cone) || node_keep(ap, cp, an, cn, eb, ef, cone);
+}
+
+// one warp per tile: hierarchical (64-cluster, 8-sub-cluster, triangle) cull against the tile bounds;
+// survivors (Morton positions, ascending) -> tile_list[t * cap ...], true count -> tile_count[t]
+template <bool REFRACT>
+__global__ void __launch_bounds__(256) k_tile_cull(const double* __restrict__ ep, uint32_t nq,
+                                                   const uint32_t* __restrict__ order,
+                                                   const ClusterRec* __restrict__ l1,
+                                                   const ClusterRec* __restrict__ l2, const TriCull* __restrict__ tc,
+                                                   uint32_t ntris, uint32_t nl1, float ef, float eb, uint32_t cap,
+                                                   uint32_t* __restrict__ tile_list, uint32_t* __restrict__ tile_count,
+                                                   unsigned int* max_count) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t ntiles = (nq + 31) / 32;
   const uint32_t nl2 = (ntris + 7) >> 3;
-  for (uint32_t q = gw; q < nq; q += nw) {
+  for (uint32_t t = gw; t < ntiles; t += nw) {
+    // tile endpoint spheres (FP32, inflated); lanes past nq duplicate the tile's first query
+    const uint32_t i = t * 32 + lane;
+    const uint32_t q = i < nq ? order[i] : order[t * 32];
     const double* e = ep + 6ull * q;
-    const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
-    const f3 x2 = {(float)e[3], (float)e[4], (float)e[5]};
-    uint32_t* row = bits + (uint64_t)q * words;
+    const f3 a0 = {(float)e[0], (float)e[1], (float)e[2]}, a2 = {(float)e[3], (float)e[4], (float)e[5]};
+    f3 s0 = a0, s2 = a2;
+    for (int off = 16; off; off >>= 1) {
+      s0.x += __shfl_xor_sync(0xffffffffu, s0.x, off);
+      s0.y += __shfl_xor_sync(0xffffffffu, s0.y, off);
+      s0.z += __shfl_xor_sync(0xffffffffu, s0.z, off);
+      s2.x += __shfl_xor_sync(0xffffffffu, s2.x, off);
+      s2.y += __shfl_xor_sync(0xffffffffu, s2.y, off);
+      s2.z += __shfl_xor_sync(0xffffffffu, s2.z, off);
+    }
+    const f3 c0 = (1.f / 32.f) * s0, c2 = (1.f / 32.f) * s2;
+    float r0 = sqrtf(dotf(a0 - c0, a0 - c0)), r2 = sqrtf(dotf(a2 - c2, a2 - c2));
+    for (int off = 16; off; off >>= 1) {
+      r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, off));
+      r2 = fmaxf(r2, __shfl_xor_sync(0xffffffffu, r2, off));
+    }
+    r0 = r0 * 1.0001f + 1e-6f * (fabsf(c0.x) + fabsf(c0.y) + fabsf(c0.z) + 1.f);
+    r2 = r2 * 1.0001f + 1e-6f * (fabsf(c2.x) + fabsf(c2.y) + fabsf(c2.z) + 1.f);
     uint32_t count = 0;
+    uint32_t* out = tile_list + (uint64_t)t * cap;
     for (uint32_t base = 0; base < nl1; base += 32) {
       const uint32_t c = base + lane;
-      const bool k1 = c < nl1 && test_cluster<REFRACT>(x0, x2, l1[c], ef, eb);
+      const bool k1 = c < nl1 && tile_node_keep<REFRACT>(c0, r0, c2, r2, l1[c].sphere, l1[c].cone, ef, eb);
       uint32_t m1 = __ballot_sync(0xffffffffu, k1);
       while (m1) {
-        // up to 4 surviving 64-clusters per round: 32 lanes test their 8 sub-clusters each
         uint32_t sel[4];
         int nsel = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int k = 0; k < 4; ++k) {
           if (m1) {
-            sel[i] = base + __ffs(m1) - 1;
+            sel[k] = base + __ffs(m1) - 1;
             m1 &= m1 - 1;
-            nsel = i + 1;
+            nsel = k + 1;
           } else {
-            sel[i] = 0;
+            sel[k] = 0;
           }
         }
         const int which = lane >> 3, sub = lane & 7;
         const uint32_t sc = sel[which] * 8 + sub;
-        const bool k2 = which < nsel && sc < nl2 && test_cluster<REFRACT>(x0, x2, l2[sc], ef, eb);
+        const bool k2 = which < nsel && sc < nl2 &&
+                        tile_node_keep<REFRACT>(c0, r0, c2, r2, l2[sc].sphere, l2[sc].cone, ef, eb);
         uint32_t m2 = __ballot_sync(0xffffffffu, k2);
-        uint32_t word = 0;  // lane i < 2*nsel owns bits [32*(i&1), 32*(i&1)+32) of cluster sel[i>>1]
+        // triangles of the surviving sub-clusters in ascending Morton order: 4 sub-clusters per step
         while (m2) {
           int pick[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) {
+          for (int k = 0; k < 4; ++k) {
             if (m2) {
-              pick[i] = __ffs(m2) - 1;
+              pick[k] = __ffs(m2) - 1;
               m2 &= m2 - 1;
             } else {
-              pick[i] = -1;
+              pick[k] = -1;
             }
           }
-          const int j = lane >> 3, t = lane & 7;
+          const int j = lane >> 3, tt = lane & 7;
           bool k3 = false;
+          uint32_t tri = 0;
           if (pick[j] >= 0) {
-            const uint32_t tri = sel[pick[j] >> 3] * 64 + (pick[j] & 7) * 8 + t;
-            if (tri < ntris) k3 = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb);
-          }
-          const uint32_t m3 = __ballot_sync(0xffffffffu, k3);
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            if (pick[i] >= 0) {
-              const int cl = pick[i] >> 3, sb = pick[i] & 7;
-              const uint32_t b8 = (m3 >> (8 * i)) & 0xFFu;
-              if (lane == 2 * cl + (sb >> 2)) word |= b8 << (8 * (sb & 3));
+            tri = sel[pick[j] >> 3] * 64 + (pick[j] & 7) * 8 + tt;
+            if (tri < ntris) {
+              const TriCull T = tc[tri];
+              k3 = tile_node_keep<REFRACT>(c0, r0, c2, r2, T.sphere, T.cone, ef, eb);
             }
           }
-        }
-        if (lane < 2 * nsel && word) {
-          row[sel[lane >> 1] * 2 + (lane & 1)] = word;
-          count += __popc(word);
+          const unsigned m3 = __ballot_sync(0xffffffffu, k3);
+          if (k3) {
+            const uint32_t pos = count + __popc(m3 & ((1u << lane) - 1u));
+            if (pos < cap) out[pos] = tri;
+          }
+          count += __popc(m3);
         }
       }
     }
-#pragma unroll
-    for (int off = 16; off; off >>= 1) count += __shfl_xor_sync(0xffffffffu, count, off);
-    if (lane == 0) counts[q] = count;
+    if (lane == 0) {
+      tile_count[t] = count;
+      atomicMax(max_count, count);
+    }
   }
 }
 
-void launch_cull_bits(const double* ep, uint32_t nq, const DeviceMesh& M, int refract, uint32_t* bits, uint32_t words,
-                      uint32_t* counts, int nsm, cudaStream_t st) {
-  if (!nq) return;
+void launch_tile_cull(const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M, int refract,
+                      uint32_t cap, uint32_t* tile_list, uint32_t* tile_count, unsigned int* max_count, int nsm,
+                      cudaStream_t st) {
+  const uint32_t ntiles = (nq + 31) / 32;
+  if (!ntiles) return;
   const int threads = 256;
-  uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
-  uint64_t cap = (uint64_t)nsm * 8;
-  int blocks = (int)(want < cap ? want : cap);
+  uint64_t want = ((uint64_t)ntiles * 32 + threads - 1) / threads;
+  uint64_t capb = (uint64_t)nsm * 8;
+  const int blocks = (int)(want < capb ? want : capb);
   if (refract)
-    k_cull_bits<true><<<blocks, threads, 0, st>>>(ep, nq, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
-                                                   M.eta_front, M.eta_back, bits, words, counts);
+    k_tile_cull<true><<<blocks, threads, 0, st>>>(ep, nq, order, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
+                                                   M.eta_front, M.eta_back, cap, tile_list, tile_count, max_count);
   else
-    k_cull_bits<false><<<blocks, threads, 0, st>>>(ep, nq, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
-                                                    M.eta_front, M.eta_back, bits, words, counts);
+    k_tile_cull<false><<<blocks, threads, 0, st>>>(ep, nq, order, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters,
+                                                    M.eta_front, M.eta_back, cap, tile_list, tile_count, max_count);
 }
 
-// bitmask rows -> query-major work list at the scanned offsets; one warp per query
-__global__ void k_expand_bits(const uint32_t* __restrict__ bits, uint32_t words, uint32_t nq,
-                              const unsigned long long* __restrict__ offsets, uint32_t* pq, uint32_t* pt) {
+// one warp per (sorted) query: exact per-query triangle test on its tile's survivors; pass 0 counts,
+// pass 1 writes the query-major work list at the scanned offsets (ascending Morton order)
+template <bool REFRACT>
+__global__ void __launch_bounds__(256) k_query_cull(int pass, const double* __restrict__ ep, uint32_t nq,
+                                                    const uint32_t* __restrict__ order, const TriCull* __restrict__ tc,
+                                                    float ef, float eb, uint32_t cap,
+                                                    const uint32_t* __restrict__ tile_list,
+                                                    const uint32_t* __restrict__ tile_count, uint32_t* counts,
+                                                    const unsigned long long* __restrict__ offsets,
+                                                    uint32_t* __restrict__ pq, uint32_t* __restrict__ pt) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t q = gw; q < nq; q += nw) {
-    const uint32_t* row = bits + (uint64_t)q * words;
-    unsigned long long pos = offsets[q];
-    for (uint32_t w0 = 0; w0 < words; w0 += 32) {
-      const uint32_t wi = w0 + lane;
-      uint32_t word = wi < words ? row[wi] : 0u;
-      const uint32_t c = __popc(word);
-      uint32_t incl = c;
-#pragma unroll
-      for (int off = 1; off < 32; off <<= 1) {
-        uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += t;
+  for (uint32_t i = gw; i < nq; i += nw) {
+    const uint32_t q = order[i], t = i / 32;
+    const double* e = ep + 6ull * q;
+    const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
+    const f3 x2 = {(float)e[3], (float)e[4], (float)e[5]};
+    const uint32_t n = tile_count[t];
+    const uint32_t* list = tile_list + (uint64_t)t * cap;
+    uint32_t count = 0;
+    unsigned long long wpos = pass ? offsets[q] : 0ull;
+    for (uint32_t b = 0; b < n; b += 32) {
+      const uint32_t j = b + lane;
+      bool k = false;
+      uint32_t tri = 0;
+      if (j < n) {
+        tri = list[j];
+        k = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb);
       }
-      unsigned long long p = pos + incl - c;
-      while (word) {
-        const int b = __ffs(word) - 1;
-        word &= word - 1;
-        pq[p] = q;
-        pt[p] = wi * 32 + b;
-        ++p;
+      const unsigned m = __ballot_sync(0xffffffffu, k);
+      if (pass && k) {
+        const unsigned long long pos = wpos + __popc(m & ((1u << lane) - 1u));
+        pq[pos] = q;
+        pt[pos] = tri;
       }
-      pos += __shfl_sync(0xffffffffu, incl, 31);
+      wpos += __popc(m);
+      count += __popc(m);
     }
+    if (!pass && lane == 0) counts[q] = count;
   }
 }
 
-void launch_expand_bits(const uint32_t* bits, uint32_t words, uint32_t nq, const unsigned long long* offsets,
-                        uint32_t* pq, uint32_t* pt, int nsm, cudaStream_t st) {
+void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M,
+                       int refract, uint32_t cap, const uint32_t* tile_list, const uint32_t* tile_count,
+                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
+                       cudaStream_t st) {
   if (!nq) return;
-  k_expand_bits<<<nsm * 16, 256, 0, st>>>(bits, words, nq, offsets, pq, pt);
+  const int threads = 256;
+  uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
+  uint64_t capb = (uint64_t)nsm * 16;
+  const int blocks = (int)(want < capb ? want : capb);
+  if (refract)
+    k_query_cull<true><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.eta_front, M.eta_back, cap,
+                                                    tile_list, tile_count, counts, offsets, pq, pt);
+  else
+    k_query_cull<false><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.eta_front, M.eta_back, cap,
+                                                     tile_list, tile_count, counts, offsets, pq, pt);
 }
 
 // no cull: every (query, triangle) pair, query-major, Morton order

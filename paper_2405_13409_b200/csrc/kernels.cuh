@@ -11,11 +11,16 @@ void launch_build_tris(const float* pos, const float* nrm, const uint32_t* tri, 
 void launch_build_clusters(const TriRec* recs, uint32_t ntris, float margin, ClusterRec* l1, ClusterRec* l2,
                            cudaStream_t st);
 
-// cull.cu: hierarchical cone cull into a per-query bitmask (one bit per Morton position), then expand
-void launch_cull_bits(const double* ep, uint32_t nq, const DeviceMesh& M, int refract, uint32_t* bits, uint32_t words,
-                      uint32_t* counts, int nsm, cudaStream_t st);
-void launch_expand_bits(const uint32_t* bits, uint32_t words, uint32_t nq, const unsigned long long* offsets,
-                        uint32_t* pq, uint32_t* pt, int nsm, cudaStream_t st);
+// cull.cu: query-coherent hierarchical cone cull (tiles of 32 Morton-sorted queries, then per query)
+void launch_query_order(const double* ep, uint32_t nq, float* bounds, uint32_t* keys, uint32_t* idx,
+                        cudaStream_t st);
+void launch_tile_cull(const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M, int refract,
+                      uint32_t cap, uint32_t* tile_list, uint32_t* tile_count, unsigned int* max_count, int nsm,
+                      cudaStream_t st);
+void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M,
+                       int refract, uint32_t cap, const uint32_t* tile_list, const uint32_t* tile_count,
+                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
+                       cudaStream_t st);
 void launch_all_pairs_k1(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32_t nq, int k, const uint32_t* perm_of,
                         uint32_t* pair_query, uint32_t* pair_tpos, int nsm, cudaStream_t st);

@@ -186,7 +186,13 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
           }
           cnt[C_EVAL_TERMS] += NR * (NR + 1) / 2 + NR * (NR - 1) / 4;  // Bernstein + differences
           const int kfree = bernstein_root_free_level<NR>(r);
-          if (kfree > 0 && deg > 0) {
+          // kfree == 1: r is monotone on [0,1], so it has a root there iff r(0) and r(1) differ in sign
+          // (or one vanishes) -- exact, and it keeps root-free monotone pairs out of the job list
+          double r1 = 0.0;
+#pragma unroll
+          for (int t = NR - 1; t >= 0; --t) r1 += r[t];
+          const bool mono_root = !(r[0] * r1 > 0.0);
+          if (kfree > 0 && deg > 0 && (kfree > 1 || mono_root)) {
             job = true;
             meta = (uint32_t)kfree | ((uint32_t)deg << 8);
           }
@@ -277,6 +283,13 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
     for (int iu = 0; iu < nu; ++iu) {
       cnt[C_CANDIDATES]++;
       double us = ua[iu], vv = vs;
+      // the refinement below moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than 3e-3
+      // outside the simplex can neither become admissible nor land within eps_flag of an edge: reject it
+      // before refining (identical results, half the path-phase work on C2)
+      if (fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3) {
+        cnt[C_REJ_DOMAIN]++;
+        continue;
+      }
       // reading R2: <= 3 Newton steps on (a, b), keep a step only if |F| decreases and the candidate
       // stays within 1e-3 of its back-substituted position (local refinement, never a search)
       double fa, fau, fav, fb, fbu, fbv;

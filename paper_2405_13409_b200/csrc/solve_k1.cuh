@@ -195,7 +195,7 @@ struct PairOut {
 __device__ __forceinline__ double vertex_residual(d3 xp, d3 x, d3 xn, d3 n, double eta_prev, double eta_next) {
   d3 dp = normalize(x - xp), dn = normalize(xn - x), nh = normalize(n);
   d3 h = eta_next * dn - eta_prev * dp;
-  return norm(cross(h, nh)) / fmax(norm(h), 1e-3 * (eta_prev + eta_next));
+  return norm(cross(h, nh)) * fast_rcp(fmax(norm(h), 1e-3 * (eta_prev + eta_next)));
 }
 __device__ __forceinline__ bool side_ok(bool refract, d3 xp, d3 x, d3 xn, d3 n, d3 g) {
   double spn = dot(xp - x, n), snn = dot(xn - x, n), spg = dot(xp - x, g), sng = dot(xn - x, g);
@@ -211,40 +211,42 @@ __device__ double jacobian_k1(bool refract, d3 x0, d3 L, d3 x1, d3 e1, d3 e2, d3
                               double eta_out) {
   d3 w = x1 - L;
   const double lam = norm(w);
-  w = (1.0 / lam) * w;
+  w = fast_rcp(lam) * w;
   d3 g = cross(e1, e2);
   const double nn = norm(n);
-  const d3 nh = (1.0 / nn) * n;
+  const double inn = fast_rcp(nn);
+  const d3 nh = inn * n;
   d3 dref = x0 - x1;
   const double lam0 = norm(dref);
-  dref = (1.0 / lam0) * dref;
+  dref = fast_rcp(lam0) * dref;
   // orthonormal frame perpendicular to w (same construction as any: J is frame-invariant)
   d3 ax = fabs(w.x) < 0.6 ? mk3(1, 0, 0) : (fabs(w.y) < 0.6 ? mk3(0, 1, 0) : mk3(0, 0, 1));
   d3 b1 = normalize(cross(w, ax));
   d3 b2 = cross(w, b1);
   const double e11 = dot(e1, e1), e12 = dot(e1, e2), e22 = dot(e2, e2);
-  const double gdet = e11 * e22 - e12 * e12;
-  const double wg = dot(w, g);
+  const double igdet = fast_rcp(e11 * e22 - e12 * e12);
+  const double iwg = fast_rcp(dot(w, g));
   const double mu = dot(w, nh);
   const double ep = eta_in / eta_out;
   const double kk = 1.0 - ep * ep * (1.0 - mu * mu);
   const double sk = refract ? sqrt(fmax(kk, 0.0)) : 0.0;
+  const double isk = refract ? fast_rcp(sk) : 0.0;
   d3 dP[2];
 #pragma unroll
   for (int c = 0; c < 2; ++c) {
     d3 b = c == 0 ? b1 : b2;
-    d3 dy = lam * (b - (dot(b, g) / wg) * w);  // hit point moves in the triangle plane
+    d3 dy = lam * (b - (dot(b, g) * iwg) * w);  // hit point moves in the triangle plane
     double r1 = dot(e1, dy), r2 = dot(e2, dy);
-    double du = (e22 * r1 - e12 * r2) / gdet, dv = (e11 * r2 - e12 * r1) / gdet;
+    double du = (e22 * r1 - e12 * r2) * igdet, dv = (e11 * r2 - e12 * r1) * igdet;
     d3 dn = du * m1 + dv * m2;
-    d3 dnh = (1.0 / nn) * (dn - dot(nh, dn) * nh);
+    d3 dnh = inn * (dn - dot(nh, dn) * nh);
     double dmu = dot(b, nh) + dot(w, dnh);
     d3 dt;
     if (!refract) {
       dt = b - 2.0 * (dmu * nh + mu * dnh);
     } else {
       double sg = mu > 0 ? 1.0 : -1.0;
-      dt = ep * (b - dmu * nh - mu * dnh) + sg * ((ep * ep * mu * dmu / sk) * nh + sk * dnh);
+      dt = ep * (b - dmu * nh - mu * dnh) + sg * ((ep * ep * mu * dmu * isk) * nh + sk * dnh);
     }
     dP[c] = dy + lam0 * dt;
   }
