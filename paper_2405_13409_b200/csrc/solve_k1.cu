@@ -300,6 +300,8 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
         if (det == 0.0) break;
         const double idet = 1.0 / det;
         const double du = -(fbv * fa - fav * fb) * idet, dv = -(-fbu * fa + fau * fb) * idet;
+        // a step below 1e-15 cannot change the double-precision candidate: converged
+        if (fmax(fabs(du), fabs(dv)) <= 1e-15 * fmax(1.0, fmax(fabs(us), fabs(vv)))) break;
         if (!(fmax(fabs(us + du - ua[iu]), fabs(vv + dv - vs)) <= 1e-3)) break;
         double na, nau, nav, nb, nbu, nbv;
         beval<2, 3>(A, us + du, vv + dv, &na, &nau, &nav);

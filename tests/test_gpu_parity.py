@@ -259,3 +259,34 @@ def test_tt_sphere_parity(orc, sp, torch_cuda):
     ro = orc.solve(sub.mesh, "TT", sub.endpoints)
     g = _gpu_solve(sp, torch_cuda, sub.mesh, "TT", sub.endpoints)
     parity.compare(ro, g, sub.nqueries, tol_bary=1e-4)
+
+
+def test_c3_full_size_sampled(orc, sp, torch_cuda):
+    """Full C3 (262,144 receivers x 199,712 tris, T) in the bench launch configuration; sampled receivers
+    re-solved by the oracle; properties checked on every returned chain."""
+    w = W.pool_c3(res=512)
+    g = _gpu_solve(sp, torch_cuda, w.mesh, "T", w.endpoints)
+    qs = np.sort(np.random.default_rng(7).choice(w.nqueries, 24, replace=False))
+    sub = w.subset(qs)
+    ro = orc.solve(sub.mesh, "T", sub.endpoints)
+    sel = np.isin(g["query"], qs)
+    remap = {int(q): i for i, q in enumerate(qs)}
+    fsel = np.isin(g["flagged_query"], qs)
+    gs = {"query": np.array([remap[int(q)] for q in g["query"][sel]], np.uint32), "tuple": g["tuple"][sel],
+          "bary": g["bary"][sel], "per_query": g["per_query"][qs], "contribution": g["contribution"][sel],
+          "flagged_query": np.array([remap[int(q)] for q in g["flagged_query"][fsel]], np.uint32),
+          "flagged_tuple": g["flagged_tuple"][fsel]}
+    st = parity.compare(ro, gs, len(qs))
+    assert st["compared_solutions"] >= 12
+    assert np.all(g["residual"] < 1e-6)
+    b = g["bary"]
+    assert np.all(b[:, 0] >= -1e-9) and np.all(b[:, 1] >= -1e-9) and np.all(b.sum(1) <= 1 + 1e-9)
+
+
+def test_determinism_bit_identical(sp, torch_cuda):
+    """deterministic=1: two solves of the same inputs give bit-identical outputs."""
+    w = W.glints_c2(res=32)
+    a = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
+    b = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
+    for k in ("query", "tuple", "bary", "contribution", "per_query", "flagged_query"):
+        assert np.array_equal(a[k], b[k]), k
