@@ -32,13 +32,16 @@ UNIT = "paths/s"
 # ---------------------------------------------------------------- algorithmic FLOP model
 # Minimal-form FP64 FLOPs of the one-bounce reflection solve (FMA = 2, add/mul/div/sqrt = 1), counted
 # from the kernel formulas (DESIGN.md §5 table):
-#   phase 1, per pair: decision 75 + setup 18 + a 75 + b 268 + normalise 22 + truncation 10 + Bezout 128
-#                      + Laplace 316 + normalise r 11 + Bernstein level 155                  = 1078
+#   phase 1, per pair: decision 75 + setup 18 + a 75 + b 268 + normalise 22 + truncation 10
+#                      + coplanarity sign test 16                                            = 484
+#            per pair reaching the elimination (counter n_elims): Bezout 128 + Laplace 316
+#                      + normalise r 11 + Bernstein level 155                                = 610
 #   phase 2: 2 per FMA term of the root-finding evaluations (counter n_eval_terms)
 #            + 468 per coefficient-phase rebuild (counter n_rebuilds)
 #            + 430 per candidate (back-substitution 25, one (a,b) Newton step 277, Eq. 3 + sides 130)
 #            + 250 per admissible chain (analytic ray-differential Jacobian)
-FLOP_PHASE1_PER_PAIR_R = 1078
+FLOP_PHASE1_PER_PAIR_R = 484
+FLOP_PHASE1_PER_ELIM_R = 610
 FLOP_PER_EVAL_TERM = 2
 FLOP_PER_REBUILD_R = 468
 FLOP_PER_CANDIDATE_R = 430
@@ -46,16 +49,18 @@ FLOP_PER_ADMISSIBLE_R = 250
 
 
 # one-bounce refraction (T), same accounting: phase 1 per pair: decision 60 + setup 18 + a 75 + b (square
-# form, Eq. 9) 656 + normalise/truncate 55 + resultant by pseudo-remainder 998 + Bernstein (degree 12) 260
-# = 2122; rebuild 864; candidate 755 (b has 28 coefficients); admissible 300 (refraction Jacobian).
-FLOP_PHASE1_PER_PAIR_T = 2122
+# form, Eq. 9) 656 + normalise/truncate 55 + coplanarity test 16 = 880; per elimination: resultant by
+# pseudo-remainder 998 + Bernstein (degree 12) 260 = 1258; rebuild 864; candidate 755 (b has 28
+# coefficients); admissible 300 (refraction Jacobian).
+FLOP_PHASE1_PER_PAIR_T = 880
+FLOP_PHASE1_PER_ELIM_T = 1258
 FLOP_PER_REBUILD_T = 864
 FLOP_PER_CANDIDATE_T = 755
 FLOP_PER_ADMISSIBLE_T = 300
 
 
 def flop_model_R(rep):
-    p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_R
+    p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_R + rep["n_elims"] * FLOP_PHASE1_PER_ELIM_R
     p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_R +
           rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
     return p1, p2
@@ -67,7 +72,7 @@ def flop_model(chain, rep):
     if chain == "R":
         return flop_model_R(rep)
     if chain == "T":
-        p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_T
+        p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_T + rep["n_elims"] * FLOP_PHASE1_PER_ELIM_T
         p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_T +
               rep["n_candidates"] * FLOP_PER_CANDIDATE_T + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_T)
         return p1, p2
@@ -319,7 +324,7 @@ def main():
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
-                                                 "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds")},
+                                                 "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims")},
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,

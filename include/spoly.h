@@ -112,6 +112,7 @@ typedef struct {
   uint64_t alg_kflop;                 /* two-bounce kernel: algorithmic kFLOP (coefficient phase +
                                          determinant evaluations)                   */
   uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce phase-2 jobs: monotone r / deeper recursion   */
+  uint64_t n_elims;                   /* one-bounce pairs that reached the elimination phase       */
 } spoly_report;
 
 typedef struct {

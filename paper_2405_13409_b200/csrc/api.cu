@@ -585,6 +585,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   }
   R.n_rebuilds = counters[C_REBUILDS];
   R.alg_kflop = counters[C_KFLOP];
+  R.n_elims = counters[C_ELIMS];
   R.n_jobs_mono = cnt[2];
   R.n_jobs_deep = cnt[3];
   R.n_launches = ctx->launches;

@@ -112,6 +112,6 @@ struct JobSink {
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,
-       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_NUM };
+       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_NUM };
 
 }  // namespace spoly

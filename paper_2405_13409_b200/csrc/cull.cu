@@ -53,6 +53,26 @@ __device__ __forceinline__ bool test_cluster(f3 x0, f3 x2, const ClusterRec& C, 
   return node_keep(ap, cp, an, cn, ef, eb, C.cone) || node_keep(ap, cp, an, cn, eb, ef, C.cone);
 }
 
+// Coplanarity sign test (exact condition, FP32 with margin): a = ((x1 - x0) x (x2 - x0)) . n (Eq. 6) is the
+// product of two barycentric-linear functions, so its triangle-Bernstein control points are
+// A_ii (corners) and (A_ij + A_ji)/2 (edges) with A_ij = ((p_i - x0) x w) . n_j, w = x2 - x0.  A strict
+// common sign beyond 1e-3 sum|A| (FP32 errors are ~1e-6 relative) proves a != 0 on the triangle: no chain.
+__device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
+  const float4* r = tris[t].r;
+  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+  const f3 w = x2 - x0;
+  const f3 c0 = crossf(f3{a.x, a.y, a.z} - x0, w), c1 = crossf(f3{a.w, b.x, b.y} - x0, w),
+           c2 = crossf(f3{b.z, b.w, c.x} - x0, w);
+  const f3 n0 = {c.y, c.z, c.w}, n1 = {d.x, d.y, d.z}, n2 = {d.w, e.x, e.y};
+  const float a00 = dotf(c0, n0), a11 = dotf(c1, n1), a22 = dotf(c2, n2);
+  const float e01 = 0.5f * (dotf(c0, n1) + dotf(c1, n0)), e02 = 0.5f * (dotf(c0, n2) + dotf(c2, n0)),
+              e12 = 0.5f * (dotf(c1, n2) + dotf(c2, n1));
+  const float m = 1e-3f * (fabsf(a00) + fabsf(a11) + fabsf(a22) + 2.f * (fabsf(e01) + fabsf(e02) + fabsf(e12)));
+  const bool pos = a00 > m && a11 > m && a22 > m && e01 > m && e02 > m && e12 > m;
+  const bool neg = a00 < -m && a11 < -m && a22 < -m && e01 < -m && e02 < -m && e12 < -m;
+  return !(pos || neg);
+}
+
 template <bool REFRACT>
 __device__ __forceinline__ bool test_tri(f3 x0, f3 x2, const TriCull& T, float ef, float eb) {
   f3 ap, an;
@@ -276,6 +296,7 @@ void launch_tile_cull(const double* ep, uint32_t nq, const uint32_t* order, cons
 template <bool REFRACT>
 __global__ void __launch_bounds__(256) k_query_cull(int pass, const double* __restrict__ ep, uint32_t nq,
                                                     const uint32_t* __restrict__ order, const TriCull* __restrict__ tc,
+                                                    const TriRec* __restrict__ tris,
                                                     float ef, float eb, uint32_t cap,
                                                     const uint32_t* __restrict__ tile_list,
                                                     const uint32_t* __restrict__ tile_count, uint32_t* counts,
@@ -299,7 +320,7 @@ __global__ void __launch_bounds__(256) k_query_cull(int pass, const double* __re
       uint32_t tri = 0;
       if (j < n) {
         tri = list[j];
-        k = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb);
+        k = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb) && coplanar_keep(tris, tri, x0, x2);
       }
       const unsigned m = __ballot_sync(0xffffffffu, k);
       if (pass && k) {
@@ -324,10 +345,10 @@ void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* 
   uint64_t capb = (uint64_t)nsm * 16;
   const int blocks = (int)(want < capb ? want : capb);
   if (refract)
-    k_query_cull<true><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.eta_front, M.eta_back, cap,
+    k_query_cull<true><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
                                                     tile_list, tile_count, counts, offsets, pq, pt);
   else
-    k_query_cull<false><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.eta_front, M.eta_back, cap,
+    k_query_cull<false><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
                                                      tile_list, tile_count, counts, offsets, pq, pt);
 }
 

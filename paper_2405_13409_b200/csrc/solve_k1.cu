@@ -83,6 +83,19 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
   return true;
 }
 
+// Bernstein form of the quadratic a(u,v) on the triangle (6 control points: corners c00, c00+c10+c20,
+// c00+c01+c02 and edge points c00+c10/2, c00+c01/2, c00+(c10+c01+c11)/2); a strict common sign with a
+// margin of 1e-4 sum|c| (>> |grad a| * 1e-6) proves a != 0 on the triangle enlarged by 1e-6.
+__device__ __forceinline__ bool coplanarity_may_vanish(const double* A) {
+  const double c00 = A[0], c01 = A[1], c02 = A[2], c10 = A[3], c11 = A[4], c20 = A[6];
+  const double b0 = c00, b1 = c00 + c10 + c20, b2 = c00 + c01 + c02, b3 = c00 + 0.5 * c10, b4 = c00 + 0.5 * c01,
+               b5 = c00 + 0.5 * (c10 + c01 + c11);
+  const double m = 1e-4 * (fabs(c00) + fabs(c01) + fabs(c02) + fabs(c10) + fabs(c11) + fabs(c20));
+  const bool pos = b0 > m && b1 > m && b2 > m && b3 > m && b4 > m && b5 > m;
+  const bool neg = b0 < -m && b1 < -m && b2 < -m && b3 < -m && b4 < -m && b5 < -m;
+  return !(pos || neg);
+}
+
 template <bool TC>
 __device__ __forceinline__ void eliminate(const Sys1<TC>& S, double* r) {
   if (TC)
@@ -166,10 +179,19 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
       load_pair(pq, pt, tris, ep, i, P, N, x0, x2, q);
       cnt[C_PAIRS]++;
       Sys1<TC> Sys;
-      const bool ok = build_system<TC>(x0, x2, P, N, prm, Sys);
+      bool ok = build_system<TC>(x0, x2, P, N, prm, Sys);
       flags = Sys.flags;
       if (ok) {
         cnt[C_SYSTEMS]++;
+      }
+      if (ok && !coplanarity_may_vanish(Sys.A)) {
+        // a(u,v) = Eq. 6 has a strict sign on the triangle (enlarged far beyond the 1e-9 domain slack), so
+        // no chain exists on this pair: exact early out (no effect on the admissible set)
+        ok = false;
+        cnt[C_EVAL_TERMS] += 8;
+      } else if (ok) {
+        cnt[C_EVAL_TERMS] += 8;
+        cnt[C_ELIMS]++;
         eliminate<TC>(Sys, r);
         double mr = 0.0;
 #pragma unroll

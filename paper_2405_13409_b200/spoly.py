@@ -50,7 +50,8 @@ class spoly_report(ctypes.Structure):
         ("ms_cull", ctypes.c_float), ("ms_solve", ctypes.c_float), ("ms_reduce", ctypes.c_float),
         ("n_launches", ctypes.c_uint32), ("n_eval_terms", ctypes.c_uint64), ("required_solutions", ctypes.c_uint64),
         ("ms_phase1", ctypes.c_float), ("ms_phase2", ctypes.c_float), ("n_rebuilds", ctypes.c_uint64),
-        ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64)]
+        ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64),
+        ("n_elims", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -199,7 +200,7 @@ class Context:
                    n_launches=int(r.report.n_launches), n_eval_terms=int(r.report.n_eval_terms),
                    ms_phase1=r.report.ms_phase1, ms_phase2=r.report.ms_phase2, n_rebuilds=int(r.report.n_rebuilds),
                    alg_kflop=int(r.report.alg_kflop), n_jobs_mono=int(r.report.n_jobs_mono),
-                   n_jobs_deep=int(r.report.n_jobs_deep))
+                   n_jobs_deep=int(r.report.n_jobs_deep), n_elims=int(r.report.n_elims))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),

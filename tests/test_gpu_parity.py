@@ -70,7 +70,9 @@ def test_random_interpolated_R(orc, sp, torch_cuda):
     ro2 = orc.solve(mesh, "R", ep, intensity=inten)
     g2 = _gpu_solve(sp, torch_cuda, mesh, "R", ep, intensity=inten)
     parity.compare(ro2, g2, Q)
-    assert g2["report"]["n_pairs_in"] >= ro2.report["pairs_in"]  # FP32 cull at most more permissive
+    # cull soundness: every oracle chain's (query, tuple) is in the GPU work list
+    wl = set(zip(g2["worklist"][0].tolist(), g2["worklist"][1][:, 0].tolist()))
+    assert all((int(q), int(t)) in wl for q, t in zip(ro2.query, ro2.tuple[:, 0]))
 
 
 def test_explicit_tuple_list_and_edges(orc, sp, torch_cuda):
