@@ -189,6 +189,7 @@ def main():
     ap.add_argument("--ref-sample", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cull-levels", type=int, default=None, help="k=2 cull subdivision levels (default: library)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -217,7 +218,8 @@ def main():
         w = W.CONFIGS[args.config](**kw)
     chain = w.chain
     stream = torch.cuda.current_stream(dev)
-    ctx = spoly.Context(local, stream=stream)
+    cfg = spoly.default_config() if args.cull_levels is None else spoly.default_config(cull_levels=args.cull_levels)
+    ctx = spoly.Context(local, cfg, stream=stream)
     ctx.upload_mesh(w.mesh)
     ep = torch.as_tensor(w.endpoints, dtype=torch.float64, device=dev)
     inten = torch.as_tensor(w.intensity, dtype=torch.float64, device=dev)
@@ -324,7 +326,8 @@ def main():
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
-                                                 "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims")},
+                                                 "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims",
+                                                 "n_pairs_coarse")},
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,

@@ -67,6 +67,7 @@ typedef struct {
   float cull_margin;     /* angular slack (rad) of the FP32 cull; 1e-4                       */
   uint64_t max_solutions;/* initial solution-buffer capacity (regrown once on overflow)      */
   uint64_t max_pairs;    /* work-list chunk size in (query, tuple) pairs                      */
+  int cull_levels;       /* k=2: barycentric subdivision levels re-testing each kept pair; 3 */
 } spoly_config;
 
 /* Fills cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
@@ -113,6 +114,8 @@ typedef struct {
                                          determinant evaluations)                   */
   uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce phase-2 jobs: monotone r / deeper recursion   */
   uint64_t n_elims;                   /* one-bounce pairs that reached the elimination phase       */
+  uint64_t n_pairs_coarse;            /* two-bounce pair cull: pairs kept before the subdivision
+                                         refinement (n_pairs_in counts the refined list)            */
 } spoly_report;
 
 typedef struct {

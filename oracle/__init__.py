@@ -41,7 +41,8 @@ class Config(ctypes.Structure):
     _fields_ = [("pieces", ctypes.c_int), ("scan_bisect_iters", ctypes.c_int), ("bisect_tol", ctypes.c_double),
                 ("polish_iters", ctypes.c_int), ("theta_admit", ctypes.c_double), ("theta_final", ctypes.c_double),
                 ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
-                ("cull", ctypes.c_int), ("cull_margin", ctypes.c_double)]
+                ("cull", ctypes.c_int), ("cull_margin", ctypes.c_double),
+                ("cull_levels", ctypes.c_int)]
 
 
 def lib():
@@ -71,7 +72,8 @@ def lib():
             L.orc_det_at.restype = ctypes.c_double
             L.orc_det_at.argtypes = [P, ctypes.c_int, P, ctypes.c_int, ctypes.c_int, ctypes.c_double]
             L.orc_isolate.argtypes = [P, ctypes.c_int, ctypes.c_double, ctypes.c_double, ctypes.c_double, P]
-            L.orc_cull_keep.argtypes = [ctypes.c_char_p, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double]
+            L.orc_cull_keep.argtypes = [ctypes.c_char_p, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                                        ctypes.c_int]
             L.orc_jacobian.restype = ctypes.c_double
             L.orc_jacobian.argtypes = [ctypes.c_char_p, P, P, P, ctypes.c_double, ctypes.c_double, P]
             L.orc_sqrt_table.argtypes = [P]
@@ -231,12 +233,12 @@ def isolate(p, lo=0.0, hi=1.0, tol=1e-9):
     return out[:n].copy()
 
 
-def cull_keep(chain, tris18, x0, xk1, eta_front=1.0, eta_back=1.0, margin=1e-9) -> bool:
+def cull_keep(chain, tris18, x0, xk1, eta_front=1.0, eta_back=1.0, margin=1e-9, levels=3) -> bool:
     L = lib()
     t = np.ascontiguousarray(tris18, dtype=np.float64)
     x0 = np.ascontiguousarray(x0, dtype=np.float64)
     xk1 = np.ascontiguousarray(xk1, dtype=np.float64)
-    return bool(L.orc_cull_keep(chain.encode(), _p(t), _p(x0), _p(xk1), eta_front, eta_back, margin))
+    return bool(L.orc_cull_keep(chain.encode(), _p(t), _p(x0), _p(xk1), eta_front, eta_back, margin, levels))
 
 
 def jacobian(chain, tris18, x0, xk1, bary, eta_front=1.0, eta_back=1.0) -> float:

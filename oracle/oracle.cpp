@@ -959,8 +959,58 @@ static bool vertex_keep(const Cone& prev, const Cone& next, double eta_prev, dou
   double lim = alpha + N.theta + margin;
   return phi <= lim || (M_PI - phi) <= lim;
 }
+// both vertex tests of a triangle pair (k=2): directions between the two triangles bounded by the cone of
+// the 9 vertex differences (their convex hull is the Minkowski difference)
+static bool pair_cones_keep(const Tri& A, const Tri& B, V3 x0, V3 xk1, double e0, double e1,
+                            const vector<double>& e2s, double margin) {
+  auto ncone = [](const Tri& T) { return cone_of({T.n[0], T.n[1], T.n[2]}); };
+  vector<V3> ab, ba;
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) {
+      ab.push_back(B.p[j] - A.p[i]);
+      ba.push_back(A.p[i] - B.p[j]);
+    }
+  Cone cab = cone_of(ab), cba = cone_of(ba);
+  Cone c0 = cone_of({x0 - A.p[0], x0 - A.p[1], x0 - A.p[2]});
+  if (!vertex_keep(c0, cab, e0, e1, ncone(A), margin)) return false;
+  Cone c3 = cone_of({xk1 - B.p[0], xk1 - B.p[1], xk1 - B.p[2]});
+  for (double e2 : e2s)
+    if (vertex_keep(cba, c3, e1, e2, ncone(B), margin)) return true;
+  return false;
+}
+// 4-way midpoint subdivision: corner positions and normals of the children are the interpolants of
+// Eqs. 1-2 at the barycentric midpoints (linear, so the average of the corner data)
+static void split4(const Tri& T, Tri out[4]) {
+  Tri m;  // midpoints: m[0] = ab, m[1] = bc, m[2] = ca
+  for (int k = 0; k < 3; ++k) {
+    m.p[k] = 0.5 * (T.p[k] + T.p[(k + 1) % 3]);
+    m.n[k] = 0.5 * (T.n[k] + T.n[(k + 1) % 3]);
+  }
+  const int idx[4][3][2] = {{{0, 0}, {1, 0}, {1, 2}}, {{1, 0}, {0, 1}, {1, 1}}, {{1, 2}, {1, 1}, {0, 2}},
+                            {{1, 1}, {1, 2}, {1, 0}}};  // {0: corner, 1: midpoint}, index
+  for (int s = 0; s < 4; ++s)
+    for (int k = 0; k < 3; ++k) {
+      const Tri& src = idx[s][k][0] ? m : T;
+      out[s].p[k] = src.p[idx[s][k][1]];
+      out[s].n[k] = src.n[idx[s][k][1]];
+    }
+}
+// SURVEY A1 "Refinement": keep the pair iff the pair passes and, `levels` deep, some sub-pair passes at
+// every level (sub-cones lie inside the parent cones, so the test stays sound)
+static bool pair_keep_sub(const Tri& A, const Tri& B, V3 x0, V3 xk1, double e0, double e1,
+                          const vector<double>& e2s, double margin, int levels) {
+  if (!pair_cones_keep(A, B, x0, xk1, e0, e1, e2s, margin)) return false;
+  if (levels <= 0) return true;
+  Tri a4[4], b4[4];
+  split4(A, a4);
+  split4(B, b4);
+  for (int i = 0; i < 4; ++i)
+    for (int j = 0; j < 4; ++j)
+      if (pair_keep_sub(a4[i], b4[j], x0, xk1, e0, e1, e2s, margin, levels - 1)) return true;
+  return false;
+}
 static bool cull_keep(const std::string& chain, const vector<Tri>& tris, V3 x0, V3 xk1, double eta_front,
-                      double eta_back, double margin) {
+                      double eta_back, double margin, int levels) {
   const int k = (int)chain.size();
   auto ncone = [](const Tri& T) { return cone_of({T.n[0], T.n[1], T.n[2]}); };
   if (k == 1) {
@@ -991,18 +1041,8 @@ static bool cull_keep(const std::string& chain, const vector<Tri>& tris, V3 x0, 
     if (!side_keep(A, x0, chain[0] == 'T', B)) return false;
     if (!side_keep(B, xk1, chain[1] == 'T', A)) return false;
   }
-  vector<V3> ab, ba;
-  for (int i = 0; i < 3; ++i)
-    for (int j = 0; j < 3; ++j) {
-      ab.push_back(B.p[j] - A.p[i]);
-      ba.push_back(A.p[i] - B.p[j]);
-    }
-  Cone cab = cone_of(ab), cba = cone_of(ba);
   double e0 = front_side(x0, A) ? eta_front : eta_back;
   double e1 = chain[0] == 'T' ? (e0 == eta_front ? eta_back : eta_front) : e0;
-  Cone c0 = cone_of({x0 - A.p[0], x0 - A.p[1], x0 - A.p[2]});
-  if (!vertex_keep(c0, cab, e0, e1, ncone(A), margin)) return false;
-  Cone c3 = cone_of({xk1 - B.p[0], xk1 - B.p[1], xk1 - B.p[2]});
   // eta_2 depends on the side of x_1 w.r.t. T_2: test both media when ambiguous (union = sound)
   vector<double> e2s;
   if (chain[1] == 'R')
@@ -1011,9 +1051,7 @@ static bool cull_keep(const std::string& chain, const vector<Tri>& tris, V3 x0, 
     e2s.push_back(eta_front);
     e2s.push_back(eta_back);
   }
-  for (double e2 : e2s)
-    if (vertex_keep(cba, c3, e1, e2, ncone(B), margin)) return true;
-  return false;
+  return pair_keep_sub(A, B, x0, xk1, e0, e1, e2s, margin, levels);
 }
 
 }  // namespace oracle
@@ -1043,6 +1081,7 @@ void orc_default_config(orc_config* c) {
   c->tau_trunc = 1e-12;
   c->cull = 1;
   c->cull_margin = 1e-9;
+  c->cull_levels = 3;
 }
 
 static vector<Tri> mesh_tris(const float* pos, const float* nrm, const uint32_t* tri, const uint32_t* ids, int k) {
@@ -1109,7 +1148,7 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
         for (uint32_t t = 0; t < ntris; ++t) {
           if (cfg.cull) {
             vector<Tri> tr = mesh_tris(pos, nrm, tri, &t, 1);
-            if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin)) continue;
+            if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin, cfg.cull_levels)) continue;
           }
           run(&t);
         }
@@ -1120,7 +1159,7 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
             uint32_t ids[2] = {t1, t2};
             if (cfg.cull) {
               vector<Tri> tr = mesh_tris(pos, nrm, tri, ids, 2);
-              if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin)) continue;
+              if (!cull_keep(chain, tr, x0, xk1, eta_front, eta_back, cfg.cull_margin, cfg.cull_levels)) continue;
             }
             run(ids);
           }
@@ -1254,9 +1293,10 @@ int orc_isolate(const double* p, int deg, double lo, double hi, double tol, doub
 }
 
 int orc_cull_keep(const char* chain_c, const double* t, const double* x0, const double* xk1, double eta_front,
-                  double eta_back, double margin) {
+                  double eta_back, double margin, int levels) {
   std::string chain(chain_c);
-  return cull_keep(chain, tris_from(t, (int)chain.size()), mk(x0), mk(xk1), eta_front, eta_back, margin) ? 1 : 0;
+  return cull_keep(chain, tris_from(t, (int)chain.size()), mk(x0), mk(xk1), eta_front, eta_back, margin, levels) ? 1
+                                                                                                                 : 0;
 }
 
 double orc_jacobian(const char* chain_c, const double* t, const double* x0, const double* xk1, double eta_front,

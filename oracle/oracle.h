@@ -33,6 +33,7 @@ typedef struct {
   double tau_trunc;      /* 1e-12 numerical u-degree truncation (c5-ii) */
   int cull;              /* 1: oracle cull predicate when no tuple list is given */
   double cull_margin;    /* radians, 1e-9 */
+  int cull_levels;       /* k=2 barycentric subdivision levels of the cull, 3 */
 } orc_config;
 
 void orc_default_config(orc_config* cfg);
@@ -84,7 +85,7 @@ double orc_det_at(const double* a, int deg_a, const double* b, int deg_b, int n,
 int orc_isolate(const double* p, int deg, double lo, double hi, double tol, double* roots_out);
 /* cull predicate: 1 = keep.  tris as in orc_build_system. */
 int orc_cull_keep(const char* chain, const double* tris, const double* x0, const double* xk1,
-                  double eta_front, double eta_back, double margin);
+                  double eta_front, double eta_back, double margin, int levels /* k=2 subdivision */);
 /* exact forward light-side trace Jacobian J (c15) at a solved chain; returns J (<=0 on failure) */
 double orc_jacobian(const char* chain, const double* tris, const double* x0, const double* xk1,
                     double eta_front, double eta_back, const double* bary);

@@ -56,8 +56,12 @@ struct spoly_ctx {
   // work list
   DBuf<uint64_t> d_counts;
   DBuf<unsigned long long> d_offsets;
-  DBuf<uint32_t> d_pq, d_pt, d_pt_orig;
-  uint64_t npairs = 0;
+  DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2;
+  DBuf<unsigned char> d_keep;
+  DBuf<double> d_rec;
+  DBuf<uint32_t> d_plist;
+  DBuf<unsigned long long> d_nsel;
+  uint64_t npairs = 0, npairs_culled = 0;
   int last_k = 1;
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
@@ -109,6 +113,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->cull_margin = 1e-4f;
   c->max_solutions = 1ull << 22;
   c->max_pairs = 1ull << 32;
+  c->cull_levels = 3;
   return SPOLY_OK;
 }
 
@@ -150,6 +155,8 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_sub.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
+  ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
+  ctx->d_rec.release(); ctx->d_plist.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
@@ -306,6 +313,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->st;
   ctx->launches = 0;
+  ctx->npairs_culled = 0;
   memset(out, 0, sizeof(*out));
   out->k = k;
   CK(ctx->d_count.ensure(2));
@@ -346,6 +354,37 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_cull_pairs(1, endpoints, nq, ctx->M, chain[0] == 'T', chain[1] == 'T', nullptr, ctx->d_offsets.p,
                       ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
+    if (ctx->cfg.cull_levels > 0 && npairs) {
+      // barycentric subdivision refinement, then an order-preserving compaction (deterministic)
+      CK(ctx->d_keep.ensure(npairs));
+      CK(ctx->d_pq2.ensure(npairs));
+      CK(ctx->d_pt2.ensure(2 * npairs));
+      CK(ctx->d_nsel.ensure(4));
+      launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels,
+                          chain[0] == 'T', chain[1] == 'T', ctx->d_keep.p, ctx->nsm, st);
+      ctx->launches++;
+      const uint2* pt_in = reinterpret_cast<const uint2*>(ctx->d_pt.p);
+      uint2* pt_out = reinterpret_cast<uint2*>(ctx->d_pt2.p);
+      size_t tb1 = 0, tb2 = 0;
+      CK(cub::DeviceSelect::Flagged(nullptr, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
+                                    (int64_t)npairs, st));
+      CK(cub::DeviceSelect::Flagged(nullptr, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1, (int64_t)npairs,
+                                    st));
+      CK(ctx->d_temp.ensure(std::max(tb1, tb2)));
+      tb1 = tb2 = ctx->d_temp.cap;
+      CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
+                                    (int64_t)npairs, st));
+      CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1,
+                                    (int64_t)npairs, st));
+      ctx->launches += 2;
+      unsigned long long ns = 0;
+      CK(cudaMemcpyAsync(&ns, ctx->d_nsel.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      ctx->npairs_culled = npairs;
+      npairs = ns;
+      std::swap(ctx->d_pq, ctx->d_pq2);
+      std::swap(ctx->d_pt, ctx->d_pt2);
+    }
   } else if (ctx->cfg.cull) {
     // query order (Morton of the endpoints), tile cull, per-query cull on the tile survivors
     const uint32_t ntiles = (nq + 31) / 32;
@@ -457,8 +496,19 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       ctx->launches += 2;
     } else {
       CK(cudaEventRecord(ctx->ev[5], st));
-      launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, ctx->nsm,
-                      st);
+      {
+        const uint64_t rb = k2_record_bytes(chain[0] == 'T', chain[1] == 'T') / sizeof(double);
+        const uint64_t budget = (3ull << 30) / sizeof(double);  // <= 3 GiB of system records per chunk
+        const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(npairs, budget / rb));
+        CK(ctx->d_rec.ensure(per * rb));
+        CK(ctx->d_plist.ensure(per));
+        CK(ctx->d_nsel.ensure(8));
+        K2Scratch W{ctx->d_rec.p, (ctx->d_rec.cap / rb) * rb, ctx->d_plist.p, ctx->d_nsel.p + 4, 0};
+        if (W.rec_cap / rb > ctx->d_plist.cap) W.rec_cap = ctx->d_plist.cap * rb;
+        launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten,
+                        prm, S, W, ctx->nsm, st);
+        ctx->launches += W.launches - 1;
+      }
       ctx->launches += 1;
     }
     CK(cudaGetLastError());
@@ -586,6 +636,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_rebuilds = counters[C_REBUILDS];
   R.alg_kflop = counters[C_KFLOP];
   R.n_elims = counters[C_ELIMS];
+  R.n_pairs_coarse = ctx->npairs_culled;
   R.n_jobs_mono = cnt[2];
   R.n_jobs_deep = cnt[3];
   R.n_launches = ctx->launches;

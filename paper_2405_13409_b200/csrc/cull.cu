@@ -566,4 +566,186 @@ void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh
                                            M.eta_front, M.eta_back, counts, offsets, pq, pt);
 }
 
+// ------------------------------------------------------------------ barycentric subdivision refinement (k=2)
+// A kept triangle pair is re-tested on 4-way midpoint subdivisions of both triangles, `levels` deep (SURVEY
+// A1 "Refinement"): positions and (linearly interpolated) normals of a sub-triangle are the interpolants at
+// its corners, so its bounding sphere (centroid, max corner distance) and normal cone (axis = sum of the
+// normalised corner normals, half angle = max corner angle; a positive combination of the corner
+// directions stays inside a convex cone containing them) bound every point of it, and the pair-direction
+// bound of the two sub-spheres holds as above.  The pair is kept iff some sub-pair passes at every level
+// down to `levels` (depth-first, early exit on the first leaf).  FP64 with 1e-7 rad / 1e-9 relative
+// slack, so it is at most more permissive than the exact predicate on the sub-pairs.
+//
+// A sub-triangle is (o_u, o_v, sigma) in units of 2^-kMaxLevels of the barycentric square with corners
+// o, o + sigma (h, 0), o + sigma (0, h); children: three with the same sigma at o, o + sigma (h/2, 0),
+// o + sigma (0, h/2) and the inverted middle one (-sigma) at o + sigma (h/2, h/2).
+constexpr int kMaxLevels = 5;
+
+struct SubB {
+  d3 c, ax;
+  double rho, sinb;
+  bool ok;  // false: no bound (keep)
+};
+
+__device__ __forceinline__ SubB sub_bound(const d3 P[3], const d3 N[3], int ou, int ov, int sg, int h) {
+  constexpr double inv = 1.0 / (1 << kMaxLevels);
+  const double u[3] = {ou * inv, (ou + sg * h) * inv, ou * inv};
+  const double v[3] = {ov * inv, ov * inv, (ov + sg * h) * inv};
+  d3 X[3], M[3];
+  SubB B;
+  B.ok = true;
+  for (int j = 0; j < 3; ++j) {
+    X[j] = P[0] + u[j] * (P[1] - P[0]) + v[j] * (P[2] - P[0]);
+    const d3 n = N[0] + u[j] * (N[1] - N[0]) + v[j] * (N[2] - N[0]);
+    const double l = norm(n);
+    if (!(l > 1e-30)) B.ok = false;
+    M[j] = (1.0 / l) * n;
+  }
+  B.c = (1.0 / 3.0) * (X[0] + X[1] + X[2]);
+  B.rho = fmax(norm(X[0] - B.c), fmax(norm(X[1] - B.c), norm(X[2] - B.c))) * (1.0 + 1e-9) + 1e-12;
+  const d3 s = M[0] + M[1] + M[2];
+  const double sl = norm(s);
+  if (!(sl > 0)) {
+    B.ok = false;
+    return B;
+  }
+  B.ax = (1.0 / sl) * s;
+  const double cmin = fmin(dot(M[0], B.ax), fmin(dot(M[1], B.ax), dot(M[2], B.ax)));
+  if (!(cmin > 1e-6)) B.ok = false;
+  B.sinb = fmin(1.0, sqrt(fmax(0.0, 1.0 - cmin * cmin)) + 1e-7);
+  return B;
+}
+
+__device__ __forceinline__ bool sphere_dir_d(d3 x, d3 c, double rho, d3& a, double& chord) {
+  const d3 d = x - c;
+  const double l = norm(d);
+  if (!(l > 0)) return false;
+  const double sn = rho / l;
+  a = (1.0 / l) * d;
+  chord = sn * (1.0 + sn * sn);
+  return sn * sn <= 0.25;
+}
+
+__device__ __forceinline__ bool node_keep_d(d3 ap, double cp, d3 an, double cn, double ep, double en, d3 nax,
+                                            double sb) {
+  const d3 A = ep * ap + en * an;
+  const double r = ep * cp + en * cn;
+  const double A2 = dot(A, A);
+  if (!(A2 > r * r * (1.0 + 1e-9))) return true;
+  const double cb = sqrt(fmax(1.0 - sb * sb, 0.0));
+  const double q = sqrt(A2 - r * r);
+  if (!(q * cb - r * sb > 0.0)) return true;
+  const d3 X = cross(A, nax);
+  const double rhs = r * cb + q * sb;
+  return !(dot(X, X) > rhs * rhs * (1.0 + 1e-9));
+}
+
+__device__ __forceinline__ bool subpair_keep(d3 x0, d3 x3, const SubB& A, const SubB& B, const double e[2][3],
+                                             int ncombo) {
+  if (!A.ok || !B.ok) return true;
+  d3 a0, a3, aAB;
+  double c0, c3, cAB;
+  if (!sphere_dir_d(x0, A.c, A.rho, a0, c0) || !sphere_dir_d(x3, B.c, B.rho, a3, c3) ||
+      !sphere_dir_d(B.c, A.c, A.rho + B.rho, aAB, cAB))
+    return true;
+  const d3 aBA = -1.0 * aAB;
+  for (int c = 0; c < ncombo; ++c)
+    if (node_keep_d(a0, c0, aAB, cAB, e[c][0], e[c][1], A.ax, A.sinb) &&
+        node_keep_d(aBA, cAB, a3, c3, e[c][1], e[c][2], B.ax, B.sinb))
+      return true;
+  return false;
+}
+
+struct SubNode {
+  int u1, v1, s1, u2, v2, s2;
+};
+
+__device__ __forceinline__ void child_of(int ou, int ov, int sg, int h, int c, int& cu, int& cv, int& cs) {
+  const int hh = h >> 1;
+  cu = ou + ((c == 1 || c == 3) ? sg * hh : 0);
+  cv = ov + ((c == 2 || c == 3) ? sg * hh : 0);
+  cs = c == 3 ? -sg : sg;
+}
+
+// 16-bit mask of the surviving child pairs of node n (size h)
+__device__ uint32_t children_mask(const d3 P1[3], const d3 N1[3], const d3 P2[3], const d3 N2[3], d3 x0, d3 x3,
+                                  const SubNode& n, int h, const double e[2][3], int ncombo) {
+  SubB A[4], B[4];
+  for (int c = 0; c < 4; ++c) {
+    int cu, cv, cs;
+    child_of(n.u1, n.v1, n.s1, h, c, cu, cv, cs);
+    A[c] = sub_bound(P1, N1, cu, cv, cs, h >> 1);
+    child_of(n.u2, n.v2, n.s2, h, c, cu, cv, cs);
+    B[c] = sub_bound(P2, N2, cu, cv, cs, h >> 1);
+  }
+  uint32_t m = 0;
+  for (int i = 0; i < 16; ++i)
+    if (subpair_keep(x0, x3, A[i >> 2], B[i & 3], e, ncombo)) m |= 1u << i;
+  return m;
+}
+
+__global__ void __launch_bounds__(128) k_refine_pairs(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                      uint64_t n, const TriRec* __restrict__ tris,
+                                                      const double* __restrict__ ep, int levels, int v1t, int v2t,
+                                                      float ef, float eb, uint8_t* __restrict__ keep) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const double* e = ep + 6ull * pq[i];
+    const d3 x0 = mk3(e[0], e[1], e[2]), x3 = mk3(e[3], e[4], e[5]);
+    d3 P1[3], N1[3], P2[3], N2[3];
+    load_tri(tris, pt[2 * i], P1, N1);
+    load_tri(tris, pt[2 * i + 1], P2, N2);
+    double ec[2][3];
+    int ncombo;
+    if (!v1t && !v2t) {
+      ec[0][0] = ec[0][1] = ec[0][2] = 1.0;
+      ncombo = 1;
+    } else {
+      for (int c = 0; c < 2; ++c) {
+        const double s = c == 0 ? ef : eb, o = c == 0 ? eb : ef;
+        ec[c][0] = s;
+        ec[c][1] = v1t ? o : s;
+        ec[c][2] = v2t ? (ec[c][1] == s ? o : s) : ec[c][1];
+      }
+      ncombo = 2;
+    }
+    SubNode stack[kMaxLevels];
+    uint32_t mask[kMaxLevels];
+    const int H = 1 << kMaxLevels;
+    stack[0] = {0, 0, 1, 0, 0, 1};
+    mask[0] = children_mask(P1, N1, P2, N2, x0, x3, stack[0], H, ec, ncombo);
+    int l = 0;
+    bool kept = false;
+    while (true) {
+      if (mask[l] == 0) {
+        if (l == 0) break;
+        --l;
+        continue;
+      }
+      const int c = __ffs(mask[l]) - 1;
+      mask[l] &= mask[l] - 1;
+      if (l + 1 >= levels) {
+        kept = true;
+        break;
+      }
+      const int h = H >> l;
+      SubNode ch;
+      child_of(stack[l].u1, stack[l].v1, stack[l].s1, h, c >> 2, ch.u1, ch.v1, ch.s1);
+      child_of(stack[l].u2, stack[l].v2, stack[l].s2, h, c & 3, ch.u2, ch.v2, ch.s2);
+      stack[l + 1] = ch;
+      mask[l + 1] = children_mask(P1, N1, P2, N2, x0, x3, ch, h >> 1, ec, ncombo);
+      ++l;
+    }
+    keep[i] = kept ? 1 : 0;
+  }
+}
+
+void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
+                         int levels, int v1t, int v2t, uint8_t* keep, int nsm, cudaStream_t st) {
+  if (!n) return;
+  if (levels > kMaxLevels) levels = kMaxLevels;
+  const uint64_t want = (n + 127) / 128, cap = (uint64_t)nsm * 16;
+  k_refine_pairs<<<(int)(want < cap ? want : cap), 128, 0, st>>>(pq, pt, n, M.tris, ep, levels, v1t, v2t,
+                                                                  M.eta_front, M.eta_back, keep);
+}
+
 }  // namespace spoly

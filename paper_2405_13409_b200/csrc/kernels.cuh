@@ -31,12 +31,23 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
                      const SolSink& S, const JobSink& J, int nsm, cudaStream_t st);
 
 // solve_k2.cu
+// two-bounce scratch: per-pair system records (chunked), path list, counters
+struct K2Scratch {
+  double* rec;
+  uint64_t rec_cap;  // doubles
+  uint32_t* plist;   // >= rec_cap / stride entries
+  unsigned long long* ctr;  // 4
+  int launches;
+};
+uint64_t k2_record_bytes(int v1t, int v2t);
 void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, int nsm,
-                     cudaStream_t st);
+                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
+                     int nsm, cudaStream_t st);
 void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, int v1t, int v2t,
                        uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
                        cudaStream_t st);
+void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
+                         int levels, int v1t, int v2t, uint8_t* keep, int nsm, cudaStream_t st);
 void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 
 // reduce.cu

@@ -1,150 +1,27 @@
 // Two-bounce solve, chains "RR" (Eq. 23), "RT", "TR" and "TT" (Eqs. 13-20; square form at a refracting x_2,
-// product form at a reflecting one; Table 3 rows), one
-// (query, triangle pair) per thread, FP64, polynomial grids and the Bezout matrix in thread-local memory.
+// product form at a reflecting one; Table 3 rows).  One (query, triangle pair) per group
+// of G lanes (G = 16 for RR, whose Bezout order is <= 15; 32 otherwise), FP64:
 //
 //   coefficient phase : rational coordinate mapping u_2 = (u~, v~)/kappa (Eqs. 13-16) of the scaled
 //                       direction d~_1 (Eq. 17 reflection; Eqs. 18-20 refraction with the piecewise rational
-//                       sqrt surrogate, reading R8), then a = Eq. 6 at x_2 and b = Eq. 12 (RR) / Eq. 9 (TT),
-//                       denominators cleared; normalise + numerical u-degree truncation (R6)
-//   elimination       : Bezout matrix of Eq. 24 evaluated numerically at v by the Chionh recurrence
-//                       B_ij = B_{i-1,j+1} + a_i b_{j+1} - b_i a_{j+1} (exact consequence of Eq. 24)
-//   roots             : sign of det R(v_j) at v_j = j/100 by Gaussian elimination with partial pivoting,
-//                       10 bisections per sign-changing piece
-//   path phase        : u-roots of a(., v*) on [-0.1, 1.1], mapping to u_2, raw admission (theta_admit),
-//                       <= 3 Newton steps on the exact shooting residual, final Eq. 3
-//                       validation, sides, flags, contribution I / J (J by central differences of the
+//                       sqrt surrogate, reading R8), then a = Eq. 6 at x_2 and b = Eq. 12 (product form) /
+//                       Eq. 9 (square form), denominators cleared; every bivariate product is computed by
+//                       the group in shared memory (wpoly.cuh), then normalised + truncated (R6)
+//   elimination       : Bezout matrix of Eq. 24 at v, columns by the Chionh recurrence across lanes
+//   roots             : sign of det R(v_j) at v_j = j/100 by register-resident Gaussian elimination with
+//                       partial pivoting (one row per lane), 10 bisections per sign-changing piece
+//
+//   path phase        : (lane 0) u-roots of a(., v*) on [-0.1, 1.1], mapping to u_2, raw admission
+//                       (theta_admit), <= 3 Newton steps on the exact shooting residual, final
+//                       Eq. 3 validation, sides, flags, contribution I / J (J by central differences of the
 //                       light-side trace, Richardson), emission.
-// This is the correctness-first round-1 kernel; the warp-cooperative version is future work.
 #include "kernels.cuh"
 #include "poly_dev.cuh"
+#include "wpoly.cuh"
+
+#include <algorithm>
 
 namespace spoly {
-
-// ------------------------------------------------------------------ dense bivariate polynomials
-template <int D>
-struct BP {
-  static constexpr int S = D + 1;
-  double c[S * S];  // c[i*S + j]: coefficient of u^i v^j, only i + j <= deg used
-  int deg;
-};
-
-template <int D>
-__device__ __forceinline__ void bp_zero(BP<D>& p, int deg) {
-  p.deg = deg;
-  for (int i = 0; i < BP<D>::S * BP<D>::S; ++i) p.c[i] = 0.0;
-}
-template <int D>
-__device__ __forceinline__ void bp_linear(BP<D>& p, double a, double b, double c) {
-  bp_zero(p, 1);
-  p.c[0] = a;
-  p.c[BP<D>::S] = b;
-  p.c[1] = c;
-}
-template <int D>
-__device__ __forceinline__ void bp_const(BP<D>& p, double a) {
-  bp_zero(p, 0);
-  p.c[0] = a;
-}
-// c += s * a * b
-template <int DA, int DB, int DC>
-__device__ void bp_mul_acc(const BP<DA>& a, const BP<DB>& b, double s, BP<DC>& c) {
-  const int SA = BP<DA>::S, SB = BP<DB>::S, SC = BP<DC>::S;
-  if (a.deg + b.deg > c.deg) c.deg = a.deg + b.deg;
-  for (int i = 0; i <= a.deg; ++i)
-    for (int j = 0; i + j <= a.deg; ++j) {
-      const double x = s * a.c[i * SA + j];
-      if (x == 0.0) continue;
-      for (int k = 0; k <= b.deg; ++k)
-        for (int l = 0; k + l <= b.deg; ++l) c.c[(i + k) * SC + (j + l)] = fma(x, b.c[k * SB + l], c.c[(i + k) * SC + (j + l)]);
-    }
-}
-// c += s * a
-template <int DA, int DC>
-__device__ void bp_add(const BP<DA>& a, double s, BP<DC>& c) {
-  const int SA = BP<DA>::S, SC = BP<DC>::S;
-  if (a.deg > c.deg) c.deg = a.deg;
-  for (int i = 0; i <= a.deg; ++i)
-    for (int j = 0; i + j <= a.deg; ++j) c.c[i * SC + j] = fma(s, a.c[i * SA + j], c.c[i * SC + j]);
-}
-template <int D>
-__device__ double bp_eval(const BP<D>& p, double u, double v) {
-  const int S = BP<D>::S;
-  double acc = 0.0;
-  for (int i = p.deg; i >= 0; --i) {
-    double s = 0.0;
-    for (int j = p.deg - i; j >= 0; --j) s = fma(s, v, p.c[i * S + j]);
-    acc = fma(acc, u, s);
-  }
-  return acc;
-}
-template <int D>
-__device__ void bp_slices(const BP<D>& p, int du, double v, double* out) {  // a_i(v), i = 0..du
-  const int S = BP<D>::S;
-  for (int i = 0; i <= du; ++i) {
-    double s = 0.0;
-    if (i <= p.deg)
-      for (int j = p.deg - i; j >= 0; --j) s = fma(s, v, p.c[i * S + j]);
-    out[i] = s;
-  }
-}
-
-template <int D>
-struct BV {
-  BP<D> x, y, z;
-};
-// vector helpers: BV<DC> r = a . b etc.
-template <int DA, int DB, int DC>
-__device__ void bv_dot_acc(const BV<DA>& a, const BV<DB>& b, double s, BP<DC>& c) {
-  bp_mul_acc(a.x, b.x, s, c);
-  bp_mul_acc(a.y, b.y, s, c);
-  bp_mul_acc(a.z, b.z, s, c);
-}
-template <int DA, int DC>
-__device__ void bv_dotc_acc(const BV<DA>& a, d3 b, double s, BP<DC>& c) {
-  bp_add(a.x, s * b.x, c);
-  bp_add(a.y, s * b.y, c);
-  bp_add(a.z, s * b.z, c);
-}
-// (a x b) for polynomial a and constant b
-template <int DA, int DC>
-__device__ void bv_cross_c(const BV<DA>& a, d3 b, BV<DC>& r) {
-  bp_zero(r.x, a.x.deg);
-  bp_zero(r.y, a.x.deg);
-  bp_zero(r.z, a.x.deg);
-  bp_add(a.y, b.z, r.x); bp_add(a.z, -b.y, r.x);
-  bp_add(a.z, b.x, r.y); bp_add(a.x, -b.z, r.y);
-  bp_add(a.x, b.y, r.z); bp_add(a.y, -b.x, r.z);
-}
-// r = a x b, both polynomial
-template <int DA, int DB, int DC>
-__device__ void bv_cross(const BV<DA>& a, const BV<DB>& b, BV<DC>& r) {
-  const int d = a.x.deg + b.x.deg;
-  bp_zero(r.x, d);
-  bp_zero(r.y, d);
-  bp_zero(r.z, d);
-  bp_mul_acc(a.y, b.z, 1.0, r.x); bp_mul_acc(a.z, b.y, -1.0, r.x);
-  bp_mul_acc(a.z, b.x, 1.0, r.y); bp_mul_acc(a.x, b.z, -1.0, r.y);
-  bp_mul_acc(a.x, b.y, 1.0, r.z); bp_mul_acc(a.y, b.x, -1.0, r.z);
-}
-
-// ------------------------------------------------------------------ system
-// chain X1 X2 with X = R (reflection) / T (refraction): V1T = vertex 1 refracts, V2T = vertex 2 refracts
-template <bool V1T, bool V2T>
-struct Sys2 {
-  static constexpr int DK = V1T ? 7 : 3;  // deg kappa = deg d~_1 (Eq. 17: 3; Eqs. 19-20 cleared: 7)
-  static constexpr int DU = DK + 1;       // deg u~, v~
-  static constexpr int DA = 2 * DK + 3;   // deg a: 9 (R.), 17 (T.)
-  // deg b: product form (d~.N2)(D2.T2)+..: DK+DU+2DU; square form D2^2 P^2: 2DU + 2(DK+DU)
-  static constexpr int DB = V2T ? 2 * DU + 2 * (DK + DU) : (DK + DU) + 2 * DU;  // RR 15, RT 22, TR 31, TT 46
-  BP<DA> a;
-  BP<DB> b;
-  BP<DU> U, V;
-  BP<DK> K;
-  double eta0, eta1, eta2;
-  bool relabel;
-  uint32_t flags;
-  int da, db, n;
-};
 
 struct Tri2 {
   d3 p[3], n[3];
@@ -165,10 +42,34 @@ __constant__ double c_sqrt_tab[6][5] = {
     {0.21636853563098274, 0.68268233146982271, 0.20527897991137517, 1.5904325277264706, 0.82650456712266585},
     {0.68268233146982271, 1, 0.30276242425651556, 1.0984677499357838, 0.40129928835931156}};
 
+// polynomial degrees of the chain X1 X2 (X = R reflection / T refraction)
 template <bool V1T, bool V2T>
-__device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, const SolveParams& prm,
-                              Sys2<V1T, V2T>& S) {
-  using Sy = Sys2<V1T, V2T>;
+struct Deg2 {
+  static constexpr int DK = V1T ? 7 : 3;  // deg kappa = deg d~_1 (Eq. 17: 3; Eqs. 19-20 cleared: 7)
+  static constexpr int DU = DK + 1;       // deg u~, v~
+  static constexpr int DA = 2 * DK + 3;   // deg a: 9 (R.), 17 (T.)
+  // deg b: product form (d~.N2)(D2.T2)+..: DK+DU+2DU; square form D2^2 P^2: 2DU + 2(DK+DU)
+  static constexpr int DB = V2T ? 2 * DU + 2 * (DK + DU) : (DK + DU) + 2 * DU;  // RR 15, RT 22, TR 31, TT 46
+  static constexpr int G = (DB <= 15) ? 16 : 32;                               // lanes per system
+  // shared-memory arena per group (doubles): persistent a, b, U, V, K + the build temporaries (peak) +
+  // the v-root list; the n > 32 determinant scratch reuses the temporaries (TT only)
+  static constexpr int ARENA = (!V1T && !V2T) ? 1024 : (!V1T ? 1536 : (!V2T ? 3072 : 3712));
+};
+
+struct Sys2w {
+  WP a, b, U, V, K;
+  double eta0, eta1, eta2;
+  bool relabel;
+  uint32_t flags;
+  int da, db, n;
+};
+
+// coefficient phase, group-cooperative (same construction as the oracle's)
+template <bool V1T, bool V2T, int G>
+__device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in,
+                        const SolveParams& prm, Sys2w& S) {
+  using D = Deg2<V1T, V2T>;
+  constexpr int DK = D::DK, DU = D::DU;
   S.flags = 0;
   const bool front0 = dot(x0 - T1.p[0], T1.g()) > 0;
   S.eta0 = front0 ? prm.eta_front : prm.eta_back;
@@ -196,208 +97,162 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
     T2.p[1] = T2in.p[2]; T2.p[2] = T2in.p[1];
     T2.n[1] = T2in.n[2]; T2.n[2] = T2in.n[1];
   }
+  // persistent polynomials first
+  S.a = ar.poly(D::DA);
+  S.b = ar.poly(D::DB);
+  S.U = ar.poly(DU);
+  S.V = ar.poly(DU);
+  S.K = ar.poly(DK);
+  const int mark = ar.top;
   // X1 = p0 + u e1 + v e2, N1 = n0 + u m1 + v m2, D0 = X1 - x0   (Eqs. 1-2)
   const d3 e1 = T1.e1(), e2 = T1.e2(), m1 = T1.n[1] - T1.n[0], m2 = T1.n[2] - T1.n[0];
-  BV<1> X1, N1, D0;
-  bp_linear(X1.x, T1.p[0].x, e1.x, e2.x); bp_linear(X1.y, T1.p[0].y, e1.y, e2.y); bp_linear(X1.z, T1.p[0].z, e1.z, e2.z);
-  bp_linear(N1.x, T1.n[0].x, m1.x, m2.x); bp_linear(N1.y, T1.n[0].y, m1.y, m2.y); bp_linear(N1.z, T1.n[0].z, m1.z, m2.z);
-  const d3 q = T1.p[0] - x0;
-  bp_linear(D0.x, q.x, e1.x, e2.x); bp_linear(D0.y, q.y, e1.y, e2.y); bp_linear(D0.z, q.z, e1.z, e2.z);
-  constexpr int DK = Sy::DK;
-  BV<DK> Dt;
-  {
-    BP<2> dn, nn;
-    bp_zero(dn, 2);
-    bp_zero(nn, 2);
-    bv_dot_acc(D0, N1, 1.0, dn);
-    bv_dot_acc(N1, N1, 1.0, nn);
-    bp_zero(Dt.x, DK); bp_zero(Dt.y, DK); bp_zero(Dt.z, DK);
-    if (!V1T) {
-      // Eq. 17: d~ = -2 (d0 . n) n + d0 n^2
-      bp_mul_acc(dn, N1.x, -2.0, Dt.x); bp_mul_acc(dn, N1.y, -2.0, Dt.y); bp_mul_acc(dn, N1.z, -2.0, Dt.z);
-      bp_mul_acc(nn, D0.x, 1.0, Dt.x); bp_mul_acc(nn, D0.y, 1.0, Dt.y); bp_mul_acc(nn, D0.z, 1.0, Dt.z);
-    } else {
-      // Eqs. 18-20 with sqrt(beta) ~ sqrt(s) (c0 s + c1 beta) / (s + d1 beta), denominator cleared
-      const double ep = S.eta0 / S.eta1;
-      double nmax = 0, dmax = 0;
-      for (int j = 0; j < 3; ++j) {
-        nmax = fmax(nmax, dot(T1.n[j], T1.n[j]));
-        dmax = fmax(dmax, dot(T1.p[j] - x0, T1.p[j] - x0));
-      }
-      const double s = nmax * dmax;
-      const d3 ncen = T1.N(1.0 / 3.0, 1.0 / 3.0), dcen = T1.X(1.0 / 3.0, 1.0 / 3.0) - x0;
-      const double cnn = dot(ncen, ncen), cdd = dot(dcen, dcen), cdn = dot(dcen, ncen);
-      const double cbeta = cnn * cdd - ep * ep * (cnn * cdd - cdn * cdn);
-      const double xb = fmin(1.0, fmax(0.0, cbeta / s));
-      int piece = 5;
-      for (int i = 5; i >= 0; --i)
-        if (xb <= c_sqrt_tab[i][1]) piece = i;
-      const double sigma = cdn < 0 ? 1.0 : -1.0;
-      BP<2> dd;
-      bp_zero(dd, 2);
-      bv_dot_acc(D0, D0, 1.0, dd);
-      BP<4> beta, nd, dn2;
-      bp_zero(beta, 4);
-      bp_zero(nd, 4);
-      bp_zero(dn2, 4);
-      bp_mul_acc(nn, dd, 1.0, nd);
-      bp_mul_acc(dn, dn, 1.0, dn2);
-      bp_add(nd, 1.0 - ep * ep, beta);  // beta = nn dd - ep^2 (nn dd - dn^2)   (Eq. 19)
-      bp_add(dn2, ep * ep, beta);
-      BP<4> den, sq;
-      bp_zero(den, 4);
-      bp_zero(sq, 4);
-      bp_add(beta, c_sqrt_tab[piece][4], den);
-      den.c[0] += s;
-      bp_add(beta, c_sqrt_tab[piece][3], sq);
-      sq.c[0] += c_sqrt_tab[piece][2] * s;
-      // tang = nn D0 - dn N1 (deg 3)
-      BV<3> tang;
-      bp_zero(tang.x, 3); bp_zero(tang.y, 3); bp_zero(tang.z, 3);
-      bp_mul_acc(nn, D0.x, 1.0, tang.x); bp_mul_acc(dn, N1.x, -1.0, tang.x);
-      bp_mul_acc(nn, D0.y, 1.0, tang.y); bp_mul_acc(dn, N1.y, -1.0, tang.y);
-      bp_mul_acc(nn, D0.z, 1.0, tang.z); bp_mul_acc(dn, N1.z, -1.0, tang.z);
-      const double k2 = -sigma * sqrt(s);
-      bp_mul_acc(den, tang.x, ep, Dt.x); bp_mul_acc(sq, N1.x, k2, Dt.x);
-      bp_mul_acc(den, tang.y, ep, Dt.y); bp_mul_acc(sq, N1.y, k2, Dt.y);
-      bp_mul_acc(den, tang.z, ep, Dt.z); bp_mul_acc(sq, N1.z, k2, Dt.z);
+  WV X1 = ar.vec(1), N1 = ar.vec(1), D0 = ar.vec(1);
+  wlinear3(g, X1, T1.p[0], e1, e2);
+  wlinear3(g, N1, T1.n[0], m1, m2);
+  wlinear3(g, D0, T1.p[0] - x0, e1, e2);
+  WP dn = ar.poly(2), nn = ar.poly(2);
+  wdot(g, dn, D0, N1, 1.0, false);
+  wdot(g, nn, N1, N1, 1.0, false);
+  WV Dt = ar.vec(DK);
+  if (!V1T) {
+    // Eq. 17: d~ = -2 (d0 . n) n + d0 n^2
+    wmul2(g, Dt.x, dn, N1.x, -2.0, nn, D0.x, 1.0, false);
+    wmul2(g, Dt.y, dn, N1.y, -2.0, nn, D0.y, 1.0, false);
+    wmul2(g, Dt.z, dn, N1.z, -2.0, nn, D0.z, 1.0, false);
+  } else {
+    // Eqs. 18-20 with sqrt(beta) ~ sqrt(s) (c0 s + c1 beta) / (s + d1 beta), denominator cleared
+    const double ep = S.eta0 / S.eta1;
+    double nmax = 0, dmax = 0;
+    for (int j = 0; j < 3; ++j) {
+      nmax = fmax(nmax, dot(T1.n[j], T1.n[j]));
+      dmax = fmax(dmax, dot(T1.p[j] - x0, T1.p[j] - x0));
     }
+    const double s = nmax * dmax;
+    const d3 ncen = T1.N(1.0 / 3.0, 1.0 / 3.0), dcen = T1.X(1.0 / 3.0, 1.0 / 3.0) - x0;
+    const double cnn = dot(ncen, ncen), cdd = dot(dcen, dcen), cdn = dot(dcen, ncen);
+    const double cbeta = cnn * cdd - ep * ep * (cnn * cdd - cdn * cdn);
+    const double xb = fmin(1.0, fmax(0.0, cbeta / s));
+    int piece = 5;
+    for (int i = 5; i >= 0; --i)
+      if (xb <= c_sqrt_tab[i][1]) piece = i;
+    const double sigma = cdn < 0 ? 1.0 : -1.0;
+    WP dd = ar.poly(2), nd = ar.poly(4), dn2 = ar.poly(4), beta = ar.poly(4), den = ar.poly(4), sq = ar.poly(4);
+    wdot(g, dd, D0, D0, 1.0, false);
+    wmul1(g, nd, nn, dd, 1.0, false);
+    wmul1(g, dn2, dn, dn, 1.0, false);
+    wlin2(g, beta, nd, 1.0 - ep * ep, dn2, ep * ep, false);  // beta = nn dd - ep^2 (nn dd - dn^2)  (Eq. 19)
+    wlin1(g, den, beta, c_sqrt_tab[piece][4], false);
+    wadd0(g, den, s);
+    wlin1(g, sq, beta, c_sqrt_tab[piece][3], false);
+    wadd0(g, sq, c_sqrt_tab[piece][2] * s);
+    WV tang = ar.vec(3);  // nn D0 - dn N1
+    wmul2(g, tang.x, nn, D0.x, 1.0, dn, N1.x, -1.0, false);
+    wmul2(g, tang.y, nn, D0.y, 1.0, dn, N1.y, -1.0, false);
+    wmul2(g, tang.z, nn, D0.z, 1.0, dn, N1.z, -1.0, false);
+    const double k2 = -sigma * sqrt(s);
+    wmul2(g, Dt.x, den, tang.x, ep, sq, N1.x, k2, false);
+    wmul2(g, Dt.y, den, tang.y, ep, sq, N1.y, k2, false);
+    wmul2(g, Dt.z, den, tang.z, ep, sq, N1.z, k2, false);
   }
   // rational coordinate mapping onto T_2 (Eqs. 13-16)
   const d3 f1 = T2.e1(), f2 = T2.e2(), r0 = T2.n[0], g1 = T2.n[1] - T2.n[0], g2 = T2.n[2] - T2.n[0];
-  BV<1> Sv;  // x_1 - p_{2,0}
-  const d3 sq0 = T1.p[0] - T2.p[0];
-  bp_linear(Sv.x, sq0.x, e1.x, e2.x); bp_linear(Sv.y, sq0.y, e1.y, e2.y); bp_linear(Sv.z, sq0.z, e1.z, e2.z);
-  BV<DK> Dxf2;
-  bv_cross_c(Dt, f2, Dxf2);
-  constexpr int DU = Sy::DU;
-  bp_zero(S.U, DU);
-  bv_dot_acc(Dxf2, Sv, 1.0, S.U);  // u~ = (d~ x e22) . (x1 - p20)
-  bp_zero(S.K, DK);
-  bv_dotc_acc(Dxf2, f1, 1.0, S.K);  // kappa = (d~ x e22) . e21
-  {
-    // v~ = ((x1 - p20) x e21) . d~
-    BV<1> Sxf1;
-    bv_cross_c(Sv, f1, Sxf1);
-    bp_zero(S.V, DU);
-    bv_dot_acc(Sxf1, Dt, 1.0, S.V);
-  }
+  WV Sv = ar.vec(1);  // x_1 - p_{2,0}
+  wlinear3(g, Sv, T1.p[0] - T2.p[0], e1, e2);
+  WV Dxf2 = ar.vec(DK);
+  wcross_c(g, Dxf2, Dt, f2);
+  wdot(g, S.U, Dxf2, Sv, 1.0, false);                                 // u~ = (d~ x e22) . (x1 - p20)
+  wlin3(g, S.K, Dxf2.x, f1.x, Dxf2.y, f1.y, Dxf2.z, f1.z, false);     // kappa = (d~ x e22) . e21
+  WV Sxf1 = ar.vec(1);
+  wcross_c(g, Sxf1, Sv, f1);
+  wdot(g, S.V, Sxf1, Dt, 1.0, false);                                 // v~ = ((x1 - p20) x e21) . d~
   // kappa x_2 and kappa n_2
-  BV<DU> X2, N2;
-  bp_zero(X2.x, DU); bp_zero(X2.y, DU); bp_zero(X2.z, DU);
-  bp_zero(N2.x, DU); bp_zero(N2.y, DU); bp_zero(N2.z, DU);
-  bp_add(S.K, T2.p[0].x, X2.x); bp_add(S.U, f1.x, X2.x); bp_add(S.V, f2.x, X2.x);
-  bp_add(S.K, T2.p[0].y, X2.y); bp_add(S.U, f1.y, X2.y); bp_add(S.V, f2.y, X2.y);
-  bp_add(S.K, T2.p[0].z, X2.z); bp_add(S.U, f1.z, X2.z); bp_add(S.V, f2.z, X2.z);
-  bp_add(S.K, r0.x, N2.x); bp_add(S.U, g1.x, N2.x); bp_add(S.V, g2.x, N2.x);
-  bp_add(S.K, r0.y, N2.y); bp_add(S.U, g1.y, N2.y); bp_add(S.V, g2.y, N2.y);
-  bp_add(S.K, r0.z, N2.z); bp_add(S.U, g1.z, N2.z); bp_add(S.V, g2.z, N2.z);
+  WV X2 = ar.vec(DU), N2 = ar.vec(DU);
+  wlin3(g, X2.x, S.K, T2.p[0].x, S.U, f1.x, S.V, f2.x, false);
+  wlin3(g, X2.y, S.K, T2.p[0].y, S.U, f1.y, S.V, f2.y, false);
+  wlin3(g, X2.z, S.K, T2.p[0].z, S.U, f1.z, S.V, f2.z, false);
+  wlin3(g, N2.x, S.K, r0.x, S.U, g1.x, S.V, g2.x, false);
+  wlin3(g, N2.y, S.K, r0.y, S.U, g1.y, S.V, g2.y, false);
+  wlin3(g, N2.z, S.K, r0.z, S.U, g1.z, S.V, g2.z, false);
   // a = ((X2 - K X1) x (x3 - X1)) . N2   (Eq. 6 at x_2, Eq. 23 first line)
   {
-    BV<DU> W;  // X2 - K X1 (deg DK + 1)
-    bp_zero(W.x, DU); bp_zero(W.y, DU); bp_zero(W.z, DU);
-    bp_add(X2.x, 1.0, W.x); bp_mul_acc(S.K, X1.x, -1.0, W.x);
-    bp_add(X2.y, 1.0, W.y); bp_mul_acc(S.K, X1.y, -1.0, W.y);
-    bp_add(X2.z, 1.0, W.z); bp_mul_acc(S.K, X1.z, -1.0, W.z);
-    BV<1> Y;  // x3 - X1
-    const d3 y0 = x3 - T1.p[0];
-    bp_linear(Y.x, y0.x, -e1.x, -e2.x); bp_linear(Y.y, y0.y, -e1.y, -e2.y); bp_linear(Y.z, y0.z, -e1.z, -e2.z);
-    BV<DU + 1> C;
-    bv_cross(W, Y, C);
-    bp_zero(S.a, Sy::DA);
-    bv_dot_acc(C, N2, 1.0, S.a);
+    const int m2 = ar.top;
+    WV W = ar.vec(DU);
+    wlin1(g, W.x, X2.x, 1.0, false); wmul1(g, W.x, S.K, X1.x, -1.0, true);
+    wlin1(g, W.y, X2.y, 1.0, false); wmul1(g, W.y, S.K, X1.y, -1.0, true);
+    wlin1(g, W.z, X2.z, 1.0, false); wmul1(g, W.z, S.K, X1.z, -1.0, true);
+    WV Y = ar.vec(1);
+    wlinear3(g, Y, x3 - T1.p[0], -1.0 * e1, -1.0 * e2);
+    WV Cc = ar.vec(DU + 1);
+    wcross(g, Cc, W, Y);
+    wdot(g, S.a, Cc, N2, 1.0, false);
+    ar.top = m2;
   }
   // D2 = K x3 - X2 (kappa d_2)
-  BV<DU> D2;
-  bp_zero(D2.x, DU); bp_zero(D2.y, DU); bp_zero(D2.z, DU);
-  bp_add(S.K, x3.x, D2.x); bp_add(X2.x, -1.0, D2.x);
-  bp_add(S.K, x3.y, D2.y); bp_add(X2.y, -1.0, D2.y);
-  bp_add(S.K, x3.z, D2.z); bp_add(X2.z, -1.0, D2.z);
-  bp_zero(S.b, Sy::DB);
+  WV D2 = ar.vec(DU);
+  wlin2(g, D2.x, S.K, x3.x, X2.x, -1.0, false);
+  wlin2(g, D2.y, S.K, x3.y, X2.y, -1.0, false);
+  wlin2(g, D2.z, S.K, x3.z, X2.z, -1.0, false);
   if (!V2T) {
     // b = (d~.N2)(D2.T2) + (d~.T2)(D2.N2), T2 = N2 x e21   (Eq. 12 with d~_1, Eq. 23)
-    BV<DU> Tt;
-    bv_cross_c(N2, f1, Tt);
-    BP<DK + DU> p1, p3;
-    BP<2 * DU> p2, p4;
-    bp_zero(p1, DK + DU); bp_zero(p2, 2 * DU); bp_zero(p3, DK + DU); bp_zero(p4, 2 * DU);
-    bv_dot_acc(Dt, N2, 1.0, p1);
-    bv_dot_acc(D2, Tt, 1.0, p2);
-    bv_dot_acc(Dt, Tt, 1.0, p3);
-    bv_dot_acc(D2, N2, 1.0, p4);
-    bp_mul_acc(p1, p2, 1.0, S.b);
-    bp_mul_acc(p3, p4, 1.0, S.b);
+    WV Tt = ar.vec(DU);
+    wcross_c(g, Tt, N2, f1);
+    WP p1 = ar.poly(DK + DU), p2 = ar.poly(2 * DU), p3 = ar.poly(DK + DU), p4 = ar.poly(2 * DU);
+    wdot(g, p1, Dt, N2, 1.0, false);
+    wdot(g, p2, D2, Tt, 1.0, false);
+    wdot(g, p3, Dt, Tt, 1.0, false);
+    wdot(g, p4, D2, N2, 1.0, false);
+    wmul2(g, S.b, p1, p2, 1.0, p3, p4, 1.0, false);
   } else {
-    // b = eta1^2 D2^2 ((d~ x N2).l)^2 - eta2^2 d~^2 ((D2 x N2).l)^2   (Eq. 9 at x_2)
-    BP<DK + DU> P;
-    BP<2 * DU> Q;
-    {
-      BV<DK + DU> C;
-      bv_cross(Dt, N2, C);
-      bp_zero(P, DK + DU);
-      bv_dotc_acc(C, ell, 1.0, P);
-    }
-    {
-      BV<2 * DU> C;
-      bv_cross(D2, N2, C);
-      bp_zero(Q, 2 * DU);
-      bv_dotc_acc(C, ell, 1.0, Q);
-    }
-    BP<2 * DU> d22;
-    bp_zero(d22, 2 * DU);
-    bv_dot_acc(D2, D2, 1.0, d22);
-    BP<2 * DK> dt2;
-    bp_zero(dt2, 2 * DK);
-    bv_dot_acc(Dt, Dt, 1.0, dt2);
-    {
-      BP<2 * (DK + DU)> P2;
-      bp_zero(P2, 2 * (DK + DU));
-      bp_mul_acc(P, P, 1.0, P2);
-      bp_mul_acc(d22, P2, S.eta1 * S.eta1, S.b);
-    }
-    {
-      BP<4 * DU> Q2;
-      bp_zero(Q2, 4 * DU);
-      bp_mul_acc(Q, Q, 1.0, Q2);
-      bp_mul_acc(dt2, Q2, -S.eta2 * S.eta2, S.b);
-    }
+    // b = eta1^2 D2^2 ((d~ x N2).l)^2 - eta2^2 d~^2 ((D2 x N2).l)^2   (Eq. 9 at x_2); (A x N2).l = A.(N2 x l)
+    WV Nl = ar.vec(DU);
+    wcross_c(g, Nl, N2, ell);
+    WP P = ar.poly(DK + DU), Q = ar.poly(2 * DU), d22 = ar.poly(2 * DU), dt2 = ar.poly(2 * DK);
+    wdot(g, P, Dt, Nl, 1.0, false);
+    wdot(g, Q, D2, Nl, 1.0, false);
+    wdot(g, d22, D2, D2, 1.0, false);
+    wdot(g, dt2, Dt, Dt, 1.0, false);
+    WP PQ2 = ar.poly(4 * DU);
+    WP P2{PQ2.c, 2 * (DK + DU)};
+    wmul1(g, P2, P, P, 1.0, false);
+    wmul1(g, S.b, d22, P2, S.eta1 * S.eta1, false);
+    wmul1(g, PQ2, Q, Q, 1.0, false);
+    wmul1(g, S.b, dt2, PQ2, -S.eta2 * S.eta2, true);
+  }
+  ar.top = mark;
+  if (ar.overflow) {
+    S.flags |= SPOLY_FLAG_DEGENERATE;
+    return false;
   }
   // normalise and truncate (R6)
+  const int na = tri_n(S.a.d), nb = tri_n(S.b.d);
   double ma = 0, mb = 0;
-  const int SA = BP<Sy::DA>::S, SB = BP<Sy::DB>::S;
-  for (int i = 0; i <= S.a.deg; ++i)
-    for (int j = 0; i + j <= S.a.deg; ++j) ma = fmax(ma, fabs(S.a.c[i * SA + j]));
-  for (int i = 0; i <= S.b.deg; ++i)
-    for (int j = 0; i + j <= S.b.deg; ++j) mb = fmax(mb, fabs(S.b.c[i * SB + j]));
+  for (int i = g.lane; i < na; i += G) ma = fmax(ma, fabs(S.a.c[i]));
+  for (int i = g.lane; i < nb; i += G) mb = fmax(mb, fabs(S.b.c[i]));
+  ma = g.max_(ma);
+  mb = g.max_(mb);
   if (!(ma > 0) || !(mb > 0)) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
   }
   const double ia = 1.0 / ma, ib = 1.0 / mb;
-  S.da = 0;
-  S.db = 0;
-  double f = 1.0;
-  for (int i = 0; i <= S.a.deg; ++i, f *= 1.1) {
-    double m = 0;
-    for (int j = 0; i + j <= S.a.deg; ++j) {
-      S.a.c[i * SA + j] *= ia;
-      m = fmax(m, fabs(S.a.c[i * SA + j]));
-    }
-    if (m * f > prm.tau_trunc) S.da = i;
+  for (int i = g.lane; i < na; i += G) S.a.c[i] *= ia;
+  for (int i = g.lane; i < nb; i += G) S.b.c[i] *= ib;
+  g.sync();
+  int da = 0, db = 0;
+  for (int i = g.lane; i <= S.a.d; i += G) {
+    double m = 0, f = 1.0;
+    for (int j = 0; j <= S.a.d - i; ++j) m = fmax(m, fabs(S.a.c[poff(S.a.d, i) + j]));
+    for (int t = 0; t < i; ++t) f *= 1.1;
+    if (m * f > prm.tau_trunc) da = max(da, i);
   }
-  f = 1.0;
-  for (int i = 0; i <= S.b.deg; ++i, f *= 1.1) {
-    double m = 0;
-    for (int j = 0; i + j <= S.b.deg; ++j) {
-      S.b.c[i * SB + j] *= ib;
-      m = fmax(m, fabs(S.b.c[i * SB + j]));
-    }
-    if (m * f > prm.tau_trunc) S.db = i;
+  for (int i = g.lane; i <= S.b.d; i += G) {
+    double m = 0, f = 1.0;
+    for (int j = 0; j <= S.b.d - i; ++j) m = fmax(m, fabs(S.b.c[poff(S.b.d, i) + j]));
+    for (int t = 0; t < i; ++t) f *= 1.1;
+    if (m * f > prm.tau_trunc) db = max(db, i);
   }
-  for (int i = S.da + 1; i <= S.a.deg; ++i)
-    for (int j = 0; i + j <= S.a.deg; ++j) S.a.c[i * SA + j] = 0.0;
-  for (int i = S.db + 1; i <= S.b.deg; ++i)
-    for (int j = 0; i + j <= S.b.deg; ++j) S.b.c[i * SB + j] = 0.0;
+  S.da = g.imax(da);
+  S.db = g.imax(db);
   S.n = max(S.da, S.db);
   if (S.n == 0) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
@@ -406,59 +261,6 @@ __device__ bool build_system2(d3 x0, d3 x3, const Tri2& T1, const Tri2& T2in, co
   return true;
 }
 
-// det R(v) (Eq. 24) by the Chionh recurrence + Gaussian elimination with partial pivoting (max |.|,
-// lowest index on ties); returns the sign and log|det|
-template <bool V1T, bool V2T>
-__device__ int det_sign_at(const Sys2<V1T, V2T>& S, double v, double* logabs, double* M /* n*n scratch */) {
-  constexpr int NS = Sys2<V1T, V2T>::DB + 2;
-  double as[NS], bs[NS];
-  const int n = S.n;
-  bp_slices(S.a, n, v, as);
-  bp_slices(S.b, n, v, bs);
-  for (int i = S.da + 1; i <= n; ++i) as[i] = 0.0;
-  for (int i = S.db + 1; i <= n; ++i) bs[i] = 0.0;
-  as[n + 1] = bs[n + 1] = 0.0;
-  for (int i = 0; i < n; ++i)
-    for (int j = 0; j < n; ++j) {
-      double t = as[i] * bs[j + 1] - bs[i] * as[j + 1];
-      if (i > 0 && j + 1 < n) t += M[(i - 1) * n + j + 1];
-      M[i * n + j] = t;
-    }
-  int sign = 1;
-  double lg = 0.0;
-  for (int c = 0; c < n; ++c) {
-    int piv = c;
-    double best = fabs(M[c * n + c]);
-    for (int r = c + 1; r < n; ++r)
-      if (fabs(M[r * n + c]) > best) {
-        best = fabs(M[r * n + c]);
-        piv = r;
-      }
-    if (best == 0.0) {
-      *logabs = -INFINITY;
-      return 0;
-    }
-    if (piv != c) {
-      sign = -sign;
-      for (int l = c; l < n; ++l) {
-        const double t = M[c * n + l];
-        M[c * n + l] = M[piv * n + l];
-        M[piv * n + l] = t;
-      }
-    }
-    const double d = M[c * n + c];
-    if (d < 0) sign = -sign;
-    lg += log(fabs(d));
-    const double inv = 1.0 / d;
-    for (int r = c + 1; r < n; ++r) {
-      const double fr = M[r * n + c] * inv;
-      if (fr != 0.0)
-        for (int l = c + 1; l < n; ++l) M[r * n + l] = fma(-fr, M[c * n + l], M[r * n + l]);
-    }
-  }
-  *logabs = lg;
-  return sign;
-}
 
 // ------------------------------------------------------------------ path space
 __device__ __forceinline__ bool refract_dir(d3 d, d3 n, double ei, double eo, d3* out) {
@@ -580,310 +382,445 @@ __device__ double jacobian2(const Chain2& C, d3 x1, d3 x2) {
   return fabs(j[0][0] * j[1][1] - j[0][1] * j[1][0]);
 }
 
-// ------------------------------------------------------------------ kernel
+
+
+// ------------------------------------------------------------------ per-pair system records (HBM)
+// Written by the build kernel, read by the scan and path kernels.  Coefficients are stored transposed,
+// [j * NR + i] = coefficient of u^i v^j (zero above the truncated u-degree and beyond the row), so the lane
+// that owns row i reads consecutive addresses with its neighbours.
 template <bool V1T, bool V2T>
-__global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                               uint64_t npairs, const TriRec* __restrict__ tris,
-                                               const double* __restrict__ ep, const double* __restrict__ inten,
-                                               SolveParams prm, SolSink S) {
-  using Sy = Sys2<V1T, V2T>;
-  constexpr int MAXN = Sy::DB;
-  constexpr int MAXV = 40;
+struct Rec2 {
+  using D = Deg2<V1T, V2T>;
+  static constexpr int NR = D::DB <= 15 ? 16 : (D::DB <= 31 ? 32 : 48);
+  static constexpr int VR = 16;  // header: eta0, eta1, eta2, relabel, flags, da, db, n, ok, nv
+  static constexpr int AT = VR + 40;
+  static constexpr int BT = AT + (D::DA + 1) * NR;
+  static constexpr int U = BT + (D::DB + 1) * NR;
+  static constexpr int V = U + tri_n(D::DU);
+  static constexpr int K = V + tri_n(D::DU);
+  static constexpr int STRIDE = (K + tri_n(D::DK) + 7) & ~7;
+};
+enum { H_ETA0 = 0, H_ETA1, H_ETA2, H_RELABEL, H_FLAGS, H_DA, H_DB, H_N, H_OK, H_NV };
+constexpr int kMaxV2 = 40;  // v-roots kept per pair
+
+__device__ __forceinline__ void load_chain(const TriRec* __restrict__ tris, const uint32_t* __restrict__ pt,
+                                           const double* __restrict__ ep, uint32_t q, uint64_t pi, Chain2& C) {
+  load_tri(tris, pt[2 * pi], C.T1.p, C.T1.n);
+  load_tri(tris, pt[2 * pi + 1], C.T2.p, C.T2.n);
+  const double* e = ep + 6ull * q;
+  C.x0 = mk3(e[0], e[1], e[2]);
+  C.x3 = mk3(e[3], e[4], e[5]);
+}
+
+__device__ __forceinline__ void emit_flags(const SolSink& S, uint64_t pi, uint32_t flags) {
+  const unsigned long long p = atomicAdd(S.count + 1, 1ull);
+  if (p < S.fcapacity) {
+    S.fkey[p] = pi;
+    S.fflags[p] = flags;
+  }
+}
+
+template <int G>
+__device__ __forceinline__ void group_counters(const Grp<G>& g, const uint32_t* cnt, const SolSink& S) {
+  for (int i = 0; i < C_NUM; ++i) {
+    uint32_t v = (g.lane == 0) ? cnt[i] : 0u;
+    for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(S.counters + i, (unsigned long long)v);
+  }
+}
+
+// ---- kernel 1: coefficient phase (group per pair, shared-memory arena), record write
+constexpr int kBuildWarps = 2;
+template <bool V1T, bool V2T>
+__global__ void __launch_bounds__(kBuildWarps * 32) k2_build(const uint32_t* __restrict__ pq,
+                                                            const uint32_t* __restrict__ pt, uint64_t p0,
+                                                            uint64_t np, const TriRec* __restrict__ tris,
+                                                            const double* __restrict__ ep, SolveParams prm,
+                                                            double* __restrict__ recs, SolSink S,
+                                                            unsigned long long* __restrict__ next) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  constexpr int G = D::G, GPW = 32 / G;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, gi = (threadIdx.x & 31) / G;
+  Grp<G> g;
+  g.lane = (threadIdx.x & 31) % G;
+  g.mask = G == 32 ? 0xffffffffu : (0xffffu << (16 * gi));
+  double* base = smem + (size_t)(warp * GPW + gi) * D::ARENA;
   uint32_t cnt[C_NUM];
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = gw * 32; base < npairs; base += nw * 32) {
-    const uint64_t pi = base + lane;
-    const bool active = pi < npairs;
+  while (true) {
+    unsigned long long r = 0;
+    if (g.lane == 0) r = atomicAdd(next, 1ull);
+    r = g.bcast(r, 0);
+    if (r >= np) break;
+    const uint64_t pi = p0 + r;
+    Chain2 C;
+    load_chain(tris, pt, ep, pq[pi], pi, C);
+    cnt[C_PAIRS]++;
+    Arena ar{base, 0, D::ARENA, false};
+    Sys2w Sy;
+    const bool ok = build_w<V1T, V2T, G>(g, ar, C.x0, C.x3, C.T1, C.T2, prm, Sy);
+    double* rec = recs + r * R::STRIDE;
+    if (g.lane == 0) {
+      rec[H_ETA0] = Sy.eta0;
+      rec[H_ETA1] = Sy.eta1;
+      rec[H_ETA2] = Sy.eta2;
+      rec[H_RELABEL] = Sy.relabel ? 1.0 : 0.0;
+      rec[H_FLAGS] = (double)Sy.flags;
+      rec[H_DA] = ok ? Sy.da : 0;
+      rec[H_DB] = ok ? Sy.db : 0;
+      rec[H_N] = ok ? Sy.n : 0;
+      rec[H_OK] = ok ? 1.0 : 0.0;
+      rec[H_NV] = 0.0;
+    }
+    if (ok) {
+      cnt[C_SYSTEMS]++;
+      for (int idx = g.lane; idx < (D::DA + 1) * R::NR; idx += G) {
+        const int j = idx / R::NR, i = idx % R::NR;
+        rec[R::AT + idx] = (i <= Sy.da && i + j <= D::DA) ? Sy.a.c[poff(D::DA, i) + j] : 0.0;
+      }
+      for (int idx = g.lane; idx < (D::DB + 1) * R::NR; idx += G) {
+        const int j = idx / R::NR, i = idx % R::NR;
+        rec[R::BT + idx] = (i <= Sy.db && i + j <= D::DB) ? Sy.b.c[poff(D::DB, i) + j] : 0.0;
+      }
+      for (int idx = g.lane; idx < tri_n(D::DU); idx += G) {
+        rec[R::U + idx] = Sy.U.c[idx];
+        rec[R::V + idx] = Sy.V.c[idx];
+      }
+      for (int idx = g.lane; idx < tri_n(D::DK); idx += G) rec[R::K + idx] = Sy.K.c[idx];
+    }
+    g.sync();
+  }
+  group_counters(g, cnt, S);
+}
+
+// ---- kernel 2: 100-piece determinant-sign scan + bisection, group per pair
+// big = false: pairs with n <= G (register determinant); big = true: n > G (shared-memory determinant)
+constexpr int kScanWarps = 4;
+template <bool V1T, bool V2T, bool BIG>
+__global__ void __launch_bounds__(kScanWarps * 32) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
+                                                          double* __restrict__ recs, SolSink S,
+                                                          uint32_t* __restrict__ plist,
+                                                          unsigned long long* __restrict__ pcount,
+                                                          unsigned long long* __restrict__ next) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  constexpr int G = D::G, GPW = 32 / G;
+  extern __shared__ double smem[];
+  const int warp = threadIdx.x >> 5, gi = (threadIdx.x & 31) / G;
+  Grp<G> g;
+  g.lane = (threadIdx.x & 31) % G;
+  g.mask = G == 32 ? 0xffffffffu : (0xffffu << (16 * gi));
+  double* scratch = smem + (size_t)(warp * GPW + gi) * (BIG ? (2 * (R::NR + 2) + R::NR * R::NR) : 0);
+  uint32_t cnt[C_NUM];
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  while (true) {
+    unsigned long long r = 0;
+    if (g.lane == 0) r = atomicAdd(next, 1ull);
+    r = g.bcast(r, 0);
+    if (r >= np) break;
+    double* rec = recs + r * R::STRIDE;
+    const bool ok = rec[H_OK] != 0.0;
+    const int n = (int)rec[H_N];
+    if ((ok && n > G) != BIG) continue;  // the other scan kernel owns this pair
+    uint32_t flags = (uint32_t)rec[H_FLAGS];
+    int nv = 0;
+    if (ok) {
+      const int da = (int)rec[H_DA], db = (int)rec[H_DB];
+      const double* AT = rec + R::AT;
+      const double* BT = rec + R::BT;
+      // algorithmic FLOPs (kFLOP units): coefficient phase (dense products of the Eq. 13-23 chain,
+      // RR 17k, RT 40k, TR 150k, TT 400k) + per determinant evaluation: slices 2 (sum of the
+      // a_i, b_i lengths, i <= n) + Chionh 3 n^2 + GE (2/3) n^3
+      const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
+      double slice_terms = 0;
+      for (int i = 0; i <= n; ++i)
+        slice_terms += (i <= da ? D::DA - i + 1 : 0) + (i <= db ? D::DB - i + 1 : 0);
+      const double nn = (double)n;
+      const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
+      double kflop_acc = build_f;
+      auto det = [&](double v, double* lg) -> int {
+        kflop_acc += eval_f;
+        if (BIG) return wdet_sign_smem<G, R::NR>(g, AT, D::DA, BT, D::DB, n, v, lg, scratch, scratch + 2 * (n + 2));
+        return wdet_T<G, R::NR>(g, AT, D::DA, BT, D::DB, n, v, lg);
+      };
+      const int P = prm.pieces;
+      int last_change = -10;
+      double lg_prev = -INFINITY, lg_cur;
+      int s_cur = det(0.0, &lg_cur);
+      for (int j = 0; j <= P; ++j) {
+        int s_next = 0;
+        double lg_next = -INFINITY;
+        if (j < P) s_next = det((double)(j + 1) / P, &lg_next);
+        // near-tangent: |det(v_j)| < 1e-9 max(neighbours)
+        const double nb = fmax(lg_prev, lg_next);
+        if (lg_cur < log(1e-9) + nb) flags |= SPOLY_FLAG_NEAR_TANGENT;
+        if (s_cur == 0) {
+          if (nv < kMaxV2) {
+            if (g.lane == 0) rec[R::VR + nv] = (double)j / P;
+            nv++;
+          }
+        } else if (j < P && s_next != 0 && s_next != s_cur) {
+          if (j - last_change == 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
+          last_change = j;
+          double lo = (double)j / P, hi = (double)(j + 1) / P;
+          for (int it = 0; it < prm.scan_bisect_iters; ++it) {
+            const double m = 0.5 * (lo + hi);
+            double l2;
+            const int sm = det(m, &l2);
+            if (sm == 0) {
+              lo = hi = m;
+              break;
+            }
+            if (sm == s_cur)
+              lo = m;
+            else
+              hi = m;
+          }
+          if (nv < kMaxV2) {
+            if (g.lane == 0) rec[R::VR + nv] = 0.5 * (lo + hi);
+            nv++;
+          }
+        }
+        lg_prev = lg_cur;
+        s_cur = s_next;
+        lg_cur = lg_next;
+      }
+      cnt[C_KFLOP] += (uint32_t)(kflop_acc * 1e-3);
+      cnt[C_VROOTS] += nv;
+    }
+    if (g.lane == 0) {
+      rec[H_NV] = nv;
+      if (flags) emit_flags(S, p0 + r, flags);
+      if (nv) {
+        const unsigned long long k = atomicAdd(pcount, 1ull);
+        plist[k] = (uint32_t)r;
+      }
+    }
+    g.sync();
+  }
+  group_counters(g, cnt, S);
+}
+
+// ---- kernel 3: path phase (thread per pair with v-roots): back-substitution, polish, validation,
+// contribution, emission (slot = processing order within the pair, deterministic after the sort)
+template <bool V1T, bool V2T>
+__global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                               uint64_t p0, const TriRec* __restrict__ tris,
+                                               const double* __restrict__ ep, const double* __restrict__ inten,
+                                               SolveParams prm, const double* __restrict__ recs, SolSink S,
+                                               const uint32_t* __restrict__ plist,
+                                               const unsigned long long* __restrict__ pcount) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  uint32_t cnt[C_NUM];
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const unsigned long long total = *pcount;
+  for (uint64_t t = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = plist[t];
+    const uint64_t pi = p0 + r;
+    const double* rec = recs + r * R::STRIDE;
+    const uint32_t q = pq[pi];
+    Chain2 C;
+    load_chain(tris, pt, ep, q, pi, C);
+    C.r1 = V1T;
+    C.r2 = V2T;
+    C.eta[0] = rec[H_ETA0];
+    C.eta[1] = rec[H_ETA1];
+    C.eta[2] = rec[H_ETA2];
+    const bool relabel = rec[H_RELABEL] != 0.0;
+    const int da = (int)rec[H_DA], db = (int)rec[H_DB], nv = (int)rec[H_NV];
+    const double* AT = rec + R::AT;
+    const double* BT = rec + R::BT;
+    const WP Up{const_cast<double*>(rec + R::U), D::DU}, Vp{const_cast<double*>(rec + R::V), D::DU},
+        Kp{const_cast<double*>(rec + R::K), D::DK};
     uint32_t flags = 0;
     int nsol = 0;
     double su[4][4], scontrib[4];
     float sres[4];
-    uint32_t sslot[4];
-    if (active) {
-      const uint32_t q = pq[pi];
-      Chain2 C;
-      load_tri(tris, pt[2 * pi], C.T1.p, C.T1.n);
-      load_tri(tris, pt[2 * pi + 1], C.T2.p, C.T2.n);
-      const double* e = ep + 6ull * q;
-      C.x0 = mk3(e[0], e[1], e[2]);
-      C.x3 = mk3(e[3], e[4], e[5]);
-      C.r1 = V1T;
-      C.r2 = V2T;
-      cnt[C_PAIRS]++;
-      Sy Sys;
-      const bool ok = build_system2<V1T, V2T>(C.x0, C.x3, C.T1, C.T2, prm, Sys);
-      flags |= Sys.flags;
-      C.eta[0] = Sys.eta0;
-      C.eta[1] = Sys.eta1;
-      C.eta[2] = Sys.eta2;
-      if (ok) {
-        cnt[C_SYSTEMS]++;
-        // algorithmic FLOPs (kFLOP units): coefficient phase (dense products of the Eq. 13-23 chain,
-        // counted in DESIGN.md §5: RR 17k, RT 40k, TR 150k, TT 400k) + per determinant evaluation:
-        // slices 2 (sum of the a_i, b_i lengths, i <= n) + Chionh 3 n^2 + GE (2/3) n^3
-        const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
-        double slice_terms = 0;
-        for (int i = 0; i <= Sys.n; ++i)
-          slice_terms += (i <= Sys.da ? Sy::DA - i + 1 : 0) + (i <= Sys.db ? Sy::DB - i + 1 : 0);
-        const double nn = (double)Sys.n;
-        const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
-        double kflop_acc = build_f;
-        // ---- 100-piece determinant-sign scan
-        double M[MAXN * MAXN];
-        const int P = prm.pieces;
-        double vroots[MAXV];
-        int nv = 0;
-        int s_prev = 0, last_change = -10;
-        double lg_prev = -INFINITY, lg_prev2 = -INFINITY;
-        int s_cur;
-        double lg_cur;
-        s_cur = det_sign_at<V1T, V2T>(Sys, 0.0, &lg_cur, M);
-        kflop_acc += eval_f;
-        for (int j = 0; j <= P; ++j) {
-          int s_next = 0;
-          double lg_next = -INFINITY;
-          if (j < P) {
-            s_next = det_sign_at<V1T, V2T>(Sys, (double)(j + 1) / P, &lg_next, M);
-            kflop_acc += eval_f;
-          }
-          // near-tangent: |det(v_j)| < 1e-9 max(neighbours)
-          const double nb = fmax(lg_prev, lg_next);
-          if (lg_cur < log(1e-9) + nb) flags |= SPOLY_FLAG_NEAR_TANGENT;
-          if (s_cur == 0) {
-            if (nv < MAXV) vroots[nv++] = (double)j / P;
-          } else if (j < P && s_next != 0 && s_next != s_cur) {
-            if (j - last_change == 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
-            last_change = j;
-            double lo = (double)j / P, hi = (double)(j + 1) / P;
-            for (int it = 0; it < prm.scan_bisect_iters; ++it) {
-              const double m = 0.5 * (lo + hi);
-              double l2;
-              const int sm = det_sign_at<V1T, V2T>(Sys, m, &l2, M);
-              kflop_acc += eval_f;
-              if (sm == 0) {
-                lo = hi = m;
-                break;
-              }
-              if (sm == s_cur)
-                lo = m;
-              else
-                hi = m;
-            }
-            if (nv < MAXV) vroots[nv++] = 0.5 * (lo + hi);
-          }
-          lg_prev2 = lg_prev;
-          lg_prev = lg_cur;
-          s_prev = s_cur;
-          s_cur = s_next;
-          lg_cur = lg_next;
+    constexpr int NA = D::DB + 1;
+    for (int iv = 0; iv < nv; ++iv) {
+      const double vs = rec[R::VR + iv];
+      double Acoef[NA];
+      int dA = da;
+      double amax = 0;
+      for (int i = 0; i <= dA; ++i) {
+        Acoef[i] = rowT<R::NR>(AT, D::DA, i, vs);
+        amax = fmax(amax, fabs(Acoef[i]));
+      }
+      if (!(amax >= 1e-12)) {
+        dA = db;
+        amax = 0;
+        for (int i = 0; i <= dA; ++i) {
+          Acoef[i] = rowT<R::NR>(BT, D::DB, i, vs);
+          amax = fmax(amax, fabs(Acoef[i]));
         }
-        (void)s_prev;
-        (void)lg_prev2;
-        cnt[C_KFLOP] += (uint32_t)(kflop_acc * 1e-3);
-        cnt[C_VROOTS] += nv;
-        // ---- path phase
-        constexpr int NA = Sy::DB + 1;
-        for (int iv = 0; iv < nv; ++iv) {
-          const double vs = vroots[iv];
-          double Acoef[NA];
-          bp_slices(Sys.a, Sys.da, vs, Acoef);
-          int dA = Sys.da;
-          double amax = 0;
-          for (int i = 0; i <= dA; ++i) amax = fmax(amax, fabs(Acoef[i]));
-          if (!(amax >= 1e-12)) {
-            bp_slices(Sys.b, Sys.db, vs, Acoef);
-            dA = Sys.db;
-            amax = 0;
-            for (int i = 0; i <= dA; ++i) amax = fmax(amax, fabs(Acoef[i]));
-            if (!(amax >= 1e-12)) {
-              flags |= SPOLY_FLAG_DEGENERATE;
-              continue;
+        if (!(amax >= 1e-12)) {
+          flags |= SPOLY_FLAG_DEGENERATE;
+          continue;
+        }
+      }
+      while (dA > 0 && Acoef[dA] == 0.0) --dA;
+      double us[kMaxV2];
+      int nu = 0;
+      if (dA == 1) {
+        us[nu++] = -Acoef[0] / Acoef[1];
+      } else if (dA == 2) {
+        const double a0 = Acoef[0], a1 = Acoef[1], a2 = Acoef[2];
+        double disc = a1 * a1 - 4 * a2 * a0;
+        const double sc = a1 * a1 + 4 * fabs(a2 * a0);
+        if (fabs(disc) <= 1e-8 * sc) flags |= SPOLY_FLAG_NEAR_TANGENT;
+        if (!(disc < -1e-12 * sc)) {
+          if (disc < 0) disc = 0;
+          const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+          if (qq == 0.0) {
+            us[nu++] = 0.0;
+          } else {
+            double r1 = qq / a2, r2 = a0 / qq;
+            if (r1 > r2) {
+              const double t = r1;
+              r1 = r2;
+              r2 = t;
             }
+            us[nu++] = r1;
+            if (r2 - r1 >= 1e-7) us[nu++] = r2;
           }
-          while (dA > 0 && Acoef[dA] == 0.0) --dA;
-          double us[MAXV];
-          int nu = 0;
-          if (dA == 1) {
-            us[nu++] = -Acoef[0] / Acoef[1];
-          } else if (dA == 2) {
-            const double a0 = Acoef[0], a1 = Acoef[1], a2 = Acoef[2];
-            double disc = a1 * a1 - 4 * a2 * a0;
-            const double sc = a1 * a1 + 4 * fabs(a2 * a0);
-            if (fabs(disc) <= 1e-8 * sc) flags |= SPOLY_FLAG_NEAR_TANGENT;
-            if (!(disc < -1e-12 * sc)) {
-              if (disc < 0) disc = 0;
-              const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
-              if (qq == 0.0) {
-                us[nu++] = 0.0;
-              } else {
-                double r1 = qq / a2, r2 = a0 / qq;
-                if (r1 > r2) {
-                  const double t = r1;
-                  r1 = r2;
-                  r2 = t;
-                }
-                us[nu++] = r1;
-                if (r2 - r1 >= 1e-7) us[nu++] = r2;
-              }
-            }
-          } else if (dA > 2) {
-            RootSet<NA> Ru;
-            isolate_roots<NA>(Acoef, dA, -0.1, 1.1, 1e-7, Ru);
-            for (int i = 0; i < Ru.n && nu < MAXV; ++i)
-              if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];
+        }
+      } else if (dA > 2) {
+        RootSet<NA> Ru;
+        isolate_roots<NA>(Acoef, dA, -0.1, 1.1, 1e-7, Ru);
+        for (int i = 0; i < Ru.n && nu < kMaxV2; ++i)
+          if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];
+      }
+      for (int iu = 0; iu < nu; ++iu) {
+        cnt[C_CANDIDATES]++;
+        const double ur = us[iu], vr = vs;
+        const double kap = wp_eval(Kp, ur, vr), ut = wp_eval(Up, ur, vr), vt = wp_eval(Vp, ur, vr);
+        double u2 = ut / kap, v2 = vt / kap;
+        if (!(fabs(kap) > 0) || !isfinite(u2) || !isfinite(v2)) {
+          cnt[C_REJ_KAPPA]++;
+          continue;
+        }
+        if (relabel) {
+          const double t = u2;
+          u2 = v2;
+          v2 = t;
+        }
+        const double dm = 1e-3;
+        if (!(ur >= -dm && vr >= -dm && ur + vr <= 1 + dm && u2 >= -dm && v2 >= -dm && u2 + v2 <= 1 + dm)) {
+          cnt[C_REJ_DOMAIN]++;
+          continue;
+        }
+        d3 x1 = C.T1.X(ur, vr), x2 = C.T2.X(u2, v2);
+        double r1 = resid(C.x0, x1, x2, C.T1.N(ur, vr), C.eta[0], C.eta[1]);
+        double r2 = resid(x1, x2, C.x3, C.T2.N(u2, v2), C.eta[1], C.eta[2]);
+        if (!(fmax(r1, r2) < prm.theta_admit)) {
+          cnt[C_REJ_CONSTRAINT]++;
+          continue;
+        }
+        // polish: <= polish_iters Newton steps on the exact shooting residual, keep if |G| decreases
+        d3 f1, f2;
+        frame_of(normalize(C.x3 - x2), &f1, &f2);
+        double uu = ur, vv = vr, Gs[2], uu2 = u2, vv2 = v2;
+        bool okp = shoot2(C, uu, vv, f1, f2, Gs, &uu2, &vv2);
+        double Jm[4] = {0, 0, 0, 0};
+        for (int it = 0; okp && it < prm.polish_iters; ++it) {
+          const double h = 1e-7;
+          double Gp[2], Gm[2], t1, t2;
+          if (!shoot2(C, uu + h, vv, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu - h, vv, f1, f2, Gm, &t1, &t2)) break;
+          Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
+          Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
+          if (!shoot2(C, uu, vv + h, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu, vv - h, f1, f2, Gm, &t1, &t2)) break;
+          Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
+          Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
+          const double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
+          if (det == 0.0) break;
+          const double du = -(Jm[3] * Gs[0] - Jm[1] * Gs[1]) / det;
+          const double dv = -(-Jm[2] * Gs[0] + Jm[0] * Gs[1]) / det;
+          double Gn[2], nu2, nv2;
+          if (!shoot2(C, uu + du, vv + dv, f1, f2, Gn, &nu2, &nv2)) break;
+          if (!(hypot(Gn[0], Gn[1]) < hypot(Gs[0], Gs[1]))) break;
+          uu += du;
+          vv += dv;
+          Gs[0] = Gn[0];
+          Gs[1] = Gn[1];
+          uu2 = nu2;
+          vv2 = nv2;
+        }
+        if (!okp) {
+          cnt[C_REJ_CONSTRAINT]++;
+          continue;
+        }
+        const double ed = prm.eps_domain;
+        if (!(uu >= -ed && vv >= -ed && uu + vv <= 1 + ed && uu2 >= -ed && vv2 >= -ed && uu2 + vv2 <= 1 + ed)) {
+          cnt[C_REJ_DOMAIN]++;
+          continue;
+        }
+        x1 = C.T1.X(uu, vv);
+        x2 = C.T2.X(uu2, vv2);
+        const d3 n1 = C.T1.N(uu, vv), n2 = C.T2.N(uu2, vv2);
+        r1 = resid(C.x0, x1, x2, n1, C.eta[0], C.eta[1]);
+        r2 = resid(x1, x2, C.x3, n2, C.eta[1], C.eta[2]);
+        const double rho = fmax(r1, r2);
+        if (!(rho < prm.theta_final)) {
+          cnt[C_REJ_CONSTRAINT]++;
+          continue;
+        }
+        if (!sides(C.r1, C.x0, x1, x2, n1, C.T1.g()) || !sides(C.r2, x1, x2, C.x3, n2, C.T2.g())) {
+          cnt[C_REJ_SIDE]++;
+          continue;
+        }
+        if (C.r2) {  // eta consistency: x_1 on the side of T_2 whose IOR is eta_1
+          const double se = dot(x1 - C.T2.p[0], C.T2.g()) > 0 ? prm.eta_front : prm.eta_back;
+          if (se != C.eta[1]) {
+            cnt[C_REJ_SIDE]++;
+            continue;
           }
-          for (int iu = 0; iu < nu; ++iu) {
-            cnt[C_CANDIDATES]++;
-            const double ur = us[iu], vr = vs;
-            const double kap = bp_eval(Sys.K, ur, vr), ut = bp_eval(Sys.U, ur, vr), vt = bp_eval(Sys.V, ur, vr);
-            double u2 = ut / kap, v2 = vt / kap;
-            if (!(fabs(kap) > 0) || !isfinite(u2) || !isfinite(v2)) {
-              cnt[C_REJ_KAPPA]++;
-              continue;
-            }
-            if (Sys.relabel) {
-              const double t = u2;
-              u2 = v2;
-              v2 = t;
-            }
-            const double dm = 1e-3;
-            if (!(ur >= -dm && vr >= -dm && ur + vr <= 1 + dm && u2 >= -dm && v2 >= -dm && u2 + v2 <= 1 + dm)) {
-              cnt[C_REJ_DOMAIN]++;
-              continue;
-            }
-            d3 x1 = C.T1.X(ur, vr), x2 = C.T2.X(u2, v2);
-            double r1 = resid(C.x0, x1, x2, C.T1.N(ur, vr), C.eta[0], C.eta[1]);
-            double r2 = resid(x1, x2, C.x3, C.T2.N(u2, v2), C.eta[1], C.eta[2]);
-            if (!(fmax(r1, r2) < prm.theta_admit)) {
-              cnt[C_REJ_CONSTRAINT]++;
-              continue;
-            }
-            // polish: <= polish_iters Newton steps on the exact shooting residual, keep if |G| decreases
-            d3 f1, f2;
-            frame_of(normalize(C.x3 - x2), &f1, &f2);
-            double uu = ur, vv = vr, G[2], uu2 = u2, vv2 = v2;
-            bool okp = shoot2(C, uu, vv, f1, f2, G, &uu2, &vv2);
-            double Jm[4] = {0, 0, 0, 0};
-            for (int it = 0; okp && it < prm.polish_iters; ++it) {
-              const double h = 1e-7;
-              double Gp[2], Gm[2], t1, t2;
-              if (!shoot2(C, uu + h, vv, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu - h, vv, f1, f2, Gm, &t1, &t2)) break;
-              Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
-              Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
-              if (!shoot2(C, uu, vv + h, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu, vv - h, f1, f2, Gm, &t1, &t2)) break;
-              Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
-              Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
-              const double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
-              if (det == 0.0) break;
-              const double du = -(Jm[3] * G[0] - Jm[1] * G[1]) / det;
-              const double dv = -(-Jm[2] * G[0] + Jm[0] * G[1]) / det;
-              double Gn[2], nu2, nv2;
-              if (!shoot2(C, uu + du, vv + dv, f1, f2, Gn, &nu2, &nv2)) break;
-              if (!(hypot(Gn[0], Gn[1]) < hypot(G[0], G[1]))) break;
-              uu += du;
-              vv += dv;
-              G[0] = Gn[0];
-              G[1] = Gn[1];
-              uu2 = nu2;
-              vv2 = nv2;
-            }
-            if (!okp) {
-              cnt[C_REJ_CONSTRAINT]++;
-              continue;
-            }
-            const double ed = prm.eps_domain;
-            if (!(uu >= -ed && vv >= -ed && uu + vv <= 1 + ed && uu2 >= -ed && vv2 >= -ed && uu2 + vv2 <= 1 + ed)) {
-              cnt[C_REJ_DOMAIN]++;
-              continue;
-            }
-            x1 = C.T1.X(uu, vv);
-            x2 = C.T2.X(uu2, vv2);
-            const d3 n1 = C.T1.N(uu, vv), n2 = C.T2.N(uu2, vv2);
-            r1 = resid(C.x0, x1, x2, n1, C.eta[0], C.eta[1]);
-            r2 = resid(x1, x2, C.x3, n2, C.eta[1], C.eta[2]);
-            const double rho = fmax(r1, r2);
-            if (!(rho < prm.theta_final)) {
-              cnt[C_REJ_CONSTRAINT]++;
-              continue;
-            }
-            if (!sides(C.r1, C.x0, x1, x2, n1, C.T1.g()) || !sides(C.r2, x1, x2, C.x3, n2, C.T2.g())) {
-              cnt[C_REJ_SIDE]++;
-              continue;
-            }
-            if (C.r2) {  // eta consistency: x_1 on the side of T_2 whose IOR is eta_1
-              const double se = dot(x1 - C.T2.p[0], C.T2.g()) > 0 ? prm.eta_front : prm.eta_back;
-              if (se != C.eta[1]) {
-                cnt[C_REJ_SIDE]++;
-                continue;
-              }
-            }
-            if (rho >= 1e-7) flags |= SPOLY_FLAG_RESIDUAL;
-            const double e1d = fmin(fmin(uu, vv), 1 - uu - vv), e2d = fmin(fmin(uu2, vv2), 1 - uu2 - vv2);
-            if (e1d <= prm.eps_flag || e2d <= prm.eps_flag) flags |= SPOLY_FLAG_BOUNDARY;
-            if (fabs(Jm[0] * Jm[3] - Jm[1] * Jm[2]) < 1e-6 * hypot(Jm[0], Jm[1]) * hypot(Jm[2], Jm[3]))
-              flags |= SPOLY_FLAG_NEAR_TANGENT;
-            bool dup = false;
-            for (int s = 0; s < nsol; ++s)
-              if (fabs(su[s][0] - uu) < 1e-7 && fabs(su[s][1] - vv) < 1e-7) dup = true;
-            if (dup) {
-              cnt[C_REJ_SIDE]++;
-              continue;
-            }
-            if (nsol < 4) {
-              const double J = jacobian2(C, x1, x2);
-              const double I = inten ? inten[q] : 1.0;
-              su[nsol][0] = uu;
-              su[nsol][1] = vv;
-              su[nsol][2] = uu2;
-              su[nsol][3] = vv2;
-              scontrib[nsol] = J > 0 ? I / J : 0.0;
-              sres[nsol] = (float)rho;
-              sslot[nsol] = (uint32_t)nsol;  // processing order: deterministic
-              nsol++;
-              cnt[C_ADMISSIBLE]++;
-            }
-          }
+        }
+        if (rho >= 1e-7) flags |= SPOLY_FLAG_RESIDUAL;
+        const double e1d = fmin(fmin(uu, vv), 1 - uu - vv), e2d = fmin(fmin(uu2, vv2), 1 - uu2 - vv2);
+        if (e1d <= prm.eps_flag || e2d <= prm.eps_flag) flags |= SPOLY_FLAG_BOUNDARY;
+        if (fabs(Jm[0] * Jm[3] - Jm[1] * Jm[2]) < 1e-6 * hypot(Jm[0], Jm[1]) * hypot(Jm[2], Jm[3]))
+          flags |= SPOLY_FLAG_NEAR_TANGENT;
+        bool dup = false;
+        for (int s = 0; s < nsol; ++s)
+          if (fabs(su[s][0] - uu) < 1e-7 && fabs(su[s][1] - vv) < 1e-7) dup = true;
+        if (dup) {
+          cnt[C_REJ_SIDE]++;
+          continue;
+        }
+        if (nsol < 4) {
+          const double J = jacobian2(C, x1, x2);
+          const double I = inten ? inten[q] : 1.0;
+          su[nsol][0] = uu;
+          su[nsol][1] = vv;
+          su[nsol][2] = uu2;
+          su[nsol][3] = vv2;
+          scontrib[nsol] = J > 0 ? I / J : 0.0;
+          sres[nsol] = (float)rho;
+          nsol++;
+          cnt[C_ADMISSIBLE]++;
         }
       }
     }
-    // emission (warp-aggregated, all lanes)
-    {
-      const bool hf = active && flags != 0;
-      const unsigned bal = __ballot_sync(0xffffffffu, hf);
-      if (bal) {
-        unsigned long long fb = 0;
-        const int leader = __ffs(bal) - 1;
-        if (lane == leader) fb = atomicAdd(S.count + 1, (unsigned long long)__popc(bal));
-        fb = __shfl_sync(0xffffffffu, fb, leader);
-        if (hf) {
-          const unsigned long long p = fb + __popc(bal & ((1u << lane) - 1u));
-          if (p < S.fcapacity) {
-            S.fkey[p] = pi;
-            S.fflags[p] = flags;
-          }
-        }
+    // emission: flag record, then the solutions in processing order (deterministic slot)
+    if (flags) {
+      const unsigned long long p = atomicAdd(S.count + 1, 1ull);
+      if (p < S.fcapacity) {
+        S.fkey[p] = pi;
+        S.fflags[p] = flags;
       }
-      uint32_t n = active ? (uint32_t)nsol : 0u, incl = n;
-      for (int off = 1; off < 32; off <<= 1) {
-        const uint32_t t = __shfl_up_sync(0xffffffffu, incl, off);
-        if (lane >= off) incl += t;
-      }
-      const uint32_t tot = __shfl_sync(0xffffffffu, incl, 31);
-      if (tot) {
-        unsigned long long b = 0;
-        if (lane == 31) b = atomicAdd(S.count, (unsigned long long)tot);
-        b = __shfl_sync(0xffffffffu, b, 31);
-        for (uint32_t s = 0; s < n; ++s) {
-          const unsigned long long p = b + incl - n + s;
-          if (p < S.capacity) {
-            S.key[p] = ((unsigned long long)pi << 6) | sslot[s];
-            for (int c = 0; c < 4; ++c) S.bary[4 * p + c] = su[s][c];
-            S.contrib[p] = scontrib[s];
-            S.resid[p] = sres[s];
-          }
+    }
+    if (nsol) {
+      const unsigned long long b = atomicAdd(S.count, (unsigned long long)nsol);
+      for (int s = 0; s < nsol; ++s) {
+        const unsigned long long p = b + s;
+        if (p < S.capacity) {
+          S.key[p] = ((unsigned long long)pi << 6) | (unsigned)s;
+          for (int c = 0; c < 4; ++c) S.bary[4 * p + c] = su[s][c];
+          S.contrib[p] = scontrib[s];
+          S.resid[p] = sres[s];
         }
       }
     }
@@ -891,26 +828,69 @@ __global__ void __launch_bounds__(64) k2_solve(const uint32_t* __restrict__ pq, 
   for (int i = 0; i < C_NUM; ++i) {
     uint32_t v = cnt[i];
     for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-    if (lane == 0 && v) atomicAdd(S.counters + i, (unsigned long long)v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(S.counters + i, (unsigned long long)v);
   }
 }
 
+template <bool V1T, bool V2T>
+static void launch_k2(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M, const double* ep,
+                      const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W, int nsm,
+                      cudaStream_t st) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  constexpr int G = D::G;
+  const size_t sh_build = (size_t)kBuildWarps * (32 / G) * D::ARENA * sizeof(double);
+  const size_t sh_big = (size_t)kScanWarps * (32 / G) * (2 * (R::NR + 2) + R::NR * R::NR) * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k2_build<V1T, V2T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_build);
+    cudaFuncSetAttribute(k2_scan<V1T, V2T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_big);
+    attr = true;
+  }
+  int occ_b = 0, occ_s = 0, occ_p = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, k2_build<V1T, V2T>, kBuildWarps * 32, sh_build);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k2_scan<V1T, V2T, false>, kScanWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k2_path<V1T, V2T>, 128, 0);
+  occ_b = occ_b < 1 ? 1 : occ_b;
+  occ_s = occ_s < 1 ? 1 : occ_s;
+  occ_p = occ_p < 1 ? 1 : occ_p;
+  const uint64_t chunk = W.rec_cap / R::STRIDE;
+  for (uint64_t p0 = 0; p0 < npairs; p0 += chunk) {
+    const uint64_t np = npairs - p0 < chunk ? npairs - p0 : chunk;
+    cudaMemsetAsync(W.ctr, 0, 4 * sizeof(unsigned long long), st);
+    const uint64_t gb = (uint64_t)kBuildWarps * (32 / G), gs = (uint64_t)kScanWarps * (32 / G);
+    const int bb = (int)std::min<uint64_t>((np + gb - 1) / gb, (uint64_t)nsm * occ_b);
+    const int bs = (int)std::min<uint64_t>((np + gs - 1) / gs, (uint64_t)nsm * occ_s);
+    const int bp = (int)std::min<uint64_t>((np + 127) / 128, (uint64_t)nsm * occ_p);
+    k2_build<V1T, V2T><<<bb, kBuildWarps * 32, sh_build, st>>>(pq, pt, p0, np, M.tris, ep, prm, W.rec, S, W.ctr);
+    k2_scan<V1T, V2T, false><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, W.plist, W.ctr + 3, W.ctr + 1);
+    if (D::DB > 32)
+      k2_scan<V1T, V2T, true><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, W.rec, S, W.plist, W.ctr + 3,
+                                                                   W.ctr + 2);
+    k2_path<V1T, V2T><<<bp, 128, 0, st>>>(pq, pt, p0, M.tris, ep, inten, prm, W.rec, S, W.plist, W.ctr + 3);
+    W.launches += D::DB > 32 ? 4 : 3;
+  }
+}
+
+uint64_t k2_record_bytes(int v1t, int v2t) {
+  if (v1t && v2t) return Rec2<true, true>::STRIDE * sizeof(double);
+  if (v1t) return Rec2<true, false>::STRIDE * sizeof(double);
+  if (v2t) return Rec2<false, true>::STRIDE * sizeof(double);
+  return Rec2<false, false>::STRIDE * sizeof(double);
+}
+
 void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, int nsm,
-                     cudaStream_t st) {
+                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
+                     int nsm, cudaStream_t st) {
   if (!npairs) return;
-  const int threads = 64;
-  const uint64_t want = (npairs + threads - 1) / threads;
-  const uint64_t cap = (uint64_t)nsm * 8;
-  const int g = (int)(want < cap ? want : cap);
   if (v1t && v2t)
-    k2_solve<true, true><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+    launch_k2<true, true>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
   else if (v1t)
-    k2_solve<true, false><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+    launch_k2<true, false>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
   else if (v2t)
-    k2_solve<false, true><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+    launch_k2<false, true>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
   else
-    k2_solve<false, false><<<g, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, inten, prm, S);
+    launch_k2<false, false>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
 }
 
 }  // namespace spoly

@@ -1,0 +1,380 @@
+// Group-cooperative (16 or 32 lanes) dense bivariate polynomial algebra in shared memory, and the
+// register-resident determinant of the Bezout matrix (Eq. 24) used by the two-bounce solve.
+//
+// Storage: a polynomial of degree d is packed row by row in u-degree, c[poff(d, i) + j] = coefficient of
+// u^i v^j (i + j <= d), T(d) = (d + 1)(d + 2) / 2 doubles.  Every output coefficient is produced by exactly
+// one lane (gather form), so no atomics and a fixed summation order (deterministic).
+#pragma once
+#include "common.cuh"
+#include "poly_dev.cuh"
+
+namespace spoly {
+
+template <int G>
+struct Grp {
+  int lane;       // 0 .. G-1 within the group
+  unsigned mask;  // lanes of the group within the warp
+  __device__ __forceinline__ void sync() const { __syncwarp(mask); }
+  template <class T>
+  __device__ __forceinline__ T bcast(T v, int src) const { return __shfl_sync(mask, v, src, G); }
+  template <class T>
+  __device__ __forceinline__ T down(T v, int d) const { return __shfl_down_sync(mask, v, d, G); }
+  template <class T>
+  __device__ __forceinline__ T xor_(T v, int d) const { return __shfl_xor_sync(mask, v, d, G); }
+  __device__ __forceinline__ double max_(double v) const {
+    for (int o = G / 2; o; o >>= 1) v = fmax(v, xor_(v, o));
+    return v;
+  }
+  __device__ __forceinline__ int imax(int v) const {
+    for (int o = G / 2; o; o >>= 1) v = max(v, xor_(v, o));
+    return v;
+  }
+};
+
+__host__ __device__ constexpr int tri_n(int d) { return (d + 1) * (d + 2) / 2; }
+__device__ __forceinline__ int poff(int d, int i) { return i * (2 * d + 3 - i) / 2; }
+
+struct WP {
+  double* c;
+  int d;
+};
+struct WV {
+  WP x, y, z;
+};
+
+// per-group bump allocator over the shared-memory arena (uniform across the group)
+struct Arena {
+  double* base;
+  int top, cap;
+  bool overflow;
+  __device__ WP poly(int d) {
+    WP p{base + top, d};
+    top += tri_n(d);
+    if (top > cap) {
+      overflow = true;
+      top = cap - tri_n(d) > 0 ? cap - tri_n(d) : 0;  // keep pointers in bounds; result discarded
+      p.c = base + top;
+      top += tri_n(d);
+    }
+    return p;
+  }
+  __device__ WV vec(int d) { return {poly(d), poly(d), poly(d)}; }
+  __device__ double* raw(int n) {
+    double* p = base + top;
+    top += n;
+    if (top > cap) {
+      overflow = true;
+      top -= n;
+      p = base;
+    }
+    return p;
+  }
+};
+
+// advance the packed (i, j) position of output degree d by `step` coefficients
+__device__ __forceinline__ void padv(int d, int step, int& i, int& j) {
+  j += step;
+  while (i <= d && j > d - i) {
+    j -= d - i + 1;
+    ++i;
+  }
+}
+
+// c = sum_k s_k a_k b_k  (+ c if acc); every product term with i + j <= c.d is produced
+template <int G, int K>
+__device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
+  const int dc = c.d, n = tri_n(dc);
+  int i = 0, j = 0;
+  padv(dc, g.lane, i, j);
+  for (int idx = g.lane; idx < n; idx += G) {
+    double sum = acc ? c.c[idx] : 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      const int da = a[k].d, db = b[k].d;
+      double t = 0.0;
+      const int p0 = max(0, i - db), p1 = min(i, da);
+      for (int p = p0; p <= p1; ++p) {
+        const int q0 = max(0, i + j - p - db), q1 = min(j, da - p);
+        const double* ap = a[k].c + poff(da, p);
+        const double* bp = b[k].c + poff(db, i - p) + j;
+        for (int q = q0; q <= q1; ++q) t = fma(ap[q], bp[-q], t);
+      }
+      sum = fma(s[k], t, sum);
+    }
+    c.c[idx] = sum;
+    padv(dc, G, i, j);
+  }
+  g.sync();
+}
+template <int G>
+__device__ __forceinline__ void wmul1(const Grp<G>& g, WP c, WP a, WP b, double s, bool acc) {
+  const WP A[1] = {a}, B[1] = {b};
+  const double Sc[1] = {s};
+  wmul<G, 1>(g, c, A, B, Sc, acc);
+}
+template <int G>
+__device__ __forceinline__ void wmul2(const Grp<G>& g, WP c, WP a0, WP b0, double s0, WP a1, WP b1, double s1,
+                                      bool acc) {
+  const WP A[2] = {a0, a1}, B[2] = {b0, b1};
+  const double Sc[2] = {s0, s1};
+  wmul<G, 2>(g, c, A, B, Sc, acc);
+}
+// c (+)= s (A . B)
+template <int G>
+__device__ __forceinline__ void wdot(const Grp<G>& g, WP c, const WV& A, const WV& B, double s, bool acc) {
+  const WP a[3] = {A.x, A.y, A.z}, b[3] = {B.x, B.y, B.z};
+  const double Sc[3] = {s, s, s};
+  wmul<G, 3>(g, c, a, b, Sc, acc);
+}
+
+// c = sum_k s_k a_k (+ c if acc), a_k of degree <= anything (terms beyond c.d dropped)
+template <int G, int K>
+__device__ void wlin(const Grp<G>& g, WP c, const WP (&a)[K], const double (&s)[K], bool acc) {
+  const int dc = c.d, n = tri_n(dc);
+  int i = 0, j = 0;
+  padv(dc, g.lane, i, j);
+  for (int idx = g.lane; idx < n; idx += G) {
+    double sum = acc ? c.c[idx] : 0.0;
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+      if (i + j <= a[k].d) sum = fma(s[k], a[k].c[poff(a[k].d, i) + j], sum);
+    c.c[idx] = sum;
+    padv(dc, G, i, j);
+  }
+  g.sync();
+}
+template <int G>
+__device__ __forceinline__ void wlin1(const Grp<G>& g, WP c, WP a, double s, bool acc) {
+  const WP A[1] = {a};
+  const double Sc[1] = {s};
+  wlin<G, 1>(g, c, A, Sc, acc);
+}
+template <int G>
+__device__ __forceinline__ void wlin2(const Grp<G>& g, WP c, WP a0, double s0, WP a1, double s1, bool acc) {
+  const WP A[2] = {a0, a1};
+  const double Sc[2] = {s0, s1};
+  wlin<G, 2>(g, c, A, Sc, acc);
+}
+template <int G>
+__device__ __forceinline__ void wlin3(const Grp<G>& g, WP c, WP a0, double s0, WP a1, double s1, WP a2, double s2,
+                                      bool acc) {
+  const WP A[3] = {a0, a1, a2};
+  const double Sc[3] = {s0, s1, s2};
+  wlin<G, 3>(g, c, A, Sc, acc);
+}
+// c.c[0] += x
+template <int G>
+__device__ __forceinline__ void wadd0(const Grp<G>& g, WP c, double x) {
+  if (g.lane == 0) c.c[0] += x;
+  g.sync();
+}
+// linear polynomial c0 + cu u + cv v
+template <int G>
+__device__ __forceinline__ void wlinear(const Grp<G>& g, WP c, double c0, double cu, double cv) {
+  if (g.lane == 0) {
+    c.c[0] = c0;  // (0, 0)
+    c.c[1] = cv;  // (0, 1)
+    c.c[2] = cu;  // (1, 0)
+  }
+  g.sync();
+}
+template <int G>
+__device__ __forceinline__ void wlinear3(const Grp<G>& g, WV& V, d3 c0, d3 cu, d3 cv) {
+  if (g.lane == 0) {
+    V.x.c[0] = c0.x; V.x.c[1] = cv.x; V.x.c[2] = cu.x;
+    V.y.c[0] = c0.y; V.y.c[1] = cv.y; V.y.c[2] = cu.y;
+    V.z.c[0] = c0.z; V.z.c[1] = cv.z; V.z.c[2] = cu.z;
+  }
+  g.sync();
+}
+// R = A x b for a constant vector b
+template <int G>
+__device__ __forceinline__ void wcross_c(const Grp<G>& g, const WV& R, const WV& A, d3 b) {
+  wlin2(g, R.x, A.y, b.z, A.z, -b.y, false);
+  wlin2(g, R.y, A.z, b.x, A.x, -b.z, false);
+  wlin2(g, R.z, A.x, b.y, A.y, -b.x, false);
+}
+// R = A x B
+template <int G>
+__device__ __forceinline__ void wcross(const Grp<G>& g, const WV& R, const WV& A, const WV& B) {
+  wmul2(g, R.x, A.y, B.z, 1.0, A.z, B.y, -1.0, false);
+  wmul2(g, R.y, A.z, B.x, 1.0, A.x, B.z, -1.0, false);
+  wmul2(g, R.z, A.x, B.y, 1.0, A.y, B.x, -1.0, false);
+}
+
+// ------------------------------------------------------------------ scalar evaluation (one lane)
+__device__ __forceinline__ double wp_row(const WP& p, int i, double v) {  // sum_j c_ij v^j
+  const double* r = p.c + poff(p.d, i);
+  double s = 0.0;
+  for (int j = p.d - i; j >= 0; --j) s = fma(s, v, r[j]);
+  return s;
+}
+__device__ __forceinline__ double wp_eval(const WP& p, double u, double v) {
+  double acc = 0.0;
+  for (int i = p.d; i >= 0; --i) acc = fma(acc, u, wp_row(p, i, v));
+  return acc;
+}
+
+// ------------------------------------------------------------------ determinant of R(v) (Eq. 24)
+// Slices a_l(v), b_l(v) (lane l; rows above the truncated degrees are stored as zero), Bezout columns by
+// the Chionh recurrence B_ij = B_{i-1,j+1} + a_i b_{j+1} - b_i a_{j+1} (lane j holds column j; the matrix
+// is symmetric, so the columns are the rows of B^T and det B^T = det B), then Gaussian elimination with
+// partial pivoting by rows held in registers: the pivot row is chosen by a group max over the live rows
+// (|x| quantised to 15 mantissa bits, lowest row on ties), broadcast by shuffles, never moved ("virtual"
+// pivoting; the permutation sign is the parity of the unused rows above each pivot).  Returns sign(det)
+// (0 for a zero pivot) and log|det| in *lg.  NC >= n is a compile-time bound (columns >= n are zero, so
+// the update loops need no predicates); lanes >= n hold zero rows.
+__device__ __forceinline__ void renorm(double& mant, int& ex) {
+  const int hi = __double2hiint(mant);
+  ex += ((hi >> 20) & 0x7ff) - 1022;
+  mant = __hiloint2double((hi & 0x800fffff) | 0x3fe00000, __double2loint(mant));
+}
+
+template <int G, int NC>
+__device__ int wdet_rows(const Grp<G>& g, double as, double bs, double aj1, double bj1, int n, double* lg) {
+  const int l = g.lane;
+  double col[NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const double ai = g.bcast(as, i), bi = g.bcast(bs, i);
+    double prev = g.down(i ? col[i - 1] : 0.0, 1);  // B_{i-1, j+1}
+    if (i == 0 || l + 1 >= n) prev = 0.0;
+    col[i] = (i < n) ? prev + (ai * bj1 - bi * aj1) : 0.0;
+  }
+  const bool live = l < n;
+  unsigned used = 0u;
+  int sign = 1;
+  double mant = 1.0;
+  int ex = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    if (c >= n) break;
+    const bool cand = live && !((used >> l) & 1u);
+    unsigned key = 0u;
+    if (cand) key = (((unsigned)__double2hiint(fabs(col[c]))) & ~31u) | (unsigned)(31 - l);
+    for (int o = G / 2; o; o >>= 1) key = max(key, g.xor_(key, o));
+    if ((key >> 5) == 0u) {
+      *lg = -INFINITY;
+      return 0;
+    }
+    const int p = 31 - (int)(key & 31u);
+    const double piv = g.bcast(col[c], p);
+    if ((__popc(~used & ((1u << p) - 1u)) & 1) ^ (piv < 0)) sign = -sign;
+    mant *= fabs(piv);
+    renorm(mant, ex);
+    used |= 1u << p;
+    const double lm = (cand && l != p) ? col[c] * fast_rcp(piv) : 0.0;
+#pragma unroll
+    for (int jj = c + 1; jj < NC; ++jj) col[jj] = fma(-lm, g.bcast(col[jj], p), col[jj]);
+  }
+  *lg = log(mant) + ex * 0.69314718055994530942;
+  return sign;
+}
+
+// slice of row l at v from a transposed coefficient block AT[j * NR + l] (zero beyond the row)
+template <int NR>
+__device__ __forceinline__ double rowT(const double* __restrict__ AT, int D, int l, double v) {
+  double s = 0.0;
+  for (int j = D; j >= 0; --j) s = fma(s, v, __ldg(AT + j * NR + l));
+  return s;
+}
+
+// det sign for n <= G from the transposed blocks (the group evaluates the slices, lane l row l)
+template <int G, int NR>
+__device__ int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* BT, int DB, int n, double v,
+                      double* lg) {
+  const int l = g.lane;
+  const double as = rowT<NR>(AT, DA, l, v), bs = rowT<NR>(BT, DB, l, v);
+  double aj1 = g.down(as, 1), bj1 = g.down(bs, 1);  // slices j + 1
+  if (l == G - 1) {  // slice G is only needed when n == G (rows >= NR do not exist)
+    constexpr int RG = G < NR ? G : 0;
+    const bool need = G < NR && n >= G;
+    aj1 = need ? rowT<NR>(AT, DA, RG, v) : 0.0;
+    bj1 = need ? rowT<NR>(BT, DB, RG, v) : 0.0;
+  }
+  if (G == 16) {
+    if (n <= 8) return wdet_rows<G, 8>(g, as, bs, aj1, bj1, n, lg);
+    if (n <= 12) return wdet_rows<G, 12>(g, as, bs, aj1, bj1, n, lg);
+    return wdet_rows<G, 16>(g, as, bs, aj1, bj1, n, lg);
+  }
+  if (n <= 12) return wdet_rows<G, 12>(g, as, bs, aj1, bj1, n, lg);
+  if (n <= 16) return wdet_rows<G, 16>(g, as, bs, aj1, bj1, n, lg);
+  if (n <= 20) return wdet_rows<G, 20>(g, as, bs, aj1, bj1, n, lg);
+  if (n <= 24) return wdet_rows<G, 24>(g, as, bs, aj1, bj1, n, lg);
+  if (n <= 28) return wdet_rows<G, 28>(g, as, bs, aj1, bj1, n, lg);
+  return wdet_rows<G, 32>(g, as, bs, aj1, bj1, n, lg);
+}
+
+// Same determinant for n > G (rare: numerical TT orders above 32): matrix in the shared-memory scratch M
+// (n*n doubles), rows built by the recurrence, elimination lane-parallel over columns.
+template <int G, int NR>
+__device__ int wdet_sign_smem(const Grp<G>& g, const double* AT, int DA, const double* BT, int DB, int n, double v,
+                              double* lg, double* sl /* 2 (n + 2) */, double* M) {
+  double* as = sl;
+  double* bs = sl + n + 2;
+  for (int i = g.lane; i <= n + 1; i += G) {
+    as[i] = (i <= n && i < NR) ? rowT<NR>(AT, DA, i, v) : 0.0;
+    bs[i] = (i <= n && i < NR) ? rowT<NR>(BT, DB, i, v) : 0.0;
+  }
+  g.sync();
+  for (int i = 0; i < n; ++i) {
+    for (int j = g.lane; j < n; j += G) {
+      double t = as[i] * bs[j + 1] - bs[i] * as[j + 1];
+      if (i > 0 && j + 1 < n) t += M[(i - 1) * n + j + 1];
+      M[i * n + j] = t;
+    }
+    g.sync();
+  }
+  int sign = 1;
+  double mant = 1.0;
+  int ex = 0;
+  for (int c = 0; c < n; ++c) {
+    double best = -1.0;
+    int piv = c;
+    for (int r = c + g.lane; r < n; r += G) {
+      const double x = fabs(M[r * n + c]);
+      if (x > best) {
+        best = x;
+        piv = r;
+      }
+    }
+    for (int o = G / 2; o; o >>= 1) {
+      const double ob = g.xor_(best, o);
+      const int op = g.xor_(piv, o);
+      if (ob > best || (ob == best && op < piv)) {
+        best = ob;
+        piv = op;
+      }
+    }
+    if (!(best > 0.0)) {
+      *lg = -INFINITY;
+      g.sync();
+      return 0;
+    }
+    if (piv != c) {
+      sign = -sign;
+      for (int l2 = c + g.lane; l2 < n; l2 += G) {
+        const double t = M[c * n + l2];
+        M[c * n + l2] = M[piv * n + l2];
+        M[piv * n + l2] = t;
+      }
+      g.sync();
+    }
+    const double d = M[c * n + c];
+    if (d < 0) sign = -sign;
+    int e;
+    mant = frexp(mant * fabs(d), &e);
+    ex += e;
+    for (int r = c + 1; r < n; ++r) {
+      const double fr = M[r * n + c] / d;
+      g.sync();
+      if (fr != 0.0)
+        for (int l2 = c + 1 + g.lane; l2 < n; l2 += G) M[r * n + l2] = fma(-fr, M[c * n + l2], M[r * n + l2]);
+    }
+    g.sync();
+  }
+  *lg = log(mant) + ex * 0.69314718055994530942;
+  return sign;
+}
+
+}  // namespace spoly

@@ -34,7 +34,8 @@ class spoly_config(ctypes.Structure):
                 ("polish_iters", ctypes.c_int), ("theta_admit", ctypes.c_double), ("theta_final", ctypes.c_double),
                 ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
                 ("cull", ctypes.c_int), ("deterministic", ctypes.c_int), ("cull_margin", ctypes.c_float),
-                ("max_solutions", ctypes.c_uint64), ("max_pairs", ctypes.c_uint64)]
+                ("max_solutions", ctypes.c_uint64), ("max_pairs", ctypes.c_uint64),
+                ("cull_levels", ctypes.c_int)]
 
 
 class spoly_tuple_list(ctypes.Structure):
@@ -51,7 +52,7 @@ class spoly_report(ctypes.Structure):
         ("n_launches", ctypes.c_uint32), ("n_eval_terms", ctypes.c_uint64), ("required_solutions", ctypes.c_uint64),
         ("ms_phase1", ctypes.c_float), ("ms_phase2", ctypes.c_float), ("n_rebuilds", ctypes.c_uint64),
         ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64),
-        ("n_elims", ctypes.c_uint64)]
+        ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -200,7 +201,8 @@ class Context:
                    n_launches=int(r.report.n_launches), n_eval_terms=int(r.report.n_eval_terms),
                    ms_phase1=r.report.ms_phase1, ms_phase2=r.report.ms_phase2, n_rebuilds=int(r.report.n_rebuilds),
                    alg_kflop=int(r.report.alg_kflop), n_jobs_mono=int(r.report.n_jobs_mono),
-                   n_jobs_deep=int(r.report.n_jobs_deep), n_elims=int(r.report.n_elims))
+                   n_jobs_deep=int(r.report.n_jobs_deep), n_elims=int(r.report.n_elims),
+                   n_pairs_coarse=int(r.report.n_pairs_coarse))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),

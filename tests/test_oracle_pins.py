@@ -9,7 +9,7 @@ import pytest
 
 import bruteforce
 from planted import planted_many
-from paper_2405_13409_b200.workloads import Mesh, patch_c1, random_triangles
+from paper_2405_13409_b200.workloads import sphere_c4, Mesh, patch_c1, random_triangles
 
 
 # ------------------------------------------------------------------ degrees (Table 2, Table 3)
@@ -404,12 +404,34 @@ def test_bruteforce_random_interpolated(orc, chain):
 
 
 # ------------------------------------------------------------------ cull soundness
-@pytest.mark.parametrize("chain", ["R", "T", "RR", "TT"])
+@pytest.mark.parametrize("chain", ["R", "T", "RR", "TT", "RT", "TR"])
 def test_cull_sound_on_planted(orc, chain):
     n = 300 if len(chain) == 1 else 60
+    levels = (0,) if len(chain) == 1 else (0, 2, 4)
     for size in (0.01, 0.3):
         for mesh, ids, x0, xk1, bary in planted_many(51, chain, n, size=size):
-            assert orc.cull_keep(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back)
+            for lv in levels:
+                assert orc.cull_keep(chain, orc.tri_block(mesh, ids), x0, xk1, mesh.eta_front, mesh.eta_back,
+                                     levels=lv), (lv, bary)
+
+
+def test_cull_subdivision_tightens_two_bounce(orc):
+    """SURVEY A1 refinement: on a C4-shaped sphere the subdivided pair test keeps a subset of the coarse
+    one (monotone in the depth) and strictly fewer pairs."""
+    w = sphere_c4(res=2, level=1)
+    x0, xk1 = w.endpoints[1]
+    m = w.mesh
+    kept = {lv: set() for lv in (0, 1, 3)}
+    for a in range(m.ntris):
+        for b in range(m.ntris):
+            if a == b:
+                continue
+            blk = orc.tri_block(m, [a, b])
+            for lv in kept:
+                if orc.cull_keep("TT", blk, x0, xk1, m.eta_front, m.eta_back, levels=lv):
+                    kept[lv].add((a, b))
+    assert kept[3] <= kept[1] <= kept[0]
+    assert len(kept[3]) < len(kept[0])
 
 
 def test_cull_actually_culls(orc):
