@@ -49,7 +49,7 @@ struct spoly_ctx {
   DBuf<TriRec> d_tris;
   DBuf<TriCull> d_tcull;
   DBuf<uint32_t> d_orig, d_perm;
-  DBuf<ClusterRec> d_cl, d_sub;
+  DBuf<ClusterRec> d_cl, d_sub, d_up[4];
   DBuf<uint32_t> d_tlist, d_tcount, d_qkeys, d_qorder;
   DBuf<float> d_qbounds;
   uint32_t tile_cap = 4096, tile_used_cap = 4096;
@@ -58,6 +58,9 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_offsets;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2;
   DBuf<unsigned char> d_keep;
+  DBuf<uint64_t> d_front;
+  DBuf<unsigned long long> d_fcount;
+  DBuf<uint32_t> d_fr[2][3];
   DBuf<double> d_rec;
   DBuf<uint32_t> d_plist;
   DBuf<unsigned long long> d_nsel;
@@ -152,11 +155,13 @@ void spoly_destroy(spoly_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
   ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
-  ctx->d_sub.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
+  ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
-  ctx->d_rec.release(); ctx->d_plist.release();
+  ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_front.release(); ctx->d_fcount.release();
+  for (auto& f : ctx->d_fr)
+    for (auto& b : f) b.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
@@ -241,6 +246,20 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   launch_build_tris(dpos, dnrm, dtri, dorder, ntris, ctx->cfg.cull_margin, ctx->d_tris.p, ctx->d_tcull.p,
                     ctx->d_orig.p, ctx->d_perm.p, ctx->st);
   launch_build_clusters(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, ctx->d_cl.p, ctx->d_sub.p, ctx->st);
+  // upper levels of the implicit 8-ary hierarchy (two-bounce pair cull) until <= 8 nodes
+  ctx->M.nupper = 0;
+  {
+    uint64_t n = ncl, size = kClusterSize;
+    for (int i = 0; i < 4 && n > 8; ++i) {
+      size *= 8;
+      n = (ntris + size - 1) / size;
+      CK(ctx->d_up[i].ensure(n));
+      launch_build_upper(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, 3 + i, ctx->d_up[i].p, (uint32_t)n, ctx->st);
+      ctx->M.upper[i] = ctx->d_up[i].p;
+      ctx->M.nupper_nodes[i] = (uint32_t)n;
+      ctx->M.nupper = i + 1;
+    }
+  }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->st));
   cudaFree(dpos);
@@ -334,35 +353,61 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else if (ctx->cfg.cull && k == 2) {
-    CK(ctx->d_counts.ensure(nq));
-    CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
-    uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
-    launch_cull_pairs(0, endpoints, nq, ctx->M, chain[0] == 'T', chain[1] == 'T', c32, nullptr, nullptr, nullptr,
-                      ctx->nsm, st);
-    ctx->launches++;
-    size_t tbytes = 0;
-    CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
-    CK(ctx->d_temp.ensure(tbytes));
-    CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
-    CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
-    unsigned long long tot = 0;
-    CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nq, sizeof(tot), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-    npairs = tot;
-    CK(ctx->d_pq.ensure(npairs));
-    CK(ctx->d_pt.ensure(npairs * k));
-    launch_cull_pairs(1, endpoints, nq, ctx->M, chain[0] == 'T', chain[1] == 'T', nullptr, ctx->d_offsets.p,
-                      ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
-    ctx->launches++;
+    uint32_t P = 0;
+    const int top = cull_split_level(ctx->M, &P);
+    if (top < 1) return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "two-bounce cull supports at most 2^22 triangles");
+    const int v1t = chain[0] == 'T', v2t = chain[1] == 'T';
+    const uint32_t *fq = nullptr, *fa = nullptr, *fb = nullptr;  // implicit root frontier
+    uint64_t nf = (uint64_t)nq * P;
+    int cur = 0;
+    for (int cl = top - 1; cl >= 0; --cl) {
+      CK(ctx->d_counts.ensure(nf / 2 + 1));
+      CK(ctx->d_offsets.ensure(nf + 1));
+      uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+      launch_pair_expand(0, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, nullptr, nullptr, nullptr, nullptr,
+                         ctx->nsm, st);
+      size_t tbytes = 0;
+      CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
+      CK(ctx->d_temp.ensure(tbytes));
+      CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
+      CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
+      unsigned long long tot = 0;
+      CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nf, sizeof(tot), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      if (cl == 0) {
+        CK(ctx->d_pq.ensure(tot));
+        CK(ctx->d_pt.ensure(2 * tot));
+        launch_pair_expand(1, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
+                           ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
+      } else {
+        const int nx = 1 - cur;
+        for (int c = 0; c < 3; ++c) CK(ctx->d_fr[nx][c].ensure(tot));
+        launch_pair_expand(1, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
+                           ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
+        fq = ctx->d_fr[nx][0].p;
+        fa = ctx->d_fr[nx][1].p;
+        fb = ctx->d_fr[nx][2].p;
+        cur = nx;
+      }
+      ctx->launches += 2;
+      nf = tot;
+    }
+    npairs = nf;
     if (ctx->cfg.cull_levels > 0 && npairs) {
       // barycentric subdivision refinement, then an order-preserving compaction (deterministic)
       CK(ctx->d_keep.ensure(npairs));
       CK(ctx->d_pq2.ensure(npairs));
       CK(ctx->d_pt2.ensure(2 * npairs));
       CK(ctx->d_nsel.ensure(4));
-      launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels,
-                          chain[0] == 'T', chain[1] == 'T', ctx->d_keep.p, ctx->nsm, st);
-      ctx->launches++;
+      {
+        const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * npairs, 1ull << 20), 1ull << 27);
+        CK(ctx->d_front.ensure(2 * fcap));
+        CK(ctx->d_fcount.ensure(16));
+        RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
+        launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels,
+                            chain[0] == 'T', chain[1] == 'T', ctx->d_keep.p, RW, ctx->nsm, st);
+        ctx->launches += RW.launches;
+      }
       const uint2* pt_in = reinterpret_cast<const uint2*>(ctx->d_pt.p);
       uint2* pt_out = reinterpret_cast<uint2*>(ctx->d_pt2.p);
       size_t tb1 = 0, tb2 = 0;

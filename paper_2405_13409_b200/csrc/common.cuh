@@ -67,6 +67,17 @@ struct DeviceMesh {
   uint32_t* perm_of = nullptr;    // [ntris] original id -> Morton position
   ClusterRec* clusters = nullptr; // [ceil(ntris/64)]
   ClusterRec* sub = nullptr;      // [ceil(ntris/8)]
+  int nupper = 0;                 // levels above the 64-clusters: 512, 4096, ... triangles (until <= 8 nodes)
+  ClusterRec* upper[4] = {nullptr, nullptr, nullptr, nullptr};
+  uint32_t nupper_nodes[4] = {0, 0, 0, 0};
+};
+
+// the implicit 8-ary Morton hierarchy as seen by the pair cull: level 0 = triangles, 1 = 8, 2 = 64, ...
+struct CullLevels {
+  const TriCull* tc;
+  const ClusterRec* lv[7];
+  uint32_t n[7];
+  int top;
 };
 
 __device__ __forceinline__ void load_tri(const TriRec* __restrict__ T, uint32_t i, d3 p[3], d3 n[3]) {

@@ -427,7 +427,7 @@ __device__ __forceinline__ bool pair_dir(float4 sa, float4 sb, f3& a, float& cho
 }
 
 __device__ __forceinline__ bool pair_keep(f3 x0, f3 x3, float4 sA, float4 nA, float4 sB, float4 nB, int v1t, int v2t,
-                                          float ef, float eb) {
+                                          float ef, float eb, int side = -1 /* x_0 front (0) / back (1) of T_1 */) {
   f3 a0, a3, aAB;
   float c0, c3, cAB;
   if (!sphere_dir(x0, sA, a0, c0) || !sphere_dir(x3, sB, a3, c3) || !pair_dir(sA, sB, aAB, cAB)) return true;
@@ -447,9 +447,11 @@ __device__ __forceinline__ bool pair_keep(f3 x0, f3 x3, float4 sA, float4 nA, fl
     }
     ncombo = 2;
   }
-  for (int c = 0; c < ncombo; ++c)
+  for (int c = 0; c < ncombo; ++c) {
+    if (ncombo == 2 && side >= 0 && c != side) continue;
     if (node_keep(a0, c0, aAB, cAB, e[c][0], e[c][1], nA) && node_keep(aBA, cAB, a3, c3, e[c][1], e[c][2], nB))
       return true;
+  }
   return false;
 }
 
@@ -474,96 +476,154 @@ __device__ __forceinline__ bool side_keep(const TriRec* __restrict__ tris, uint3
   return sg * dotf(q0 - p0, g) > tol || sg * dotf(q1 - p0, g) > tol || sg * dotf(q2 - p0, g) > tol;
 }
 
-// one warp per query; pass 0 counts, pass 1 writes (same traversal order -> deterministic list)
-__global__ void __launch_bounds__(256) k_cull_pairs(int pass, const double* __restrict__ ep, uint32_t nq,
-                                                    const TriRec* __restrict__ tris,
-                                                    const ClusterRec* __restrict__ l1,
-                                                    const ClusterRec* __restrict__ l2,
-                                                    const TriCull* __restrict__ tc, uint32_t ntris, uint32_t nl1,
-                                                    int v1t, int v2t, float ef, float eb, uint32_t* counts,
-                                                    const unsigned long long* __restrict__ offsets,
-                                                    uint32_t* __restrict__ pq, uint32_t* __restrict__ pt) {
+// Level-synchronous dual-tree expansion over the implicit 8-ary Morton hierarchy (levels: triangles, 8, 64,
+// 512, 4096, ... consecutive triangles).  The root frontier is every (query, node pair) of the split level
+// (the lowest level with <= 16 nodes); each expansion gives one warp per frontier entry, which tests the
+// entry's 64 child pairs (2 per lane) and keeps them in (entry, child) order.  Pass 0 counts per entry,
+// pass 1 writes at the scanned offsets (deterministic, query-major).  Every entry costs the same 64 tests,
+// so the work is balanced however unevenly the kept pairs are spread over queries (the same-surface
+// "diagonal" blocks of a mirror keep far more pairs than the rest).
+__device__ __forceinline__ void node_bounds(const CullLevels& L, int level, uint32_t i, float4& sphere, float4& cone) {
+  if (level == 0) {
+    sphere = L.tc[i].sphere;
+    cone = L.tc[i].cone;
+  } else {
+    const ClusterRec C = L.lv[level][i];
+    sphere = C.sphere;
+    cone = C.cone;
+  }
+}
+
+// fq == nullptr: implicit root frontier (entry e -> query e / P, pair e % P of the split level), the root
+// pair itself is tested first.  cl = level of the children (0: triangle pairs, written to pq / pt).
+__global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const double* __restrict__ ep,
+                                                     const uint32_t* __restrict__ fq, const uint32_t* __restrict__ fa,
+                                                     const uint32_t* __restrict__ fb, uint64_t nf,
+                                                     const TriRec* __restrict__ tris, CullLevels L, int v1t, int v2t,
+                                                     float ef, float eb, uint32_t* __restrict__ counts,
+                                                     const unsigned long long* __restrict__ offsets,
+                                                     uint32_t* __restrict__ oq, uint32_t* __restrict__ oa,
+                                                     uint32_t* __restrict__ ob) {
   const int lane = threadIdx.x & 31;
-  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t nl2 = (ntris + 7) >> 3;
-  const uint64_t npair1 = (uint64_t)nl1 * nl1;
-  for (uint32_t q = gw; q < nq; q += nw) {
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const uint32_t nt = L.n[L.top], P = nt * nt;
+  const uint32_t ncl = L.n[cl];
+  for (uint64_t en = gw; en < nf; en += nw) {
+    uint32_t q, A, B;
+    if (fq) {
+      q = fq[en];
+      A = fa[en];
+      B = fb[en];
+    } else {
+      q = (uint32_t)(en / P);
+      A = (uint32_t)(en % P) / nt;
+      B = (uint32_t)(en % P) % nt;
+    }
     const double* e = ep + 6ull * q;
     const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
     const f3 x3 = {(float)e[3], (float)e[4], (float)e[5]};
-    uint32_t count = 0;
-    unsigned long long wpos = pass ? offsets[q] : 0ull;
-    for (uint64_t b1 = 0; b1 < npair1; b1 += 32) {
-      const uint64_t p1 = b1 + lane;
-      bool k1 = false;
-      if (p1 < npair1) {
-        const ClusterRec A = l1[p1 / nl1], B = l1[p1 % nl1];
-        k1 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb);
-      }
-      uint32_t m1 = __ballot_sync(0xffffffffu, k1);
-      while (m1) {
-        const uint64_t cp = b1 + __ffs(m1) - 1;
-        m1 &= m1 - 1;
-        const uint32_t ca = (uint32_t)(cp / nl1), cb = (uint32_t)(cp % nl1);
-        // 64 sub-cluster pairs: 2 per lane
-        uint32_t m2[2];
+    bool root_ok = true;
+    if (!fq) {
+      float4 sa, ca, sb, cb;
+      node_bounds(L, cl + 1, A, sa, ca);
+      node_bounds(L, cl + 1, B, sb, cb);
+      root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
+    }
+    bool k[2] = {false, false};
+    if (root_ok) {
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int sp = h * 32 + lane;
-          const uint32_t sa = ca * 8 + (sp >> 3), sb = cb * 8 + (sp & 7);
-          bool k2 = false;
-          if (sa < nl2 && sb < nl2) {
-            const ClusterRec A = l2[sa], B = l2[sb];
-            k2 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb);
-          }
-          m2[h] = __ballot_sync(0xffffffffu, k2);
-        }
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          while (m2[h]) {
-            const int sp = h * 32 + __ffs(m2[h]) - 1;
-            m2[h] &= m2[h] - 1;
-            const uint32_t sa = ca * 8 + (sp >> 3), sb = cb * 8 + (sp & 7);
-            // 64 triangle pairs: 2 per lane, fixed order
-#pragma unroll
-            for (int g = 0; g < 2; ++g) {
-              const int tp = g * 32 + lane;
-              const uint32_t ta = sa * 8 + (tp >> 3), tb = sb * 8 + (tp & 7);
-              bool k3 = false;
-              if (ta < ntris && tb < ntris && ta != tb) {
-                const TriCull A = tc[ta], B = tc[tb];
-                k3 = pair_keep(x0, x3, A.sphere, A.cone, B.sphere, B.cone, v1t, v2t, ef, eb) &&
-                     side_keep(tris, ta, x0, v1t, tb) && side_keep(tris, tb, x3, v2t, ta);
+      for (int h = 0; h < 2; ++h) {
+        const int c = h * 32 + lane;
+        const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
+        if (a < ncl && b < ncl) {
+          if (cl == 0) {
+            if (a != b) {
+              const TriCull TA = L.tc[a], TB = L.tc[b];
+              // eta_0 from the side of x_0 w.r.t. T_1's plane (within float noise of the plane: both)
+              int side = -1;
+              if (v1t || v2t) {
+                const float sd = dotf(ld3(TA.plane), x0) - TA.plane.w;
+                const float gl = sqrtf(dotf(ld3(TA.plane), ld3(TA.plane)));
+                if (fabsf(sd) > 1e-4f * gl * (fabsf(x0.x) + fabsf(x0.y) + fabsf(x0.z) + 1.f)) side = sd > 0.f ? 0 : 1;
               }
-              const unsigned m3 = __ballot_sync(0xffffffffu, k3);
-              if (pass && k3) {
-                const unsigned long long pos = wpos + __popc(m3 & ((1u << lane) - 1u));
-                pq[pos] = q;
-                pt[2 * pos] = ta;
-                pt[2 * pos + 1] = tb;
-              }
-              wpos += __popc(m3);
-              count += __popc(m3);
+              k[h] = pair_keep(x0, x3, TA.sphere, TA.cone, TB.sphere, TB.cone, v1t, v2t, ef, eb, side) &&
+                     side_keep(tris, a, x0, v1t, b) && side_keep(tris, b, x3, v2t, a);
             }
+          } else {
+            float4 sa, ca, sb, cb;
+            node_bounds(L, cl, a, sa, ca);
+            node_bounds(L, cl, b, sb, cb);
+            k[h] = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
           }
         }
       }
     }
-    if (!pass && lane == 0) counts[q] = count;
+    const unsigned m0 = __ballot_sync(0xffffffffu, k[0]), m1 = __ballot_sync(0xffffffffu, k[1]);
+    const uint32_t c0 = __popc(m0), tot = c0 + __popc(m1);
+    if (!pass) {
+      if (lane == 0) counts[en] = tot;
+      continue;
+    }
+    const unsigned long long base = offsets[en];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if (k[h]) {
+        const int c = h * 32 + lane;
+        const unsigned long long pos = base + (h ? c0 : 0) + __popc((h ? m1 : m0) & lt);
+        const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
+        oq[pos] = q;
+        if (cl == 0) {
+          oa[2 * pos] = a;
+          oa[2 * pos + 1] = b;
+        } else {
+          oa[pos] = a;
+          ob[pos] = b;
+        }
+      }
+    }
   }
 }
 
-void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, int v1t, int v2t,
-                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
-                       cudaStream_t st) {
-  if (!nq) return;
+static CullLevels cull_levels_of(const DeviceMesh& M) {
+  CullLevels L;
+  L.tc = M.tcull;
+  L.lv[0] = nullptr;
+  L.lv[1] = M.sub;
+  L.lv[2] = M.clusters;
+  L.n[0] = M.ntris;
+  L.n[1] = (M.ntris + 7) / 8;
+  L.n[2] = M.nclusters;
+  int top = 2;
+  for (int i = 0; i < M.nupper; ++i) {
+    L.lv[3 + i] = M.upper[i];
+    L.n[3 + i] = M.nupper_nodes[i];
+    top = 3 + i;
+  }
+  while (top > 1 && L.n[top - 1] <= 16) --top;  // split level: the lowest (>= 1) with <= 16 nodes
+  L.top = L.n[top] <= 16 ? top : -1;
+  return L;
+}
+
+int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query) {
+  const CullLevels L = cull_levels_of(M);
+  if (L.top < 0) return -1;
+  *pairs_per_query = L.n[L.top] * L.n[L.top];
+  return L.top;
+}
+
+void launch_pair_expand(int pass, int cl, const double* ep, const uint32_t* fq, const uint32_t* fa,
+                        const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
+                        const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
+                        cudaStream_t st) {
+  if (!nf) return;
+  const CullLevels L = cull_levels_of(M);
   const int threads = 256;
-  uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
-  uint64_t cap = (uint64_t)nsm * 8;
-  int blocks = (int)(want < cap ? want : cap);
-  k_cull_pairs<<<blocks, threads, 0, st>>>(pass, ep, nq, M.tris, M.clusters, M.sub, M.tcull, M.ntris, M.nclusters, v1t, v2t,
-                                           M.eta_front, M.eta_back, counts, offsets, pq, pt);
+  const uint64_t want = (nf * 32 + threads - 1) / threads, cap = (uint64_t)nsm * 64;
+  k_pair_expand<<<(int)(want < cap ? want : cap), threads, 0, st>>>(pass, cl, ep, fq, fa, fb, nf, M.tris, L, v1t, v2t,
+                                                                    M.eta_front, M.eta_back, counts, offsets, oq,
+                                                                    oa, ob);
 }
 
 // ------------------------------------------------------------------ barycentric subdivision refinement (k=2)
@@ -684,68 +744,114 @@ __device__ uint32_t children_mask(const d3 P1[3], const d3 N1[3], const d3 P2[3]
   return m;
 }
 
-__global__ void __launch_bounds__(128) k_refine_pairs(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                                      uint64_t n, const TriRec* __restrict__ tris,
-                                                      const double* __restrict__ ep, int levels, int v1t, int v2t,
-                                                      float ef, float eb, uint8_t* __restrict__ keep) {
+// eta combinations of a pair: eta_0 from the side of x_0 w.r.t. T_1's plane (reading R9; sub-triangles
+// share the plane); within 1e-9 of the plane both media are tried
+__device__ __forceinline__ int eta_combos(d3 x0, const d3 P1[3], int v1t, int v2t, float ef, float eb,
+                                          double ec[2][3]) {
+  if (!v1t && !v2t) {
+    ec[0][0] = ec[0][1] = ec[0][2] = 1.0;
+    return 1;
+  }
+  const d3 g1 = cross(P1[1] - P1[0], P1[2] - P1[0]);
+  const double sd = dot(x0 - P1[0], g1), tol = 1e-9 * norm(g1) * (norm(x0 - P1[0]) + 1e-30);
+  int ncombo = 0;
+  for (int c = 0; c < 2; ++c) {
+    if ((c == 0 && sd < -tol) || (c == 1 && sd > tol)) continue;
+    const double s = c == 0 ? ef : eb, o = c == 0 ? eb : ef;
+    ec[ncombo][0] = s;
+    ec[ncombo][1] = v1t ? o : s;
+    ec[ncombo][2] = v2t ? (ec[ncombo][1] == s ? o : s) : ec[ncombo][1];
+    ++ncombo;
+  }
+  return ncombo;
+}
+
+// Breadth-first refinement: a frontier entry is (pair, sub-triangle of T_1, sub-triangle of T_2) at the
+// current level, packed in 64 bits: pair (32) | T_1 node (11: u 5, v 5, sigma 1) | T_2 node (11), node
+// coordinates in units of 2^-kMaxLevels.  One thread per entry tests its 16 child pairs; survivors are
+// appended (order irrelevant: only the per-pair keep flag is produced), at the last level any survivor
+// sets keep[pair] = 1.  An entry whose children overflow the frontier keeps its pair (conservative, sound).
+__device__ __forceinline__ uint64_t enc_node(int u, int v, int s) { return (uint64_t)(u | (v << 5) | ((s > 0) << 10)); }
+__device__ __forceinline__ void dec_node(uint64_t c, int& u, int& v, int& s) {
+  u = (int)(c & 31);
+  v = (int)((c >> 5) & 31);
+  s = ((c >> 10) & 1) ? 1 : -1;
+}
+
+__global__ void __launch_bounds__(128) k_refine_level(int level, int last, const uint32_t* __restrict__ pq,
+                                                      const uint32_t* __restrict__ pt, uint64_t npairs,
+                                                      const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                                      int v1t, int v2t, float ef, float eb,
+                                                      const uint64_t* __restrict__ fin,
+                                                      const unsigned long long* __restrict__ nin,
+                                                      uint64_t* __restrict__ fout, unsigned long long* __restrict__ nout,
+                                                      uint64_t cap, uint8_t* __restrict__ keep) {
+  const uint64_t n = fin ? min((uint64_t)*nin, cap) : npairs;  // appends beyond cap were not written
+  const int H = 1 << kMaxLevels, h = H >> level;  // node size at this level
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const double* e = ep + 6ull * pq[i];
+    SubNode nd;
+    uint32_t r;
+    if (fin) {
+      const uint64_t ent = fin[i];
+      r = (uint32_t)(ent >> 22);
+      dec_node((ent >> 11) & 2047, nd.u1, nd.v1, nd.s1);
+      dec_node(ent & 2047, nd.u2, nd.v2, nd.s2);
+      if (keep[r]) continue;  // already proven kept through another branch
+    } else {
+      r = (uint32_t)i;
+      nd = {0, 0, 1, 0, 0, 1};
+    }
+    const double* e = ep + 6ull * pq[r];
     const d3 x0 = mk3(e[0], e[1], e[2]), x3 = mk3(e[3], e[4], e[5]);
     d3 P1[3], N1[3], P2[3], N2[3];
-    load_tri(tris, pt[2 * i], P1, N1);
-    load_tri(tris, pt[2 * i + 1], P2, N2);
+    load_tri(tris, pt[2 * r], P1, N1);
+    load_tri(tris, pt[2 * r + 1], P2, N2);
     double ec[2][3];
-    int ncombo;
-    if (!v1t && !v2t) {
-      ec[0][0] = ec[0][1] = ec[0][2] = 1.0;
-      ncombo = 1;
-    } else {
-      for (int c = 0; c < 2; ++c) {
-        const double s = c == 0 ? ef : eb, o = c == 0 ? eb : ef;
-        ec[c][0] = s;
-        ec[c][1] = v1t ? o : s;
-        ec[c][2] = v2t ? (ec[c][1] == s ? o : s) : ec[c][1];
-      }
-      ncombo = 2;
+    const int ncombo = eta_combos(x0, P1, v1t, v2t, ef, eb, ec);
+    const uint32_t m = children_mask(P1, N1, P2, N2, x0, x3, nd, h, ec, ncombo);
+    if (!m) continue;
+    if (last) {
+      keep[r] = 1;
+      continue;
     }
-    SubNode stack[kMaxLevels];
-    uint32_t mask[kMaxLevels];
-    const int H = 1 << kMaxLevels;
-    stack[0] = {0, 0, 1, 0, 0, 1};
-    mask[0] = children_mask(P1, N1, P2, N2, x0, x3, stack[0], H, ec, ncombo);
-    int l = 0;
-    bool kept = false;
-    while (true) {
-      if (mask[l] == 0) {
-        if (l == 0) break;
-        --l;
-        continue;
-      }
-      const int c = __ffs(mask[l]) - 1;
-      mask[l] &= mask[l] - 1;
-      if (l + 1 >= levels) {
-        kept = true;
-        break;
-      }
-      const int h = H >> l;
+    const unsigned long long pos = atomicAdd(nout, (unsigned long long)__popc(m));
+    if (pos + __popc(m) > cap) {
+      keep[r] = 1;
+      continue;
+    }
+    uint32_t mm = m;
+    for (unsigned long long k = pos; mm; ++k) {
+      const int c = __ffs(mm) - 1;
+      mm &= mm - 1;
       SubNode ch;
-      child_of(stack[l].u1, stack[l].v1, stack[l].s1, h, c >> 2, ch.u1, ch.v1, ch.s1);
-      child_of(stack[l].u2, stack[l].v2, stack[l].s2, h, c & 3, ch.u2, ch.v2, ch.s2);
-      stack[l + 1] = ch;
-      mask[l + 1] = children_mask(P1, N1, P2, N2, x0, x3, ch, h >> 1, ec, ncombo);
-      ++l;
+      child_of(nd.u1, nd.v1, nd.s1, h, c >> 2, ch.u1, ch.v1, ch.s1);
+      child_of(nd.u2, nd.v2, nd.s2, h, c & 3, ch.u2, ch.v2, ch.s2);
+      fout[k] = ((uint64_t)r << 22) | (enc_node(ch.u1, ch.v1, ch.s1) << 11) | enc_node(ch.u2, ch.v2, ch.s2);
     }
-    keep[i] = kept ? 1 : 0;
   }
 }
 
 void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
-                         int levels, int v1t, int v2t, uint8_t* keep, int nsm, cudaStream_t st) {
+                         int levels, int v1t, int v2t, uint8_t* keep, RefineScratch& W, int nsm, cudaStream_t st) {
   if (!n) return;
   if (levels > kMaxLevels) levels = kMaxLevels;
-  const uint64_t want = (n + 127) / 128, cap = (uint64_t)nsm * 16;
-  k_refine_pairs<<<(int)(want < cap ? want : cap), 128, 0, st>>>(pq, pt, n, M.tris, ep, levels, v1t, v2t,
-                                                                  M.eta_front, M.eta_back, keep);
+  cudaMemsetAsync(keep, 0, n, st);
+  cudaMemsetAsync(W.count, 0, 2 * levels * sizeof(unsigned long long), st);
+  const uint64_t* fin = nullptr;
+  const unsigned long long* nin = nullptr;
+  for (int l = 0; l < levels; ++l) {
+    const int last = l + 1 == levels;
+    uint64_t* fout = W.front[l & 1];
+    unsigned long long* nout = W.count + l;
+    const uint64_t work = fin ? W.cap : n;  // device-side count bounds the loop
+    const uint64_t want = (work + 127) / 128, cap = (uint64_t)nsm * 16;
+    k_refine_level<<<(int)(want < cap ? want : cap), 128, 0, st>>>(l, last, pq, pt, n, M.tris, ep, v1t, v2t,
+                                                                    M.eta_front, M.eta_back, fin, nin, fout, nout,
+                                                                    W.cap, keep);
+    fin = fout;
+    nin = nout;
+  }
+  W.launches = levels;
 }
 
 }  // namespace spoly

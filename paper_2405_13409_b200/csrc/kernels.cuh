@@ -8,6 +8,8 @@ namespace spoly {
 void launch_build_tris(const float* pos, const float* nrm, const uint32_t* tri, const uint32_t* order, uint32_t ntris,
                        float margin, TriRec* recs, TriCull* tc, uint32_t* orig_id, uint32_t* perm_of,
                        cudaStream_t st);
+void launch_build_upper(const TriRec* recs, uint32_t ntris, float margin, int level, ClusterRec* out, uint32_t n,
+                        cudaStream_t st);
 void launch_build_clusters(const TriRec* recs, uint32_t ntris, float margin, ClusterRec* l1, ClusterRec* l2,
                            cudaStream_t st);
 
@@ -43,11 +45,20 @@ uint64_t k2_record_bytes(int v1t, int v2t);
 void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
                      const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
                      int nsm, cudaStream_t st);
-void launch_cull_pairs(int pass, const double* ep, uint32_t nq, const DeviceMesh& M, int v1t, int v2t,
-                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
-                       cudaStream_t st);
+// two-bounce pair cull: split level of the implicit hierarchy (-1: > 2^22 triangles) and one expansion pass
+int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query);
+void launch_pair_expand(int pass, int cl, const double* ep, const uint32_t* fq, const uint32_t* fa,
+                        const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
+                        const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
+                        cudaStream_t st);
+struct RefineScratch {
+  uint64_t* front[2];  // frontier ping-pong, cap entries each
+  uint64_t cap;
+  unsigned long long* count;  // >= 2 * levels
+  int launches;
+};
 void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
-                         int levels, int v1t, int v2t, uint8_t* keep, int nsm, cudaStream_t st);
+                         int levels, int v1t, int v2t, uint8_t* keep, RefineScratch& W, int nsm, cudaStream_t st);
 void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 
 // reduce.cu

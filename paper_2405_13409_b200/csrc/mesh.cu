@@ -124,6 +124,18 @@ __global__ void k_build_clusters(const TriRec* __restrict__ recs, uint32_t ntris
   }
 }
 
+void launch_build_upper(const TriRec* recs, uint32_t ntris, float margin, int level /* 3.. */, ClusterRec* out,
+                        uint32_t n, cudaStream_t st) {
+  const int threads = 128, blocks = (int)((n * 32ull + threads - 1) / threads);
+  if (!n) return;
+  switch (level) {
+    case 3: k_build_clusters<512><<<blocks, threads, 0, st>>>(recs, ntris, margin, out, n); break;
+    case 4: k_build_clusters<4096><<<blocks, threads, 0, st>>>(recs, ntris, margin, out, n); break;
+    case 5: k_build_clusters<32768><<<blocks, threads, 0, st>>>(recs, ntris, margin, out, n); break;
+    default: k_build_clusters<262144><<<blocks, threads, 0, st>>>(recs, ntris, margin, out, n); break;
+  }
+}
+
 void launch_build_clusters(const TriRec* recs, uint32_t ntris, float margin, ClusterRec* l1, ClusterRec* l2,
                            cudaStream_t st) {
   const uint32_t n1 = (ntris + kClusterSize - 1) / kClusterSize, n2 = (ntris + kSubSize - 1) / kSubSize;
