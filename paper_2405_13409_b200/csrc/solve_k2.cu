@@ -53,7 +53,7 @@ struct Deg2 {
   static constexpr int G = (DB <= 15) ? 16 : 32;                               // lanes per system
   // shared-memory arena per group (doubles): persistent a, b, U, V, K + the build temporaries (peak) +
   // the v-root list; the n > 32 determinant scratch reuses the temporaries (TT only)
-  static constexpr int ARENA = (!V1T && !V2T) ? 1024 : (!V1T ? 1536 : (!V2T ? 3072 : 3712));
+  static constexpr int ARENA = (!V1T && !V2T) ? 640 : (!V1T ? 768 : (!V2T ? 1984 : 2560));
 };
 
 struct Sys2w {
@@ -192,6 +192,14 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   wlin2(g, D2.x, S.K, x3.x, X2.x, -1.0, false);
   wlin2(g, D2.y, S.K, x3.y, X2.y, -1.0, false);
   wlin2(g, D2.z, S.K, x3.z, X2.z, -1.0, false);
+  // only d~, N2, D2 are live from here: compact them to the bottom of the temporary region
+  {
+    double* dst = S.K.c + tri_n(DK);
+    dst = wmovev(g, Dt, dst);
+    dst = wmovev(g, N2, dst);
+    dst = wmovev(g, D2, dst);
+    ar.top = (int)(dst - ar.base);
+  }
   if (!V2T) {
     // b = (d~.N2)(D2.T2) + (d~.T2)(D2.N2), T2 = N2 x e21   (Eq. 12 with d~_1, Eq. 23)
     WV Tt = ar.vec(DU);
@@ -211,6 +219,18 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
     wdot(g, Q, D2, Nl, 1.0, false);
     wdot(g, d22, D2, D2, 1.0, false);
     wdot(g, dt2, Dt, Dt, 1.0, false);
+    {  // only P, Q, D2^2, d~^2 are live from here
+      double* dst = S.K.c + tri_n(DK);
+      wmove(g, P, dst);
+      dst += tri_n(P.d);
+      wmove(g, Q, dst);
+      dst += tri_n(Q.d);
+      wmove(g, d22, dst);
+      dst += tri_n(d22.d);
+      wmove(g, dt2, dst);
+      dst += tri_n(dt2.d);
+      ar.top = (int)(dst - ar.base);
+    }
     WP PQ2 = ar.poly(4 * DU);
     WP P2{PQ2.c, 2 * (DK + DU)};
     wmul1(g, P2, P, P, 1.0, false);

@@ -93,13 +93,21 @@ __device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], 
       const int da = a[k].d, db = b[k].d;
       double t = 0.0;
       const int p0 = max(0, i - db), p1 = min(i, da);
+      double t2 = 0.0;
       for (int p = p0; p <= p1; ++p) {
         const int q0 = max(0, i + j - p - db), q1 = min(j, da - p);
         const double* ap = a[k].c + poff(da, p);
         const double* bp = b[k].c + poff(db, i - p) + j;
-        for (int q = q0; q <= q1; ++q) t = fma(ap[q], bp[-q], t);
+        int q = q0;
+        for (; q + 3 <= q1; q += 4) {  // two accumulators, 4-way unrolled
+          t = fma(ap[q], bp[-q], t);
+          t2 = fma(ap[q + 1], bp[-q - 1], t2);
+          t = fma(ap[q + 2], bp[-q - 2], t);
+          t2 = fma(ap[q + 3], bp[-q - 3], t2);
+        }
+        for (; q <= q1; ++q) t = fma(ap[q], bp[-q], t);
       }
-      sum = fma(s[k], t, sum);
+      sum = fma(s[k], t + t2, sum);
     }
     c.c[idx] = sum;
     padv(dc, G, i, j);
@@ -200,6 +208,30 @@ __device__ __forceinline__ void wcross(const Grp<G>& g, const WV& R, const WV& A
   wmul2(g, R.x, A.y, B.z, 1.0, A.z, B.y, -1.0, false);
   wmul2(g, R.y, A.z, B.x, 1.0, A.x, B.z, -1.0, false);
   wmul2(g, R.z, A.x, B.y, 1.0, A.y, B.x, -1.0, false);
+}
+
+// move a polynomial to a lower address of the arena (ascending chunks: safe for overlapping ranges)
+template <int G>
+__device__ void wmove(const Grp<G>& g, WP& p, double* dst) {
+  const int n = tri_n(p.d);
+  if (dst == p.c) return;
+  for (int b0 = 0; b0 < n; b0 += G) {
+    const int i = b0 + g.lane;
+    const double v = i < n ? p.c[i] : 0.0;
+    g.sync();
+    if (i < n) dst[i] = v;
+    g.sync();
+  }
+  p.c = dst;
+}
+template <int G>
+__device__ __forceinline__ double* wmovev(const Grp<G>& g, WV& V, double* dst) {
+  wmove(g, V.x, dst);
+  dst += tri_n(V.x.d);
+  wmove(g, V.y, dst);
+  dst += tri_n(V.y.d);
+  wmove(g, V.z, dst);
+  return dst + tri_n(V.z.d);
 }
 
 // ------------------------------------------------------------------ scalar evaluation (one lane)
