@@ -36,7 +36,8 @@ UNIT = "paths/s"
 #                      + coplanarity sign test 16                                            = 484
 #            per pair reaching the elimination (counter n_elims): Bezout 128 + Laplace 316
 #                      + normalise r 11 + Bernstein level 155                                = 610
-#   phase 2: 2 per FMA term of the root-finding evaluations (counter n_eval_terms)
+#   roots  : 2 per FMA term of the root-finding evaluations (counter n_eval_terms)   [k1_roots]
+#   path   :                                                                        [k1_path]
 #            + 468 per coefficient-phase rebuild (counter n_rebuilds)
 #            + 430 per candidate (back-substitution 25, one (a,b) Newton step 277, Eq. 3 + sides 130)
 #            + 250 per admissible chain (analytic ray-differential Jacobian)
@@ -59,24 +60,21 @@ FLOP_PER_CANDIDATE_T = 755
 FLOP_PER_ADMISSIBLE_T = 300
 
 
-def flop_model_R(rep):
-    p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_R + rep["n_elims"] * FLOP_PHASE1_PER_ELIM_R
-    p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_R +
-          rep["n_candidates"] * FLOP_PER_CANDIDATE_R + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_R)
-    return p1, p2
-
-
 def flop_model(chain, rep):
-    """(phase-1 FLOPs, phase-2 FLOPs) per solve; for two bounces phase 1 is empty and phase 2 is the
-    single two-bounce kernel, whose algorithmic kFLOP the kernel counts itself (alg_kflop)."""
-    if chain == "R":
-        return flop_model_R(rep)
-    if chain == "T":
-        p1 = rep["n_pairs_in"] * FLOP_PHASE1_PER_PAIR_T + rep["n_elims"] * FLOP_PHASE1_PER_ELIM_T
-        p2 = (rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_rebuilds"] * FLOP_PER_REBUILD_T +
-              rep["n_candidates"] * FLOP_PER_CANDIDATE_T + rep["n_admissible"] * FLOP_PER_ADMISSIBLE_T)
-        return p1, p2
-    return 0.0, rep["alg_kflop"] * 1e3
+    """{kernel: algorithmic FLOPs per solve}.  One bounce: phase 1, the root kernels (k1_roots + deep jobs)
+    and the path kernel; two bounces: the build + scan kernels, whose algorithmic kFLOP the kernels count
+    themselves (alg_kflop)."""
+    if len(chain) == 1:
+        R = chain == "R"
+        p1 = rep["n_pairs_in"] * (FLOP_PHASE1_PER_PAIR_R if R else FLOP_PHASE1_PER_PAIR_T) + rep["n_elims"] * (
+            FLOP_PHASE1_PER_ELIM_R if R else FLOP_PHASE1_PER_ELIM_T)
+        roots = rep["n_eval_terms"] * FLOP_PER_EVAL_TERM
+        path = (rep["n_rebuilds"] * (FLOP_PER_REBUILD_R if R else FLOP_PER_REBUILD_T) +
+                rep["n_candidates"] * (FLOP_PER_CANDIDATE_R if R else FLOP_PER_CANDIDATE_T) +
+                rep["n_admissible"] * (FLOP_PER_ADMISSIBLE_R if R else FLOP_PER_ADMISSIBLE_T))
+        return {f"k1_phase1<{chain}>": (p1, "ms_phase1"), f"k1_roots<{chain}>": (roots, "ms_roots"),
+                f"k1_path<{chain}>": (path, "ms_path")}
+    return {f"k2_solve<{chain}>": (rep["alg_kflop"] * 1e3, "ms_phase2")}
 
 
 # FP64 ALU peak from unit counts and clocks (B200_PROFILING.md: 148 SMs, clocks.max.sm 1965 MHz;
@@ -287,13 +285,18 @@ def main():
     # ---- roofline of the dominant kernel, from its own launch's CUDA-event time (recorded by the library on
     # the launching stream around each solve kernel, averaged over the timed steps)
     rep = reports[-1]
-    f1, f2 = flop_model(chain, rep)
-    t1 = statistics.mean(x["ms_phase1"] for x in reports) / 1e3
-    t2 = statistics.mean(x["ms_phase2"] for x in reports) / 1e3
     peak = fp64_peak()
-    k1n, k2n = (f"k1_phase1<{chain}>", f"k1_phase2<{chain}>") if len(chain) == 1 else ("-", f"k2_solve<{chain}>")
-    dom = (k2n, f2, t2) if t2 >= t1 else (k1n, f1, t1)
-    achieved = dom[1] / dom[2]
+    phases = {}
+    for kname, (flop, key) in flop_model(chain, rep).items():
+        tk = statistics.mean(x[key] for x in reports) / 1e3
+        phases[kname] = {"ms": tk * 1e3, "flop": flop, "tflops": flop / tk / 1e12 if tk > 0 else None,
+                         "frac": flop / tk / peak if tk > 0 else None}
+    dname = max(phases, key=lambda kk: phases[kk]["ms"])
+    dom = (dname, phases[dname]["flop"], phases[dname]["ms"] / 1e3)
+    achieved = dom[1] / dom[2] if dom[2] > 0 else 0.0
+    tsum = sum(v["ms"] for v in phases.values()) / 1e3
+    phases["solve_total"] = {"ms": tsum * 1e3, "frac": sum(v["flop"] for v in phases.values()) / tsum / peak
+                             if tsum > 0 else None}
     traffic = None
     tp = os.path.join(ROOT, "profiles", "solve_traffic.json")
     if os.path.exists(tp):
@@ -334,10 +337,7 @@ def main():
                      "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic, "flop_per_launch": dom[1],
                      "peak_note": "FP64: 148 SMs x 64 FMA/clk x 2 x 1965 MHz (unit counts x clocks.max.sm)",
                      "measured_fp64_fma_tflops": measured_fp64 / 1e12 if measured_fp64 else None,
-                     "phases": {k1n: {"ms": t1 * 1e3, "tflops": f1 / t1 / 1e12 if t1 > 0 else None,
-                                      "frac": f1 / t1 / peak if t1 > 0 else None},
-                                k2n: {"ms": t2 * 1e3, "tflops": f2 / t2 / 1e12, "frac": f2 / t2 / peak},
-                                "solve_total": {"ms": (t1 + t2) * 1e3, "frac": (f1 + f2) / (t1 + t2) / peak}}},
+                     "phases": phases},
         "clocks": clocks,
         "gpu_launches": launches,
     }

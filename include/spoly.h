@@ -116,6 +116,8 @@ typedef struct {
   uint64_t n_elims;                   /* one-bounce pairs that reached the elimination phase       */
   uint64_t n_pairs_coarse;            /* two-bounce pair cull: pairs kept before the subdivision
                                          refinement (n_pairs_in counts the refined list)            */
+  float ms_roots, ms_path;            /* one-bounce phase 2 split: root finding (k1_roots + deep
+                                         jobs) and path kernel (incl. the count read-back)          */
 } spoly_report;
 
 typedef struct {

@@ -80,7 +80,7 @@ struct spoly_ctx {
   DBuf<double> d_ep, d_int;
   double* h_pinned = nullptr;
   size_t h_pinned_cap = 0;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev[7] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
   uint32_t launches = 0;
 };
 
@@ -538,7 +538,10 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       CK(cudaEventRecord(ctx->ev[5], st));
       launch_solve_k1(2, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
                       ctx->nsm, st);
-      ctx->launches += 2;
+      CK(cudaEventRecord(ctx->ev[6], st));
+      launch_solve_k1(3, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
+                      ctx->nsm, st);
+      ctx->launches += 4;
     } else {
       CK(cudaEventRecord(ctx->ev[5], st));
       {
@@ -677,6 +680,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   if (npairs) {
     cudaEventElapsedTime(&R.ms_phase1, ctx->ev[4], ctx->ev[5]);
     cudaEventElapsedTime(&R.ms_phase2, ctx->ev[5], ctx->ev[2]);
+  }
+  R.ms_roots = R.ms_path = 0.f;
+  if (npairs && k == 1) {
+    cudaEventElapsedTime(&R.ms_roots, ctx->ev[5], ctx->ev[6]);
+    cudaEventElapsedTime(&R.ms_path, ctx->ev[6], ctx->ev[2]);
   }
   R.n_rebuilds = counters[C_REBUILDS];
   R.alg_kflop = counters[C_KFLOP];

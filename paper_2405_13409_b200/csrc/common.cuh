@@ -119,7 +119,7 @@ struct JobSink {
   uint64_t capacity;
   uint32_t* pair;
   uint32_t* meta;  // kfree | deg << 8
-  double* r;       // kJobStride per job
+  double* r;       // kJobStride per job (phase 2 overwrites it with [count, roots...])
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,

@@ -380,64 +380,188 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
   }
 }
 
+// ---- phase 2a: roots of r on [0, 1] for the monotone jobs.  Each lane owns one job at a time and takes a
+// new one as soon as its Newton iteration converges, so the lanes of a warp stay busy however different
+// their iteration counts are (the fused per-job loop ran at 8.5 of 32 lanes).  Jobs are taken from a
+// warp-private chunk of consecutive jobs (uniform cursor, no atomics); the root overwrites the job's
+// coefficient slot: [0] = count (0 or 1), [1] = root.
+constexpr int kRootChunk = 512;
 template <bool TC>
-__global__ void __launch_bounds__(128) k1_phase2(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                                 const TriRec* __restrict__ tris, const double* __restrict__ ep,
-                                                 const double* __restrict__ inten, SolveParams prm, SolSink S,
-                                                 const unsigned long long* __restrict__ njobs_p, uint64_t jcap,
-                                                 const uint32_t* __restrict__ jpair, const uint32_t* __restrict__ jmeta,
-                                                 const double* __restrict__ jr) {
+__global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
+  constexpr int NR = Sys1<TC>::NR;
+  constexpr unsigned FULL = 0xffffffffu;
+  uint32_t cnt[C_NUM];
+#pragma unroll
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t nmono = J.count[0];
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  // chunk: enough jobs per warp to amortise the refills, small enough to spread short lists over all warps
+  uint64_t kc = (nmono + nw - 1) / nw;
+  kc = kc < 32 ? 32 : (kc > kRootChunk ? kRootChunk : (kc + 31) & ~31ull);
+  uint64_t chunk = gw;
+  uint64_t cur = chunk * kc, cend = cur + kc < nmono ? cur + kc : nmono;
+  bool busy = false;
+  uint64_t jj = 0;
+  double c[NR];
+  double a = 0.0, b = 1.0, x = 0.0, flo = 0.0;
+  int it = 0;
+  while (true) {
+    // refill idle lanes from the warp's chunk (uniform cursor)
+    unsigned idle = __ballot_sync(FULL, !busy);
+    while (idle && cur >= cend && chunk * kc < nmono) {
+      chunk += nw;
+      cur = chunk * kc;
+      cend = cur + kc < nmono ? cur + kc : nmono;
+      if (cur >= nmono) cur = cend = nmono;
+    }
+    if (!busy && cur < cend) {
+      const uint64_t my = cur + __popc(idle & lt);
+      if (my < cend) {
+        jj = my;
+#pragma unroll
+        for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * kJobStride + i);
+        double f1 = c[NR - 1];
+#pragma unroll
+        for (int i = NR - 2; i >= 0; --i) f1 += c[i];  // r(1)
+        const double f0 = c[0];
+        cnt[C_EVAL_TERMS] += 2 * NR;
+        if (f0 == 0.0 || f1 == 0.0 || (f0 < 0.0) == (f1 < 0.0)) {
+          // exact endpoint root, or (rounding) no sign change: finish at once
+          const bool has = f0 == 0.0 || f1 == 0.0;
+          J.r[jj * kJobStride] = has ? 1.0 : 0.0;
+          J.r[jj * kJobStride + 1] = f0 == 0.0 ? 0.0 : 1.0;
+          cnt[C_VROOTS] += has;
+        } else {
+          a = 0.0;
+          b = 1.0;
+          flo = f0;
+          x = -f0 / (f1 - f0);  // secant start
+          if (!(x > a && x < b)) x = 0.5;
+          it = 0;
+          busy = true;
+        }
+      }
+    }
+    if (idle) cur = cur + __popc(idle) < cend ? cur + __popc(idle) : cend;
+    if (!__any_sync(FULL, busy)) {
+      if (cur >= cend && chunk * kc >= nmono) break;
+      continue;
+    }
+    if (busy) {
+      // one safeguarded Newton step (same rule as monotone_root)
+      double f = c[NR - 1], fp = 0.0;
+#pragma unroll
+      for (int i = NR - 2; i >= 0; --i) {
+        fp = fma(fp, x, f);
+        f = fma(f, x, c[i]);
+      }
+      cnt[C_EVAL_TERMS] += 2 * NR - 1;
+      ++it;
+      bool fin = false;
+      double xr = x;
+      if (f != 0.0) {
+        if ((f < 0.0) == (flo < 0.0))
+          a = x;
+        else
+          b = x;
+        double xn = x - f * fast_rcp(fp);
+        if (!(xn > a && xn < b)) xn = 0.5 * (a + b);
+        fin = fabs(xn - x) <= 1e-12 || b - a <= 1e-15 || it >= 100;
+        xr = xn;
+        x = xn;
+      } else {
+        fin = true;
+      }
+      if (fin) {
+        J.r[jj * kJobStride] = 1.0;
+        J.r[jj * kJobStride + 1] = xr;
+        cnt[C_VROOTS]++;
+        busy = false;
+      }
+    }
+  }
+  flush_counters(S, cnt);
+}
+
+// ---- phase 2a': jobs with a deeper derivative recursion (~1%), thread per job
+template <bool TC>
+__global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint64_t jcap, SolveParams prm) {
   constexpr int NR = Sys1<TC>::NR;
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t nmono = njobs_p[0], ndeep = njobs_p[1];
-  const uint64_t njobs = nmono + ndeep;
+  const uint64_t ndeep = J.count[1];
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
-  for (uint64_t base = gw * 32; base < njobs; base += nw * 32) {
-    const uint64_t j = base + lane;
-    const bool active = j < njobs;
+  for (uint64_t base = gw * 32; base < ndeep; base += nw * 32) {
+    const uint64_t d = base + lane;
+    const bool active = d < ndeep;
+    const uint64_t jj = active ? jcap - 1 - d : 0;
+    uint32_t flags = 0, pair = 0;
+    int nv = 0;
+    double vr[NR];
+    if (active) {
+      pair = __ldg(J.pair + jj);
+      const uint32_t meta = __ldg(J.meta + jj);
+      double r[NR];
+#pragma unroll
+      for (int i = 0; i < NR; ++i) r[i] = __ldg(J.r + jj * kJobStride + i);
+      RootSet<NR> R;
+      isolate_roots<NR>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+      cnt[C_EVAL_TERMS] += R.terms;
+      if (R.flags & 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
+      if (R.min_crit_ratio <= 1e-10) flags |= SPOLY_FLAG_NEAR_TANGENT;
+      for (int i = 0; i < R.n; ++i)
+        if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
+      cnt[C_VROOTS] += nv;
+      J.r[jj * kJobStride] = (double)nv;
+      for (int i = 0; i < nv; ++i) J.r[jj * kJobStride + 1 + i] = vr[i];
+    }
+    emit_flag(active && flags != 0, flags, pair, S);
+  }
+  flush_counters(S, cnt);
+}
+
+// ---- phase 2b: back-substitution, refinement, validation, contribution, emission; thread per job (jobs
+// without roots exit at once)
+template <bool TC>
+__global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                               const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                               const double* __restrict__ inten, SolveParams prm, SolSink S,
+                                               JobSink J) {
+  constexpr int NR = Sys1<TC>::NR;
+  uint32_t cnt[C_NUM];
+#pragma unroll
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t nmono = J.count[0], n = nmono + J.count[1];
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = gw * 32; base < n; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const uint64_t jj = i < nmono ? i : J.capacity - 1 - (i - nmono);
+    const int nv = i < n ? (int)J.r[jj * kJobStride] : 0;
+    const bool active = nv > 0;
     PairOut o;
     o.nsol = 0;
     o.flags = 0;
     uint32_t pair = 0;
     if (active) {
-      const uint64_t jj = j < nmono ? j : jcap - 1 - (j - nmono);
-      pair = __ldg(jpair + jj);
-      const uint32_t meta = __ldg(jmeta + jj);
-      double r[NR];
-#pragma unroll
-      for (int t = 0; t < NR; ++t) r[t] = __ldg(jr + jj * kJobStride + t);
-      RootSet<NR> R;
-      if ((meta & 0xFF) == 1) {
-        // r' has no root in [0,1] (Bernstein): r is monotone there, at most one root, no critical point
-        R.flags = 0;
-        R.min_crit_ratio = 1.0;
-        R.terms = 0;
-        R.n = monotone_root<NR>(r, 0.0, 1.0, &R.x[0], &R.terms);
-      } else {
-        isolate_roots<NR>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
-      }
-      cnt[C_EVAL_TERMS] += R.terms;
-      if (R.flags & 1) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
-      if (R.min_crit_ratio <= 1e-10) o.flags |= SPOLY_FLAG_NEAR_TANGENT;
+      pair = __ldg(J.pair + jj);
       double vr[NR];
-      int nv = 0;
-      for (int i = 0; i < R.n; ++i)
-        if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
-      cnt[C_VROOTS] += nv;
-      if (nv > 0) {
-        d3 P[3], N[3], x0, x2;
-        uint32_t q;
-        load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
-        Sys1<TC> Sys;
-        build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
-        cnt[C_REBUILDS]++;
-        const double I = inten ? __ldg(inten + q) : 1.0;
-        path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
-      }
+      for (int k = 0; k < nv; ++k) vr[k] = J.r[jj * kJobStride + 1 + k];
+      d3 P[3], N[3], x0, x2;
+      uint32_t q;
+      load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
+      Sys1<TC> Sys;
+      build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
+      cnt[C_REBUILDS]++;
+      const double I = inten ? __ldg(inten + q) : 1.0;
+      path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
     }
     emit_flag(active && o.flags != 0, o.flags, pair, S);
     uint32_t ex;
@@ -469,13 +593,19 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
     else
       k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-  } else {
+  } else if (phase == 2) {  // roots
+    if (refract) {
+      k1_roots<true><<<(int)cap, threads, 0, st>>>(S, J);
+      k1_roots_deep<true><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
+    } else {
+      k1_roots<false><<<(int)cap, threads, 0, st>>>(S, J);
+      k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
+    }
+  } else {  // path
     if (refract)
-      k1_phase2<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
-                                                     J.meta, J.r);
+      k1_path<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
     else
-      k1_phase2<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J.count, J.capacity, J.pair,
-                                                      J.meta, J.r);
+      k1_path<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
   }
 }
 

@@ -52,7 +52,8 @@ class spoly_report(ctypes.Structure):
         ("n_launches", ctypes.c_uint32), ("n_eval_terms", ctypes.c_uint64), ("required_solutions", ctypes.c_uint64),
         ("ms_phase1", ctypes.c_float), ("ms_phase2", ctypes.c_float), ("n_rebuilds", ctypes.c_uint64),
         ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64),
-        ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64)]
+        ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64),
+        ("ms_roots", ctypes.c_float), ("ms_path", ctypes.c_float)]
 
 
 class spoly_result(ctypes.Structure):
@@ -202,7 +203,8 @@ class Context:
                    ms_phase1=r.report.ms_phase1, ms_phase2=r.report.ms_phase2, n_rebuilds=int(r.report.n_rebuilds),
                    alg_kflop=int(r.report.alg_kflop), n_jobs_mono=int(r.report.n_jobs_mono),
                    n_jobs_deep=int(r.report.n_jobs_deep), n_elims=int(r.report.n_elims),
-                   n_pairs_coarse=int(r.report.n_pairs_coarse))
+                   n_pairs_coarse=int(r.report.n_pairs_coarse), ms_roots=r.report.ms_roots,
+                   ms_path=r.report.ms_path)
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),
