@@ -58,6 +58,7 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_offsets;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2;
   DBuf<unsigned char> d_keep;
+  DBuf<uint32_t> d_qmask;
   DBuf<uint64_t> d_front;
   DBuf<unsigned long long> d_fcount;
   DBuf<uint32_t> d_fr[2][3];
@@ -159,7 +160,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
-  ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_front.release(); ctx->d_fcount.release();
+  ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
     for (auto& b : f) b.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
@@ -468,8 +469,9 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(ctx->d_counts.ensure(nq));
     CK(ctx->d_offsets.ensure((uint64_t)nq + 1));
     uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+    CK(ctx->d_qmask.ensure((uint64_t)nq * ((cap + 31) / 32)));
     launch_query_cull(0, endpoints, nq, order, ctx->M, chain[0] == 'T', cap, ctx->d_tlist.p, ctx->d_tcount.p, c32,
-                      nullptr, nullptr, nullptr, ctx->nsm, st);
+                      ctx->d_qmask.p, nullptr, nullptr, nullptr, ctx->nsm, st);
     ctx->launches++;
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
@@ -483,7 +485,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
     launch_query_cull(1, endpoints, nq, order, ctx->M, chain[0] == 'T', cap, ctx->d_tlist.p, ctx->d_tcount.p,
-                      nullptr, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+                      nullptr, ctx->d_qmask.p, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else {
     npairs = k == 1 ? (uint64_t)nq * ctx->M.ntris : (uint64_t)nq * ctx->M.ntris * (ctx->M.ntris - 1);

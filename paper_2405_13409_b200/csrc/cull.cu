@@ -294,20 +294,21 @@ void launch_tile_cull(const double* ep, uint32_t nq, const uint32_t* order, cons
                                                     M.eta_front, M.eta_back, cap, tile_list, tile_count, max_count);
 }
 
-// one warp per (sorted) query: exact per-query triangle test on its tile's survivors; pass 0 counts,
-// pass 1 writes the query-major work list at the scanned offsets (ascending Morton order)
+// per query (one warp) on its tile's surviving triangles: cone test + Eq. 6 sign test; the keep masks
+// (one 32-bit ballot per 32 tile entries) and the per-query count are stored, and k_query_expand writes
+// the query-major list from them at the scanned offsets (the tests run once).
 template <bool REFRACT>
-__global__ void __launch_bounds__(256) k_query_cull(int pass, const double* __restrict__ ep, uint32_t nq,
+__global__ void __launch_bounds__(256) k_query_cull(const double* __restrict__ ep, uint32_t nq,
                                                     const uint32_t* __restrict__ order, const TriCull* __restrict__ tc,
                                                     const TriRec* __restrict__ tris,
                                                     float ef, float eb, uint32_t cap,
                                                     const uint32_t* __restrict__ tile_list,
                                                     const uint32_t* __restrict__ tile_count, uint32_t* counts,
-                                                    const unsigned long long* __restrict__ offsets,
-                                                    uint32_t* __restrict__ pq, uint32_t* __restrict__ pt) {
+                                                    uint32_t* __restrict__ masks) {
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t words = (cap + 31) / 32;
   for (uint32_t i = gw; i < nq; i += nw) {
     const uint32_t q = order[i], t = i / 32;
     const double* e = ep + 6ull * q;
@@ -315,44 +316,68 @@ __global__ void __launch_bounds__(256) k_query_cull(int pass, const double* __re
     const f3 x2 = {(float)e[3], (float)e[4], (float)e[5]};
     const uint32_t n = tile_count[t];
     const uint32_t* list = tile_list + (uint64_t)t * cap;
+    uint32_t* mrow = masks + (uint64_t)q * words;
     uint32_t count = 0;
-    unsigned long long wpos = pass ? offsets[q] : 0ull;
     for (uint32_t b = 0; b < n; b += 32) {
       const uint32_t j = b + lane;
       bool k = false;
-      uint32_t tri = 0;
       if (j < n) {
-        tri = list[j];
+        const uint32_t tri = list[j];
         k = test_tri<REFRACT>(x0, x2, tc[tri], ef, eb) && coplanar_keep(tris, tri, x0, x2);
       }
       const unsigned m = __ballot_sync(0xffffffffu, k);
-      if (pass && k) {
-        const unsigned long long pos = wpos + __popc(m & ((1u << lane) - 1u));
-        pq[pos] = q;
-        pt[pos] = tri;
-      }
-      wpos += __popc(m);
+      if (lane == 0) mrow[b / 32] = m;
       count += __popc(m);
     }
-    if (!pass && lane == 0) counts[q] = count;
+    if (lane == 0) counts[q] = count;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_query_expand(uint32_t nq, const uint32_t* __restrict__ order, uint32_t cap,
+                                                      const uint32_t* __restrict__ tile_list,
+                                                      const uint32_t* __restrict__ tile_count,
+                                                      const uint32_t* __restrict__ masks,
+                                                      const unsigned long long* __restrict__ offsets,
+                                                      uint32_t* __restrict__ pq, uint32_t* __restrict__ pt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t words = (cap + 31) / 32;
+  for (uint32_t i = gw; i < nq; i += nw) {
+    const uint32_t q = order[i], t = i / 32;
+    const uint32_t n = tile_count[t];
+    const uint32_t* list = tile_list + (uint64_t)t * cap;
+    const uint32_t* mrow = masks + (uint64_t)q * words;
+    unsigned long long wpos = offsets[q];
+    for (uint32_t b = 0; b < n; b += 32) {
+      const unsigned m = mrow[b / 32];
+      if ((m >> lane) & 1u) {
+        const unsigned long long pos = wpos + __popc(m & ((1u << lane) - 1u));
+        pq[pos] = q;
+        pt[pos] = list[b + lane];
+      }
+      wpos += __popc(m);
+    }
   }
 }
 
 void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M,
                        int refract, uint32_t cap, const uint32_t* tile_list, const uint32_t* tile_count,
-                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
-                       cudaStream_t st) {
+                       uint32_t* counts, uint32_t* masks, const unsigned long long* offsets, uint32_t* pq,
+                       uint32_t* pt, int nsm, cudaStream_t st) {
   if (!nq) return;
   const int threads = 256;
   uint64_t want = ((uint64_t)nq * 32 + threads - 1) / threads;
   uint64_t capb = (uint64_t)nsm * 16;
   const int blocks = (int)(want < capb ? want : capb);
-  if (refract)
-    k_query_cull<true><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
-                                                    tile_list, tile_count, counts, offsets, pq, pt);
+  if (pass == 1)
+    k_query_expand<<<blocks, threads, 0, st>>>(nq, order, cap, tile_list, tile_count, masks, offsets, pq, pt);
+  else if (refract)
+    k_query_cull<true><<<blocks, threads, 0, st>>>(ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
+                                                    tile_list, tile_count, counts, masks);
   else
-    k_query_cull<false><<<blocks, threads, 0, st>>>(pass, ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
-                                                     tile_list, tile_count, counts, offsets, pq, pt);
+    k_query_cull<false><<<blocks, threads, 0, st>>>(ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
+                                                     tile_list, tile_count, counts, masks);
 }
 
 // no cull: every (query, triangle) pair, query-major, Morton order

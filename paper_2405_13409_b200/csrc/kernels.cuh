@@ -19,10 +19,11 @@ void launch_query_order(const double* ep, uint32_t nq, float* bounds, uint32_t* 
 void launch_tile_cull(const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M, int refract,
                       uint32_t cap, uint32_t* tile_list, uint32_t* tile_count, unsigned int* max_count, int nsm,
                       cudaStream_t st);
+// pass 0: tests -> keep masks + per-query counts; pass 1: query-major list from the masks
 void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* order, const DeviceMesh& M,
                        int refract, uint32_t cap, const uint32_t* tile_list, const uint32_t* tile_count,
-                       uint32_t* counts, const unsigned long long* offsets, uint32_t* pq, uint32_t* pt, int nsm,
-                       cudaStream_t st);
+                       uint32_t* counts, uint32_t* masks, const unsigned long long* offsets, uint32_t* pq,
+                       uint32_t* pt, int nsm, cudaStream_t st);
 void launch_all_pairs_k1(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32_t nq, int k, const uint32_t* perm_of,
                         uint32_t* pair_query, uint32_t* pair_tpos, int nsm, cudaStream_t st);
