@@ -63,7 +63,7 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_fcount;
   DBuf<uint32_t> d_fr[2][3];
   DBuf<double> d_rec;
-  DBuf<uint32_t> d_plist;
+  DBuf<uint32_t> d_plist, d_clist;
   DBuf<unsigned long long> d_nsel;
   uint64_t npairs = 0, npairs_culled = 0;
   int last_k = 1;
@@ -160,7 +160,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
-  ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
+  ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
     for (auto& b : f) b.release();
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
@@ -552,9 +552,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
         const uint64_t per = std::max<uint64_t>(1, std::min<uint64_t>(npairs, budget / rb));
         CK(ctx->d_rec.ensure(per * rb));
         CK(ctx->d_plist.ensure(per));
-        CK(ctx->d_nsel.ensure(8));
-        K2Scratch W{ctx->d_rec.p, (ctx->d_rec.cap / rb) * rb, ctx->d_plist.p, ctx->d_nsel.p + 4, 0};
+        CK(ctx->d_clist.ensure(8 * per));
+        CK(ctx->d_nsel.ensure(4 + 24));
+        K2Scratch W{ctx->d_rec.p, (ctx->d_rec.cap / rb) * rb, ctx->d_plist.p, ctx->d_clist.p, ctx->d_nsel.p + 4, 0};
         if (W.rec_cap / rb > ctx->d_plist.cap) W.rec_cap = ctx->d_plist.cap * rb;
+        if (W.rec_cap / rb > ctx->d_clist.cap / 8) W.rec_cap = (ctx->d_clist.cap / 8) * rb;
         launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten,
                         prm, S, W, ctx->nsm, st);
         ctx->launches += W.launches - 1;

@@ -39,7 +39,8 @@ struct K2Scratch {
   double* rec;
   uint64_t rec_cap;  // doubles
   uint32_t* plist;   // >= rec_cap / stride entries
-  unsigned long long* ctr;  // 4
+  uint32_t* clist;   // 8 * (rec_cap / stride) entries: per order class
+  unsigned long long* ctr;  // 24
   int launches;
 };
 uint64_t k2_record_bytes(int v1t, int v2t);

@@ -515,18 +515,61 @@ __global__ void __launch_bounds__(kBuildWarps * 32) k2_build(const uint32_t* __r
   group_counters(g, cnt, S);
 }
 
-// ---- kernel 2: 100-piece determinant-sign scan + bisection, group per pair
-// big = false: pairs with n <= G (register determinant); big = true: n > G (shared-memory determinant)
+// ---- binning by determinant order: one scan launch per order class keeps a single fully unrolled
+// elimination variant per kernel (mixed variants thrashed the instruction cache: 28% no_instruction stalls)
+template <int G>
+__host__ __device__ constexpr int nc_of_class(int c) {
+  return G == 16 ? (c == 0 ? 8 : (c == 1 ? 12 : 16)) : (c < 6 ? 12 + 4 * c : 0);
+}
+template <int G>
+__device__ __forceinline__ int class_of(bool ok, int n) {
+  if (!ok) return 0;
+  if (G == 16) return n <= 8 ? 0 : (n <= 12 ? 1 : 2);
+  return n <= 12 ? 0 : (n <= 16 ? 1 : (n <= 20 ? 2 : (n <= 24 ? 3 : (n <= 28 ? 4 : (n <= 32 ? 5 : 6)))));
+}
+constexpr int kMaxClasses = 8;
+
+template <bool V1T, bool V2T>
+__global__ void __launch_bounds__(256) k2_bin(uint64_t np, const double* __restrict__ recs,
+                                              uint32_t* __restrict__ clist, unsigned long long* __restrict__ ccount) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  const int lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  for (uint64_t b = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) & ~31ull; b < np;
+       b += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = b + lane;
+    int cls = -1;
+    if (r < np) {
+      const double* rec = recs + r * R::STRIDE;
+      cls = class_of<D::G>(rec[H_OK] != 0.0, (int)rec[H_N]);
+    }
+    for (int c = 0; c < kMaxClasses; ++c) {
+      const unsigned m = __ballot_sync(0xffffffffu, cls == c);
+      if (!m) continue;
+      unsigned long long base = 0;
+      if (lane == __ffs(m) - 1) base = atomicAdd(ccount + c, (unsigned long long)__popc(m));
+      base = __shfl_sync(0xffffffffu, base, __ffs(m) - 1);
+      if (cls == c) clist[(uint64_t)c * np + base + __popc(m & lt)] = (uint32_t)r;
+    }
+  }
+}
+
+// ---- kernel 2: 100-piece determinant-sign scan + bisection, group per pair of one order
+// class: NC > 0 register determinant of that class; NC = 0 orders above 32 (shared-memory determinant)
 constexpr int kScanWarps = 4;
-template <bool V1T, bool V2T, bool BIG>
+template <bool V1T, bool V2T, int NC>
 __global__ void __launch_bounds__(kScanWarps * 32) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
                                                           double* __restrict__ recs, SolSink S,
+                                                          const uint32_t* __restrict__ clist,
+                                                          const unsigned long long* __restrict__ ccount,
                                                           uint32_t* __restrict__ plist,
                                                           unsigned long long* __restrict__ pcount,
                                                           unsigned long long* __restrict__ next) {
   using D = Deg2<V1T, V2T>;
   using R = Rec2<V1T, V2T>;
   constexpr int G = D::G, GPW = 32 / G;
+  constexpr bool BIG = NC == 0;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, gi = (threadIdx.x & 31) / G;
   Grp<G> g;
@@ -535,15 +578,16 @@ __global__ void __launch_bounds__(kScanWarps * 32) k2_scan(uint64_t p0, uint64_t
   double* scratch = smem + (size_t)(warp * GPW + gi) * (BIG ? (2 * (R::NR + 2) + R::NR * R::NR) : 0);
   uint32_t cnt[C_NUM];
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const unsigned long long nlist = *ccount;
   while (true) {
-    unsigned long long r = 0;
-    if (g.lane == 0) r = atomicAdd(next, 1ull);
-    r = g.bcast(r, 0);
-    if (r >= np) break;
+    unsigned long long li = 0;
+    if (g.lane == 0) li = atomicAdd(next, 1ull);
+    li = g.bcast(li, 0);
+    if (li >= nlist) break;
+    const uint64_t r = clist[li];
     double* rec = recs + r * R::STRIDE;
     const bool ok = rec[H_OK] != 0.0;
     const int n = (int)rec[H_N];
-    if ((ok && n > G) != BIG) continue;  // the other scan kernel owns this pair
     uint32_t flags = (uint32_t)rec[H_FLAGS];
     int nv = 0;
     if (ok) {
@@ -563,7 +607,7 @@ __global__ void __launch_bounds__(kScanWarps * 32) k2_scan(uint64_t p0, uint64_t
       auto det = [&](double v, double* lg) -> int {
         kflop_acc += eval_f;
         if (BIG) return wdet_sign_smem<G, R::NR>(g, AT, D::DA, BT, D::DB, n, v, lg, scratch, scratch + 2 * (n + 2));
-        return wdet_T<G, R::NR>(g, AT, D::DA, BT, D::DB, n, v, lg);
+        return wdet_T<G, R::NR, NC>(g, AT, D::DA, BT, D::DB, n, v, lg);
       };
       const int P = prm.pieces;
       int last_change = -10;
@@ -864,31 +908,51 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, c
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k2_build<V1T, V2T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_build);
-    cudaFuncSetAttribute(k2_scan<V1T, V2T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_big);
+    cudaFuncSetAttribute(k2_scan<V1T, V2T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_big);
     attr = true;
   }
   int occ_b = 0, occ_s = 0, occ_p = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, k2_build<V1T, V2T>, kBuildWarps * 32, sh_build);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k2_scan<V1T, V2T, false>, kScanWarps * 32, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k2_scan<V1T, V2T, nc_of_class<G>(0)>, kScanWarps * 32, 0);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_p, k2_path<V1T, V2T>, 128, 0);
   occ_b = occ_b < 1 ? 1 : occ_b;
   occ_s = occ_s < 1 ? 1 : occ_s;
   occ_p = occ_p < 1 ? 1 : occ_p;
   const uint64_t chunk = W.rec_cap / R::STRIDE;
+  // counters: [0] build fetch, [1] path list count, [8 + c] class counts, [16 + c] class fetch
+  unsigned long long* cc = W.ctr + 8;
+  unsigned long long* cn = W.ctr + 16;
   for (uint64_t p0 = 0; p0 < npairs; p0 += chunk) {
     const uint64_t np = npairs - p0 < chunk ? npairs - p0 : chunk;
-    cudaMemsetAsync(W.ctr, 0, 4 * sizeof(unsigned long long), st);
+    cudaMemsetAsync(W.ctr, 0, 24 * sizeof(unsigned long long), st);
     const uint64_t gb = (uint64_t)kBuildWarps * (32 / G), gs = (uint64_t)kScanWarps * (32 / G);
     const int bb = (int)std::min<uint64_t>((np + gb - 1) / gb, (uint64_t)nsm * occ_b);
     const int bs = (int)std::min<uint64_t>((np + gs - 1) / gs, (uint64_t)nsm * occ_s);
     const int bp = (int)std::min<uint64_t>((np + 127) / 128, (uint64_t)nsm * occ_p);
     k2_build<V1T, V2T><<<bb, kBuildWarps * 32, sh_build, st>>>(pq, pt, p0, np, M.tris, ep, prm, W.rec, S, W.ctr);
-    k2_scan<V1T, V2T, false><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, W.plist, W.ctr + 3, W.ctr + 1);
-    if (D::DB > 32)
-      k2_scan<V1T, V2T, true><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, W.rec, S, W.plist, W.ctr + 3,
-                                                                   W.ctr + 2);
-    k2_path<V1T, V2T><<<bp, 128, 0, st>>>(pq, pt, p0, M.tris, ep, inten, prm, W.rec, S, W.plist, W.ctr + 3);
-    W.launches += D::DB > 32 ? 4 : 3;
+    k2_bin<V1T, V2T><<<(int)std::min<uint64_t>((np + 255) / 256, (uint64_t)nsm * 8), 256, 0, st>>>(np, W.rec, W.clist,
+                                                                                                   cc);
+    const uint32_t* L = W.clist;
+    if (G == 16) {
+      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      W.launches += 3;
+    } else {
+      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      k2_scan<V1T, V2T, nc_of_class<G>(3)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 3 * np, cc + 3, W.plist, W.ctr + 1, cn + 3);
+      k2_scan<V1T, V2T, nc_of_class<G>(4)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 4 * np, cc + 4, W.plist, W.ctr + 1, cn + 4);
+      k2_scan<V1T, V2T, nc_of_class<G>(5)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 5 * np, cc + 5, W.plist, W.ctr + 1, cn + 5);
+      W.launches += 6;
+      if (D::DB > 32) {
+        k2_scan<V1T, V2T, 0><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, W.rec, S, L + 6 * np, cc + 6, W.plist, W.ctr + 1, cn + 6);
+        W.launches += 1;
+      }
+    }
+    k2_path<V1T, V2T><<<bp, 128, 0, st>>>(pq, pt, p0, M.tris, ep, inten, prm, W.rec, S, W.plist, W.ctr + 1);
+    W.launches += 3;
   }
 }
 

@@ -312,7 +312,7 @@ __device__ __forceinline__ double rowT(const double* __restrict__ AT, int D, int
 }
 
 // det sign for n <= G from the transposed blocks (the group evaluates the slices, lane l row l)
-template <int G, int NR>
+template <int G, int NR, int NCF = 0>
 __device__ int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* BT, int DB, int n, double v,
                       double* lg) {
   const int l = g.lane;
@@ -324,6 +324,7 @@ __device__ int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* B
     aj1 = need ? rowT<NR>(AT, DA, RG, v) : 0.0;
     bj1 = need ? rowT<NR>(BT, DB, RG, v) : 0.0;
   }
+  if (NCF) return wdet_rows<G, (NCF > 0 ? NCF : 8)>(g, as, bs, aj1, bj1, n, lg);  // fixed class (binned launch)
   if (G == 16) {
     if (n <= 8) return wdet_rows<G, 8>(g, as, bs, aj1, bj1, n, lg);
     if (n <= 12) return wdet_rows<G, 12>(g, as, bs, aj1, bj1, n, lg);
