@@ -17,7 +17,6 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
 import time
 
@@ -84,51 +83,75 @@ def fp64_peak(sm_mhz=1965.0, nsm=148):
 
 
 class ClockSampler:
-    def __init__(self, gpu_index):
-        self.gpu = gpu_index
-        self.proc = None
-        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_rank{gpu_index}.csv")
+    """SM clock + throttle reasons sampled DURING the timed region: an NVML polling thread (≈2 ms period;
+    nvidia-smi's own -lms loop starts too slowly for a 60 ms timed region).  Only samples taken between
+    start() and stop() (the first and last timed step) count."""
+
+    REASONS = (("hw_slowdown", 0x8), ("hw_thermal_slowdown", 0x40), ("sw_thermal_slowdown", 0x20),
+               ("sw_power_cap", 0x4), ("hw_power_brake_slowdown", 0x80))
+
+    def __init__(self, device_index):
+        self.dev = device_index
+        self.rows = []  # (t, sm_mhz, max_mhz, reasons bitmask)
+        self.t0 = self.t1 = None
+        self._stop = False
+        self._th = None
+        self.h = None
+
+    def _handle(self):
+        import pynvml
+        pynvml.nvmlInit()
+        try:
+            import torch
+            p = torch.cuda.get_device_properties(self.dev)
+            bus = "%08X:%02X:%02X.0" % (p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
+
+    def _run(self):
+        nv, h = self.h
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self._stop:
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.rows.append((time.perf_counter(), sm, mx, rs))
+            except Exception:
+                pass
+            time.sleep(0.002)
 
     def __enter__(self):
+        import threading
         try:
-            os.makedirs(os.path.dirname(self.path), exist_ok=True)
-            self.f = open(self.path, "w")
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
-                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
-                stdout=self.f, stderr=subprocess.DEVNULL)
+            self.h = self._handle()
+            self._th = threading.Thread(target=self._run, daemon=True)
+            self._th.start()
         except Exception:
-            self.proc = None
+            self._th = None
         return self
 
+    def start(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
+
     def __exit__(self, *a):
-        if self.proc is not None:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except Exception:
-                self.proc.kill()
-            self.f.close()
+        self._stop = True
+        if self._th is not None:
+            self._th.join(timeout=2)
 
     def summary(self):
-        try:
-            rows = [l.strip().split(",") for l in open(self.path) if l.strip()]
-        except Exception:
+        if self.t0 is None:
             return None
+        t1 = self.t1 if self.t1 is not None else float("inf")
+        rows = [r for r in self.rows if self.t0 <= r[0] <= t1]
         if not rows:
             return None
-        sm = [float(r[0]) for r in rows if r[0].strip().replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = set()
-        for r in rows:
-            for i, nm in enumerate(names):
-                if len(r) > 4 + i and "Active" in r[4 + i] and "Not" not in r[4 + i]:
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(rows)}
+        reasons = sorted({nm for r in rows for nm, bit in self.REASONS if r[3] & bit})
+        return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
+                "reasons": reasons, "samples": len(rows), "source": "nvml, 2 ms period, timed region only"}
 
 
 def oracle_baseline(w, nsample, nthreads=0):
@@ -234,6 +257,8 @@ def main():
 
     step_ms, solve_ms, reports = [], [], []
     with ClockSampler(local) as clk:
+        time.sleep(0.01)  # let the sampler thread take its first sample
+        clk.start()
         for s in range(args.steps):
             flush.fill_(s & 0xFF)  # L2 flush between timed iterations (untimed)
             barrier()
@@ -246,6 +271,7 @@ def main():
             step_ms.append(e0.elapsed_time(e1))
             solve_ms.append(r.report["ms_solve"])
             reports.append(dict(r.report, n_solutions=r.n_solutions))
+        clk.stop()
     clocks = clk.summary()
     total_ms = float(sum(step_ms))
     n_paths = sum(x["n_solutions"] for x in reports)

@@ -66,7 +66,10 @@ typedef struct {
   int deterministic;     /* 1: sort solutions by (query, tuple, root) -> bit-identical output */
   float cull_margin;     /* angular slack (rad) of the FP32 cull; 1e-4                       */
   uint64_t max_solutions;/* initial solution-buffer capacity (regrown once on overflow)      */
-  uint64_t max_pairs;    /* work-list chunk size in (query, tuple) pairs                      */
+  uint64_t max_pairs;    /* k=2 cull: max node-pair frontier entries per query chunk; 2^27.
+                            Queries are culled in chunks that fit (order-preserving, so the
+                            work list is the unchunked one); SPOLY_ERR_CAPACITY if one query
+                            alone exceeds it                                                */
   int cull_levels;       /* k=2: barycentric subdivision levels re-testing each kept pair; 3 */
 } spoly_config;
 

@@ -34,6 +34,28 @@ struct DBuf {
   }
 };
 
+// Grows b to hold `need` elements, keeping its first `used` elements (stream-ordered copy).
+template <class T>
+static cudaError_t grow_keep(DBuf<T>& b, size_t used, size_t need, cudaStream_t st) {
+  if (need <= b.cap && b.p) return cudaSuccess;
+  const size_t want = std::max<size_t>({need, b.cap + b.cap / 2, 1});
+  T* np = nullptr;
+  cudaError_t e = cudaMalloc(&np, want * sizeof(T));
+  if (e != cudaSuccess) return e;
+  if (used) {
+    e = cudaMemcpyAsync(np, b.p, used * sizeof(T), cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) {
+      cudaFree(np);
+      return e;
+    }
+  }
+  if (b.p) cudaFree(b.p);
+  b.p = np;
+  b.cap = want;
+  return cudaSuccess;
+}
+
 }  // namespace
 
 struct spoly_ctx {
@@ -56,7 +78,8 @@ struct spoly_ctx {
   // work list
   DBuf<uint64_t> d_counts;
   DBuf<unsigned long long> d_offsets;
-  DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2;
+  DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2, d_pqa, d_pta;
+  uint32_t k2_chunk = 0;  // queries per two-bounce cull chunk (learned; reset by mesh upload)
   DBuf<unsigned char> d_keep;
   DBuf<uint32_t> d_qmask;
   DBuf<uint64_t> d_front;
@@ -116,7 +139,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->deterministic = 1;
   c->cull_margin = 1e-4f;
   c->max_solutions = 1ull << 22;
-  c->max_pairs = 1ull << 32;
+  c->max_pairs = 1ull << 27;
   c->cull_levels = 3;
   return SPOLY_OK;
 }
@@ -158,7 +181,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
   ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
-  ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pt_orig.release();
+  ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
   ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
@@ -278,6 +301,7 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   ctx->M.perm_of = ctx->d_perm.p;
   ctx->M.clusters = ctx->d_cl.p;
   ctx->has_mesh = true;
+  ctx->k2_chunk = 0;
   if (mesh_id) *mesh_id = 0;
   return SPOLY_OK;
 }
@@ -320,6 +344,100 @@ static int bits_for(uint64_t n) {
   return b;
 }
 
+// Two-bounce pair cull of the query chunk [q0, q0 + qn): level-synchronous node-pair expansion from the
+// split level down to triangle pairs (count pass, scan, write pass per level), then the barycentric
+// subdivision refinement and an order-preserving compaction.  On return (*kq, *kt) point at the kept
+// (query, T1, T2) list of *nkept entries (ctx-owned scratch, valid until the next chunk).  If a level's
+// frontier would exceed `budget` entries nothing is written and *over is set to its size.
+static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const double* endpoints, uint32_t q0,
+                                  uint32_t qn, int top, uint32_t P, uint64_t budget, uint64_t* ncoarse,
+                                  uint64_t* nkept, const uint32_t** kq, const uint32_t** kt, uint64_t* over) {
+  cudaStream_t st = ctx->st;
+  const int v1t = chain[0] == 'T', v2t = chain[1] == 'T';
+  const uint32_t *fq = nullptr, *fa = nullptr, *fb = nullptr;  // implicit root frontier of the chunk
+  uint64_t nf = (uint64_t)qn * P;
+  int cur = 0;
+  *over = 0;
+  for (int cl = top - 1; cl >= 0; --cl) {
+    CK(ctx->d_counts.ensure(nf / 2 + 1));
+    CK(ctx->d_offsets.ensure(nf + 1));
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+    launch_pair_expand(0, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, nullptr, nullptr, nullptr,
+                       nullptr, ctx->nsm, st);
+    size_t tbytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
+    CK(ctx->d_temp.ensure(tbytes));
+    CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
+    CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nf, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    ctx->launches += 2;
+    if (tot > budget) {
+      *over = tot;
+      return SPOLY_OK;
+    }
+    if (cl == 0) {
+      CK(ctx->d_pq.ensure(tot));
+      CK(ctx->d_pt.ensure(2 * tot));
+      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
+                         ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
+    } else {
+      const int nx = 1 - cur;
+      for (int c = 0; c < 3; ++c) CK(ctx->d_fr[nx][c].ensure(tot));
+      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
+                         ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
+      fq = ctx->d_fr[nx][0].p;
+      fa = ctx->d_fr[nx][1].p;
+      fb = ctx->d_fr[nx][2].p;
+      cur = nx;
+    }
+    nf = tot;
+  }
+  const uint64_t npairs = nf;
+  *ncoarse = npairs;
+  *nkept = npairs;
+  *kq = ctx->d_pq.p;
+  *kt = ctx->d_pt.p;
+  if (ctx->cfg.cull_levels > 0 && npairs) {
+    // barycentric subdivision refinement, then an order-preserving compaction (deterministic)
+    CK(ctx->d_keep.ensure(npairs));
+    CK(ctx->d_pq2.ensure(npairs));
+    CK(ctx->d_pt2.ensure(2 * npairs));
+    CK(ctx->d_nsel.ensure(4));
+    {
+      const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * npairs, 1ull << 20), 1ull << 27);
+      CK(ctx->d_front.ensure(2 * fcap));
+      CK(ctx->d_fcount.ensure(16));
+      RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
+      launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
+                          ctx->d_keep.p, RW, ctx->nsm, st);
+      ctx->launches += RW.launches;
+    }
+    const uint2* pt_in = reinterpret_cast<const uint2*>(ctx->d_pt.p);
+    uint2* pt_out = reinterpret_cast<uint2*>(ctx->d_pt2.p);
+    size_t tb1 = 0, tb2 = 0;
+    CK(cub::DeviceSelect::Flagged(nullptr, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
+                                  (int64_t)npairs, st));
+    CK(cub::DeviceSelect::Flagged(nullptr, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1, (int64_t)npairs,
+                                  st));
+    CK(ctx->d_temp.ensure(std::max(tb1, tb2)));
+    tb1 = tb2 = ctx->d_temp.cap;
+    CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
+                                  (int64_t)npairs, st));
+    CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1,
+                                  (int64_t)npairs, st));
+    ctx->launches += 2;
+    unsigned long long ns = 0;
+    CK(cudaMemcpyAsync(&ns, ctx->d_nsel.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    *nkept = ns;
+    *kq = ctx->d_pq2.p;
+    *kt = ctx->d_pt2.p;
+  }
+  return SPOLY_OK;
+}
+
 spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces, const double* endpoints,
                          uint32_t nq, const double* inten, const spoly_tuple_list* tuples, spoly_result* out) {
   if (!ctx || !chain || !out) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
@@ -354,83 +472,43 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
     ctx->launches++;
   } else if (ctx->cfg.cull && k == 2) {
+    // queries are culled in chunks whose node-pair frontiers fit cfg.max_pairs entries; the refined pair
+    // lists of the chunks are appended in query order, so the work list equals the unchunked one
     uint32_t P = 0;
     const int top = cull_split_level(ctx->M, &P);
     if (top < 1) return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "two-bounce cull supports at most 2^22 triangles");
-    const int v1t = chain[0] == 'T', v2t = chain[1] == 'T';
-    const uint32_t *fq = nullptr, *fa = nullptr, *fb = nullptr;  // implicit root frontier
-    uint64_t nf = (uint64_t)nq * P;
-    int cur = 0;
-    for (int cl = top - 1; cl >= 0; --cl) {
-      CK(ctx->d_counts.ensure(nf / 2 + 1));
-      CK(ctx->d_offsets.ensure(nf + 1));
-      uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
-      launch_pair_expand(0, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, nullptr, nullptr, nullptr, nullptr,
-                         ctx->nsm, st);
-      size_t tbytes = 0;
-      CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
-      CK(ctx->d_temp.ensure(tbytes));
-      CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
-      CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
-      unsigned long long tot = 0;
-      CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nf, sizeof(tot), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      if (cl == 0) {
-        CK(ctx->d_pq.ensure(tot));
-        CK(ctx->d_pt.ensure(2 * tot));
-        launch_pair_expand(1, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
-                           ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
-      } else {
-        const int nx = 1 - cur;
-        for (int c = 0; c < 3; ++c) CK(ctx->d_fr[nx][c].ensure(tot));
-        launch_pair_expand(1, cl, endpoints, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
-                           ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
-        fq = ctx->d_fr[nx][0].p;
-        fa = ctx->d_fr[nx][1].p;
-        fb = ctx->d_fr[nx][2].p;
-        cur = nx;
+    const uint64_t budget = std::max<uint64_t>(ctx->cfg.max_pairs, 2ull * P);
+    uint32_t chunk = std::max<uint32_t>(1, std::min<uint32_t>(ctx->k2_chunk ? ctx->k2_chunk : nq, nq));
+    chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunk, budget / P));
+    uint64_t acc = 0, coarse = 0;
+    for (uint32_t q0 = 0; q0 < nq;) {
+      const uint32_t qn = std::min(chunk, nq - q0);
+      uint64_t ncoarse = 0, nkept = 0, over = 0;
+      const uint32_t *kq = nullptr, *kt = nullptr;
+      spoly_status s = cull_k2_chunk(ctx, chain, endpoints, q0, qn, top, P, budget, &ncoarse, &nkept, &kq, &kt, &over);
+      if (s != SPOLY_OK) return s;
+      if (over) {  // a frontier of this chunk exceeded the budget: shrink the chunk and redo it
+        if (qn == 1) return fail(ctx, SPOLY_ERR_CAPACITY, "two-bounce cull frontier of one query exceeds max_pairs");
+        chunk = (uint32_t)std::max<double>(1.0, std::min<double>(qn / 2, 0.9 * qn * (double)budget / (double)over));
+        continue;
       }
-      ctx->launches += 2;
-      nf = tot;
-    }
-    npairs = nf;
-    if (ctx->cfg.cull_levels > 0 && npairs) {
-      // barycentric subdivision refinement, then an order-preserving compaction (deterministic)
-      CK(ctx->d_keep.ensure(npairs));
-      CK(ctx->d_pq2.ensure(npairs));
-      CK(ctx->d_pt2.ensure(2 * npairs));
-      CK(ctx->d_nsel.ensure(4));
-      {
-        const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * npairs, 1ull << 20), 1ull << 27);
-        CK(ctx->d_front.ensure(2 * fcap));
-        CK(ctx->d_fcount.ensure(16));
-        RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
-        launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels,
-                            chain[0] == 'T', chain[1] == 'T', ctx->d_keep.p, RW, ctx->nsm, st);
-        ctx->launches += RW.launches;
+      CK(grow_keep(ctx->d_pqa, acc, acc + nkept, st));
+      CK(grow_keep(ctx->d_pta, 2 * acc, 2 * (acc + nkept), st));
+      if (nkept) {
+        CK(cudaMemcpyAsync(ctx->d_pqa.p + acc, kq, nkept * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        CK(cudaMemcpyAsync(ctx->d_pta.p + 2 * acc, kt, 2 * nkept * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
       }
-      const uint2* pt_in = reinterpret_cast<const uint2*>(ctx->d_pt.p);
-      uint2* pt_out = reinterpret_cast<uint2*>(ctx->d_pt2.p);
-      size_t tb1 = 0, tb2 = 0;
-      CK(cub::DeviceSelect::Flagged(nullptr, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
-                                    (int64_t)npairs, st));
-      CK(cub::DeviceSelect::Flagged(nullptr, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1, (int64_t)npairs,
-                                    st));
-      CK(ctx->d_temp.ensure(std::max(tb1, tb2)));
-      tb1 = tb2 = ctx->d_temp.cap;
-      CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb1, ctx->d_pq.p, ctx->d_keep.p, ctx->d_pq2.p, ctx->d_nsel.p,
-                                    (int64_t)npairs, st));
-      CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb2, pt_in, ctx->d_keep.p, pt_out, ctx->d_nsel.p + 1,
-                                    (int64_t)npairs, st));
-      ctx->launches += 2;
-      unsigned long long ns = 0;
-      CK(cudaMemcpyAsync(&ns, ctx->d_nsel.p, sizeof(ns), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      ctx->npairs_culled = npairs;
-      npairs = ns;
-      std::swap(ctx->d_pq, ctx->d_pq2);
-      std::swap(ctx->d_pt, ctx->d_pt2);
+      acc += nkept;
+      coarse += ncoarse;
+      q0 += qn;
     }
+    ctx->k2_chunk = chunk;
+    CK(ctx->d_pqa.ensure(1));
+    CK(ctx->d_pta.ensure(2));
+    std::swap(ctx->d_pq, ctx->d_pqa);
+    std::swap(ctx->d_pt, ctx->d_pta);
+    ctx->npairs_culled = ctx->cfg.cull_levels > 0 ? coarse : 0;
+    npairs = acc;
   } else if (ctx->cfg.cull) {
     // query order (Morton of the endpoints), tile cull, per-query cull on the tile survivors
     const uint32_t ntiles = (nq + 31) / 32;

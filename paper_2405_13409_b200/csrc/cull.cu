@@ -522,7 +522,7 @@ __device__ __forceinline__ void node_bounds(const CullLevels& L, int level, uint
 // fq == nullptr: implicit root frontier (entry e -> query e / P, pair e % P of the split level), the root
 // pair itself is tested first.  cl = level of the children (0: triangle pairs, written to pq / pt).
 __global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const double* __restrict__ ep,
-                                                     const uint32_t* __restrict__ fq, const uint32_t* __restrict__ fa,
+                                                     uint32_t qbase, const uint32_t* __restrict__ fq, const uint32_t* __restrict__ fa,
                                                      const uint32_t* __restrict__ fb, uint64_t nf,
                                                      const TriRec* __restrict__ tris, CullLevels L, int v1t, int v2t,
                                                      float ef, float eb, uint32_t* __restrict__ counts,
@@ -542,7 +542,7 @@ __global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const dou
       A = fa[en];
       B = fb[en];
     } else {
-      q = (uint32_t)(en / P);
+      q = qbase + (uint32_t)(en / P);  // implicit root frontier of the query chunk [qbase, qbase + nf / P)
       A = (uint32_t)(en % P) / nt;
       B = (uint32_t)(en % P) % nt;
     }
@@ -638,7 +638,7 @@ int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query) {
   return L.top;
 }
 
-void launch_pair_expand(int pass, int cl, const double* ep, const uint32_t* fq, const uint32_t* fa,
+void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
                         const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
                         const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
                         cudaStream_t st) {
@@ -646,7 +646,7 @@ void launch_pair_expand(int pass, int cl, const double* ep, const uint32_t* fq, 
   const CullLevels L = cull_levels_of(M);
   const int threads = 256;
   const uint64_t want = (nf * 32 + threads - 1) / threads, cap = (uint64_t)nsm * 64;
-  k_pair_expand<<<(int)(want < cap ? want : cap), threads, 0, st>>>(pass, cl, ep, fq, fa, fb, nf, M.tris, L, v1t, v2t,
+  k_pair_expand<<<(int)(want < cap ? want : cap), threads, 0, st>>>(pass, cl, ep, qbase, fq, fa, fb, nf, M.tris, L, v1t, v2t,
                                                                     M.eta_front, M.eta_back, counts, offsets, oq,
                                                                     oa, ob);
 }

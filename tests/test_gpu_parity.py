@@ -292,3 +292,20 @@ def test_determinism_bit_identical(sp, torch_cuda):
     b = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
     for k in ("query", "tuple", "bary", "contribution", "per_query", "flagged_query"):
         assert np.array_equal(a[k], b[k]), k
+
+
+@pytest.mark.parametrize("chain,make", [("RR", lambda: W.mirrors_rr(res=8, quads=16)),
+                                        ("TT", lambda: W.shell_c5(res=8))])
+def test_two_bounce_query_chunking_identical(sp, torch_cuda, chain, make):
+    """cfg.max_pairs small enough that the k=2 cull runs in many query chunks: the work list, solutions and
+    per-query sums are bit-identical to the single-chunk run (chunks append in query order)."""
+    w = make()
+    a = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints)
+    # one query's frontiers stay below 2^16 entries on these meshes (shell: ~20k triangle pairs per query),
+    # the 64 queries' do not: the cull runs in several chunks
+    b = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints, cfg=sp.default_config(max_pairs=1 << 16))
+    assert a["report"]["n_pairs_in"] == b["report"]["n_pairs_in"] > 0
+    assert np.array_equal(a["worklist"][0], b["worklist"][0])
+    assert np.array_equal(a["worklist"][1], b["worklist"][1])
+    for k in ("query", "tuple", "bary", "contribution", "per_query", "flagged_query", "flagged_tuple"):
+        assert np.array_equal(a[k], b[k]), k
