@@ -77,7 +77,7 @@ struct spoly_ctx {
   uint32_t tile_cap = 4096, tile_used_cap = 4096;
   // work list
   DBuf<uint64_t> d_counts;
-  DBuf<unsigned long long> d_offsets;
+  DBuf<unsigned long long> d_offsets, d_emask;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2, d_pqa, d_pta;
   uint32_t k2_chunk = 0;  // queries per two-bounce cull chunk (learned; reset by mesh upload)
   DBuf<unsigned char> d_keep;
@@ -181,7 +181,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
   ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
-  ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
+  ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_emask.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
   ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
@@ -362,8 +362,9 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
     CK(ctx->d_counts.ensure(nf / 2 + 1));
     CK(ctx->d_offsets.ensure(nf + 1));
     uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
-    launch_pair_expand(0, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, nullptr, nullptr, nullptr,
-                       nullptr, ctx->nsm, st);
+    CK(ctx->d_emask.ensure(nf));
+    launch_pair_expand(0, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, ctx->d_emask.p, nullptr, nullptr,
+                       nullptr, nullptr, ctx->nsm, st);
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
     CK(ctx->d_temp.ensure(tbytes));
@@ -380,13 +381,13 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
     if (cl == 0) {
       CK(ctx->d_pq.ensure(tot));
       CK(ctx->d_pt.ensure(2 * tot));
-      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
-                         ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
+      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
+                         ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
     } else {
       const int nx = 1 - cur;
       for (int c = 0; c < 3; ++c) CK(ctx->d_fr[nx][c].ensure(tot));
-      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_offsets.p,
-                         ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
+      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
+                         ctx->d_offsets.p, ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
       fq = ctx->d_fr[nx][0].p;
       fa = ctx->d_fr[nx][1].p;
       fb = ctx->d_fr[nx][2].p;

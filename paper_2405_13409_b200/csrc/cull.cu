@@ -472,6 +472,7 @@ __device__ __forceinline__ bool pair_keep(f3 x0, f3 x3, float4 sA, float4 nA, fl
     }
     ncombo = 2;
   }
+#pragma unroll
   for (int c = 0; c < ncombo; ++c) {
     if (ncombo == 2 && side >= 0 && c != side) continue;
     if (node_keep(a0, c0, aAB, cAB, e[c][0], e[c][1], nA) && node_keep(aBA, cAB, a3, c3, e[c][1], e[c][2], nB))
@@ -519,22 +520,130 @@ __device__ __forceinline__ void node_bounds(const CullLevels& L, int level, uint
   }
 }
 
-// fq == nullptr: implicit root frontier (entry e -> query e / P, pair e % P of the split level), the root
-// pair itself is tested first.  cl = level of the children (0: triangle pairs, written to pq / pt).
-__global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const double* __restrict__ ep,
+// Per-child record of one frontier entry, staged in shared memory: every one of the entry's 64 child
+// pairs (a, b) combines child a of node A with child b of node B, so the per-node parts of pair_keep /
+// side_keep (the direction bound to x_0 or x_3, and at the triangle level the plane and side data) are
+// computed once per child (16 per entry) instead of once per pair (64).  The arithmetic is the same
+// expressions in the same order as pair_keep / side_keep, so the kept set is unchanged.
+struct ChildRec {
+  float4 sph, cone;  // bounding sphere, normal cone
+  float4 dir;        // axis (x_0 or x_3 -> node) and chord of sphere_dir
+  float4 g;          // triangle level: geometric normal e1 x e2 (xyz), side tolerance (w)
+  float4 p0, p1, p2; // triangle level: vertices; p0.w = side sign sg, p1.w / p2.w unused
+  int flags;         // bit 0: valid child, 1: sphere_dir bound ok, 2: side filter keeps all (sref == 0),
+                     // 3-4: eta side of x_0 w.r.t. the plane + 1 (0: both media)
+};
+
+__device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels& L, const TriRec* __restrict__ tris,
+                                           uint32_t i, f3 xend, int refract, int want_side) {
+  R.flags = 0;
+  if (i >= L.n[cl]) return;
+  R.flags = 1;
+  if (cl == 0) {
+    const TriCull T = L.tc[i];
+    R.sph = T.sphere;
+    R.cone = T.cone;
+    if (want_side) {
+      // eta_0 from the side of x_0 w.r.t. T_1's plane (within float noise of the plane: both)
+      const float sd = dotf(ld3(T.plane), xend) - T.plane.w;
+      const float gl = sqrtf(dotf(ld3(T.plane), ld3(T.plane)));
+      int side = -1;
+      if (fabsf(sd) > 1e-4f * gl * (fabsf(xend.x) + fabsf(xend.y) + fabsf(xend.z) + 1.f)) side = sd > 0.f ? 0 : 1;
+      R.flags |= (side + 1) << 3;
+    }
+    // side_keep's per-triangle part (plane, reference side, tolerance)
+    const float4* r = tris[i].r;
+    const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2);
+    const f3 p0 = {a.x, a.y, a.z}, p1 = {a.w, b.x, b.y}, p2 = {b.z, b.w, c.x};
+    const f3 e1 = p1 - p0, e2 = p2 - p0;
+    const f3 g = crossf(e1, e2);
+    const float gl = sqrtf(dotf(g, g)), sc = sqrtf(fmaxf(dotf(e1, e1), dotf(e2, e2)));
+    const float sref = dotf(xend - p0, g);
+    if (sref == 0.f) R.flags |= 4;
+    const float sg = (sref > 0.f) == (refract == 0) ? 1.f : -1.f;
+    R.g = make_float4(g.x, g.y, g.z, 0.5e-6f * gl * sc);
+    R.p0 = make_float4(p0.x, p0.y, p0.z, sg);
+    R.p1 = make_float4(p1.x, p1.y, p1.z, 0.f);
+    R.p2 = make_float4(p2.x, p2.y, p2.z, 0.f);
+  } else {
+    const ClusterRec C = L.lv[cl][i];
+    R.sph = C.sphere;
+    R.cone = C.cone;
+  }
+  f3 d;
+  float ch;
+  if (sphere_dir(xend, R.sph, d, ch)) R.flags |= 2;
+  R.dir = make_float4(d.x, d.y, d.z, ch);
+}
+
+// side_keep(tris, t, xref, refract, o) with t's part precomputed in record it and o's vertices in record io
+// (records in the warp's SoA staging f[field][child], flags fl[child])
+__device__ __forceinline__ bool side_keep_rec(const float4 (*f)[16], const int* fl, int it, int io) {
+  if (fl[it] & 4) return true;
+  const float4 G = f[3][it], P0 = f[4][it];
+  const f3 g = ld3(G), p0 = ld3(P0);
+  const float sg = P0.w, tol = G.w;
+  return sg * dotf(ld3(f[4][io]) - p0, g) > tol || sg * dotf(ld3(f[5][io]) - p0, g) > tol ||
+         sg * dotf(ld3(f[6][io]) - p0, g) > tol;
+}
+
+// pair_keep(x0, x3, sA, cA, sB, cB, ...) with the per-node direction bounds precomputed
+__device__ __forceinline__ bool pair_keep_rec(const float4 (*f)[16], const int* fl, int ia, int ib, int v1t, int v2t,
+                                              float ef, float eb, int side) {
+  f3 aAB;
+  float cAB;
+  if (!(fl[ia] & 2) || !(fl[ib] & 2) || !pair_dir(f[0][ia], f[0][ib], aAB, cAB)) return true;
+  const float4 DA = f[2][ia], DB = f[2][ib];
+  const f3 a0 = ld3(DA), a3 = ld3(DB);
+  const float c0 = DA.w, c3 = DB.w;
+  const f3 aBA = {-aAB.x, -aAB.y, -aAB.z};
+  float e[2][3];
+  int ncombo = 0;
+  if (!v1t && !v2t) {
+    e[0][0] = e[0][1] = e[0][2] = 1.f;
+    ncombo = 1;
+  } else {
+    for (int c = 0; c < 2; ++c) {
+      const float s = c == 0 ? ef : eb, o = c == 0 ? eb : ef;
+      e[c][0] = s;
+      e[c][1] = v1t ? o : s;
+      e[c][2] = v2t ? (e[c][1] == s ? o : s) : e[c][1];
+    }
+    ncombo = 2;
+  }
+#pragma unroll
+  for (int c = 0; c < ncombo; ++c) {
+    if (ncombo == 2 && side >= 0 && c != side) continue;
+    if (node_keep(a0, c0, aAB, cAB, e[c][0], e[c][1], f[1][ia]) &&
+        node_keep(aBA, cAB, a3, c3, e[c][1], e[c][2], f[1][ib]))
+      return true;
+  }
+  return false;
+}
+
+// fq == nullptr: implicit root frontier (entry e -> query qbase + e / P, pair e % P of the split level), the
+// root pair itself is tested first.  cl = level of the children (0: triangle pairs, written to pq / pt).
+// Pass 0 tests the 64 child pairs of every entry (one warp per entry, 2 per lane; lanes 0-7 / 8-15 first
+// stage the entry's 8 + 8 child records) and stores the 64-bit keep mask and its popcount; pass 1 writes
+// the kept pairs from the masks at the scanned offsets in (entry, child) order (deterministic, query-major).
+constexpr int kExpandThreads = 256;
+__global__ void __launch_bounds__(kExpandThreads, 3) k_pair_expand(int pass, int cl, const double* __restrict__ ep,
                                                      uint32_t qbase, const uint32_t* __restrict__ fq, const uint32_t* __restrict__ fa,
                                                      const uint32_t* __restrict__ fb, uint64_t nf,
                                                      const TriRec* __restrict__ tris, CullLevels L, int v1t, int v2t,
                                                      float ef, float eb, uint32_t* __restrict__ counts,
+                                                     unsigned long long* __restrict__ masks,
                                                      const unsigned long long* __restrict__ offsets,
                                                      uint32_t* __restrict__ oq, uint32_t* __restrict__ oa,
                                                      uint32_t* __restrict__ ob) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
+  // structure-of-arrays staging: field f of child i at smf[warp][f][i], so the 4 (A side) or 8 (B side)
+  // distinct records a warp-wide load touches sit in distinct banks (broadcast, no conflicts)
+  __shared__ float4 smf[kExpandThreads / 32][7][16];
+  __shared__ int smk[kExpandThreads / 32][16];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t nt = L.n[L.top], P = nt * nt;
-  const uint32_t ncl = L.n[cl];
   for (uint64_t en = gw; en < nf; en += nw) {
     uint32_t q, A, B;
     if (fq) {
@@ -542,9 +651,31 @@ __global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const dou
       A = fa[en];
       B = fb[en];
     } else {
-      q = qbase + (uint32_t)(en / P);  // implicit root frontier of the query chunk [qbase, qbase + nf / P)
+      q = qbase + (uint32_t)(en / P);
       A = (uint32_t)(en % P) / nt;
       B = (uint32_t)(en % P) % nt;
+    }
+    if (pass) {
+      const unsigned long long m = masks[en];
+      if (!m) continue;
+      const unsigned long long base = offsets[en];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int c = h * 32 + lane;
+        if ((m >> c) & 1ull) {
+          const unsigned long long pos = base + __popcll(m & ((1ull << c) - 1ull));
+          const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
+          oq[pos] = q;
+          if (cl == 0) {
+            oa[2 * pos] = a;
+            oa[2 * pos + 1] = b;
+          } else {
+            oa[pos] = a;
+            ob[pos] = b;
+          }
+        }
+      }
+      continue;
     }
     const double* e = ep + 6ull * q;
     const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
@@ -556,57 +687,47 @@ __global__ void __launch_bounds__(256) k_pair_expand(int pass, int cl, const dou
       node_bounds(L, cl + 1, B, sb, cb);
       root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
     }
-    bool k[2] = {false, false};
+    unsigned long long m = 0;
     if (root_ok) {
+      __syncwarp();
+      if (lane < 16) {
+        const bool isB = lane >= 8;
+        ChildRec R;
+        make_child(R, cl, L, tris, (isB ? B : A) * 8 + (lane & 7), isB ? x3 : x0, isB ? v2t : v1t,
+                   !isB && (v1t || v2t));
+        smf[wib][0][lane] = R.sph;
+        smf[wib][1][lane] = R.cone;
+        smf[wib][2][lane] = R.dir;
+        smf[wib][3][lane] = R.g;
+        smf[wib][4][lane] = R.p0;
+        smf[wib][5][lane] = R.p1;
+        smf[wib][6][lane] = R.p2;
+        smk[wib][lane] = R.flags;
+      }
+      __syncwarp();
+      bool k[2];
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c = h * 32 + lane;
-        const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
-        if (a < ncl && b < ncl) {
+        const int ia = c >> 3, ib = 8 + (c & 7);
+        const int fa_ = smk[wib][ia], fb_ = smk[wib][ib];
+        k[h] = false;
+        if ((fa_ & 1) && (fb_ & 1)) {
           if (cl == 0) {
-            if (a != b) {
-              const TriCull TA = L.tc[a], TB = L.tc[b];
-              // eta_0 from the side of x_0 w.r.t. T_1's plane (within float noise of the plane: both)
-              int side = -1;
-              if (v1t || v2t) {
-                const float sd = dotf(ld3(TA.plane), x0) - TA.plane.w;
-                const float gl = sqrtf(dotf(ld3(TA.plane), ld3(TA.plane)));
-                if (fabsf(sd) > 1e-4f * gl * (fabsf(x0.x) + fabsf(x0.y) + fabsf(x0.z) + 1.f)) side = sd > 0.f ? 0 : 1;
-              }
-              k[h] = pair_keep(x0, x3, TA.sphere, TA.cone, TB.sphere, TB.cone, v1t, v2t, ef, eb, side) &&
-                     side_keep(tris, a, x0, v1t, b) && side_keep(tris, b, x3, v2t, a);
-            }
+            if (A * 8 + ia != B * 8 + (c & 7))
+              k[h] = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, ((fa_ >> 3) & 3) - 1) &&
+                     side_keep_rec(smf[wib], smk[wib], ia, ib) && side_keep_rec(smf[wib], smk[wib], ib, ia);
           } else {
-            float4 sa, ca, sb, cb;
-            node_bounds(L, cl, a, sa, ca);
-            node_bounds(L, cl, b, sb, cb);
-            k[h] = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
+            k[h] = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, -1);
           }
         }
       }
+      m = (unsigned long long)__ballot_sync(0xffffffffu, k[0]) |
+          ((unsigned long long)__ballot_sync(0xffffffffu, k[1]) << 32);
     }
-    const unsigned m0 = __ballot_sync(0xffffffffu, k[0]), m1 = __ballot_sync(0xffffffffu, k[1]);
-    const uint32_t c0 = __popc(m0), tot = c0 + __popc(m1);
-    if (!pass) {
-      if (lane == 0) counts[en] = tot;
-      continue;
-    }
-    const unsigned long long base = offsets[en];
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if (k[h]) {
-        const int c = h * 32 + lane;
-        const unsigned long long pos = base + (h ? c0 : 0) + __popc((h ? m1 : m0) & lt);
-        const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
-        oq[pos] = q;
-        if (cl == 0) {
-          oa[2 * pos] = a;
-          oa[2 * pos + 1] = b;
-        } else {
-          oa[pos] = a;
-          ob[pos] = b;
-        }
-      }
+    if (lane == 0) {
+      counts[en] = (uint32_t)__popcll(m);
+      masks[en] = m;
     }
   }
 }
@@ -640,14 +761,14 @@ int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query) {
 
 void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
                         const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
-                        const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
+                        unsigned long long* masks, const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
                         cudaStream_t st) {
   if (!nf) return;
   const CullLevels L = cull_levels_of(M);
   const int threads = 256;
   const uint64_t want = (nf * 32 + threads - 1) / threads, cap = (uint64_t)nsm * 64;
   k_pair_expand<<<(int)(want < cap ? want : cap), threads, 0, st>>>(pass, cl, ep, qbase, fq, fa, fb, nf, M.tris, L, v1t, v2t,
-                                                                    M.eta_front, M.eta_back, counts, offsets, oq,
+                                                                    M.eta_front, M.eta_back, counts, masks, offsets, oq,
                                                                     oa, ob);
 }
 

@@ -51,7 +51,7 @@ void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, u
 int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query);
 void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
                         const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
-                        const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
+                        unsigned long long* masks, const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
                         cudaStream_t st);
 struct RefineScratch {
   uint64_t* front[2];  // frontier ping-pong, cap entries each

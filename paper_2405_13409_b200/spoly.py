@@ -14,7 +14,8 @@ from dataclasses import dataclass
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libspoly.so")
+# SPOLY_LIB: alternative build of the same library (A/B kernel variants); default the in-tree build
+LIB_PATH = os.environ.get("SPOLY_LIB") or os.path.join(HERE, "libspoly.so")
 
 SPOLY_OK = 0
 STATUS = {0: "SPOLY_OK", 1: "SPOLY_ERR_INVALID_ARG", 2: "SPOLY_ERR_BAD_MESH", 3: "SPOLY_ERR_UNSUPPORTED_CHAIN",

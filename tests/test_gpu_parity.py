@@ -301,9 +301,10 @@ def test_two_bounce_query_chunking_identical(sp, torch_cuda, chain, make):
     per-query sums are bit-identical to the single-chunk run (chunks append in query order)."""
     w = make()
     a = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints)
-    # one query's frontiers stay below 2^16 entries on these meshes (shell: ~20k triangle pairs per query),
-    # the 64 queries' do not: the cull runs in several chunks
-    b = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints, cfg=sp.default_config(max_pairs=1 << 16))
+    # a budget of a third of the whole frame's triangle-pair frontier: several chunks, each within budget
+    budget = a["report"]["n_pairs_coarse"] // 3 + 1
+    b = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints, cfg=sp.default_config(max_pairs=budget))
+    assert b["report"]["n_pairs_coarse"] == a["report"]["n_pairs_coarse"]
     assert a["report"]["n_pairs_in"] == b["report"]["n_pairs_in"] > 0
     assert np.array_equal(a["worklist"][0], b["worklist"][0])
     assert np.array_equal(a["worklist"][1], b["worklist"][1])
