@@ -207,8 +207,13 @@ __device__ __forceinline__ double solve_piece(const double* g, const double* h, 
     else
       hi = x;
     double xn = x - f * fast_rcp(fp);
+    // convergence before the bracket safeguard (a sub-ulp step may land on the endpoint x just became)
+    if (fabs(xn - x) <= 1e-12) {
+      *its = it + 1;
+      return fmin(fmax(xn, lo), hi);
+    }
     if (!(xn > lo && xn < hi)) xn = 0.5 * (lo + hi);
-    if (fabs(xn - x) <= 1e-12 || hi - lo <= 1e-15) {
+    if (hi - lo <= 1e-15) {
       *its = it + 1;
       return xn;
     }
@@ -256,8 +261,13 @@ __device__ __forceinline__ int monotone_root(const double* c, double lo, double 
     else
       b = x;
     double xn = x - f * fast_rcp(fp);
+    // convergence before the bracket safeguard (a sub-ulp step may land on the endpoint x just became)
+    if (fabs(xn - x) <= 1e-12) {
+      x = fmin(fmax(xn, a), b);
+      break;
+    }
     if (!(xn > a && xn < b)) xn = 0.5 * (a + b);
-    if (fabs(xn - x) <= 1e-12 || b - a <= 1e-15) {
+    if (b - a <= 1e-15) {
       x = xn;
       break;
     }

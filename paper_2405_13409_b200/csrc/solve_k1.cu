@@ -468,8 +468,14 @@ __global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
         else
           b = x;
         double xn = x - f * fast_rcp(fp);
-        if (!(xn > a && xn < b)) xn = 0.5 * (a + b);
-        fin = fabs(xn - x) <= 1e-12 || b - a <= 1e-15 || it >= 100;
+        // convergence is tested before the bracket safeguard: at the root the Newton step is below an ulp
+        // and may land on the endpoint x just became, which must not trigger a bisection from a far bracket
+        const bool conv = fabs(xn - x) <= 1e-12;
+        if (conv)
+          xn = fmin(fmax(xn, a), b);
+        else if (!(xn > a && xn < b))
+          xn = 0.5 * (a + b);
+        fin = conv || b - a <= 1e-15 || it >= 100;
         xr = xn;
         x = xn;
       } else {
