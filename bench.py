@@ -36,26 +36,30 @@ UNIT = "paths/s"
 #            per pair reaching the elimination (counter n_elims): Bezout 128 + Laplace 316
 #                      + normalise r 11 + Bernstein level 155                                = 610
 #   roots  : 2 per FMA term of the root-finding evaluations (counter n_eval_terms)   [k1_roots]
-#   path   :                                                                        [k1_path]
-#            + 468 per coefficient-phase rebuild (counter n_rebuilds)
-#            + 430 per candidate (back-substitution 25, one (a,b) Newton step 277, Eq. 3 + sides 130)
+#   path   :                                                              [k1_cand + k1_path]
+#            + 25 per candidate (back-substitution: a(., v*) slices + stable quadratic)
+#            + 407 per refined candidate (past the domain pre-check, counter n_refined: one (a,b)
+#              Newton step 277, Eq. 3 residual + sides 130)
 #            + 250 per admissible chain (analytic ray-differential Jacobian)
+#            The path kernels recompute the coefficient phase from the geometry instead of storing it;
+#            that recomputation is implementation overhead, already counted once in phase 1, and is
+#            not charged again.
 FLOP_PHASE1_PER_PAIR_R = 484
 FLOP_PHASE1_PER_ELIM_R = 610
 FLOP_PER_EVAL_TERM = 2
-FLOP_PER_REBUILD_R = 468
-FLOP_PER_CANDIDATE_R = 430
+FLOP_PER_CANDIDATE_R = 25
+FLOP_PER_REFINED_R = 407
 FLOP_PER_ADMISSIBLE_R = 250
 
 
 # one-bounce refraction (T), same accounting: phase 1 per pair: decision 60 + setup 18 + a 75 + b (square
 # form, Eq. 9) 656 + normalise/truncate 55 + coplanarity test 16 = 880; per elimination: resultant by
-# pseudo-remainder 998 + Bernstein (degree 12) 260 = 1258; rebuild 864; candidate 755 (b has 28
-# coefficients); admissible 300 (refraction Jacobian).
+# pseudo-remainder 998 + Bernstein (degree 12) 260 = 1258; candidate 25 (back-substitution); refined
+# candidate 730 (b has 28 coefficients); admissible 300 (refraction Jacobian).
 FLOP_PHASE1_PER_PAIR_T = 880
 FLOP_PHASE1_PER_ELIM_T = 1258
-FLOP_PER_REBUILD_T = 864
-FLOP_PER_CANDIDATE_T = 755
+FLOP_PER_CANDIDATE_T = 25
+FLOP_PER_REFINED_T = 730
 FLOP_PER_ADMISSIBLE_T = 300
 
 
@@ -68,8 +72,8 @@ def flop_model(chain, rep):
         p1 = rep["n_pairs_in"] * (FLOP_PHASE1_PER_PAIR_R if R else FLOP_PHASE1_PER_PAIR_T) + rep["n_elims"] * (
             FLOP_PHASE1_PER_ELIM_R if R else FLOP_PHASE1_PER_ELIM_T)
         roots = rep["n_eval_terms"] * FLOP_PER_EVAL_TERM
-        path = (rep["n_rebuilds"] * (FLOP_PER_REBUILD_R if R else FLOP_PER_REBUILD_T) +
-                rep["n_candidates"] * (FLOP_PER_CANDIDATE_R if R else FLOP_PER_CANDIDATE_T) +
+        path = (rep["n_candidates"] * (FLOP_PER_CANDIDATE_R if R else FLOP_PER_CANDIDATE_T) +
+                rep["n_refined"] * (FLOP_PER_REFINED_R if R else FLOP_PER_REFINED_T) +
                 rep["n_admissible"] * (FLOP_PER_ADMISSIBLE_R if R else FLOP_PER_ADMISSIBLE_T))
         return {f"k1_phase1<{chain}>": (p1, "ms_phase1"), f"k1_roots<{chain}>": (roots, "ms_roots"),
                 f"k1_path<{chain}>": (path, "ms_path")}
@@ -356,7 +360,7 @@ def main():
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
                                                  "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims",
-                                                 "n_pairs_coarse")},
+                                                 "n_pairs_coarse", "n_refined", "n_cand_jobs", "n_path_jobs")},
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,

@@ -120,7 +120,11 @@ typedef struct {
   uint64_t n_pairs_coarse;            /* two-bounce pair cull: pairs kept before the subdivision
                                          refinement (n_pairs_in counts the refined list)            */
   float ms_roots, ms_path;            /* one-bounce phase 2 split: root finding (k1_roots + deep
-                                         jobs) and path kernel (incl. the count read-back)          */
+                                         jobs) and path kernels (incl. the count read-back)         */
+  uint64_t n_refined;                 /* one-bounce candidates past the domain pre-check (refined,
+                                         reading R2; FLOP model)                                     */
+  uint64_t n_cand_jobs, n_path_jobs;  /* one-bounce monotone jobs with a root seen by the candidate
+                                         pre-pass / jobs the path kernel ran (pre-pass list + deep)  */
 } spoly_report;
 
 typedef struct {

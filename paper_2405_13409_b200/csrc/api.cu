@@ -455,7 +455,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   ctx->npairs_culled = 0;
   memset(out, 0, sizeof(*out));
   out->k = k;
-  CK(ctx->d_count.ensure(2));
+  CK(ctx->d_count.ensure(6));
   CK(ctx->d_counters.ensure(C_NUM));
   CK(ctx->o_per_query.ensure(nq));
   CK(cudaEventRecord(ctx->ev[0], st));
@@ -597,13 +597,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   spoly_status s = ensure_sink(ctx, std::max<uint64_t>(ctx->d_key.cap, ctx->cfg.max_solutions),
                                std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
   if (s != SPOLY_OK) return s;
-  CK(ctx->d_count.ensure(4));
+  CK(ctx->d_count.ensure(6));
   CK(ctx->d_jpair.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jmeta.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jr.ensure(k == 1 ? npairs * kJobStride : kJobStride));
-  unsigned long long cnt[4] = {0, 0, 0, 0};
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
-    CK(cudaMemsetAsync(ctx->d_count.p, 0, 4 * sizeof(unsigned long long), st));
+    CK(cudaMemsetAsync(ctx->d_count.p, 0, 6 * sizeof(unsigned long long), st));
     CK(cudaMemsetAsync(ctx->d_counters.p, 0, C_NUM * sizeof(unsigned long long), st));
     SolSink S = raw_sink(ctx);
     JobSink J;
@@ -612,6 +612,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
+    J.lcount = ctx->d_count.p + 4;
     CK(cudaEventRecord(ctx->ev[4], st));
     if (k == 1) {
       launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
@@ -622,7 +623,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       CK(cudaEventRecord(ctx->ev[6], st));
       launch_solve_k1(3, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
                       ctx->nsm, st);
-      ctx->launches += 4;
+      ctx->launches += 5;
     } else {
       CK(cudaEventRecord(ctx->ev[5], st));
       {
@@ -777,6 +778,9 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_jobs_deep = cnt[3];
   R.n_launches = ctx->launches;
   R.n_eval_terms = counters[C_EVAL_TERMS];
+  R.n_refined = counters[C_REFINED];
+  R.n_cand_jobs = counters[C_CAND_JOBS];
+  R.n_path_jobs = cnt[4];
   return SPOLY_OK;
 }
 

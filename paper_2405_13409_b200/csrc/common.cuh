@@ -120,9 +120,10 @@ struct JobSink {
   uint32_t* pair;
   uint32_t* meta;  // kfree | deg << 8
   double* r;       // kJobStride per job (phase 2 overwrites it with [count, roots...])
+  unsigned long long* lcount;  // path-phase job list length (candidate pre-pass output)
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,
-       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_NUM };
+       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_REFINED, C_CAND_JOBS, C_NUM };
 
 }  // namespace spoly

@@ -27,8 +27,9 @@ struct Sys1 {
   int da, db, n;
 };
 
-// decisions + coefficient phase + normalisation/truncation; false when the system is degenerate
-template <bool TC>
+// decisions + coefficient phase + normalisation/truncation; false when the system is degenerate.
+// WITH_B = false builds only a (same arithmetic, bit-identical A) for the candidate pre-pass.
+template <bool TC, bool WITH_B = true>
 __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], const d3 N_in[3],
                                              const SolveParams& prm, Sys1<TC>& S) {
   constexpr int DB = Sys1<TC>::DB;
@@ -58,22 +59,25 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
   const d3 e1 = p1 - p0, e2 = p2 - p0, m1 = n1 - n0, m2 = n2 - n0;
   const d3 q = p0 - x0, w = x2 - x0;
   build_a(q, w, e1, e2, n0, m1, m2, S.A);
-  if (TC) {
-    const d3 l = ln > 0 ? (1.0 / ln) * lc : mk3(1, 0, 0);
-    build_b_T(q, w, e1, e2, n0, m1, m2, l, S.eta0, S.eta1, S.B);
-  } else {
-    build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
+  if (WITH_B) {
+    if (TC) {
+      const d3 l = ln > 0 ? (1.0 / ln) * lc : mk3(1, 0, 0);
+      build_b_T(q, w, e1, e2, n0, m1, m2, l, S.eta0, S.eta1, S.B);
+    } else {
+      build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
+    }
   }
-  const double ma = bmaxabs<2, 3>(S.A), mb = bmaxabs<DB, DB + 1>(S.B);
+  const double ma = bmaxabs<2, 3>(S.A), mb = WITH_B ? bmaxabs<DB, DB + 1>(S.B) : 1.0;
   if (!(ma > 0) || !(mb > 0)) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
   }
   bscale<2, 3>(S.A, 1.0 / ma);
-  bscale<DB, DB + 1>(S.B, 1.0 / mb);
+  if (WITH_B) bscale<DB, DB + 1>(S.B, 1.0 / mb);
   S.da = bnum_udeg<2, 3>(S.A, prm.tau_trunc);
-  S.db = bnum_udeg<DB, DB + 1>(S.B, prm.tau_trunc);
   btrunc_u<2, 3>(S.A, S.da);
+  if (!WITH_B) return true;
+  S.db = bnum_udeg<DB, DB + 1>(S.B, prm.tau_trunc);
   btrunc_u<DB, DB + 1>(S.B, S.db);
   S.n = max(S.da, S.db);
   if (S.n == 0) {
@@ -239,6 +243,41 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
   flush_counters(S, cnt);
 }
 
+// real roots u of a(., v*) when a is quadratic / linear in u (stable formula, disc clamp; reading R4),
+// sorted, merged below 1e-7
+__device__ __forceinline__ int quadratic_u_roots(const double al[3], double* ua, uint32_t* flags) {
+  int nu = 0;
+  if (al[2] != 0.0) {
+    const double a0 = al[0], a1 = al[1], a2 = al[2];
+    double disc = a1 * a1 - 4.0 * a2 * a0;
+    const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
+    if (fabs(disc) <= 1e-8 * sc) *flags |= SPOLY_FLAG_NEAR_TANGENT;
+    if (!(disc < -1e-12 * sc)) {
+      if (disc < 0) disc = 0;
+      const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+      if (qq == 0.0) {
+        ua[nu++] = 0.0;
+      } else {
+        double r1 = qq / a2, r2 = a0 / qq;
+        if (r1 > r2) {
+          const double t = r1;
+          r1 = r2;
+          r2 = t;
+        }
+        ua[nu++] = r1;
+        if (r2 - r1 >= 1e-7) ua[nu++] = r2;
+      }
+    }
+  } else if (al[1] != 0.0) {
+    ua[nu++] = -al[0] / al[1];
+  }
+  return nu;
+}
+
+// the refinement (reading R2) moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than
+// 3e-3 outside the simplex can neither become admissible nor land within eps_flag of an edge
+__device__ __forceinline__ bool precheck_reject(double us, double vv) { return fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3; }
+
 // ---------------------------------------------------------------------------------------------
 template <bool TC>
 __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
@@ -257,31 +296,7 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
     int nu = 0;
     const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
     if (amax >= 1e-12) {
-      // quadratic / linear in u (stable formula, disc clamp; reading R4)
-      if (al[2] != 0.0) {
-        const double a0 = al[0], a1 = al[1], a2 = al[2];
-        double disc = a1 * a1 - 4.0 * a2 * a0;
-        const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
-        if (fabs(disc) <= 1e-8 * sc) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
-        if (!(disc < -1e-12 * sc)) {
-          if (disc < 0) disc = 0;
-          const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
-          if (qq == 0.0) {
-            ua[nu++] = 0.0;
-          } else {
-            double r1 = qq / a2, r2 = a0 / qq;
-            if (r1 > r2) {
-              const double t = r1;
-              r1 = r2;
-              r2 = t;
-            }
-            ua[nu++] = r1;
-            if (r2 - r1 >= 1e-7) ua[nu++] = r2;
-          }
-        }
-      } else if (al[1] != 0.0) {
-        ua[nu++] = -al[0] / al[1];
-      }
+      nu = quadratic_u_roots(al, ua, &out.flags);
     } else {
       // fallback (c11): a(., v*) == 0 -> roots of b(., v*) on [-0.1, 1.1]
       double bl[DB + 1];
@@ -305,13 +320,12 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
     for (int iu = 0; iu < nu; ++iu) {
       cnt[C_CANDIDATES]++;
       double us = ua[iu], vv = vs;
-      // the refinement below moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than 3e-3
-      // outside the simplex can neither become admissible nor land within eps_flag of an edge: reject it
-      // before refining (identical results, half the path-phase work on C2)
-      if (fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3) {
+      // reject before refining (identical results, half the path-phase work on C2)
+      if (precheck_reject(us, vv)) {
         cnt[C_REJ_DOMAIN]++;
         continue;
       }
+      cnt[C_REFINED]++;
       // reading R2: <= 3 Newton steps on (a, b), keep a step only if |F| decreases and the candidate
       // stays within 1e-3 of its back-substituted position (local refinement, never a search)
       double fa, fau, fav, fb, fbu, fbv;
@@ -532,8 +546,66 @@ __global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint6
   flush_counters(S, cnt);
 }
 
-// ---- phase 2b: back-substitution, refinement, validation, contribution, emission; thread per job (jobs
-// without roots exit at once)
+// ---- phase 2b0: candidate pre-pass over the monotone jobs, thread per job.  Rebuilds only a (bit-identical
+// to phase 1), back-substitutes v* (the same quadratic as the path phase) and applies the same domain
+// pre-check; a job whose every candidate is rejected there and that raises no flag is finished here (its
+// candidates are counted), every other job goes to the path kernel's list (J.meta[0..lcount), free after
+// the root kernels).  The path kernel then runs fewer, less divergent jobs; outputs are unchanged.
+template <bool TC>
+__global__ void __launch_bounds__(128) k1_cand(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                               const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                               SolveParams prm, SolSink S, JobSink J) {
+  uint32_t cnt[C_NUM];
+#pragma unroll
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t nmono = J.count[0];
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = gw * 32; base < nmono; base += nw * 32) {
+    const uint64_t jj = base + lane;
+    bool keep = false;
+    if (jj < nmono && J.r[jj * kJobStride] != 0.0) {
+      cnt[C_CAND_JOBS]++;
+      const uint32_t pair = __ldg(J.pair + jj);
+      const double vs = J.r[jj * kJobStride + 1];
+      d3 P[3], N[3], x0, x2;
+      uint32_t q;
+      load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
+      Sys1<TC> Sys;
+      build_system<TC, false>(x0, x2, P, N, prm, Sys);
+      double al[3];
+      bslices_at<2, 3>(Sys.A, vs, al);
+      const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+      if (!(amax >= 1e-12)) {
+        keep = true;  // a(., v*) == 0: the b fallback runs in the path kernel
+      } else {
+        uint32_t fl = 0, nc = 0, nrej = 0;
+        double ua[2];
+        const int nu = quadratic_u_roots(al, ua, &fl);
+        for (int iu = 0; iu < nu; ++iu) {
+          ++nc;
+          if (precheck_reject(ua[iu], vs))
+            ++nrej;
+          else
+            keep = true;
+        }
+        if (fl) keep = true;
+        if (!keep) {
+          cnt[C_CANDIDATES] += nc;
+          cnt[C_REJ_DOMAIN] += nrej;
+        }
+      }
+    }
+    uint32_t ex;
+    const unsigned long long b = warp_alloc(J.lcount, keep ? 1u : 0u, &ex);
+    if (keep) J.meta[b + ex] = (uint32_t)jj;
+  }
+  flush_counters(S, cnt);
+}
+
+// ---- phase 2b: back-substitution, refinement, validation, contribution, emission; thread per job of the
+// pre-pass list, then the deep jobs (jobs without roots exit at once)
 template <bool TC>
 __global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                const TriRec* __restrict__ tris, const double* __restrict__ ep,
@@ -543,13 +615,13 @@ __global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, 
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t nmono = J.count[0], n = nmono + J.count[1];
+  const uint64_t nl = *J.lcount, n = nl + J.count[1];
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (uint64_t base = gw * 32; base < n; base += nw * 32) {
     const uint64_t i = base + lane;
-    const uint64_t jj = i < nmono ? i : J.capacity - 1 - (i - nmono);
+    const uint64_t jj = i < nl ? (uint64_t)J.meta[i] : J.capacity - 1 - (i - nl);
     const int nv = i < n ? (int)J.r[jj * kJobStride] : 0;
     const bool active = nv > 0;
     PairOut o;
@@ -608,10 +680,13 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
     }
   } else {  // path
-    if (refract)
+    if (refract) {
+      k1_cand<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, prm, S, J);
       k1_path<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
-    else
+    } else {
+      k1_cand<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, prm, S, J);
       k1_path<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
+    }
   }
 }
 
