@@ -117,8 +117,9 @@ typedef struct {
                                          determinant evaluations)                   */
   uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce phase-2 jobs: monotone r / deeper recursion   */
   uint64_t n_elims;                   /* one-bounce pairs that reached the elimination phase       */
-  uint64_t n_pairs_coarse;            /* two-bounce pair cull: pairs kept before the subdivision
-                                         refinement (n_pairs_in counts the refined list)            */
+  uint64_t n_pairs_coarse;            /* pairs kept before the last exact filter: two-bounce pair cull
+                                         before the subdivision refinement; one-bounce R before the
+                                         product-form sign test (n_pairs_in counts the final list)   */
   float ms_roots, ms_path;            /* one-bounce phase 2 split: root finding (k1_roots + deep
                                          jobs) and path kernels (incl. the count read-back)         */
   uint64_t n_refined;                 /* one-bounce candidates past the domain pre-check (refined,

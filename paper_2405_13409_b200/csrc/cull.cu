@@ -73,6 +73,70 @@ __device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, u
   return !(pos || neg);
 }
 
+// Product-form sign test (exact condition, FP32 with margin; reading R21): every admissible
+// reflection zeroes b = (d0.n)(d1.t) + (d0.t)(d1.n) (Eq. 12) for ANY tangent field t perpendicular to n, here
+// t = n x e1.  With barycentric lambda, d0 = sum l_i (p_i - x0), d1 = sum l_i (x2 - p_i), n = sum l_j n_j and
+// t = sum l_j (n_j x e1) are linear, so each factor is a quadratic form whose triangle-Bernstein coefficients
+// are its symmetrised matrix entries, and b's 15 degree-4 Bernstein coefficients follow from the product
+// rule of Bernstein polynomials.  A strict common sign beyond 1e-4 of the term-magnitude bound
+// M = max|d0| max|n| max|d1| max|t| + max|d0| max|t| max|d1| max|n| (FP32 errors are ~1e-6 M) proves b != 0
+// on the closed triangle: no reflection chain, the pair is dropped.
+__device__ __forceinline__ bool bprod_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
+  const float4* r = tris[t].r;
+  const float4 a = __ldg(r), b = __ldg(r + 1), c4 = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+  const f3 p[3] = {{a.x, a.y, a.z}, {a.w, b.x, b.y}, {b.z, b.w, c4.x}};
+  const f3 n[3] = {{c4.y, c4.z, c4.w}, {d.x, d.y, d.z}, {d.w, e.x, e.y}};
+  const f3 e1 = p[1] - p[0];
+  f3 D[3], E[3], T[3];
+  float mD = 0.f, mE = 0.f, mN = 0.f, mT = 0.f;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    D[i] = p[i] - x0;
+    E[i] = x2 - p[i];
+    T[i] = crossf(n[i], e1);
+    mD = fmaxf(mD, dotf(D[i], D[i]));
+    mE = fmaxf(mE, dotf(E[i], E[i]));
+    mN = fmaxf(mN, dotf(n[i], n[i]));
+    mT = fmaxf(mT, dotf(T[i], T[i]));
+  }
+  // symmetrised quadratic forms, Bernstein order (00, 11, 22, 01, 02, 12): P = d0.n, Q = d1.t, R = d0.t, U = d1.n
+  float P[6], Q[6], R[6], U[6];
+  constexpr int I0[6] = {0, 1, 2, 0, 0, 1}, I1[6] = {0, 1, 2, 1, 2, 2};
+#pragma unroll
+  for (int k = 0; k < 6; ++k) {
+    const int i = I0[k], j = I1[k];
+    P[k] = 0.5f * (dotf(D[i], n[j]) + dotf(D[j], n[i]));
+    Q[k] = 0.5f * (dotf(E[i], T[j]) + dotf(E[j], T[i]));
+    R[k] = 0.5f * (dotf(D[i], T[j]) + dotf(D[j], T[i]));
+    U[k] = 0.5f * (dotf(E[i], n[j]) + dotf(E[j], n[i]));
+  }
+  float c[15];
+  c[0] = (P[2] * Q[2] + R[2] * U[2]);
+  c[1] = 0.5f * (P[2] * Q[5] + P[5] * Q[2] + R[2] * U[5] + R[5] * U[2]);
+  c[2] = 0.16666666666666666f * (P[1] * Q[2] + P[2] * Q[1] + R[1] * U[2] + R[2] * U[1]) + 0.6666666666666666f * (P[5] * Q[5] + R[5] * U[5]);
+  c[3] = 0.5f * (P[1] * Q[5] + P[5] * Q[1] + R[1] * U[5] + R[5] * U[1]);
+  c[4] = (P[1] * Q[1] + R[1] * U[1]);
+  c[5] = 0.5f * (P[2] * Q[4] + P[4] * Q[2] + R[2] * U[4] + R[4] * U[2]);
+  c[6] = 0.16666666666666666f * (P[2] * Q[3] + P[3] * Q[2] + R[2] * U[3] + R[3] * U[2]) + 0.3333333333333333f * (P[4] * Q[5] + P[5] * Q[4] + R[4] * U[5] + R[5] * U[4]);
+  c[7] = 0.16666666666666666f * (P[1] * Q[4] + P[4] * Q[1] + R[1] * U[4] + R[4] * U[1]) + 0.3333333333333333f * (P[3] * Q[5] + P[5] * Q[3] + R[3] * U[5] + R[5] * U[3]);
+  c[8] = 0.5f * (P[1] * Q[3] + P[3] * Q[1] + R[1] * U[3] + R[3] * U[1]);
+  c[9] = 0.16666666666666666f * (P[0] * Q[2] + P[2] * Q[0] + R[0] * U[2] + R[2] * U[0]) + 0.6666666666666666f * (P[4] * Q[4] + R[4] * U[4]);
+  c[10] = 0.16666666666666666f * (P[0] * Q[5] + P[5] * Q[0] + R[0] * U[5] + R[5] * U[0]) + 0.3333333333333333f * (P[3] * Q[4] + P[4] * Q[3] + R[3] * U[4] + R[4] * U[3]);
+  c[11] = 0.16666666666666666f * (P[0] * Q[1] + P[1] * Q[0] + R[0] * U[1] + R[1] * U[0]) + 0.6666666666666666f * (P[3] * Q[3] + R[3] * U[3]);
+  c[12] = 0.5f * (P[0] * Q[4] + P[4] * Q[0] + R[0] * U[4] + R[4] * U[0]);
+  c[13] = 0.5f * (P[0] * Q[3] + P[3] * Q[0] + R[0] * U[3] + R[3] * U[0]);
+  c[14] = (P[0] * Q[0] + R[0] * U[0]);
+  const float M = sqrtf(mD * mN * mE * mT) * 2.f;
+  const float m = 1e-4f * M;
+  bool pos = true, neg = true;
+#pragma unroll
+  for (int k = 0; k < 15; ++k) {
+    pos = pos && c[k] > m;
+    neg = neg && c[k] < -m;
+  }
+  return !(pos || neg);
+}
+
 template <bool REFRACT>
 __device__ __forceinline__ bool test_tri(f3 x0, f3 x2, const TriCull& T, float ef, float eb) {
   f3 ap, an;
@@ -305,7 +369,8 @@ __global__ void __launch_bounds__(256) k_query_cull(const double* __restrict__ e
                                                     const uint32_t* __restrict__ tile_list,
                                                     const uint32_t* __restrict__ tile_count, uint32_t* counts,
                                                     uint32_t* __restrict__ masks) {
-  const int lane = threadIdx.x & 31;
+  __shared__ uint32_t squeue[8][64];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   const uint32_t words = (cap + 31) / 32;
@@ -318,6 +383,7 @@ __global__ void __launch_bounds__(256) k_query_cull(const double* __restrict__ e
     const uint32_t* list = tile_list + (uint64_t)t * cap;
     uint32_t* mrow = masks + (uint64_t)q * words;
     uint32_t count = 0;
+    int qn = 0;  // R: positions j passing the cone + coplanarity tests, queued for the product-form test
     for (uint32_t b = 0; b < n; b += 32) {
       const uint32_t j = b + lane;
       bool k = false;
@@ -328,6 +394,27 @@ __global__ void __launch_bounds__(256) k_query_cull(const double* __restrict__ e
       const unsigned m = __ballot_sync(0xffffffffu, k);
       if (lane == 0) mrow[b / 32] = m;
       count += __popc(m);
+      if (!REFRACT) {
+        // product-form sign test (reading R21) on full warps of queued survivors: a failing pair clears its
+        // mask bit (same warp, ordered by __syncwarp)
+        if (k) squeue[wib][qn + __popc(m & ((1u << lane) - 1u))] = j;
+        qn += __popc(m);
+        const bool last = b + 32 >= n;
+        while (qn >= 32 || (last && qn > 0)) {
+          __syncwarp();
+          const int take = qn < 32 ? qn : 32;
+          bool fail = false;
+          uint32_t jj = 0;
+          if (lane < take) {
+            jj = squeue[wib][qn - take + lane];
+            fail = !bprod_keep(tris, list[jj], x0, x2);
+          }
+          __syncwarp();
+          if (fail) atomicAnd(mrow + jj / 32, ~(1u << (jj & 31)));
+          count -= __popc(__ballot_sync(0xffffffffu, fail));
+          qn -= take;
+        }
+      }
     }
     if (lane == 0) counts[q] = count;
   }
