@@ -93,7 +93,7 @@ struct spoly_ctx {
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
-  DBuf<double> d_bary, d_contrib, d_jr;
+  DBuf<double> d_bary, d_contrib, d_jr, d_jroot;
   DBuf<float> d_resid;
   // sorted output
   DBuf<uint32_t> o_query, o_tuple, o_flags, o_fquery, o_ftuple, o_fflags;
@@ -189,7 +189,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
-  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release();
+  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
   ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
@@ -601,6 +601,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(ctx->d_jpair.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jmeta.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jr.ensure(k == 1 ? npairs * kJobStride : kJobStride));
+  CK(ctx->d_jroot.ensure(k == 1 ? npairs : 1));
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     CK(cudaMemsetAsync(ctx->d_count.p, 0, 6 * sizeof(unsigned long long), st));
@@ -608,11 +609,12 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     SolSink S = raw_sink(ctx);
     JobSink J;
     J.count = ctx->d_count.p + 2;
-    J.capacity = std::min(ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride);
+    J.capacity = std::min({ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride, ctx->d_jroot.cap});
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
     J.lcount = ctx->d_count.p + 4;
+    J.root = ctx->d_jroot.p;
     CK(cudaEventRecord(ctx->ev[4], st));
     if (k == 1) {
       launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,

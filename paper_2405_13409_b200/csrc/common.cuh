@@ -112,14 +112,15 @@ struct SolSink {
   uint32_t* fflags;
   unsigned long long* counters;  // [C_NUM]
 };
-constexpr int kJobStride = 13;  // doubles per job (r(v) up to degree 12)
+constexpr int kJobStride = 13;  // max doubles per job (r(v) up to degree 12; R uses 10)
 // dense job list between the two solve phases
 struct JobSink {
   unsigned long long* count;
   uint64_t capacity;
   uint32_t* pair;
   uint32_t* meta;  // kfree | deg << 8
-  double* r;       // kJobStride per job (phase 2 overwrites it with [count, roots...])
+  double* r;       // NR (coefficients of r) per job; deep jobs: phase 2 overwrites it with [count, roots...]
+  double* root;    // per job: the root of a monotone job (NaN: none), written by the root kernel
   unsigned long long* lcount;  // path-phase job list length (candidate pre-pass output)
 };
 

@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
       J.pair[p] = (uint32_t)i;
       J.meta[p] = meta;
 #pragma unroll
-      for (int t = 0; t < NR; ++t) J.r[p * kJobStride + t] = r[t];
+      for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
     }
   }
   flush_counters(S, cnt);
@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
       if (my < cend) {
         jj = my;
 #pragma unroll
-        for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * kJobStride + i);
+        for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * NR + i);
         double f1 = c[NR - 1];
 #pragma unroll
         for (int i = NR - 2; i >= 0; --i) f1 += c[i];  // r(1)
@@ -445,8 +445,7 @@ __global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
         if (f0 == 0.0 || f1 == 0.0 || (f0 < 0.0) == (f1 < 0.0)) {
           // exact endpoint root, or (rounding) no sign change: finish at once
           const bool has = f0 == 0.0 || f1 == 0.0;
-          J.r[jj * kJobStride] = has ? 1.0 : 0.0;
-          J.r[jj * kJobStride + 1] = f0 == 0.0 ? 0.0 : 1.0;
+          J.root[jj] = has ? (f0 == 0.0 ? 0.0 : 1.0) : __longlong_as_double(0x7ff8000000000000ll);
           cnt[C_VROOTS] += has;
         } else {
           a = 0.0;
@@ -496,8 +495,7 @@ __global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
         fin = true;
       }
       if (fin) {
-        J.r[jj * kJobStride] = 1.0;
-        J.r[jj * kJobStride + 1] = xr;
+        J.root[jj] = xr;
         cnt[C_VROOTS]++;
         busy = false;
       }
@@ -529,7 +527,7 @@ __global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint6
       const uint32_t meta = __ldg(J.meta + jj);
       double r[NR];
 #pragma unroll
-      for (int i = 0; i < NR; ++i) r[i] = __ldg(J.r + jj * kJobStride + i);
+      for (int i = 0; i < NR; ++i) r[i] = __ldg(J.r + jj * NR + i);
       RootSet<NR> R;
       isolate_roots<NR>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
       cnt[C_EVAL_TERMS] += R.terms;
@@ -538,8 +536,8 @@ __global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint6
       for (int i = 0; i < R.n; ++i)
         if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
       cnt[C_VROOTS] += nv;
-      J.r[jj * kJobStride] = (double)nv;
-      for (int i = 0; i < nv; ++i) J.r[jj * kJobStride + 1 + i] = vr[i];
+      J.r[jj * NR] = (double)nv;
+      for (int i = 0; i < nv; ++i) J.r[jj * NR + 1 + i] = vr[i];
     }
     emit_flag(active && flags != 0, flags, pair, S);
   }
@@ -565,10 +563,10 @@ __global__ void __launch_bounds__(128) k1_cand(const uint32_t* __restrict__ pq, 
   for (uint64_t base = gw * 32; base < nmono; base += nw * 32) {
     const uint64_t jj = base + lane;
     bool keep = false;
-    if (jj < nmono && J.r[jj * kJobStride] != 0.0) {
+    const double vs = jj < nmono ? J.root[jj] : 0.0;
+    if (jj < nmono && !isnan(vs)) {
       cnt[C_CAND_JOBS]++;
       const uint32_t pair = __ldg(J.pair + jj);
-      const double vs = J.r[jj * kJobStride + 1];
       d3 P[3], N[3], x0, x2;
       uint32_t q;
       load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
@@ -622,7 +620,9 @@ __global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, 
   for (uint64_t base = gw * 32; base < n; base += nw * 32) {
     const uint64_t i = base + lane;
     const uint64_t jj = i < nl ? (uint64_t)J.meta[i] : J.capacity - 1 - (i - nl);
-    const int nv = i < n ? (int)J.r[jj * kJobStride] : 0;
+    // monotone jobs (pre-pass list): the compact root; deep jobs: [count, roots...] in place of r
+    const double r0 = i < nl ? J.root[jj] : 0.0;
+    const int nv = i < nl ? (isnan(r0) ? 0 : 1) : (i < n ? (int)J.r[jj * NR] : 0);
     const bool active = nv > 0;
     PairOut o;
     o.nsol = 0;
@@ -631,7 +631,10 @@ __global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, 
     if (active) {
       pair = __ldg(J.pair + jj);
       double vr[NR];
-      for (int k = 0; k < nv; ++k) vr[k] = J.r[jj * kJobStride + 1 + k];
+      if (i < nl)
+        vr[0] = r0;
+      else
+        for (int k = 0; k < nv; ++k) vr[k] = J.r[jj * NR + 1 + k];
       d3 P[3], N[3], x0, x2;
       uint32_t q;
       load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
