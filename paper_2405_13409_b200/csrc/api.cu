@@ -93,13 +93,14 @@ struct spoly_ctx {
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
-  DBuf<double> d_bary, d_contrib, d_jr, d_jroot;
+  DBuf<double> d_bary, d_contrib, d_jr, d_jroot, d_jA;
   DBuf<float> d_resid;
   // sorted output
   DBuf<uint32_t> o_query, o_tuple, o_flags, o_fquery, o_ftuple, o_fflags;
   DBuf<double> o_bary, o_contrib, o_per_query;
   DBuf<float> o_resid;
   DBuf<unsigned char> d_temp;
+  DBuf<uint32_t> d_k32;
   // host staging
   DBuf<double> d_ep, d_int;
   double* h_pinned = nullptr;
@@ -189,11 +190,11 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
-  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release();
+  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release(); ctx->d_jA.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
   ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
-  ctx->o_per_query.release(); ctx->o_resid.release(); ctx->d_temp.release(); ctx->d_ep.release(); ctx->d_int.release();
+  ctx->o_per_query.release(); ctx->o_resid.release(); ctx->d_temp.release(); ctx->d_k32.release(); ctx->d_ep.release(); ctx->d_int.release();
   if (ctx->h_pinned) cudaFreeHost(ctx->h_pinned);
   for (auto& e : ctx->ev)
     if (e) cudaEventDestroy(e);
@@ -602,6 +603,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(ctx->d_jmeta.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jr.ensure(k == 1 ? npairs * kJobStride : kJobStride));
   CK(ctx->d_jroot.ensure(k == 1 ? npairs : 1));
+  CK(ctx->d_jA.ensure(k == 1 ? npairs * 6 : 6));
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     CK(cudaMemsetAsync(ctx->d_count.p, 0, 6 * sizeof(unsigned long long), st));
@@ -609,12 +611,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     SolSink S = raw_sink(ctx);
     JobSink J;
     J.count = ctx->d_count.p + 2;
-    J.capacity = std::min({ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride, ctx->d_jroot.cap});
+    J.capacity = std::min({ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride, ctx->d_jroot.cap, ctx->d_jA.cap / 6});
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
     J.lcount = ctx->d_count.p + 4;
     J.root = ctx->d_jroot.p;
+    J.A = ctx->d_jA.p;
     CK(cudaEventRecord(ctx->ev[4], st));
     if (k == 1) {
       launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
@@ -718,14 +721,27 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_iota(ctx->d_perm_in.p, n, st);
     ctx->launches++;
     size_t tb = 0;
-    CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p, ctx->d_perm_out.p,
-                                       (int64_t)n, 0, end_bit, st));
-    CK(ctx->d_temp.ensure(tb));
-    CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p,
-                                       ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
-    launch_gather_solutions(ctx->d_perm_out.p, ctx->d_key2.p, n, k, in, ctx->d_pq.p, ctx->d_pt.p, ctx->M.orig_id, o,
-                            st);
-    launch_solution_flags(ctx->d_key2.p, n, ctx->d_upair.p, ctx->d_uflags.p, nf, o.flags, st);
+    const uint32_t* k32 = nullptr;
+    if (end_bit <= 32) {
+      CK(ctx->d_k32.ensure(2 * n));
+      launch_key32(ctx->d_key.p, n, ctx->d_k32.p, st);
+      ctx->launches++;
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_k32.p, ctx->d_k32.p + n, ctx->d_perm_in.p,
+                                         ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
+      CK(ctx->d_temp.ensure(tb));
+      CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_k32.p, ctx->d_k32.p + n, ctx->d_perm_in.p,
+                                         ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
+      k32 = ctx->d_k32.p + n;
+    } else {
+      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p,
+                                         ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
+      CK(ctx->d_temp.ensure(tb));
+      CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_key.p, ctx->d_key2.p, ctx->d_perm_in.p,
+                                         ctx->d_perm_out.p, (int64_t)n, 0, end_bit, st));
+    }
+    launch_gather_solutions(ctx->d_perm_out.p, ctx->d_key2.p, k32, n, k, in, ctx->d_pq.p, ctx->d_pt.p,
+                            ctx->M.orig_id, o, st);
+    launch_solution_flags(ctx->d_key2.p, k32, n, ctx->d_upair.p, ctx->d_uflags.p, nf, o.flags, st);
     ctx->launches += 2;
   }
   launch_per_query_sorted(ctx->o_query.p, ctx->o_contrib.p, n, nq, ctx->o_per_query.p, st);

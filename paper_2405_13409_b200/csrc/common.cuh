@@ -120,7 +120,8 @@ struct JobSink {
   uint32_t* pair;
   uint32_t* meta;  // kfree | deg << 8
   double* r;       // NR (coefficients of r) per job; deep jobs: phase 2 overwrites it with [count, roots...]
-  double* root;    // per job: the root of a monotone job (NaN: none), written by the root kernel
+  double* root;    // per job: the root of a monotone job kept for the path kernel (NaN: none / finished)
+  double* A;       // per monotone job: phase 1's normalised a (6 coefficients: u^0 v^0..2, u v^0..1, u^2)
   unsigned long long* lcount;  // path-phase job list length (candidate pre-pass output)
 };
 

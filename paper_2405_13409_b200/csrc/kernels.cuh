@@ -71,14 +71,16 @@ struct OutArrays {
 };
 void launch_map_ids(const uint32_t* tpos, uint64_t n, const uint32_t* orig_id, uint32_t* out, cudaStream_t st);
 void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
-void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, uint64_t n, int k,
-                             const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
+void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, const uint32_t* skey32, uint64_t n,
+                             int k, const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
                              const OutArrays& out, cudaStream_t st);
+void launch_key32(const unsigned long long* key, uint64_t n, uint32_t* out, cudaStream_t st);
 void launch_gather_flagged(const unsigned long long* upair, const uint32_t* uflags, uint64_t n, int k,
                            const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id, const OutArrays& out,
                            cudaStream_t st);
-void launch_solution_flags(const unsigned long long* skey, uint64_t n, const unsigned long long* upair,
-                           const uint32_t* uflags, uint64_t nf, uint32_t* flags, cudaStream_t st);
+void launch_solution_flags(const unsigned long long* skey, const uint32_t* skey32, uint64_t n,
+                           const unsigned long long* upair, const uint32_t* uflags, uint64_t nf, uint32_t* flags,
+                           cudaStream_t st);
 void launch_per_query_sorted(const uint32_t* query, const double* contrib, uint64_t n, uint32_t nq, double* per_query,
                              cudaStream_t st);
 

@@ -23,12 +23,13 @@ void launch_map_ids(const uint32_t* tpos, uint64_t n, const uint32_t* orig_id, u
   if (n) k_map_ids<<<1024, 256, 0, st>>>(tpos, n, orig_id, out);
 }
 
-__global__ void k_gather_solutions(const uint32_t* __restrict__ perm, const unsigned long long* __restrict__ skey,
+template <class KeyT>
+__global__ void k_gather_solutions(const uint32_t* __restrict__ perm, const KeyT* __restrict__ skey,
                                    uint64_t n, int k, SolSink in, const uint32_t* __restrict__ pq,
                                    const uint32_t* __restrict__ pt, const uint32_t* __restrict__ orig, OutArrays out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t s = perm[i];
-    const uint64_t pair = skey[i] >> 6;
+    const uint64_t pair = (uint64_t)skey[i] >> 6;
     out.query[i] = pq[pair];
     for (int j = 0; j < k; ++j) out.tuple[(uint64_t)k * i + j] = orig[pt[(uint64_t)k * pair + j]];
     for (int j = 0; j < 2 * k; ++j) out.bary[(uint64_t)2 * k * i + j] = in.bary[(uint64_t)2 * k * s + j];
@@ -36,10 +37,23 @@ __global__ void k_gather_solutions(const uint32_t* __restrict__ perm, const unsi
     out.resid[i] = in.resid[s];
   }
 }
-void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, uint64_t n, int k,
-                             const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
+void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, const uint32_t* skey32, uint64_t n,
+                             int k, const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
                              const OutArrays& out, cudaStream_t st) {
-  if (n) k_gather_solutions<<<2048, 256, 0, st>>>(perm, skey, n, k, in, pq, pt, orig_id, out);
+  if (!n) return;
+  if (skey32)
+    k_gather_solutions<uint32_t><<<2048, 256, 0, st>>>(perm, skey32, n, k, in, pq, pt, orig_id, out);
+  else
+    k_gather_solutions<unsigned long long><<<2048, 256, 0, st>>>(perm, skey, n, k, in, pq, pt, orig_id, out);
+}
+
+// keys below 2^32 (pair index << 6 | slot): sorted as 32-bit keys (two thirds of the radix-sort traffic)
+__global__ void k_key32(const unsigned long long* __restrict__ key, uint64_t n, uint32_t* __restrict__ out) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    out[i] = (uint32_t)key[i];
+}
+void launch_key32(const unsigned long long* key, uint64_t n, uint32_t* out, cudaStream_t st) {
+  if (n) k_key32<<<1024, 256, 0, st>>>(key, n, out);
 }
 
 __global__ void k_gather_flagged(const unsigned long long* __restrict__ upair, const uint32_t* __restrict__ uflags,
@@ -59,11 +73,12 @@ void launch_gather_flagged(const unsigned long long* upair, const uint32_t* ufla
 }
 
 // every solution carries its tuple's (OR-reduced) flags: binary search of its pair in the sorted list
-__global__ void k_solution_flags(const unsigned long long* __restrict__ skey, uint64_t n,
+template <class KeyT>
+__global__ void k_solution_flags(const KeyT* __restrict__ skey, uint64_t n,
                                  const unsigned long long* __restrict__ upair, const uint32_t* __restrict__ uflags,
                                  uint64_t nf, uint32_t* flags) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long pair = skey[i] >> 6;
+    const unsigned long long pair = (unsigned long long)skey[i] >> 6;
     uint64_t lo = 0, hi = nf;
     while (lo < hi) {
       const uint64_t m = (lo + hi) >> 1;
@@ -72,9 +87,14 @@ __global__ void k_solution_flags(const unsigned long long* __restrict__ skey, ui
     flags[i] = (lo < nf && upair[lo] == pair) ? uflags[lo] : 0u;
   }
 }
-void launch_solution_flags(const unsigned long long* skey, uint64_t n, const unsigned long long* upair,
-                           const uint32_t* uflags, uint64_t nf, uint32_t* flags, cudaStream_t st) {
-  if (n) k_solution_flags<<<2048, 256, 0, st>>>(skey, n, upair, uflags, nf, flags);
+void launch_solution_flags(const unsigned long long* skey, const uint32_t* skey32, uint64_t n,
+                           const unsigned long long* upair, const uint32_t* uflags, uint64_t nf, uint32_t* flags,
+                           cudaStream_t st) {
+  if (!n) return;
+  if (skey32)
+    k_solution_flags<uint32_t><<<2048, 256, 0, st>>>(skey32, n, upair, uflags, nf, flags);
+  else
+    k_solution_flags<unsigned long long><<<2048, 256, 0, st>>>(skey, n, upair, uflags, nf, flags);
 }
 
 // one warp per query: binary-search its range in the query-sorted solution list, then a fixed-order

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
     const bool active = i < npairs;
     bool job = false;
     uint32_t flags = 0, meta = 0;
-    double r[NR];
+    double r[NR], Aj[6];
     if (active) {
       d3 P[3], N[3], x0, x2;
       uint32_t q;
@@ -196,6 +196,8 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
       } else if (ok) {
         cnt[C_EVAL_TERMS] += 8;
         cnt[C_ELIMS]++;
+        Aj[0] = Sys.A[0]; Aj[1] = Sys.A[1]; Aj[2] = Sys.A[2];
+        Aj[3] = Sys.A[3]; Aj[4] = Sys.A[4]; Aj[5] = Sys.A[6];
         eliminate<TC>(Sys, r);
         double mr = 0.0;
 #pragma unroll
@@ -238,6 +240,10 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
       J.meta[p] = meta;
 #pragma unroll
       for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
+      if (mono) {
+#pragma unroll
+        for (int t = 0; t < 6; ++t) J.A[p * 6 + t] = Aj[t];
+      }
     }
   }
   flush_counters(S, cnt);
@@ -544,15 +550,12 @@ __global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint6
   flush_counters(S, cnt);
 }
 
-// ---- phase 2b0: candidate pre-pass over the monotone jobs, thread per job.  Rebuilds only a (bit-identical
-// to phase 1), back-substitutes v* (the same quadratic as the path phase) and applies the same domain
-// pre-check; a job whose every candidate is rejected there and that raises no flag is finished here (its
-// candidates are counted), every other job goes to the path kernel's list (J.meta[0..lcount), free after
-// the root kernels).  The path kernel then runs fewer, less divergent jobs; outputs are unchanged.
-template <bool TC>
-__global__ void __launch_bounds__(128) k1_cand(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
-                                               const TriRec* __restrict__ tris, const double* __restrict__ ep,
-                                               SolveParams prm, SolSink S, JobSink J) {
+// ---- phase 2b0: candidate pre-pass over the monotone jobs, thread per job.  Back-substitutes v* in phase 1's
+// stored (normalised) a (the same quadratic as the path phase) and applies the same domain pre-check; a job
+// whose every candidate is rejected there and that raises no flag is finished here (its candidates are
+// counted), every other job goes to the path kernel's list (J.meta[0..lcount), free after the root
+// kernels).  The path kernel then runs fewer, less divergent jobs; outputs are unchanged.
+__global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
@@ -566,14 +569,12 @@ __global__ void __launch_bounds__(128) k1_cand(const uint32_t* __restrict__ pq, 
     const double vs = jj < nmono ? J.root[jj] : 0.0;
     if (jj < nmono && !isnan(vs)) {
       cnt[C_CAND_JOBS]++;
-      const uint32_t pair = __ldg(J.pair + jj);
-      d3 P[3], N[3], x0, x2;
-      uint32_t q;
-      load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
-      Sys1<TC> Sys;
-      build_system<TC, false>(x0, x2, P, N, prm, Sys);
+      double A[9];
+      A[0] = J.A[jj * 6]; A[1] = J.A[jj * 6 + 1]; A[2] = J.A[jj * 6 + 2];
+      A[3] = J.A[jj * 6 + 3]; A[4] = J.A[jj * 6 + 4]; A[6] = J.A[jj * 6 + 5];
+      A[5] = A[7] = A[8] = 0.0;
       double al[3];
-      bslices_at<2, 3>(Sys.A, vs, al);
+      bslices_at<2, 3>(A, vs, al);
       const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
       if (!(amax >= 1e-12)) {
         keep = true;  // a(., v*) == 0: the b fallback runs in the path kernel
@@ -683,13 +684,11 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
     }
   } else {  // path
-    if (refract) {
-      k1_cand<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, prm, S, J);
+    k1_cand<<<nsm * 8, 256, 0, st>>>(S, J);
+    if (refract)
       k1_path<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
-    } else {
-      k1_cand<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, prm, S, J);
+    else
       k1_path<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
-    }
   }
 }
 

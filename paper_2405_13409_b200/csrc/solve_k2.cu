@@ -558,8 +558,11 @@ __global__ void __launch_bounds__(256) k2_bin(uint64_t np, const double* __restr
 // ---- kernel 2: 100-piece determinant-sign scan + bisection, group per pair of one order
 // class: NC > 0 register determinant of that class; NC = 0 orders above 32 (shared-memory determinant)
 constexpr int kScanWarps = 4;
+// resident blocks per SM the register budget must allow: the scan is latency-bound (dependent shuffles and
+// FP64 chains), so occupancy matters more than the compiler's unconstrained register use (252 for TT)
+__host__ __device__ constexpr int scan_min_blocks(int nc) { return nc == 0 ? 1 : (nc <= 16 ? 4 : (nc <= 24 ? 3 : 2)); }
 template <bool V1T, bool V2T, int NC>
-__global__ void __launch_bounds__(kScanWarps * 32) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
+__global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
                                                           double* __restrict__ recs, SolSink S,
                                                           const uint32_t* __restrict__ clist,
                                                           const unsigned long long* __restrict__ ccount,
