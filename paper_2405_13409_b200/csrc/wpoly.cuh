@@ -80,37 +80,76 @@ __device__ __forceinline__ void padv(int d, int step, int& i, int& j) {
   }
 }
 
-// c = sum_k s_k a_k b_k  (+ c if acc); every product term with i + j <= c.d is produced
+// advance the (row i, chunk start j0) position of output degree d by `step` chunks of W coefficients
+template <int W>
+__device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
+  while (step > 0 && i <= d) {
+    const int left = (d - i + 1 - j0 + W - 1) / W;  // chunks from j0 to the end of row i
+    if (step < left) {
+      j0 += step * W;
+      step = 0;
+    } else {
+      step -= left;
+      ++i;
+      j0 = 0;
+    }
+  }
+}
+
+// c = sum_k s_k a_k b_k  (+ c if acc); every product term with i + j <= c.d is produced.
+// Register-windowed gather: a lane owns W consecutive coefficients (i, j0..j0+W-1) of one output row; for
+// every operand row pair (p, i - p) it walks q once, so each a coefficient is loaded once for the W outputs
+// and the b operands slide through a W-register window (one new load per step): 2 shared-memory loads per W
+// FMAs instead of 2 per FMA.  Out-of-row b positions read as 0 (predicated), so the W outputs may share the
+// union of their q ranges.
 template <int G, int K>
 __device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
-  const int dc = c.d, n = tri_n(dc);
-  int i = 0, j = 0;
-  padv(dc, g.lane, i, j);
-  for (int idx = g.lane; idx < n; idx += G) {
-    double sum = acc ? c.c[idx] : 0.0;
+  constexpr int W = 4;
+  const int dc = c.d;
+  int i = 0, j0 = 0;
+  tadv<W>(dc, g.lane, i, j0);
+  while (i <= dc) {
+    const int rowlen = dc - i + 1;
+    double* cp = c.c + poff(dc, i);
+    double out[W];
 #pragma unroll
-    for (int k = 0; k < K; ++k) {
-      const int da = a[k].d, db = b[k].d;
-      double t = 0.0;
+    for (int k = 0; k < W; ++k) out[k] = (acc && j0 + k < rowlen) ? cp[j0 + k] : 0.0;
+#pragma unroll
+    for (int kk = 0; kk < K; ++kk) {
+      const int da = a[kk].d, db = b[kk].d;
+      double t[W];
+#pragma unroll
+      for (int k = 0; k < W; ++k) t[k] = 0.0;
       const int p0 = max(0, i - db), p1 = min(i, da);
-      double t2 = 0.0;
       for (int p = p0; p <= p1; ++p) {
-        const int q0 = max(0, i + j - p - db), q1 = min(j, da - p);
-        const double* ap = a[k].c + poff(da, p);
-        const double* bp = b[k].c + poff(db, i - p) + j;
-        int q = q0;
-        for (; q + 3 <= q1; q += 4) {  // two accumulators, 4-way unrolled
-          t = fma(ap[q], bp[-q], t);
-          t2 = fma(ap[q + 1], bp[-q - 1], t2);
-          t = fma(ap[q + 2], bp[-q - 2], t);
-          t2 = fma(ap[q + 3], bp[-q - 3], t2);
+        const int blen = db - (i - p);  // b row i - p holds indices 0..blen
+        const double* ap = a[kk].c + poff(da, p);
+        const double* bp = b[kk].c + poff(db, i - p);
+        const int qlo = max(0, j0 - blen), qhi = min(j0 + W - 1, da - p);
+        if (qlo > qhi) continue;
+        double w[W];
+#pragma unroll
+        for (int k = 0; k < W; ++k) {
+          const int jb = j0 + k - qlo;
+          w[k] = (jb >= 0 && jb <= blen) ? bp[jb] : 0.0;
         }
-        for (; q <= q1; ++q) t = fma(ap[q], bp[-q], t);
+        for (int q = qlo; q <= qhi; ++q) {
+          const double av = ap[q];
+#pragma unroll
+          for (int k = 0; k < W; ++k) t[k] = fma(av, w[k], t[k]);
+#pragma unroll
+          for (int k = W - 1; k > 0; --k) w[k] = w[k - 1];
+          const int jb = j0 - q - 1;  // <= blen - 1 because q >= qlo >= j0 - blen
+          w[0] = jb >= 0 ? bp[jb] : 0.0;
+        }
       }
-      sum = fma(s[k], t + t2, sum);
+#pragma unroll
+      for (int k = 0; k < W; ++k) out[k] = fma(s[kk], t[k], out[k]);
     }
-    c.c[idx] = sum;
-    padv(dc, G, i, j);
+#pragma unroll
+    for (int k = 0; k < W; ++k)
+      if (j0 + k < rowlen) cp[j0 + k] = out[k];
+    tadv<W>(dc, G, i, j0);
   }
   g.sync();
 }

@@ -18,7 +18,9 @@ out = {}
 for r in rows[2:]:
     name = r[h.index('Kernel Name')].split('(')[0].strip()
     lines.append(f"| {name} | " + " | ".join(r[h.index(k)] for k in keys) + " |")
-    nm = name.replace('void ', '').replace('<0>', '<R>').replace('<1>', '<T>')
+    nm = name.replace('void ', '').replace('spoly::', '').replace('<0>', '<R>').replace('<1>', '<T>')
+    if nm in out:  # several captured launches of one kernel: keep the first
+        continue
     out[nm] = {"dram_bytes_per_launch": conv(r,'dram__bytes_read.sum') + conv(r,'dram__bytes_write.sum'),
                "duration_ms_ncu": conv(r,'gpu__time_duration.sum'),
                "warp_efficiency_threads": float(r[h.index('smsp__thread_inst_executed_per_inst_executed.ratio')]),
@@ -41,5 +43,12 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
 print("\n".join(lines))
 return_json = sys.argv[4] if len(sys.argv) > 4 else None
 if return_json:
+    # bench.py reports the path phase (k1_cand + k1_path launches) under "k1_path<..>": its traffic is the sum
+    for ch in ("R", "T"):
+        if "k1_cand" in out and f"k1_path<{ch}>" in out:
+            c, pth = out["k1_cand"], out[f"k1_path<{ch}>"]
+            out[f"k1_path<{ch}>"] = dict(pth, dram_bytes_per_launch=c["dram_bytes_per_launch"] + pth["dram_bytes_per_launch"],
+                                        duration_ms_ncu=c["duration_ms_ncu"] + pth["duration_ms_ncu"],
+                                        note="phase = k1_cand + k1_path launches")
     out["_note"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture at the C2 bench config (" + tag + ")"
     json.dump(out, open(return_json, 'w'), indent=1)
