@@ -97,14 +97,14 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 }
 
 // c = sum_k s_k a_k b_k  (+ c if acc); every product term with i + j <= c.d is produced.
-// Register-windowed gather: a lane owns W consecutive coefficients (i, j0..j0+W-1) of one output row; for
+// Register-windowed gather (W = 8): a lane owns W consecutive coefficients (i, j0..j0+W-1) of one output row; for
 // every operand row pair (p, i - p) it walks q once, so each a coefficient is loaded once for the W outputs
 // and the b operands slide through a W-register window (one new load per step): 2 shared-memory loads per W
 // FMAs instead of 2 per FMA.  Out-of-row b positions read as 0 (predicated), so the W outputs may share the
 // union of their q ranges.
 template <int G, int K>
 __device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
-  constexpr int W = 4;
+  constexpr int W = 8;
   const int dc = c.d;
   int i = 0, j0 = 0;
   tadv<W>(dc, g.lane, i, j0);
@@ -323,7 +323,10 @@ __device__ int wdet_rows(const Grp<G>& g, double as, double bs, double aj1, doub
     const bool cand = live && !((used >> l) & 1u);
     unsigned key = 0u;
     if (cand) key = (((unsigned)__double2hiint(fabs(col[c]))) & ~31u) | (unsigned)(31 - l);
-    for (int o = G / 2; o; o >>= 1) key = max(key, g.xor_(key, o));
+    if (G == 32)
+      key = __reduce_max_sync(0xffffffffu, key);  // one REDUX instead of a 5-step shuffle butterfly
+    else
+      for (int o = G / 2; o; o >>= 1) key = max(key, g.xor_(key, o));
     if ((key >> 5) == 0u) {
       *lg = -INFINITY;
       return 0;
