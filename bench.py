@@ -360,7 +360,10 @@ def main():
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
                                                  "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims",
-                                                 "n_pairs_coarse", "n_refined", "n_cand_jobs", "n_path_jobs")},
+                                                 "n_pairs_coarse", "n_refined", "n_cand_jobs", "n_path_jobs",
+                                                 "n_cull_tests")},
+        "cull_tests_per_s": reports[-1]["n_cull_tests"] / (statistics.mean(x["ms_cull"] for x in reports) / 1e3)
+        if reports[-1]["n_cull_tests"] else None,
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
                      "reduce": statistics.mean(x["ms_reduce"] for x in reports)},
         "roofline": {"bound": "alu", "kernel": dom[0], "achieved": achieved / 1e12, "peak": peak / 1e12,

@@ -126,6 +126,9 @@ typedef struct {
                                          reading R2; FLOP model)                                     */
   uint64_t n_cand_jobs, n_path_jobs;  /* one-bounce monotone jobs with a root seen by the candidate
                                          pre-pass / jobs the path kernel ran (pre-pass list + deep)  */
+  uint64_t n_cull_tests;              /* cull work of the last solve: one bounce, triangle tests of the
+                                         per-query cull; two bounces, node-pair tests of the pair
+                                         expansion + sub-pair tests of the subdivision refinement    */
 } spoly_report;
 
 typedef struct {

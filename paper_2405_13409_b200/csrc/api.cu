@@ -88,7 +88,7 @@ struct spoly_ctx {
   DBuf<double> d_rec;
   DBuf<uint32_t> d_plist, d_clist;
   DBuf<unsigned long long> d_nsel;
-  uint64_t npairs = 0, npairs_culled = 0;
+  uint64_t npairs = 0, npairs_culled = 0, cull_tests = 0;
   int last_k = 1;
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
@@ -366,6 +366,7 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
     CK(ctx->d_emask.ensure(nf));
     launch_pair_expand(0, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, ctx->d_emask.p, nullptr, nullptr,
                        nullptr, nullptr, ctx->nsm, st);
+    ctx->cull_tests += nf * (64 + (fq ? 0 : 1));  // child node-pair tests (+ the root pair test)
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
     CK(ctx->d_temp.ensure(tbytes));
@@ -415,6 +416,17 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
       launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
                           ctx->d_keep.p, RW, ctx->nsm, st);
       ctx->launches += RW.launches;
+      {
+        unsigned long long fc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        const int lv = std::min(ctx->cfg.cull_levels, 5);
+        CK(cudaMemcpyAsync(fc, ctx->d_fcount.p, sizeof(unsigned long long) * (size_t)lv, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
+        uint64_t entries = npairs;  // level 0 runs on every coarse pair
+        for (int l = 0; l < lv; ++l) {
+          ctx->cull_tests += 16ull * entries;
+          entries = std::min<uint64_t>(fc[l], fcap);
+        }
+      }
     }
     const uint2* pt_in = reinterpret_cast<const uint2*>(ctx->d_pt.p);
     uint2* pt_out = reinterpret_cast<uint2*>(ctx->d_pt2.p);
@@ -454,6 +466,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   cudaStream_t st = ctx->st;
   ctx->launches = 0;
   ctx->npairs_culled = 0;
+  ctx->cull_tests = 0;
   memset(out, 0, sizeof(*out));
   out->k = k;
   CK(ctx->d_count.ensure(6));
@@ -560,6 +573,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int)nq, st));
     unsigned long long tot = 0;
     CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + nq, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    {
+      // cull work: every query tests its tile's surviving triangles (32 queries per tile; the last tile ragged)
+      std::vector<uint32_t> tc(ntiles);
+      CK(cudaMemcpyAsync(tc.data(), ctx->d_tcount.p, sizeof(uint32_t) * ntiles, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      for (uint32_t t = 0; t < ntiles; ++t) ctx->cull_tests += (uint64_t)tc[t] * std::min<uint32_t>(32, nq - 32 * t);
+    }
     CK(cudaStreamSynchronize(st));
     npairs = tot;
     CK(ctx->d_pq.ensure(npairs));
@@ -799,6 +819,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_refined = counters[C_REFINED];
   R.n_cand_jobs = counters[C_CAND_JOBS];
   R.n_path_jobs = cnt[4];
+  R.n_cull_tests = ctx->cull_tests;
   return SPOLY_OK;
 }
 

@@ -55,7 +55,7 @@ class spoly_report(ctypes.Structure):
         ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64),
         ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64),
         ("ms_roots", ctypes.c_float), ("ms_path", ctypes.c_float), ("n_refined", ctypes.c_uint64),
-        ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64)]
+        ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64), ("n_cull_tests", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -207,7 +207,8 @@ class Context:
                    n_jobs_deep=int(r.report.n_jobs_deep), n_elims=int(r.report.n_elims),
                    n_pairs_coarse=int(r.report.n_pairs_coarse), ms_roots=r.report.ms_roots,
                    ms_path=r.report.ms_path, n_refined=int(r.report.n_refined),
-                   n_cand_jobs=int(r.report.n_cand_jobs), n_path_jobs=int(r.report.n_path_jobs))
+                   n_cand_jobs=int(r.report.n_cand_jobs), n_path_jobs=int(r.report.n_path_jobs),
+                   n_cull_tests=int(r.report.n_cull_tests))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),
