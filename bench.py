@@ -236,11 +236,20 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
 
+    scaling = "weak"
+    shard_idx = None
     if args.config == "C2":
         w = W.glints_c2(res=args.res or 256, seed_strata=2 + rank)  # weak scaling: one full frame per rank
     else:
         kw = {} if args.res is None else {"res": args.res}
         w = W.CONFIGS[args.config](**kw)
+        if world > 1:
+            # strong scaling of one frame: query tiles round-robin over the ranks
+            from paper_2405_13409_b200 import dist as D
+            nq_full = w.nqueries
+            shard_idx = D.shard_tiles(nq_full, world, rank)
+            w = w.subset(shard_idx)
+            scaling = "strong"
     chain = w.chain
     stream = torch.cuda.current_stream(dev)
     cfg = spoly.default_config() if args.cull_levels is None else spoly.default_config(cull_levels=args.cull_levels)
@@ -309,8 +318,11 @@ def main():
         n_paths, n_pairs, launches = int(c[0]), int(c[1]), int(c[2])
         if e2e:
             e2e = [int(c[3]), e2e_max]
-        gathered = [torch.empty_like(r.per_query) for _ in range(world)]
-        dist.all_gather(gathered, r.per_query.contiguous())
+        if shard_idx is None:
+            gathered = [torch.empty_like(r.per_query) for _ in range(world)]
+            dist.all_gather(gathered, r.per_query.contiguous())
+        else:  # ragged shards: padded gather + scatter back to query order
+            D.gather_per_query(r.per_query.contiguous(), shard_idx, nq_full)
 
     # ---- roofline of the dominant kernel, from its own launch's CUDA-event time (recorded by the library on
     # the launching stream around each solve kernel, averaged over the timed steps)
@@ -349,13 +361,14 @@ def main():
     line = {
         "metric": METRIC, "value": n_paths / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "query_tuple_solves_per_s": n_pairs / (total_ms / 1e3),
         "config": {"workload": ("C2 glints: %d light samples x %d-tri normal-mapped bumpy plane, one-bounce R, "
                                 "cull pre-pass + fused FP64 solve + deterministic compaction" % (w.nqueries, w.mesh.ntris))
                    if args.config == "C2" else "%s %s: %d queries x %d tris, chain %s, cull + solve + compaction" % (
                        args.config, w.name, w.nqueries, w.mesh.ntris, chain),
                    "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": chain,
+                   "queries_total": w.nqueries * world if shard_idx is None else int(nq_full),
                    "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",

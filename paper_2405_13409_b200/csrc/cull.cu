@@ -665,7 +665,7 @@ __device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels
 
 // side_keep(tris, t, xref, refract, o) with t's part precomputed in record it and o's vertices in record io
 // (records in the warp's SoA staging f[field][child], flags fl[child])
-__device__ __forceinline__ bool side_keep_rec(const float4 (*f)[16], const int* fl, int it, int io) {
+__device__ __forceinline__ bool side_keep_rec(const float4 (*f)[32], const int* fl, int it, int io) {
   if (fl[it] & 4) return true;
   const float4 G = f[3][it], P0 = f[4][it];
   const f3 g = ld3(G), p0 = ld3(P0);
@@ -675,7 +675,7 @@ __device__ __forceinline__ bool side_keep_rec(const float4 (*f)[16], const int* 
 }
 
 // pair_keep(x0, x3, sA, cA, sB, cB, ...) with the per-node direction bounds precomputed
-__device__ __forceinline__ bool pair_keep_rec(const float4 (*f)[16], const int* fl, int ia, int ib, int v1t, int v2t,
+__device__ __forceinline__ bool pair_keep_rec(const float4 (*f)[32], const int* fl, int ia, int ib, int v1t, int v2t,
                                               float ef, float eb, int side) {
   f3 aAB;
   float cAB;
@@ -723,96 +723,105 @@ __global__ void __launch_bounds__(kExpandThreads, 3) k_pair_expand(int pass, int
                                                      const unsigned long long* __restrict__ offsets,
                                                      uint32_t* __restrict__ oq, uint32_t* __restrict__ oa,
                                                      uint32_t* __restrict__ ob) {
-  // structure-of-arrays staging: field f of child i at smf[warp][f][i], so the 4 (A side) or 8 (B side)
-  // distinct records a warp-wide load touches sit in distinct banks (broadcast, no conflicts)
-  __shared__ float4 smf[kExpandThreads / 32][7][16];
-  __shared__ int smk[kExpandThreads / 32][16];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  // Two frontier entries per warp: half-warp h (lanes 16h..16h+15) stages its entry's 8 + 8 child records
+  // and tests the entry's 64 child pairs, 4 per lane.  Structure-of-arrays staging, record i of half h at
+  // slot 2i + h of smf[warp][field][.], so the records a warp-wide load touches sit in distinct banks.
+  __shared__ float4 smf[kExpandThreads / 32][7][32];
+  __shared__ int smk[kExpandThreads / 32][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5, h = lane >> 4, hl = lane & 15;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const uint32_t nt = L.n[L.top], P = nt * nt;
-  for (uint64_t en = gw; en < nf; en += nw) {
-    uint32_t q, A, B;
-    if (fq) {
-      q = fq[en];
-      A = fa[en];
-      B = fb[en];
-    } else {
-      q = qbase + (uint32_t)(en / P);
-      A = (uint32_t)(en % P) / nt;
-      B = (uint32_t)(en % P) % nt;
+  for (uint64_t e0 = 2 * gw; e0 < nf; e0 += 2 * nw) {
+    const uint64_t en = e0 + h;
+    const bool valid = en < nf;
+    uint32_t q = 0, A = 0, B = 0;
+    if (valid) {
+      if (fq) {
+        q = fq[en];
+        A = fa[en];
+        B = fb[en];
+      } else {
+        q = qbase + (uint32_t)(en / P);
+        A = (uint32_t)(en % P) / nt;
+        B = (uint32_t)(en % P) % nt;
+      }
     }
     if (pass) {
-      const unsigned long long m = masks[en];
-      if (!m) continue;
-      const unsigned long long base = offsets[en];
+      const unsigned long long m = valid ? masks[en] : 0ull;
+      if (m) {
+        const unsigned long long base = offsets[en];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = h * 32 + lane;
-        if ((m >> c) & 1ull) {
-          const unsigned long long pos = base + __popcll(m & ((1ull << c) - 1ull));
-          const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
-          oq[pos] = q;
-          if (cl == 0) {
-            oa[2 * pos] = a;
-            oa[2 * pos + 1] = b;
-          } else {
-            oa[pos] = a;
-            ob[pos] = b;
+        for (int t = 0; t < 4; ++t) {
+          const int c = t * 16 + hl;
+          if ((m >> c) & 1ull) {
+            const unsigned long long pos = base + __popcll(m & ((1ull << c) - 1ull));
+            const uint32_t a = A * 8 + (c >> 3), b = B * 8 + (c & 7);
+            oq[pos] = q;
+            if (cl == 0) {
+              oa[2 * pos] = a;
+              oa[2 * pos + 1] = b;
+            } else {
+              oa[pos] = a;
+              ob[pos] = b;
+            }
           }
         }
       }
       continue;
     }
-    const double* e = ep + 6ull * q;
-    const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]};
-    const f3 x3 = {(float)e[3], (float)e[4], (float)e[5]};
-    bool root_ok = true;
-    if (!fq) {
-      float4 sa, ca, sb, cb;
-      node_bounds(L, cl + 1, A, sa, ca);
-      node_bounds(L, cl + 1, B, sb, cb);
-      root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
-    }
-    unsigned long long m = 0;
-    if (root_ok) {
-      __syncwarp();
-      if (lane < 16) {
-        const bool isB = lane >= 8;
-        ChildRec R;
-        make_child(R, cl, L, tris, (isB ? B : A) * 8 + (lane & 7), isB ? x3 : x0, isB ? v2t : v1t,
-                   !isB && (v1t || v2t));
-        smf[wib][0][lane] = R.sph;
-        smf[wib][1][lane] = R.cone;
-        smf[wib][2][lane] = R.dir;
-        smf[wib][3][lane] = R.g;
-        smf[wib][4][lane] = R.p0;
-        smf[wib][5][lane] = R.p1;
-        smf[wib][6][lane] = R.p2;
-        smk[wib][lane] = R.flags;
+    f3 x0 = {0.f, 0.f, 0.f}, x3 = {0.f, 0.f, 0.f};
+    bool root_ok = valid;
+    if (valid) {
+      const double* e = ep + 6ull * q;
+      x0 = {(float)e[0], (float)e[1], (float)e[2]};
+      x3 = {(float)e[3], (float)e[4], (float)e[5]};
+      if (!fq) {
+        float4 sa, ca, sb, cb;
+        node_bounds(L, cl + 1, A, sa, ca);
+        node_bounds(L, cl + 1, B, sb, cb);
+        root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
       }
-      __syncwarp();
-      bool k[2];
+    }
+    __syncwarp();
+    {
+      const bool isB = hl >= 8;
+      ChildRec R;
+      R.flags = 0;
+      if (root_ok)
+        make_child(R, cl, L, tris, (isB ? B : A) * 8 + (hl & 7), isB ? x3 : x0, isB ? v2t : v1t,
+                   !isB && (v1t || v2t));
+      const int sl = 2 * hl + h;
+      smf[wib][0][sl] = R.sph;
+      smf[wib][1][sl] = R.cone;
+      smf[wib][2][sl] = R.dir;
+      smf[wib][3][sl] = R.g;
+      smf[wib][4][sl] = R.p0;
+      smf[wib][5][sl] = R.p1;
+      smf[wib][6][sl] = R.p2;
+      smk[wib][sl] = R.flags;
+    }
+    __syncwarp();
+    unsigned long long m = 0;
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int c = h * 32 + lane;
-        const int ia = c >> 3, ib = 8 + (c & 7);
-        const int fa_ = smk[wib][ia], fb_ = smk[wib][ib];
-        k[h] = false;
-        if ((fa_ & 1) && (fb_ & 1)) {
-          if (cl == 0) {
-            if (A * 8 + ia != B * 8 + (c & 7))
-              k[h] = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, ((fa_ >> 3) & 3) - 1) &&
-                     side_keep_rec(smf[wib], smk[wib], ia, ib) && side_keep_rec(smf[wib], smk[wib], ib, ia);
-          } else {
-            k[h] = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, -1);
-          }
+    for (int t = 0; t < 4; ++t) {
+      const int c = t * 16 + hl;
+      const int ia = 2 * (c >> 3) + h, ib = 2 * (8 + (c & 7)) + h;
+      const int fa_ = smk[wib][ia], fb_ = smk[wib][ib];
+      bool k = false;
+      if ((fa_ & 1) && (fb_ & 1)) {
+        if (cl == 0) {
+          if (A * 8 + (c >> 3) != B * 8 + (c & 7))
+            k = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, ((fa_ >> 3) & 3) - 1) &&
+                side_keep_rec(smf[wib], smk[wib], ia, ib) && side_keep_rec(smf[wib], smk[wib], ib, ia);
+        } else {
+          k = pair_keep_rec(smf[wib], smk[wib], ia, ib, v1t, v2t, ef, eb, -1);
         }
       }
-      m = (unsigned long long)__ballot_sync(0xffffffffu, k[0]) |
-          ((unsigned long long)__ballot_sync(0xffffffffu, k[1]) << 32);
+      const unsigned bal = __ballot_sync(0xffffffffu, k);
+      m |= (unsigned long long)((bal >> (16 * h)) & 0xffffu) << (16 * t);
     }
-    if (lane == 0) {
+    if (valid && hl == 0) {
       counts[en] = (uint32_t)__popcll(m);
       masks[en] = m;
     }

@@ -34,19 +34,22 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
                                              const SolveParams& prm, Sys1<TC>& S) {
   constexpr int DB = Sys1<TC>::DB;
   S.flags = 0;
-  // reading R1: incidence-plane normal l_c = (x2 - x0) x n(centroid)
+  // reading R1: incidence-plane normal l_c = (x2 - x0) x n(centroid); the tests below are the reading's
+  // comparisons squared and cross-multiplied (no square roots or divisions; equal up to rounding at ties)
   const d3 nc = (1.0 / 3.0) * (N_in[0] + N_in[1] + N_in[2]);
-  const d3 lc = cross(x2 - x0, nc);
-  const double ln = norm(lc);
-  if (!(ln > 1e-12 * norm(x2 - x0) * norm(nc))) S.flags |= SPOLY_FLAG_DEGENERATE;
+  const d3 w0 = x2 - x0;
+  const d3 lc = cross(w0, nc);
+  const double ln2 = dot(lc, lc);
+  if (!(ln2 > 1e-24 * dot(w0, w0) * dot(nc, nc))) S.flags |= SPOLY_FLAG_DEGENERATE;
   const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
   S.relabel = false;
   S.eta0 = S.eta1 = 1.0;
   if (!TC) {
-    // product form: t = n x e1 unless e2 is further out of the incidence plane (relabel p1 <-> p2)
-    if (ln > 0) {
-      const double s1 = fabs(dot(e1o, lc)) / (norm(e1o) * ln), s2 = fabs(dot(e2o, lc)) / (norm(e2o) * ln);
-      S.relabel = s1 < s2;
+    // product form: t = n x e1 unless e2 is further out of the incidence plane (relabel p1 <-> p2):
+    // |e1.lc| / |e1| < |e2.lc| / |e2|
+    if (ln2 > 0) {
+      const double d1 = dot(e1o, lc), d2 = dot(e2o, lc);
+      S.relabel = d1 * d1 * dot(e2o, e2o) < d2 * d2 * dot(e1o, e1o);
     }
   } else {
     // c7: eta_0 from the side of x_0 w.r.t. the triangle's geometric plane; refraction flips the medium
@@ -61,6 +64,7 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
   build_a(q, w, e1, e2, n0, m1, m2, S.A);
   if (WITH_B) {
     if (TC) {
+      const double ln = sqrt(ln2);
       const d3 l = ln > 0 ? (1.0 / ln) * lc : mk3(1, 0, 0);
       build_b_T(q, w, e1, e2, n0, m1, m2, l, S.eta0, S.eta1, S.B);
     } else {
