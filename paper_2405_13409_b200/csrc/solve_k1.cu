@@ -242,11 +242,19 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
       const unsigned long long p = mono ? b1 + ex1 : J.capacity - 1 - (b2 + ex2);
       J.pair[p] = (uint32_t)i;
       J.meta[p] = meta;
+      if (NR % 2 == 0) {  // R: 80 B per job, 16-byte aligned
+        double2* r2 = reinterpret_cast<double2*>(J.r + p * NR);
 #pragma unroll
-      for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
-      if (mono) {
+        for (int t = 0; t < NR / 2; ++t) r2[t] = make_double2(r[2 * t], r[2 * t + 1]);
+      } else {
 #pragma unroll
-        for (int t = 0; t < 6; ++t) J.A[p * 6 + t] = Aj[t];
+        for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
+      }
+      if (mono) {  // 48 B per job, 16-byte aligned: three vector stores
+        double2* a2 = reinterpret_cast<double2*>(J.A + p * 6);
+        a2[0] = make_double2(Aj[0], Aj[1]);
+        a2[1] = make_double2(Aj[2], Aj[3]);
+        a2[2] = make_double2(Aj[4], Aj[5]);
       }
     }
   }
@@ -445,8 +453,18 @@ __global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
       const uint64_t my = cur + __popc(idle & lt);
       if (my < cend) {
         jj = my;
+        if (NR % 2 == 0) {
+          const double2* r2 = reinterpret_cast<const double2*>(J.r + jj * NR);
 #pragma unroll
-        for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * NR + i);
+          for (int i = 0; i < NR / 2; ++i) {
+            const double2 v = __ldg(r2 + i);
+            c[2 * i] = v.x;
+            c[2 * i + 1] = v.y;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * NR + i);
+        }
         double f1 = c[NR - 1];
 #pragma unroll
         for (int i = NR - 2; i >= 0; --i) f1 += c[i];  // r(1)
@@ -574,8 +592,10 @@ __global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
     if (jj < nmono && !isnan(vs)) {
       cnt[C_CAND_JOBS]++;
       double A[9];
-      A[0] = J.A[jj * 6]; A[1] = J.A[jj * 6 + 1]; A[2] = J.A[jj * 6 + 2];
-      A[3] = J.A[jj * 6 + 3]; A[4] = J.A[jj * 6 + 4]; A[6] = J.A[jj * 6 + 5];
+      const double2* a2 = reinterpret_cast<const double2*>(J.A + jj * 6);
+      const double2 c01 = __ldg(a2), c23 = __ldg(a2 + 1), c45 = __ldg(a2 + 2);
+      A[0] = c01.x; A[1] = c01.y; A[2] = c23.x;
+      A[3] = c23.y; A[4] = c45.x; A[6] = c45.y;
       A[5] = A[7] = A[8] = 0.0;
       double al[3];
       bslices_at<2, 3>(A, vs, al);
