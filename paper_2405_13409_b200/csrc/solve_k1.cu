@@ -585,44 +585,61 @@ __global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
-  for (uint64_t base = gw * 32; base < nmono; base += nw * 32) {
-    const uint64_t jj = base + lane;
-    bool keep = false;
-    const double vs = jj < nmono ? J.root[jj] : 0.0;
-    if (jj < nmono && !isnan(vs)) {
-      cnt[C_CAND_JOBS]++;
-      double A[9];
-      const double2* a2 = reinterpret_cast<const double2*>(J.A + jj * 6);
-      const double2 c01 = __ldg(a2), c23 = __ldg(a2 + 1), c45 = __ldg(a2 + 2);
-      A[0] = c01.x; A[1] = c01.y; A[2] = c23.x;
-      A[3] = c23.y; A[4] = c45.x; A[6] = c45.y;
-      A[5] = A[7] = A[8] = 0.0;
-      double al[3];
-      bslices_at<2, 3>(A, vs, al);
-      const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
-      if (!(amax >= 1e-12)) {
-        keep = true;  // a(., v*) == 0: the b fallback runs in the path kernel
-      } else {
-        uint32_t fl = 0, nc = 0, nrej = 0;
-        double ua[2];
-        const int nu = quadratic_u_roots(al, ua, &fl);
-        for (int iu = 0; iu < nu; ++iu) {
-          ++nc;
-          if (precheck_reject(ua[iu], vs))
-            ++nrej;
-          else
-            keep = true;
-        }
-        if (fl) keep = true;
-        if (!keep) {
-          cnt[C_CANDIDATES] += nc;
-          cnt[C_REJ_DOMAIN] += nrej;
+  const unsigned lt = (1u << lane) - 1u;
+  // a warp owns chunks of kCandChunk x 32 consecutive jobs and appends a chunk's kept jobs with ONE atomic
+  // (one same-address atomic per 32 jobs would serialise in L2)
+  constexpr int kCandChunk = 16;
+  for (uint64_t cb = gw * (32 * kCandChunk); cb < nmono; cb += nw * (32 * kCandChunk)) {
+    unsigned bal[kCandChunk];
+#pragma unroll
+    for (int t = 0; t < kCandChunk; ++t) {
+      const uint64_t jj = cb + 32 * t + lane;
+      bool keep = false;
+      const double vs = jj < nmono ? J.root[jj] : 0.0;
+      if (jj < nmono && !isnan(vs)) {
+        cnt[C_CAND_JOBS]++;
+        double A[9];
+        const double2* a2 = reinterpret_cast<const double2*>(J.A + jj * 6);
+        const double2 c01 = __ldg(a2), c23 = __ldg(a2 + 1), c45 = __ldg(a2 + 2);
+        A[0] = c01.x; A[1] = c01.y; A[2] = c23.x;
+        A[3] = c23.y; A[4] = c45.x; A[6] = c45.y;
+        A[5] = A[7] = A[8] = 0.0;
+        double al[3];
+        bslices_at<2, 3>(A, vs, al);
+        const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+        if (!(amax >= 1e-12)) {
+          keep = true;  // a(., v*) == 0: the b fallback runs in the path kernel
+        } else {
+          uint32_t fl = 0, nc = 0, nrej = 0;
+          double ua[2];
+          const int nu = quadratic_u_roots(al, ua, &fl);
+          for (int iu = 0; iu < nu; ++iu) {
+            ++nc;
+            if (precheck_reject(ua[iu], vs))
+              ++nrej;
+            else
+              keep = true;
+          }
+          if (fl) keep = true;
+          if (!keep) {
+            cnt[C_CANDIDATES] += nc;
+            cnt[C_REJ_DOMAIN] += nrej;
+          }
         }
       }
+      bal[t] = __ballot_sync(0xffffffffu, keep);
     }
-    uint32_t ex;
-    const unsigned long long b = warp_alloc(J.lcount, keep ? 1u : 0u, &ex);
-    if (keep) J.meta[b + ex] = (uint32_t)jj;
+    uint32_t tot = 0;
+#pragma unroll
+    for (int t = 0; t < kCandChunk; ++t) tot += __popc(bal[t]);
+    unsigned long long b = 0;
+    if (lane == 0 && tot) b = atomicAdd(J.lcount, (unsigned long long)tot);
+    b = __shfl_sync(0xffffffffu, b, 0);
+#pragma unroll
+    for (int t = 0; t < kCandChunk; ++t) {
+      if ((bal[t] >> lane) & 1u) J.meta[b + __popc(bal[t] & lt)] = (uint32_t)(cb + 32 * t + lane);
+      b += __popc(bal[t]);
+    }
   }
   flush_counters(S, cnt);
 }
