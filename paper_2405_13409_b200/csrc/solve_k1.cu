@@ -172,11 +172,13 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  for (uint64_t base = gw * 32; base < npairs; base += nw * 32) {
-    const uint64_t i = base + lane;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // block-uniform loop (same pair mapping as a warp-strided loop): the monotone-job append is aggregated
+  // over the block's 4 warps, one atomic per 128 pairs (same-address atomics serialise in L2)
+  __shared__ uint32_t s_off[4];
+  __shared__ unsigned long long s_base;
+  for (uint64_t bb = (uint64_t)blockIdx.x * blockDim.x; bb < npairs; bb += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = bb + threadIdx.x;
     const bool active = i < npairs;
     bool job = false;
     uint32_t flags = 0, meta = 0;
@@ -235,8 +237,23 @@ __global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__
     // two-ended dense job list: monotone jobs (kfree == 1) from the front, deeper recursions from the back,
     // so that phase-2 warps see one job class
     const bool mono = job && (meta & 0xFF) == 1;
-    uint32_t ex1, ex2;
-    const unsigned long long b1 = warp_alloc(J.count, mono ? 1u : 0u, &ex1);
+    const unsigned mb = __ballot_sync(0xffffffffu, mono);
+    if (lane == 0) s_off[warp] = __popc(mb);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t acc = 0;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const uint32_t c = s_off[w];
+        s_off[w] = acc;
+        acc += c;
+      }
+      s_base = acc ? atomicAdd(J.count, (unsigned long long)acc) : 0ull;
+    }
+    __syncthreads();
+    const uint32_t ex1 = s_off[warp] + __popc(mb & ((1u << lane) - 1u));
+    const unsigned long long b1 = s_base;
+    uint32_t ex2;
     const unsigned long long b2 = warp_alloc(J.count + 1, (job && !mono) ? 1u : 0u, &ex2);
     if (job && (mono ? b1 + ex1 : b2 + ex2) < J.capacity) {
       const unsigned long long p = mono ? b1 + ex1 : J.capacity - 1 - (b2 + ex2);
