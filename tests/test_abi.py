@@ -57,3 +57,21 @@ def test_no_oracle_import_in_product():
         if f.endswith((".py", ".cu", ".cuh", ".h")):
             txt = open(f).read()
             assert "import oracle" not in txt and "oracle/" not in txt.replace("oracle/ ", ""), f
+
+
+def test_ctypes_structs_match_the_header(tmp_path):
+    """The binding's ctypes mirrors of spoly_config / spoly_report / spoly_result have the C layout."""
+    import ctypes
+    from paper_2405_13409_b200 import spoly
+    src = tmp_path / "sz.c"
+    src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "spoly.h"\nint main(void) {\n'
+                   'printf("%zu %zu %zu %zu %zu\\n", sizeof(spoly_config), sizeof(spoly_report), sizeof(spoly_result),'
+                   ' offsetof(spoly_report, n_cull_tests), offsetof(spoly_result, report));\nreturn 0;\n}\n')
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    c_cfg, c_rep, c_res, c_off, c_roff = map(int, subprocess.check_output([str(exe)]).decode().split())
+    assert ctypes.sizeof(spoly.spoly_config) == c_cfg
+    assert ctypes.sizeof(spoly.spoly_report) == c_rep
+    assert ctypes.sizeof(spoly.spoly_result) == c_res
+    assert spoly.spoly_report.n_cull_tests.offset == c_off
+    assert spoly.spoly_result.report.offset == c_roff
