@@ -101,6 +101,7 @@ class ClockSampler:
         self._stop = False
         self._th = None
         self.h = None
+        self.mx = None
 
     def _handle(self):
         import pynvml
@@ -113,22 +114,29 @@ class ClockSampler:
         except Exception:
             return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.dev)
 
-    def _run(self):
+    def sample_now(self):
+        """One sample from the calling thread (the timed loop calls it after every step's launches, so a
+        short timed region has samples even when the polling thread is not scheduled)."""
+        if self.h is None:
+            return
         nv, h = self.h
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+            self.rows.append((time.perf_counter(), sm, self.mx, rs))
+        except Exception:
+            pass
+
+    def _run(self):
         while not self._stop:
-            try:
-                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.rows.append((time.perf_counter(), sm, mx, rs))
-            except Exception:
-                pass
+            self.sample_now()
             time.sleep(0.002)
 
     def __enter__(self):
         import threading
         try:
             self.h = self._handle()
+            self.mx = self.h[0].nvmlDeviceGetMaxClockInfo(self.h[1], self.h[0].NVML_CLOCK_SM)
             self._th = threading.Thread(target=self._run, daemon=True)
             self._th.start()
         except Exception:
@@ -155,7 +163,7 @@ class ClockSampler:
             return None
         reasons = sorted({nm for r in rows for nm, bit in self.REASONS if r[3] & bit})
         return {"sm_mhz": statistics.median(r[1] for r in rows), "sm_max_mhz": max(r[2] for r in rows),
-                "reasons": reasons, "samples": len(rows), "source": "nvml, 2 ms period, timed region only"}
+                "reasons": reasons, "samples": len(rows), "source": "nvml: 2 ms polling thread + one sample per timed step, timed region only"}
 
 
 def oracle_baseline(w, nsample, nthreads=0):
@@ -280,6 +288,7 @@ def main():
             e0.record(stream)
             r = ctx.solve(chain, ep, inten)
             e1.record(stream)
+            clk.sample_now()
             torch.cuda.synchronize(dev)
             step_ms.append(e0.elapsed_time(e1))
             solve_ms.append(r.report["ms_solve"])
