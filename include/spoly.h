@@ -65,7 +65,9 @@ typedef struct {
   int cull;              /* 1: run the cull pre-pass when no tuple list is given             */
   int deterministic;     /* 1: sort solutions by (query, tuple, root) -> bit-identical output */
   float cull_margin;     /* angular slack (rad) of the FP32 cull; 1e-4                       */
-  uint64_t max_solutions;/* initial solution-buffer capacity (regrown once on overflow)      */
+  uint64_t max_solutions;/* minimum initial solution-buffer capacity; the library also sizes the
+                            solution / flag sinks from the work list (k=1: pairs/2, pairs/64;
+                            k=2: pairs/32, pairs/8) and regrows them once on overflow       */
   uint64_t max_pairs;    /* k=2 cull: max node-pair frontier entries per query chunk; 2^27.
                             Queries are culled in chunks that fit (order-preserving, so the
                             work list is the unchunked one); SPOLY_ERR_CAPACITY if one query

@@ -615,8 +615,12 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   prm.polish_iters = ctx->cfg.polish_iters;
   prm.eta_front = ctx->M.eta_front;
   prm.eta_back = ctx->M.eta_back;
-  spoly_status s = ensure_sink(ctx, std::max<uint64_t>(ctx->d_key.cap, ctx->cfg.max_solutions),
-                               std::max<uint64_t>(ctx->d_fkey.cap, 1ull << 16), k);
+  // initial sink capacities from the work list (an overflow re-runs the whole solve once): solutions
+  // ~0.3 per pair on C2 (k=1), ~0.2% per refined pair for k=2; flagged tuples ~1e-5 (k=1) / ~1.3% (k=2)
+  const uint64_t sol_guess = k == 1 ? npairs / 2 : npairs / 32;
+  const uint64_t flag_guess = k == 1 ? npairs / 64 : npairs / 8;
+  spoly_status s = ensure_sink(ctx, std::max({ctx->d_key.cap, (uint64_t)ctx->cfg.max_solutions, sol_guess}),
+                               std::max({ctx->d_fkey.cap, (uint64_t)(1ull << 16), flag_guess}), k);
   if (s != SPOLY_OK) return s;
   CK(ctx->d_count.ensure(6));
   CK(ctx->d_jpair.ensure(k == 1 ? npairs : 1));
