@@ -50,32 +50,37 @@ __device__ __forceinline__ void bmul_acc(const double* A, const double* B, doubl
 }
 
 template <int D, int S>
-__device__ __forceinline__ double bmaxabs(const double* G) {
-  double m = 0.0;
-#pragma unroll
-  for (int i = 0; i <= D; ++i)
-#pragma unroll
-    for (int j = 0; i + j <= D; ++j) m = fmax(m, fabs(G[i * S + j]));
-  return m;
-}
-template <int D, int S>
 __device__ __forceinline__ void bscale(double* G, double s) {
 #pragma unroll
   for (int i = 0; i <= D; ++i)
 #pragma unroll
     for (int j = 0; i + j <= D; ++j) G[i * S + j] *= s;
 }
-// numerical u-degree: max{i : max_j |c_ij| 1.1^i > tau}
+// per-u-row max |c_ij| in one pass (rm[i]) and the overall max (return value).  Scaling by s > 0 is monotone
+// under rounding, so max_j fl(|c_ij| s) = fl(rm[i] s): the numerical u-degree of the scaled grid can be taken
+// from the unscaled row maxima (bit-identical to taking the maxima after scaling; one max pass instead of two)
 template <int D, int S>
-__device__ __forceinline__ int bnum_udeg(const double* G, double tau) {
+__device__ __forceinline__ double browmax(const double* G, double* rm) {
+  double m = 0.0;
+#pragma unroll
+  for (int i = 0; i <= D; ++i) {
+    double r = 0.0;
+#pragma unroll
+    for (int j = 0; i + j <= D; ++j) r = fmax(r, fabs(G[i * S + j]));
+    rm[i] = r;
+    m = fmax(m, r);
+  }
+  return m;
+}
+// numerical u-degree of the grid scaled by s: max{i : max_j |s c_ij| 1.1^i > tau}, from the
+// unscaled row maxima (see browmax)
+template <int D>
+__device__ __forceinline__ int bnum_udeg_rows(const double* rm, double s, double tau) {
   int d = 0;
   double f = 1.0;
 #pragma unroll
   for (int i = 0; i <= D; ++i) {
-    double m = 0.0;
-#pragma unroll
-    for (int j = 0; i + j <= D; ++j) m = fmax(m, fabs(G[i * S + j]));
-    if (m * f > tau) d = i;
+    if ((rm[i] * s) * f > tau) d = i;
     f *= 1.1;
   }
   return d;

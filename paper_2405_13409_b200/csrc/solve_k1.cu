@@ -71,17 +71,19 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
       build_b_R(q, w, e1, e2, n0, m1, m2, S.B);
     }
   }
-  const double ma = bmaxabs<2, 3>(S.A), mb = WITH_B ? bmaxabs<DB, DB + 1>(S.B) : 1.0;
+  double rma[3], rmb[DB + 1];
+  const double ma = browmax<2, 3>(S.A, rma), mb = WITH_B ? browmax<DB, DB + 1>(S.B, rmb) : 1.0;
   if (!(ma > 0) || !(mb > 0)) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
   }
-  bscale<2, 3>(S.A, 1.0 / ma);
-  if (WITH_B) bscale<DB, DB + 1>(S.B, 1.0 / mb);
-  S.da = bnum_udeg<2, 3>(S.A, prm.tau_trunc);
+  const double sa = 1.0 / ma, sb = 1.0 / mb;
+  bscale<2, 3>(S.A, sa);
+  if (WITH_B) bscale<DB, DB + 1>(S.B, sb);
+  S.da = bnum_udeg_rows<2>(rma, sa, prm.tau_trunc);
   btrunc_u<2, 3>(S.A, S.da);
   if (!WITH_B) return true;
-  S.db = bnum_udeg<DB, DB + 1>(S.B, prm.tau_trunc);
+  S.db = bnum_udeg_rows<DB>(rmb, sb, prm.tau_trunc);
   btrunc_u<DB, DB + 1>(S.B, S.db);
   S.n = max(S.da, S.db);
   if (S.n == 0) {
@@ -163,8 +165,14 @@ __device__ __forceinline__ void load_pair(const uint32_t* __restrict__ pq, const
 }
 
 // ---------------------------------------------------------------------------------------------
+#ifndef SPOLY_P1_MINB
+#define SPOLY_P1_MINB 4
+#endif
+#ifndef SPOLY_PATH_MINB
+#define SPOLY_PATH_MINB 1
+#endif
 template <bool TC>
-__global__ void __launch_bounds__(128, 4) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+__global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                     uint64_t npairs, const TriRec* __restrict__ tris,
                                                     const double* __restrict__ ep, SolveParams prm, SolSink S,
                                                     JobSink J) {
@@ -664,7 +672,7 @@ __global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
 // ---- phase 2b: back-substitution, refinement, validation, contribution, emission; thread per job of the
 // pre-pass list, then the deep jobs (jobs without roots exit at once)
 template <bool TC>
-__global__ void __launch_bounds__(128) k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+__global__ void __launch_bounds__(128, SPOLY_PATH_MINB) k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                const TriRec* __restrict__ tris, const double* __restrict__ ep,
                                                const double* __restrict__ inten, SolveParams prm, SolSink S,
                                                JobSink J) {

@@ -59,15 +59,24 @@ __device__ __forceinline__ int bernstein_root_free_level(const double* r) {
     for (int i = 0; i <= k; ++i) acc = fma(N == 10 ? c_bern9[k][i] : c_bern12[k][i], r[i], acc);
     b[k] = acc;
   }
+  // strict signs from the high words (integer min/max on the ALU pipe instead of FP64 compares): hi > 0 is
+  // a positive value, hi in (INT_MIN, 0) a negative one; +-0 and denormals below 2^-1022 read as "no strict
+  // sign" (conservative: a later level or the full recursion).  Non-finite r never takes a shortcut.
+  int fin = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i) fin = max(fin, __double2hiint(r[i]) & 0x7fffffff);
   int level = N;
+  if (fin >= 0x7ff00000) return level;
 #pragma unroll
   for (int k = 0; k < N - 1; ++k) {
-    bool pos = true, neg = true;
+    int mn = __double2hiint(b[0]), mx = mn;
 #pragma unroll
-    for (int i = 0; i < N - k; ++i) {
-      pos = pos && (b[i] > 0.0);
-      neg = neg && (b[i] < 0.0);
+    for (int i = 1; i < N - k; ++i) {
+      const int h = __double2hiint(b[i]);
+      mn = min(mn, h);
+      mx = max(mx, h);
     }
+    const bool pos = mn > 0x000fffff, neg = mx < 0 && mn > (int)0x800fffff;
     if ((pos || neg) && level == N) level = k;
 #pragma unroll
     for (int i = 0; i < N - 1 - k; ++i) b[i] = b[i + 1] - b[i];
