@@ -185,12 +185,15 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
   // over the block's 4 warps, one atomic per 128 pairs (same-address atomics serialise in L2)
   __shared__ uint32_t s_off[4];
   __shared__ unsigned long long s_base;
+  // a's 6 coefficients wait in shared memory (not registers) through the elimination and the Bernstein
+  // test, until the job slot is known; [coefficient][thread], conflict-free
+  __shared__ double s_aj[6][128];
   for (uint64_t bb = (uint64_t)blockIdx.x * blockDim.x; bb < npairs; bb += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = bb + threadIdx.x;
     const bool active = i < npairs;
     bool job = false;
     uint32_t flags = 0, meta = 0;
-    double r[NR], Aj[6];
+    double r[NR];
     if (active) {
       d3 P[3], N[3], x0, x2;
       uint32_t q;
@@ -210,8 +213,8 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
       } else if (ok) {
         cnt[C_EVAL_TERMS] += 8;
         cnt[C_ELIMS]++;
-        Aj[0] = Sys.A[0]; Aj[1] = Sys.A[1]; Aj[2] = Sys.A[2];
-        Aj[3] = Sys.A[3]; Aj[4] = Sys.A[4]; Aj[5] = Sys.A[6];
+        s_aj[0][threadIdx.x] = Sys.A[0]; s_aj[1][threadIdx.x] = Sys.A[1]; s_aj[2][threadIdx.x] = Sys.A[2];
+        s_aj[3][threadIdx.x] = Sys.A[3]; s_aj[4][threadIdx.x] = Sys.A[4]; s_aj[5][threadIdx.x] = Sys.A[6];
         eliminate<TC>(Sys, r);
         double mr = 0.0;
 #pragma unroll
@@ -277,9 +280,9 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
       }
       if (mono) {  // 48 B per job, 16-byte aligned: three vector stores
         double2* a2 = reinterpret_cast<double2*>(J.A + p * 6);
-        a2[0] = make_double2(Aj[0], Aj[1]);
-        a2[1] = make_double2(Aj[2], Aj[3]);
-        a2[2] = make_double2(Aj[4], Aj[5]);
+        a2[0] = make_double2(s_aj[0][threadIdx.x], s_aj[1][threadIdx.x]);
+        a2[1] = make_double2(s_aj[2][threadIdx.x], s_aj[3][threadIdx.x]);
+        a2[2] = make_double2(s_aj[4][threadIdx.x], s_aj[5][threadIdx.x]);
       }
     }
   }
