@@ -168,8 +168,10 @@ __device__ __forceinline__ void load_pair(const uint32_t* __restrict__ pq, const
 #ifndef SPOLY_P1_MINB
 #define SPOLY_P1_MINB 4
 #endif
-#ifndef SPOLY_PATH_MINB
-#define SPOLY_PATH_MINB 1
+#ifdef SPOLY_PATH_MINB
+#define SPOLY_PATH_BOUNDS __launch_bounds__(128, SPOLY_PATH_MINB)
+#else
+#define SPOLY_PATH_BOUNDS __launch_bounds__(128)
 #endif
 template <bool TC>
 __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
@@ -675,7 +677,7 @@ __global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
 // ---- phase 2b: back-substitution, refinement, validation, contribution, emission; thread per job of the
 // pre-pass list, then the deep jobs (jobs without roots exit at once)
 template <bool TC>
-__global__ void __launch_bounds__(128, SPOLY_PATH_MINB) k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+__global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                const TriRec* __restrict__ tris, const double* __restrict__ ep,
                                                const double* __restrict__ inten, SolveParams prm, SolSink S,
                                                JobSink J) {
