@@ -2,6 +2,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <cub/cub.cuh>
 #include <string>
@@ -92,6 +93,8 @@ struct spoly_ctx {
   int last_k = 1;
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
+  DBuf<unsigned long long> d_pmask;  // counting order: one slot bit per (pair, slot)
+  DBuf<uint32_t> d_pcnt;             // counting order: per-pair counts, then their exclusive scan
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
   DBuf<double> d_bary, d_contrib, d_jr, d_jroot, d_jA;
   DBuf<float> d_resid;
@@ -192,6 +195,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
   ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release(); ctx->d_jA.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
+  ctx->d_pmask.release(); ctx->d_pcnt.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
   ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
   ctx->o_per_query.release(); ctx->o_resid.release(); ctx->d_temp.release(); ctx->d_k32.release(); ctx->d_ep.release(); ctx->d_int.release();
@@ -741,7 +745,29 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_gather_flagged(ctx->d_upair.p, ctx->d_uflags.p, nf, k, ctx->d_pq.p, ctx->d_pt.p, ctx->M.orig_id, o, st);
     ctx->launches++;
   }
-  if (n) {
+  // counting order (same order as the key sort, without its radix passes) when the per-pair arrays (16 B
+  // per pair, memset + scan) cost less than sorting the solutions: measured on B200, C3 (1.3 M pairs, 0.26 M
+  // solutions) 0.46 -> 0.41 ms, C2 (24.5 M pairs, 7.7 M solutions) 0.71 -> 0.77 ms, i.e. counting pays
+  // while npairs <~ 2 n + 4 M.  SPOLY_SORT_ORDER=1 / =0 forces the sort / the counting order (A/B, tests).
+  const char* force = getenv("SPOLY_SORT_ORDER");
+  const bool counting_fits = n && n < (1ull << 32) && npairs <= (1ull << 30);
+  const bool counting = counting_fits && (force && force[0] == '1'   ? false
+                                          : force && force[0] == '0' ? true
+                                                                     : npairs <= 2 * n + (1ull << 22));
+  if (counting) {
+    CK(ctx->d_pmask.ensure(npairs));
+    CK(ctx->d_pcnt.ensure(2 * npairs));
+    CK(cudaMemsetAsync(ctx->d_pmask.p, 0, npairs * sizeof(unsigned long long), st));
+    launch_slot_masks(ctx->d_key.p, n, ctx->d_pmask.p, npairs, ctx->d_pcnt.p, st);
+    size_t tb = 0;
+    CK(cub::DeviceScan::ExclusiveSum(nullptr, tb, ctx->d_pcnt.p, ctx->d_pcnt.p + npairs, (int64_t)npairs, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceScan::ExclusiveSum(ctx->d_temp.p, tb, ctx->d_pcnt.p, ctx->d_pcnt.p + npairs, (int64_t)npairs, st));
+    launch_scatter_solutions(ctx->d_key.p, n, ctx->d_pmask.p, ctx->d_pcnt.p + npairs, k, in, ctx->d_pq.p,
+                             ctx->d_pt.p, ctx->M.orig_id, o, ctx->d_key2.p, st);
+    launch_solution_flags(ctx->d_key2.p, nullptr, n, ctx->d_upair.p, ctx->d_uflags.p, nf, o.flags, st);
+    ctx->launches += 4;
+  } else if (n) {
     launch_iota(ctx->d_perm_in.p, n, st);
     ctx->launches++;
     size_t tb = 0;

@@ -74,6 +74,12 @@ void launch_iota(uint32_t* v, uint64_t n, cudaStream_t st);
 void launch_gather_solutions(const uint32_t* perm, const unsigned long long* skey, const uint32_t* skey32, uint64_t n,
                              int k, const SolSink& in, const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id,
                              const OutArrays& out, cudaStream_t st);
+void launch_slot_masks(const unsigned long long* key, uint64_t n, unsigned long long* mask, uint64_t npairs,
+                       uint32_t* cnt, cudaStream_t st);
+void launch_scatter_solutions(const unsigned long long* key, uint64_t n, const unsigned long long* mask,
+                              const uint32_t* off, int k, const SolSink& in, const uint32_t* pq, const uint32_t* pt,
+                              const uint32_t* orig_id, const OutArrays& out, unsigned long long* skey,
+                              cudaStream_t st);
 void launch_key32(const unsigned long long* key, uint64_t n, uint32_t* out, cudaStream_t st);
 void launch_gather_flagged(const unsigned long long* upair, const uint32_t* uflags, uint64_t n, int k,
                            const uint32_t* pq, const uint32_t* pt, const uint32_t* orig_id, const OutArrays& out,

@@ -47,6 +47,48 @@ void launch_gather_solutions(const uint32_t* perm, const unsigned long long* ske
     k_gather_solutions<unsigned long long><<<2048, 256, 0, st>>>(perm, skey, n, k, in, pq, pt, orig_id, out);
 }
 
+// Counting order (replaces the key sort when the per-pair arrays fit): keys are unique and slot < 64, so
+// the rank of a solution in key order is (solutions of lower pairs) + (lower slots of its own pair).
+// k_slot_masks sets one bit per (pair, slot); the pair counts (popcounts) are exclusive-scanned; the
+// scatter writes every record straight to its rank -- the same order as the sort, no sort passes.
+__global__ void k_slot_masks(const unsigned long long* __restrict__ key, uint64_t n, unsigned long long* mask) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long kk = key[i];
+    atomicOr(mask + (kk >> 6), 1ull << (kk & 63));
+  }
+}
+__global__ void k_mask_counts(const unsigned long long* __restrict__ mask, uint64_t np, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < np; i += (uint64_t)gridDim.x * blockDim.x)
+    cnt[i] = (uint32_t)__popcll(mask[i]);
+}
+__global__ void k_scatter_solutions(const unsigned long long* __restrict__ key, uint64_t n,
+                                    const unsigned long long* __restrict__ mask, const uint32_t* __restrict__ off,
+                                    int k, SolSink in, const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                    const uint32_t* __restrict__ orig, OutArrays out, unsigned long long* skey) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long kk = key[i];
+    const uint64_t pair = kk >> 6;
+    const uint64_t p = (uint64_t)off[pair] + __popcll(mask[pair] & ((1ull << (kk & 63)) - 1ull));
+    skey[p] = kk;
+    out.query[p] = pq[pair];
+    for (int j = 0; j < k; ++j) out.tuple[(uint64_t)k * p + j] = orig[pt[(uint64_t)k * pair + j]];
+    for (int j = 0; j < 2 * k; ++j) out.bary[(uint64_t)2 * k * p + j] = in.bary[(uint64_t)2 * k * i + j];
+    out.contrib[p] = in.contrib[i];
+    out.resid[p] = in.resid[i];
+  }
+}
+void launch_slot_masks(const unsigned long long* key, uint64_t n, unsigned long long* mask, uint64_t npairs,
+                       uint32_t* cnt, cudaStream_t st) {
+  if (n) k_slot_masks<<<1024, 256, 0, st>>>(key, n, mask);
+  if (npairs) k_mask_counts<<<2048, 256, 0, st>>>(mask, npairs, cnt);
+}
+void launch_scatter_solutions(const unsigned long long* key, uint64_t n, const unsigned long long* mask,
+                              const uint32_t* off, int k, const SolSink& in, const uint32_t* pq, const uint32_t* pt,
+                              const uint32_t* orig_id, const OutArrays& out, unsigned long long* skey,
+                              cudaStream_t st) {
+  if (n) k_scatter_solutions<<<2048, 256, 0, st>>>(key, n, mask, off, k, in, pq, pt, orig_id, out, skey);
+}
+
 // keys below 2^32 (pair index << 6 | slot): sorted as 32-bit keys (two thirds of the radix-sort traffic)
 __global__ void k_key32(const unsigned long long* __restrict__ key, uint64_t n, uint32_t* __restrict__ out) {
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)

@@ -294,6 +294,22 @@ def test_determinism_bit_identical(sp, torch_cuda):
         assert np.array_equal(a[k], b[k]), k
 
 
+@pytest.mark.parametrize("chain,make", [("R", lambda: W.glints_c2(res=48)), ("T", lambda: W.pool_c3(res=64)),
+                                        ("TT", lambda: W.shell_c5(res=8))])
+def test_counting_order_equals_key_sort(sp, torch_cuda, monkeypatch, chain, make):
+    """The counting order (slot masks + scanned pair counts + scatter) writes the solutions in exactly the
+    order of the (pair << 6 | slot) key sort it replaces: every output array is bit-identical."""
+    w = make()
+    monkeypatch.setenv("SPOLY_SORT_ORDER", "0")
+    a = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints, intensity=w.intensity)
+    monkeypatch.setenv("SPOLY_SORT_ORDER", "1")
+    b = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints, intensity=w.intensity)
+    assert a["report"]["n_admissible"] > 0
+    for k in ("query", "tuple", "bary", "contribution", "residual", "flags", "per_query", "flagged_query",
+              "flagged_flags"):
+        assert np.array_equal(a[k], b[k]), k
+
+
 @pytest.mark.parametrize("chain,make", [("RR", lambda: W.mirrors_rr(res=8, quads=16)),
                                         ("TT", lambda: W.shell_c5(res=8))])
 def test_two_bounce_query_chunking_identical(sp, torch_cuda, chain, make):
