@@ -138,7 +138,9 @@ typedef struct {
   uint64_t n_flagged;   /* tuples carrying a flag                                           */
   int k;                /* bounces                                                          */
   /* device pointers owned by the ctx, sorted by (query, tuple position, root) when
-   * deterministic=1 */
+   * deterministic=1.  The order comes from a radix sort of the (pair << 6 | slot) keys or, when the
+   * work list is small relative to the solution count, from an equivalent counting order (identical
+   * output); the environment variable SPOLY_SORT_ORDER=1 / =0 forces the sort / the counting order. */
   const uint32_t* query;        /* [n_solutions]                                            */
   const uint32_t* tuple;        /* [n_solutions * k] original triangle ids                  */
   const double* bary;           /* [n_solutions * 2k] (u_1, v_1[, u_2, v_2]), Eq. 1          */
