@@ -739,8 +739,12 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
   if (npairs == 0) return;
   const int threads = 128;
   const uint64_t cap = (uint64_t)nsm * 16;
+#ifndef SPOLY_P1_GRID
+#define SPOLY_P1_GRID 64  // blocks per SM (grid-stride); A/B on C2: 4 -> 2.22, 16 -> 2.15, 64 -> 2.07, 256 -> 2.20 ms
+#endif
+  const uint64_t cap1 = (uint64_t)nsm * SPOLY_P1_GRID;
   const uint64_t want1 = (npairs + threads - 1) / threads;
-  const int g1 = (int)(want1 < cap ? want1 : cap);
+  const int g1 = (int)(want1 < cap1 ? want1 : cap1);
   if (phase == 1) {
     if (refract)
       k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
