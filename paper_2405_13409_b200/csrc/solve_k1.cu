@@ -759,11 +759,14 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
     }
   } else {  // path
+#ifndef SPOLY_PATH_GRID
+#define SPOLY_PATH_GRID 4  // blocks per SM (2 resident at 243 registers); A/B: 16 -> 4 took k1_path<R> 2.04 -> 2.03 ms, <T> 0.167 -> 0.155 ms
+#endif
     k1_cand<<<nsm * 8, 256, 0, st>>>(S, J);
     if (refract)
-      k1_path<true><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
+      k1_path<true><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
     else
-      k1_path<false><<<(int)cap, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
+      k1_path<false><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
   }
 }
 
