@@ -751,18 +751,24 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
     else
       k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
   } else if (phase == 2) {  // roots
+#ifndef SPOLY_ROOTS_GRID
+#define SPOLY_ROOTS_GRID 32  // blocks per SM (two waves, smaller warp chunks); A/B: 8 -> 0.61, 16 -> 0.60, 32 -> 0.575 ms
+#endif
     if (refract) {
-      k1_roots<true><<<(int)cap, threads, 0, st>>>(S, J);
+      k1_roots<true><<<nsm * SPOLY_ROOTS_GRID, threads, 0, st>>>(S, J);
       k1_roots_deep<true><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
     } else {
-      k1_roots<false><<<(int)cap, threads, 0, st>>>(S, J);
+      k1_roots<false><<<nsm * SPOLY_ROOTS_GRID, threads, 0, st>>>(S, J);
       k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
     }
   } else {  // path
 #ifndef SPOLY_PATH_GRID
 #define SPOLY_PATH_GRID 4  // blocks per SM (2 resident at 243 registers); A/B: 16 -> 4 took k1_path<R> 2.04 -> 2.03 ms, <T> 0.167 -> 0.155 ms
 #endif
-    k1_cand<<<nsm * 8, 256, 0, st>>>(S, J);
+#ifndef SPOLY_CAND_GRID
+#define SPOLY_CAND_GRID 8
+#endif
+    k1_cand<<<nsm * SPOLY_CAND_GRID, 256, 0, st>>>(S, J);
     if (refract)
       k1_path<true><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
     else
