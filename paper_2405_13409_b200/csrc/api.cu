@@ -94,6 +94,7 @@ struct spoly_ctx {
   // raw sink + job list
   DBuf<unsigned long long> d_count, d_counters, d_key, d_key2, d_fkey, d_fkey2, d_upair, d_nruns;
   DBuf<unsigned long long> d_pmask;  // counting order: one slot bit per (pair, slot)
+  DBuf<unsigned long long> d_qrange;  // per-query [begin, end) in the sorted solution list
   DBuf<uint32_t> d_pcnt;             // counting order: per-pair counts, then their exclusive scan
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
   DBuf<double> d_bary, d_contrib, d_jr, d_jroot, d_jA;
@@ -195,7 +196,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
   ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release(); ctx->d_jA.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
-  ctx->d_pmask.release(); ctx->d_pcnt.release();
+  ctx->d_pmask.release(); ctx->d_pcnt.release(); ctx->d_qrange.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
   ctx->o_ftuple.release(); ctx->o_fflags.release(); ctx->o_bary.release(); ctx->o_contrib.release();
   ctx->o_per_query.release(); ctx->o_resid.release(); ctx->d_temp.release(); ctx->d_k32.release(); ctx->d_ep.release(); ctx->d_int.release();
@@ -794,8 +795,9 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     launch_solution_flags(ctx->d_key2.p, k32, n, ctx->d_upair.p, ctx->d_uflags.p, nf, o.flags, st);
     ctx->launches += 2;
   }
-  launch_per_query_sorted(ctx->o_query.p, ctx->o_contrib.p, n, nq, ctx->o_per_query.p, st);
-  ctx->launches++;
+  CK(ctx->d_qrange.ensure(2ull * nq));
+  launch_per_query_sorted(ctx->o_query.p, ctx->o_contrib.p, n, nq, ctx->o_per_query.p, ctx->d_qrange.p, st);
+  ctx->launches += n ? 2 : 1;
   CK(cudaGetLastError());
   CK(cudaEventRecord(ctx->ev[3], st));
   unsigned long long counters[C_NUM];

@@ -88,7 +88,7 @@ void launch_solution_flags(const unsigned long long* skey, const uint32_t* skey3
                            const unsigned long long* upair, const uint32_t* uflags, uint64_t nf, uint32_t* flags,
                            cudaStream_t st);
 void launch_per_query_sorted(const uint32_t* query, const double* contrib, uint64_t n, uint32_t nq, double* per_query,
-                             cudaStream_t st);
+                             unsigned long long* range, cudaStream_t st);
 
 // fma_peak.cu
 void launch_fma_peak(int fp64, int iters, double* sink, int nsm, cudaStream_t st, int* blocks_out, int* threads_out,

@@ -139,26 +139,24 @@ void launch_solution_flags(const unsigned long long* skey, const uint32_t* skey3
     k_solution_flags<unsigned long long><<<2048, 256, 0, st>>>(skey, n, upair, uflags, nf, flags);
 }
 
-// one warp per query: binary-search its range in the query-sorted solution list, then a fixed-order
-// sum (lane-strided partial sums + fixed xor tree) -> bit-reproducible per-query totals.
-__global__ void k_per_query_sorted(const uint32_t* __restrict__ query, const double* __restrict__ contrib, uint64_t n,
+// query ranges of the query-sorted solution list in one pass: a run of equal query ids starts / ends where
+// the neighbour differs (queries without solutions keep the zeroed empty range [0, 0))
+__global__ void k_query_ranges(const uint32_t* __restrict__ query, uint64_t n, unsigned long long* range) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t q = query[i];
+    if (i == 0 || query[i - 1] != q) range[2ull * q] = i;
+    if (i + 1 == n || query[i + 1] != q) range[2ull * q + 1] = i + 1;
+  }
+}
+// one warp per query over its range: fixed-order sum (lane-strided partial sums + fixed xor tree) ->
+// bit-reproducible per-query totals.
+__global__ void k_per_query_sorted(const unsigned long long* __restrict__ range, const double* __restrict__ contrib,
                                    uint32_t nq, double* per_query) {
   const int lane = threadIdx.x & 31;
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   for (uint64_t q = gw; q < nq; q += nw) {
-    uint64_t lo = 0, hi = n;
-    while (lo < hi) {
-      uint64_t m = (lo + hi) >> 1;
-      if (query[m] < q) lo = m + 1; else hi = m;
-    }
-    const uint64_t b = lo;
-    hi = n;
-    while (lo < hi) {
-      uint64_t m = (lo + hi) >> 1;
-      if (query[m] <= q) lo = m + 1; else hi = m;
-    }
-    const uint64_t e = lo;
+    const uint64_t b = range[2 * q], e = range[2 * q + 1];
     double s = 0.0;
     for (uint64_t i = b + lane; i < e; i += 32) s += contrib[i];
 #pragma unroll
@@ -167,11 +165,13 @@ __global__ void k_per_query_sorted(const uint32_t* __restrict__ query, const dou
   }
 }
 void launch_per_query_sorted(const uint32_t* query, const double* contrib, uint64_t n, uint32_t nq, double* per_query,
-                             cudaStream_t st) {
+                             unsigned long long* range, cudaStream_t st) {
   if (!nq) return;
+  cudaMemsetAsync(range, 0, 2ull * nq * sizeof(unsigned long long), st);
+  if (n) k_query_ranges<<<1024, 256, 0, st>>>(query, n, range);
   uint64_t blocks = ((uint64_t)nq * 32 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
-  k_per_query_sorted<<<(int)blocks, 256, 0, st>>>(query, contrib, n, nq, per_query);
+  k_per_query_sorted<<<(int)blocks, 256, 0, st>>>(range, contrib, nq, per_query);
 }
 
 }  // namespace spoly
