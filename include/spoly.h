@@ -49,6 +49,9 @@ typedef enum {
 #define SPOLY_FLAG_BOUNDARY 2u     /* a valid chain within eps_flag of a triangle edge           */
 #define SPOLY_FLAG_RESIDUAL 4u     /* accepted chain with residual in [1e-7, theta_final)        */
 #define SPOLY_FLAG_DEGENERATE 8u   /* a or b identically zero, u-free system, degenerate basis   */
+#define SPOLY_FLAG_TRUNCATED 16u   /* a fixed per-tuple capacity of the kernels was exceeded (more v-roots,
+                                      u-roots or admissible chains than the kernel keeps): the tuple's
+                                      solution set may be incomplete; counted in report.n_truncated  */
 
 typedef struct spoly_ctx spoly_ctx;
 
@@ -56,14 +59,15 @@ typedef struct {
   int pieces;            /* k>=2 determinant scan pieces; 100                 */
   int scan_bisect_iters; /* k>=2 bisections per sign-changing piece; 10       */
   double bisect_tol;     /* k=1 root bracket threshold; 1e-9                  */
-  int polish_iters;      /* Newton steps on the exact shooting residual (k=2); 3             */
+  int polish_iters;      /* Newton steps on the exact shooting residual (k=2); 5 (reading R23) */
   double theta_admit;    /* raw-root residual gate before polish (k=2); 1e-3                 */
   double theta_final;    /* final Eq. 3 residual gate; 1e-6 (north_star)                     */
   double eps_domain;     /* barycentric slack of the inside test; 1e-9                       */
   double eps_flag;       /* near-tangent / boundary flag distance; 1e-6                      */
   double tau_trunc;      /* numerical u-degree truncation threshold; 1e-12       */
   int cull;              /* 1: run the cull pre-pass when no tuple list is given             */
-  int deterministic;     /* 1: sort solutions by (query, tuple, root) -> bit-identical output */
+  int deterministic;     /* ignored: the output is always in the deterministic (query, tuple,
+                            root) order and bit-identical run to run (kept for ABI stability) */
   float cull_margin;     /* angular slack (rad) of the FP32 cull; 1e-4                       */
   uint64_t max_solutions;/* minimum initial solution-buffer capacity; the library also sizes the
                             solution / flag sinks from the work list (k=1: pairs/2, pairs/64;
@@ -131,6 +135,10 @@ typedef struct {
   uint64_t n_cull_tests;              /* cull work of the last solve: one bounce, triangle tests of the
                                          per-query cull; two bounces, node-pair tests of the pair
                                          expansion + sub-pair tests of the subdivision refinement    */
+  uint64_t n_truncated;               /* roots / chains dropped at a per-tuple kernel capacity (each such
+                                         tuple carries SPOLY_FLAG_TRUNCATED)                          */
+  uint64_t n_big_scan;                /* two bounces: tuples whose Bezout order n > 32 took the
+                                         shared-memory determinant                                    */
 } spoly_report;
 
 typedef struct {
@@ -176,6 +184,13 @@ spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chai
  * is retained when the solve was chunked (*n_pairs then counts that chunk). */
 spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pair_query,
                                  const uint32_t** pair_tuple, uint64_t* n_pairs);
+
+/* The piecewise rational sqrt surrogate of Eq. 20 the two-bounce kernels use for a
+ * refracting first vertex: 6 rows of (lo, hi, c0, c1, d1), sqrt(x) ~ (c0 + c1 x) / (1 + d1 x) on [lo, hi]
+ * (our minimax fit, reading R8).  out30: HOST, 30 doubles.  from_device = 0: the host copy
+ * compiled into the library (ctx may be NULL, no GPU needed); 1: the table read back from the device's
+ * constant memory (needs a ctx).  Lets the tests pin the kernels' copy to tests/golden/sqrt_table.txt. */
+spoly_status spoly_sqrt_table(spoly_ctx* ctx, int from_device, double* out30);
 
 /* FMA-throughput microbenchmark on the ctx's device (roofline denominator): independent FMA
  * chains on every SM for about `seconds`.  fp64=1: double, 0: float.  Returns FLOP/s. */

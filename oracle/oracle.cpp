@@ -3,7 +3,8 @@
 // step in the paper's order and notation.  Shares no code with the CUDA path.
 //
 // Parity status per function (DESIGN.md §3 lists every reading):
-//   build_system (Eqs. 6, 9, 12, 13-20, 21-23) ............ pinned (tests/test_oracle_system.py)
+//   build_system (Eqs. 6, 9, 12, 13-20, 21-23) ............ pinned (tests/test_oracle_pins.py: degrees,
+//                                                            vanishing at forward-traced planted chains)
 //   bezout (Eq. 24) / det_laplace (Sec. 5.2) .............. pinned (Sylvester resultant, sympy-free)
 //   isolate (Sec. 5.2 derivative recursion) ............... pinned (planted roots, numpy.roots)
 //   scan (Sec. 5.2 piecewise bisection) ................... pinned (planted RR/TT, brute force)
@@ -51,6 +52,12 @@ struct Tri {
   V3 X(double u, double v) const { return p[0] + u * e1() + v * e2(); }                       // Eq. 1
   V3 N(double u, double v) const { return n[0] + u * (n[1] - n[0]) + v * (n[2] - n[0]); }  // Eq. 2
 };
+// face mode (Table 2 "F"): the three vertex normals are equal, n_i = n_{i,0} constant
+static bool face_mode(const Tri& T) {
+  for (int k = 1; k < 3; ++k)
+    if (T.n[k].x != T.n[0].x || T.n[k].y != T.n[0].y || T.n[k].z != T.n[0].z) return false;
+  return true;
+}
 static Tri load_tri(const double* t) {
   Tri T;
   for (int k = 0; k < 3; ++k) T.p[k] = mk(t + 3 * k);
@@ -215,7 +222,11 @@ static void build_system(const std::string& chain, const vector<Tri>& tris, V3 x
   Biv V = dot(cross(S, F1), Dt);                // Eq. 15
   Biv K = dot(cross(Dt, F2), F1);               // Eq. 16
   BVec3 X2 = K * Q0 + U * F1 + V * F2;          // kappa x_2
-  BVec3 N2 = K * BVec3::constant(r0) + U * BVec3::constant(g1) + V * BVec3::constant(g2);  // kappa n_2
+  // kappa n_2 (Eq. 2 at u_2 = (u~, v~)/kappa).  Face mode ("n_i = n_{i,0} is a constant"):
+  // kappa n_2 would be kappa n_{2,0}, a factor kappa common to a and b (det R == 0 identically), so a
+  // face-normal T_2 enters with its constant normal n_{2,0} (reading R22)
+  BVec3 N2 = face_mode(T2) ? BVec3::constant(r0)
+                           : K * BVec3::constant(r0) + U * BVec3::constant(g1) + V * BVec3::constant(g2);
   // Eq. 6 at x_2 (Eq. 23 first line), times kappa^2
   a = dot(cross(X2 - K * X1, Xk - X1), N2);
   BVec3 D2 = K * Xk - X2;  // kappa d_2
@@ -562,6 +573,63 @@ static bool shoot(const Shoot& S, double u1, double v1, double G[2], double* u2,
   return true;
 }
 
+// reading R2: <= 3 Newton steps on F = (a, b) (normalised system, relabeled coordinates), a step is kept only if
+// |F| decreases and the candidate stays within 1e-3 (max-norm) of where back-substitution put it: a refinement of
+// a located root, never a search (SPEC newton_polish_2d).  The bisection threshold 1e-9 on v
+// is otherwise amplified by 1/|da/du| in u.
+static void refine_ab(const Biv& a, const Biv& b, double& us_, double& vs_) {
+  const double u_start = us_, v_start = vs_;
+  double fa = a(us_, vs_), fb = b(us_, vs_);
+  for (int it = 0; it < 3; ++it) {
+    double au = a.du(us_, vs_), av = a.dv(us_, vs_), bu = b.du(us_, vs_), bv = b.dv(us_, vs_);
+    double det = au * bv - av * bu;
+    if (det == 0) break;
+    double du = -(bv * fa - av * fb) / det, dv = -(-bu * fa + au * fb) / det;
+    if (!(std::max(std::fabs(us_ + du - u_start), std::fabs(vs_ + dv - v_start)) <= 1e-3)) break;
+    double na = a(us_ + du, vs_ + dv), nb = b(us_ + du, vs_ + dv);
+    if (!(std::hypot(na, nb) < std::hypot(fa, fb))) break;
+    us_ += du;
+    vs_ += dv;
+    fa = na;
+    fb = nb;
+  }
+}
+
+// c13 polish: <= iters Newton steps on the exact shooting residual G(u1, v1) (central differences,
+// h = 1e-7), a step kept only if |G| decreases.  Returns false when the start cannot be shot; Jm receives the last
+// Jacobian (zero if none was formed), (u2, v2) the hit on T_2.
+static bool polish(const Shoot& S, int iters, double& uu, double& vv, double& uu2, double& vv2, double Jm[4]) {
+  double G[2];
+  for (int i = 0; i < 4; ++i) Jm[i] = 0;
+  bool ok = shoot(S, uu, vv, G, &uu2, &vv2);
+  for (int it = 0; ok && it < iters; ++it) {
+    const double h = 1e-7;
+    double Gp[2], Gm[2], t1, t2;
+    bool f = shoot(S, uu + h, vv, Gp, &t1, &t2) && shoot(S, uu - h, vv, Gm, &t1, &t2);
+    if (!f) break;
+    Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
+    Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
+    f = shoot(S, uu, vv + h, Gp, &t1, &t2) && shoot(S, uu, vv - h, Gm, &t1, &t2);
+    if (!f) break;
+    Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
+    Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
+    double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
+    if (det == 0) break;
+    double du = -(Jm[3] * G[0] - Jm[1] * G[1]) / det;
+    double dv = -(-Jm[2] * G[0] + Jm[0] * G[1]) / det;
+    double Gn[2], nu2, nv2;
+    if (!shoot(S, uu + du, vv + dv, Gn, &nu2, &nv2)) break;
+    if (!(std::hypot(Gn[0], Gn[1]) < std::hypot(G[0], G[1]))) break;
+    uu += du;
+    vv += dv;
+    G[0] = Gn[0];
+    G[1] = Gn[1];
+    uu2 = nu2;
+    vv2 = nv2;
+  }
+  return ok;
+}
+
 // ------------------------------------------------------------------ per-tuple solve
 struct Sol {
   double bary[4];
@@ -578,11 +646,14 @@ struct TupleResult {
   uint32_t flags = 0;
 };
 
+// c14 probe of a near-tangency condition (reading R11): domain slack, and how far the k = 2 polish may move a probe
+constexpr double kProbeDomain = 1e-3, kProbeMove = 1e-2;
 static bool in_domain(double u, double v, double eps) { return u >= -eps && v >= -eps && u + v <= 1 + eps; }
 static double edge_dist(double u, double v) { return std::min(std::min(u, v), 1 - u - v); }
 
-// candidate u-roots of the univariate polynomial A(u) (back-substitution; c11)
-static vector<double> u_roots(Uni A, double tol, uint32_t* flags) {
+// candidate u-roots of the univariate polynomial A(u) (back-substitution; c11).  A quadratic with
+// |disc| <= 1e-8 scale (two u-roots about to merge, c14) reports the double root's position in *udouble.
+static vector<double> u_roots(Uni A, double tol, double* udouble) {
   A.trim();
   vector<double> r;
   if (A.deg() <= 0) return r;
@@ -593,7 +664,7 @@ static vector<double> u_roots(Uni A, double tol, uint32_t* flags) {
   if (A.deg() == 2) {
     double a0 = A.c[0], a1 = A.c[1], a2 = A.c[2];
     double disc = a1 * a1 - 4 * a2 * a0, scale = a1 * a1 + 4 * std::fabs(a2 * a0);
-    if (std::fabs(disc) <= 1e-8 * scale) *flags |= ORC_FLAG_NEAR_TANGENT;
+    if (std::fabs(disc) <= 1e-8 * scale && udouble) *udouble = -a1 / (2 * a2);
     if (disc < -1e-12 * scale) return r;
     if (disc < 0) disc = 0;
     double q = -0.5 * (a1 + std::copysign(std::sqrt(disc), a1));
@@ -643,6 +714,8 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
 
   // ---- univariate roots v*
   vector<double> vroots;
+  vector<double> vprobes;                      // v of c14 near-tangency conditions (reading R11)
+  vector<std::pair<double, double>> uprobes;  // (u, v) of near-double u-roots of a(., v*)
   if (k == 1) {
     Uni r = det_laplace(bezout(a, b, n));
     double mr = r.maxabs();
@@ -653,14 +726,15 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
     }
     r = (1.0 / mr) * r;
     vector<double> raw = isolate(r, 0.0, 1.0, cfg.bisect_tol);
+    // c14 near-tangency conditions (probed below, reading R11): two v-roots closer than eps_flag ...
     for (size_t i = 1; i < raw.size(); ++i)
-      if (raw[i] - raw[i - 1] < cfg.eps_flag) out.flags |= ORC_FLAG_NEAR_TANGENT;
-    // c14: a critical point of r in [0,1] with |r(c)| <= 1e-10 max_[0,1] |r|
+      if (raw[i] - raw[i - 1] < cfg.eps_flag) vprobes.push_back(0.5 * (raw[i] + raw[i - 1]));
+    // ... or a critical point of r in [0,1] with |r(c)| <= 1e-10 max_[0,1] |r| (a double root bisection misses)
     vector<double> crit = isolate(derivative(r), 0.0, 1.0, cfg.bisect_tol);
     double rmax = std::max(std::fabs(r(0.0)), std::fabs(r(1.0)));
     for (double c : crit) rmax = std::max(rmax, std::fabs(r(c)));
     for (double c : crit)
-      if (std::fabs(r(c)) <= 1e-10 * rmax) out.flags |= ORC_FLAG_NEAR_TANGENT;
+      if (std::fabs(r(c)) <= 1e-10 * rmax) vprobes.push_back(c);
     vroots = dedup(raw, 1e-7);
   } else {
     // k >= 2: sign scan of det R(v_j) at v_j = j/pieces, then bisection
@@ -672,17 +746,18 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
       double nb = -INFINITY;
       if (j > 0) nb = std::max(nb, lg[j - 1]);
       if (j < P) nb = std::max(nb, lg[j + 1]);
-      if (lg[j] < std::log(1e-9) + nb) out.flags |= ORC_FLAG_NEAR_TANGENT;
+      // c14: |det R(v_j)| < 1e-9 max(neighbours): a root within ~1e-11 of the sample (probed, reading R11)
+      if (lg[j] < std::log(1e-9) + nb) vprobes.push_back((double)j / P);
     }
-    int last_change = -10;
+    // (sign changes in adjacent pieces are found as two roots; the sign at the sample between them is exact
+    // unless the |det| test above probes it, so adjacency alone is no ambiguity -- reading R11)
     for (int j = 0; j <= P; ++j) {
       if (s[j] == 0) {
         vroots.push_back((double)j / P);
         continue;
       }
       if (j < P && s[j + 1] != 0 && s[j] != s[j + 1]) {
-        if (j - last_change == 1) out.flags |= ORC_FLAG_NEAR_TANGENT;  // changes in adjacent pieces
-        last_change = j;
+
         double lo = (double)j / P, hi = (double)(j + 1) / P;
         int slo = s[j];
         for (int it = 0; it < cfg.scan_bisect_iters; ++it) {
@@ -725,31 +800,14 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
         continue;
       }
     }
-    vector<double> us = u_roots(A, cfg.bisect_tol, &out.flags);
+    double ud = NAN;
+    vector<double> us = u_roots(A, cfg.bisect_tol, &ud);
+    if (!std::isnan(ud)) uprobes.push_back({ud, vs});
     for (double us_ : us) {
       C.c[3]++;
       double vs_ = vs;
       if (k == 1) {
-        // reading R2: <= 3 Newton steps on F = (a, b) (normalised system, relabeled coordinates),
-        // a step is kept only if |F| decreases and the candidate stays within 1e-3 (max-norm) of where
-        // back-substitution put it: a refinement of a located root, never a search (SPEC
-        // newton_polish_2d).  The bisection threshold 1e-9 on v is
-        // otherwise amplified by 1/|da/du| in u.
-        const double u_start = us_, v_start = vs_;
-        double fa = a(us_, vs_), fb = b(us_, vs_);
-        for (int it = 0; it < 3; ++it) {
-          double au = a.du(us_, vs_), av = a.dv(us_, vs_), bu = b.du(us_, vs_), bv = b.dv(us_, vs_);
-          double det = au * bv - av * bu;
-          if (det == 0) break;
-          double du = -(bv * fa - av * fb) / det, dv = -(-bu * fa + au * fb) / det;
-          if (!(std::max(std::fabs(us_ + du - u_start), std::fabs(vs_ + dv - v_start)) <= 1e-3)) break;
-          double na = a(us_ + du, vs_ + dv), nb = b(us_ + du, vs_ + dv);
-          if (!(std::hypot(na, nb) < std::hypot(fa, fb))) break;
-          us_ += du;
-          vs_ += dv;
-          fa = na;
-          fb = nb;
-        }
+        refine_ab(a, b, us_, vs_);
       }
       // map back to the ORIGINAL labeling
       double bary[4];
@@ -826,34 +884,8 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
       }
       // polish: <= polish_iters Newton steps on the exact shooting residual, accept if |G| decreases
       frame(normalize(xk1 - x2), &S.f1, &S.f2);
-      double uu = ur, vv = vr, G[2], uu2 = u2, vv2 = v2;
-      bool ok = shoot(S, uu, vv, G, &uu2, &vv2);
-      double Jm[4] = {0, 0, 0, 0};
-      for (int it = 0; ok && it < cfg.polish_iters; ++it) {
-        const double h = 1e-7;
-        double Gp[2], Gm[2], t1, t2;
-        bool f = shoot(S, uu + h, vv, Gp, &t1, &t2) && shoot(S, uu - h, vv, Gm, &t1, &t2);
-        if (!f) break;
-        Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
-        Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
-        f = shoot(S, uu, vv + h, Gp, &t1, &t2) && shoot(S, uu, vv - h, Gm, &t1, &t2);
-        if (!f) break;
-        Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
-        Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
-        double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
-        if (det == 0) break;
-        double du = -(Jm[3] * G[0] - Jm[1] * G[1]) / det;
-        double dv = -(-Jm[2] * G[0] + Jm[0] * G[1]) / det;
-        double Gn[2], nu2, nv2;
-        if (!shoot(S, uu + du, vv + dv, Gn, &nu2, &nv2)) break;
-        if (!(std::hypot(Gn[0], Gn[1]) < std::hypot(G[0], G[1]))) break;
-        uu += du;
-        vv += dv;
-        G[0] = Gn[0];
-        G[1] = Gn[1];
-        uu2 = nu2;
-        vv2 = nv2;
-      }
+      double uu = ur, vv = vr, uu2 = u2, vv2 = v2, Jm[4];
+      bool ok = polish(S, cfg.polish_iters, uu, vv, uu2, vv2, Jm);
       if (!ok) {
         C.c[5]++;
         continue;
@@ -900,6 +932,48 @@ static TupleResult solve_tuple(const std::string& chain, const vector<Tri>& tris
       s.contribution = J > 0 ? intensity / J : 0.0;
       found.push_back(s);
     }
+  }
+  // c14 NEAR_TANGENT (reading R11): a near-tangency condition raises the flag only where it sits at an (almost)
+  // admissible chain, i.e. where the ambiguity of counting a double root can change the admissible set.  Probe:
+  // each back-substituted candidate there is refined exactly like a root (k = 1: the (a, b) refinement of reading
+  // R2; k = 2: within kProbeDomain of both triangles, then the c13 polish, kept within kProbeMove of its start);
+  // the flag is raised if one lands within kProbeDomain of every triangle with Eq. 3 residual < theta_final.
+  // Ghost double roots (the square form's P = Q = 0 points, where Eq. 9's projection is blind) and tangencies far
+  // outside the triangles stay unflagged: they cannot produce an admissible chain.
+  {
+    auto probe_uv = [&](double us_, double vs_) -> bool {
+      if (k == 1) {
+        refine_ab(a, b, us_, vs_);
+        double ur = us_, vr = vs_;
+        if (D.relabel) std::swap(ur, vr);
+        if (!in_domain(ur, vr, kProbeDomain)) return false;
+        const Tri& T = tris_in[0];
+        return vertex_residual(x0, T.X(ur, vr), xk1, T.N(ur, vr), D.eta[0], D.eta[1]) < cfg.theta_final;
+      }
+      double kap = K(us_, vs_), u2 = U(us_, vs_) / kap, v2 = V(us_, vs_) / kap;
+      if (!(std::fabs(kap) > 0) || !std::isfinite(u2) || !std::isfinite(v2)) return false;
+      if (D.relabel) std::swap(u2, v2);
+      if (!in_domain(us_, vs_, kProbeDomain) || !in_domain(u2, v2, kProbeDomain)) return false;
+      double uu = us_, vv = vs_, uu2 = u2, vv2 = v2, Jm[4];
+      frame(normalize(xk1 - tris_in[1].X(u2, v2)), &S.f1, &S.f2);
+      if (!polish(S, cfg.polish_iters, uu, vv, uu2, vv2, Jm)) return false;
+      if (std::max(std::fabs(uu - us_), std::fabs(vv - vs_)) > kProbeMove) return false;
+      if (!in_domain(uu, vv, kProbeDomain) || !in_domain(uu2, vv2, kProbeDomain)) return false;
+      V3 x1 = tris_in[0].X(uu, vv), x2 = tris_in[1].X(uu2, vv2);
+      double r1 = vertex_residual(x0, x1, x2, tris_in[0].N(uu, vv), D.eta[0], D.eta[1]);
+      double r2 = vertex_residual(x1, x2, xk1, tris_in[1].N(uu2, vv2), D.eta[1], D.eta[2]);
+      return std::max(r1, r2) < cfg.theta_final;
+    };
+    bool hit = false;
+    for (auto& p : uprobes) hit = hit || probe_uv(p.first, p.second);
+    for (double v : vprobes) {
+      if (hit) break;
+      Uni A = a.at_v(v);
+      if (!(A.maxabs() >= 1e-12)) A = b.at_v(v);
+      if (!(A.maxabs() >= 1e-12)) continue;
+      for (double u : u_roots(A, cfg.bisect_tol, nullptr)) hit = hit || probe_uv(u, v);
+    }
+    if (hit) out.flags |= ORC_FLAG_NEAR_TANGENT;
   }
   // dedup admissible chains closer than 1e-7 in (u1, v1) (polished candidates may coincide)
   for (const Sol& s : found) {
@@ -1073,8 +1147,8 @@ void orc_default_config(orc_config* c) {
   c->pieces = 100;
   c->scan_bisect_iters = 10;
   c->bisect_tol = 1e-9;
-  c->polish_iters = 3;
-  c->theta_admit = 1e-3;
+  c->polish_iters = 5;
+  c->theta_admit = 3e-2;
   c->theta_final = 1e-6;
   c->eps_domain = 1e-9;
   c->eps_flag = 1e-6;

@@ -25,8 +25,8 @@ typedef struct {
   int pieces;            /* k>=2 scan pieces, 100 */
   int scan_bisect_iters; /* 10 */
   double bisect_tol;     /* 1e-9 */
-  int polish_iters;      /* 3 ("one iteration"; c13) */
-  double theta_admit;    /* 1e-3 raw-root residual gate (k>=2) */
+  int polish_iters;      /* 5 ("one iteration"; c13, DESIGN reading R23) */
+  double theta_admit;    /* 3e-2 raw-root residual gate (k>=2; DESIGN reading R24) */
   double theta_final;    /* 1e-6 final residual gate (north_star) */
   double eps_domain;     /* 1e-9 */
   double eps_flag;       /* 1e-6 */

@@ -82,6 +82,7 @@ struct spoly_ctx {
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2, d_pqa, d_pta;
   uint32_t k2_chunk = 0;  // queries per two-bounce cull chunk (learned; reset by mesh upload)
   DBuf<unsigned char> d_keep;
+  DBuf<unsigned int> d_lerr;  // explicit tuple list validation word
   DBuf<uint32_t> d_qmask;
   DBuf<uint64_t> d_front;
   DBuf<unsigned long long> d_fcount;
@@ -134,7 +135,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->pieces = 100;
   c->scan_bisect_iters = 10;
   c->bisect_tol = 1e-9;
-  c->polish_iters = 3;
+  c->polish_iters = 5;
   c->theta_admit = 1e-3;
   c->theta_final = 1e-6;
   c->eps_domain = 1e-9;
@@ -187,7 +188,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_emask.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
-  ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_nsel.release();
+  ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_lerr.release(); ctx->d_nsel.release();
   ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
     for (auto& b : f) b.release();
@@ -489,8 +490,16 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     npairs = tot;
     CK(ctx->d_pq.ensure(npairs));
     CK(ctx->d_pt.ensure(npairs * k));
-    launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm, st);
+    CK(ctx->d_lerr.ensure(1));
+    CK(cudaMemsetAsync(ctx->d_lerr.p, 0, sizeof(unsigned int), st));
+    launch_expand_list(tuples->offsets, tuples->tri_ids, nq, k, ctx->M.perm_of, ctx->M.ntris, npairs, ctx->d_pq.p,
+                       ctx->d_pt.p, ctx->d_lerr.p, ctx->nsm, st);
     ctx->launches++;
+    unsigned int lerr = 0;
+    CK(cudaMemcpyAsync(&lerr, ctx->d_lerr.p, sizeof(lerr), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    if (lerr & 1u) return fail(ctx, SPOLY_ERR_INVALID_ARG, "tuple list holds a triangle id >= ntris");
+    if (lerr & 2u) return fail(ctx, SPOLY_ERR_INVALID_ARG, "tuple list offsets are not monotone");
   } else if (ctx->cfg.cull && k == 2) {
     // queries are culled in chunks whose node-pair frontiers fit cfg.max_pairs entries; the refined pair
     // lists of the chunks are appended in query order, so the work list equals the unchunked one
@@ -852,6 +861,8 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_cand_jobs = counters[C_CAND_JOBS];
   R.n_path_jobs = cnt[4];
   R.n_cull_tests = ctx->cull_tests;
+  R.n_truncated = counters[C_TRUNCATED];
+  R.n_big_scan = counters[C_BIG_SCAN];
   return SPOLY_OK;
 }
 
@@ -896,6 +907,17 @@ spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pq, cons
   *pq = c->d_pq.p;
   *pt = c->d_pt_orig.p;
   *n = c->npairs;
+  return SPOLY_OK;
+}
+
+spoly_status spoly_sqrt_table(spoly_ctx* ctx, int from_device, double* out30) {
+  if (!out30 || (from_device && !ctx)) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
+  if (from_device) CK(cudaSetDevice(ctx->device));
+  cudaError_t e = k2_sqrt_table(from_device, out30);
+  if (e != cudaSuccess) {
+    if (ctx) ctx->err = cudaGetErrorString(e);
+    return SPOLY_ERR_CUDA;
+  }
   return SPOLY_OK;
 }
 

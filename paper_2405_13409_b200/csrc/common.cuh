@@ -126,6 +126,6 @@ struct JobSink {
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,
-       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_REFINED, C_CAND_JOBS, C_NUM };
+       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_REFINED, C_CAND_JOBS, C_TRUNCATED, C_BIG_SCAN, C_NUM };
 
 }  // namespace spoly

@@ -502,21 +502,34 @@ void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint
 
 // explicit CSR tuple list (original ids) -> work list (Morton positions); one warp per query
 __global__ void k_expand_list(const uint32_t* __restrict__ off, const uint32_t* __restrict__ ids, uint32_t nq, int k,
-                              const uint32_t* __restrict__ perm_of, uint32_t* pq, uint32_t* pt) {
+                              const uint32_t* __restrict__ perm_of, uint32_t ntris, uint64_t total, uint32_t* pq,
+                              uint32_t* pt, unsigned int* err) {
+  // caller-supplied ids are checked here (an out-of-range id would otherwise fault and poison the context):
+  // a bad id or a non-monotone / out-of-range CSR row sets *err and writes position 0 in its place
   const int lane = threadIdx.x & 31;
   const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t q = gw; q < nq; q += nw) {
-    for (uint32_t i = off[q] + lane; i < off[q + 1]; i += 32) {
+    const uint32_t b = off[q], e = off[q + 1];
+    if (e < b || e > total) {
+      if (lane == 0) atomicOr(err, 2u);
+      continue;
+    }
+    for (uint32_t i = b + lane; i < e; i += 32) {
       pq[i] = q;
-      for (int j = 0; j < k; ++j) pt[(uint64_t)k * i + j] = perm_of[ids[(uint64_t)k * i + j]];
+      for (int j = 0; j < k; ++j) {
+        const uint32_t id = ids[(uint64_t)k * i + j];
+        if (id >= ntris) atomicOr(err, 1u);
+        pt[(uint64_t)k * i + j] = id < ntris ? perm_of[id] : 0u;
+      }
     }
   }
 }
 void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32_t nq, int k, const uint32_t* perm_of,
-                        uint32_t* pair_query, uint32_t* pair_tpos, int nsm, cudaStream_t st) {
+                        uint32_t ntris, uint64_t total, uint32_t* pair_query, uint32_t* pair_tpos, unsigned int* err,
+                        int nsm, cudaStream_t st) {
   if (!nq) return;
-  k_expand_list<<<nsm * 8, 256, 0, st>>>(offsets, tri_ids, nq, k, perm_of, pair_query, pair_tpos);
+  k_expand_list<<<nsm * 8, 256, 0, st>>>(offsets, tri_ids, nq, k, perm_of, ntris, total, pair_query, pair_tpos, err);
 }
 
 }  // namespace spoly

@@ -25,8 +25,10 @@ void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* 
                        uint32_t* counts, uint32_t* masks, const unsigned long long* offsets, uint32_t* pq,
                        uint32_t* pt, int nsm, cudaStream_t st);
 void launch_all_pairs_k1(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
+// explicit tuple list -> work list; *err |= 1 for an id >= ntris, 2 for a malformed CSR row (err zeroed by the caller)
 void launch_expand_list(const uint32_t* offsets, const uint32_t* tri_ids, uint32_t nq, int k, const uint32_t* perm_of,
-                        uint32_t* pair_query, uint32_t* pair_tpos, int nsm, cudaStream_t st);
+                        uint32_t ntris, uint64_t total, uint32_t* pair_query, uint32_t* pair_tpos, unsigned int* err,
+                        int nsm, cudaStream_t st);
 
 // solve_k1.cu
 void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs,
@@ -44,6 +46,8 @@ struct K2Scratch {
   int launches;
 };
 uint64_t k2_record_bytes(int v1t, int v2t);
+// the Eq. 20 sqrt surrogate table (6 x (lo, hi, c0, c1, d1)): host copy, or read back from constant memory
+cudaError_t k2_sqrt_table(int from_device, double* out30);
 void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
                      const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
                      int nsm, cudaStream_t st);

@@ -362,8 +362,15 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
       }
       RootSet<DB + 1> Rb;
       isolate_roots<DB + 1>(bl, bd, -0.1, 1.1, 1e-7, Rb);
-      for (int i = 0; i < Rb.n && nu < 4; ++i)
-        if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) ua[nu++] = Rb.x[i];
+      for (int i = 0; i < Rb.n; ++i)
+        if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) {
+          if (nu < 4) {
+            ua[nu++] = Rb.x[i];
+          } else {  // slot capacity (4 u-roots per v-root): flagged, never silent
+            out.flags |= SPOLY_FLAG_TRUNCATED;
+            cnt[C_TRUNCATED]++;
+          }
+        }
     }
     for (int iu = 0; iu < nu; ++iu) {
       cnt[C_CANDIDATES]++;
@@ -437,6 +444,9 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
         out.resid[s] = (float)rho;
         out.slot[s] = (uint32_t)(iv * 4 + iu);
         cnt[C_ADMISSIBLE]++;
+      } else {  // per-pair capacity: flagged, never silent
+        out.flags |= SPOLY_FLAG_TRUNCATED;
+        cnt[C_TRUNCATED]++;
       }
     }
   }

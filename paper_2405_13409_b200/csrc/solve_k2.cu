@@ -33,14 +33,24 @@ struct Tri2 {
   __device__ d3 c() const { return (1.0 / 3.0) * (p[0] + p[1] + p[2]); }
 };
 
-// piecewise rational sqrt surrogate (Eq. 20): literal copy of tests/golden/sqrt_table.txt (our fit, R8)
-__constant__ double c_sqrt_tab[6][5] = {
-    {0, 0.00042432536375417839, 0.00089999999999879705, 154.92902483814683, 5615.7008147954339},
-    {0.00042432536375417839, 0.0077313602416299448, 0.013714746392967799, 21.253136166194601, 135.24944765874642},
-    {0.0077313602416299448, 0.051793068389647277, 0.04635497395617269, 6.7900571325924943, 14.594946360257405},
-    {0.051793068389647277, 0.21636853563098274, 0.10736470812718857, 3.006160575603614, 2.9223382765562778},
-    {0.21636853563098274, 0.68268233146982271, 0.20527897991137517, 1.5904325277264706, 0.82650456712266585},
-    {0.68268233146982271, 1, 0.30276242425651556, 1.0984677499357838, 0.40129928835931156}};
+// piecewise rational sqrt surrogate (Eq. 20): literal copy of tests/golden/sqrt_table.txt (our fit, R8); the
+// same literal fills the device table and the host copy spoly_sqrt_table() returns, and the tests compare
+// both (the device one read back from constant memory) with the golden file
+#define SPOLY_SQRT_TAB                                                                                            \
+  {{0, 0.00042432536375417839, 0.00089999999999879705, 154.92902483814683, 5615.7008147954339},                 \
+   {0.00042432536375417839, 0.0077313602416299448, 0.013714746392967799, 21.253136166194601, 135.24944765874642}, \
+   {0.0077313602416299448, 0.051793068389647277, 0.04635497395617269, 6.7900571325924943, 14.594946360257405},    \
+   {0.051793068389647277, 0.21636853563098274, 0.10736470812718857, 3.006160575603614, 2.9223382765562778},       \
+   {0.21636853563098274, 0.68268233146982271, 0.20527897991137517, 1.5904325277264706, 0.82650456712266585},      \
+   {0.68268233146982271, 1, 0.30276242425651556, 1.0984677499357838, 0.40129928835931156}}
+__constant__ double c_sqrt_tab[6][5] = SPOLY_SQRT_TAB;
+static const double h_sqrt_tab[6][5] = SPOLY_SQRT_TAB;
+
+cudaError_t k2_sqrt_table(int from_device, double* out30) {
+  if (from_device) return cudaMemcpyFromSymbol(out30, c_sqrt_tab, sizeof(h_sqrt_tab));
+  for (int i = 0; i < 30; ++i) out30[i] = h_sqrt_tab[i / 5][i % 5];
+  return cudaSuccess;
+}
 
 // polynomial degrees of the chain X1 X2 (X = R reflection / T refraction)
 template <bool V1T, bool V2T>
@@ -156,6 +166,8 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   }
   // rational coordinate mapping onto T_2 (Eqs. 13-16)
   const d3 f1 = T2.e1(), f2 = T2.e2(), r0 = T2.n[0], g1 = T2.n[1] - T2.n[0], g2 = T2.n[2] - T2.n[0];
+  const bool face2 = T2.n[1].x == r0.x && T2.n[1].y == r0.y && T2.n[1].z == r0.z && T2.n[2].x == r0.x &&
+                     T2.n[2].y == r0.y && T2.n[2].z == r0.z;
   WV Sv = ar.vec(1);  // x_1 - p_{2,0}
   wlinear3(g, Sv, T1.p[0] - T2.p[0], e1, e2);
   WV Dxf2 = ar.vec(DK);
@@ -170,9 +182,20 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   wlin3(g, X2.x, S.K, T2.p[0].x, S.U, f1.x, S.V, f2.x, false);
   wlin3(g, X2.y, S.K, T2.p[0].y, S.U, f1.y, S.V, f2.y, false);
   wlin3(g, X2.z, S.K, T2.p[0].z, S.U, f1.z, S.V, f2.z, false);
-  wlin3(g, N2.x, S.K, r0.x, S.U, g1.x, S.V, g2.x, false);
-  wlin3(g, N2.y, S.K, r0.y, S.U, g1.y, S.V, g2.y, false);
-  wlin3(g, N2.z, S.K, r0.z, S.U, g1.z, S.V, g2.z, false);
+  if (face2) {
+    // face mode (n_2 = n_{2,0} constant): kappa n_2 would be kappa n_{2,0}, a factor kappa common
+    // to a and b (det R == 0 identically), so the constant normal enters instead (reading R22)
+    for (int i = g.lane; i < tri_n(DU); i += G) {
+      N2.x.c[i] = i == 0 ? r0.x : 0.0;
+      N2.y.c[i] = i == 0 ? r0.y : 0.0;
+      N2.z.c[i] = i == 0 ? r0.z : 0.0;
+    }
+    g.sync();
+  } else {
+    wlin3(g, N2.x, S.K, r0.x, S.U, g1.x, S.V, g2.x, false);
+    wlin3(g, N2.y, S.K, r0.y, S.U, g1.y, S.V, g2.y, false);
+    wlin3(g, N2.z, S.K, r0.z, S.U, g1.z, S.V, g2.z, false);
+  }
   // a = ((X2 - K X1) x (x3 - X1)) . N2   (Eq. 6 at x_2, Eq. 23 first line)
   {
     const int m2 = ar.top;
@@ -421,7 +444,8 @@ struct Rec2 {
   static constexpr int STRIDE = (K + tri_n(D::DK) + 7) & ~7;
 };
 enum { H_ETA0 = 0, H_ETA1, H_ETA2, H_RELABEL, H_FLAGS, H_DA, H_DB, H_N, H_OK, H_NV };
-constexpr int kMaxV2 = 40;  // v-roots kept per pair
+constexpr int kMaxV2 = 40;   // v-roots kept per pair (more: SPOLY_FLAG_TRUNCATED)
+constexpr int kMaxSol2 = 8;  // admissible chains kept per pair (more: SPOLY_FLAG_TRUNCATED)
 
 __device__ __forceinline__ void load_chain(const TriRec* __restrict__ tris, const uint32_t* __restrict__ pt,
                                            const double* __restrict__ ep, uint32_t q, uint64_t pi, Chain2& C) {
@@ -594,6 +618,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
     uint32_t flags = (uint32_t)rec[H_FLAGS];
     int nv = 0;
     if (ok) {
+      if (BIG) cnt[C_BIG_SCAN]++;
       const int da = (int)rec[H_DA], db = (int)rec[H_DB];
       const double* AT = rec + R::AT;
       const double* BT = rec + R::BT;
@@ -627,6 +652,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
           if (nv < kMaxV2) {
             if (g.lane == 0) rec[R::VR + nv] = (double)j / P;
             nv++;
+          } else {
+            flags |= SPOLY_FLAG_TRUNCATED;
+            cnt[C_TRUNCATED]++;
           }
         } else if (j < P && s_next != 0 && s_next != s_cur) {
           if (j - last_change == 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
@@ -648,6 +676,9 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
           if (nv < kMaxV2) {
             if (g.lane == 0) rec[R::VR + nv] = 0.5 * (lo + hi);
             nv++;
+          } else {
+            flags |= SPOLY_FLAG_TRUNCATED;
+            cnt[C_TRUNCATED]++;
           }
         }
         lg_prev = lg_cur;
@@ -704,8 +735,8 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
         Kp{const_cast<double*>(rec + R::K), D::DK};
     uint32_t flags = 0;
     int nsol = 0;
-    double su[4][4], scontrib[4];
-    float sres[4];
+    double su[kMaxSol2][4], scontrib[kMaxSol2];
+    float sres[kMaxSol2];
     constexpr int NA = D::DB + 1;
     for (int iv = 0; iv < nv; ++iv) {
       const double vs = rec[R::VR + iv];
@@ -729,7 +760,7 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
         }
       }
       while (dA > 0 && Acoef[dA] == 0.0) --dA;
-      double us[kMaxV2];
+      double us[NA];
       int nu = 0;
       if (dA == 1) {
         us[nu++] = -Acoef[0] / Acoef[1];
@@ -757,8 +788,8 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
       } else if (dA > 2) {
         RootSet<NA> Ru;
         isolate_roots<NA>(Acoef, dA, -0.1, 1.1, 1e-7, Ru);
-        for (int i = 0; i < Ru.n && nu < kMaxV2; ++i)
-          if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];
+        for (int i = 0; i < Ru.n; ++i)
+          if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];  // Ru.n <= dA < NA
       }
       for (int iu = 0; iu < nu; ++iu) {
         cnt[C_CANDIDATES]++;
@@ -857,7 +888,10 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
           cnt[C_REJ_SIDE]++;
           continue;
         }
-        if (nsol < 4) {
+        if (nsol >= kMaxSol2) {  // per-pair capacity: flagged, never silent
+          flags |= SPOLY_FLAG_TRUNCATED;
+          cnt[C_TRUNCATED]++;
+        } else {
           const double J = jacobian2(C, x1, x2);
           const double I = inten ? inten[q] : 1.0;
           su[nsol][0] = uu;
@@ -908,12 +942,10 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, c
   constexpr int G = D::G;
   const size_t sh_build = (size_t)kBuildWarps * (32 / G) * D::ARENA * sizeof(double);
   const size_t sh_big = (size_t)kScanWarps * (32 / G) * (2 * (R::NR + 2) + R::NR * R::NR) * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k2_build<V1T, V2T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_build);
-    cudaFuncSetAttribute(k2_scan<V1T, V2T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_big);
-    attr = true;
-  }
+  // the attribute is per device: set it on every launch (cheap; a process-wide "done" flag would skip it on a
+  // second context's device, and is not thread-safe)
+  cudaFuncSetAttribute(k2_build<V1T, V2T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_build);
+  cudaFuncSetAttribute(k2_scan<V1T, V2T, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sh_big);
   int occ_b = 0, occ_s = 0, occ_p = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_b, k2_build<V1T, V2T>, kBuildWarps * 32, sh_build);
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ_s, k2_scan<V1T, V2T, nc_of_class<G>(0)>, kScanWarps * 32, 0);

@@ -20,10 +20,10 @@ LIB_PATH = os.environ.get("SPOLY_LIB") or os.path.join(HERE, "libspoly.so")
 SPOLY_OK = 0
 STATUS = {0: "SPOLY_OK", 1: "SPOLY_ERR_INVALID_ARG", 2: "SPOLY_ERR_BAD_MESH", 3: "SPOLY_ERR_UNSUPPORTED_CHAIN",
           4: "SPOLY_ERR_OOM", 5: "SPOLY_ERR_CAPACITY", 6: "SPOLY_ERR_CUDA"}
-FLAG_NEAR_TANGENT, FLAG_BOUNDARY, FLAG_RESIDUAL, FLAG_DEGENERATE = 1, 2, 4, 8
+FLAG_NEAR_TANGENT, FLAG_BOUNDARY, FLAG_RESIDUAL, FLAG_DEGENERATE, FLAG_TRUNCATED = 1, 2, 4, 8, 16
 
 EXPORTS = ["spoly_default_config", "spoly_create", "spoly_destroy", "spoly_last_error", "spoly_upload_mesh",
-           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma"]
+           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma", "spoly_sqrt_table"]
 
 
 class SpolyError(RuntimeError):
@@ -55,7 +55,8 @@ class spoly_report(ctypes.Structure):
         ("alg_kflop", ctypes.c_uint64), ("n_jobs_mono", ctypes.c_uint64), ("n_jobs_deep", ctypes.c_uint64),
         ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64),
         ("ms_roots", ctypes.c_float), ("ms_path", ctypes.c_float), ("n_refined", ctypes.c_uint64),
-        ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64), ("n_cull_tests", ctypes.c_uint64)]
+        ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64), ("n_cull_tests", ctypes.c_uint64),
+        ("n_truncated", ctypes.c_uint64), ("n_big_scan", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -89,8 +90,20 @@ def lib():
         L.spoly_solve_host.argtypes = [P, U32, ctypes.c_char_p, I, P, U32, P, P, P]
         L.spoly_last_worklist.argtypes = [P, P, P, P]
         L.spoly_bench_fma.argtypes = [P, I, D, P]
+        L.spoly_sqrt_table.argtypes = [P, I, P]
         _lib = L
     return _lib
+
+
+def sqrt_table(ctx=None) -> np.ndarray:
+    """The Eq. 20 sqrt-surrogate table compiled into the library (6 x 5): the host copy (ctx None) or the
+    device's constant-memory copy (ctx a Context)."""
+    out = np.zeros(30, np.float64)
+    h = ctx._h if ctx is not None else None
+    rc = lib().spoly_sqrt_table(h, 1 if ctx is not None else 0, out.ctypes.data)
+    if rc != SPOLY_OK:
+        raise SpolyError(f"spoly_sqrt_table: {STATUS.get(rc, rc)}")
+    return out.reshape(6, 5)
 
 
 def default_config(**kw) -> spoly_config:
@@ -208,7 +221,8 @@ class Context:
                    n_pairs_coarse=int(r.report.n_pairs_coarse), ms_roots=r.report.ms_roots,
                    ms_path=r.report.ms_path, n_refined=int(r.report.n_refined),
                    n_cand_jobs=int(r.report.n_cand_jobs), n_path_jobs=int(r.report.n_path_jobs),
-                   n_cull_tests=int(r.report.n_cull_tests))
+                   n_cull_tests=int(r.report.n_cull_tests), n_truncated=int(r.report.n_truncated),
+                   n_big_scan=int(r.report.n_big_scan))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),
