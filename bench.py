@@ -5,8 +5,10 @@ Workload (BASELINE.json configs[1]): C2 "glints" — 256x256 light samples (quer
 normal-mapped bumpy plane, one-bounce reflection (R), cull pre-pass + fused solve + deterministic
 compaction.  One step = one spoly_solve over all 65,536 queries with inputs resident in HBM.
 
-Multi-GPU (torchrun): the path shards by query; every rank solves its own full C2 frame (different light
-stratification seed) -> weak scaling; NCCL only all-reduces the counters and gathers per-query sums.
+Multi-GPU (torchrun): strong scaling of ONE frame: the frame's query grid is cut into 64 x 64 tiles dealt
+round-robin to the ranks; each rank solves its tiles with no collective inside the solve; NCCL
+reduces the counters exactly (int64), takes the max (and mean) of the ranks' device times and gathers the per-query
+sums back to frame order.
 
 --impl reference: the CPU oracle (plain FP64 C++ transcription of the paper) timed on the host cores on a
 bounded sample of the same workload (the reference arm for this tier).
@@ -31,51 +33,51 @@ UNIT = "paths/s"
 # ---------------------------------------------------------------- algorithmic FLOP model
 # Minimal-form FP64 FLOPs of the one-bounce reflection solve (FMA = 2, add/mul/div/sqrt = 1), counted
 # from the kernel formulas (DESIGN.md §5 table):
-#   phase 1, per pair: decision 75 + setup 18 + a 75 + b 268 + normalise 22 + truncation 10
-#                      + coplanarity sign test 16                                            = 484
+#   phase 1 (k1_phase1: coefficient phase, elimination, Bernstein level, monotone root, pre-check), per pair:
+#            decision 75 + setup 18 + a 75 + b 268 + normalise 22 + truncation 10 + coplanarity sign test 16 = 484
 #            per pair reaching the elimination (counter n_elims): Bezout 128 + Laplace 316
 #                      + normalise r 11 + Bernstein level 155                                = 610
-#   roots  : 2 per FMA term of the root-finding evaluations (counter n_eval_terms)   [k1_roots]
-#   path   :                                                              [k1_cand + k1_path]
-#            + 25 per candidate (back-substitution: a(., v*) slices + stable quadratic)
+#            + 2 per FMA term of the monotone jobs' Newton evaluations (counter n_eval_terms)
+#            + 25 per monotone job with a root (back-substitution: a(., v*) slices + stable quadratic, n_cand_jobs)
+#   deep jobs (k1_roots_deep): 2 per FMA term of the derivative recursion (counter n_eval_deep)
+#   path (k1_path):
 #            + 407 per refined candidate (past the domain pre-check, counter n_refined: one (a,b)
 #              Newton step 277, Eq. 3 residual + sides 130)
 #            + 250 per admissible chain (analytic ray-differential Jacobian)
-#            The path kernels recompute the coefficient phase from the geometry instead of storing it;
+#            The path kernel recomputes the coefficient phase from the geometry instead of storing it;
 #            that recomputation is implementation overhead, already counted once in phase 1, and is
 #            not charged again.
 FLOP_PHASE1_PER_PAIR_R = 484
 FLOP_PHASE1_PER_ELIM_R = 610
 FLOP_PER_EVAL_TERM = 2
-FLOP_PER_CANDIDATE_R = 25
+FLOP_PER_CANDJOB = 25
 FLOP_PER_REFINED_R = 407
 FLOP_PER_ADMISSIBLE_R = 250
 
 
 # one-bounce refraction (T), same accounting: phase 1 per pair: decision 60 + setup 18 + a 75 + b (square
 # form, Eq. 9) 656 + normalise/truncate 55 + coplanarity test 16 = 880; per elimination: resultant by
-# pseudo-remainder 998 + Bernstein (degree 12) 260 = 1258; candidate 25 (back-substitution); refined
-# candidate 730 (b has 28 coefficients); admissible 300 (refraction Jacobian).
+# pseudo-remainder 998 + Bernstein (degree 12) 260 = 1258; refined candidate 730 (b has 28 coefficients);
+# admissible 300 (refraction Jacobian).
 FLOP_PHASE1_PER_PAIR_T = 880
 FLOP_PHASE1_PER_ELIM_T = 1258
-FLOP_PER_CANDIDATE_T = 25
 FLOP_PER_REFINED_T = 730
 FLOP_PER_ADMISSIBLE_T = 300
 
 
 def flop_model(chain, rep):
-    """{kernel: algorithmic FLOPs per solve}.  One bounce: phase 1, the root kernels (k1_roots + deep jobs)
-    and the path kernel; two bounces: the build + scan kernels, whose algorithmic kFLOP the kernels count
-    themselves (alg_kflop)."""
+    """{kernel: (algorithmic FLOPs per solve, report time key)}.  One bounce: phase 1 (incl. the monotone roots),
+    the deep-job kernel and the path kernel; two bounces: the build + scan kernels, whose algorithmic kFLOP the
+    kernels count themselves (alg_kflop)."""
     if len(chain) == 1:
         R = chain == "R"
-        p1 = rep["n_pairs_in"] * (FLOP_PHASE1_PER_PAIR_R if R else FLOP_PHASE1_PER_PAIR_T) + rep["n_elims"] * (
-            FLOP_PHASE1_PER_ELIM_R if R else FLOP_PHASE1_PER_ELIM_T)
-        roots = rep["n_eval_terms"] * FLOP_PER_EVAL_TERM
-        path = (rep["n_candidates"] * (FLOP_PER_CANDIDATE_R if R else FLOP_PER_CANDIDATE_T) +
-                rep["n_refined"] * (FLOP_PER_REFINED_R if R else FLOP_PER_REFINED_T) +
+        p1 = (rep["n_pairs_in"] * (FLOP_PHASE1_PER_PAIR_R if R else FLOP_PHASE1_PER_PAIR_T) +
+              rep["n_elims"] * (FLOP_PHASE1_PER_ELIM_R if R else FLOP_PHASE1_PER_ELIM_T) +
+              rep["n_eval_terms"] * FLOP_PER_EVAL_TERM + rep["n_cand_jobs"] * FLOP_PER_CANDJOB)
+        deep = rep["n_eval_deep"] * FLOP_PER_EVAL_TERM
+        path = (rep["n_refined"] * (FLOP_PER_REFINED_R if R else FLOP_PER_REFINED_T) +
                 rep["n_admissible"] * (FLOP_PER_ADMISSIBLE_R if R else FLOP_PER_ADMISSIBLE_T))
-        return {f"k1_phase1<{chain}>": (p1, "ms_phase1"), f"k1_roots<{chain}>": (roots, "ms_roots"),
+        return {f"k1_phase1<{chain}>": (p1, "ms_phase1"), f"k1_roots_deep<{chain}>": (deep, "ms_roots"),
                 f"k1_path<{chain}>": (path, "ms_path")}
     return {f"k2_solve<{chain}>": (rep["alg_kflop"] * 1e3, "ms_phase2")}
 
@@ -239,25 +241,31 @@ def main():
     from paper_2405_13409_b200 import spoly
     from paper_2405_13409_b200 import workloads as W
 
+    # one process per GPU; SPOLY_DIST_BACKEND=gloo + more ranks than GPUs is only a functional check of the plumbing
+    # (ranks sharing a GPU time-slice it), never a scaling measurement
+    local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("SPOLY_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
-    scaling = "weak"
+    scaling = "strong" if world > 1 else "weak"
     shard_idx = None
-    if args.config == "C2":
-        w = W.glints_c2(res=args.res or 256, seed_strata=2 + rank)  # weak scaling: one full frame per rank
-    else:
-        kw = {} if args.res is None else {"res": args.res}
-        w = W.CONFIGS[args.config](**kw)
-        if world > 1:
-            # strong scaling of one frame: query tiles round-robin over the ranks
-            from paper_2405_13409_b200 import dist as D
-            nq_full = w.nqueries
-            shard_idx = D.shard_tiles(nq_full, world, rank)
-            w = w.subset(shard_idx)
-            scaling = "strong"
+    kw = {} if args.res is None else {"res": args.res}
+    w = W.CONFIGS[args.config](**kw)
+    nq_full = w.nqueries
+    if world > 1:
+        # strong scaling of ONE frame: the frame's res x res query grid in 64 x 64 tiles, tile t ->
+        # rank t mod world; every rank uploads the whole mesh and solves its tiles; no collective inside the solve
+        from paper_2405_13409_b200 import dist as D
+        side = int(round(nq_full ** 0.5))
+        shard_idx = (D.shard_grid_tiles(side, side, world, rank) if side * side == nq_full
+                     else D.shard_tiles(nq_full, world, rank))
+        w = w.subset(shard_idx)
     chain = w.chain
     stream = torch.cuda.current_stream(dev)
     cfg = spoly.default_config() if args.cull_levels is None else spoly.default_config(cull_levels=args.cull_levels)
@@ -317,21 +325,19 @@ def main():
             e2e_paths += rr.n_solutions
         e2e = [e2e_paths, e2e_t]
 
-    # ---- cross-rank aggregation (NCCL): counters sum, time max; per-query sums gathered to every rank
+    # ---- cross-rank aggregation (NCCL): exact int64 counter sums, device time max (and mean: imbalance), per-query
+    # sums gathered back to frame order
+    rank_ms = None
     if world > 1:
-        t = torch.tensor([total_ms, e2e[1] if e2e else 0.0], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        c = torch.tensor([n_paths, n_pairs, launches, e2e[0] if e2e else 0], dtype=torch.float64, device=dev)
-        dist.all_reduce(c, op=dist.ReduceOp.SUM)
-        total_ms, e2e_max = float(t[0]), float(t[1])
-        n_paths, n_pairs, launches = int(c[0]), int(c[1]), int(c[2])
+        rank_ms = D.allreduce_max_mean(total_ms, dev)
+        total_ms = rank_ms[0]
+        cnt = D.allreduce_counters({"paths": n_paths, "pairs": n_pairs, "launches": launches,
+                                    "e2e_paths": e2e[0] if e2e else 0}, dev)
+        n_paths, n_pairs, launches = cnt["paths"], cnt["pairs"], cnt["launches"]
         if e2e:
-            e2e = [int(c[3]), e2e_max]
-        if shard_idx is None:
-            gathered = [torch.empty_like(r.per_query) for _ in range(world)]
-            dist.all_gather(gathered, r.per_query.contiguous())
-        else:  # ragged shards: padded gather + scatter back to query order
-            D.gather_per_query(r.per_query.contiguous(), shard_idx, nq_full)
+            e2e = [cnt["e2e_paths"], D.allreduce_max_mean(e2e[1], dev)[0]]
+        full_pq = D.gather_per_query(r.per_query.contiguous(), shard_idx, nq_full)
+        frame_sum = float(full_pq.sum())
 
     # ---- roofline of the dominant kernel, from its own launch's CUDA-event time (recorded by the library on
     # the launching stream around each solve kernel, averaged over the timed steps)
@@ -373,17 +379,19 @@ def main():
         "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "query_tuple_solves_per_s": n_pairs / (total_ms / 1e3),
         "config": {"workload": ("C2 glints: %d light samples x %d-tri normal-mapped bumpy plane, one-bounce R, "
-                                "cull pre-pass + fused FP64 solve + deterministic compaction" % (w.nqueries, w.mesh.ntris))
+                                "cull pre-pass + fused FP64 solve + deterministic compaction" % (nq_full, w.mesh.ntris))
                    if args.config == "C2" else "%s %s: %d queries x %d tris, chain %s, cull + solve + compaction" % (
-                       args.config, w.name, w.nqueries, w.mesh.ntris, chain),
+                       args.config, w.name, nq_full, w.mesh.ntris, chain),
                    "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": chain,
-                   "queries_total": w.nqueries * world if shard_idx is None else int(nq_full),
-                   "l2": "flushed between timed steps (256 MB write)", "parallelism": f"query-sharded x{world}"},
+                   "queries_total": int(nq_full),
+                   "l2": "flushed between timed steps (256 MB write)",
+                   "parallelism": ("one frame, 64x64 query tiles round-robin over %d ranks (strong scaling)" % world
+                                   if world > 1 else "single GPU")},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",
                                                  "n_jobs_mono", "n_jobs_deep", "n_eval_terms", "n_rebuilds", "n_elims",
                                                  "n_pairs_coarse", "n_refined", "n_cand_jobs", "n_path_jobs",
-                                                 "n_cull_tests")},
+                                                 "n_cull_tests", "n_eval_deep", "n_truncated", "n_big_scan")},
         "cull_tests_per_s": reports[-1]["n_cull_tests"] / (statistics.mean(x["ms_cull"] for x in reports) / 1e3)
         if reports[-1]["n_cull_tests"] else None,
         "phase_ms": {"cull": statistics.mean(x["ms_cull"] for x in reports), "solve": statistics.mean(solve_ms),
@@ -396,6 +404,11 @@ def main():
         "clocks": clocks,
         "gpu_launches": launches,
     }
+    if rank_ms is not None:
+        line["ranks"] = {"ms_max": rank_ms[0] / args.steps, "ms_mean": rank_ms[1] / args.steps,
+                         "imbalance": rank_ms[0] / rank_ms[1] if rank_ms[1] > 0 else None,
+                         "frame_per_query_sum": frame_sum,
+                         "note": "per-step device time of the slowest rank (max) and the mean over ranks"}
     if e2e:
         line["e2e"] = {"value": e2e[0] / e2e[1], "unit": UNIT, "h2d_bytes_per_step": int(w.endpoints.nbytes +
                                                                                          w.intensity.nbytes),

@@ -60,7 +60,7 @@ typedef struct {
   int scan_bisect_iters; /* k>=2 bisections per sign-changing piece; 10       */
   double bisect_tol;     /* k=1 root bracket threshold; 1e-9                  */
   int polish_iters;      /* Newton steps on the exact shooting residual (k=2); 5 (reading R23) */
-  double theta_admit;    /* raw-root residual gate before polish (k=2); 1e-3                 */
+  double theta_admit;    /* raw-root residual gate before polish (k=2); 3e-2 (reading R24)   */
   double theta_final;    /* final Eq. 3 residual gate; 1e-6 (north_star)                     */
   double eps_domain;     /* barycentric slack of the inside test; 1e-9                       */
   double eps_flag;       /* near-tangent / boundary flag distance; 1e-6                      */
@@ -113,25 +113,26 @@ typedef struct {
       n_rej_kappa, n_flagged, n_admissible;
   float ms_cull, ms_solve, ms_reduce; /* CUDA-event times of the phases of the last solve       */
   uint32_t n_launches;                /* kernels this library launched in the last solve        */
-  uint64_t n_eval_terms;              /* FMA terms of the univariate root-finding evaluations
-                                         (input of the algorithmic FLOP model)     */
+  uint64_t n_eval_terms;              /* FMA terms of the univariate root-finding evaluations of the
+                                         monotone jobs in phase 1 (FLOP model)      */
   uint64_t required_solutions;        /* set with SPOLY_ERR_CAPACITY                            */
   float ms_phase1, ms_phase2;         /* CUDA-event times of the two solve kernels (phase 2 incl.
                                          the count read-back)                                    */
   uint64_t n_rebuilds;                /* phase-2 coefficient-phase recomputations (FLOP model)   */
   uint64_t alg_kflop;                 /* two-bounce kernel: algorithmic kFLOP (coefficient phase +
                                          determinant evaluations)                   */
-  uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce phase-2 jobs: monotone r / deeper recursion   */
+  uint64_t n_jobs_mono, n_jobs_deep;  /* one-bounce jobs: monotone r with a root in [0,1] (solved in
+                                         phase 1) / deeper derivative recursion (deep-job kernel)  */
   uint64_t n_elims;                   /* one-bounce pairs that reached the elimination phase       */
   uint64_t n_pairs_coarse;            /* pairs kept before the last exact filter: two-bounce pair cull
                                          before the subdivision refinement; one-bounce R before the
                                          product-form sign test (n_pairs_in counts the final list)   */
-  float ms_roots, ms_path;            /* one-bounce phase 2 split: root finding (k1_roots + deep
-                                         jobs) and path kernels (incl. the count read-back)         */
+  float ms_roots, ms_path;            /* one-bounce phase 2 split: deep-job root isolation and the
+                                         path kernel (incl. the count read-back)                    */
   uint64_t n_refined;                 /* one-bounce candidates past the domain pre-check (refined,
                                          reading R2; FLOP model)                                     */
-  uint64_t n_cand_jobs, n_path_jobs;  /* one-bounce monotone jobs with a root seen by the candidate
-                                         pre-pass / jobs the path kernel ran (pre-pass list + deep)  */
+  uint64_t n_cand_jobs, n_path_jobs;  /* one-bounce monotone jobs with a root (back-substitution
+                                         pre-check in phase 1) / jobs the path kernel ran           */
   uint64_t n_cull_tests;              /* cull work of the last solve: one bounce, triangle tests of the
                                          per-query cull; two bounces, node-pair tests of the pair
                                          expansion + sub-pair tests of the subdivision refinement    */
@@ -139,6 +140,8 @@ typedef struct {
                                          tuple carries SPOLY_FLAG_TRUNCATED)                          */
   uint64_t n_big_scan;                /* two bounces: tuples whose Bezout order n > 32 took the
                                          shared-memory determinant                                    */
+  uint64_t n_eval_deep;               /* one bounce: FMA terms of the deep jobs' root isolation (the
+                                         monotone jobs' Newton terms are in n_eval_terms)              */
 } spoly_report;
 
 typedef struct {

@@ -64,6 +64,9 @@ def lib():
             L.orc_get_flagged.argtypes = [P] * 4
             L.orc_get_per_query.argtypes = [P, P]
             L.orc_get_report.argtypes = [P, P]
+            L.orc_n_worklist.restype = ctypes.c_uint64
+            L.orc_n_worklist.argtypes = [P]
+            L.orc_get_worklist.argtypes = [P, P, P]
             L.orc_default_config.argtypes = [P]
             L.orc_build_system.argtypes = [ctypes.c_char_p, P, P, P, ctypes.c_double, ctypes.c_double, P, P, P, P,
                                            P, P]
@@ -156,10 +159,16 @@ def solve(mesh, chain: str, endpoints: np.ndarray, intensity=None, offsets=None,
         L.orc_get_per_query(h, _p(pq))
         rep = np.zeros(10, np.uint64)
         L.orc_get_report(h, _p(rep))
+        nw = L.orc_n_worklist(h)
+        wq = np.zeros(nw, np.uint32)
+        wt = np.zeros(nw * k, np.uint32)
+        L.orc_get_worklist(h, _p(wq), _p(wt))
     finally:
         L.orc_free(h)
-    return Result(k, q, t.reshape(n, k), b.reshape(n, 2 * k), c, r, f, fq, ft.reshape(m, k), ff, pq,
-                  dict(zip(REPORT_KEYS, (int(x) for x in rep))))
+    res = Result(k, q, t.reshape(n, k), b.reshape(n, 2 * k), c, r, f, fq, ft.reshape(m, k), ff, pq,
+                 dict(zip(REPORT_KEYS, (int(x) for x in rep))))
+    res.worklist = (wq, wt.reshape(nw, k))  # the (query, tuple) pairs the oracle solved (after its cull)
+    return res
 
 
 def tri_block(mesh, ids) -> np.ndarray:

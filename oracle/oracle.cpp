@@ -1136,7 +1136,7 @@ using namespace oracle;
 struct orc_result {
   int k = 1;
   uint32_t nq = 0;
-  vector<uint32_t> q, tup, flags, fq, ftup, fflags;
+  vector<uint32_t> q, tup, flags, fq, ftup, fflags, wq, wtup;
   vector<double> bary, contrib, resid, per_query;
   uint64_t counters[10] = {0};
 };
@@ -1189,7 +1189,7 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
   else
     orc_default_config(&cfg);
   struct PerQ {
-    vector<uint32_t> tup, ftup, fflags;
+    vector<uint32_t> tup, ftup, fflags, wl;  // wl: the tuples this query solved (after the cull), k ids each
     vector<Sol> sols;
     Counters C;
     double sum = 0;
@@ -1205,6 +1205,7 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
       double I = intensity ? intensity[qi] : 1.0;
       auto run = [&](const uint32_t* ids) {
         vector<Tri> tris = mesh_tris(pos, nrm, tri, ids, k);
+        for (int i = 0; i < k; ++i) P.wl.push_back(ids[i]);
         TupleResult R = solve_tuple(chain, tris, x0, xk1, eta_front, eta_back, I, cfg, P.C);
         for (const Sol& s : R.sols) {
           P.sols.push_back(s);
@@ -1265,6 +1266,10 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
       for (int i = 0; i < k; ++i) R->ftup.push_back(P.ftup[f * k + i]);
       R->fflags.push_back(P.fflags[f]);
     }
+    for (size_t t = 0; t < P.wl.size() / k; ++t) {
+      R->wq.push_back(qi);
+      for (int i = 0; i < k; ++i) R->wtup.push_back(P.wl[t * k + i]);
+    }
     R->per_query[qi] = P.sum;
     for (int c = 0; c < 10; ++c) R->counters[c] += P.C.c[c];
   }
@@ -1288,6 +1293,11 @@ void orc_get_flagged(const orc_result* r, uint32_t* query, uint32_t* tuple, uint
   std::copy(r->fq.begin(), r->fq.end(), query);
   std::copy(r->ftup.begin(), r->ftup.end(), tuple);
   std::copy(r->fflags.begin(), r->fflags.end(), flags);
+}
+uint64_t orc_n_worklist(const orc_result* r) { return r->wq.size(); }
+void orc_get_worklist(const orc_result* r, uint32_t* query, uint32_t* tuple) {
+  std::copy(r->wq.begin(), r->wq.end(), query);
+  std::copy(r->wtup.begin(), r->wtup.end(), tuple);
 }
 void orc_get_per_query(const orc_result* r, double* out) { std::copy(r->per_query.begin(), r->per_query.end(), out); }
 void orc_get_report(const orc_result* r, uint64_t c[10]) { std::copy(r->counters, r->counters + 10, c); }

@@ -61,6 +61,9 @@ void orc_get_solutions(const orc_result*, uint32_t* query, uint32_t* tuple, doub
 /* flagged tuples: query[m], tuple[m*k], flags[m] */
 void orc_get_flagged(const orc_result*, uint32_t* query, uint32_t* tuple, uint32_t* flags);
 void orc_get_per_query(const orc_result*, double* per_query /* Q */);
+/* the (query, tuple) pairs the oracle solved (after its cull): query[n], tuple[n*k] */
+uint64_t orc_n_worklist(const orc_result*);
+void orc_get_worklist(const orc_result*, uint32_t* query, uint32_t* tuple);
 /* counters: pairs_in, systems, vroots, candidates, rej_domain, rej_constraint, rej_side,
  *           rej_kappa, flagged, admissible */
 void orc_get_report(const orc_result*, uint64_t counters[10]);

@@ -98,7 +98,7 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_qrange;  // per-query [begin, end) in the sorted solution list
   DBuf<uint32_t> d_pcnt;             // counting order: per-pair counts, then their exclusive scan
   DBuf<uint32_t> d_fflags, d_fflags2, d_uflags, d_perm_in, d_perm_out, d_jpair, d_jmeta;
-  DBuf<double> d_bary, d_contrib, d_jr, d_jroot, d_jA;
+  DBuf<double> d_bary, d_contrib, d_jr, d_jroot;
   DBuf<float> d_resid;
   // sorted output
   DBuf<uint32_t> o_query, o_tuple, o_flags, o_fquery, o_ftuple, o_fflags;
@@ -136,7 +136,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->scan_bisect_iters = 10;
   c->bisect_tol = 1e-9;
   c->polish_iters = 5;
-  c->theta_admit = 1e-3;
+  c->theta_admit = 3e-2;
   c->theta_final = 1e-6;
   c->eps_domain = 1e-9;
   c->eps_flag = 1e-6;
@@ -195,7 +195,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_count.release(); ctx->d_counters.release(); ctx->d_key.release(); ctx->d_key2.release();
   ctx->d_fkey.release(); ctx->d_fkey2.release(); ctx->d_upair.release(); ctx->d_nruns.release();
   ctx->d_fflags.release(); ctx->d_fflags2.release(); ctx->d_uflags.release(); ctx->d_perm_in.release();
-  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release(); ctx->d_jA.release();
+  ctx->d_perm_out.release(); ctx->d_jpair.release(); ctx->d_jmeta.release(); ctx->d_jr.release(); ctx->d_jroot.release();
   ctx->d_bary.release(); ctx->d_contrib.release(); ctx->d_resid.release();
   ctx->d_pmask.release(); ctx->d_pcnt.release(); ctx->d_qrange.release();
   ctx->o_query.release(); ctx->o_tuple.release(); ctx->o_flags.release(); ctx->o_fquery.release();
@@ -641,7 +641,6 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(ctx->d_jmeta.ensure(k == 1 ? npairs : 1));
   CK(ctx->d_jr.ensure(k == 1 ? npairs * kJobStride : kJobStride));
   CK(ctx->d_jroot.ensure(k == 1 ? npairs : 1));
-  CK(ctx->d_jA.ensure(k == 1 ? npairs * 6 : 6));
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   for (int attempt = 0; attempt < 2; ++attempt) {
     CK(cudaMemsetAsync(ctx->d_count.p, 0, 6 * sizeof(unsigned long long), st));
@@ -649,13 +648,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     SolSink S = raw_sink(ctx);
     JobSink J;
     J.count = ctx->d_count.p + 2;
-    J.capacity = std::min({ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride, ctx->d_jroot.cap, ctx->d_jA.cap / 6});
+    J.capacity = std::min({ctx->d_jpair.cap, ctx->d_jr.cap / kJobStride, ctx->d_jroot.cap});
     J.pair = ctx->d_jpair.p;
     J.meta = ctx->d_jmeta.p;
     J.r = ctx->d_jr.p;
-    J.lcount = ctx->d_count.p + 4;
     J.root = ctx->d_jroot.p;
-    J.A = ctx->d_jA.p;
     CK(cudaEventRecord(ctx->ev[4], st));
     if (k == 1) {
       launch_solve_k1(1, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
@@ -666,7 +663,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       CK(cudaEventRecord(ctx->ev[6], st));
       launch_solve_k1(3, chain[0] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten, prm, S, J,
                       ctx->nsm, st);
-      ctx->launches += 5;
+      ctx->launches += 4;
     } else {
       CK(cudaEventRecord(ctx->ev[5], st));
       {
@@ -853,13 +850,14 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.alg_kflop = counters[C_KFLOP];
   R.n_elims = counters[C_ELIMS];
   R.n_pairs_coarse = ctx->npairs_culled;
-  R.n_jobs_mono = cnt[2];
+  R.n_jobs_mono = counters[C_CAND_JOBS];
   R.n_jobs_deep = cnt[3];
   R.n_launches = ctx->launches;
   R.n_eval_terms = counters[C_EVAL_TERMS];
   R.n_refined = counters[C_REFINED];
   R.n_cand_jobs = counters[C_CAND_JOBS];
-  R.n_path_jobs = cnt[4];
+  R.n_path_jobs = cnt[2] + cnt[3];
+  R.n_eval_deep = counters[C_EVAL_DEEP];
   R.n_cull_tests = ctx->cull_tests;
   R.n_truncated = counters[C_TRUNCATED];
   R.n_big_scan = counters[C_BIG_SCAN];

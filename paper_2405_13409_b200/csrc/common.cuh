@@ -113,19 +113,19 @@ struct SolSink {
   unsigned long long* counters;  // [C_NUM]
 };
 constexpr int kJobStride = 13;  // max doubles per job (r(v) up to degree 12; R uses 10)
-// dense job list between the two solve phases
+// two-ended dense list between the one-bounce kernels: [0, count[0]) path entries (pair, root) of the monotone
+// jobs phase 1 solved and could not finish; (capacity - 1 - d) for d < count[1]: deep jobs (pair, meta, r)
 struct JobSink {
   unsigned long long* count;
   uint64_t capacity;
   uint32_t* pair;
-  uint32_t* meta;  // kfree | deg << 8
-  double* r;       // NR (coefficients of r) per job; deep jobs: phase 2 overwrites it with [count, roots...]
-  double* root;    // per job: the root of a monotone job kept for the path kernel (NaN: none / finished)
-  double* A;       // per monotone job: phase 1's normalised a (6 coefficients: u^0 v^0..2, u v^0..1, u^2)
-  unsigned long long* lcount;  // path-phase job list length (candidate pre-pass output)
+  uint32_t* meta;  // deep jobs: kfree | deg << 8
+  double* r;       // deep jobs: NR coefficients of r; the deep kernel overwrites them with [nv | np << 8, roots, probes]
+  double* root;    // path entries: the v-root
 };
 
 enum { C_PAIRS = 0, C_SYSTEMS, C_VROOTS, C_CANDIDATES, C_REJ_DOMAIN, C_REJ_CONSTRAINT, C_REJ_SIDE, C_REJ_KAPPA,
-       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_REFINED, C_CAND_JOBS, C_TRUNCATED, C_BIG_SCAN, C_NUM };
+       C_FLAGGED, C_ADMISSIBLE, C_EVAL_TERMS, C_REBUILDS, C_KFLOP, C_ELIMS, C_REFINED, C_CAND_JOBS, C_TRUNCATED, C_BIG_SCAN,
+       C_EVAL_DEEP, C_NUM };
 
 }  // namespace spoly

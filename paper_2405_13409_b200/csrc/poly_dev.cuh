@@ -141,13 +141,17 @@ __device__ __forceinline__ void bslices_at(const double* G, double v, double* ou
 // 1e-9 bracket threshold, so the roots agree with the oracle's to well inside the parity tolerance.
 // Also returns, for the top level (p itself), the critical points' |p| and max_[lo,hi] |p| for the
 // near-tangent flag.
-template <int N>
+template <int N, bool PROBES = false>
 struct RootSet {
   double x[N];
   int n;
   double min_crit_ratio;  // min over critical points c in (lo,hi) of |p(c)| / max|p| (1 if none)
   int flags;              // 1: roots closer than eps
   uint32_t terms;         // FMA terms evaluated (FLOP model)
+  // PROBES: positions of the c14 near-tangency conditions (reading R11): midpoints of root pairs closer than eps,
+  // critical points c with |p(c)| <= 1e-10 max_[lo,hi] |p|
+  double probe[PROBES ? 2 * N : 1];
+  int nprobe;
 };
 
 // falling factorials F[k][i] = i!/(i-k)! (0 for i < k), for the derivative levels p^(k)
@@ -285,13 +289,15 @@ __device__ __forceinline__ int monotone_root(const double* c, double lo, double 
 // kstart: a derivative level known to have no root in (lo, hi) (so p^(kstart-1) is monotone there and
 // the recursion starts at level kstart-1 with no critical points); kstart < 0 or >= deg-1 runs the plain
 // recursion from the linear level deg-1.
-template <int N>
-__device__ void isolate_roots(const double* c, int deg, double lo, double hi, double eps_close, RootSet<N>& R,
+template <int N, bool PROBES = false>
+__device__ void isolate_roots(const double* c, int deg, double lo, double hi, double eps_close, RootSet<N, PROBES>& R,
                               int kstart = -1) {
   R.terms = 0;
   R.n = 0;
   R.min_crit_ratio = 1.0;
   R.flags = 0;
+  R.nprobe = 0;
+  double fc[PROBES ? N : 1];  // |p| at the critical points (PROBES)
   if (deg <= 0) return;
   double prev[N];
   int nprev = 0;
@@ -329,7 +335,10 @@ __device__ void isolate_roots(const double* c, int deg, double lo, double hi, do
       double fb = level_eval<N>(g, h, k, deg, xb, &dummy);
       if (k == 0) {
         fmax_ = fmax(fmax_, fabs(fb));
-        if (i < nprev) cmin = fmin(cmin, fabs(fb));
+        if (i < nprev) {
+          cmin = fmin(cmin, fabs(fb));
+          if (PROBES) fc[i] = fabs(fb);
+        }
       }
       if (fa == 0.0) {
         cur[ncur++] = xa;
@@ -345,10 +354,16 @@ __device__ void isolate_roots(const double* c, int deg, double lo, double hi, do
     if (k == 0) {
       if (nprev > 0 && fmax_ > 0) R.min_crit_ratio = cmin / fmax_;
       for (int i = 0; i < ncur; ++i) {
-        if (i > 0 && cur[i] - cur[i - 1] < eps_close) R.flags |= 1;
+        if (i > 0 && cur[i] - cur[i - 1] < eps_close) {
+          R.flags |= 1;
+          if (PROBES) R.probe[R.nprobe++] = 0.5 * (cur[i] + cur[i - 1]);
+        }
         R.x[i] = cur[i];
       }
       R.n = ncur;
+      if (PROBES)
+        for (int i = 0; i < nprev; ++i)
+          if (fc[i] <= 1e-10 * fmax_) R.probe[R.nprobe++] = prev[i];
       return;
     }
     nprev = 0;

@@ -164,6 +164,43 @@ __device__ __forceinline__ void load_pair(const uint32_t* __restrict__ pq, const
   x2 = mk3(__ldg(e + 3), __ldg(e + 4), __ldg(e + 5));
 }
 
+// real roots u of a(., v*) when a is quadratic / linear in u (stable formula, disc clamp; reading R4),
+// sorted, merged below 1e-7.  |disc| <= 1e-8 scale (two u-roots about to merge, c14) reports the double root's
+// position in *udouble (a near-tangency condition probed by the path kernel, reading R11), else NaN.
+__device__ __forceinline__ int quadratic_u_roots(const double al[3], double* ua, double* udouble) {
+  int nu = 0;
+  *udouble = __longlong_as_double(0x7ff8000000000000ll);
+  if (al[2] != 0.0) {
+    const double a0 = al[0], a1 = al[1], a2 = al[2];
+    double disc = a1 * a1 - 4.0 * a2 * a0;
+    const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
+    if (fabs(disc) <= 1e-8 * sc) *udouble = -a1 / (2.0 * a2);
+    if (!(disc < -1e-12 * sc)) {
+      if (disc < 0) disc = 0;
+      const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+      if (qq == 0.0) {
+        ua[nu++] = 0.0;
+      } else {
+        double r1 = qq / a2, r2 = a0 / qq;
+        if (r1 > r2) {
+          const double t = r1;
+          r1 = r2;
+          r2 = t;
+        }
+        ua[nu++] = r1;
+        if (r2 - r1 >= 1e-7) ua[nu++] = r2;
+      }
+    }
+  } else if (al[1] != 0.0) {
+    ua[nu++] = -al[0] / al[1];
+  }
+  return nu;
+}
+
+// the refinement (reading R2) moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than
+// 3e-3 outside the simplex can neither become admissible nor land within eps_flag of an edge
+__device__ __forceinline__ bool precheck_reject(double us, double vv) { return fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3; }
+
 // ---------------------------------------------------------------------------------------------
 #ifndef SPOLY_P1_MINB
 #define SPOLY_P1_MINB 4
@@ -211,9 +248,7 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
         // a(u,v) = Eq. 6 has a strict sign on the triangle (enlarged far beyond the 1e-9 domain slack), so
         // no chain exists on this pair: exact early out (no effect on the admissible set)
         ok = false;
-        cnt[C_EVAL_TERMS] += 8;
       } else if (ok) {
-        cnt[C_EVAL_TERMS] += 8;
         cnt[C_ELIMS]++;
         s_aj[0][threadIdx.x] = Sys.A[0]; s_aj[1][threadIdx.x] = Sys.A[1]; s_aj[2][threadIdx.x] = Sys.A[2];
         s_aj[3][threadIdx.x] = Sys.A[3]; s_aj[4][threadIdx.x] = Sys.A[4]; s_aj[5][threadIdx.x] = Sys.A[6];
@@ -231,7 +266,6 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
             r[t] *= inv;
             if (r[t] != 0.0) deg = t;
           }
-          cnt[C_EVAL_TERMS] += NR * (NR + 1) / 2 + NR * (NR - 1) / 4;  // Bernstein + differences
           const int kfree = bernstein_root_free_level<NR>(r);
           // kfree == 1: r is monotone on [0,1], so it has a root there iff r(0) and r(1) differ in sign
           // (or one vanishes) -- exact, and it keeps root-free monotone pairs out of the job list
@@ -246,11 +280,92 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
         }
       }
     }
-    emit_flag(active && flags != 0, flags, i, S);
-    // two-ended dense job list: monotone jobs (kfree == 1) from the front, deeper recursions from the back,
-    // so that phase-2 warps see one job class
+    // ---- monotone jobs (kfree == 1, ~99% of the jobs): the root of r on [0, 1] by the safeguarded Newton
+    // iteration of the derivative recursion's monotone piece (reading R13), then the back-substitution
+    // pre-check (reading R2's 1e-3 refinement radius): a job whose every candidate lies > 3e-3 outside the triangle
+    // and that raises no c14 condition is finished here.  Only (pair, root) of the survivors leaves the kernel
+    // (12 B instead of the 128 B job record of round 1).  Lanes iterate independently (3.1 steps on average).
     const bool mono = job && (meta & 0xFF) == 1;
-    const unsigned mb = __ballot_sync(0xffffffffu, mono);
+    bool to_path = false, complex_job = false;
+    double root = 0.0;
+    if (mono) {
+      double f1 = 0.0;
+#pragma unroll
+      for (int t = NR - 1; t >= 0; --t) f1 += r[t];  // r(1)
+      const double f0 = r[0];
+      cnt[C_EVAL_TERMS] += 2 * NR;
+      bool has = true;
+      if (f0 == 0.0 || f1 == 0.0) {
+        root = f0 == 0.0 ? 0.0 : 1.0;  // exact endpoint root
+      } else if ((f0 < 0.0) == (f1 < 0.0)) {
+        has = false;  // rounding: no sign change after all
+      } else {
+        double a = 0.0, b = 1.0, x = -f0 / (f1 - f0);  // secant start
+        if (!(x > a && x < b)) x = 0.5;
+        for (int it = 0; it < 100; ++it) {
+          double f = r[NR - 1], fp = 0.0;
+#pragma unroll
+          for (int t = NR - 2; t >= 0; --t) {
+            fp = fma(fp, x, f);
+            f = fma(f, x, r[t]);
+          }
+          cnt[C_EVAL_TERMS] += 2 * NR - 1;
+          if (f == 0.0) break;
+          if ((f < 0.0) == (f0 < 0.0))
+            a = x;
+          else
+            b = x;
+          double xn = x - f * fast_rcp(fp);
+          // convergence is tested before the bracket safeguard: at the root the Newton step is below an ulp and may
+          // land on the endpoint x just became, which must not trigger a bisection from a far bracket
+          const bool conv = fabs(xn - x) <= 1e-12;
+          if (conv)
+            xn = fmin(fmax(xn, a), b);
+          else if (!(xn > a && xn < b))
+            xn = 0.5 * (a + b);
+          x = xn;
+          if (conv || b - a <= 1e-15) break;
+        }
+        root = x;
+      }
+      if (has) {
+        cnt[C_VROOTS]++;
+        cnt[C_CAND_JOBS]++;
+        // back-substitution in a (phase 1's normalised coefficients, parked in shared memory) + domain pre-check
+        double A[9];
+        A[0] = s_aj[0][threadIdx.x]; A[1] = s_aj[1][threadIdx.x]; A[2] = s_aj[2][threadIdx.x];
+        A[3] = s_aj[3][threadIdx.x]; A[4] = s_aj[4][threadIdx.x]; A[6] = s_aj[5][threadIdx.x];
+        A[5] = A[7] = A[8] = 0.0;
+        double al[3];
+        bslices_at<2, 3>(A, root, al);
+        const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+        if (!(amax >= 1e-12)) {
+          complex_job = true;  // a(., v*) == 0: the b fallback runs in the general path kernel
+        } else {
+          uint32_t nc = 0, nrej = 0;
+          double ua[2], ud;
+          const int nu = quadratic_u_roots(al, ua, &ud);
+          for (int iu = 0; iu < nu; ++iu) {
+            ++nc;
+            if (precheck_reject(ua[iu], root))
+              ++nrej;
+            else
+              to_path = true;
+          }
+          if (!isnan(ud)) complex_job = true;  // a near-double u-root: the general path kernel probes it (R11)
+          if (complex_job)
+            to_path = false;
+          if (!to_path && !complex_job) {
+            cnt[C_CANDIDATES] += nc;
+            cnt[C_REJ_DOMAIN] += nrej;
+          }
+        }
+      }
+    }
+    emit_flag(active && flags != 0, flags, i, S);
+    // two-ended dense list: path entries (pair, root) from the front, block-aggregated (one atomic per 128 pairs;
+    // same-address atomics serialise in L2); deeper recursions (pair, meta, r) from the back
+    const unsigned mb = __ballot_sync(0xffffffffu, to_path);
     if (lane == 0) s_off[warp] = __popc(mb);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -266,10 +381,17 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
     __syncthreads();
     const uint32_t ex1 = s_off[warp] + __popc(mb & ((1u << lane) - 1u));
     const unsigned long long b1 = s_base;
+    // deep list: deeper recursions, and the rare monotone jobs whose back-substitution needs the b fallback or
+    // a c14 probe (the deep kernel re-isolates their single root; the general path kernel finishes them)
+    const bool deep = job && (!mono || complex_job);
     uint32_t ex2;
-    const unsigned long long b2 = warp_alloc(J.count + 1, (job && !mono) ? 1u : 0u, &ex2);
-    if (job && (mono ? b1 + ex1 : b2 + ex2) < J.capacity) {
-      const unsigned long long p = mono ? b1 + ex1 : J.capacity - 1 - (b2 + ex2);
+    const unsigned long long b2 = warp_alloc(J.count + 1, deep ? 1u : 0u, &ex2);
+    if (to_path && b1 + ex1 < J.capacity) {
+      J.pair[b1 + ex1] = (uint32_t)i;
+      J.root[b1 + ex1] = root;
+    }
+    if (deep && b2 + ex2 < J.capacity) {
+      const unsigned long long p = J.capacity - 1 - (b2 + ex2);
       J.pair[p] = (uint32_t)i;
       J.meta[p] = meta;
       if (NR % 2 == 0) {  // R: 80 B per job, 16-byte aligned
@@ -280,98 +402,107 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
 #pragma unroll
         for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
       }
-      if (mono) {  // 48 B per job, 16-byte aligned: three vector stores
-        double2* a2 = reinterpret_cast<double2*>(J.A + p * 6);
-        a2[0] = make_double2(s_aj[0][threadIdx.x], s_aj[1][threadIdx.x]);
-        a2[1] = make_double2(s_aj[2][threadIdx.x], s_aj[3][threadIdx.x]);
-        a2[2] = make_double2(s_aj[4][threadIdx.x], s_aj[5][threadIdx.x]);
-      }
     }
   }
   flush_counters(S, cnt);
 }
 
-// real roots u of a(., v*) when a is quadratic / linear in u (stable formula, disc clamp; reading R4),
-// sorted, merged below 1e-7
-__device__ __forceinline__ int quadratic_u_roots(const double al[3], double* ua, uint32_t* flags) {
-  int nu = 0;
-  if (al[2] != 0.0) {
-    const double a0 = al[0], a1 = al[1], a2 = al[2];
-    double disc = a1 * a1 - 4.0 * a2 * a0;
-    const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
-    if (fabs(disc) <= 1e-8 * sc) *flags |= SPOLY_FLAG_NEAR_TANGENT;
-    if (!(disc < -1e-12 * sc)) {
-      if (disc < 0) disc = 0;
-      const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
-      if (qq == 0.0) {
-        ua[nu++] = 0.0;
-      } else {
-        double r1 = qq / a2, r2 = a0 / qq;
-        if (r1 > r2) {
-          const double t = r1;
-          r1 = r2;
-          r2 = t;
-        }
-        ua[nu++] = r1;
-        if (r2 - r1 >= 1e-7) ua[nu++] = r2;
-      }
-    }
-  } else if (al[1] != 0.0) {
-    ua[nu++] = -al[0] / al[1];
+// reading R2: <= 3 Newton steps on (a, b) from (us, vv), keeping a step only if |F| decreases and the candidate
+// stays within 1e-3 of (u0, v0) (local refinement, never a search); returns the final partial derivatives
+template <bool TC>
+__device__ __forceinline__ void refine_ab(const double* A, const double* B, double u0, double v0, double& us,
+                                          double& vv, double& fau, double& fav, double& fbu, double& fbv) {
+  constexpr int DB = Sys1<TC>::DB;
+  double fa, fb;
+  beval<2, 3>(A, us, vv, &fa, &fau, &fav);
+  beval<DB, DB + 1>(B, us, vv, &fb, &fbu, &fbv);
+  for (int it = 0; it < 3; ++it) {
+    const double det = fau * fbv - fav * fbu;
+    if (det == 0.0) break;
+    const double idet = 1.0 / det;
+    const double du = -(fbv * fa - fav * fb) * idet, dv = -(-fbu * fa + fau * fb) * idet;
+    // a step below 1e-15 cannot change the double-precision candidate: converged
+    if (fmax(fabs(du), fabs(dv)) <= 1e-15 * fmax(1.0, fmax(fabs(us), fabs(vv)))) break;
+    if (!(fmax(fabs(us + du - u0), fabs(vv + dv - v0)) <= 1e-3)) break;
+    double na, nau, nav, nb, nbu, nbv;
+    beval<2, 3>(A, us + du, vv + dv, &na, &nau, &nav);
+    beval<DB, DB + 1>(B, us + du, vv + dv, &nb, &nbu, &nbv);
+    if (!(na * na + nb * nb < fa * fa + fb * fb)) break;
+    us += du;
+    vv += dv;
+    fa = na; fau = nau; fav = nav;
+    fb = nb; fbu = nbu; fbv = nbv;
   }
-  return nu;
 }
 
-// the refinement (reading R2) moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than
-// 3e-3 outside the simplex can neither become admissible nor land within eps_flag of an edge
-__device__ __forceinline__ bool precheck_reject(double us, double vv) { return fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3; }
+// c14 probe (reading R11): does the near-tangency condition at (u0, v0) sit at an (almost) admissible chain?  The
+// candidate is refined like a root, then must lie within kProbeDomain of the triangle with Eq. 3 residual below
+// theta_final.  Ghost double roots (the square form's P = Q = 0 points) fail it and raise no flag.
+constexpr double kProbeDomain = 1e-3;
+template <bool TC>
+__device__ __forceinline__ bool probe_admissible(d3 x0, d3 x2, const d3 P_in[3], const d3 N_in[3],
+                                                 const SolveParams& prm, const Sys1<TC>& Sys, double u0, double v0) {
+  double us = u0, vv = v0, fau, fav, fbu, fbv;
+  refine_ab<TC>(Sys.A, Sys.B, u0, v0, us, vv, fau, fav, fbu, fbv);
+  const double ur = Sys.relabel ? vv : us, vr_ = Sys.relabel ? us : vv;
+  if (!(ur >= -kProbeDomain && vr_ >= -kProbeDomain && ur + vr_ <= 1.0 + kProbeDomain)) return false;
+  const d3 x1 = P_in[0] + ur * (P_in[1] - P_in[0]) + vr_ * (P_in[2] - P_in[0]);
+  const d3 nx = N_in[0] + ur * (N_in[1] - N_in[0]) + vr_ * (N_in[2] - N_in[0]);
+  return vertex_residual(x0, x1, x2, nx, Sys.eta0, Sys.eta1) < prm.theta_final;
+}
+
+// candidates u of the back-substitution at v (a(., v); b(., v) when a(., v) == 0, c11), at most 4
+template <bool TC>
+__device__ __forceinline__ int back_substitute(const Sys1<TC>& Sys, double vs, double* ua, double* udouble,
+                                               uint32_t* flags, uint32_t* cnt) {
+  constexpr int DB = Sys1<TC>::DB;
+  double al[3];
+  bslices_at<2, 3>(Sys.A, vs, al);
+  *udouble = __longlong_as_double(0x7ff8000000000000ll);
+  const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+  if (amax >= 1e-12) return quadratic_u_roots(al, ua, udouble);
+  // fallback (c11): a(., v*) == 0 -> roots of b(., v*) on [-0.1, 1.1]
+  double bl[DB + 1];
+  bslices_at<DB, DB + 1>(Sys.B, vs, bl);
+  double bmax = 0.0;
+  int bd = 0;
+#pragma unroll
+  for (int i = 0; i <= DB; ++i) {
+    bmax = fmax(bmax, fabs(bl[i]));
+    if (bl[i] != 0.0) bd = i;
+  }
+  if (!(bmax >= 1e-12)) {
+    *flags |= SPOLY_FLAG_DEGENERATE;
+    return 0;
+  }
+  RootSet<DB + 1> Rb;
+  isolate_roots<DB + 1>(bl, bd, -0.1, 1.1, 1e-7, Rb);
+  int nu = 0;
+  for (int i = 0; i < Rb.n; ++i)
+    if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) {
+      if (nu < 4) {
+        ua[nu++] = Rb.x[i];
+      } else {  // slot capacity (4 u-roots per v-root): flagged, never silent
+        *flags |= SPOLY_FLAG_TRUNCATED;
+        cnt[C_TRUNCATED]++;
+      }
+    }
+  return nu;
+}
 
 // ---------------------------------------------------------------------------------------------
 template <bool TC>
 __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], const d3 N_in[3],
-                           const SolveParams& prm, const Sys1<TC>& Sys, const double* vr, int nv, PairOut& out,
-                           uint32_t* cnt) {
-  constexpr int DB = Sys1<TC>::DB;
+                           const SolveParams& prm, const Sys1<TC>& Sys, const double* vr, int nv, const double* vp,
+                           int np, PairOut& out, uint32_t* cnt) {
   const d3 e1o = P_in[1] - P_in[0], e2o = P_in[2] - P_in[0];
   const d3 g_geo = cross(e1o, e2o);
-  const double* A = Sys.A;
-  const double* B = Sys.B;
+  bool tangent = false;  // a probed near-tangency condition sits at an admissible chain (NEAR_TANGENT)
   for (int iv = 0; iv < nv; ++iv) {
     const double vs = vr[iv];
-    double al[3];
-    bslices_at<2, 3>(A, vs, al);
-    double ua[4];
-    int nu = 0;
-    const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
-    if (amax >= 1e-12) {
-      nu = quadratic_u_roots(al, ua, &out.flags);
-    } else {
-      // fallback (c11): a(., v*) == 0 -> roots of b(., v*) on [-0.1, 1.1]
-      double bl[DB + 1];
-      bslices_at<DB, DB + 1>(B, vs, bl);
-      double bmax = 0.0;
-      int bd = 0;
-#pragma unroll
-      for (int i = 0; i <= DB; ++i) {
-        bmax = fmax(bmax, fabs(bl[i]));
-        if (bl[i] != 0.0) bd = i;
-      }
-      if (!(bmax >= 1e-12)) {
-        out.flags |= SPOLY_FLAG_DEGENERATE;
-        continue;
-      }
-      RootSet<DB + 1> Rb;
-      isolate_roots<DB + 1>(bl, bd, -0.1, 1.1, 1e-7, Rb);
-      for (int i = 0; i < Rb.n; ++i)
-        if (nu == 0 || Rb.x[i] - ua[nu - 1] >= 1e-7) {
-          if (nu < 4) {
-            ua[nu++] = Rb.x[i];
-          } else {  // slot capacity (4 u-roots per v-root): flagged, never silent
-            out.flags |= SPOLY_FLAG_TRUNCATED;
-            cnt[C_TRUNCATED]++;
-          }
-        }
-    }
+    double ua[4], ud;
+    const int nu = back_substitute<TC>(Sys, vs, ua, &ud, &out.flags, cnt);
+    if (!tangent && !isnan(ud)) tangent = probe_admissible<TC>(x0, x2, P_in, N_in, prm, Sys, ud, vs);
     for (int iu = 0; iu < nu; ++iu) {
       cnt[C_CANDIDATES]++;
       double us = ua[iu], vv = vs;
@@ -381,28 +512,8 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
         continue;
       }
       cnt[C_REFINED]++;
-      // reading R2: <= 3 Newton steps on (a, b), keep a step only if |F| decreases and the candidate
-      // stays within 1e-3 of its back-substituted position (local refinement, never a search)
-      double fa, fau, fav, fb, fbu, fbv;
-      beval<2, 3>(A, us, vv, &fa, &fau, &fav);
-      beval<DB, DB + 1>(B, us, vv, &fb, &fbu, &fbv);
-      for (int it = 0; it < 3; ++it) {
-        const double det = fau * fbv - fav * fbu;
-        if (det == 0.0) break;
-        const double idet = 1.0 / det;
-        const double du = -(fbv * fa - fav * fb) * idet, dv = -(-fbu * fa + fau * fb) * idet;
-        // a step below 1e-15 cannot change the double-precision candidate: converged
-        if (fmax(fabs(du), fabs(dv)) <= 1e-15 * fmax(1.0, fmax(fabs(us), fabs(vv)))) break;
-        if (!(fmax(fabs(us + du - ua[iu]), fabs(vv + dv - vs)) <= 1e-3)) break;
-        double na, nau, nav, nb, nbu, nbv;
-        beval<2, 3>(A, us + du, vv + dv, &na, &nau, &nav);
-        beval<DB, DB + 1>(B, us + du, vv + dv, &nb, &nbu, &nbv);
-        if (!(na * na + nb * nb < fa * fa + fb * fb)) break;
-        us += du;
-        vv += dv;
-        fa = na; fau = nau; fav = nav;
-        fb = nb; fbu = nbu; fbv = nbv;
-      }
+      double fau, fav, fbu, fbv;
+      refine_ab<TC>(Sys.A, Sys.B, ua[iu], vs, us, vv, fau, fav, fbu, fbv);
       const double ur = Sys.relabel ? vv : us, vr_ = Sys.relabel ? us : vv;  // original labeling
       const d3 x1 = P_in[0] + ur * e1o + vr_ * e2o;
       const d3 nx = N_in[0] + ur * (N_in[1] - N_in[0]) + vr_ * (N_in[2] - N_in[0]);
@@ -450,126 +561,14 @@ __device__ void path_phase(d3 x0, d3 x2, double intensity, const d3 P_in[3], con
       }
     }
   }
-}
-
-// ---- phase 2a: roots of r on [0, 1] for the monotone jobs.  Each lane owns one job at a time and takes a
-// new one as soon as its Newton iteration converges, so the lanes of a warp stay busy however different
-// their iteration counts are (the fused per-job loop ran at 8.5 of 32 lanes).  Jobs are taken from a
-// warp-private chunk of consecutive jobs (uniform cursor, no atomics); the root overwrites the job's
-// coefficient slot: [0] = count (0 or 1), [1] = root.
-constexpr int kRootChunk = 512;
-template <bool TC>
-__global__ void __launch_bounds__(128) k1_roots(SolSink S, JobSink J) {
-  constexpr int NR = Sys1<TC>::NR;
-  constexpr unsigned FULL = 0xffffffffu;
-  uint32_t cnt[C_NUM];
-#pragma unroll
-  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t nmono = J.count[0];
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  // chunk: enough jobs per warp to amortise the refills, small enough to spread short lists over all warps
-  uint64_t kc = (nmono + nw - 1) / nw;
-  kc = kc < 32 ? 32 : (kc > kRootChunk ? kRootChunk : (kc + 31) & ~31ull);
-  uint64_t chunk = gw;
-  uint64_t cur = chunk * kc, cend = cur + kc < nmono ? cur + kc : nmono;
-  bool busy = false;
-  uint64_t jj = 0;
-  double c[NR];
-  double a = 0.0, b = 1.0, x = 0.0, flo = 0.0;
-  int it = 0;
-  while (true) {
-    // refill idle lanes from the warp's chunk (uniform cursor)
-    unsigned idle = __ballot_sync(FULL, !busy);
-    while (idle && cur >= cend && chunk * kc < nmono) {
-      chunk += nw;
-      cur = chunk * kc;
-      cend = cur + kc < nmono ? cur + kc : nmono;
-      if (cur >= nmono) cur = cend = nmono;
-    }
-    if (!busy && cur < cend) {
-      const uint64_t my = cur + __popc(idle & lt);
-      if (my < cend) {
-        jj = my;
-        if (NR % 2 == 0) {
-          const double2* r2 = reinterpret_cast<const double2*>(J.r + jj * NR);
-#pragma unroll
-          for (int i = 0; i < NR / 2; ++i) {
-            const double2 v = __ldg(r2 + i);
-            c[2 * i] = v.x;
-            c[2 * i + 1] = v.y;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < NR; ++i) c[i] = __ldg(J.r + jj * NR + i);
-        }
-        double f1 = c[NR - 1];
-#pragma unroll
-        for (int i = NR - 2; i >= 0; --i) f1 += c[i];  // r(1)
-        const double f0 = c[0];
-        cnt[C_EVAL_TERMS] += 2 * NR;
-        if (f0 == 0.0 || f1 == 0.0 || (f0 < 0.0) == (f1 < 0.0)) {
-          // exact endpoint root, or (rounding) no sign change: finish at once
-          const bool has = f0 == 0.0 || f1 == 0.0;
-          J.root[jj] = has ? (f0 == 0.0 ? 0.0 : 1.0) : __longlong_as_double(0x7ff8000000000000ll);
-          cnt[C_VROOTS] += has;
-        } else {
-          a = 0.0;
-          b = 1.0;
-          flo = f0;
-          x = -f0 / (f1 - f0);  // secant start
-          if (!(x > a && x < b)) x = 0.5;
-          it = 0;
-          busy = true;
-        }
-      }
-    }
-    if (idle) cur = cur + __popc(idle) < cend ? cur + __popc(idle) : cend;
-    if (!__any_sync(FULL, busy)) {
-      if (cur >= cend && chunk * kc >= nmono) break;
-      continue;
-    }
-    if (busy) {
-      // one safeguarded Newton step (same rule as monotone_root)
-      double f = c[NR - 1], fp = 0.0;
-#pragma unroll
-      for (int i = NR - 2; i >= 0; --i) {
-        fp = fma(fp, x, f);
-        f = fma(f, x, c[i]);
-      }
-      cnt[C_EVAL_TERMS] += 2 * NR - 1;
-      ++it;
-      bool fin = false;
-      double xr = x;
-      if (f != 0.0) {
-        if ((f < 0.0) == (flo < 0.0))
-          a = x;
-        else
-          b = x;
-        double xn = x - f * fast_rcp(fp);
-        // convergence is tested before the bracket safeguard: at the root the Newton step is below an ulp
-        // and may land on the endpoint x just became, which must not trigger a bisection from a far bracket
-        const bool conv = fabs(xn - x) <= 1e-12;
-        if (conv)
-          xn = fmin(fmax(xn, a), b);
-        else if (!(xn > a && xn < b))
-          xn = 0.5 * (a + b);
-        fin = conv || b - a <= 1e-15 || it >= 100;
-        xr = xn;
-        x = xn;
-      } else {
-        fin = true;
-      }
-      if (fin) {
-        J.root[jj] = xr;
-        cnt[C_VROOTS]++;
-        busy = false;
-      }
-    }
+  // c14 conditions of the root isolation (deep jobs): close v-roots, tiny critical values (reading R11)
+  for (int ip = 0; ip < np && !tangent; ++ip) {
+    double ua[4], ud;
+    uint32_t fdummy = 0;
+    const int nu = back_substitute<TC>(Sys, vp[ip], ua, &ud, &fdummy, cnt);
+    for (int iu = 0; iu < nu && !tangent; ++iu) tangent = probe_admissible<TC>(x0, x2, P_in, N_in, prm, Sys, ua[iu], vp[ip]);
   }
-  flush_counters(S, cnt);
+  if (tangent) out.flags |= SPOLY_FLAG_NEAR_TANGENT;
 }
 
 // ---- phase 2a': jobs with a deeper derivative recursion (~1%), thread per job
@@ -596,90 +595,21 @@ __global__ void __launch_bounds__(128) k1_roots_deep(SolSink S, JobSink J, uint6
       double r[NR];
 #pragma unroll
       for (int i = 0; i < NR; ++i) r[i] = __ldg(J.r + jj * NR + i);
-      RootSet<NR> R;
-      isolate_roots<NR>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
-      cnt[C_EVAL_TERMS] += R.terms;
-      if (R.flags & 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
-      if (R.min_crit_ratio <= 1e-10) flags |= SPOLY_FLAG_NEAR_TANGENT;
+      RootSet<NR, true> R;
+      isolate_roots<NR, true>(r, (int)(meta >> 8), 0.0, 1.0, prm.eps_flag, R, (int)(meta & 0xFF));
+      cnt[C_EVAL_DEEP] += R.terms;
       for (int i = 0; i < R.n; ++i)
         if (nv == 0 || R.x[i] - vr[nv - 1] >= 1e-7) vr[nv++] = R.x[i];
       cnt[C_VROOTS] += nv;
-      J.r[jj * NR] = (double)nv;
+      // [nv | np << 8, roots..., probes...]: the c14 near-tangency conditions go to the path kernel, which probes
+      // them (reading R11); probes that do not fit flag the tuple conservatively
+      const int np = min(R.nprobe, NR - 1 - nv);
+      if (np < R.nprobe) flags |= SPOLY_FLAG_NEAR_TANGENT;
+      J.r[jj * NR] = (double)(nv | (np << 8));
       for (int i = 0; i < nv; ++i) J.r[jj * NR + 1 + i] = vr[i];
+      for (int i = 0; i < np; ++i) J.r[jj * NR + 1 + nv + i] = R.probe[i];
     }
     emit_flag(active && flags != 0, flags, pair, S);
-  }
-  flush_counters(S, cnt);
-}
-
-// ---- phase 2b0: candidate pre-pass over the monotone jobs, thread per job.  Back-substitutes v* in phase 1's
-// stored (normalised) a (the same quadratic as the path phase) and applies the same domain pre-check; a job
-// whose every candidate is rejected there and that raises no flag is finished here (its candidates are
-// counted), every other job goes to the path kernel's list (J.meta[0..lcount), free after the root
-// kernels).  The path kernel then runs fewer, less divergent jobs; outputs are unchanged.
-__global__ void __launch_bounds__(256) k1_cand(SolSink S, JobSink J) {
-  uint32_t cnt[C_NUM];
-#pragma unroll
-  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t nmono = J.count[0];
-  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  // a warp owns chunks of kCandChunk x 32 consecutive jobs and appends a chunk's kept jobs with ONE atomic
-  // (one same-address atomic per 32 jobs would serialise in L2)
-  constexpr int kCandChunk = 16;
-  for (uint64_t cb = gw * (32 * kCandChunk); cb < nmono; cb += nw * (32 * kCandChunk)) {
-    unsigned bal[kCandChunk];
-#pragma unroll
-    for (int t = 0; t < kCandChunk; ++t) {
-      const uint64_t jj = cb + 32 * t + lane;
-      bool keep = false;
-      const double vs = jj < nmono ? J.root[jj] : 0.0;
-      if (jj < nmono && !isnan(vs)) {
-        cnt[C_CAND_JOBS]++;
-        double A[9];
-        const double2* a2 = reinterpret_cast<const double2*>(J.A + jj * 6);
-        const double2 c01 = __ldg(a2), c23 = __ldg(a2 + 1), c45 = __ldg(a2 + 2);
-        A[0] = c01.x; A[1] = c01.y; A[2] = c23.x;
-        A[3] = c23.y; A[4] = c45.x; A[6] = c45.y;
-        A[5] = A[7] = A[8] = 0.0;
-        double al[3];
-        bslices_at<2, 3>(A, vs, al);
-        const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
-        if (!(amax >= 1e-12)) {
-          keep = true;  // a(., v*) == 0: the b fallback runs in the path kernel
-        } else {
-          uint32_t fl = 0, nc = 0, nrej = 0;
-          double ua[2];
-          const int nu = quadratic_u_roots(al, ua, &fl);
-          for (int iu = 0; iu < nu; ++iu) {
-            ++nc;
-            if (precheck_reject(ua[iu], vs))
-              ++nrej;
-            else
-              keep = true;
-          }
-          if (fl) keep = true;
-          if (!keep) {
-            cnt[C_CANDIDATES] += nc;
-            cnt[C_REJ_DOMAIN] += nrej;
-          }
-        }
-      }
-      bal[t] = __ballot_sync(0xffffffffu, keep);
-    }
-    uint32_t tot = 0;
-#pragma unroll
-    for (int t = 0; t < kCandChunk; ++t) tot += __popc(bal[t]);
-    unsigned long long b = 0;
-    if (lane == 0 && tot) b = atomicAdd(J.lcount, (unsigned long long)tot);
-    b = __shfl_sync(0xffffffffu, b, 0);
-#pragma unroll
-    for (int t = 0; t < kCandChunk; ++t) {
-      if ((bal[t] >> lane) & 1u) J.meta[b + __popc(bal[t] & lt)] = (uint32_t)(cb + 32 * t + lane);
-      b += __popc(bal[t]);
-    }
   }
   flush_counters(S, cnt);
 }
@@ -695,28 +625,31 @@ __global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const
   uint32_t cnt[C_NUM];
 #pragma unroll
   for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
-  const uint64_t nl = *J.lcount, n = nl + J.count[1];
+  const uint64_t nl = 0, n = J.count[1];  // deep entries only (the path entries run in k1_path_fast)
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
   for (uint64_t base = gw * 32; base < n; base += nw * 32) {
     const uint64_t i = base + lane;
-    const uint64_t jj = i < nl ? (uint64_t)J.meta[i] : J.capacity - 1 - (i - nl);
-    // monotone jobs (pre-pass list): the compact root; deep jobs: [count, roots...] in place of r
+    const uint64_t jj = i < nl ? i : J.capacity - 1 - (i - nl);
+    // front: (pair, root) of phase 1's surviving monotone jobs; back: deep jobs, [nv | np << 8, roots..., probes...]
     const double r0 = i < nl ? J.root[jj] : 0.0;
-    const int nv = i < nl ? (isnan(r0) ? 0 : 1) : (i < n ? (int)J.r[jj * NR] : 0);
-    const bool active = nv > 0;
+    const int hdr = i < nl ? 1 : (i < n ? (int)J.r[jj * NR] : 0);
+    const int nv = hdr & 0xFF, np = hdr >> 8;
+    const bool active = nv > 0 || np > 0;
     PairOut o;
     o.nsol = 0;
     o.flags = 0;
     uint32_t pair = 0;
     if (active) {
       pair = __ldg(J.pair + jj);
-      double vr[NR];
-      if (i < nl)
+      double vr[NR], vp[NR];
+      if (i < nl) {
         vr[0] = r0;
-      else
+      } else {
         for (int k = 0; k < nv; ++k) vr[k] = J.r[jj * NR + 1 + k];
+        for (int k = 0; k < np; ++k) vp[k] = J.r[jj * NR + 1 + nv + k];
+      }
       d3 P[3], N[3], x0, x2;
       uint32_t q;
       load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
@@ -724,7 +657,7 @@ __global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const
       build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
       cnt[C_REBUILDS]++;
       const double I = inten ? __ldg(inten + q) : 1.0;
-      path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, o, cnt);
+      path_phase<TC>(x0, x2, I, P, N, prm, Sys, vr, nv, vp, np, o, cnt);
     }
     emit_flag(active && o.flags != 0, o.flags, pair, S);
     uint32_t ex;
@@ -743,12 +676,120 @@ __global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const
   flush_counters(S, cnt);
 }
 
+// ---- phase 2c: the common case, thread per path entry (pair, root) of phase 1: the quadratic back-substitution
+// (<= 2 candidates, no b fallback, no c14 probe: phase 1 routed those jobs to the deep list), (a, b) refinement
+// (reading R2), Eq. 3 validation, sides, flags, analytic contribution (c15), <= 2 chains emitted with
+// warp-aggregated appends.  Same arithmetic and slots as path_phase(), with the lean state of one root.
+#ifdef SPOLY_FAST_MINB
+#define SPOLY_FAST_BOUNDS __launch_bounds__(128, SPOLY_FAST_MINB)
+#else
+#define SPOLY_FAST_BOUNDS __launch_bounds__(128)
+#endif
+template <bool TC>
+__global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+                                                    const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                                    const double* __restrict__ inten, SolveParams prm, SolSink S,
+                                                    JobSink J) {
+  uint32_t cnt[C_NUM];
+#pragma unroll
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const uint64_t n = J.count[0];
+  const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  for (uint64_t base = gw * 32; base < n; base += nw * 32) {
+    const uint64_t i = base + lane;
+    const bool active = i < n;
+    uint32_t flags = 0, pair = 0;
+    int nsol = 0;
+    double su[2], sv[2], sc[2];
+    float sr[2];
+    uint32_t ss[2];
+    if (active) {
+      pair = __ldg(J.pair + i);
+      const double vs = __ldg(J.root + i);
+      d3 P[3], N[3], x0, x2;
+      uint32_t q;
+      load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
+      Sys1<TC> Sys;
+      build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
+      cnt[C_REBUILDS]++;
+      const double I = inten ? __ldg(inten + q) : 1.0;
+      const d3 e1o = P[1] - P[0], e2o = P[2] - P[0];
+      const d3 g_geo = cross(e1o, e2o);
+      double al[3], ua[2], ud;
+      bslices_at<2, 3>(Sys.A, vs, al);
+      const int nu = quadratic_u_roots(al, ua, &ud);
+      for (int iu = 0; iu < nu; ++iu) {
+        cnt[C_CANDIDATES]++;
+        double us = ua[iu], vv = vs;
+        if (precheck_reject(us, vv)) {
+          cnt[C_REJ_DOMAIN]++;
+          continue;
+        }
+        cnt[C_REFINED]++;
+        double fau, fav, fbu, fbv;
+        refine_ab<TC>(Sys.A, Sys.B, ua[iu], vs, us, vv, fau, fav, fbu, fbv);
+        const double ur = Sys.relabel ? vv : us, vr_ = Sys.relabel ? us : vv;  // original labeling
+        const d3 x1 = P[0] + ur * e1o + vr_ * e2o;
+        const d3 nx = N[0] + ur * (N[1] - N[0]) + vr_ * (N[2] - N[0]);
+        const double ed = fmin(fmin(ur, vr_), 1.0 - ur - vr_);
+        const bool inside = ur >= -prm.eps_domain && vr_ >= -prm.eps_domain && ur + vr_ <= 1.0 + prm.eps_domain;
+        const double rho = vertex_residual(x0, x1, x2, nx, Sys.eta0, Sys.eta1);
+        if (!inside) {
+          if (ed >= -prm.eps_flag && rho < prm.theta_final && side_ok(TC, x0, x1, x2, nx, g_geo))
+            flags |= SPOLY_FLAG_BOUNDARY;
+          cnt[C_REJ_DOMAIN]++;
+          continue;
+        }
+        if (!(rho < prm.theta_final)) {
+          cnt[C_REJ_CONSTRAINT]++;
+          continue;
+        }
+        if (!side_ok(TC, x0, x1, x2, nx, g_geo)) {
+          cnt[C_REJ_SIDE]++;
+          continue;
+        }
+        if (rho >= 1e-7) flags |= SPOLY_FLAG_RESIDUAL;
+        if (ed <= prm.eps_flag) flags |= SPOLY_FLAG_BOUNDARY;
+        if (fabs(fau * fbv - fav * fbu) < 1e-6 * hypot(fau, fav) * hypot(fbu, fbv)) flags |= SPOLY_FLAG_NEAR_TANGENT;
+        if (nsol == 1 && fabs(su[0] - ur) < 1e-7 && fabs(sv[0] - vr_) < 1e-7) {  // dedup (1e-7)
+          cnt[C_REJ_SIDE]++;
+          continue;
+        }
+        const double J1 = jacobian_k1(TC, x0, x2, x1, e1o, e2o, N[1] - N[0], N[2] - N[0], nx, Sys.eta1, Sys.eta0);
+        su[nsol] = ur;
+        sv[nsol] = vr_;
+        sc[nsol] = J1 > 0 ? I / J1 : 0.0;
+        sr[nsol] = (float)rho;
+        ss[nsol] = (uint32_t)iu;  // slot iv * 4 + iu with iv = 0
+        nsol++;
+        cnt[C_ADMISSIBLE]++;
+      }
+    }
+    emit_flag(active && flags != 0, flags, pair, S);
+    uint32_t ex;
+    const unsigned long long b = warp_alloc(S.count, (uint32_t)nsol, &ex);
+#pragma unroll
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const unsigned long long p = b + ex + s2;
+      if (s2 < nsol && p < S.capacity) {
+        S.key[p] = ((unsigned long long)pair << 6) | ss[s2];
+        S.bary[2 * p] = su[s2];
+        S.bary[2 * p + 1] = sv[s2];
+        S.contrib[p] = sc[s2];
+        S.resid[p] = sr[s2];
+      }
+    }
+  }
+  flush_counters(S, cnt);
+}
+
 void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t* pt, uint64_t npairs,
                      const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
                      const SolSink& S, const JobSink& J, int nsm, cudaStream_t st) {
   if (npairs == 0) return;
   const int threads = 128;
-  const uint64_t cap = (uint64_t)nsm * 16;
 #ifndef SPOLY_P1_GRID
 #define SPOLY_P1_GRID 64  // blocks per SM (grid-stride); A/B on C2: 4 -> 2.22, 16 -> 2.15, 64 -> 2.07, 256 -> 2.20 ms
 #endif
@@ -760,29 +801,25 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_phase1<true><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
     else
       k1_phase1<false><<<g1, threads, 0, st>>>(pq, pt, npairs, M.tris, ep, prm, S, J);
-  } else if (phase == 2) {  // roots
-#ifndef SPOLY_ROOTS_GRID
-#define SPOLY_ROOTS_GRID 32  // blocks per SM (two waves, smaller warp chunks); A/B: 8 -> 0.61, 16 -> 0.60, 32 -> 0.575 ms
-#endif
-    if (refract) {
-      k1_roots<true><<<nsm * SPOLY_ROOTS_GRID, threads, 0, st>>>(S, J);
+  } else if (phase == 2) {  // deep jobs (derivative recursion below level 1, ~1% of the jobs)
+    if (refract)
       k1_roots_deep<true><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
-    } else {
-      k1_roots<false><<<nsm * SPOLY_ROOTS_GRID, threads, 0, st>>>(S, J);
+    else
       k1_roots_deep<false><<<nsm * 2, threads, 0, st>>>(S, J, J.capacity, prm);
-    }
   } else {  // path
 #ifndef SPOLY_PATH_GRID
 #define SPOLY_PATH_GRID 4  // blocks per SM (2 resident at 243 registers); A/B: 16 -> 4 took k1_path<R> 2.04 -> 2.03 ms, <T> 0.167 -> 0.155 ms
 #endif
-#ifndef SPOLY_CAND_GRID
-#define SPOLY_CAND_GRID 8
+#ifndef SPOLY_FAST_GRID
+#define SPOLY_FAST_GRID 8
 #endif
-    k1_cand<<<nsm * SPOLY_CAND_GRID, 256, 0, st>>>(S, J);
-    if (refract)
+    if (refract) {
+      k1_path_fast<true><<<nsm * SPOLY_FAST_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
       k1_path<true><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
-    else
+    } else {
+      k1_path_fast<false><<<nsm * SPOLY_FAST_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
       k1_path<false><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
+    }
   }
 }
 

@@ -431,12 +431,13 @@ __device__ double jacobian2(const Chain2& C, d3 x1, d3 x2) {
 // Written by the build kernel, read by the scan and path kernels.  Coefficients are stored transposed,
 // [j * NR + i] = coefficient of u^i v^j (zero above the truncated u-degree and beyond the row), so the lane
 // that owns row i reads consecutive addresses with its neighbours.
+constexpr int kMaxV2 = 208;  // v-roots + c14 probes kept per pair: 100 pieces give <= 101 of each (more: TRUNCATED)
 template <bool V1T, bool V2T>
 struct Rec2 {
   using D = Deg2<V1T, V2T>;
   static constexpr int NR = D::DB <= 15 ? 16 : (D::DB <= 31 ? 32 : 48);
   static constexpr int VR = 16;  // header: eta0, eta1, eta2, relabel, flags, da, db, n, ok, nv
-  static constexpr int AT = VR + 40;
+  static constexpr int AT = VR + kMaxV2;
   static constexpr int BT = AT + (D::DA + 1) * NR;
   static constexpr int U = BT + (D::DB + 1) * NR;
   static constexpr int V = U + tri_n(D::DU);
@@ -444,7 +445,6 @@ struct Rec2 {
   static constexpr int STRIDE = (K + tri_n(D::DK) + 7) & ~7;
 };
 enum { H_ETA0 = 0, H_ETA1, H_ETA2, H_RELABEL, H_FLAGS, H_DA, H_DB, H_N, H_OK, H_NV };
-constexpr int kMaxV2 = 40;   // v-roots kept per pair (more: SPOLY_FLAG_TRUNCATED)
 constexpr int kMaxSol2 = 8;  // admissible chains kept per pair (more: SPOLY_FLAG_TRUNCATED)
 
 __device__ __forceinline__ void load_chain(const TriRec* __restrict__ tris, const uint32_t* __restrict__ pt,
@@ -638,16 +638,25 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
         return wdet_T<G, R::NR, NC>(g, AT, D::DA, BT, D::DB, n, v, lg);
       };
       const int P = prm.pieces;
-      int last_change = -10;
+      int nprobe = 0;
       double lg_prev = -INFINITY, lg_cur;
       int s_cur = det(0.0, &lg_cur);
       for (int j = 0; j <= P; ++j) {
         int s_next = 0;
         double lg_next = -INFINITY;
         if (j < P) s_next = det((double)(j + 1) / P, &lg_next);
-        // near-tangent: |det(v_j)| < 1e-9 max(neighbours)
+        // c14: |det(v_j)| < 1e-9 max(neighbours), a root within ~1e-11 of the sample: a near-tangency condition the
+        // path kernel probes (stored as v_j + 2 among the v-roots; reading R11); one that does not fit flags
         const double nb = fmax(lg_prev, lg_next);
-        if (lg_cur < log(1e-9) + nb) flags |= SPOLY_FLAG_NEAR_TANGENT;
+        if (lg_cur < log(1e-9) + nb) {
+          if (nv < kMaxV2) {
+            if (g.lane == 0) rec[R::VR + nv] = 2.0 + (double)j / P;
+            nv++;
+            nprobe++;
+          } else {
+            flags |= SPOLY_FLAG_NEAR_TANGENT;
+          }
+        }
         if (s_cur == 0) {
           if (nv < kMaxV2) {
             if (g.lane == 0) rec[R::VR + nv] = (double)j / P;
@@ -657,8 +666,6 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
             cnt[C_TRUNCATED]++;
           }
         } else if (j < P && s_next != 0 && s_next != s_cur) {
-          if (j - last_change == 1) flags |= SPOLY_FLAG_NEAR_TANGENT;
-          last_change = j;
           double lo = (double)j / P, hi = (double)(j + 1) / P;
           for (int it = 0; it < prm.scan_bisect_iters; ++it) {
             const double m = 0.5 * (lo + hi);
@@ -686,7 +693,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
         lg_cur = lg_next;
       }
       cnt[C_KFLOP] += (uint32_t)(kflop_acc * 1e-3);
-      cnt[C_VROOTS] += nv;
+      cnt[C_VROOTS] += nv - nprobe;
     }
     if (g.lane == 0) {
       rec[H_NV] = nv;
@@ -699,6 +706,130 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
     g.sync();
   }
   group_counters(g, cnt, S);
+}
+
+// back-substitution (c11): u-roots of a(., v) -- b(., v) when a(., v) == 0 -- on [-0.1, 1.1]; a
+// quadratic with |disc| <= 1e-8 scale reports its double root in *udouble (a c14 condition, probed), else NaN
+template <bool V1T, bool V2T>
+__device__ int k2_back_sub(const double* AT, const double* BT, int da, int db, double vs, double* us, double* udouble,
+                           uint32_t* flags) {
+  using D = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  constexpr int NA = D::DB + 1;
+  *udouble = __longlong_as_double(0x7ff8000000000000ll);
+  double Acoef[NA];
+  int dA = da;
+  double amax = 0;
+  for (int i = 0; i <= dA; ++i) {
+    Acoef[i] = rowT<R::NR>(AT, D::DA, i, vs);
+    amax = fmax(amax, fabs(Acoef[i]));
+  }
+  if (!(amax >= 1e-12)) {
+    dA = db;
+    amax = 0;
+    for (int i = 0; i <= dA; ++i) {
+      Acoef[i] = rowT<R::NR>(BT, D::DB, i, vs);
+      amax = fmax(amax, fabs(Acoef[i]));
+    }
+    if (!(amax >= 1e-12)) {
+      *flags |= SPOLY_FLAG_DEGENERATE;
+      return 0;
+    }
+  }
+  while (dA > 0 && Acoef[dA] == 0.0) --dA;
+  int nu = 0;
+  if (dA == 1) {
+    us[nu++] = -Acoef[0] / Acoef[1];
+  } else if (dA == 2) {
+    const double a0 = Acoef[0], a1 = Acoef[1], a2 = Acoef[2];
+    double disc = a1 * a1 - 4 * a2 * a0;
+    const double sc = a1 * a1 + 4 * fabs(a2 * a0);
+    if (fabs(disc) <= 1e-8 * sc) *udouble = -a1 / (2 * a2);
+    if (!(disc < -1e-12 * sc)) {
+      if (disc < 0) disc = 0;
+      const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+      if (qq == 0.0) {
+        us[nu++] = 0.0;
+      } else {
+        double r1 = qq / a2, r2 = a0 / qq;
+        if (r1 > r2) {
+          const double t = r1;
+          r1 = r2;
+          r2 = t;
+        }
+        us[nu++] = r1;
+        if (r2 - r1 >= 1e-7) us[nu++] = r2;
+      }
+    }
+  } else if (dA > 2) {
+    RootSet<NA> Ru;
+    isolate_roots<NA>(Acoef, dA, -0.1, 1.1, 1e-7, Ru);
+    for (int i = 0; i < Ru.n; ++i)
+      if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];  // Ru.n <= dA < NA
+  }
+  return nu;
+}
+
+// c13 polish: <= iters Newton steps on the exact shooting residual (central differences, h = 1e-7),
+// a step kept only if |G| decreases; Jm receives the last Jacobian (zero if none was formed)
+__device__ bool polish2(const Chain2& C, int iters, d3 f1, d3 f2, double& uu, double& vv, double& uu2, double& vv2,
+                        double Jm[4]) {
+  double Gs[2];
+  Jm[0] = Jm[1] = Jm[2] = Jm[3] = 0.0;
+  const bool okp = shoot2(C, uu, vv, f1, f2, Gs, &uu2, &vv2);
+  for (int it = 0; okp && it < iters; ++it) {
+    const double h = 1e-7;
+    double Gp[2], Gm[2], t1, t2;
+    if (!shoot2(C, uu + h, vv, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu - h, vv, f1, f2, Gm, &t1, &t2)) break;
+    Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
+    Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
+    if (!shoot2(C, uu, vv + h, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu, vv - h, f1, f2, Gm, &t1, &t2)) break;
+    Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
+    Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
+    const double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
+    if (det == 0.0) break;
+    const double du = -(Jm[3] * Gs[0] - Jm[1] * Gs[1]) / det;
+    const double dv = -(-Jm[2] * Gs[0] + Jm[0] * Gs[1]) / det;
+    double Gn[2], nu2, nv2;
+    if (!shoot2(C, uu + du, vv + dv, f1, f2, Gn, &nu2, &nv2)) break;
+    if (!(hypot(Gn[0], Gn[1]) < hypot(Gs[0], Gs[1]))) break;
+    uu += du;
+    vv += dv;
+    Gs[0] = Gn[0];
+    Gs[1] = Gn[1];
+    uu2 = nu2;
+    vv2 = nv2;
+  }
+  return okp;
+}
+
+__device__ __forceinline__ bool in_tri(double u, double v, double e) { return u >= -e && v >= -e && u + v <= 1 + e; }
+
+// c14 probe (reading R11): does the near-tangency condition at (u1, v1) sit at an (almost) admissible chain?  Within
+// kProbeDomain of both triangles, polished (moving at most kProbeMove), still within kProbeDomain, residual below
+// theta_final.  Ghost double roots of the square form fail it and raise no flag.
+constexpr double kProbeDomain2 = 1e-3, kProbeMove = 1e-2;
+__device__ bool probe2(const Chain2& C, const SolveParams& prm, const WP& Up, const WP& Vp, const WP& Kp, bool relabel,
+                       double u1, double v1) {
+  const double kap = wp_eval(Kp, u1, v1);
+  double u2 = wp_eval(Up, u1, v1) / kap, v2 = wp_eval(Vp, u1, v1) / kap;
+  if (!(fabs(kap) > 0) || !isfinite(u2) || !isfinite(v2)) return false;
+  if (relabel) {
+    const double t = u2;
+    u2 = v2;
+    v2 = t;
+  }
+  if (!in_tri(u1, v1, kProbeDomain2) || !in_tri(u2, v2, kProbeDomain2)) return false;
+  d3 f1, f2;
+  frame_of(normalize(C.x3 - C.T2.X(u2, v2)), &f1, &f2);
+  double uu = u1, vv = v1, uu2 = u2, vv2 = v2, Jm[4];
+  if (!polish2(C, prm.polish_iters, f1, f2, uu, vv, uu2, vv2, Jm)) return false;
+  if (fmax(fabs(uu - u1), fabs(vv - v1)) > kProbeMove) return false;
+  if (!in_tri(uu, vv, kProbeDomain2) || !in_tri(uu2, vv2, kProbeDomain2)) return false;
+  const d3 x1 = C.T1.X(uu, vv), x2 = C.T2.X(uu2, vv2);
+  const double r1 = resid(C.x0, x1, x2, C.T1.N(uu, vv), C.eta[0], C.eta[1]);
+  const double r2 = resid(x1, x2, C.x3, C.T2.N(uu2, vv2), C.eta[1], C.eta[2]);
+  return fmax(r1, r2) < prm.theta_final;
 }
 
 // ---- kernel 3: path phase (thread per pair with v-roots): back-substitution, polish, validation,
@@ -734,63 +865,24 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
     const WP Up{const_cast<double*>(rec + R::U), D::DU}, Vp{const_cast<double*>(rec + R::V), D::DU},
         Kp{const_cast<double*>(rec + R::K), D::DK};
     uint32_t flags = 0;
+    bool tangent = false;  // a probed c14 condition sits at an admissible chain (NEAR_TANGENT, reading R11)
     int nsol = 0;
     double su[kMaxSol2][4], scontrib[kMaxSol2];
     float sres[kMaxSol2];
     constexpr int NA = D::DB + 1;
     for (int iv = 0; iv < nv; ++iv) {
-      const double vs = rec[R::VR + iv];
-      double Acoef[NA];
-      int dA = da;
-      double amax = 0;
-      for (int i = 0; i <= dA; ++i) {
-        Acoef[i] = rowT<R::NR>(AT, D::DA, i, vs);
-        amax = fmax(amax, fabs(Acoef[i]));
+      const double ve = rec[R::VR + iv];
+      const bool is_probe = ve >= 2.0;  // a scan sample with |det| ~ 0 (stored as v + 2)
+      const double vs = is_probe ? ve - 2.0 : ve;
+      double us[NA], ud;
+      uint32_t fl = 0;
+      const int nu = k2_back_sub<V1T, V2T>(AT, BT, da, db, vs, us, &ud, &fl);
+      if (is_probe) {
+        for (int iu = 0; iu < nu && !tangent; ++iu) tangent = probe2(C, prm, Up, Vp, Kp, relabel, us[iu], vs);
+        continue;
       }
-      if (!(amax >= 1e-12)) {
-        dA = db;
-        amax = 0;
-        for (int i = 0; i <= dA; ++i) {
-          Acoef[i] = rowT<R::NR>(BT, D::DB, i, vs);
-          amax = fmax(amax, fabs(Acoef[i]));
-        }
-        if (!(amax >= 1e-12)) {
-          flags |= SPOLY_FLAG_DEGENERATE;
-          continue;
-        }
-      }
-      while (dA > 0 && Acoef[dA] == 0.0) --dA;
-      double us[NA];
-      int nu = 0;
-      if (dA == 1) {
-        us[nu++] = -Acoef[0] / Acoef[1];
-      } else if (dA == 2) {
-        const double a0 = Acoef[0], a1 = Acoef[1], a2 = Acoef[2];
-        double disc = a1 * a1 - 4 * a2 * a0;
-        const double sc = a1 * a1 + 4 * fabs(a2 * a0);
-        if (fabs(disc) <= 1e-8 * sc) flags |= SPOLY_FLAG_NEAR_TANGENT;
-        if (!(disc < -1e-12 * sc)) {
-          if (disc < 0) disc = 0;
-          const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
-          if (qq == 0.0) {
-            us[nu++] = 0.0;
-          } else {
-            double r1 = qq / a2, r2 = a0 / qq;
-            if (r1 > r2) {
-              const double t = r1;
-              r1 = r2;
-              r2 = t;
-            }
-            us[nu++] = r1;
-            if (r2 - r1 >= 1e-7) us[nu++] = r2;
-          }
-        }
-      } else if (dA > 2) {
-        RootSet<NA> Ru;
-        isolate_roots<NA>(Acoef, dA, -0.1, 1.1, 1e-7, Ru);
-        for (int i = 0; i < Ru.n; ++i)
-          if (nu == 0 || Ru.x[i] - us[nu - 1] >= 1e-7) us[nu++] = Ru.x[i];  // Ru.n <= dA < NA
-      }
+      flags |= fl;
+      if (!tangent && !isnan(ud)) tangent = probe2(C, prm, Up, Vp, Kp, relabel, ud, vs);
       for (int iu = 0; iu < nu; ++iu) {
         cnt[C_CANDIDATES]++;
         const double ur = us[iu], vr = vs;
@@ -806,7 +898,7 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
           v2 = t;
         }
         const double dm = 1e-3;
-        if (!(ur >= -dm && vr >= -dm && ur + vr <= 1 + dm && u2 >= -dm && v2 >= -dm && u2 + v2 <= 1 + dm)) {
+        if (!(in_tri(ur, vr, dm) && in_tri(u2, v2, dm))) {
           cnt[C_REJ_DOMAIN]++;
           continue;
         }
@@ -820,38 +912,13 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
         // polish: <= polish_iters Newton steps on the exact shooting residual, keep if |G| decreases
         d3 f1, f2;
         frame_of(normalize(C.x3 - x2), &f1, &f2);
-        double uu = ur, vv = vr, Gs[2], uu2 = u2, vv2 = v2;
-        bool okp = shoot2(C, uu, vv, f1, f2, Gs, &uu2, &vv2);
-        double Jm[4] = {0, 0, 0, 0};
-        for (int it = 0; okp && it < prm.polish_iters; ++it) {
-          const double h = 1e-7;
-          double Gp[2], Gm[2], t1, t2;
-          if (!shoot2(C, uu + h, vv, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu - h, vv, f1, f2, Gm, &t1, &t2)) break;
-          Jm[0] = (Gp[0] - Gm[0]) / (2 * h);
-          Jm[2] = (Gp[1] - Gm[1]) / (2 * h);
-          if (!shoot2(C, uu, vv + h, f1, f2, Gp, &t1, &t2) || !shoot2(C, uu, vv - h, f1, f2, Gm, &t1, &t2)) break;
-          Jm[1] = (Gp[0] - Gm[0]) / (2 * h);
-          Jm[3] = (Gp[1] - Gm[1]) / (2 * h);
-          const double det = Jm[0] * Jm[3] - Jm[1] * Jm[2];
-          if (det == 0.0) break;
-          const double du = -(Jm[3] * Gs[0] - Jm[1] * Gs[1]) / det;
-          const double dv = -(-Jm[2] * Gs[0] + Jm[0] * Gs[1]) / det;
-          double Gn[2], nu2, nv2;
-          if (!shoot2(C, uu + du, vv + dv, f1, f2, Gn, &nu2, &nv2)) break;
-          if (!(hypot(Gn[0], Gn[1]) < hypot(Gs[0], Gs[1]))) break;
-          uu += du;
-          vv += dv;
-          Gs[0] = Gn[0];
-          Gs[1] = Gn[1];
-          uu2 = nu2;
-          vv2 = nv2;
-        }
-        if (!okp) {
+        double uu = ur, vv = vr, uu2 = u2, vv2 = v2, Jm[4];
+        if (!polish2(C, prm.polish_iters, f1, f2, uu, vv, uu2, vv2, Jm)) {
           cnt[C_REJ_CONSTRAINT]++;
           continue;
         }
         const double ed = prm.eps_domain;
-        if (!(uu >= -ed && vv >= -ed && uu + vv <= 1 + ed && uu2 >= -ed && vv2 >= -ed && uu2 + vv2 <= 1 + ed)) {
+        if (!(in_tri(uu, vv, ed) && in_tri(uu2, vv2, ed))) {
           cnt[C_REJ_DOMAIN]++;
           continue;
         }
@@ -905,6 +972,7 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
         }
       }
     }
+    if (tangent) flags |= SPOLY_FLAG_NEAR_TANGENT;
     // emission: flag record, then the solutions in processing order (deterministic slot)
     if (flags) {
       const unsigned long long p = atomicAdd(S.count + 1, 1ull);

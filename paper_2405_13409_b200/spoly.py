@@ -56,7 +56,7 @@ class spoly_report(ctypes.Structure):
         ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64),
         ("ms_roots", ctypes.c_float), ("ms_path", ctypes.c_float), ("n_refined", ctypes.c_uint64),
         ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64), ("n_cull_tests", ctypes.c_uint64),
-        ("n_truncated", ctypes.c_uint64), ("n_big_scan", ctypes.c_uint64)]
+        ("n_truncated", ctypes.c_uint64), ("n_big_scan", ctypes.c_uint64), ("n_eval_deep", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -222,7 +222,7 @@ class Context:
                    ms_path=r.report.ms_path, n_refined=int(r.report.n_refined),
                    n_cand_jobs=int(r.report.n_cand_jobs), n_path_jobs=int(r.report.n_path_jobs),
                    n_cull_tests=int(r.report.n_cull_tests), n_truncated=int(r.report.n_truncated),
-                   n_big_scan=int(r.report.n_big_scan))
+                   n_big_scan=int(r.report.n_big_scan), n_eval_deep=int(r.report.n_eval_deep))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),

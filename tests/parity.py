@@ -55,12 +55,15 @@ def compare(orc, gpu: dict, nq: int, tol_bary=1e-5, tol_rad=1e-4, max_flag_frac=
     if gpu_worklist is None and "worklist" in gpu:
         wq, wt = gpu["worklist"]
         gpu_worklist = _keyset(wq, wt, k)
+    orc_worklist = _keyset(*orc.worklist, k) if getattr(orc, "worklist", None) is not None else None
     only_g = flag_g - flag_o
     only_o = flag_o - flag_g
+    # a tuple only one side's cull kept was never solved by the other: its flag is not a disagreement (the two
+    # culls are different sound predicates, SURVEY §8(c) "Cull differences")
+    if orc_worklist is not None:
+        only_g = {t for t in only_g if t in orc_worklist}
     if gpu_worklist is not None:
-        # a tuple only the (more permissive, FP32) GPU cull kept was never solved by the oracle: its flag is not
-        # a disagreement.  The oracle solves a subset of the GPU list (cull soundness, checked separately).
-        only_g = {t for t in only_g if t in gpu_worklist}
+        only_o = {t for t in only_o if t in gpu_worklist}
     one_sided = len(only_g) + len(only_o)
     keys = set(og) | set(gg)
     worst = 0.0
@@ -96,7 +99,7 @@ def compare(orc, gpu: dict, nq: int, tol_bary=1e-5, tol_rad=1e-4, max_flag_frac=
             rel = abs(ro - rg) / max(abs(ro), 1e-300) if ro != 0 else abs(rg)
             assert rel <= tol_rad, f"{label} radiance mismatch at query {q}: oracle {ro!r} gpu {rg!r} rel {rel:.3g}"
             rad_worst = max(rad_worst, rel)
-            n_rad += ro != 0
+            n_rad += int(ro != 0)
     st = {"label": label, "compared_solutions": n_cmp, "worst_bary": worst, "worst_rad_rel": rad_worst,
           "compared_radiance": n_rad, "flagged_tuples": len(flagged), "flagged_queries": len(flagged_q),
           "keys": len(keys), "flag_frac_oracle": frac_o, "flag_frac_gpu": frac_g, "flagged_oracle": len(flag_o),
@@ -105,7 +108,7 @@ def compare(orc, gpu: dict, nq: int, tol_bary=1e-5, tol_rad=1e-4, max_flag_frac=
     log = os.environ.get("SPOLY_PARITY_LOG")
     if log:
         with open(log, "a") as f:
-            f.write(json.dumps(st) + "\n")
+            f.write(json.dumps(st, default=float) + "\n")
     assert n_cmp >= min_compared, f"{label} only {n_cmp} unflagged chains compared (< {min_compared}): {st}"
     assert frac_o <= max_flag_frac, f"{label} oracle flagged {frac_o:.3%} of its tuples (> {max_flag_frac:.1%}): {st}"
     assert frac_g <= max_flag_frac, f"{label} GPU flagged {frac_g:.3%} of its tuples (> {max_flag_frac:.1%}): {st}"

@@ -30,6 +30,20 @@ def test_shard_tiles_partition():
         assert max(sizes) - min(sizes) <= tile
 
 
+def test_shard_grid_tiles_partition():
+    """64 x 64 tiles of a row-major grid, round-robin: a partition of the queries, every tile square and whole."""
+    for w, h, world in [(256, 256, 8), (1024, 1024, 8), (100, 70, 3), (64, 64, 2), (1, 1, 4)]:
+        parts = [D.shard_grid_tiles(w, h, world, r) for r in range(world)]
+        allq = np.sort(np.concatenate(parts))
+        assert np.array_equal(allq, np.arange(w * h))
+        ntiles = ((w + 63) // 64) * ((h + 63) // 64)
+        for r, p in enumerate(parts):
+            assert len(p) <= ((ntiles - r + world - 1) // world) * 64 * 64
+            if len(p):
+                y, x = np.divmod(p[:64 * 64], w)
+                assert y.max() - y.min() < 64 and x.max() - x.min() < 64  # first tile is a 64 x 64 block
+
+
 def _worker(rank, world, port, ret):
     import torch
     import torch.distributed as dist
@@ -45,10 +59,17 @@ def _worker(rank, world, port, ret):
     idx = D.shard_tiles(nq, world, rank, tile=5)
     r = oracle.solve(w.mesh, "R", ep[idx], cfg=oracle.default_config(), nthreads=1)
     full = D.gather_per_query(torch.as_tensor(r.per_query), idx, nq)
-    cnt = D.allreduce_counters({"admissible": r.report["admissible"], "pairs": r.report["pairs_in"]}, "cpu")
+    cnt = D.allreduce_counters({"admissible": r.report["admissible"], "pairs": r.report["pairs_in"],
+                                "big": (1 << 60) + rank}, "cpu")
+    # solution rows (query, u, v) gathered in chunks of 3 rows: ragged counts, many rounds
+    rows = torch.as_tensor(np.c_[idx[r.query], r.bary])
+    allrows = D.gather_rows(rows, chunk=3)
+    mx, mean = D.allreduce_max_mean(float(rank + 1), "cpu")
     if rank == 0:
         ret["full"] = full.numpy().tolist()
         ret["cnt"] = cnt
+        ret["rows"] = allrows.numpy().tolist()
+        ret["maxmean"] = (mx, mean)
     dist.barrier()
     dist.destroy_process_group()
 
@@ -68,3 +89,9 @@ def test_gather_matches_single_process():
     assert np.array_equal(np.array(ret["full"]), ref.per_query)
     assert ret["cnt"]["admissible"] == ref.report["admissible"]
     assert ret["cnt"]["pairs"] == ref.report["pairs_in"]
+    assert ret["cnt"]["big"] == 2 * (1 << 60) + 1  # exact int64 reduction (a float64 sum would round)
+    rows = np.array(ret["rows"])
+    got = sorted(map(tuple, rows))
+    want = sorted(map(tuple, np.c_[ref.query, ref.bary]))
+    assert got == want
+    assert ret["maxmean"] == (2.0, 1.5)

@@ -1,6 +1,8 @@
 """GPU (CUDA path through the C-ABI) vs oracle parity — needs a B200.
 
-Inputs are the seeded synthetic workloads; the oracle is the plain FP64 CPU transcription.
+Inputs are the seeded synthetic workloads; the oracle is the plain FP64 CPU transcription.  Every comparison
+goes through tests/parity.py, which bounds each side's flagged fraction (2%), the tuples flagged on one side
+only, and requires a minimum number of compared unflagged chains.
 """
 import numpy as np
 import pytest
@@ -42,16 +44,62 @@ def _gpu_solve(sp, torch, mesh, chain, ep, cfg=None, offsets=None, tri_ids=None,
     return out
 
 
+def _restrict(g, qs, k):
+    """The GPU result of a full-size run restricted to the sampled queries qs (renumbered 0..len(qs)-1), with the
+    sampled queries' work list as a CSR tuple list the oracle can solve (the identical tuples)."""
+    remap = {int(q): i for i, q in enumerate(qs)}
+    sel = np.isin(g["query"], qs)
+    fsel = np.isin(g["flagged_query"], qs)
+    pq, pt = g["worklist"]
+    wsel = np.isin(pq, qs)
+    wq = np.array([remap[int(q)] for q in pq[wsel]], np.uint32)
+    wt = pt[wsel]
+    order = np.argsort(wq, kind="stable")
+    wq, wt = wq[order], wt[order]
+    offsets = np.zeros(len(qs) + 1, np.uint32)
+    np.add.at(offsets, wq + 1, 1)
+    offsets = np.cumsum(offsets).astype(np.uint32)
+    out = {"query": np.array([remap[int(q)] for q in g["query"][sel]], np.uint32), "tuple": g["tuple"][sel],
+           "bary": g["bary"][sel], "per_query": g["per_query"][qs], "contribution": g["contribution"][sel],
+           "residual": g["residual"][sel],
+           "flagged_query": np.array([remap[int(q)] for q in g["flagged_query"][fsel]], np.uint32),
+           "flagged_tuple": g["flagged_tuple"][fsel], "worklist": (wq, wt)}
+    return out, offsets, np.ascontiguousarray(wt.reshape(-1)).astype(np.uint32), int(wsel.sum())
+
+
+def test_sqrt_table_device_copy_matches_golden(sp, torch_cuda):
+    """The kernels' constant-memory copy of the Eq. 20 sqrt surrogate (reading R8) is the golden table."""
+    import os
+    g = np.loadtxt(os.path.join(os.path.dirname(__file__), "golden", "sqrt_table.txt"))
+    with sp.Context(0) as ctx:
+        assert np.array_equal(sp.sqrt_table(ctx), g[:, :5])
+
+
 def test_c1_patch_parity(orc, sp, torch_cuda):
     w = W.patch_c1()
     ro = orc.solve(w.mesh, "R", w.endpoints, cfg=orc.default_config(cull=0))
     g = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints, cfg=sp.default_config(cull=0))
-    st = parity.compare(ro, g, w.nqueries)
+    parity.compare(ro, g, w.nqueries, min_compared=1, label="C1")
     assert g["report"]["n_pairs_in"] == w.mesh.ntris
-    assert st["compared_solutions"] >= 1
     # culled run finds the same chains
     gc = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
-    parity.compare(ro, gc, w.nqueries)
+    parity.compare(ro, gc, w.nqueries, min_compared=1, label="C1 culled")
+
+
+def test_flat_mirror_fixture_on_gpu(orc, sp, torch_cuda):
+    """SURVEY §8(c) fixed point 1 on the GPU: the relabel decision (reading R1) picks e_2, a(., 1/3)
+    is identically zero and the b fallback (c11) gives u = 1/2: x_1 = (0.5, 0, 0), (u, v) = (0.5, 1/3),
+    J = (d_0 + d_1)^2."""
+    pos = np.array([[-1, -1, 0], [2, -1, 0], [-1, 2, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    mesh = W.Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32))
+    ep = np.array([[[0, 0, 1], [1, 0, 1]]], float)
+    g = _gpu_solve(sp, torch_cuda, mesh, "R", ep, cfg=sp.default_config(cull=0))
+    assert g["query"].shape[0] == 1 and len(g["flagged_query"]) == 0
+    assert np.allclose(g["bary"][0], [0.5, 1 / 3], atol=1e-9)
+    assert np.isclose(1 / g["contribution"][0], (2 * np.sqrt(1.25)) ** 2, rtol=1e-8)
+    ro = orc.solve(mesh, "R", ep, cfg=orc.default_config(cull=0))
+    parity.compare(ro, g, 1, min_compared=1, label="S:520")
 
 
 def test_random_interpolated_R(orc, sp, torch_cuda):
@@ -64,12 +112,11 @@ def test_random_interpolated_R(orc, sp, torch_cuda):
     inten = rng.uniform(0.5, 2.0, Q)
     ro = orc.solve(mesh, "R", ep, intensity=inten, cfg=orc.default_config(cull=0))
     g = _gpu_solve(sp, torch_cuda, mesh, "R", ep, cfg=sp.default_config(cull=0), intensity=inten)
-    st = parity.compare(ro, g, Q)
-    assert st["compared_solutions"] > 50, st
+    parity.compare(ro, g, Q, min_compared=50, label="random R")
     # with the cull on both sides
     ro2 = orc.solve(mesh, "R", ep, intensity=inten)
     g2 = _gpu_solve(sp, torch_cuda, mesh, "R", ep, intensity=inten)
-    parity.compare(ro2, g2, Q)
+    parity.compare(ro2, g2, Q, min_compared=50, label="random R culled")
     # cull soundness: every oracle chain's (query, tuple) is in the GPU work list
     wl = set(zip(g2["worklist"][0].tolist(), g2["worklist"][1][:, 0].tolist()))
     assert all((int(q), int(t)) in wl for q, t in zip(ro2.query, ro2.tuple[:, 0]))
@@ -79,15 +126,16 @@ def test_explicit_tuple_list_and_edges(orc, sp, torch_cuda):
     w = W.patch_c1()
     ep = np.repeat(w.endpoints, 3, axis=0)
     ep[1, 1] += [0.05, -0.02, 0.0]
-    # ragged CSR: 0 tuples for query 2
-    ids = np.arange(0, 256, 3, dtype=np.uint32)
-    offsets = np.array([0, len(ids), 2 * len(ids), 2 * len(ids)], np.uint32)
-    tri_ids = np.concatenate([ids, ids])
+    # ragged CSR: every triangle for query 0, every third for query 1, 0 tuples for query 2
+    ids0 = np.arange(0, 256, dtype=np.uint32)
+    ids1 = np.arange(0, 256, 3, dtype=np.uint32)
+    offsets = np.array([0, len(ids0), len(ids0) + len(ids1), len(ids0) + len(ids1)], np.uint32)
+    tri_ids = np.concatenate([ids0, ids1])
     ro = orc.solve(w.mesh, "R", ep, offsets=offsets, tri_ids=tri_ids)
     g = _gpu_solve(sp, torch_cuda, w.mesh, "R", ep, offsets=offsets, tri_ids=tri_ids)
-    parity.compare(ro, g, 3)
+    parity.compare(ro, g, 3, min_compared=1, label="explicit list")
     assert g["per_query"][2] == 0.0
-    assert g["report"]["n_pairs_in"] == 2 * len(ids)
+    assert g["report"]["n_pairs_in"] == len(tri_ids)
 
 
 def test_empty_and_errors(sp, torch_cuda):
@@ -99,6 +147,17 @@ def test_empty_and_errors(sp, torch_cuda):
     assert r.n_solutions == 0
     with pytest.raises(sp.SpolyError):
         ctx.solve("Q", torch.zeros((1, 2, 3), dtype=torch.float64, device="cuda"))
+    # a triangle id out of range in an explicit tuple list: an error status, and the context stays usable
+    ep = torch.as_tensor(w.endpoints, dtype=torch.float64, device="cuda")
+    off = torch.as_tensor(np.array([0, 2], np.int32), device="cuda")
+    bad_ids = torch.as_tensor(np.array([3, 100000], np.int32), device="cuda")
+    with pytest.raises(sp.SpolyError):
+        ctx.solve("R", ep, None, off, bad_ids)
+    bad_off = torch.as_tensor(np.array([2, 1], np.int32), device="cuda")
+    with pytest.raises(sp.SpolyError):
+        ctx.solve("R", ep, None, bad_off, bad_ids)
+    r = ctx.solve("R", ep)
+    assert r.n_solutions >= 1
     bad = W.Mesh(np.zeros((3, 3), np.float32), np.tile([0, 0, 1], (3, 1)).astype(np.float32),
                  np.array([[0, 1, 2]], np.uint32))
     with pytest.raises(sp.SpolyError):
@@ -112,35 +171,26 @@ def test_c2_subset_parity(orc, sp, torch_cuda):
     sub = w.subset(np.arange(0, 65536, 65536 // 24)[:24])
     ro = orc.solve(sub.mesh, "R", sub.endpoints)
     g = _gpu_solve(sp, torch_cuda, sub.mesh, "R", sub.endpoints)
-    st = parity.compare(ro, g, sub.nqueries)
-    assert st["compared_solutions"] > 1000, st
-    assert st["flagged_tuples"] <= 0.01 * g["report"]["n_pairs_in"], st
+    parity.compare(ro, g, sub.nqueries, min_compared=1000, label="C2 subset")
 
 
 def test_c2_full_size_sampled(orc, sp, torch_cuda):
-    """Full C2 (65,536 queries) in the bench launch configuration; sampled queries re-solved by the oracle."""
+    """Full C2 (65,536 queries) in the bench launch configuration; sampled queries re-solved by the oracle (its own
+    cull), properties checked on every returned chain."""
     w = W.glints_c2(res=256)
     g = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
-    rng = np.random.default_rng(99)
-    qs = np.sort(rng.choice(w.nqueries, 6, replace=False))
+    qs = np.sort(np.random.default_rng(99).choice(w.nqueries, 6, replace=False))
     sub = w.subset(qs)
     ro = orc.solve(sub.mesh, "R", sub.endpoints)
-    # restrict the GPU result to the sampled queries, renumbered 0..5
-    sel = np.isin(g["query"], qs)
-    remap = {int(q): i for i, q in enumerate(qs)}
-    gs = {"query": np.array([remap[int(q)] for q in g["query"][sel]], np.uint32), "tuple": g["tuple"][sel],
-          "bary": g["bary"][sel], "per_query": g["per_query"][qs]}
-    fsel = np.isin(g["flagged_query"], qs)
-    gs["flagged_query"] = np.array([remap[int(q)] for q in g["flagged_query"][fsel]], np.uint32)
-    gs["flagged_tuple"] = g["flagged_tuple"][fsel]
-    gs["contribution"] = g["contribution"][sel]
-    st = parity.compare(ro, gs, len(qs))
-    assert st["compared_solutions"] > 100
+    gs, _, _, npairs = _restrict(g, qs, 1)
+    parity.compare(ro, gs, len(qs), min_compared=100, gpu_pairs=npairs, label="C2 full sampled")
     # properties at full size: every returned vertex inside the triangle and specular (Eq. 3)
     assert np.all(g["residual"] < 1e-6)
     b = g["bary"]
     assert np.all(b[:, 0] >= -1e-9) and np.all(b[:, 1] >= -1e-9) and np.all(b.sum(1) <= 1 + 1e-9)
     assert abs(g["per_query"].sum() - g["contribution"].sum()) <= 1e-9 * abs(g["contribution"].sum())
+    assert g["report"]["n_truncated"] == 0
+    assert len(g["flagged_query"]) <= 0.02 * g["report"]["n_pairs_in"]
 
 
 # ---------------------------------------------------------------- one-bounce refraction (T, Eq. 22)
@@ -155,11 +205,10 @@ def test_random_interpolated_T(orc, sp, torch_cuda):
     ep[Q // 2:] = ep[Q // 2:, ::-1]  # half the queries from below (both media orders)
     ro = orc.solve(mesh, "T", ep, cfg=orc.default_config(cull=0))
     g = _gpu_solve(sp, torch_cuda, mesh, "T", ep, cfg=sp.default_config(cull=0))
-    st = parity.compare(ro, g, Q)
-    assert st["compared_solutions"] > 30, st
+    parity.compare(ro, g, Q, min_compared=30, label="random T")
     ro2 = orc.solve(mesh, "T", ep)
     g2 = _gpu_solve(sp, torch_cuda, mesh, "T", ep)
-    parity.compare(ro2, g2, Q)
+    parity.compare(ro2, g2, Q, min_compared=30, label="random T culled")
 
 
 def test_flat_interface_T(orc, sp, torch_cuda):
@@ -172,7 +221,7 @@ def test_flat_interface_T(orc, sp, torch_cuda):
     ep[:, 1] = np.c_[rng.uniform(-0.8, 0.8, (32, 2)), -rng.uniform(0.5, 2, 32)]
     ro = orc.solve(mesh, "T", ep, cfg=orc.default_config(cull=0))
     g = _gpu_solve(sp, torch_cuda, mesh, "T", ep, cfg=sp.default_config(cull=0))
-    parity.compare(ro, g, 32)
+    parity.compare(ro, g, 32, min_compared=32, label="flat interface")
     assert g["query"].shape[0] == 32  # exactly one refraction path per query
 
 
@@ -182,15 +231,72 @@ def test_c3_pool_subset_parity(orc, sp, torch_cuda):
     sub = w.subset(np.linspace(0, w.nqueries - 1, 48).astype(np.int64))
     ro = orc.solve(sub.mesh, "T", sub.endpoints)
     g = _gpu_solve(sp, torch_cuda, sub.mesh, "T", sub.endpoints)
-    st = parity.compare(ro, g, sub.nqueries)
-    assert st["compared_solutions"] >= 20, st
+    parity.compare(ro, g, sub.nqueries, min_compared=20, label="C3 subset")
     assert np.all(g["residual"] < 1e-6)
 
 
+def test_near_tangent_flags_at_folds_on_gpu(orc, sp, torch_cuda):
+    """Fold configurations of a focusing interpolated-normal mirror (located by the oracle, pinned in
+    test_oracle_pins_k2.py::test_near_tangent_flag_at_folds): the GPU flags NEAR_TANGENT there too, and the
+    flag-aware parity holds on every configuration of the walk."""
+    mesh = W.Mesh(*_concave_mirror_arrays())
+    rng = np.random.default_rng(0)
+    Q = 4000
+    ep = np.zeros((Q, 2, 3))
+    ep[:, 0] = rng.uniform(-2, 2, (Q, 3)) * [1, 1, 0] + [0, 0, 1] * rng.uniform(0.2, 3, (Q, 1))
+    ep[:, 1] = rng.uniform(-2, 2, (Q, 3)) * [1, 1, 0] + [0, 0, 1] * rng.uniform(0.2, 3, (Q, 1))
+    cfg = orc.default_config(cull=0)
+    r = orc.solve(mesh, "R", ep, cfg=cfg)
+    two = np.where(np.bincount(r.query, minlength=Q) == 2)[0]
+    fold_eps = []
+    for q in two[:6]:
+        x0, x2 = ep[q]
+        for trial in range(6):
+            d = rng.normal(size=3)
+            d /= np.linalg.norm(d)
+            walk = np.array([[x0, x2 + s * d] for s in np.linspace(0, 1, 101)[1:]])
+            rw = orc.solve(mesh, "R", walk, cfg=cfg)
+            cnt = np.bincount(rw.query, minlength=len(walk))
+            if cnt[0] != 2 or not np.any(cnt != 2):
+                continue
+            j = int(np.argmax(cnt != 2))
+            if cnt[j] != 0:
+                continue
+            lo, hi = (j) / 100.0, (j + 1) / 100.0
+            for _ in range(60):
+                m = 0.5 * (lo + hi)
+                rm = orc.solve(mesh, "R", np.array([[x0, x2 + m * d]]), cfg=cfg)
+                if rm.n_solutions == 2:
+                    lo = m
+                else:
+                    hi = m
+            ra = orc.solve(mesh, "R", np.array([[x0, x2 + lo * d]]), cfg=cfg)
+            if ra.n_solutions == 2 and np.max(np.abs(ra.bary[0] - ra.bary[1])) < 1e-3:
+                fold_eps += [[x0, x2 + lo * d], [x0, x2 + hi * d], [x0, x2 + 0.5 * lo * d]]
+            break
+    assert len(fold_eps) >= 6
+    fe = np.array(fold_eps)
+    ro = orc.solve(mesh, "R", fe, cfg=cfg)
+    g = _gpu_solve(sp, torch_cuda, mesh, "R", fe, cfg=sp.default_config(cull=0))
+    gflag = {int(q): int(f) for q, f in zip(g["flagged_query"], g["flagged_flags"])}
+    for i in range(0, len(fe), 3):
+        assert gflag.get(i, 0) & sp.FLAG_NEAR_TANGENT and gflag.get(i + 1, 0) & sp.FLAG_NEAR_TANGENT, (i, gflag)
+    # the flagged fraction here is 2/3 by construction: only the one-sided flags and the counts are held
+    parity.compare(ro, g, len(fe), min_compared=1, max_flag_frac=1.0, label="folds")
+
+
+def _concave_mirror_arrays(kappa=0.8):
+    P = np.array([[-1, -1, 0], [1.2, -0.9, 0], [-0.8, 1.1, 0]], float)
+    c = P.mean(0)
+    N = np.array([np.array([0, 0, 1.0]) - kappa * (p - c) for p in P])
+    N /= np.linalg.norm(N, axis=1)[:, None]
+    return P.astype(np.float32), N.astype(np.float32), np.array([[0, 1, 2]], np.uint32)
+
+
 # ---------------------------------------------------------------- two bounces (RR, TT; 100-piece scan)
-def _planted_batch(chain, n, seed, size=0.15):
+def _planted_batch(chain, n, seed, size=0.15, face=False):
     from planted import planted_many
-    cases = planted_many(seed, chain, n, size=size)
+    cases = planted_many(seed, chain, n, size=size, face=face)
     pos, nrm, tri, eps = [], [], [], []
     for i, (m, ids, x0, xk1, bary) in enumerate(cases):
         pos.append(m.pos)
@@ -205,9 +311,10 @@ def _planted_batch(chain, n, seed, size=0.15):
     ids = []
     for i in range(len(cases)):
         tl = [(2 * i, 2 * i + 1)]
-        for _ in range(2):  # decoy pairs from other configurations
+        while len(tl) < 3:  # two distinct decoy pairs from other configurations
             j, l = rng.integers(0, len(cases), 2)
-            tl.append((2 * int(j), 2 * int(l) + 1))
+            if (2 * int(j), 2 * int(l) + 1) not in tl:
+                tl.append((2 * int(j), 2 * int(l) + 1))
         for a, b in tl:
             ids += [a, b]
         offsets.append(offsets[-1] + len(tl))
@@ -216,11 +323,10 @@ def _planted_batch(chain, n, seed, size=0.15):
 
 @pytest.mark.parametrize("chain", ["RR", "TT", "RT", "TR"])
 def test_two_bounce_planted_parity(orc, sp, torch_cuda, chain):
-    mesh, ep, off, ids, truth = _planted_batch(chain, 16 if chain[0] == "R" else 8, 61)
+    mesh, ep, off, ids, truth = _planted_batch(chain, 40, 61)
     ro = orc.solve(mesh, chain, ep, offsets=off, tri_ids=ids)
     g = _gpu_solve(sp, torch_cuda, mesh, chain, ep, offsets=off, tri_ids=ids)
-    st = parity.compare(ro, g, len(ep), tol_bary=1e-4)
-    assert st["compared_solutions"] >= len(ep) // 2, st
+    parity.compare(ro, g, len(ep), tol_bary=1e-4, min_compared=int(0.85 * len(ep)), label=f"planted {chain}")
     assert np.all(g["residual"] < 1e-6)
     # the planted chain is recovered on the GPU for most queries (100-piece scan misses are by design)
     hit = 0
@@ -228,7 +334,32 @@ def test_two_bounce_planted_parity(orc, sp, torch_cuda, chain):
         sel = g["query"] == qi
         if any(np.max(np.abs(x - b)) < 1e-6 for x in g["bary"][sel]):
             hit += 1
-    assert hit >= int(0.85 * len(truth)), (hit, len(truth))
+    assert hit >= int(0.9 * len(truth)), (hit, len(truth))
+
+
+@pytest.mark.parametrize("chain", ["RR", "RT", "TR", "TT"])
+def test_face_mode_planted_on_gpu(orc, sp, torch_cuda, chain):
+    """Face-normal triangles (reading R22): 40/40 planted chains recovered unflagged on the GPU, parity
+    with the oracle; RR on flat face mirrors has J = L^2 (unfolded path length)."""
+    mesh, ep, off, ids, truth = _planted_batch(chain, 40, 171, face=True)
+    ro = orc.solve(mesh, chain, ep, offsets=off, tri_ids=ids)
+    g = _gpu_solve(sp, torch_cuda, mesh, chain, ep, offsets=off, tri_ids=ids)
+    parity.compare(ro, g, len(ep), tol_bary=1e-4, min_compared=len(ep), label=f"face {chain}")
+    for qi, b in enumerate(truth):
+        sel = (g["query"] == qi) & (g["tuple"][:, 0] == 2 * qi) & (g["tuple"][:, 1] == 2 * qi + 1)
+        d = [np.max(np.abs(x - b)) for x in g["bary"][sel]]
+        assert d and min(d) < 1e-6, (qi, d)
+        assert not np.any((g["flagged_query"] == qi) & (g["flagged_tuple"][:, 0] == 2 * qi)
+                          & (g["flagged_tuple"][:, 1] == 2 * qi + 1))
+        if chain == "RR":
+            i = np.flatnonzero(sel)[int(np.argmin(d))]
+            bb = g["bary"][i]
+            P1 = mesh.pos[mesh.tri[2 * qi]].astype(float)
+            P2 = mesh.pos[mesh.tri[2 * qi + 1]].astype(float)
+            x1 = P1[0] + bb[0] * (P1[1] - P1[0]) + bb[1] * (P1[2] - P1[0])
+            x2 = P2[0] + bb[2] * (P2[1] - P2[0]) + bb[3] * (P2[2] - P2[0])
+            L = np.linalg.norm(x1 - ep[qi, 0]) + np.linalg.norm(x2 - x1) + np.linalg.norm(ep[qi, 1] - x2)
+            assert abs((1 / g["contribution"][i]) / (L * L) - 1) < 1e-6
 
 
 @pytest.mark.parametrize("chain", ["RR", "TT"])
@@ -240,7 +371,7 @@ def test_two_bounce_cull_sound_on_planted(orc, sp, torch_cuda, chain):
     for qi in range(len(ep)):
         assert np.any((pq == qi) & (pt[:, 0] == 2 * qi) & (pt[:, 1] == 2 * qi + 1)), qi
     ro = orc.solve(mesh, chain, ep)  # the oracle's own cull
-    parity.compare(ro, g, len(ep), tol_bary=1e-4)
+    parity.compare(ro, g, len(ep), tol_bary=1e-4, min_compared=int(0.8 * len(ep)), label=f"cull {chain}")
 
 
 def test_rr_mirrors_parity(orc, sp, torch_cuda):
@@ -249,18 +380,54 @@ def test_rr_mirrors_parity(orc, sp, torch_cuda):
     sub = w.subset(np.arange(0, 64, 8))
     ro = orc.solve(sub.mesh, "RR", sub.endpoints)
     g = _gpu_solve(sp, torch_cuda, sub.mesh, "RR", sub.endpoints)
-    st = parity.compare(ro, g, sub.nqueries, tol_bary=1e-4)
-    assert st["compared_solutions"] >= 10, st
+    parity.compare(ro, g, sub.nqueries, tol_bary=1e-4, min_compared=10, label="RR mirrors")
     assert g["report"]["n_pairs_in"] >= ro.report["pairs_in"]
 
 
 def test_tt_sphere_parity(orc, sp, torch_cuda):
     """C4-shaped dielectric icosphere (level 2, 320 tris), TT through it: GPU cull + solve vs the oracle."""
-    w = W.sphere_c4(res=4, level=2)
-    sub = w.subset([5, 6])
+    w = W.sphere_c4(res=8, level=2)
+    sub = w.subset([18, 19, 20, 27, 28, 29, 36, 37])
     ro = orc.solve(sub.mesh, "TT", sub.endpoints)
     g = _gpu_solve(sp, torch_cuda, sub.mesh, "TT", sub.endpoints)
-    parity.compare(ro, g, sub.nqueries, tol_bary=1e-4)
+    parity.compare(ro, g, sub.nqueries, tol_bary=1e-4, min_compared=8, label="TT sphere L2")
+
+
+def test_tt_big_order_branch(orc, sp, torch_cuda):
+    """Level-1 icosphere (80 large triangles): about half the TT tuples keep a numerical Bezout order n > 32
+    (reading R6), which the scan evaluates with the shared-memory elimination; the report's counter proves the
+    branch ran, and the parity holds on those tuples too."""
+    w = W.sphere_c4(res=8, level=1)
+    sub = w.subset([18, 19, 27, 28, 36, 37])
+    ro = orc.solve(sub.mesh, "TT", sub.endpoints)
+    g = _gpu_solve(sp, torch_cuda, sub.mesh, "TT", sub.endpoints)
+    assert g["report"]["n_big_scan"] > 0, g["report"]
+    parity.compare(ro, g, sub.nqueries, tol_bary=1e-4, min_compared=4, label="TT sphere L1 (n > 32)")
+
+
+@pytest.mark.parametrize("name,make,nsample", [("C4", lambda: W.sphere_c4(res=128, level=4), 8),
+                                               ("C5", lambda: W.shell_c5(res=128, level=3), 8)])
+def test_two_bounce_full_size_sampled(orc, sp, torch_cuda, name, make, nsample):
+    """Full-size k=2 frames in the bench launch configuration (C4: 16,384 receivers x 5,120-tri sphere, TT; C5 shell
+    at the bench's 16,384 receivers): sampled receivers re-solved by the oracle on the identical tuples (the GPU's
+    refined pair list of those receivers); every returned chain satisfies Eq. 3 and the domain, and no per-tuple
+    capacity was hit."""
+    w = make()
+    g = _gpu_solve(sp, torch_cuda, w.mesh, "TT", w.endpoints)
+    rep = g["report"]
+    assert rep["n_admissible"] > 1000 and rep["n_truncated"] == 0
+    assert len(g["flagged_query"]) <= 0.02 * rep["n_pairs_in"], (len(g["flagged_query"]), rep["n_pairs_in"])
+    # sampled receivers: those with chains, spread over the frame
+    with_sol = np.unique(g["query"])
+    qs = np.sort(np.random.default_rng(5).choice(with_sol, nsample, replace=False))
+    gs, off, ids, npairs = _restrict(g, qs, 2)
+    sub = w.subset(qs)
+    ro = orc.solve(sub.mesh, "TT", sub.endpoints, offsets=off, tri_ids=ids)
+    parity.compare(ro, gs, len(qs), tol_bary=1e-4, min_compared=nsample, gpu_pairs=npairs, label=f"{name} full sampled")
+    assert np.all(g["residual"] < 1e-6)
+    b = g["bary"]
+    for c in (0, 2):
+        assert np.all(b[:, c] >= -1e-9) and np.all(b[:, c + 1] >= -1e-9) and np.all(b[:, c] + b[:, c + 1] <= 1 + 1e-9)
 
 
 def test_c3_full_size_sampled(orc, sp, torch_cuda):
@@ -271,22 +438,16 @@ def test_c3_full_size_sampled(orc, sp, torch_cuda):
     qs = np.sort(np.random.default_rng(7).choice(w.nqueries, 24, replace=False))
     sub = w.subset(qs)
     ro = orc.solve(sub.mesh, "T", sub.endpoints)
-    sel = np.isin(g["query"], qs)
-    remap = {int(q): i for i, q in enumerate(qs)}
-    fsel = np.isin(g["flagged_query"], qs)
-    gs = {"query": np.array([remap[int(q)] for q in g["query"][sel]], np.uint32), "tuple": g["tuple"][sel],
-          "bary": g["bary"][sel], "per_query": g["per_query"][qs], "contribution": g["contribution"][sel],
-          "flagged_query": np.array([remap[int(q)] for q in g["flagged_query"][fsel]], np.uint32),
-          "flagged_tuple": g["flagged_tuple"][fsel]}
-    st = parity.compare(ro, gs, len(qs))
-    assert st["compared_solutions"] >= 12
+    gs, _, _, npairs = _restrict(g, qs, 1)
+    parity.compare(ro, gs, len(qs), min_compared=12, gpu_pairs=npairs, label="C3 full sampled")
     assert np.all(g["residual"] < 1e-6)
     b = g["bary"]
     assert np.all(b[:, 0] >= -1e-9) and np.all(b[:, 1] >= -1e-9) and np.all(b.sum(1) <= 1 + 1e-9)
+    assert len(g["flagged_query"]) <= 0.02 * g["report"]["n_pairs_in"]
 
 
 def test_determinism_bit_identical(sp, torch_cuda):
-    """deterministic=1: two solves of the same inputs give bit-identical outputs."""
+    """Two solves of the same inputs give bit-identical outputs."""
     w = W.glints_c2(res=32)
     a = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
     b = _gpu_solve(sp, torch_cuda, w.mesh, "R", w.endpoints)
