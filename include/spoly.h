@@ -77,6 +77,10 @@ typedef struct {
                             work list is the unchunked one); SPOLY_ERR_CAPACITY if one query
                             alone exceeds it                                                */
   int cull_levels;       /* k=2: barycentric subdivision levels re-testing each kept pair; 3 */
+  int visibility;        /* 1: the path phase's visibility test: a chain with a blocked segment
+                            x_i -> x_{i+1} is dropped (scene = the specular mesh + the occluders of
+                            spoly_upload_occluders; the chain's own triangles at a segment's ends are skipped;
+                            a hit is t in (1e-7, 1 - 1e-7) inside the closed triangle); 0 (default)          */
 } spoly_config;
 
 /* Fills cfg with the defaults listed above.  Never fails for a non-NULL cfg. */
@@ -99,6 +103,12 @@ const char* spoly_last_error(const spoly_ctx* ctx);
 spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts,
                                const uint32_t* tri, uint32_t ntris, float eta_front, float eta_back,
                                uint32_t* mesh_id);
+
+/* Uploads (HOST pointers, copied) an occluder-only mesh for the visibility test (cfg.visibility): triangles that
+ * block segments but are never specular (no normals).  pos: nverts x 3 float32, tri: ntris x 3 uint32.  ntris = 0
+ * removes the occluders.  The specular mesh always occludes as well. */
+spoly_status spoly_upload_occluders(spoly_ctx* ctx, const float* pos, uint32_t nverts, const uint32_t* tri,
+                                    uint32_t ntris);
 
 /* Optional explicit tuple list (device pointers): CSR offsets[nqueries+1] into tri_ids, which holds
  * k uint32 triangle ids per tuple (ORIGINAL mesh indices). */
@@ -142,6 +152,7 @@ typedef struct {
                                          shared-memory determinant                                    */
   uint64_t n_eval_deep;               /* one bounce: FMA terms of the deep jobs' root isolation (the
                                          monotone jobs' Newton terms are in n_eval_terms)              */
+  uint64_t n_rej_visibility;          /* admissible chains dropped by the visibility test             */
 } spoly_report;
 
 typedef struct {

@@ -42,7 +42,7 @@ class Config(ctypes.Structure):
                 ("polish_iters", ctypes.c_int), ("theta_admit", ctypes.c_double), ("theta_final", ctypes.c_double),
                 ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
                 ("cull", ctypes.c_int), ("cull_margin", ctypes.c_double),
-                ("cull_levels", ctypes.c_int)]
+                ("cull_levels", ctypes.c_int), ("visibility", ctypes.c_int)]
 
 
 def lib():
@@ -54,7 +54,8 @@ def lib():
             P = ctypes.c_void_p
             L.orc_solve.restype = P
             L.orc_solve.argtypes = [P, P, ctypes.c_uint32, P, ctypes.c_uint32, ctypes.c_float, ctypes.c_float,
-                                    ctypes.c_char_p, P, ctypes.c_uint32, P, P, P, P, ctypes.c_int]
+                                    ctypes.c_char_p, P, ctypes.c_uint32, P, P, P, P, ctypes.c_int, P,
+                                    ctypes.c_uint32, P, ctypes.c_uint32]
             L.orc_free.argtypes = [P]
             for f in ("orc_n_solutions", "orc_n_flagged"):
                 getattr(L, f).restype = ctypes.c_uint64
@@ -121,11 +122,12 @@ class Result:
 
 
 REPORT_KEYS = ["pairs_in", "systems", "vroots", "candidates", "rej_domain", "rej_constraint", "rej_side",
-               "rej_kappa", "flagged", "admissible"]
+               "rej_kappa", "flagged", "admissible", "rej_visibility"]
 
 
 def solve(mesh, chain: str, endpoints: np.ndarray, intensity=None, offsets=None, tri_ids=None, cfg: Config = None,
-          nthreads: int = 0) -> Result:
+          nthreads: int = 0, occluders=None) -> Result:
+    """occluders: optional non-specular Mesh blocking segments when cfg.visibility."""
     L = lib()
     pos = np.ascontiguousarray(mesh.pos, dtype=np.float32)
     nrm = np.ascontiguousarray(mesh.nrm, dtype=np.float32)
@@ -136,8 +138,13 @@ def solve(mesh, chain: str, endpoints: np.ndarray, intensity=None, offsets=None,
     off = None if offsets is None else np.ascontiguousarray(offsets, dtype=np.uint32)
     ids = None if tri_ids is None else np.ascontiguousarray(tri_ids, dtype=np.uint32)
     cfg = cfg or default_config()
+    opos = otri = None
+    if occluders is not None:
+        opos = np.ascontiguousarray(occluders.pos, dtype=np.float32)
+        otri = np.ascontiguousarray(occluders.tri, dtype=np.uint32)
     h = L.orc_solve(_p(pos), _p(nrm), pos.shape[0], _p(tri), tri.shape[0], mesh.eta_front, mesh.eta_back,
-                    chain.encode(), _p(ep), nq, _p(inten), _p(off), _p(ids), ctypes.byref(cfg), nthreads)
+                    chain.encode(), _p(ep), nq, _p(inten), _p(off), _p(ids), ctypes.byref(cfg), nthreads,
+                    _p(opos), 0 if opos is None else opos.shape[0], _p(otri), 0 if otri is None else otri.shape[0])
     if not h:
         raise ValueError("oracle rejected the input")
     try:
@@ -157,7 +164,7 @@ def solve(mesh, chain: str, endpoints: np.ndarray, intensity=None, offsets=None,
         L.orc_get_flagged(h, _p(fq), _p(ft), _p(ff))
         pq = np.zeros(nq, np.float64)
         L.orc_get_per_query(h, _p(pq))
-        rep = np.zeros(10, np.uint64)
+        rep = np.zeros(11, np.uint64)
         L.orc_get_report(h, _p(rep))
         nw = L.orc_n_worklist(h)
         wq = np.zeros(nw, np.uint32)

@@ -638,8 +638,8 @@ struct Sol {
   uint32_t flags;
 };
 struct Counters {
-  uint64_t c[10] = {0};  // pairs_in, systems, vroots, candidates, rej_domain, rej_constraint, rej_side,
-                         // rej_kappa, flagged, admissible
+  uint64_t c[11] = {0};  // pairs_in, systems, vroots, candidates, rej_domain, rej_constraint, rej_side,
+                         // rej_kappa, flagged, admissible, rej_visibility
 };
 struct TupleResult {
   vector<Sol> sols;
@@ -1138,7 +1138,7 @@ struct orc_result {
   uint32_t nq = 0;
   vector<uint32_t> q, tup, flags, fq, ftup, fflags, wq, wtup;
   vector<double> bary, contrib, resid, per_query;
-  uint64_t counters[10] = {0};
+  uint64_t counters[11] = {0};
 };
 
 extern "C" {
@@ -1156,6 +1156,7 @@ void orc_default_config(orc_config* c) {
   c->cull = 1;
   c->cull_margin = 1e-9;
   c->cull_levels = 3;
+  c->visibility = 0;
 }
 
 static vector<Tri> mesh_tris(const float* pos, const float* nrm, const uint32_t* tri, const uint32_t* ids, int k) {
@@ -1171,10 +1172,54 @@ static vector<Tri> mesh_tris(const float* pos, const float* nrm, const uint32_t*
   return out;
 }
 
+// ------------------------------------------------------------------ visibility (Sec. 5.3)
+// "An admissible path will be rejected when the ray from any vertex x_i towards the next vertex x_{i+1} is blocked."
+// Plain brute force: the segment x_i -> x_{i+1} against every scene triangle (the specular mesh and the optional
+// occluder mesh), Moller-Trumbore, a hit iff t in (kVisEps, 1 - kVisEps) and the hit inside the closed triangle; the
+// chain's own triangles at the segment's two endpoints are skipped (the vertices lie on them).
+constexpr double kVisEps = 1e-7;
+static bool segment_hits(V3 a, V3 b, const V3 p[3]) {
+  V3 d = b - a, e1 = p[1] - p[0], e2 = p[2] - p[0];
+  V3 P = cross(d, e2);
+  double det = dot(e1, P);
+  if (det == 0) return false;
+  V3 s = a - p[0];
+  double u = dot(s, P) / det;
+  V3 Q = cross(s, e1);
+  double v = dot(d, Q) / det;
+  double t = dot(e2, Q) / det;
+  return t > kVisEps && t < 1 - kVisEps && u >= 0 && v >= 0 && u + v <= 1;
+}
+struct Scene {
+  const float *pos, *opos;
+  const uint32_t *tri, *otri;
+  uint32_t ntris, ontris;
+  void corners(const float* P, const uint32_t* T, uint32_t t, V3 out[3]) const {
+    for (int j = 0; j < 3; ++j) {
+      uint32_t vi = T[3 * t + j];
+      out[j] = {(double)P[3 * vi], (double)P[3 * vi + 1], (double)P[3 * vi + 2]};
+    }
+  }
+  bool blocked(V3 a, V3 b, int64_t skip1, int64_t skip2) const {
+    V3 c[3];
+    for (uint32_t t = 0; t < ntris; ++t) {
+      if ((int64_t)t == skip1 || (int64_t)t == skip2) continue;
+      corners(pos, tri, t, c);
+      if (segment_hits(a, b, c)) return true;
+    }
+    for (uint32_t t = 0; t < ontris; ++t) {
+      corners(opos, otri, t, c);
+      if (segment_hits(a, b, c)) return true;
+    }
+    return false;
+  }
+};
+
 orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri, uint32_t ntris,
                       float eta_front, float eta_back, const char* chain_c, const double* endpoints, uint32_t nq,
                       const double* intensity, const uint32_t* offsets, const uint32_t* tri_ids,
-                      const orc_config* cfg_in, int nthreads) {
+                      const orc_config* cfg_in, int nthreads, const float* occ_pos, uint32_t occ_nverts,
+                      const uint32_t* occ_tri, uint32_t occ_ntris) {
   if (!pos || !nrm || !tri || !chain_c || !endpoints) return nullptr;
   std::string chain(chain_c);
   const int k = (int)chain.size();
@@ -1183,6 +1228,10 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
     if (ch != 'R' && ch != 'T') return nullptr;
   for (uint64_t i = 0; i < 3ull * ntris; ++i)
     if (tri[i] >= nverts) return nullptr;
+  if (occ_ntris && (!occ_pos || !occ_tri)) return nullptr;
+  for (uint64_t i = 0; i < 3ull * occ_ntris; ++i)
+    if (occ_tri[i] >= occ_nverts) return nullptr;
+  const Scene scene{pos, occ_pos, tri, occ_tri, ntris, occ_ntris};
   orc_config cfg;
   if (cfg_in)
     cfg = *cfg_in;
@@ -1208,6 +1257,20 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
         for (int i = 0; i < k; ++i) P.wl.push_back(ids[i]);
         TupleResult R = solve_tuple(chain, tris, x0, xk1, eta_front, eta_back, I, cfg, P.C);
         for (const Sol& s : R.sols) {
+          if (cfg.visibility) {  // reject the chain if any segment x_i -> x_{i+1} is blocked
+            V3 x[4];
+            x[0] = x0;
+            for (int i = 0; i < k; ++i) x[i + 1] = tris[i].X(s.bary[2 * i], s.bary[2 * i + 1]);
+            x[k + 1] = xk1;
+            bool blk = false;
+            for (int i = 0; i <= k && !blk; ++i)
+              blk = scene.blocked(x[i], x[i + 1], i >= 1 ? (int64_t)ids[i - 1] : -1, i < k ? (int64_t)ids[i] : -1);
+            if (blk) {
+              P.C.c[9]--;   // no longer admissible
+              P.C.c[10]++;  // rejected by the visibility test
+              continue;
+            }
+          }
           P.sols.push_back(s);
           for (int i = 0; i < k; ++i) P.tup.push_back(ids[i]);
           P.sum += s.contribution;
@@ -1271,7 +1334,7 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
       for (int i = 0; i < k; ++i) R->wtup.push_back(P.wl[t * k + i]);
     }
     R->per_query[qi] = P.sum;
-    for (int c = 0; c < 10; ++c) R->counters[c] += P.C.c[c];
+    for (int c = 0; c < 11; ++c) R->counters[c] += P.C.c[c];
   }
   return R;
 }
@@ -1300,7 +1363,7 @@ void orc_get_worklist(const orc_result* r, uint32_t* query, uint32_t* tuple) {
   std::copy(r->wtup.begin(), r->wtup.end(), tuple);
 }
 void orc_get_per_query(const orc_result* r, double* out) { std::copy(r->per_query.begin(), r->per_query.end(), out); }
-void orc_get_report(const orc_result* r, uint64_t c[10]) { std::copy(r->counters, r->counters + 10, c); }
+void orc_get_report(const orc_result* r, uint64_t c[11]) { std::copy(r->counters, r->counters + 11, c); }
 
 // ---- pieces
 static vector<Tri> tris_from(const double* t, int k) {

@@ -34,6 +34,7 @@ typedef struct {
   int cull;              /* 1: oracle cull predicate when no tuple list is given */
   double cull_margin;    /* radians, 1e-9 */
   int cull_levels;       /* k=2 barycentric subdivision levels of the cull, 3 */
+  int visibility;        /* 1: reject chains with a blocked segment, 0 */
 } orc_config;
 
 void orc_default_config(orc_config* cfg);
@@ -49,7 +50,8 @@ orc_result* orc_solve(const float* pos, const float* nrm, uint32_t nverts, const
                       uint32_t ntris, float eta_front, float eta_back, const char* chain,
                       const double* endpoints, uint32_t nq, const double* intensity,
                       const uint32_t* offsets, const uint32_t* tri_ids, const orc_config* cfg,
-                      int nthreads);
+                      int nthreads, const float* occ_pos, uint32_t occ_nverts, const uint32_t* occ_tri,
+                      uint32_t occ_ntris /* optional non-specular occluders for the visibility test (may be 0) */);
 void orc_free(orc_result*);
 /* sizes */
 uint64_t orc_n_solutions(const orc_result*);
@@ -65,8 +67,8 @@ void orc_get_per_query(const orc_result*, double* per_query /* Q */);
 uint64_t orc_n_worklist(const orc_result*);
 void orc_get_worklist(const orc_result*, uint32_t* query, uint32_t* tuple);
 /* counters: pairs_in, systems, vroots, candidates, rej_domain, rej_constraint, rej_side,
- *           rej_kappa, flagged, admissible */
-void orc_get_report(const orc_result*, uint64_t counters[10]);
+ *           rej_kappa, flagged, admissible, rej_visibility */
+void orc_get_report(const orc_result*, uint64_t counters[11]);
 
 /* --- pieces, exported for the pins in tests/ ---------------------------- */
 /* Build the bivariate system (a,b) for one tuple (Sec. 4.5, Eqs. 21-23).

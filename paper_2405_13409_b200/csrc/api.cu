@@ -69,7 +69,14 @@ struct spoly_ctx {
   // mesh
   bool has_mesh = false;
   DeviceMesh M;
-  DBuf<TriRec> d_tris;
+  DBuf<TriRec> d_tris, d_occ;
+  DBuf<float4> d_box[kMaxAabbLevels], d_obox[kMaxAabbLevels];  // visibility hierarchies (mesh, occluders)
+  AabbTree mesh_tree, occ_tree;
+  DBuf<uint8_t> d_vkeep;
+  DBuf<uint32_t> d_vsel, d_viota;
+  DBuf<unsigned long long> d_vkey, d_vn;
+  DBuf<double> d_vbary, d_vcontrib;
+  DBuf<float> d_vresid;
   DBuf<TriCull> d_tcull;
   DBuf<uint32_t> d_orig, d_perm;
   DBuf<ClusterRec> d_cl, d_sub, d_up[4];
@@ -147,6 +154,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->max_solutions = 1ull << 22;
   c->max_pairs = 1ull << 27;
   c->cull_levels = 3;
+  c->visibility = 0;
   return SPOLY_OK;
 }
 
@@ -184,7 +192,11 @@ void spoly_destroy(spoly_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
-  ctx->d_tris.release(); ctx->d_tcull.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
+  ctx->d_tris.release(); ctx->d_occ.release(); ctx->d_tcull.release();
+  for (auto& b : ctx->d_box) b.release();
+  for (auto& b : ctx->d_obox) b.release();
+  ctx->d_vkeep.release(); ctx->d_vsel.release(); ctx->d_viota.release(); ctx->d_vkey.release(); ctx->d_vn.release();
+  ctx->d_vbary.release(); ctx->d_vcontrib.release(); ctx->d_vresid.release(); ctx->d_orig.release(); ctx->d_perm.release(); ctx->d_cl.release();
   ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_emask.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
@@ -210,22 +222,15 @@ void spoly_destroy(spoly_ctx* ctx) {
 
 const char* spoly_last_error(const spoly_ctx* ctx) { return ctx ? ctx->err.c_str() : "null ctx"; }
 
-spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri,
-                               uint32_t ntris, float eta_front, float eta_back, uint32_t* mesh_id) {
-  if (!ctx || !pos || !nrm || !tri || ntris == 0 || nverts == 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null mesh");
-  if (!(eta_front > 0) || !(eta_back > 0)) return fail(ctx, SPOLY_ERR_INVALID_ARG, "eta must be > 0");
-  CK(cudaSetDevice(ctx->device));
-  // host-side validation + Morton order of the centroids (one-time scene setup)
+// triangle order along the 30-bit Morton code of the centroids in the mesh's bounding box (host, scene setup);
+// returns false on a degenerate triangle (|e1 x e2| <= 1e-12 diag^2)
+static bool morton_order(const float* pos, uint32_t nverts, const uint32_t* tri, uint32_t ntris, std::vector<uint32_t>& order,
+                         bool check_degenerate) {
   double lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (uint64_t i = 0; i < 3ull * ntris; ++i)
-    if (tri[i] >= nverts) return fail(ctx, SPOLY_ERR_BAD_MESH, "triangle index out of range");
   for (uint32_t v = 0; v < nverts; ++v)
     for (int c = 0; c < 3; ++c) {
-      double x = pos[3ull * v + c];
-      if (!std::isfinite(x) || !std::isfinite((double)nrm[3ull * v + c]))
-        return fail(ctx, SPOLY_ERR_BAD_MESH, "non-finite vertex");
-      lo[c] = std::min(lo[c], x);
-      hi[c] = std::max(hi[c], x);
+      lo[c] = std::min(lo[c], (double)pos[3ull * v + c]);
+      hi[c] = std::max(hi[c], (double)pos[3ull * v + c]);
     }
   const double diag2 = (hi[0] - lo[0]) * (hi[0] - lo[0]) + (hi[1] - lo[1]) * (hi[1] - lo[1]) +
                        (hi[2] - lo[2]) * (hi[2] - lo[2]);
@@ -240,22 +245,83 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
       e2[c] = P[2][c] - P[0][c];
     }
     double g[3] = {e1[1] * e2[2] - e1[2] * e2[1], e1[2] * e2[0] - e1[0] * e2[2], e1[0] * e2[1] - e1[1] * e2[0]};
-    if (!(std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]) > 1e-12 * diag2))
-      return fail(ctx, SPOLY_ERR_BAD_MESH, "degenerate triangle");
+    if (check_degenerate && !(std::sqrt(g[0] * g[0] + g[1] * g[1] + g[2] * g[2]) > 1e-12 * diag2)) return false;
     uint32_t code = 0;
     uint32_t ix[3];
     for (int c = 0; c < 3; ++c) {
       double m = (P[0][c] + P[1][c] + P[2][c]) / 3.0;
-      double s = hi[c] > lo[c] ? (m - lo[c]) / (hi[c] - lo[c]) : 0.0;
-      ix[c] = (uint32_t)std::min(1023.0, std::max(0.0, s * 1024.0));
+      double sc = hi[c] > lo[c] ? (m - lo[c]) / (hi[c] - lo[c]) : 0.0;
+      ix[c] = (uint32_t)std::min(1023.0, std::max(0.0, sc * 1024.0));
     }
     for (int b = 9; b >= 0; --b)
       for (int c = 0; c < 3; ++c) code = (code << 1) | ((ix[c] >> b) & 1u);
     key[t] = ((uint64_t)code << 32) | t;
   }
   std::sort(key.begin(), key.end());
-  std::vector<uint32_t> order(ntris);
+  order.resize(ntris);
   for (uint32_t i = 0; i < ntris; ++i) order[i] = (uint32_t)(key[i] & 0xffffffffu);
+  return true;
+}
+
+// AABB hierarchy (visibility) over the triangle records recs: levels in bufs, tree in T
+static spoly_status build_tree(spoly_ctx* ctx, const TriRec* recs, uint32_t ntris, DBuf<float4>* bufs, AabbTree& T) {
+  T = AabbTree();
+  T.tris = recs;
+  T.top = aabb_levels(ntris, T.n);
+  for (int l = 1; l <= T.top; ++l) {
+    CK(bufs[l].ensure(2ull * T.n[l]));
+    T.box[l] = bufs[l].p;
+  }
+  launch_build_aabbs(recs, T, ctx->st);
+  CK(cudaGetLastError());
+  return SPOLY_OK;
+}
+
+spoly_status spoly_upload_occluders(spoly_ctx* ctx, const float* pos, uint32_t nverts, const uint32_t* tri,
+                                    uint32_t ntris) {
+  if (!ctx) return SPOLY_ERR_INVALID_ARG;
+  CK(cudaSetDevice(ctx->device));
+  if (ntris == 0) {
+    ctx->occ_tree = AabbTree();
+    return SPOLY_OK;
+  }
+  if (!pos || !tri || nverts == 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null occluder mesh");
+  for (uint64_t i = 0; i < 3ull * ntris; ++i)
+    if (tri[i] >= nverts) return fail(ctx, SPOLY_ERR_BAD_MESH, "occluder index out of range");
+  for (uint64_t i = 0; i < 3ull * nverts; ++i)
+    if (!std::isfinite(pos[i])) return fail(ctx, SPOLY_ERR_BAD_MESH, "non-finite occluder vertex");
+  std::vector<uint32_t> order;
+  morton_order(pos, nverts, tri, ntris, order, false);
+  float* dpos = nullptr;
+  uint32_t *dtri = nullptr, *dorder = nullptr;
+  CK(cudaMalloc(&dpos, sizeof(float) * 3ull * nverts));
+  CK(cudaMalloc(&dtri, sizeof(uint32_t) * 3ull * ntris));
+  CK(cudaMalloc(&dorder, sizeof(uint32_t) * ntris));
+  CK(cudaMemcpyAsync(dpos, pos, sizeof(float) * 3ull * nverts, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dtri, tri, sizeof(uint32_t) * 3ull * ntris, cudaMemcpyHostToDevice, ctx->st));
+  CK(cudaMemcpyAsync(dorder, order.data(), sizeof(uint32_t) * ntris, cudaMemcpyHostToDevice, ctx->st));
+  CK(ctx->d_occ.ensure(ntris));
+  launch_occ_tris(dpos, dtri, dorder, ntris, ctx->d_occ.p, ctx->st);
+  spoly_status s = build_tree(ctx, ctx->d_occ.p, ntris, ctx->d_obox, ctx->occ_tree);
+  CK(cudaStreamSynchronize(ctx->st));
+  cudaFree(dpos);
+  cudaFree(dtri);
+  cudaFree(dorder);
+  return s;
+}
+
+spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri,
+                               uint32_t ntris, float eta_front, float eta_back, uint32_t* mesh_id) {
+  if (!ctx || !pos || !nrm || !tri || ntris == 0 || nverts == 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null mesh");
+  if (!(eta_front > 0) || !(eta_back > 0)) return fail(ctx, SPOLY_ERR_INVALID_ARG, "eta must be > 0");
+  CK(cudaSetDevice(ctx->device));
+  // host-side validation + Morton order of the centroids (one-time scene setup)
+  for (uint64_t i = 0; i < 3ull * ntris; ++i)
+    if (tri[i] >= nverts) return fail(ctx, SPOLY_ERR_BAD_MESH, "triangle index out of range");
+  for (uint64_t i = 0; i < 3ull * nverts; ++i)
+    if (!std::isfinite(pos[i]) || !std::isfinite(nrm[i])) return fail(ctx, SPOLY_ERR_BAD_MESH, "non-finite vertex");
+  std::vector<uint32_t> order;
+  if (!morton_order(pos, nverts, tri, ntris, order, true)) return fail(ctx, SPOLY_ERR_BAD_MESH, "degenerate triangle");
 
   float *dpos = nullptr, *dnrm = nullptr;
   uint32_t *dtri = nullptr, *dorder = nullptr;
@@ -290,6 +356,10 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
       ctx->M.nupper_nodes[i] = (uint32_t)n;
       ctx->M.nupper = i + 1;
     }
+  }
+  {
+    spoly_status bs = build_tree(ctx, ctx->d_tris.p, ntris, ctx->d_box, ctx->mesh_tree);
+    if (bs != SPOLY_OK) return bs;
   }
   CK(cudaGetLastError());
   CK(cudaStreamSynchronize(ctx->st));
@@ -695,10 +765,40 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     s = ensure_sink(ctx, (uint64_t)(cnt[0] * 1.25) + 1024, (uint64_t)(cnt[1] * 1.25) + 1024, k);
     if (s != SPOLY_OK) return s;
   }
+  // ---------------- visibility: drop chains with a blocked segment, keys preserved
+  uint64_t n_raw = cnt[0];
+  if (ctx->cfg.visibility && n_raw) {
+    CK(ctx->d_vkeep.ensure(n_raw));
+    CK(ctx->d_vsel.ensure(n_raw));
+    CK(ctx->d_vn.ensure(1));
+    launch_visibility(k, n_raw, raw_sink(ctx), ctx->d_pq.p, ctx->d_pt.p, endpoints, ctx->mesh_tree, ctx->occ_tree,
+                      ctx->d_vkeep.p, ctx->nsm, st);
+    size_t tb = 0;
+    cub::CountingInputIterator<uint32_t> iota(0);
+    CK(cub::DeviceSelect::Flagged(nullptr, tb, iota, ctx->d_vkeep.p, ctx->d_vsel.p, ctx->d_vn.p, (int64_t)n_raw, st));
+    CK(ctx->d_temp.ensure(tb));
+    CK(cub::DeviceSelect::Flagged(ctx->d_temp.p, tb, iota, ctx->d_vkeep.p, ctx->d_vsel.p, ctx->d_vn.p, (int64_t)n_raw,
+                                  st));
+    unsigned long long nk = 0;
+    CK(cudaMemcpyAsync(&nk, ctx->d_vn.p, sizeof(nk), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(ctx->d_vkey.ensure(ctx->d_key.cap));
+    CK(ctx->d_vbary.ensure(ctx->d_bary.cap));
+    CK(ctx->d_vcontrib.ensure(ctx->d_contrib.cap));
+    CK(ctx->d_vresid.ensure(ctx->d_resid.cap));
+    launch_gather_raw(ctx->d_vsel.p, nk, k, raw_sink(ctx), ctx->d_vkey.p, ctx->d_vbary.p, ctx->d_vcontrib.p,
+                      ctx->d_vresid.p, st);
+    std::swap(ctx->d_key, ctx->d_vkey);
+    std::swap(ctx->d_bary, ctx->d_vbary);
+    std::swap(ctx->d_contrib, ctx->d_vcontrib);
+    std::swap(ctx->d_resid, ctx->d_vresid);
+    ctx->launches += 4;
+    n_raw = nk;
+  }
   CK(cudaEventRecord(ctx->ev[2], st));
 
   // ---------------- deterministic order + per-query sums
-  const uint64_t n = cnt[0], nf_raw = cnt[1];
+  const uint64_t n = n_raw, nf_raw = cnt[1];
   CK(ctx->o_query.ensure(n));
   CK(ctx->o_tuple.ensure(n * k));
   CK(ctx->o_bary.ensure(n * 2 * k));
@@ -858,6 +958,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   R.n_cand_jobs = counters[C_CAND_JOBS];
   R.n_path_jobs = cnt[2] + cnt[3];
   R.n_eval_deep = counters[C_EVAL_DEEP];
+  R.n_rej_visibility = counters[C_REJ_VIS];
   R.n_cull_tests = ctx->cull_tests;
   R.n_truncated = counters[C_TRUNCATED];
   R.n_big_scan = counters[C_BIG_SCAN];

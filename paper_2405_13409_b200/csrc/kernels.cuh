@@ -94,6 +94,16 @@ void launch_solution_flags(const unsigned long long* skey, const uint32_t* skey3
 void launch_per_query_sorted(const uint32_t* query, const double* contrib, uint64_t n, uint32_t nq, double* per_query,
                              unsigned long long* range, cudaStream_t st);
 
+// visibility.cu
+int aabb_levels(uint32_t ntris, uint32_t* n);  // fills n[0..top], returns top
+void launch_build_aabbs(const TriRec* recs, AabbTree& T, cudaStream_t st);
+void launch_occ_tris(const float* pos, const uint32_t* tri, const uint32_t* order, uint32_t ntris, TriRec* recs,
+                     cudaStream_t st);
+void launch_visibility(int k, uint64_t n, const SolSink& S, const uint32_t* pq, const uint32_t* pt, const double* ep,
+                       const AabbTree& mesh, const AabbTree& occ, uint8_t* keep, int nsm, cudaStream_t st);
+void launch_gather_raw(const uint32_t* sel, uint64_t n, int k, const SolSink& in, unsigned long long* okey,
+                       double* obary, double* ocontrib, float* oresid, cudaStream_t st);
+
 // fma_peak.cu
 void launch_fma_peak(int fp64, int iters, double* sink, int nsm, cudaStream_t st, int* blocks_out, int* threads_out,
                      int* flops_per_thread_iter);

@@ -66,9 +66,9 @@ __device__ __forceinline__ double browmax(const double* G, double* rm) {
   for (int i = 0; i <= D; ++i) {
     double r = 0.0;
 #pragma unroll
-    for (int j = 0; i + j <= D; ++j) r = fmax(r, fabs(G[i * S + j]));
+    for (int j = 0; i + j <= D; ++j) r = dmax(r, fabs(G[i * S + j]));
     rm[i] = r;
-    m = fmax(m, r);
+    m = dmax(m, r);
   }
   return m;
 }

@@ -197,13 +197,46 @@ __device__ __forceinline__ int quadratic_u_roots(const double al[3], double* ua,
   return nu;
 }
 
+// phase 1's pre-check only needs the candidates to ~1e-12 (it rejects those > 3e-3 outside the triangle, the
+// refinement moves them <= 1e-3): the same stable formula with reciprocals instead of correctly rounded divisions
+__device__ __forceinline__ int quadratic_u_roots_precheck(const double al[3], double* ua, bool* near_double) {
+  int nu = 0;
+  *near_double = false;
+  if (al[2] != 0.0) {
+    const double a0 = al[0], a1 = al[1], a2 = al[2];
+    double disc = a1 * a1 - 4.0 * a2 * a0;
+    const double sc = a1 * a1 + 4.0 * fabs(a2 * a0);
+    if (fabs(disc) <= 1e-8 * sc) *near_double = true;
+    if (!(disc < -1e-12 * sc)) {
+      if (disc < 0) disc = 0;
+      const double qq = -0.5 * (a1 + copysign(sqrt(disc), a1));
+      if (qq == 0.0) {
+        ua[nu++] = 0.0;
+      } else {
+        ua[nu++] = qq * fast_rcp(a2);
+        ua[nu++] = a0 * fast_rcp(qq);
+      }
+    }
+  } else if (al[1] != 0.0) {
+    ua[nu++] = -al[0] * fast_rcp(al[1]);
+  }
+  return nu;
+}
+
 // the refinement (reading R2) moves u and v by at most 1e-3 each (1 - u - v by 2e-3), so a candidate more than
 // 3e-3 outside the simplex can neither become admissible nor land within eps_flag of an edge
-__device__ __forceinline__ bool precheck_reject(double us, double vv) { return fmin(fmin(us, vv), 1.0 - us - vv) < -3e-3; }
+__device__ __forceinline__ bool precheck_reject(double us, double vv) {
+  return us < -3e-3 || vv < -3e-3 || 1.0 - us - vv < -3e-3;
+}
 
 // ---------------------------------------------------------------------------------------------
+// resident blocks per SM (A/B on C2, R: 4 -> 5 (<= 96 registers, 156 B spill) took phase 1 2.48 -> 2.38 ms; T spills
+// 1.2 KB at 5 and keeps 4)
 #ifndef SPOLY_P1_MINB
-#define SPOLY_P1_MINB 4
+#define SPOLY_P1_MINB 5
+#endif
+#ifndef SPOLY_P1_MINB_T
+#define SPOLY_P1_MINB_T 4
 #endif
 #ifdef SPOLY_PATH_MINB
 #define SPOLY_PATH_BOUNDS __launch_bounds__(128, SPOLY_PATH_MINB)
@@ -211,7 +244,7 @@ __device__ __forceinline__ bool precheck_reject(double us, double vv) { return f
 #define SPOLY_PATH_BOUNDS __launch_bounds__(128)
 #endif
 template <bool TC>
-__global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
+__global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_phase1(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                     uint64_t npairs, const TriRec* __restrict__ tris,
                                                     const double* __restrict__ ep, SolveParams prm, SolSink S,
                                                     JobSink J) {
@@ -255,7 +288,7 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
         eliminate<TC>(Sys, r);
         double mr = 0.0;
 #pragma unroll
-        for (int t = 0; t < NR; ++t) mr = fmax(mr, fabs(r[t]));
+        for (int t = 0; t < NR; ++t) mr = dmax(mr, fabs(r[t]));
         if (!(mr > 0)) {
           flags |= SPOLY_FLAG_DEGENERATE;
         } else {
@@ -301,6 +334,7 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
         has = false;  // rounding: no sign change after all
       } else {
         double a = 0.0, b = 1.0, x = -f0 / (f1 - f0);  // secant start
+        bool conv = false;
         if (!(x > a && x < b)) x = 0.5;
         for (int it = 0; it < 100; ++it) {
           double f = r[NR - 1], fp = 0.0;
@@ -317,16 +351,18 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
             b = x;
           double xn = x - f * fast_rcp(fp);
           // convergence is tested before the bracket safeguard: at the root the Newton step is below an ulp and may
-          // land on the endpoint x just became, which must not trigger a bisection from a far bracket
-          const bool conv = fabs(xn - x) <= 1e-12;
-          if (conv)
-            xn = fmin(fmax(xn, a), b);
-          else if (!(xn > a && xn < b))
-            xn = 0.5 * (a + b);
+          // land on the endpoint x just became, which must not trigger a bisection from a far bracket (the
+          // converged step is clamped into the bracket once, after the loop)
+          if (fabs(xn - x) <= 1e-12) {
+            x = xn;
+            conv = true;
+            break;
+          }
+          if (!(xn > a && xn < b)) xn = 0.5 * (a + b);
           x = xn;
-          if (conv || b - a <= 1e-15) break;
+          if (b - a <= 1e-15) break;
         }
-        root = x;
+        root = conv ? dmin(dmax(a, x), b) : x;
       }
       if (has) {
         cnt[C_VROOTS]++;
@@ -338,13 +374,14 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
         A[5] = A[7] = A[8] = 0.0;
         double al[3];
         bslices_at<2, 3>(A, root, al);
-        const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+        const double amax = dmax(fabs(al[0]), dmax(fabs(al[1]), fabs(al[2])));
         if (!(amax >= 1e-12)) {
           complex_job = true;  // a(., v*) == 0: the b fallback runs in the general path kernel
         } else {
           uint32_t nc = 0, nrej = 0;
-          double ua[2], ud;
-          const int nu = quadratic_u_roots(al, ua, &ud);
+          double ua[2];
+          bool near_double;
+          const int nu = quadratic_u_roots_precheck(al, ua, &near_double);
           for (int iu = 0; iu < nu; ++iu) {
             ++nc;
             if (precheck_reject(ua[iu], root))
@@ -352,7 +389,7 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
             else
               to_path = true;
           }
-          if (!isnan(ud)) complex_job = true;  // a near-double u-root: the general path kernel probes it (R11)
+          if (near_double) complex_job = true;  // a near-double u-root: the general path kernel probes it (R11)
           if (complex_job)
             to_path = false;
           if (!to_path && !complex_job) {
@@ -365,6 +402,11 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
     emit_flag(active && flags != 0, flags, i, S);
     // two-ended dense list: path entries (pair, root) from the front, block-aggregated (one atomic per 128 pairs;
     // same-address atomics serialise in L2); deeper recursions (pair, meta, r) from the back
+#ifdef SPOLY_P1_WARP_APPEND
+    // warp-level append: no block barrier (the warps' Newton loops end at different times)
+    uint32_t ex1;
+    const unsigned long long b1 = warp_alloc(J.count, to_path ? 1u : 0u, &ex1);
+#else
     const unsigned mb = __ballot_sync(0xffffffffu, to_path);
     if (lane == 0) s_off[warp] = __popc(mb);
     __syncthreads();
@@ -381,6 +423,7 @@ __global__ void __launch_bounds__(128, SPOLY_P1_MINB) k1_phase1(const uint32_t* 
     __syncthreads();
     const uint32_t ex1 = s_off[warp] + __popc(mb & ((1u << lane) - 1u));
     const unsigned long long b1 = s_base;
+#endif
     // deep list: deeper recursions, and the rare monotone jobs whose back-substitution needs the b fallback or
     // a c14 probe (the deep kernel re-isolates their single root; the general path kernel finishes them)
     const bool deep = job && (!mono || complex_job);
@@ -459,7 +502,7 @@ __device__ __forceinline__ int back_substitute(const Sys1<TC>& Sys, double vs, d
   double al[3];
   bslices_at<2, 3>(Sys.A, vs, al);
   *udouble = __longlong_as_double(0x7ff8000000000000ll);
-  const double amax = fmax(fabs(al[0]), fmax(fabs(al[1]), fabs(al[2])));
+  const double amax = dmax(fabs(al[0]), dmax(fabs(al[1]), fabs(al[2])));
   if (amax >= 1e-12) return quadratic_u_roots(al, ua, udouble);
   // fallback (c11): a(., v*) == 0 -> roots of b(., v*) on [-0.1, 1.1]
   double bl[DB + 1];
@@ -468,7 +511,7 @@ __device__ __forceinline__ int back_substitute(const Sys1<TC>& Sys, double vs, d
   int bd = 0;
 #pragma unroll
   for (int i = 0; i <= DB; ++i) {
-    bmax = fmax(bmax, fabs(bl[i]));
+    bmax = dmax(bmax, fabs(bl[i]));
     if (bl[i] != 0.0) bd = i;
   }
   if (!(bmax >= 1e-12)) {
@@ -680,11 +723,10 @@ __global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const
 // (<= 2 candidates, no b fallback, no c14 probe: phase 1 routed those jobs to the deep list), (a, b) refinement
 // (reading R2), Eq. 3 validation, sides, flags, analytic contribution (c15), <= 2 chains emitted with
 // warp-aggregated appends.  Same arithmetic and slots as path_phase(), with the lean state of one root.
-#ifdef SPOLY_FAST_MINB
-#define SPOLY_FAST_BOUNDS __launch_bounds__(128, SPOLY_FAST_MINB)
-#else
-#define SPOLY_FAST_BOUNDS __launch_bounds__(128)
+#ifndef SPOLY_FAST_MINB
+#define SPOLY_FAST_MINB 4  // <= 128 registers (A/B: 222 unbounded -> 1.59, 128 -> 1.54 ms on C2)
 #endif
+#define SPOLY_FAST_BOUNDS __launch_bounds__(128, SPOLY_FAST_MINB)
 template <bool TC>
 __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                     const TriRec* __restrict__ tris, const double* __restrict__ ep,

@@ -23,7 +23,7 @@ STATUS = {0: "SPOLY_OK", 1: "SPOLY_ERR_INVALID_ARG", 2: "SPOLY_ERR_BAD_MESH", 3:
 FLAG_NEAR_TANGENT, FLAG_BOUNDARY, FLAG_RESIDUAL, FLAG_DEGENERATE, FLAG_TRUNCATED = 1, 2, 4, 8, 16
 
 EXPORTS = ["spoly_default_config", "spoly_create", "spoly_destroy", "spoly_last_error", "spoly_upload_mesh",
-           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma", "spoly_sqrt_table"]
+           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma", "spoly_sqrt_table", "spoly_upload_occluders"]
 
 
 class SpolyError(RuntimeError):
@@ -36,7 +36,7 @@ class spoly_config(ctypes.Structure):
                 ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
                 ("cull", ctypes.c_int), ("deterministic", ctypes.c_int), ("cull_margin", ctypes.c_float),
                 ("max_solutions", ctypes.c_uint64), ("max_pairs", ctypes.c_uint64),
-                ("cull_levels", ctypes.c_int)]
+                ("cull_levels", ctypes.c_int), ("visibility", ctypes.c_int)]
 
 
 class spoly_tuple_list(ctypes.Structure):
@@ -56,7 +56,8 @@ class spoly_report(ctypes.Structure):
         ("n_elims", ctypes.c_uint64), ("n_pairs_coarse", ctypes.c_uint64),
         ("ms_roots", ctypes.c_float), ("ms_path", ctypes.c_float), ("n_refined", ctypes.c_uint64),
         ("n_cand_jobs", ctypes.c_uint64), ("n_path_jobs", ctypes.c_uint64), ("n_cull_tests", ctypes.c_uint64),
-        ("n_truncated", ctypes.c_uint64), ("n_big_scan", ctypes.c_uint64), ("n_eval_deep", ctypes.c_uint64)]
+        ("n_truncated", ctypes.c_uint64), ("n_big_scan", ctypes.c_uint64), ("n_eval_deep", ctypes.c_uint64),
+        ("n_rej_visibility", ctypes.c_uint64)]
 
 
 class spoly_result(ctypes.Structure):
@@ -91,6 +92,7 @@ def lib():
         L.spoly_last_worklist.argtypes = [P, P, P, P]
         L.spoly_bench_fma.argtypes = [P, I, D, P]
         L.spoly_sqrt_table.argtypes = [P, I, P]
+        L.spoly_upload_occluders.argtypes = [P, P, U32, P, U32]
         _lib = L
     return _lib
 
@@ -209,6 +211,16 @@ class Context:
         self._check(rc, "spoly_upload_mesh")
         return mid.value
 
+    def upload_occluders(self, mesh=None):
+        """Occluder-only triangles for the visibility test (cfg.visibility); None removes them."""
+        if mesh is None:
+            self._check(self._L.spoly_upload_occluders(self._h, None, 0, None, 0), "spoly_upload_occluders")
+            return
+        pos = np.ascontiguousarray(mesh.pos, dtype=np.float32)
+        tri = np.ascontiguousarray(mesh.tri, dtype=np.uint32)
+        rc = self._L.spoly_upload_occluders(self._h, pos.ctypes.data, pos.shape[0], tri.ctypes.data, tri.shape[0])
+        self._check(rc, "spoly_upload_occluders")
+
     def _wrap(self, r: spoly_result, nq: int):
         dev = f"cuda:{self.device}"
         n, m, k = int(r.n_solutions), int(r.n_flagged), int(r.k)
@@ -222,7 +234,8 @@ class Context:
                    ms_path=r.report.ms_path, n_refined=int(r.report.n_refined),
                    n_cand_jobs=int(r.report.n_cand_jobs), n_path_jobs=int(r.report.n_path_jobs),
                    n_cull_tests=int(r.report.n_cull_tests), n_truncated=int(r.report.n_truncated),
-                   n_big_scan=int(r.report.n_big_scan), n_eval_deep=int(r.report.n_eval_deep))
+                   n_big_scan=int(r.report.n_big_scan), n_eval_deep=int(r.report.n_eval_deep),
+                   n_rej_visibility=int(r.report.n_rej_visibility))
         return Result(n, m, k, _view(r.query, (n,), "<u4", dev), _view(r.tuple, (n, k), "<u4", dev),
                       _view(r.bary, (n, 2 * k), "<f8", dev), _view(r.contribution, (n,), "<f8", dev),
                       _view(r.residual, (n,), "<f4", dev), _view(r.flags, (n,), "<u4", dev),

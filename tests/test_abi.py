@@ -66,14 +66,14 @@ def test_ctypes_structs_match_the_header(tmp_path):
     src = tmp_path / "sz.c"
     src.write_text('#include <stdio.h>\n#include <stddef.h>\n#include "spoly.h"\nint main(void) {\n'
                    'printf("%zu %zu %zu %zu %zu\\n", sizeof(spoly_config), sizeof(spoly_report), sizeof(spoly_result),'
-                   ' offsetof(spoly_report, n_eval_deep), offsetof(spoly_result, report));\nreturn 0;\n}\n')
+                   ' offsetof(spoly_report, n_rej_visibility), offsetof(spoly_result, report));\nreturn 0;\n}\n')
     exe = tmp_path / "sz"
     subprocess.check_call(["gcc", "-std=c11", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
     c_cfg, c_rep, c_res, c_off, c_roff = map(int, subprocess.check_output([str(exe)]).decode().split())
     assert ctypes.sizeof(spoly.spoly_config) == c_cfg
     assert ctypes.sizeof(spoly.spoly_report) == c_rep
     assert ctypes.sizeof(spoly.spoly_result) == c_res
-    assert spoly.spoly_report.n_eval_deep.offset == c_off
+    assert spoly.spoly_report.n_rej_visibility.offset == c_off
     assert spoly.spoly_result.report.offset == c_roff
 
 

@@ -487,3 +487,55 @@ def test_two_bounce_query_chunking_identical(sp, torch_cuda, chain, make):
     assert np.array_equal(a["worklist"][1], b["worklist"][1])
     for k in ("query", "tuple", "bary", "contribution", "per_query", "flagged_query", "flagged_tuple"):
         assert np.array_equal(a[k], b[k]), k
+
+
+# ---------------------------------------------------------------- visibility
+def _blockers(rng, n, center, spread, size):
+    P = []
+    for _ in range(n):
+        c = np.asarray(center) + rng.uniform(-1, 1, 3) * spread
+        P.append(c + rng.normal(size=(3, 3)) * size)
+    P = np.concatenate(P).astype(np.float32)
+    return W.Mesh(P, np.tile([0, 0, 1], (len(P), 1)).astype(np.float32), np.arange(len(P), dtype=np.uint32).reshape(-1, 3))
+
+
+@pytest.mark.parametrize("chain", ["R", "RR", "TT"])
+def test_visibility_parity(orc, sp, torch_cuda, chain):
+    """cfg.visibility = 1 with occluders floating over the chains (and the specular mesh occluding itself): the GPU's
+    AABB-hierarchy segment test drops exactly the chains the oracle's brute force drops (same counts, same survivors,
+    same per-query sums)."""
+    rng = np.random.default_rng(201)
+    if chain == "R":
+        w = W.glints_c2(res=256)
+        sub = w.subset(np.arange(0, 65536, 65536 // 16)[:16])
+        mesh, ep, off, ids = sub.mesh, sub.endpoints, None, None
+        occ = _blockers(rng, 400, (0.0, 0.0, 0.4), np.array([1.0, 1.0, 0.3]), 0.03)
+    else:
+        mesh, ep, off, ids, _ = _planted_batch(chain, 30, 211)
+        # blockers around the segments of the planted chains
+        pts = []
+        for q in range(len(ep)):
+            a, b = ep[q]
+            pts.append(a + rng.uniform(0.2, 0.8) * (b - a))
+        occ = _blockers(rng, 1, (0, 0, 0), np.zeros(3), 0.0)
+        P = np.concatenate([p + rng.normal(size=(3, 3)) * 0.08 for p in pts]).astype(np.float32)
+        occ = W.Mesh(P, np.tile([0, 0, 1], (len(P), 1)).astype(np.float32), np.arange(len(P), dtype=np.uint32).reshape(-1, 3))
+    ro = orc.solve(mesh, chain, ep, offsets=off, tri_ids=ids, cfg=orc.default_config(visibility=1), occluders=occ)
+    ctx = sp.Context(0, sp.default_config(visibility=1))
+    ctx.upload_mesh(mesh)
+    ctx.upload_occluders(occ)
+    torch = torch_cuda
+    e = torch.as_tensor(np.ascontiguousarray(ep), dtype=torch.float64, device="cuda")
+    o = None if off is None else torch.as_tensor(off.astype(np.int32), device="cuda")
+    t = None if ids is None else torch.as_tensor(ids.astype(np.int32), device="cuda")
+    r = ctx.solve(chain, e, None, o, t)
+    g = r.to_numpy()
+    g["report"] = r.report
+    wl = ctx.last_worklist()
+    g["worklist"] = (wl[0].cpu().numpy().view(np.uint32), wl[1].cpu().numpy().view(np.uint32).reshape(-1, len(chain)))
+    ctx.close()
+    assert ro.report["rej_visibility"] > 0
+    assert g["report"]["n_rej_visibility"] == ro.report["rej_visibility"], (g["report"]["n_rej_visibility"],
+                                                                             ro.report["rej_visibility"])
+    parity.compare(ro, g, len(ep), tol_bary=1e-5 if len(chain) == 1 else 1e-4, min_compared=5 if len(chain) == 1 else 3,
+                   label=f"visibility {chain}")

@@ -347,3 +347,87 @@ def test_generic_planted_chains_unflagged(orc):
             tot += 1
             fl += len(r.flagged_flags) > 0
     assert fl <= 0.02 * tot, (fl, tot)
+
+
+# ------------------------------------------------------------------ visibility
+def _seg_tri_numpy(a, b, P):
+    """Independent segment/triangle test: intersect the segment with the triangle's plane, then the barycentric
+    coordinates of the hit from signed sub-triangle areas (not Moller-Trumbore).  Returns (hit, t)."""
+    n = np.cross(P[1] - P[0], P[2] - P[0])
+    da, db = np.dot(a - P[0], n), np.dot(b - P[0], n)
+    if da * db > 0 or da == db:
+        return False, None
+    t = da / (da - db)
+    x = a + t * (b - a)
+    A = [np.dot(np.cross(P[(i + 1) % 3] - x, P[(i + 2) % 3] - x), n) for i in range(3)]
+    return all(s >= 0 for s in A) or all(s <= 0 for s in A), t
+
+
+def test_visibility_blocker_closed_form(orc):
+    """A flat mirror chain (S:520 geometry) with a small blocker triangle straddling the segment x_0 -> x_1: the chain
+    is rejected with visibility on, kept with visibility off or with the blocker moved aside; a blocker across
+    x_1 -> x_2 rejects it too; the mirror triangle itself never blocks its own vertex."""
+    pos = np.array([[-1, -1, 0], [2, -1, 0], [-1, 2, 0]], np.float32)
+    nrm = np.tile([0, 0, 1], (3, 1)).astype(np.float32)
+    mesh = Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32))
+    ep = np.array([[[0, 0, 1], [1, 0, 1]]], float)
+    x1 = np.array([0.5, 0, 0])
+
+    def blocker(center):
+        c = np.asarray(center, float)
+        P = np.array([c + [-0.1, -0.1, 0.02], c + [0.1, -0.1, -0.02], c + [0.0, 0.15, 0.0]], np.float32)
+        return Mesh(P, np.tile([0, 0, 1], (3, 1)).astype(np.float32), np.array([[0, 1, 2]], np.uint32))
+    on = orc.default_config(cull=0, visibility=1)
+    r = orc.solve(mesh, "R", ep, cfg=orc.default_config(cull=0), occluders=blocker(0.5 * (ep[0, 0] + x1)))
+    assert r.n_solutions == 1
+    r = orc.solve(mesh, "R", ep, cfg=on, occluders=blocker(0.5 * (ep[0, 0] + x1)))
+    assert r.n_solutions == 0 and r.report["rej_visibility"] == 1 and r.per_query[0] == 0
+    r = orc.solve(mesh, "R", ep, cfg=on, occluders=blocker(0.5 * (ep[0, 1] + x1)))
+    assert r.n_solutions == 0 and r.report["rej_visibility"] == 1
+    r = orc.solve(mesh, "R", ep, cfg=on, occluders=blocker(0.5 * (ep[0, 0] + x1) + [0, 0.6, 0]))
+    assert r.n_solutions == 1 and r.report["rej_visibility"] == 0
+    r = orc.solve(mesh, "R", ep, cfg=on)
+    assert r.n_solutions == 1
+
+
+@pytest.mark.parametrize("chain", ["R", "RR", "TT"])
+def test_visibility_matches_independent_segment_test(orc, chain):
+    """Random occluders over planted chains: with visibility on, the oracle returns exactly the chains whose every
+    segment misses every scene triangle (other than the chain's own triangles at the segment's ends) according to
+    an independent numpy segment test (plane crossing + signed areas)."""
+    rng = np.random.default_rng(181)
+    cases = planted_many(191, chain, 30, size=0.15)
+    n_blocked = n_kept = 0
+    for mesh, ids, x0, xk1, bary in cases:
+        # occluders: small random triangles near the chain's segments
+        r0 = _solve1(orc, mesh, chain, x0, xk1, ids)
+        if r0.n_solutions == 0:
+            continue
+        b = r0.bary[0]
+        tris = [mesh.pos[mesh.tri[t]].astype(float) for t in ids]
+        xs = [x0] + [tris[i][0] + b[2 * i] * (tris[i][1] - tris[i][0]) + b[2 * i + 1] * (tris[i][2] - tris[i][0])
+                     for i in range(len(ids))] + [xk1]
+        occ = []
+        for _ in range(6):
+            i = rng.integers(0, len(xs) - 1)
+            c = xs[i] + rng.uniform(0.2, 0.8) * (xs[i + 1] - xs[i]) + rng.normal(size=3) * 0.08
+            occ.append(c + rng.normal(size=(3, 3)) * 0.06)
+        opos = np.concatenate(occ).astype(np.float32)
+        omesh = Mesh(opos, np.tile([0, 0, 1], (len(opos), 1)).astype(np.float32),
+                     np.arange(len(opos), dtype=np.uint32).reshape(-1, 3))
+        r1 = orc.solve(mesh, chain, np.array([[x0, xk1]]), offsets=np.array([0, 1], np.uint32),
+                       tri_ids=np.array(ids, np.uint32), cfg=orc.default_config(cull=0, visibility=1), occluders=omesh)
+        kept = {tuple(np.round(x, 12)) for x in r1.bary}
+        for bb in r0.bary:
+            pts = [x0] + [tris[i][0] + bb[2 * i] * (tris[i][1] - tris[i][0]) + bb[2 * i + 1] * (tris[i][2] - tris[i][0])
+                          for i in range(len(ids))] + [xk1]
+            blocked = False
+            for s in range(len(pts) - 1):
+                for P in [opos[3 * j:3 * j + 3].astype(float) for j in range(len(occ))]:
+                    hit, t = _seg_tri_numpy(pts[s], pts[s + 1], P)
+                    if hit and 1e-6 < t < 1 - 1e-6:
+                        blocked = True
+            assert blocked == (tuple(np.round(bb, 12)) not in kept), (chain, bb, blocked)
+            n_blocked += blocked
+            n_kept += not blocked
+    assert n_blocked >= 3 and n_kept >= 3, (n_blocked, n_kept)
