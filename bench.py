@@ -225,6 +225,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cull-levels", type=int, default=None, help="k=2 cull subdivision levels (default: library)")
+    ap.add_argument("--scan-restrict", type=int, default=None, help="k=2 scan restriction (reading R25; default on)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -268,7 +269,12 @@ def main():
         w = w.subset(shard_idx)
     chain = w.chain
     stream = torch.cuda.current_stream(dev)
-    cfg = spoly.default_config() if args.cull_levels is None else spoly.default_config(cull_levels=args.cull_levels)
+    kwc = {}
+    if args.cull_levels is not None:
+        kwc["cull_levels"] = args.cull_levels
+    if args.scan_restrict is not None:
+        kwc["scan_restrict"] = args.scan_restrict
+    cfg = spoly.default_config(**kwc)
     ctx = spoly.Context(local, cfg, stream=stream)
     ctx.upload_mesh(w.mesh)
     ep = torch.as_tensor(w.endpoints, dtype=torch.float64, device=dev)

@@ -81,6 +81,9 @@ typedef struct {
                             x_i -> x_{i+1} is dropped (scene = the specular mesh + the occluders of
                             spoly_upload_occluders; the chain's own triangles at a segment's ends are skipped;
                             a hit is t in (1e-7, 1 - 1e-7) inside the closed triangle); 0 (default)          */
+  int scan_restrict;     /* k=2 with the cull: the 100-piece determinant scan skips the pieces outside
+                            the v-range of T_1's surviving subdivision cells (+1 piece each side): the cull
+                            predicate is sound, so no admissible chain lies there (reading R25); 1 (default)    */
 } spoly_config;
 
 /* Fills cfg with the defaults listed above.  Never fails for a non-NULL cfg. */

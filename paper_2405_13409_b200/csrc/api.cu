@@ -87,6 +87,8 @@ struct spoly_ctx {
   DBuf<uint64_t> d_counts;
   DBuf<unsigned long long> d_offsets, d_emask;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2, d_pqa, d_pta;
+  DBuf<uint32_t> d_vr, d_vr2, d_vra;  // k=2: per-pair v-range of the surviving cull cells (reading R25)
+  bool have_vr = false;
   uint32_t k2_chunk = 0;  // queries per two-bounce cull chunk (learned; reset by mesh upload)
   DBuf<unsigned char> d_keep;
   DBuf<unsigned int> d_lerr;  // explicit tuple list validation word
@@ -155,6 +157,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->max_pairs = 1ull << 27;
   c->cull_levels = 3;
   c->visibility = 0;
+  c->scan_restrict = 1;
   return SPOLY_OK;
 }
 
@@ -200,7 +203,8 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_sub.release(); for (auto& u : ctx->d_up) u.release(); ctx->d_tlist.release(); ctx->d_tcount.release(); ctx->d_qkeys.release();
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_emask.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
-  ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_keep.release(); ctx->d_lerr.release(); ctx->d_nsel.release();
+  ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_vr.release(); ctx->d_vr2.release(); ctx->d_vra.release();
+  ctx->d_keep.release(); ctx->d_lerr.release(); ctx->d_nsel.release();
   ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
     for (auto& b : f) b.release();
@@ -428,7 +432,8 @@ static int bits_for(uint64_t n) {
 // frontier would exceed `budget` entries nothing is written and *over is set to its size.
 static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const double* endpoints, uint32_t q0,
                                   uint32_t qn, int top, uint32_t P, uint64_t budget, uint64_t* ncoarse,
-                                  uint64_t* nkept, const uint32_t** kq, const uint32_t** kt, uint64_t* over) {
+                                  uint64_t* nkept, const uint32_t** kq, const uint32_t** kt, const uint32_t** kv,
+                                  uint64_t* over) {
   cudaStream_t st = ctx->st;
   const int v1t = chain[0] == 'T', v2t = chain[1] == 'T';
   const uint32_t *fq = nullptr, *fa = nullptr, *fb = nullptr;  // implicit root frontier of the chunk
@@ -478,11 +483,13 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
   *nkept = npairs;
   *kq = ctx->d_pq.p;
   *kt = ctx->d_pt.p;
+  *kv = nullptr;
   if (ctx->cfg.cull_levels > 0 && npairs) {
     // barycentric subdivision refinement, then an order-preserving compaction (deterministic)
     CK(ctx->d_keep.ensure(npairs));
     CK(ctx->d_pq2.ensure(npairs));
     CK(ctx->d_pt2.ensure(2 * npairs));
+    CK(ctx->d_vr2.ensure(2 * npairs));
     CK(ctx->d_nsel.ensure(4));
     {
       const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * npairs, 1ull << 20), 1ull << 27);
@@ -490,7 +497,7 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
       CK(ctx->d_fcount.ensure(16));
       RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
       launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
-                          ctx->d_keep.p, RW, ctx->nsm, st);
+                          ctx->d_keep.p, nullptr, RW, ctx->nsm, st);
       ctx->launches += RW.launches;
       {
         unsigned long long fc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -524,6 +531,16 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
     *nkept = ns;
     *kq = ctx->d_pq2.p;
     *kt = ctx->d_pt2.p;
+    if (ns) {
+      // reading R25: the v-range of T_1's surviving cells of every kept pair (the same refinement on the kept pairs
+      // only, walking every surviving branch instead of stopping at the first)
+      const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * ns, 1ull << 20), 1ull << 27);
+      RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
+      launch_refine_pairs(ctx->d_pq2.p, ctx->d_pt2.p, ns, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
+                          ctx->d_keep.p, ctx->d_vr2.p, RW, ctx->nsm, st);
+      ctx->launches += RW.launches + 1;
+      *kv = ctx->d_vr2.p;
+    }
   }
   return SPOLY_OK;
 }
@@ -541,6 +558,7 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   CK(cudaSetDevice(ctx->device));
   cudaStream_t st = ctx->st;
   ctx->launches = 0;
+  ctx->have_vr = false;
   ctx->npairs_culled = 0;
   ctx->cull_tests = 0;
   memset(out, 0, sizeof(*out));
@@ -580,11 +598,13 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     uint32_t chunk = std::max<uint32_t>(1, std::min<uint32_t>(ctx->k2_chunk ? ctx->k2_chunk : nq, nq));
     chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunk, budget / P));
     uint64_t acc = 0, coarse = 0;
+    bool have_vr = ctx->cfg.cull_levels > 0;
     for (uint32_t q0 = 0; q0 < nq;) {
       const uint32_t qn = std::min(chunk, nq - q0);
       uint64_t ncoarse = 0, nkept = 0, over = 0;
-      const uint32_t *kq = nullptr, *kt = nullptr;
-      spoly_status s = cull_k2_chunk(ctx, chain, endpoints, q0, qn, top, P, budget, &ncoarse, &nkept, &kq, &kt, &over);
+      const uint32_t *kq = nullptr, *kt = nullptr, *kv = nullptr;
+      spoly_status s =
+          cull_k2_chunk(ctx, chain, endpoints, q0, qn, top, P, budget, &ncoarse, &nkept, &kq, &kt, &kv, &over);
       if (s != SPOLY_OK) return s;
       if (over) {  // a frontier of this chunk exceeded the budget: shrink the chunk and redo it
         if (qn == 1) return fail(ctx, SPOLY_ERR_CAPACITY, "two-bounce cull frontier of one query exceeds max_pairs");
@@ -593,10 +613,14 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
       }
       CK(grow_keep(ctx->d_pqa, acc, acc + nkept, st));
       CK(grow_keep(ctx->d_pta, 2 * acc, 2 * (acc + nkept), st));
+      CK(grow_keep(ctx->d_vra, 2 * acc, 2 * (acc + nkept), st));
       if (nkept) {
         CK(cudaMemcpyAsync(ctx->d_pqa.p + acc, kq, nkept * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
         CK(cudaMemcpyAsync(ctx->d_pta.p + 2 * acc, kt, 2 * nkept * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+        if (kv)
+          CK(cudaMemcpyAsync(ctx->d_vra.p + 2 * acc, kv, 2 * nkept * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
       }
+      if (nkept && !kv) have_vr = false;  // (cull_levels == 0: no cells, no ranges)
       acc += nkept;
       coarse += ncoarse;
       q0 += qn;
@@ -604,8 +628,10 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     ctx->k2_chunk = chunk;
     CK(ctx->d_pqa.ensure(1));
     CK(ctx->d_pta.ensure(2));
+    CK(ctx->d_vra.ensure(2));
     std::swap(ctx->d_pq, ctx->d_pqa);
     std::swap(ctx->d_pt, ctx->d_pta);
+    ctx->have_vr = have_vr && acc > 0;
     ctx->npairs_culled = ctx->cfg.cull_levels > 0 ? coarse : 0;
     npairs = acc;
   } else if (ctx->cfg.cull) {
@@ -747,8 +773,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
         K2Scratch W{ctx->d_rec.p, (ctx->d_rec.cap / rb) * rb, ctx->d_plist.p, ctx->d_clist.p, ctx->d_nsel.p + 4, 0};
         if (W.rec_cap / rb > ctx->d_plist.cap) W.rec_cap = ctx->d_plist.cap * rb;
         if (W.rec_cap / rb > ctx->d_clist.cap / 8) W.rec_cap = (ctx->d_clist.cap / 8) * rb;
-        launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, inten,
-                        prm, S, W, ctx->nsm, st);
+        // the pairs' surviving-cell v-ranges restrict the determinant scan (reading R25); the d_vra buffer holds
+        // them while the work list is the accumulated one (swapped into d_pq / d_pt above)
+        launch_solve_k2(chain[0] == 'T', chain[1] == 'T', ctx->d_pq.p, ctx->d_pt.p,
+                        ctx->have_vr && ctx->cfg.scan_restrict ? ctx->d_vra.p : nullptr, npairs, ctx->M, endpoints,
+                        inten, prm, S, W, ctx->nsm, st);
         ctx->launches += W.launches - 1;
       }
       ctx->launches += 1;

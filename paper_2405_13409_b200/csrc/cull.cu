@@ -12,6 +12,8 @@
 // Hierarchy: 64-triangle clusters -> 8-triangle sub-clusters -> triangles (all in Morton order), first
 // per tile of 32 Morton-sorted queries (tile endpoint spheres), then per query on the tile's survivors;
 // the work list is query-major and Morton-ordered (deterministic).
+#include <algorithm>
+
 #include "kernels.cuh"
 
 namespace spoly {
@@ -903,6 +905,7 @@ struct SubB {
   d3 c, ax;
   double rho, sinb;
   bool ok;  // false: no bound (keep)
+  d3 X[3];  // the cell's corners (exact direction cones)
 };
 
 __device__ __forceinline__ SubB sub_bound(const d3 P[3], const d3 N[3], int ou, int ov, int sg, int h) {
@@ -919,6 +922,9 @@ __device__ __forceinline__ SubB sub_bound(const d3 P[3], const d3 N[3], int ou, 
     if (!(l > 1e-30)) B.ok = false;
     M[j] = (1.0 / l) * n;
   }
+  B.X[0] = X[0];
+  B.X[1] = X[1];
+  B.X[2] = X[2];
   B.c = (1.0 / 3.0) * (X[0] + X[1] + X[2]);
   B.rho = fmax(norm(X[0] - B.c), fmax(norm(X[1] - B.c), norm(X[2] - B.c))) * (1.0 + 1e-9) + 1e-12;
   const d3 s = M[0] + M[1] + M[2];
@@ -974,6 +980,53 @@ __device__ __forceinline__ bool subpair_keep(d3 x0, d3 x3, const SubB& A, const 
   return false;
 }
 
+// exact direction cone of a point set (the oracle's cone_of): axis = normalised sum of the unit
+// directions, chord = max |w_j - axis| (+1e-9 relative slack).  Every direction to / between points of the convex
+// hulls is a positive combination of these, so it lies in the cap {w : |w - axis| <= chord}.  false: no bound.
+template <int M>
+__device__ __forceinline__ bool exact_cone(const d3 (&d)[M], d3& axis, double& chord) {
+  d3 w[M];
+  d3 s = mk3(0, 0, 0);
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const double l2 = dot(d[j], d[j]);
+    if (!(l2 > 0)) return false;
+    w[j] = (1.0 / sqrt(l2)) * d[j];
+    s = s + w[j];
+  }
+  const double sl = norm(s);
+  if (!(sl > 0)) return false;
+  axis = (1.0 / sl) * s;
+  double c2 = 0;
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const d3 t = w[j] - axis;
+    c2 = fmax(c2, dot(t, t));
+  }
+  chord = sqrt(c2) * (1.0 + 1e-9) + 1e-12;
+  return true;
+}
+
+// sub-pair test with exact vertex cones (tighter than the sphere bounds of subpair_keep, same predicate)
+__device__ __forceinline__ bool subpair_keep_exact(const SubB& A, const SubB& B, d3 a0, double c0, bool ok0, d3 a3,
+                                                   double c3, bool ok3, const double e[2][3], int ncombo) {
+  if (!A.ok || !B.ok || !ok0 || !ok3) return true;
+  d3 d[9];
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+#pragma unroll
+    for (int j = 0; j < 3; ++j) d[3 * i + j] = B.X[j] - A.X[i];
+  d3 aAB;
+  double cAB;
+  if (!exact_cone<9>(d, aAB, cAB)) return true;
+  const d3 aBA = -1.0 * aAB;
+  for (int c = 0; c < ncombo; ++c)
+    if (node_keep_d(a0, c0, aAB, cAB, e[c][0], e[c][1], A.ax, A.sinb) &&
+        node_keep_d(aBA, cAB, a3, c3, e[c][1], e[c][2], B.ax, B.sinb))
+      return true;
+  return false;
+}
+
 struct SubNode {
   int u1, v1, s1, u2, v2, s2;
 };
@@ -997,8 +1050,25 @@ __device__ uint32_t children_mask(const d3 P1[3], const d3 N1[3], const d3 P2[3]
     B[c] = sub_bound(P2, N2, cu, cv, cs, h >> 1);
   }
   uint32_t m = 0;
+#ifndef SPOLY_REFINE_SPHERE
+  // exact cones of the directions from each cell to its endpoint, once per cell
+  d3 a0[4], a3[4];
+  double c0[4], c3[4];
+  bool ok0[4], ok3[4];
+  for (int c = 0; c < 4; ++c) {
+    d3 d0[3] = {x0 - A[c].X[0], x0 - A[c].X[1], x0 - A[c].X[2]};
+    ok0[c] = exact_cone<3>(d0, a0[c], c0[c]);
+    d3 d3_[3] = {x3 - B[c].X[0], x3 - B[c].X[1], x3 - B[c].X[2]};
+    ok3[c] = exact_cone<3>(d3_, a3[c], c3[c]);
+  }
+  for (int i = 0; i < 16; ++i) {
+    const int ia = i >> 2, ib = i & 3;
+    if (subpair_keep_exact(A[ia], B[ib], a0[ia], c0[ia], ok0[ia], a3[ib], c3[ib], ok3[ib], e, ncombo)) m |= 1u << i;
+  }
+#else
   for (int i = 0; i < 16; ++i)
     if (subpair_keep(x0, x3, A[i >> 2], B[i & 3], e, ncombo)) m |= 1u << i;
+#endif
   return m;
 }
 
@@ -1043,7 +1113,8 @@ __global__ void __launch_bounds__(128) k_refine_level(int level, int last, const
                                                       const uint64_t* __restrict__ fin,
                                                       const unsigned long long* __restrict__ nin,
                                                       uint64_t* __restrict__ fout, unsigned long long* __restrict__ nout,
-                                                      uint64_t cap, uint8_t* __restrict__ keep) {
+                                                      uint64_t cap, uint8_t* __restrict__ keep,
+                                                      uint32_t* __restrict__ vrange) {
   const uint64_t n = fin ? min((uint64_t)*nin, cap) : npairs;  // appends beyond cap were not written
   const int H = 1 << kMaxLevels, h = H >> level;  // node size at this level
   for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
@@ -1054,7 +1125,9 @@ __global__ void __launch_bounds__(128) k_refine_level(int level, int last, const
       r = (uint32_t)(ent >> 22);
       dec_node((ent >> 11) & 2047, nd.u1, nd.v1, nd.s1);
       dec_node(ent & 2047, nd.u2, nd.v2, nd.s2);
-      if (keep[r]) continue;  // already proven kept through another branch
+      // already proven kept through another branch (without v-ranges: every surviving branch must be walked to
+      // bound the surviving v-range)
+      if (!vrange && keep[r]) continue;
     } else {
       r = (uint32_t)i;
       nd = {0, 0, 1, 0, 0, 1};
@@ -1070,11 +1143,30 @@ __global__ void __launch_bounds__(128) k_refine_level(int level, int last, const
     if (!m) continue;
     if (last) {
       keep[r] = 1;
+      if (vrange) {
+        // v-range (units of 2^-kMaxLevels) of the surviving T_1 cells: a chain of this pair can only have its x_1
+        // there (the predicate is sound), so the determinant scan may skip the pieces outside it (reading R25)
+        int lo = 1 << kMaxLevels, hi = 0;
+        for (int c = 0; c < 4; ++c) {
+          if (!((m >> (4 * c)) & 15u)) continue;
+          int cu, cv, cs;
+          child_of(nd.u1, nd.v1, nd.s1, h, c, cu, cv, cs);
+          const int a = cs > 0 ? cv : cv - (h >> 1), b = cs > 0 ? cv + (h >> 1) : cv;
+          lo = min(lo, a);
+          hi = max(hi, b);
+        }
+        atomicMin(vrange + 2 * r, (uint32_t)lo);
+        atomicMax(vrange + 2 * r + 1, (uint32_t)hi);
+      }
       continue;
     }
     const unsigned long long pos = atomicAdd(nout, (unsigned long long)__popc(m));
     if (pos + __popc(m) > cap) {
       keep[r] = 1;
+      if (vrange) {  // not refined further: the whole triangle
+        atomicMin(vrange + 2 * r, 0u);
+        atomicMax(vrange + 2 * r + 1, (uint32_t)(1 << kMaxLevels));
+      }
       continue;
     }
     uint32_t mm = m;
@@ -1089,11 +1181,97 @@ __global__ void __launch_bounds__(128) k_refine_level(int level, int last, const
   }
 }
 
+// Depth-first refinement, thread per pair (no frontier: the breadth-first frontier overflowed its cap at level 2 on
+// C4 and kept whole pairs conservatively): a stack of (level, T_1 cell, T_2 cell); a pair is kept as soon as one
+// cell pair survives `levels` deep (vrange == NULL), or every surviving leaf is visited and the v-range of its T_1
+// cells recorded (vrange != NULL, reading R25).
+__global__ void __launch_bounds__(128) k_refine_dfs(int levels, const uint32_t* __restrict__ pq,
+                                                    const uint32_t* __restrict__ pt, uint64_t npairs,
+                                                    const TriRec* __restrict__ tris, const double* __restrict__ ep,
+                                                    int v1t, int v2t, float ef, float eb, uint8_t* __restrict__ keep,
+                                                    uint32_t* __restrict__ vrange, unsigned long long* __restrict__ ntests) {
+  constexpr int H = 1 << kMaxLevels;
+  unsigned long long tests = 0;
+  for (uint64_t r = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; r < npairs; r += (uint64_t)gridDim.x * blockDim.x) {
+    const double* e = ep + 6ull * pq[r];
+    const d3 x0 = mk3(e[0], e[1], e[2]), x3 = mk3(e[3], e[4], e[5]);
+    d3 P1[3], N1[3], P2[3], N2[3];
+    load_tri(tris, pt[2 * r], P1, N1);
+    load_tri(tris, pt[2 * r + 1], P2, N2);
+    double ec[2][3];
+    const int ncombo = eta_combos(x0, P1, v1t, v2t, ef, eb, ec);
+    uint32_t stack[16 * kMaxLevels + 1];  // level (3) | T_1 cell (11) | T_2 cell (11)
+    int sp = 0;
+    stack[sp++] = (uint32_t)((enc_node(0, 0, 1) << 11) | enc_node(0, 0, 1));
+    bool kept = false;
+    int lo = H, hi = 0;
+    while (sp > 0) {
+      const uint32_t ent = stack[--sp];
+      const int level = (int)(ent >> 22);
+      SubNode nd;
+      dec_node((ent >> 11) & 2047, nd.u1, nd.v1, nd.s1);
+      dec_node(ent & 2047, nd.u2, nd.v2, nd.s2);
+      const int h = H >> level;
+      const uint32_t m = children_mask(P1, N1, P2, N2, x0, x3, nd, h, ec, ncombo);
+      tests += 16;
+      if (!m) continue;
+      if (level + 1 == levels) {
+        kept = true;
+        if (!vrange) break;
+        for (int c = 0; c < 4; ++c) {
+          if (!((m >> (4 * c)) & 15u)) continue;
+          int cu, cv, cs;
+          child_of(nd.u1, nd.v1, nd.s1, h, c, cu, cv, cs);
+          lo = min(lo, cs > 0 ? cv : cv - (h >> 1));
+          hi = max(hi, cs > 0 ? cv + (h >> 1) : cv);
+        }
+        continue;
+      }
+      uint32_t mm = m;
+      while (mm) {
+        const int c = __ffs(mm) - 1;
+        mm &= mm - 1;
+        SubNode ch;
+        child_of(nd.u1, nd.v1, nd.s1, h, c >> 2, ch.u1, ch.v1, ch.s1);
+        child_of(nd.u2, nd.v2, nd.s2, h, c & 3, ch.u2, ch.v2, ch.s2);
+        stack[sp++] = ((uint32_t)(level + 1) << 22) | (uint32_t)((enc_node(ch.u1, ch.v1, ch.s1) << 11) |
+                                                                 enc_node(ch.u2, ch.v2, ch.s2));
+      }
+    }
+    keep[r] = kept ? 1 : 0;
+    if (vrange) {
+      vrange[2 * r] = kept ? (uint32_t)lo : (uint32_t)H;
+      vrange[2 * r + 1] = kept ? (uint32_t)hi : 0u;
+    }
+  }
+  for (int off = 16; off > 0; off >>= 1) tests += __shfl_xor_sync(0xffffffffu, tests, off);
+  if ((threadIdx.x & 31) == 0 && tests) atomicAdd(ntests, tests);
+}
+
+__global__ void k_vrange_init(uint32_t* vr, uint64_t n) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    vr[2 * i] = 1u << kMaxLevels;
+    vr[2 * i + 1] = 0u;
+  }
+}
+
 void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
-                         int levels, int v1t, int v2t, uint8_t* keep, RefineScratch& W, int nsm, cudaStream_t st) {
+                         int levels, int v1t, int v2t, uint8_t* keep, uint32_t* vrange, RefineScratch& W, int nsm,
+                         cudaStream_t st) {
   if (!n) return;
   if (levels > kMaxLevels) levels = kMaxLevels;
+#ifdef SPOLY_REFINE_DFS  // A/B: thread-per-pair depth-first (C4: same pairs, cull 0.56 -> 1.14 s: divergence)
+  {
+    cudaMemsetAsync(W.count, 0, sizeof(unsigned long long), st);
+    const uint64_t want = (n + 127) / 128, cap = (uint64_t)nsm * 32;
+    k_refine_dfs<<<(int)(want < cap ? want : cap), 128, 0, st>>>(levels, pq, pt, n, M.tris, ep, v1t, v2t,
+                                                                  M.eta_front, M.eta_back, keep, vrange, W.count);
+    W.launches = 1;
+    return;
+  }
+#endif
   cudaMemsetAsync(keep, 0, n, st);
+  if (vrange) k_vrange_init<<<(int)std::min<uint64_t>((n + 255) / 256, (uint64_t)nsm * 8), 256, 0, st>>>(vrange, n);
   cudaMemsetAsync(W.count, 0, 2 * levels * sizeof(unsigned long long), st);
   const uint64_t* fin = nullptr;
   const unsigned long long* nin = nullptr;
@@ -1105,7 +1283,7 @@ void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, con
     const uint64_t want = (work + 127) / 128, cap = (uint64_t)nsm * 16;
     k_refine_level<<<(int)(want < cap ? want : cap), 128, 0, st>>>(l, last, pq, pt, n, M.tris, ep, v1t, v2t,
                                                                     M.eta_front, M.eta_back, fin, nin, fout, nout,
-                                                                    W.cap, keep);
+                                                                    W.cap, keep, vrange);
     fin = fout;
     nin = nout;
   }

@@ -48,9 +48,10 @@ struct K2Scratch {
 uint64_t k2_record_bytes(int v1t, int v2t);
 // the Eq. 20 sqrt surrogate table (6 x (lo, hi, c0, c1, d1)): host copy, or read back from constant memory
 cudaError_t k2_sqrt_table(int from_device, double* out30);
-void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
-                     int nsm, cudaStream_t st);
+// vrange: per pair [lo, hi] v-range (1/32 units) of the surviving cull cells, or NULL (whole [0, 1])
+void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, const uint32_t* vrange, uint64_t npairs,
+                     const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
+                     const SolSink& S, K2Scratch& W, int nsm, cudaStream_t st);
 // two-bounce pair cull: split level of the implicit hierarchy (-1: > 2^22 triangles) and one expansion pass
 int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query);
 void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
@@ -63,8 +64,11 @@ struct RefineScratch {
   unsigned long long* count;  // >= 2 * levels
   int launches;
 };
+// keep[i] = 1 for the pairs some subdivision cell pair survives `levels` deep; vrange (optional, 2 x uint32 per pair):
+// [lo, hi] v-range of T_1's surviving cells in units of 1/32 (reading R25)
 void launch_refine_pairs(const uint32_t* pq, const uint32_t* pt, uint64_t n, const DeviceMesh& M, const double* ep,
-                         int levels, int v1t, int v2t, uint8_t* keep, RefineScratch& W, int nsm, cudaStream_t st);
+                         int levels, int v1t, int v2t, uint8_t* keep, uint32_t* vrange, RefineScratch& W, int nsm,
+                         cudaStream_t st);
 void launch_all_pairs_k2(uint32_t nq, uint32_t ntris, uint32_t* pair_query, uint32_t* pair_tpos, cudaStream_t st);
 
 // reduce.cu

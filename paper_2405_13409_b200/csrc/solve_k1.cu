@@ -260,6 +260,11 @@ __global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_
   // a's 6 coefficients wait in shared memory (not registers) through the elimination and the Bernstein
   // test, until the job slot is known; [coefficient][thread], conflict-free
   __shared__ double s_aj[6][128];
+#if defined(SPOLY_P1_WARP_BUFFER)
+  __shared__ uint32_t s_wpair[4][64];
+  __shared__ double s_wroot[4][64];
+  int wbuf_n = 0;  // warp-uniform
+#endif
   for (uint64_t bb = (uint64_t)blockIdx.x * blockDim.x; bb < npairs; bb += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = bb + threadIdx.x;
     const bool active = i < npairs;
@@ -400,39 +405,12 @@ __global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_
       }
     }
     emit_flag(active && flags != 0, flags, i, S);
-    // two-ended dense list: path entries (pair, root) from the front, block-aggregated (one atomic per 128 pairs;
-    // same-address atomics serialise in L2); deeper recursions (pair, meta, r) from the back
-#ifdef SPOLY_P1_WARP_APPEND
-    // warp-level append: no block barrier (the warps' Newton loops end at different times)
-    uint32_t ex1;
-    const unsigned long long b1 = warp_alloc(J.count, to_path ? 1u : 0u, &ex1);
-#else
-    const unsigned mb = __ballot_sync(0xffffffffu, to_path);
-    if (lane == 0) s_off[warp] = __popc(mb);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      uint32_t acc = 0;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        const uint32_t c = s_off[w];
-        s_off[w] = acc;
-        acc += c;
-      }
-      s_base = acc ? atomicAdd(J.count, (unsigned long long)acc) : 0ull;
-    }
-    __syncthreads();
-    const uint32_t ex1 = s_off[warp] + __popc(mb & ((1u << lane) - 1u));
-    const unsigned long long b1 = s_base;
-#endif
+    // two-ended dense list: deeper recursions (pair, meta, r) from the back, path entries (pair, root) from the front
     // deep list: deeper recursions, and the rare monotone jobs whose back-substitution needs the b fallback or
     // a c14 probe (the deep kernel re-isolates their single root; the general path kernel finishes them)
     const bool deep = job && (!mono || complex_job);
     uint32_t ex2;
     const unsigned long long b2 = warp_alloc(J.count + 1, deep ? 1u : 0u, &ex2);
-    if (to_path && b1 + ex1 < J.capacity) {
-      J.pair[b1 + ex1] = (uint32_t)i;
-      J.root[b1 + ex1] = root;
-    }
     if (deep && b2 + ex2 < J.capacity) {
       const unsigned long long p = J.capacity - 1 - (b2 + ex2);
       J.pair[p] = (uint32_t)i;
@@ -446,7 +424,73 @@ __global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_
         for (int t = 0; t < NR; ++t) J.r[p * NR + t] = r[t];
       }
     }
+    // path entries (pair, root) from the front
+#if defined(SPOLY_P1_WARP_BUFFER)
+    // per-warp staging in shared memory, flushed 32 at a time with one atomic: no block barrier (the warps'
+    // Newton loops end at different times), one global atomic per ~100 pairs
+    {
+      const unsigned mb = __ballot_sync(0xffffffffu, to_path);
+      if (to_path) {
+        const int pos = wbuf_n + __popc(mb & ((1u << lane) - 1u));
+        s_wpair[warp][pos] = (uint32_t)i;
+        s_wroot[warp][pos] = root;
+      }
+      wbuf_n += __popc(mb);
+      __syncwarp();
+      if (wbuf_n >= 32) {
+        unsigned long long b = 0;
+        if (lane == 0) b = atomicAdd(J.count, 32ull);
+        b = __shfl_sync(0xffffffffu, b, 0);
+        if (b + lane < J.capacity) {
+          J.pair[b + lane] = s_wpair[warp][lane];
+          J.root[b + lane] = s_wroot[warp][lane];
+        }
+        __syncwarp();
+        if (lane < wbuf_n - 32) {
+          s_wpair[warp][lane] = s_wpair[warp][32 + lane];
+          s_wroot[warp][lane] = s_wroot[warp][32 + lane];
+        }
+        wbuf_n -= 32;
+        __syncwarp();
+      }
+    }
+#else
+    {
+      // block-aggregated: one atomic per 128 pairs (same-address atomics serialise in L2)
+      const unsigned mb = __ballot_sync(0xffffffffu, to_path);
+      if (lane == 0) s_off[warp] = __popc(mb);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t acc = 0;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          const uint32_t c = s_off[w];
+          s_off[w] = acc;
+          acc += c;
+        }
+        s_base = acc ? atomicAdd(J.count, (unsigned long long)acc) : 0ull;
+      }
+      __syncthreads();
+      const uint32_t ex1 = s_off[warp] + __popc(mb & ((1u << lane) - 1u));
+      const unsigned long long b1 = s_base;
+      if (to_path && b1 + ex1 < J.capacity) {
+        J.pair[b1 + ex1] = (uint32_t)i;
+        J.root[b1 + ex1] = root;
+      }
+    }
+#endif
   }
+#if defined(SPOLY_P1_WARP_BUFFER)
+  if (wbuf_n > 0) {  // final partial flush
+    unsigned long long b = 0;
+    if (lane == 0) b = atomicAdd(J.count, (unsigned long long)wbuf_n);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (lane < wbuf_n && b + lane < J.capacity) {
+      J.pair[b + lane] = s_wpair[warp][lane];
+      J.root[b + lane] = s_wroot[warp][lane];
+    }
+  }
+#endif
   flush_counters(S, cnt);
 }
 

@@ -587,6 +587,7 @@ constexpr int kScanWarps = 4;
 __host__ __device__ constexpr int scan_min_blocks(int nc) { return nc == 0 ? 1 : (nc <= 16 ? 4 : (nc <= 24 ? 3 : 2)); }
 template <bool V1T, bool V2T, int NC>
 __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
+                                                          const uint32_t* __restrict__ vrange,
                                                           double* __restrict__ recs, SolSink S,
                                                           const uint32_t* __restrict__ clist,
                                                           const unsigned long long* __restrict__ ccount,
@@ -638,13 +639,22 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
         return wdet_T<G, R::NR, NC>(g, AT, D::DA, BT, D::DB, n, v, lg);
       };
       const int P = prm.pieces;
+      // reading R25: only the pieces that overlap the v-range of T_1's surviving cull cells, +1 piece each side
+      // (a chain elsewhere is excluded by the sound cull predicate); samples j in [jlo, jhi] on the same grid
+      int jlo = 0, jhi = P;
+      if (vrange) {
+        const uint32_t lo = vrange[2 * (p0 + r)], hi = vrange[2 * (p0 + r) + 1];
+        jlo = max(0, (int)((lo * (uint32_t)P) / 32u) - 1);
+        jhi = min(P, (int)((hi * (uint32_t)P + 31u) / 32u) + 1);
+        if (jhi < jlo) jhi = jlo;
+      }
       int nprobe = 0;
       double lg_prev = -INFINITY, lg_cur;
-      int s_cur = det(0.0, &lg_cur);
-      for (int j = 0; j <= P; ++j) {
+      int s_cur = det((double)jlo / P, &lg_cur);
+      for (int j = jlo; j <= jhi; ++j) {
         int s_next = 0;
         double lg_next = -INFINITY;
-        if (j < P) s_next = det((double)(j + 1) / P, &lg_next);
+        if (j < jhi) s_next = det((double)(j + 1) / P, &lg_next);
         // c14: |det(v_j)| < 1e-9 max(neighbours), a root within ~1e-11 of the sample: a near-tangency condition the
         // path kernel probes (stored as v_j + 2 among the v-roots; reading R11); one that does not fit flags
         const double nb = fmax(lg_prev, lg_next);
@@ -665,7 +675,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
             flags |= SPOLY_FLAG_TRUNCATED;
             cnt[C_TRUNCATED]++;
           }
-        } else if (j < P && s_next != 0 && s_next != s_cur) {
+        } else if (j < jhi && s_next != 0 && s_next != s_cur) {
           double lo = (double)j / P, hi = (double)(j + 1) / P;
           for (int it = 0; it < prm.scan_bisect_iters; ++it) {
             const double m = 0.5 * (lo + hi);
@@ -1002,7 +1012,8 @@ __global__ void __launch_bounds__(128) k2_path(const uint32_t* __restrict__ pq, 
 }
 
 template <bool V1T, bool V2T>
-static void launch_k2(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M, const double* ep,
+static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr, uint64_t npairs, const DeviceMesh& M,
+                      const double* ep,
                       const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W, int nsm,
                       cudaStream_t st) {
   using D = Deg2<V1T, V2T>;
@@ -1037,20 +1048,20 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, uint64_t npairs, c
                                                                                                    cc);
     const uint32_t* L = W.clist;
     if (G == 16) {
-      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
-      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
-      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
       W.launches += 3;
     } else {
-      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
-      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
-      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
-      k2_scan<V1T, V2T, nc_of_class<G>(3)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 3 * np, cc + 3, W.plist, W.ctr + 1, cn + 3);
-      k2_scan<V1T, V2T, nc_of_class<G>(4)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 4 * np, cc + 4, W.plist, W.ctr + 1, cn + 4);
-      k2_scan<V1T, V2T, nc_of_class<G>(5)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, W.rec, S, L + 5 * np, cc + 5, W.plist, W.ctr + 1, cn + 5);
+      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      k2_scan<V1T, V2T, nc_of_class<G>(3)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 3 * np, cc + 3, W.plist, W.ctr + 1, cn + 3);
+      k2_scan<V1T, V2T, nc_of_class<G>(4)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 4 * np, cc + 4, W.plist, W.ctr + 1, cn + 4);
+      k2_scan<V1T, V2T, nc_of_class<G>(5)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 5 * np, cc + 5, W.plist, W.ctr + 1, cn + 5);
       W.launches += 6;
       if (D::DB > 32) {
-        k2_scan<V1T, V2T, 0><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, W.rec, S, L + 6 * np, cc + 6, W.plist, W.ctr + 1, cn + 6);
+        k2_scan<V1T, V2T, 0><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, vr, W.rec, S, L + 6 * np, cc + 6, W.plist, W.ctr + 1, cn + 6);
         W.launches += 1;
       }
     }
@@ -1066,18 +1077,18 @@ uint64_t k2_record_bytes(int v1t, int v2t) {
   return Rec2<false, false>::STRIDE * sizeof(double);
 }
 
-void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, uint64_t npairs, const DeviceMesh& M,
-                     const double* ep, const double* inten, const SolveParams& prm, const SolSink& S, K2Scratch& W,
-                     int nsm, cudaStream_t st) {
+void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, const uint32_t* vr, uint64_t npairs,
+                     const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
+                     const SolSink& S, K2Scratch& W, int nsm, cudaStream_t st) {
   if (!npairs) return;
   if (v1t && v2t)
-    launch_k2<true, true>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
+    launch_k2<true, true>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
   else if (v1t)
-    launch_k2<true, false>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
+    launch_k2<true, false>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
   else if (v2t)
-    launch_k2<false, true>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
+    launch_k2<false, true>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
   else
-    launch_k2<false, false>(pq, pt, npairs, M, ep, inten, prm, S, W, nsm, st);
+    launch_k2<false, false>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
 }
 
 }  // namespace spoly
