@@ -226,6 +226,7 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cull-levels", type=int, default=None, help="k=2 cull subdivision levels (default: library)")
     ap.add_argument("--scan-restrict", type=int, default=None, help="k=2 scan restriction (reading R25; default on)")
+    ap.add_argument("--k2-tiles", type=int, default=None, help="k=2 cull in query tiles (default on)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", 0))
@@ -274,6 +275,8 @@ def main():
         kwc["cull_levels"] = args.cull_levels
     if args.scan_restrict is not None:
         kwc["scan_restrict"] = args.scan_restrict
+    if args.k2_tiles is not None:
+        kwc["k2_tiles"] = args.k2_tiles
     cfg = spoly.default_config(**kwc)
     ctx = spoly.Context(local, cfg, stream=stream)
     ctx.upload_mesh(w.mesh)

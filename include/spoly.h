@@ -84,6 +84,9 @@ typedef struct {
   int scan_restrict;     /* k=2 with the cull: the 100-piece determinant scan skips the pieces outside
                             the v-range of T_1's surviving subdivision cells (+1 piece each side): the cull
                             predicate is sound, so no admissible chain lies there (reading R25); 1 (default)    */
+  int k2_tiles;          /* k=2 cull: expand the node-pair hierarchy once per tile of 32 Morton-sorted queries
+                            (endpoint spheres), then test each query exactly on its tile's triangle pairs; the
+                            work list is query-major in that order; 1 (default), 0: per-query expansion     */
 } spoly_config;
 
 /* Fills cfg with the defaults listed above.  Never fails for a non-NULL cfg. */

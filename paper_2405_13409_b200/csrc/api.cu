@@ -88,6 +88,9 @@ struct spoly_ctx {
   DBuf<unsigned long long> d_offsets, d_emask;
   DBuf<uint32_t> d_pq, d_pt, d_pt_orig, d_pq2, d_pt2, d_pqa, d_pta;
   DBuf<uint32_t> d_vr, d_vr2, d_vra;  // k=2: per-pair v-range of the surviving cull cells (reading R25)
+  DBuf<float4> d_tsph;                 // k=2 query tiles: endpoint spheres
+  DBuf<uint32_t> d_tq, d_tp;           // k=2 query tiles: (tile, T_1, T_2) lists
+  DBuf<unsigned long long> d_toff, d_moff;
   bool have_vr = false;
   uint32_t k2_chunk = 0;  // queries per two-bounce cull chunk (learned; reset by mesh upload)
   DBuf<unsigned char> d_keep;
@@ -158,6 +161,7 @@ spoly_status spoly_default_config(spoly_config* c) {
   c->cull_levels = 3;
   c->visibility = 0;
   c->scan_restrict = 1;
+  c->k2_tiles = 1;
   return SPOLY_OK;
 }
 
@@ -204,6 +208,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   ctx->d_qorder.release(); ctx->d_qbounds.release();
   ctx->d_counts.release(); ctx->d_offsets.release(); ctx->d_emask.release(); ctx->d_pq.release(); ctx->d_pt.release(); ctx->d_pqa.release(); ctx->d_pta.release(); ctx->d_pt_orig.release();
   ctx->d_pq2.release(); ctx->d_pt2.release(); ctx->d_vr.release(); ctx->d_vr2.release(); ctx->d_vra.release();
+  ctx->d_tsph.release(); ctx->d_tq.release(); ctx->d_tp.release(); ctx->d_toff.release(); ctx->d_moff.release();
   ctx->d_keep.release(); ctx->d_lerr.release(); ctx->d_nsel.release();
   ctx->d_rec.release(); ctx->d_plist.release(); ctx->d_clist.release(); ctx->d_qmask.release(); ctx->d_front.release(); ctx->d_fcount.release();
   for (auto& f : ctx->d_fr)
@@ -430,14 +435,25 @@ static int bits_for(uint64_t n) {
 // subdivision refinement and an order-preserving compaction.  On return (*kq, *kt) point at the kept
 // (query, T1, T2) list of *nkept entries (ctx-owned scratch, valid until the next chunk).  If a level's
 // frontier would exceed `budget` entries nothing is written and *over is set to its size.
+// Tiled variant (order != NULL): q0 / qn are SORTED positions, multiples of 32 (tiles of 32 Morton-sorted queries,
+// the last one ragged); the expansion runs once per tile against the tile's endpoint spheres, then every query
+// tests its tile's triangle pairs exactly (launch_query_pairs).  The coarse list is query-major in sorted order.
 static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const double* endpoints, uint32_t q0,
                                   uint32_t qn, int top, uint32_t P, uint64_t budget, uint64_t* ncoarse,
                                   uint64_t* nkept, const uint32_t** kq, const uint32_t** kt, const uint32_t** kv,
-                                  uint64_t* over) {
+                                  uint64_t* over, const uint32_t* order, uint32_t nq_total, uint32_t ts) {
   cudaStream_t st = ctx->st;
   const int v1t = chain[0] == 'T', v2t = chain[1] == 'T';
   const uint32_t *fq = nullptr, *fa = nullptr, *fb = nullptr;  // implicit root frontier of the chunk
-  uint64_t nf = (uint64_t)qn * P;
+  const uint32_t ntl = order ? (qn + ts - 1) / ts : 0;
+  const float4* tsph = nullptr;
+  if (order) {
+    CK(ctx->d_tsph.ensure(2ull * ntl));
+    launch_tile_spheres(endpoints, nq_total, order, q0, ntl, ts, ctx->d_tsph.p, ctx->nsm, st);
+    tsph = ctx->d_tsph.p;
+    ctx->launches++;
+  }
+  uint64_t nf = (uint64_t)(order ? ntl : qn) * P;
   int cur = 0;
   *over = 0;
   for (int cl = top - 1; cl >= 0; --cl) {
@@ -445,8 +461,8 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
     CK(ctx->d_offsets.ensure(nf + 1));
     uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
     CK(ctx->d_emask.ensure(nf));
-    launch_pair_expand(0, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, ctx->d_emask.p, nullptr, nullptr,
-                       nullptr, nullptr, ctx->nsm, st);
+    launch_pair_expand(0, cl, endpoints, order ? 0 : q0, fq, fa, fb, nf, ctx->M, v1t, v2t, c32, ctx->d_emask.p,
+                       nullptr, nullptr, nullptr, nullptr, ctx->nsm, st, tsph);
     ctx->cull_tests += nf * (64 + (fq ? 0 : 1));  // child node-pair tests (+ the root pair test)
     size_t tbytes = 0;
     CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)nf, st));
@@ -462,21 +478,70 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
       return SPOLY_OK;
     }
     if (cl == 0) {
-      CK(ctx->d_pq.ensure(tot));
-      CK(ctx->d_pt.ensure(2 * tot));
-      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
-                         ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, nullptr, ctx->nsm, st);
+      // per-query mode: the coarse list; tile mode: the tiles' triangle-pair lists (tile-major)
+      CK((order ? ctx->d_tq : ctx->d_pq).ensure(tot));
+      CK((order ? ctx->d_tp : ctx->d_pt).ensure(2 * tot));
+      launch_pair_expand(1, cl, endpoints, order ? 0 : q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
+                         ctx->d_offsets.p, order ? ctx->d_tq.p : ctx->d_pq.p, order ? ctx->d_tp.p : ctx->d_pt.p,
+                         nullptr, ctx->nsm, st, tsph);
     } else {
       const int nx = 1 - cur;
       for (int c = 0; c < 3; ++c) CK(ctx->d_fr[nx][c].ensure(tot));
-      launch_pair_expand(1, cl, endpoints, q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
-                         ctx->d_offsets.p, ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st);
+      launch_pair_expand(1, cl, endpoints, order ? 0 : q0, fq, fa, fb, nf, ctx->M, v1t, v2t, nullptr, ctx->d_emask.p,
+                         ctx->d_offsets.p, ctx->d_fr[nx][0].p, ctx->d_fr[nx][1].p, ctx->d_fr[nx][2].p, ctx->nsm, st,
+                         tsph);
       fq = ctx->d_fr[nx][0].p;
       fa = ctx->d_fr[nx][1].p;
       fb = ctx->d_fr[nx][2].p;
       cur = nx;
     }
     nf = tot;
+  }
+  if (order) {
+    // tile offsets of the tile-major pair list, the per-query mask layout, then the exact per-query pass
+    const uint64_t ntp = nf;
+    CK(ctx->d_toff.ensure(ntl + 1));
+    CK(cudaMemsetAsync(ctx->d_toff.p, 0, (ntl + 1) * sizeof(unsigned long long), st));
+    launch_tile_hist(ctx->d_tq.p, ntp, ctx->d_toff.p + 1, ctx->nsm, st);
+    std::vector<unsigned long long> hoff(ntl + 1), hmoff(ntl + 1);
+    CK(cudaMemcpyAsync(hoff.data(), ctx->d_toff.p, (ntl + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    hmoff[0] = 0;
+    for (uint32_t t = 0; t < ntl; ++t) {
+      const unsigned long long c = hoff[t + 1];
+      hoff[t + 1] = hoff[t] + c;
+      hmoff[t + 1] = hmoff[t] + (unsigned long long)ts * ((c + 31) / 32);
+    }
+    CK(ctx->d_moff.ensure(ntl + 1));
+    CK(cudaMemcpyAsync(ctx->d_toff.p, hoff.data(), (ntl + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(ctx->d_moff.p, hmoff.data(), (ntl + 1) * sizeof(unsigned long long), cudaMemcpyHostToDevice, st));
+    CK(ctx->d_qmask.ensure(std::max<unsigned long long>(hmoff[ntl], 1)));
+    CK(ctx->d_counts.ensure(qn / 2 + 1));
+    CK(ctx->d_offsets.ensure(qn + 1));
+    uint32_t* c32 = reinterpret_cast<uint32_t*>(ctx->d_counts.p);
+    launch_query_pairs(0, endpoints, nq_total, order, q0, qn, ts, ctx->d_toff.p, ctx->d_tp.p, ctx->M, v1t, v2t,
+                       ctx->d_moff.p, ctx->d_qmask.p, c32, nullptr, nullptr, nullptr, ctx->nsm, st);
+    for (uint32_t t = 0; t < ntl; ++t)
+      ctx->cull_tests += (hoff[t + 1] - hoff[t]) * (uint64_t)std::min<uint32_t>(ts, qn - ts * t);
+    size_t tbytes = 0;
+    CK(cub::DeviceScan::InclusiveSum(nullptr, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)qn, st));
+    CK(ctx->d_temp.ensure(tbytes));
+    CK(cudaMemsetAsync(ctx->d_offsets.p, 0, sizeof(unsigned long long), st));
+    CK(cub::DeviceScan::InclusiveSum(ctx->d_temp.p, tbytes, c32, ctx->d_offsets.p + 1, (int64_t)qn, st));
+    unsigned long long tot = 0;
+    CK(cudaMemcpyAsync(&tot, ctx->d_offsets.p + qn, sizeof(tot), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    CK(ctx->d_pq.ensure(tot));
+    CK(ctx->d_pt.ensure(2 * tot));
+    launch_query_pairs(1, endpoints, nq_total, order, q0, qn, ts, ctx->d_toff.p, ctx->d_tp.p, ctx->M, v1t, v2t,
+                       ctx->d_moff.p, ctx->d_qmask.p, nullptr, ctx->d_offsets.p, ctx->d_pq.p, ctx->d_pt.p, ctx->nsm,
+                       st);
+    ctx->launches += 5;
+    nf = tot;
+    if (tot > 4 * budget) {  // bound the chunk's coarse list (memory, refinement) like the frontiers
+      *over = tot;
+      return SPOLY_OK;
+    }
   }
   const uint64_t npairs = nf;
   *ncoarse = npairs;
@@ -495,16 +560,20 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
       const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * npairs, 1ull << 20), 1ull << 27);
       CK(ctx->d_front.ensure(2 * fcap));
       CK(ctx->d_fcount.ensure(16));
-      RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
-      launch_refine_pairs(ctx->d_pq.p, ctx->d_pt.p, npairs, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
-                          ctx->d_keep.p, nullptr, RW, ctx->nsm, st);
-      ctx->launches += RW.launches;
-      {
+      // blocks of coarse pairs small enough that a level's frontier (<= 16 children per entry) stays under the cap
+      // (an overflowing entry keeps its pair: sound but loose)
+      const uint64_t blk = std::max<uint64_t>(fcap / 16, 1);
+      for (uint64_t b0 = 0; b0 < npairs; b0 += blk) {
+        const uint64_t nb = std::min(blk, npairs - b0);
+        RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
+        launch_refine_pairs(ctx->d_pq.p + b0, ctx->d_pt.p + 2 * b0, nb, ctx->M, endpoints, ctx->cfg.cull_levels, v1t,
+                            v2t, ctx->d_keep.p + b0, nullptr, RW, ctx->nsm, st);
+        ctx->launches += RW.launches;
         unsigned long long fc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         const int lv = std::min(ctx->cfg.cull_levels, 5);
         CK(cudaMemcpyAsync(fc, ctx->d_fcount.p, sizeof(unsigned long long) * (size_t)lv, cudaMemcpyDeviceToHost, st));
         CK(cudaStreamSynchronize(st));
-        uint64_t entries = npairs;  // level 0 runs on every coarse pair
+        uint64_t entries = nb;  // level 0 runs on every coarse pair
         for (int l = 0; l < lv; ++l) {
           ctx->cull_tests += 16ull * entries;
           entries = std::min<uint64_t>(fc[l], fcap);
@@ -535,13 +604,35 @@ static spoly_status cull_k2_chunk(spoly_ctx* ctx, const char* chain, const doubl
       // reading R25: the v-range of T_1's surviving cells of every kept pair (the same refinement on the kept pairs
       // only, walking every surviving branch instead of stopping at the first)
       const uint64_t fcap = std::min<uint64_t>(std::max<uint64_t>(16 * ns, 1ull << 20), 1ull << 27);
-      RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
-      launch_refine_pairs(ctx->d_pq2.p, ctx->d_pt2.p, ns, ctx->M, endpoints, ctx->cfg.cull_levels, v1t, v2t,
-                          ctx->d_keep.p, ctx->d_vr2.p, RW, ctx->nsm, st);
-      ctx->launches += RW.launches + 1;
+      const uint64_t blk = std::max<uint64_t>(fcap / 16, 1);
+      for (uint64_t b0 = 0; b0 < ns; b0 += blk) {
+        const uint64_t nb = std::min<uint64_t>(blk, ns - b0);
+        RefineScratch RW{{ctx->d_front.p, ctx->d_front.p + fcap}, fcap, ctx->d_fcount.p, 0};
+        launch_refine_pairs(ctx->d_pq2.p + b0, ctx->d_pt2.p + 2 * b0, nb, ctx->M, endpoints, ctx->cfg.cull_levels, v1t,
+                            v2t, ctx->d_keep.p + b0, ctx->d_vr2.p + 2 * b0, RW, ctx->nsm, st);
+        ctx->launches += RW.launches + 1;
+      }
       *kv = ctx->d_vr2.p;
     }
   }
+  return SPOLY_OK;
+}
+
+// queries sorted along a 30-bit Morton code of their endpoints (k=1 and k=2 query tiles): *order[i] = query id
+static spoly_status sort_queries(spoly_ctx* ctx, const double* endpoints, uint32_t nq, const uint32_t** order) {
+  cudaStream_t st = ctx->st;
+  CK(ctx->d_qbounds.ensure(12));
+  CK(ctx->d_qkeys.ensure(2ull * nq));
+  CK(ctx->d_qorder.ensure(2ull * nq));
+  launch_query_order(endpoints, nq, ctx->d_qbounds.p, ctx->d_qkeys.p, ctx->d_qorder.p, st);
+  ctx->launches += 2;
+  size_t tb = 0;
+  CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
+                                     ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
+  CK(ctx->d_temp.ensure(tb));
+  CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
+                                     ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
+  *order = ctx->d_qorder.p + nq;
   return SPOLY_OK;
 }
 
@@ -595,20 +686,36 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
     const int top = cull_split_level(ctx->M, &P);
     if (top < 1) return fail(ctx, SPOLY_ERR_UNSUPPORTED_CHAIN, "two-bounce cull supports at most 2^22 triangles");
     const uint64_t budget = std::max<uint64_t>(ctx->cfg.max_pairs, 2ull * P);
-    uint32_t chunk = std::max<uint32_t>(1, std::min<uint32_t>(ctx->k2_chunk ? ctx->k2_chunk : nq, nq));
-    chunk = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(chunk, budget / P));
+    // query tiles (reading R14 on tiles): Morton order of the queries, chunks of whole tiles
+    const uint32_t* order = nullptr;
+    if (ctx->cfg.k2_tiles) {
+      spoly_status os = sort_queries(ctx, endpoints, nq, &order);
+      if (os != SPOLY_OK) return os;
+    }
+    uint32_t ts = order ? 32 : 1;  // queries per tile (halved when one tile alone exceeds the budget)
+    uint32_t unit = ts;            // chunks in whole tiles
+    uint32_t chunk = std::max<uint32_t>(unit, std::min<uint32_t>(ctx->k2_chunk ? ctx->k2_chunk : nq, nq));
+    chunk = (uint32_t)std::max<uint64_t>(unit, std::min<uint64_t>(chunk, unit * std::max<uint64_t>(1, budget / P)));
+    chunk = (chunk + unit - 1) / unit * unit;
     uint64_t acc = 0, coarse = 0;
     bool have_vr = ctx->cfg.cull_levels > 0;
     for (uint32_t q0 = 0; q0 < nq;) {
       const uint32_t qn = std::min(chunk, nq - q0);
       uint64_t ncoarse = 0, nkept = 0, over = 0;
       const uint32_t *kq = nullptr, *kt = nullptr, *kv = nullptr;
-      spoly_status s =
-          cull_k2_chunk(ctx, chain, endpoints, q0, qn, top, P, budget, &ncoarse, &nkept, &kq, &kt, &kv, &over);
+      spoly_status s = cull_k2_chunk(ctx, chain, endpoints, q0, qn, top, P, budget, &ncoarse, &nkept, &kq, &kt, &kv,
+                                     &over, order, nq, ts);
       if (s != SPOLY_OK) return s;
-      if (over) {  // a frontier of this chunk exceeded the budget: shrink the chunk and redo it
-        if (qn == 1) return fail(ctx, SPOLY_ERR_CAPACITY, "two-bounce cull frontier of one query exceeds max_pairs");
+      if (over) {  // a frontier of this chunk exceeded the budget: shrink the chunk (then the tiles) and redo it
+        if (qn <= unit) {
+          if (ts == 1) return fail(ctx, SPOLY_ERR_CAPACITY, "two-bounce cull frontier of one query exceeds max_pairs");
+          ts /= 2;  // smaller tiles (their spheres are tighter, their union of pairs smaller); kept for the rest
+          unit = ts;
+          chunk = ts;
+          continue;
+        }
         chunk = (uint32_t)std::max<double>(1.0, std::min<double>(qn / 2, 0.9 * qn * (double)budget / (double)over));
+        chunk = std::max<uint32_t>(unit, chunk / unit * unit);
         continue;
       }
       CK(grow_keep(ctx->d_pqa, acc, acc + nkept, st));
@@ -637,20 +744,11 @@ spoly_status spoly_solve(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, in
   } else if (ctx->cfg.cull) {
     // query order (Morton of the endpoints), tile cull, per-query cull on the tile survivors
     const uint32_t ntiles = (nq + 31) / 32;
-    CK(ctx->d_qbounds.ensure(12));
-    CK(ctx->d_qkeys.ensure(2ull * nq));
-    CK(ctx->d_qorder.ensure(2ull * nq));
-    launch_query_order(endpoints, nq, ctx->d_qbounds.p, ctx->d_qkeys.p, ctx->d_qorder.p, st);
-    ctx->launches += 2;
+    const uint32_t* order = nullptr;
     {
-      size_t tb = 0;
-      CK(cub::DeviceRadixSort::SortPairs(nullptr, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
-                                         ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
-      CK(ctx->d_temp.ensure(tb));
-      CK(cub::DeviceRadixSort::SortPairs(ctx->d_temp.p, tb, ctx->d_qkeys.p, ctx->d_qkeys.p + nq, ctx->d_qorder.p,
-                                         ctx->d_qorder.p + nq, (int)nq, 0, 30, st));
+      spoly_status os = sort_queries(ctx, endpoints, nq, &order);
+      if (os != SPOLY_OK) return os;
     }
-    const uint32_t* order = ctx->d_qorder.p + nq;
     CK(ctx->d_tcount.ensure(ntiles + 1));
     for (int attempt = 0; attempt < 2; ++attempt) {
       const uint32_t cap = std::max<uint32_t>(64, std::min<uint32_t>(ctx->tile_cap, ctx->M.ntris));

@@ -557,10 +557,11 @@ __device__ __forceinline__ bool pair_dir(float4 sa, float4 sb, f3& a, float& cho
 }
 
 __device__ __forceinline__ bool pair_keep(f3 x0, f3 x3, float4 sA, float4 nA, float4 sB, float4 nB, int v1t, int v2t,
-                                          float ef, float eb, int side = -1 /* x_0 front (0) / back (1) of T_1 */) {
+                                          float ef, float eb, int side = -1 /* x_0 front (0) / back (1) of T_1 */,
+                                          float r0 = 0.f, float r3 = 0.f /* endpoint sphere radii (query tiles) */) {
   f3 a0, a3, aAB;
   float c0, c3, cAB;
-  if (!sphere_dir(x0, sA, a0, c0) || !sphere_dir(x3, sB, a3, c3) || !pair_dir(sA, sB, aAB, cAB)) return true;
+  if (!sphere_dir2(x0, r0, sA, a0, c0) || !sphere_dir2(x3, r3, sB, a3, c3) || !pair_dir(sA, sB, aAB, cAB)) return true;
   const f3 aBA = {-aAB.x, -aAB.y, -aAB.z};
   float e[2][3];
   int ncombo = 0;
@@ -640,7 +641,9 @@ struct ChildRec {
 };
 
 __device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels& L, const TriRec* __restrict__ tris,
-                                           uint32_t i, f3 xend, int refract, int want_side) {
+                                           uint32_t i, f3 xend, float rend, int refract, int want_side) {
+  // rend > 0: the endpoint is a sphere (a tile of queries); the side decisions fall back to "both" / "keep all"
+  // when the sphere reaches the plane
   R.flags = 0;
   if (i >= L.n[cl]) return;
   R.flags = 1;
@@ -653,7 +656,8 @@ __device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels
       const float sd = dotf(ld3(T.plane), xend) - T.plane.w;
       const float gl = sqrtf(dotf(ld3(T.plane), ld3(T.plane)));
       int side = -1;
-      if (fabsf(sd) > 1e-4f * gl * (fabsf(xend.x) + fabsf(xend.y) + fabsf(xend.z) + 1.f)) side = sd > 0.f ? 0 : 1;
+      if (fabsf(sd) > 1e-4f * gl * (fabsf(xend.x) + fabsf(xend.y) + fabsf(xend.z) + 1.f) + rend * gl)
+        side = sd > 0.f ? 0 : 1;
       R.flags |= (side + 1) << 3;
     }
     // side_keep's per-triangle part (plane, reference side, tolerance)
@@ -664,7 +668,7 @@ __device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels
     const f3 g = crossf(e1, e2);
     const float gl = sqrtf(dotf(g, g)), sc = sqrtf(fmaxf(dotf(e1, e1), dotf(e2, e2)));
     const float sref = dotf(xend - p0, g);
-    if (sref == 0.f) R.flags |= 4;
+    if (sref == 0.f || fabsf(sref) <= rend * gl * 1.0001f) R.flags |= 4;
     const float sg = (sref > 0.f) == (refract == 0) ? 1.f : -1.f;
     R.g = make_float4(g.x, g.y, g.z, 0.5e-6f * gl * sc);
     R.p0 = make_float4(p0.x, p0.y, p0.z, sg);
@@ -677,7 +681,7 @@ __device__ __forceinline__ void make_child(ChildRec& R, int cl, const CullLevels
   }
   f3 d;
   float ch;
-  if (sphere_dir(xend, R.sph, d, ch)) R.flags |= 2;
+  if (sphere_dir2(xend, rend, R.sph, d, ch)) R.flags |= 2;
   R.dir = make_float4(d.x, d.y, d.z, ch);
 }
 
@@ -740,7 +744,9 @@ __global__ void __launch_bounds__(kExpandThreads, 3) k_pair_expand(int pass, int
                                                      unsigned long long* __restrict__ masks,
                                                      const unsigned long long* __restrict__ offsets,
                                                      uint32_t* __restrict__ oq, uint32_t* __restrict__ oa,
-                                                     uint32_t* __restrict__ ob) {
+                                                     uint32_t* __restrict__ ob, const float4* __restrict__ tsph) {
+  // tsph != NULL: frontier entries are (query TILE, node, node) and the endpoints are the tile's spheres
+  // tsph[2 t] = (c0, r0), tsph[2 t + 1] = (c3, r3)
   // Two frontier entries per warp: half-warp h (lanes 16h..16h+15) stages its entry's 8 + 8 child records
   // and tests the entry's 64 child pairs, 4 per lane.  Structure-of-arrays staging, record i of half h at
   // slot 2i + h of smf[warp][field][.], so the records a warp-wide load touches sit in distinct banks.
@@ -789,16 +795,25 @@ __global__ void __launch_bounds__(kExpandThreads, 3) k_pair_expand(int pass, int
       continue;
     }
     f3 x0 = {0.f, 0.f, 0.f}, x3 = {0.f, 0.f, 0.f};
+    float r0 = 0.f, r3 = 0.f;
     bool root_ok = valid;
     if (valid) {
-      const double* e = ep + 6ull * q;
-      x0 = {(float)e[0], (float)e[1], (float)e[2]};
-      x3 = {(float)e[3], (float)e[4], (float)e[5]};
+      if (tsph) {
+        const float4 s0 = tsph[2 * q], s3 = tsph[2 * q + 1];
+        x0 = {s0.x, s0.y, s0.z};
+        r0 = s0.w;
+        x3 = {s3.x, s3.y, s3.z};
+        r3 = s3.w;
+      } else {
+        const double* e = ep + 6ull * q;
+        x0 = {(float)e[0], (float)e[1], (float)e[2]};
+        x3 = {(float)e[3], (float)e[4], (float)e[5]};
+      }
       if (!fq) {
         float4 sa, ca, sb, cb;
         node_bounds(L, cl + 1, A, sa, ca);
         node_bounds(L, cl + 1, B, sb, cb);
-        root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb);
+        root_ok = pair_keep(x0, x3, sa, ca, sb, cb, v1t, v2t, ef, eb, -1, r0, r3);
       }
     }
     __syncwarp();
@@ -807,7 +822,7 @@ __global__ void __launch_bounds__(kExpandThreads, 3) k_pair_expand(int pass, int
       ChildRec R;
       R.flags = 0;
       if (root_ok)
-        make_child(R, cl, L, tris, (isB ? B : A) * 8 + (hl & 7), isB ? x3 : x0, isB ? v2t : v1t,
+        make_child(R, cl, L, tris, (isB ? B : A) * 8 + (hl & 7), isB ? x3 : x0, isB ? r3 : r0, isB ? v2t : v1t,
                    !isB && (v1t || v2t));
       const int sl = 2 * hl + h;
       smf[wib][0][sl] = R.sph;
@@ -876,14 +891,146 @@ int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query) {
 void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
                         const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
                         unsigned long long* masks, const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
-                        cudaStream_t st) {
+                        cudaStream_t st, const float4* tsph) {
   if (!nf) return;
   const CullLevels L = cull_levels_of(M);
   const int threads = 256;
   const uint64_t want = (nf * 32 + threads - 1) / threads, cap = (uint64_t)nsm * 64;
   k_pair_expand<<<(int)(want < cap ? want : cap), threads, 0, st>>>(pass, cl, ep, qbase, fq, fa, fb, nf, M.tris, L, v1t, v2t,
                                                                     M.eta_front, M.eta_back, counts, masks, offsets, oq,
-                                                                    oa, ob);
+                                                                    oa, ob, tsph);
+}
+
+// ------------------------------------------------------------------ two-bounce query tiles
+// Tiles of 32 consecutive Morton-sorted queries share one node-pair expansion against their endpoint spheres
+// (the same predicate with the direction sets from a node to a sphere of endpoints, and "both / keep" side
+// decisions when a sphere reaches a plane: a superset of every member query's pairs); each query then tests its
+// tile's triangle pairs exactly (the triangle-level test of the per-query expansion).
+__global__ void k_tile_spheres(const double* __restrict__ ep, uint32_t nq, const uint32_t* __restrict__ order,
+                               uint32_t s0, uint32_t ntiles, uint32_t ts, float4* __restrict__ tsph) {
+  // tiles of ts (<= 32) consecutive sorted queries; lanes past the tile or past nq repeat its first member
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t t = gw; t < ntiles; t += nw) {
+    const uint32_t i = s0 + t * ts + (uint32_t)lane;
+    const uint32_t q = order[((uint32_t)lane < ts && i < nq) ? i : s0 + t * ts];
+    const double* e = ep + 6ull * q;
+    const f3 a0 = {(float)e[0], (float)e[1], (float)e[2]}, a3 = {(float)e[3], (float)e[4], (float)e[5]};
+    f3 s0v = a0, s3v = a3;
+    for (int off = 16; off; off >>= 1) {
+      s0v.x += __shfl_xor_sync(0xffffffffu, s0v.x, off);
+      s0v.y += __shfl_xor_sync(0xffffffffu, s0v.y, off);
+      s0v.z += __shfl_xor_sync(0xffffffffu, s0v.z, off);
+      s3v.x += __shfl_xor_sync(0xffffffffu, s3v.x, off);
+      s3v.y += __shfl_xor_sync(0xffffffffu, s3v.y, off);
+      s3v.z += __shfl_xor_sync(0xffffffffu, s3v.z, off);
+    }
+    const f3 c0 = (1.f / 32.f) * s0v, c3 = (1.f / 32.f) * s3v;
+    float r0 = sqrtf(dotf(a0 - c0, a0 - c0)), r3 = sqrtf(dotf(a3 - c3, a3 - c3));
+    for (int off = 16; off; off >>= 1) {
+      r0 = fmaxf(r0, __shfl_xor_sync(0xffffffffu, r0, off));
+      r3 = fmaxf(r3, __shfl_xor_sync(0xffffffffu, r3, off));
+    }
+    // inflated for the float rounding of the members and the centre
+    r0 = r0 * 1.0001f + 1e-6f * (fabsf(c0.x) + fabsf(c0.y) + fabsf(c0.z) + 1.f);
+    r3 = r3 * 1.0001f + 1e-6f * (fabsf(c3.x) + fabsf(c3.y) + fabsf(c3.z) + 1.f);
+    if (lane == 0) {
+      tsph[2 * t] = make_float4(c0.x, c0.y, c0.z, r0);
+      tsph[2 * t + 1] = make_float4(c3.x, c3.y, c3.z, r3);
+    }
+  }
+}
+
+// per query (warp) over its tile's triangle pairs [toff[t], toff[t + 1]): the exact triangle-level test of the
+// per-query expansion (pair bound with the query's endpoints, eta side of x_0, both side filters).  Pass 0: keep
+// masks (one word per 32 tile pairs) + per-query counts; pass 1: the query-major list at the scanned offsets.
+__global__ void __launch_bounds__(256) k_query_pairs(int pass, const double* __restrict__ ep, uint32_t nq,
+                                                     const uint32_t* __restrict__ order, uint32_t s0, uint32_t sn,
+                                                     uint32_t ts, const unsigned long long* __restrict__ toff,
+                                                     const uint32_t* __restrict__ tpair, const TriRec* __restrict__ tris,
+                                                     const TriCull* __restrict__ tc, int v1t, int v2t, float ef,
+                                                     float eb, const unsigned long long* __restrict__ moff,
+                                                     uint32_t* __restrict__ masks, uint32_t* __restrict__ counts,
+                                                     const unsigned long long* __restrict__ offsets,
+                                                     uint32_t* __restrict__ oq, uint32_t* __restrict__ ot) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t k = gw; k < sn; k += nw) {
+    const uint32_t i = s0 + k;
+    if (i >= nq) continue;
+    const uint32_t q = order[i], t = k / ts;
+    const unsigned long long b0 = toff[t], b1 = toff[t + 1];
+    uint32_t* mrow = masks + moff[t] + (unsigned long long)(k % ts) * ((b1 - b0 + 31) / 32);
+    if (pass) {
+      unsigned long long pos = offsets[k];
+      for (unsigned long long b = b0; b < b1; b += 32) {
+        const uint32_t m = mrow[(b - b0) / 32];
+        const unsigned long long j = b + lane;
+        if ((m >> lane) & 1u) {
+          const unsigned long long p = pos + __popc(m & ((1u << lane) - 1u));
+          oq[p] = q;
+          ot[2 * p] = tpair[2 * j];
+          ot[2 * p + 1] = tpair[2 * j + 1];
+        }
+        pos += __popc(m);
+      }
+      continue;
+    }
+    const double* e = ep + 6ull * q;
+    const f3 x0 = {(float)e[0], (float)e[1], (float)e[2]}, x3 = {(float)e[3], (float)e[4], (float)e[5]};
+    uint32_t count = 0;
+    for (unsigned long long b = b0; b < b1; b += 32) {
+      const unsigned long long j = b + lane;
+      bool kp = false;
+      if (j < b1) {
+        const uint32_t A = tpair[2 * j], B = tpair[2 * j + 1];
+        const TriCull TA = tc[A], TB = tc[B];
+        int side = -1;
+        if (v1t || v2t) {
+          const float sd = dotf(ld3(TA.plane), x0) - TA.plane.w;
+          const float gl = sqrtf(dotf(ld3(TA.plane), ld3(TA.plane)));
+          if (fabsf(sd) > 1e-4f * gl * (fabsf(x0.x) + fabsf(x0.y) + fabsf(x0.z) + 1.f)) side = sd > 0.f ? 0 : 1;
+        }
+        kp = pair_keep(x0, x3, TA.sphere, TA.cone, TB.sphere, TB.cone, v1t, v2t, ef, eb, side) &&
+             side_keep(tris, A, x0, v1t, B) && side_keep(tris, B, x3, v2t, A);
+      }
+      const uint32_t m = __ballot_sync(0xffffffffu, kp);
+      if (lane == 0) mrow[(b - b0) / 32] = m;
+      count += __popc(m);
+    }
+    if (lane == 0) counts[k] = count;
+  }
+}
+
+void launch_tile_spheres(const double* ep, uint32_t nq, const uint32_t* order, uint32_t s0, uint32_t ntiles,
+                         uint32_t ts, float4* tsph, int nsm, cudaStream_t st) {
+  if (!ntiles) return;
+  const uint64_t want = ((uint64_t)ntiles * 32 + 255) / 256, cap = (uint64_t)nsm * 16;
+  k_tile_spheres<<<(int)(want < cap ? want : cap), 256, 0, st>>>(ep, nq, order, s0, ntiles, ts, tsph);
+}
+
+void launch_query_pairs(int pass, const double* ep, uint32_t nq, const uint32_t* order, uint32_t s0, uint32_t sn,
+                        uint32_t ts, const unsigned long long* toff, const uint32_t* tpair, const DeviceMesh& M,
+                        int v1t, int v2t, const unsigned long long* moff, uint32_t* masks, uint32_t* counts,
+                        const unsigned long long* offsets, uint32_t* oq, uint32_t* ot, int nsm, cudaStream_t st) {
+  if (!sn) return;
+  const uint64_t want = ((uint64_t)sn * 32 + 255) / 256, cap = (uint64_t)nsm * 32;
+  k_query_pairs<<<(int)(want < cap ? want : cap), 256, 0, st>>>(pass, ep, nq, order, s0, sn, ts, toff, tpair, M.tris,
+                                                                 M.tcull, v1t, v2t, M.eta_front, M.eta_back, moff,
+                                                                 masks, counts, offsets, oq, ot);
+}
+
+// per-tile counts of a tile-major (tile, pair) list -> exclusive offsets computed by the caller's scan
+__global__ void k_tile_hist(const uint32_t* __restrict__ tq, uint64_t n, unsigned long long* __restrict__ cnt) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(cnt + tq[i], 1ull);
+}
+void launch_tile_hist(const uint32_t* tq, uint64_t n, unsigned long long* cnt, int nsm, cudaStream_t st) {
+  if (!n) return;
+  const uint64_t want = (n + 255) / 256, cap = (uint64_t)nsm * 16;
+  k_tile_hist<<<(int)(want < cap ? want : cap), 256, 0, st>>>(tq, n, cnt);
 }
 
 // ------------------------------------------------------------------ barycentric subdivision refinement (k=2)

@@ -57,7 +57,16 @@ int cull_split_level(const DeviceMesh& M, uint32_t* pairs_per_query);
 void launch_pair_expand(int pass, int cl, const double* ep, uint32_t qbase, const uint32_t* fq, const uint32_t* fa,
                         const uint32_t* fb, uint64_t nf, const DeviceMesh& M, int v1t, int v2t, uint32_t* counts,
                         unsigned long long* masks, const unsigned long long* offsets, uint32_t* oq, uint32_t* oa, uint32_t* ob, int nsm,
-                        cudaStream_t st);
+                        cudaStream_t st, const float4* tsph = nullptr);
+// two-bounce query tiles (32 Morton-sorted queries): endpoint spheres of tiles [0, ntiles) starting at sorted
+// position s0; per-query exact test of the tile's triangle pairs (pass 0 masks + counts, pass 1 list)
+void launch_tile_spheres(const double* ep, uint32_t nq, const uint32_t* order, uint32_t s0, uint32_t ntiles,
+                         uint32_t ts, float4* tsph, int nsm, cudaStream_t st);
+void launch_query_pairs(int pass, const double* ep, uint32_t nq, const uint32_t* order, uint32_t s0, uint32_t sn,
+                        uint32_t ts, const unsigned long long* toff, const uint32_t* tpair, const DeviceMesh& M,
+                        int v1t, int v2t, const unsigned long long* moff, uint32_t* masks, uint32_t* counts,
+                        const unsigned long long* offsets, uint32_t* oq, uint32_t* ot, int nsm, cudaStream_t st);
+void launch_tile_hist(const uint32_t* tq, uint64_t n, unsigned long long* cnt, int nsm, cudaStream_t st);
 struct RefineScratch {
   uint64_t* front[2];  // frontier ping-pong, cap entries each
   uint64_t cap;

@@ -36,7 +36,8 @@ class spoly_config(ctypes.Structure):
                 ("eps_domain", ctypes.c_double), ("eps_flag", ctypes.c_double), ("tau_trunc", ctypes.c_double),
                 ("cull", ctypes.c_int), ("deterministic", ctypes.c_int), ("cull_margin", ctypes.c_float),
                 ("max_solutions", ctypes.c_uint64), ("max_pairs", ctypes.c_uint64),
-                ("cull_levels", ctypes.c_int), ("visibility", ctypes.c_int), ("scan_restrict", ctypes.c_int)]
+                ("cull_levels", ctypes.c_int), ("visibility", ctypes.c_int), ("scan_restrict", ctypes.c_int),
+                ("k2_tiles", ctypes.c_int)]
 
 
 class spoly_tuple_list(ctypes.Structure):

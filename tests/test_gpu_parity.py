@@ -362,6 +362,18 @@ def test_face_mode_planted_on_gpu(orc, sp, torch_cuda, chain):
             assert abs((1 / g["contribution"][i]) / (L * L) - 1) < 1e-6
 
 
+def test_two_bounce_tiles_vs_per_query_cull(sp, torch_cuda):
+    """The tiled k=2 cull (32-query endpoint spheres + an exact per-query triangle-pair test) keeps every chain the
+    per-query expansion finds: identical solution sets on a C4 subset (both culls are sound)."""
+    w = W.sphere_c4(res=32, level=4)
+    a = _gpu_solve(sp, torch_cuda, w.mesh, "TT", w.endpoints, cfg=sp.default_config(k2_tiles=0))
+    b = _gpu_solve(sp, torch_cuda, w.mesh, "TT", w.endpoints, cfg=sp.default_config(k2_tiles=1))
+    key = lambda g: sorted(zip(g["query"].tolist(), map(tuple, g["tuple"].tolist()), map(tuple, np.round(g["bary"], 12).tolist())))
+    assert a["report"]["n_admissible"] > 100
+    assert key(a) == key(b)
+    assert np.array_equal(a["per_query"], b["per_query"])
+
+
 @pytest.mark.parametrize("chain", ["RR", "TT"])
 def test_two_bounce_cull_sound_on_planted(orc, sp, torch_cuda, chain):
     """GPU pair cull (no tuple list) keeps every planted pair and the solve recovers the planted chains."""
@@ -471,11 +483,12 @@ def test_counting_order_equals_key_sort(sp, torch_cuda, monkeypatch, chain, make
         assert np.array_equal(a[k], b[k]), k
 
 
-@pytest.mark.parametrize("chain,make", [("RR", lambda: W.mirrors_rr(res=8, quads=16)),
-                                        ("TT", lambda: W.shell_c5(res=8))])
+@pytest.mark.parametrize("chain,make", [("RR", lambda: W.mirrors_rr(res=16, quads=16)),
+                                        ("TT", lambda: W.shell_c5(res=16))])
 def test_two_bounce_query_chunking_identical(sp, torch_cuda, chain, make):
-    """cfg.max_pairs small enough that the k=2 cull runs in many query chunks: the work list, solutions and
-    per-query sums are bit-identical to the single-chunk run (chunks append in query order)."""
+    """cfg.max_pairs small enough that the k=2 cull runs in many query chunks (whole tiles of 32 Morton-sorted
+    queries): the work list, solutions and per-query sums are bit-identical to the single-chunk run (chunks append
+    in sorted-query order)."""
     w = make()
     a = _gpu_solve(sp, torch_cuda, w.mesh, chain, w.endpoints)
     # a budget of a third of the whole frame's triangle-pair frontier: several chunks, each within budget
