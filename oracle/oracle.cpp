@@ -2,15 +2,24 @@
 // --impl reference).  Plain, slow, FP64 transcription of Specular Polynomials, step by
 // step in the paper's order and notation.  Shares no code with the CUDA path.
 //
-// Parity status per function (DESIGN.md §3 lists every reading):
-//   build_system (Eqs. 6, 9, 12, 13-20, 21-23) ............ pinned (tests/test_oracle_pins.py: degrees,
-//                                                            vanishing at forward-traced planted chains)
-//   bezout (Eq. 24) / det_laplace (Sec. 5.2) .............. pinned (Sylvester resultant, sympy-free)
-//   isolate (Sec. 5.2 derivative recursion) ............... pinned (planted roots, numpy.roots)
-//   scan (Sec. 5.2 piecewise bisection) ................... pinned (planted RR/TT, brute force)
-//   validate / contribution / cull ......................... pinned (closed forms, brute force)
-//   sqrt surrogate table (Eq. 20) .......................... pinned (certified error < 1e-3);
-//       the paper's own coefficients are unavailable -> "parity unpinned" vs the paper's table.
+// Parity status per function (DESIGN.md §3 lists every reading; every pin is in tests/test_oracle_pins*.py):
+//   build_system (Eqs. 6, 9, 12, 13-20, 21-23) ............ pinned: degrees vs Table 2/3 (incl. face mode), a and b
+//                                                            vanish at forward-traced planted chains
+//   face mode (R22) ........................................ pinned: two flat mirrors vs the image-source construction
+//   bezout (Eq. 24) / det_laplace (Sec. 5.2) .............. pinned: Sylvester resultant, numpy det
+//   isolate (Sec. 5.2 derivative recursion) ............... pinned: planted roots, numpy.roots
+//   scan (Sec. 5.2 piecewise bisection) ................... pinned: planted RR/RT/TR/TT, camera- and light-side brute
+//                                                            force (recall >= 0.95, every chain confirmed)
+//   validate / polish ...................................... pinned: Eq. 3 residual recomputed, flat interface Fermat
+//   contribution (c15) ..................................... pinned: flat mirror J = L^2 (k = 1, 2), index-matched
+//                                                            J = d^2 / L^2, inverse-map Jacobian of the exact-path
+//                                                            solver (all chains), scale covariance
+//   flags (c14, R11) ....................................... pinned: NEAR_TANGENT at folds (both sides), BOUNDARY on an
+//                                                            edge, DEGENERATE at normal incidence, generic chains clean
+//   cull ................................................... pinned: soundness on planted chains, monotone refinement
+//   visibility (R26) ....................................... pinned: closed-form blocker, independent numpy segment test
+//   sqrt surrogate table (Eq. 20) .......................... pinned (certified error < 1e-3); the paper's own
+//       coefficients are unavailable -> "parity unpinned" vs the paper's table.
 #include "oracle.h"
 
 #include <algorithm>

@@ -80,11 +80,13 @@ __device__ __forceinline__ bool build_system(d3 x0, d3 x2, const d3 P_in[3], con
   const double sa = 1.0 / ma, sb = 1.0 / mb;
   bscale<2, 3>(S.A, sa);
   if (WITH_B) bscale<DB, DB + 1>(S.B, sb);
+  // numerical u-degree truncation (R6): rarely active for one bounce, so the zeroing is branched around (not
+  // predicated over every coefficient)
   S.da = bnum_udeg_rows<2>(rma, sa, prm.tau_trunc);
-  btrunc_u<2, 3>(S.A, S.da);
+  if (S.da < 2) btrunc_u<2, 3>(S.A, S.da);
   if (!WITH_B) return true;
   S.db = bnum_udeg_rows<DB>(rmb, sb, prm.tau_trunc);
-  btrunc_u<DB, DB + 1>(S.B, S.db);
+  if (S.db < (TC ? DB : DB - 1)) btrunc_u<DB, DB + 1>(S.B, S.db);  // R: row 4 is structurally zero already
   S.n = max(S.da, S.db);
   if (S.n == 0) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
@@ -297,13 +299,11 @@ __global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_
         if (!(mr > 0)) {
           flags |= SPOLY_FLAG_DEGENERATE;
         } else {
-          int deg = 0;
           const double inv = 1.0 / mr;
 #pragma unroll
-          for (int t = 0; t < NR; ++t) {
-            r[t] *= inv;
-            if (r[t] != 0.0) deg = t;
-          }
+          for (int t = 0; t < NR; ++t) r[t] *= inv;
+          int deg = NR - 1;  // exact structural zeros at the top are rare (face mode, special geometry)
+          while (deg > 0 && r[deg] == 0.0) --deg;
           const int kfree = bernstein_root_free_level<NR>(r);
           // kfree == 1: r is monotone on [0,1], so it has a root there iff r(0) and r(1) differ in sign
           // (or one vanishes) -- exact, and it keeps root-free monotone pairs out of the job list
@@ -379,8 +379,7 @@ __global__ void __launch_bounds__(128, TC ? SPOLY_P1_MINB_T : SPOLY_P1_MINB) k1_
         A[5] = A[7] = A[8] = 0.0;
         double al[3];
         bslices_at<2, 3>(A, root, al);
-        const double amax = dmax(fabs(al[0]), dmax(fabs(al[1]), fabs(al[2])));
-        if (!(amax >= 1e-12)) {
+        if (!(fabs(al[0]) >= 1e-12 || fabs(al[1]) >= 1e-12 || fabs(al[2]) >= 1e-12)) {  // max|a(., v*)| < 1e-12
           complex_job = true;  // a(., v*) == 0: the b fallback runs in the general path kernel
         } else {
           uint32_t nc = 0, nrej = 0;
