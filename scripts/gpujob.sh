@@ -6,6 +6,7 @@ d=json.loads(open('gpurun_out/k2ab.json').read().strip().splitlines()[-1])
 print('$1 $2 ${SPOLY_LIB}', 'ms %.1f'%d['ms_per_step'], {k:round(v,1) for k,v in d['phase_ms'].items()}, d['counters']['n_admissible'], d['pairs_per_step_per_gpu'], d['roofline']['frac'])
 "
 }
-unset SPOLY_LIB
-run C4 ""; run "C5 --res 128" ""
-python variants/hash.py C4; python variants/hash.py C5
+for v in default refl0 refsph; do
+  if [ $v = default ]; then unset SPOLY_LIB; else export SPOLY_LIB=$PWD/variants/$v.so; fi
+  run C4 ""; run "C5 --res 128" ""
+done
