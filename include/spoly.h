@@ -199,6 +199,30 @@ spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chai
                               const double* light_intensity_host, double* per_query_host,
                               spoly_result* out);
 
+/* Glossy (near-specular) vertices, PAPER.md:857-859 ("After sampling the normal offset for glossy vertices, the
+ * admissible chains corresponding to the offset remain finite, and the problem reduces to pure specular
+ * situations"), reading R28.  slopes: HOST, ntris x 2 float64 (p, q) in ORIGINAL triangle order,
+ * microfacet slopes sampled by the caller (e.g. Beckmann: p, q ~ N(0, alpha^2 / 2)).  Every triangle's three
+ * shading normals become n_j' = fl32(n_j + p T + q B), (T, B) the orthonormal frame of the triangle plane
+ * (T = e1 / |e1|, B = g^ x T, g = e1 x e2), computed in FP64 on the device from the UPLOADED normals (offsets do
+ * not accumulate); the cull bounds are rebuilt.  Later solves see the perturbed surface.  slopes = NULL restores
+ * the uploaded normals.  Errors: INVALID_ARG (no mesh, ntris != mesh triangle count, non-finite slope). */
+spoly_status spoly_set_normal_offsets(spoly_ctx* ctx, const double* slopes, uint32_t ntris);
+
+/* Deterministic splat renderer (the application layer of PAPER.md:680 "apply it on both glints rendering and
+ * caustics rendering"; SPEC S:661-669 cmd_render without Monte Carlo): the width x height queries (row-major
+ * pixels; endpoints DEVICE nqueries x 2 x 3 float64 as spoly_solve: x_0 = the pixel's diffuse receiver point,
+ * x_{k+1} = the light) are solved once per sample s < nsamples with the sample's normal offsets (slopes: HOST,
+ * nsamples x ntris x 2 float64 as spoly_set_normal_offsets, or NULL = pure specular, one solve), and
+ *     radiance[q] = sum_s (albedo / pi / nsamples) * per_query_s[q]      (accumulated in sample order)
+ * radiance: DEVICE, nqueries float64 (linear).  srgb: DEVICE, nqueries x 3 uint8 or NULL:
+ *     c = rint(255 * min(1, max(0, exposure * radiance))^(1 / 2.2)) in every channel (gray).
+ * light_intensity as spoly_solve.  The uploaded normals are restored on return.  Errors: as spoly_solve,
+ * INVALID_ARG for a zero or > 2^32 image, negative albedo or exposure. */
+spoly_status spoly_render(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces, const double* endpoints,
+                          uint32_t width, uint32_t height, const double* light_intensity, uint32_t nsamples,
+                          const double* slopes, double albedo, double exposure, double* radiance, uint8_t* srgb);
+
 /* Device pointers of the (query, tuple) work list of the LAST solve (cull output or the given list),
  * query-major: pair_query[n_pairs], pair_tuple[n_pairs * k] (original ids).  Only the last chunk
  * is retained when the solve was chunked (*n_pairs then counts that chunk). */

@@ -274,3 +274,67 @@ def sqrt_table() -> np.ndarray:
 
 def sqrt_approx(x: float) -> float:
     return lib().orc_sqrt_approx(float(x))
+
+
+# ----------------------------------------------------------------------------- glossy vertices + splat renderer
+
+class MeshArrays:
+    """Plain container with the attributes solve() reads (pos, nrm, tri, eta_front, eta_back)."""
+
+    def __init__(self, pos, nrm, tri, eta_front=1.0, eta_back=1.0):
+        self.pos, self.nrm, self.tri = pos, nrm, tri
+        self.eta_front, self.eta_back = eta_front, eta_back
+
+
+def perturb_normals(mesh, slopes: np.ndarray) -> MeshArrays:
+    """Glossy vertices: "After sampling the normal offset for glossy vertices, the admissible chains
+    corresponding to the offset remain finite, and the problem reduces to pure specular situations."
+    reading R28: triangle t's three shading normals get the offset p_t T_t + q_t B_t, with T_t = e1 / |e1| and
+    B_t = g^ x T_t (g = e1 x e2) the orthonormal frame of its plane, n_j' = fl32(n_j + p T + q B) in FP64.
+    slopes: (ntris, 2) float64.  Returns a de-indexed mesh (three own vertices per triangle, same triangle ids) so
+    that shared vertices can carry each triangle's own normal.  Pinned by tests/test_glossy_render.py (frame
+    properties, tilt angle, zero-offset identity, brute-force shooting on the perturbed surface)."""
+    tri = np.asarray(mesh.tri, dtype=np.int64)
+    P = np.asarray(mesh.pos, dtype=np.float32)[tri].astype(np.float64)      # (T, 3, 3)
+    N = np.asarray(mesh.nrm, dtype=np.float32)[tri].astype(np.float64)
+    s = np.asarray(slopes, dtype=np.float64).reshape(len(tri), 2)
+    e1 = P[:, 1] - P[:, 0]
+    e2 = P[:, 2] - P[:, 0]
+    g = np.cross(e1, e2)
+    gh = g / np.sqrt(np.sum(g * g, axis=1))[:, None]
+    T = e1 / np.sqrt(np.sum(e1 * e1, axis=1))[:, None]
+    B = np.cross(gh, T)
+    h = s[:, 0:1] * T + s[:, 1:2] * B
+    N2 = (N + h[:, None, :]).astype(np.float32)
+    pos = P.astype(np.float32).reshape(-1, 3)
+    return MeshArrays(pos, N2.reshape(-1, 3), np.arange(3 * len(tri), dtype=np.uint32).reshape(-1, 3),
+                      mesh.eta_front, mesh.eta_back)
+
+
+def tonemap_srgb(radiance: np.ndarray, exposure: float = 1.0) -> np.ndarray:
+    """8-bit gamma-2.2 gray code ("binary PPM (P6, 8-bit, sRGB with gamma 2.2)"):
+    c = rint(255 * min(1, max(0, exposure * L))^(1/2.2)), replicated over 3 channels."""
+    v = np.minimum(1.0, np.maximum(0.0, exposure * np.asarray(radiance, dtype=np.float64)))
+    c = np.rint(255.0 * v ** (1.0 / 2.2)).astype(np.uint8)
+    return np.repeat(c[..., None], 3, axis=-1)
+
+
+def render(mesh, chain: str, endpoints: np.ndarray, width: int, height: int, intensity=None, slopes=None,
+           albedo: float = 1.0, exposure: float = 1.0, cfg: Config = None, nthreads: int = 0):
+    """Deterministic splat renderer (SPEC S:661-669 cmd_render, no Monte Carlo): pixel q is query q
+    (row-major); per offset sample s the chains are solved on the perturbed surface and
+        radiance[q] = sum_s (albedo / pi / S) * per_query_s[q]   (samples in order).
+    slopes: (S, ntris, 2) or None (one pure specular solve).  Returns (radiance (H, W), srgb (H, W, 3) uint8,
+    [oracle Result per sample]).  Pinned by tests/test_glossy_render.py (image-source mask IoU = 1 and radiance
+    albedo/pi * I / L^2 of a flat-mirror caustic, sample averaging, gamma codes of known values)."""
+    S = 1 if slopes is None else int(np.asarray(slopes).shape[0])
+    nq = width * height
+    acc = np.zeros(nq)
+    scale = albedo / np.pi / S
+    results = []
+    for s in range(S):
+        m = mesh if slopes is None else perturb_normals(mesh, np.asarray(slopes)[s])
+        r = solve(m, chain, endpoints, intensity, cfg=cfg, nthreads=nthreads)
+        acc += scale * r.per_query
+        results.append(r)
+    return acc.reshape(height, width), tonemap_srgb(acc, exposure).reshape(height, width, 3), results

@@ -70,6 +70,9 @@ struct spoly_ctx {
   bool has_mesh = false;
   DeviceMesh M;
   DBuf<TriRec> d_tris, d_occ;
+  DBuf<TriRec> d_tris_base;  // uploaded records while glossy normal offsets are applied (reading R28)
+  bool has_base = false;
+  DBuf<double> d_slopes, d_acc;
   DBuf<float4> d_box[kMaxAabbLevels], d_obox[kMaxAabbLevels];  // visibility hierarchies (mesh, occluders)
   AabbTree mesh_tree, occ_tree;
   DBuf<uint8_t> d_vkeep;
@@ -200,6 +203,7 @@ void spoly_destroy(spoly_ctx* ctx) {
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->st);
   ctx->d_tris.release(); ctx->d_occ.release(); ctx->d_tcull.release();
+  ctx->d_tris_base.release(); ctx->d_slopes.release(); ctx->d_acc.release();
   for (auto& b : ctx->d_box) b.release();
   for (auto& b : ctx->d_obox) b.release();
   ctx->d_vkeep.release(); ctx->d_vsel.release(); ctx->d_viota.release(); ctx->d_vkey.release(); ctx->d_vn.release();
@@ -319,6 +323,25 @@ spoly_status spoly_upload_occluders(spoly_ctx* ctx, const float* pos, uint32_t n
   return s;
 }
 
+// cluster bounds of the current triangle records: levels 1-2 and the upper levels of the implicit 8-ary hierarchy
+// (two-bounce pair cull) until <= 8 nodes
+static spoly_status build_bounds(spoly_ctx* ctx, uint32_t ntris) {
+  const uint32_t ncl = (ntris + kClusterSize - 1) / kClusterSize;
+  launch_build_clusters(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, ctx->d_cl.p, ctx->d_sub.p, ctx->st);
+  ctx->M.nupper = 0;
+  uint64_t n = ncl, size = kClusterSize;
+  for (int i = 0; i < 4 && n > 8; ++i) {
+    size *= 8;
+    n = (ntris + size - 1) / size;
+    CK(ctx->d_up[i].ensure(n));
+    launch_build_upper(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, 3 + i, ctx->d_up[i].p, (uint32_t)n, ctx->st);
+    ctx->M.upper[i] = ctx->d_up[i].p;
+    ctx->M.nupper_nodes[i] = (uint32_t)n;
+    ctx->M.nupper = i + 1;
+  }
+  return SPOLY_OK;
+}
+
 spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nrm, uint32_t nverts, const uint32_t* tri,
                                uint32_t ntris, float eta_front, float eta_back, uint32_t* mesh_id) {
   if (!ctx || !pos || !nrm || !tri || ntris == 0 || nverts == 0) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null mesh");
@@ -351,20 +374,9 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   CK(ctx->d_sub.ensure(nsub));
   launch_build_tris(dpos, dnrm, dtri, dorder, ntris, ctx->cfg.cull_margin, ctx->d_tris.p, ctx->d_tcull.p,
                     ctx->d_orig.p, ctx->d_perm.p, ctx->st);
-  launch_build_clusters(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, ctx->d_cl.p, ctx->d_sub.p, ctx->st);
-  // upper levels of the implicit 8-ary hierarchy (two-bounce pair cull) until <= 8 nodes
-  ctx->M.nupper = 0;
   {
-    uint64_t n = ncl, size = kClusterSize;
-    for (int i = 0; i < 4 && n > 8; ++i) {
-      size *= 8;
-      n = (ntris + size - 1) / size;
-      CK(ctx->d_up[i].ensure(n));
-      launch_build_upper(ctx->d_tris.p, ntris, ctx->cfg.cull_margin, 3 + i, ctx->d_up[i].p, (uint32_t)n, ctx->st);
-      ctx->M.upper[i] = ctx->d_up[i].p;
-      ctx->M.nupper_nodes[i] = (uint32_t)n;
-      ctx->M.nupper = i + 1;
-    }
+    spoly_status bs = build_bounds(ctx, ntris);
+    if (bs != SPOLY_OK) return bs;
   }
   {
     spoly_status bs = build_tree(ctx, ctx->d_tris.p, ntris, ctx->d_box, ctx->mesh_tree);
@@ -387,6 +399,7 @@ spoly_status spoly_upload_mesh(spoly_ctx* ctx, const float* pos, const float* nr
   ctx->M.perm_of = ctx->d_perm.p;
   ctx->M.clusters = ctx->d_cl.p;
   ctx->has_mesh = true;
+  ctx->has_base = false;
   ctx->k2_chunk = 0;
   if (mesh_id) *mesh_id = 0;
   return SPOLY_OK;
@@ -1121,6 +1134,75 @@ spoly_status spoly_solve_host(spoly_ctx* ctx, uint32_t mesh_id, const char* chai
   CK(cudaMemcpyAsync(ctx->h_pinned, r->per_query, sizeof(double) * nq, cudaMemcpyDeviceToHost, ctx->st));
   CK(cudaStreamSynchronize(ctx->st));
   memcpy(per_query_host, ctx->h_pinned, sizeof(double) * nq);
+  return SPOLY_OK;
+}
+
+spoly_status spoly_set_normal_offsets(spoly_ctx* ctx, const double* slopes, uint32_t ntris) {
+  if (!ctx) return SPOLY_ERR_INVALID_ARG;
+  if (!ctx->has_mesh) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no mesh uploaded");
+  const uint32_t n = ctx->M.ntris;
+  if (slopes && ntris != n) return fail(ctx, SPOLY_ERR_INVALID_ARG, "slopes must hold 2 values per mesh triangle");
+  for (uint64_t i = 0; slopes && i < 2ull * n; ++i)
+    if (!std::isfinite(slopes[i])) return fail(ctx, SPOLY_ERR_INVALID_ARG, "non-finite slope");
+  CK(cudaSetDevice(ctx->device));
+  if (!slopes) {
+    if (ctx->has_base)
+      CK(cudaMemcpyAsync(ctx->d_tris.p, ctx->d_tris_base.p, sizeof(TriRec) * n, cudaMemcpyDeviceToDevice, ctx->st));
+  } else {
+    if (!ctx->has_base) {
+      CK(ctx->d_tris_base.ensure(n));
+      CK(cudaMemcpyAsync(ctx->d_tris_base.p, ctx->d_tris.p, sizeof(TriRec) * n, cudaMemcpyDeviceToDevice, ctx->st));
+      ctx->has_base = true;
+    }
+    CK(ctx->d_slopes.ensure(2ull * n));
+    CK(cudaMemcpyAsync(ctx->d_slopes.p, slopes, sizeof(double) * 2ull * n, cudaMemcpyHostToDevice, ctx->st));
+  }
+  if (ctx->has_base) {
+    if (slopes)
+      launch_perturb_tris(ctx->d_tris_base.p, ctx->d_slopes.p, ctx->M.orig_id, n, ctx->cfg.cull_margin, ctx->d_tris.p,
+                          ctx->d_tcull.p, ctx->st);
+    else
+      launch_rebuild_tcull(ctx->d_tris.p, n, ctx->cfg.cull_margin, ctx->d_tcull.p, ctx->st);
+    spoly_status bs = build_bounds(ctx, n);
+    if (bs != SPOLY_OK) return bs;
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st));
+  return SPOLY_OK;
+}
+
+spoly_status spoly_render(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, int bounces, const double* endpoints,
+                          uint32_t width, uint32_t height, const double* light_intensity, uint32_t nsamples,
+                          const double* slopes, double albedo, double exposure, double* radiance, uint8_t* srgb) {
+  if (!ctx || !endpoints || !radiance) return fail(ctx, SPOLY_ERR_INVALID_ARG, "null argument");
+  if (!ctx->has_mesh) return fail(ctx, SPOLY_ERR_INVALID_ARG, "no mesh uploaded");
+  const uint64_t nq64 = (uint64_t)width * height;
+  if (nq64 == 0 || nq64 > 0xffffffffull) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bad image size");
+  if (!(albedo >= 0) || !std::isfinite(albedo) || !(exposure >= 0)) return fail(ctx, SPOLY_ERR_INVALID_ARG, "bad albedo/exposure");
+  const uint32_t nq = (uint32_t)nq64, S = nsamples ? nsamples : 1;
+  CK(cudaSetDevice(ctx->device));
+  CK(ctx->d_acc.ensure(nq));
+  CK(cudaMemsetAsync(ctx->d_acc.p, 0, sizeof(double) * nq, ctx->st));
+  const double scale = albedo / 3.14159265358979323846 / S;
+  spoly_status s = SPOLY_OK;
+  for (uint32_t i = 0; i < S && s == SPOLY_OK; ++i) {
+    if (slopes) {
+      s = spoly_set_normal_offsets(ctx, slopes + 2ull * ctx->M.ntris * i, ctx->M.ntris);
+      if (s != SPOLY_OK) break;
+    }
+    spoly_result r;
+    s = spoly_solve(ctx, mesh_id, chain, bounces, endpoints, nq, light_intensity, nullptr, &r);
+    if (s == SPOLY_OK) launch_splat(r.per_query, nq, scale, ctx->d_acc.p, ctx->st);
+  }
+  if (slopes) {
+    spoly_status r2 = spoly_set_normal_offsets(ctx, nullptr, 0);
+    if (s == SPOLY_OK) s = r2;
+  }
+  if (s != SPOLY_OK) return s;
+  CK(cudaMemcpyAsync(radiance, ctx->d_acc.p, sizeof(double) * nq, cudaMemcpyDeviceToDevice, ctx->st));
+  if (srgb) launch_tonemap(ctx->d_acc.p, nq, exposure, srgb, ctx->st);
+  CK(cudaGetLastError());
+  CK(cudaStreamSynchronize(ctx->st));
   return SPOLY_OK;
 }
 

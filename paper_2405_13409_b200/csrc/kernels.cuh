@@ -12,6 +12,11 @@ void launch_build_upper(const TriRec* recs, uint32_t ntris, float margin, int le
                         cudaStream_t st);
 void launch_build_clusters(const TriRec* recs, uint32_t ntris, float margin, ClusterRec* l1, ClusterRec* l2,
                            cudaStream_t st);
+void launch_perturb_tris(const TriRec* base, const double* slopes, const uint32_t* orig_id, uint32_t ntris,
+                         float margin, TriRec* recs, TriCull* tc, cudaStream_t st);
+void launch_rebuild_tcull(const TriRec* recs, uint32_t ntris, float margin, TriCull* tc, cudaStream_t st);
+void launch_splat(const double* per_query, uint32_t nq, double scale, double* acc, cudaStream_t st);
+void launch_tonemap(const double* L, uint32_t nq, double exposure, uint8_t* rgb, cudaStream_t st);
 
 // cull.cu: query-coherent hierarchical cone cull (tiles of 32 Morton-sorted queries, then per query)
 void launch_query_order(const double* ep, uint32_t nq, float* bounds, uint32_t* keys, uint32_t* idx,

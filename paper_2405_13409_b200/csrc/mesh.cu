@@ -12,6 +12,27 @@ __device__ __forceinline__ float cone_sin(double theta, double margin) {
   return b >= 1.5707963 ? 1.0f : (float)fmin(1.0, sin(b) * (1.0 + 1e-6) + 1e-7);
 }
 
+// per-triangle cull node: centroid sphere, cone of the normalised vertex normals, geometric plane
+__device__ TriCull make_tcull(const float* p, const float* n, float margin) {
+  d3 P[3] = {mk3(p[0], p[1], p[2]), mk3(p[3], p[4], p[5]), mk3(p[6], p[7], p[8])};
+  d3 N[3] = {normalize(mk3(n[0], n[1], n[2])), normalize(mk3(n[3], n[4], n[5])), normalize(mk3(n[6], n[7], n[8]))};
+  d3 c = (1.0 / 3.0) * (P[0] + P[1] + P[2]);
+  double rho = fmax(norm(P[0] - c), fmax(norm(P[1] - c), norm(P[2] - c)));
+  d3 ax = N[0] + N[1] + N[2];
+  double al = norm(ax), th = 4.0;
+  if (al > 0) {
+    ax = (1.0 / al) * ax;
+    th = 0;
+    for (int j = 0; j < 3; ++j) th = fmax(th, atan2(norm(cross(N[j], ax)), dot(N[j], ax)));
+  }
+  d3 g = cross(P[1] - P[0], P[2] - P[0]);
+  TriCull T;
+  T.sphere = make_float4((float)c.x, (float)c.y, (float)c.z, (float)(rho * (1.0 + 1e-5) + 1e-6));
+  T.cone = make_float4((float)ax.x, (float)ax.y, (float)ax.z, cone_sin(th, margin));
+  T.plane = make_float4((float)g.x, (float)g.y, (float)g.z, (float)dot(g, P[0]));
+  return T;
+}
+
 __global__ void k_build_tris(const float* __restrict__ pos, const float* __restrict__ nrm,
                              const uint32_t* __restrict__ tri, const uint32_t* __restrict__ order, uint32_t ntris,
                              float margin, TriRec* recs, TriCull* tc, uint32_t* orig_id, uint32_t* perm_of) {
@@ -37,23 +58,7 @@ __global__ void k_build_tris(const float* __restrict__ pos, const float* __restr
   recs[i] = R;
   orig_id[i] = t;
   perm_of[t] = i;
-  d3 P[3] = {mk3(p[0], p[1], p[2]), mk3(p[3], p[4], p[5]), mk3(p[6], p[7], p[8])};
-  d3 N[3] = {normalize(mk3(n[0], n[1], n[2])), normalize(mk3(n[3], n[4], n[5])), normalize(mk3(n[6], n[7], n[8]))};
-  d3 c = (1.0 / 3.0) * (P[0] + P[1] + P[2]);
-  double rho = fmax(norm(P[0] - c), fmax(norm(P[1] - c), norm(P[2] - c)));
-  d3 ax = N[0] + N[1] + N[2];
-  double al = norm(ax), th = 4.0;
-  if (al > 0) {
-    ax = (1.0 / al) * ax;
-    th = 0;
-    for (int j = 0; j < 3; ++j) th = fmax(th, atan2(norm(cross(N[j], ax)), dot(N[j], ax)));
-  }
-  d3 g = cross(P[1] - P[0], P[2] - P[0]);
-  TriCull T;
-  T.sphere = make_float4((float)c.x, (float)c.y, (float)c.z, (float)(rho * (1.0 + 1e-5) + 1e-6));
-  T.cone = make_float4((float)ax.x, (float)ax.y, (float)ax.z, cone_sin(th, margin));
-  T.plane = make_float4((float)g.x, (float)g.y, (float)g.z, (float)dot(g, P[0]));
-  tc[i] = T;
+  tc[i] = make_tcull(p, n, margin);
 }
 
 void launch_build_tris(const float* pos, const float* nrm, const uint32_t* tri, const uint32_t* order, uint32_t ntris,
@@ -61,6 +66,88 @@ void launch_build_tris(const float* pos, const float* nrm, const uint32_t* tri, 
                        cudaStream_t st) {
   if (!ntris) return;
   k_build_tris<<<(ntris + 255) / 256, 256, 0, st>>>(pos, nrm, tri, order, ntris, margin, recs, tc, orig_id, perm_of);
+}
+
+// Glossy vertices (reading R28): every triangle's three shading normals get the same microfacet
+// offset p T + q B, with (T, B) the orthonormal frame of the triangle plane (T along e1, B = g^ x T),
+// n_j' = fl32(n_j + p T + q B) computed in FP64 from the uploaded (base) record; the cull node is rebuilt from the
+// perturbed normals.  slopes: [ntris][2] in ORIGINAL triangle order.
+__global__ void k_perturb_tris(const TriRec* __restrict__ base, const double* __restrict__ slopes,
+                               const uint32_t* __restrict__ orig_id, uint32_t ntris, float margin, TriRec* recs,
+                               TriCull* tc) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntris) return;
+  TriRec R = base[i];
+  float f[20];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    f[4 * j] = R.r[j].x; f[4 * j + 1] = R.r[j].y; f[4 * j + 2] = R.r[j].z; f[4 * j + 3] = R.r[j].w;
+  }
+  const float* p = f;      // p[0..8]
+  float* n = f + 9;        // n[0..8]
+  const uint32_t t = orig_id[i];
+  const double sp = slopes[2ull * t], sq = slopes[2ull * t + 1];
+  const d3 P0 = mk3(p[0], p[1], p[2]), e1 = mk3(p[3], p[4], p[5]) - P0, e2 = mk3(p[6], p[7], p[8]) - P0;
+  const d3 gh = normalize(cross(e1, e2)), T = normalize(e1), B = cross(gh, T);
+  const d3 h = sp * T + sq * B;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    n[3 * j] = (float)((double)n[3 * j] + h.x);
+    n[3 * j + 1] = (float)((double)n[3 * j + 1] + h.y);
+    n[3 * j + 2] = (float)((double)n[3 * j + 2] + h.z);
+  }
+#pragma unroll
+  for (int j = 0; j < 5; ++j) R.r[j] = make_float4(f[4 * j], f[4 * j + 1], f[4 * j + 2], f[4 * j + 3]);
+  recs[i] = R;
+  tc[i] = make_tcull(p, n, margin);
+}
+
+void launch_perturb_tris(const TriRec* base, const double* slopes, const uint32_t* orig_id, uint32_t ntris,
+                         float margin, TriRec* recs, TriCull* tc, cudaStream_t st) {
+  if (!ntris) return;
+  k_perturb_tris<<<(ntris + 255) / 256, 256, 0, st>>>(base, slopes, orig_id, ntris, margin, recs, tc);
+}
+
+// cull nodes of the current records (after restoring the uploaded normals)
+__global__ void k_rebuild_tcull(const TriRec* __restrict__ recs, uint32_t ntris, float margin, TriCull* tc) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ntris) return;
+  const TriRec R = recs[i];
+  float f[20];
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    f[4 * j] = R.r[j].x; f[4 * j + 1] = R.r[j].y; f[4 * j + 2] = R.r[j].z; f[4 * j + 3] = R.r[j].w;
+  }
+  tc[i] = make_tcull(f, f + 9, margin);
+}
+
+void launch_rebuild_tcull(const TriRec* recs, uint32_t ntris, float margin, TriCull* tc, cudaStream_t st) {
+  if (ntris) k_rebuild_tcull<<<(ntris + 255) / 256, 256, 0, st>>>(recs, ntris, margin, tc);
+}
+
+// Renderer splat (SPEC S:661-669 cmd_render): acc[q] += scale * per_query[q]
+__global__ void k_splat(const double* __restrict__ per_query, uint32_t nq, double scale, double* acc) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x)
+    acc[q] += scale * per_query[q];
+}
+
+// 8-bit sRGB-gamma code of the linear radiance (gray): c = round(255 * min(1, exposure * L)^(1/2.2))
+__global__ void k_tonemap(const double* __restrict__ L, uint32_t nq, double exposure, uint8_t* rgb) {
+  for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += gridDim.x * blockDim.x) {
+    const double v = fmin(1.0, fmax(0.0, exposure * L[q]));
+    const uint8_t c = (uint8_t)rint(255.0 * pow(v, 1.0 / 2.2));
+    rgb[3ull * q] = c;
+    rgb[3ull * q + 1] = c;
+    rgb[3ull * q + 2] = c;
+  }
+}
+
+void launch_splat(const double* per_query, uint32_t nq, double scale, double* acc, cudaStream_t st) {
+  if (nq) k_splat<<<(nq + 255) / 256 < 4096 ? (nq + 255) / 256 : 4096, 256, 0, st>>>(per_query, nq, scale, acc);
+}
+
+void launch_tonemap(const double* L, uint32_t nq, double exposure, uint8_t* rgb, cudaStream_t st) {
+  if (nq) k_tonemap<<<(nq + 255) / 256 < 4096 ? (nq + 255) / 256 : 4096, 256, 0, st>>>(L, nq, exposure, rgb);
 }
 
 // one warp per cluster of G consecutive Morton triangles: bounding sphere of all vertices around their

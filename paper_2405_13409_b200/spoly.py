@@ -23,7 +23,8 @@ STATUS = {0: "SPOLY_OK", 1: "SPOLY_ERR_INVALID_ARG", 2: "SPOLY_ERR_BAD_MESH", 3:
 FLAG_NEAR_TANGENT, FLAG_BOUNDARY, FLAG_RESIDUAL, FLAG_DEGENERATE, FLAG_TRUNCATED = 1, 2, 4, 8, 16
 
 EXPORTS = ["spoly_default_config", "spoly_create", "spoly_destroy", "spoly_last_error", "spoly_upload_mesh",
-           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma", "spoly_sqrt_table", "spoly_upload_occluders"]
+           "spoly_solve", "spoly_solve_host", "spoly_last_worklist", "spoly_bench_fma", "spoly_sqrt_table", "spoly_upload_occluders",
+           "spoly_set_normal_offsets", "spoly_render"]
 
 
 class SpolyError(RuntimeError):
@@ -94,6 +95,8 @@ def lib():
         L.spoly_bench_fma.argtypes = [P, I, D, P]
         L.spoly_sqrt_table.argtypes = [P, I, P]
         L.spoly_upload_occluders.argtypes = [P, P, U32, P, U32]
+        L.spoly_set_normal_offsets.argtypes = [P, P, U32]
+        L.spoly_render.argtypes = [P, U32, ctypes.c_char_p, I, P, U32, U32, P, U32, P, D, D, P, P]
         _lib = L
     return _lib
 
@@ -221,6 +224,37 @@ class Context:
         tri = np.ascontiguousarray(mesh.tri, dtype=np.uint32)
         rc = self._L.spoly_upload_occluders(self._h, pos.ctypes.data, pos.shape[0], tri.ctypes.data, tri.shape[0])
         self._check(rc, "spoly_upload_occluders")
+
+    def set_normal_offsets(self, slopes=None):
+        """Glossy microfacet offsets (reading R28): slopes (ntris, 2) float64 numpy in original
+        triangle order, or None to restore the uploaded normals."""
+        if slopes is None:
+            self._check(self._L.spoly_set_normal_offsets(self._h, None, 0), "spoly_set_normal_offsets")
+            return
+        sl = np.ascontiguousarray(slopes, dtype=np.float64)
+        self._check(self._L.spoly_set_normal_offsets(self._h, sl.ctypes.data, sl.shape[0]),
+                    "spoly_set_normal_offsets")
+
+    def render(self, chain: str, endpoints, width: int, height: int, intensity=None, slopes=None, albedo=1.0,
+               exposure=1.0, srgb: bool = True, mesh_id: int = 0):
+        """Deterministic splat renderer (spoly_render).  endpoints: CUDA float64 (W*H, 2, 3), row-major pixels;
+        slopes: numpy (S, ntris, 2) float64 or None.  Returns (radiance CUDA float64 (H, W), sRGB CUDA uint8
+        (H, W, 3) or None)."""
+        import torch
+        assert endpoints.is_cuda and endpoints.dtype == torch.float64 and endpoints.is_contiguous()
+        nq = width * height
+        assert endpoints.shape[0] == nq
+        dev = endpoints.device
+        rad = torch.empty(nq, dtype=torch.float64, device=dev)
+        rgb = torch.empty((nq, 3), dtype=torch.uint8, device=dev) if srgb else None
+        sl = None if slopes is None else np.ascontiguousarray(slopes, dtype=np.float64)
+        ns = 0 if sl is None else sl.shape[0]
+        rc = self._L.spoly_render(self._h, mesh_id, chain.encode(), len(chain), endpoints.data_ptr(), width, height,
+                                  intensity.data_ptr() if intensity is not None else None, ns,
+                                  sl.ctypes.data if sl is not None else None, float(albedo), float(exposure),
+                                  rad.data_ptr(), rgb.data_ptr() if rgb is not None else None)
+        self._check(rc, "spoly_render")
+        return rad.view(height, width), (rgb.view(height, width, 3) if rgb is not None else None)
 
     def _wrap(self, r: spoly_result, nq: int):
         dev = f"cuda:{self.device}"

@@ -332,3 +332,30 @@ CONFIGS = {
     "C5": shell_c5,
     "C5RR": mirrors_rr,
 }
+
+
+# ----------------------------------------------------------------------------- glossy + renderer inputs
+
+def beckmann_slopes(seed: int, nsamples: int, ntris: int, alpha: float) -> np.ndarray:
+    """Microfacet slope samples for the glossy extension (reading R28): Beckmann slopes p, q are
+    independent N(0, alpha^2 / 2).  Returns (nsamples, ntris, 2) float64 (the random numbers the method draws,
+    passed to both sides as inputs)."""
+    rng = np.random.default_rng(seed)
+    return rng.normal(0.0, alpha / np.sqrt(2.0), size=(nsamples, ntris, 2))
+
+
+MIRROR_LIGHT = (0.1, -0.05, 0.5)
+
+
+def mirror_caustic(res: int = 128, half: float = 1.5) -> Workload:
+    """Renderer fixture ("flat-mirror caustic line fixture"): one face-normal mirror triangle in the plane
+    z = 1 facing down (normals (0,0,-1)), a point light at MIRROR_LIGHT below it, and res x res receivers at the pixel
+    centres of [-half, half]^2 on z = 0 (row-major, x fastest).  Chain R (x_0 = receiver, x_2 = light)."""
+    pos = np.array([[-0.21, -0.175, 1.0], [0.0, 0.2275, 1.0], [0.245, -0.105, 1.0]], np.float32)
+    nrm = np.tile([0.0, 0.0, -1.0], (3, 1)).astype(np.float32)
+    mesh = Mesh(pos, nrm, np.array([[0, 1, 2]], np.uint32))
+    c = -half + (np.arange(res) + 0.5) * (2 * half / res)
+    X, Y = np.meshgrid(c, c)
+    x0 = np.stack([X.ravel(), Y.ravel(), np.zeros(res * res)], 1)
+    ep = np.stack([x0, np.tile(np.array(MIRROR_LIGHT), (res * res, 1))], 1)
+    return Workload("mirror_caustic", "R", mesh, np.ascontiguousarray(ep), np.ones(res * res), {"res": res})
