@@ -168,18 +168,35 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows), "source": "nvml: 2 ms polling thread + one sample per timed step, timed region only"}
 
 
-def oracle_baseline(w, nsample, nthreads=0):
-    """The oracle as it stands on a bounded, strided sample of the workload's queries."""
+def oracle_baseline(w, nsample, nthreads=0, worklist=None):
+    """The oracle as it stands on a bounded, strided sample of the workload's queries.  worklist (query ids,
+    (n, k) tuples of original triangle ids): give the oracle these pairs of the sampled queries as an explicit tuple
+    list instead of running its own O(T^2)-per-query two-bounce cull (used at 65,536 triangles, where one query's
+    oracle cull alone takes more than 10 minutes)."""
     import oracle
     oracle.build()
     idx = np.linspace(0, w.nqueries - 1, nsample).astype(np.int64)
     sub = w.subset(idx)
+    off = ids = None
+    what = "oracle cull + solve"
+    if worklist is not None:
+        wq, wt = worklist
+        off = [0]
+        ids = []
+        for q in idx:
+            t = wt[wq == q]
+            ids.append(t.reshape(-1))
+            off.append(off[-1] + len(t))
+        off = np.array(off, np.uint32)
+        ids = np.concatenate(ids).astype(np.uint32)
+        what = "oracle solve of the GPU cull's work list for those queries"
     t0 = time.perf_counter()
-    r = oracle.solve(sub.mesh, w.chain, sub.endpoints, intensity=sub.intensity, nthreads=nthreads)
+    r = oracle.solve(sub.mesh, w.chain, sub.endpoints, intensity=sub.intensity, offsets=off, tri_ids=ids,
+                     nthreads=nthreads)
     dt = time.perf_counter() - t0
     cores = nthreads if nthreads > 0 else (os.cpu_count() or 1)
     return {"value": r.n_solutions / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
-            "sample": f"{nsample} of {w.nqueries} queries (strided), full mesh, oracle cull + solve; "
+            "sample": f"{nsample} of {w.nqueries} queries (strided), full mesh, {what}; "
                       f"{r.n_solutions} paths, {r.report['pairs_in']} pairs in {dt:.2f} s",
             "solves_per_s": r.report["pairs_in"] / dt, "seconds": dt}
 
@@ -379,7 +396,12 @@ def main():
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_baseline(w, min(args.cpu_sample, w.nqueries) if len(chain) == 1 else min(4, w.nqueries))
+        wl = None
+        if len(chain) == 2 and w.mesh.ntris > 20000:
+            lq, lt = ctx.last_worklist()
+            wl = (lq.cpu().numpy().view(np.uint32), lt.cpu().numpy().view(np.uint32).reshape(-1, 2))
+        cpu = oracle_baseline(w, min(args.cpu_sample, w.nqueries) if len(chain) == 1 else min(4, w.nqueries),
+                              worklist=wl)
         cpu.pop("seconds", None)
 
     line = {

@@ -224,8 +224,8 @@ spoly_status spoly_render(spoly_ctx* ctx, uint32_t mesh_id, const char* chain, i
                           const double* slopes, double albedo, double exposure, double* radiance, uint8_t* srgb);
 
 /* Device pointers of the (query, tuple) work list of the LAST solve (cull output or the given list),
- * query-major: pair_query[n_pairs], pair_tuple[n_pairs * k] (original ids).  Only the last chunk
- * is retained when the solve was chunked (*n_pairs then counts that chunk). */
+ * query-major: pair_query[n_pairs], pair_tuple[n_pairs * k] (original ids).  A chunked two-bounce cull
+ * keeps every chunk's pairs, concatenated in chunk order (*n_pairs counts them all). */
 spoly_status spoly_last_worklist(const spoly_ctx* ctx, const uint32_t** pair_query,
                                  const uint32_t** pair_tuple, uint64_t* n_pairs);
 

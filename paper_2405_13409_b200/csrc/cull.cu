@@ -1219,6 +1219,168 @@ __device__ uint32_t children_mask(const d3 P1[3], const d3 N1[3], const d3 P2[3]
   return m;
 }
 
+// ---- FP32 refinement (default; SPOLY_REFINE_FP64 restores the FP64 predicate above).  Same cells, same exact
+// vertex cones, evaluated in FP32 with every bound inflated by its rounding error, so the kept set is a superset
+// of the exact predicate's:
+//  - cell corners X = p0 + u e1 + v e2 (u, v dyadic: exact) carry an absolute error <= 3 * 2^-24 (|p0|+|e1|+|e2|);
+//    a direction d = X_b - X_a between two such points (or an endpoint rounded to FP32) is off by at most
+//    eps_d <= 1.2e-6 (|X_a| + |X_b|) (the scales include the triangle's own), so its unit vector moves by at most
+//    eps_d / |d| + 1e-6 (normalisation rounding); each cone chord is inflated by the largest such bound;
+//  - normal cones: unit corner normals (error <= 1e-6), half-angle sine from |M_j x axis| + 4e-6 (no 1 - c^2
+//    cancellation); no bound (keep) when a corner normal is within 89.9 deg of 90 from the axis;
+//  - the final separation test keeps the pair unless it fails by a relative 1e-5.
+struct SubBf {
+  f3 X[3];
+  float S[3];  // |X_j| + the triangle scale: the error scale of directions from X_j
+  f3 ax;
+  float sinb;
+  bool ok;
+};
+
+__device__ __forceinline__ float fnorm(f3 a) { return sqrtf(dotf(a, a)); }
+
+__device__ __forceinline__ SubBf sub_bound_f(const f3 P[3], const f3 N[3], float tscale, int ou, int ov, int sg,
+                                             int h) {
+  constexpr float inv = 1.f / (1 << kMaxLevels);
+  const float u[3] = {ou * inv, (ou + sg * h) * inv, ou * inv};
+  const float v[3] = {ov * inv, ov * inv, (ov + sg * h) * inv};
+  const f3 e1 = P[1] - P[0], e2 = P[2] - P[0], m1 = N[1] - N[0], m2 = N[2] - N[0];
+  SubBf B;
+  B.ok = true;
+  f3 M[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    B.X[j] = P[0] + u[j] * e1 + v[j] * e2;
+    B.S[j] = fnorm(B.X[j]) + tscale;
+    const f3 n = N[0] + u[j] * m1 + v[j] * m2;
+    const float l2 = dotf(n, n);
+    if (!(l2 > 1e-30f)) B.ok = false;
+    M[j] = rsqrtf(l2) * n;
+  }
+  const f3 s = M[0] + M[1] + M[2];
+  const float sl2 = dotf(s, s);
+  if (!(sl2 > 1e-12f)) {
+    B.ok = false;
+    return B;
+  }
+  B.ax = rsqrtf(sl2) * s;
+  float sb = 0.f;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    if (!(dotf(M[j], B.ax) > 2e-3f)) B.ok = false;
+    sb = fmaxf(sb, fnorm(crossf(M[j], B.ax)));
+  }
+  B.sinb = fminf(1.f, sb + 4e-6f);
+  return B;
+}
+
+// exact direction cone of M directions d_j with error scales S_j (see above): axis, inflated chord
+template <int M>
+__device__ __forceinline__ bool exact_cone_f(const f3 (&d)[M], const float (&S)[M], f3& axis, float& chord) {
+  f3 w[M];
+  float er[M];
+  f3 s = {0.f, 0.f, 0.f};
+#pragma unroll
+  for (int j = 0; j < M; ++j) {
+    const float l2 = dotf(d[j], d[j]);
+    if (!(l2 > 1e-30f)) return false;
+    const float il = rsqrtf(l2);
+    w[j] = il * d[j];
+    er[j] = 1.2e-6f * S[j] * il + 1e-6f;
+    s = s + w[j];
+  }
+  const float sl2 = dotf(s, s);
+  if (!(sl2 > 1e-12f)) return false;
+  axis = rsqrtf(sl2) * s;
+  float c = 0.f;
+#pragma unroll
+  for (int j = 0; j < M; ++j) c = fmaxf(c, fnorm(w[j] - axis) + er[j]);
+  chord = c * (1.f + 1e-5f) + 2e-6f;
+  return true;
+}
+
+// node_keep with a relative 1e-5 margin on the final separation test
+__device__ __forceinline__ bool node_keep_r(f3 ap, float cp, f3 an, float cn, float ep, float en, f3 nax, float sb) {
+  const f3 A = ep * ap + en * an;
+  const float r = ep * cp + en * cn;
+  const float A2 = dotf(A, A);
+  if (!(A2 > r * r * 1.0001f + 1e-12f)) return true;
+  const float cb = sqrtf(fmaxf(1.f - sb * sb, 0.f));
+  const float q = sqrtf(A2 - r * r);
+  if (!(q * cb - r * sb > 1e-6f * sqrtf(A2))) return true;
+  const f3 X = crossf(A, nax);
+  const float rhs = r * cb + q * sb;
+  return !(dotf(X, X) > rhs * rhs * (1.f + 1e-5f) + 1e-12f * A2);
+}
+
+// 16-bit mask of the surviving child pairs of node n (size h), FP32
+__device__ uint32_t children_mask_f(const f3 P1[3], const f3 N1[3], float s1, const f3 P2[3], const f3 N2[3], float s2,
+                                    f3 x0, float n0, f3 x3, float n3, const SubNode& n, int h, const float e[2][3],
+                                    int ncombo) {
+  SubBf A[4], B[4];
+  f3 a0[4], a3[4];
+  float c0[4], c3[4];
+  bool ok0[4], ok3[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    int cu, cv, cs;
+    child_of(n.u1, n.v1, n.s1, h, c, cu, cv, cs);
+    A[c] = sub_bound_f(P1, N1, s1, cu, cv, cs, h >> 1);
+    child_of(n.u2, n.v2, n.s2, h, c, cu, cv, cs);
+    B[c] = sub_bound_f(P2, N2, s2, cu, cv, cs, h >> 1);
+    const f3 d0[3] = {x0 - A[c].X[0], x0 - A[c].X[1], x0 - A[c].X[2]};
+    const float S0[3] = {A[c].S[0] + n0, A[c].S[1] + n0, A[c].S[2] + n0};
+    ok0[c] = exact_cone_f<3>(d0, S0, a0[c], c0[c]);
+    const f3 d3_[3] = {x3 - B[c].X[0], x3 - B[c].X[1], x3 - B[c].X[2]};
+    const float S3[3] = {B[c].S[0] + n3, B[c].S[1] + n3, B[c].S[2] + n3};
+    ok3[c] = exact_cone_f<3>(d3_, S3, a3[c], c3[c]);
+  }
+  uint32_t m = 0;
+#pragma unroll
+  for (int ia = 0; ia < 4; ++ia)
+#pragma unroll 1
+  for (int ib = 0; ib < 4; ++ib) {
+    const int i = 4 * ia + ib;
+    const SubBf& SA = A[ia];
+    const SubBf& SB = B[ib];
+    bool keep = true;
+    if (SA.ok && SB.ok && ok0[ia] && ok3[ib]) {
+      f3 d[9];
+      float S[9];
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          d[3 * a + b] = SB.X[b] - SA.X[a];
+          S[3 * a + b] = SA.S[a] + SB.S[b];
+        }
+      f3 aAB;
+      float cAB;
+      if (exact_cone_f<9>(d, S, aAB, cAB)) {
+        const f3 aBA = {-aAB.x, -aAB.y, -aAB.z};
+        keep = false;
+        for (int c = 0; c < ncombo && !keep; ++c)
+          keep = node_keep_r(a0[ia], c0[ia], aAB, cAB, e[c][0], e[c][1], SA.ax, SA.sinb) &&
+                 node_keep_r(aBA, cAB, a3[ib], c3[ib], e[c][1], e[c][2], SB.ax, SB.sinb);
+      }
+    }
+    if (keep) m |= 1u << i;
+  }
+  return m;
+}
+
+__device__ __forceinline__ void load_tri_f(const TriRec* __restrict__ T, uint32_t i, f3 p[3], f3 n[3], float& scale) {
+  const float4* r = T[i].r;
+  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+  p[0] = {a.x, a.y, a.z};
+  p[1] = {a.w, b.x, b.y};
+  p[2] = {b.z, b.w, c.x};
+  n[0] = {c.y, c.z, c.w};
+  n[1] = {d.x, d.y, d.z};
+  n[2] = {d.w, e.x, e.y};
+  scale = fnorm(p[0]) + fnorm(p[1] - p[0]) + fnorm(p[2] - p[0]);
+}
+
 // eta combinations of a pair: eta_0 from the side of x_0 w.r.t. T_1's plane (reading R9; sub-triangles
 // share the plane); within 1e-9 of the plane both media are tried
 __device__ __forceinline__ int eta_combos(d3 x0, const d3 P1[3], int v1t, int v2t, float ef, float eb,
@@ -1281,12 +1443,31 @@ __global__ void __launch_bounds__(128) k_refine_level(int level, int last, const
     }
     const double* e = ep + 6ull * pq[r];
     const d3 x0 = mk3(e[0], e[1], e[2]), x3 = mk3(e[3], e[4], e[5]);
+#ifdef SPOLY_REFINE_FP64
     d3 P1[3], N1[3], P2[3], N2[3];
     load_tri(tris, pt[2 * r], P1, N1);
     load_tri(tris, pt[2 * r + 1], P2, N2);
     double ec[2][3];
     const int ncombo = eta_combos(x0, P1, v1t, v2t, ef, eb, ec);
     const uint32_t m = children_mask(P1, N1, P2, N2, x0, x3, nd, h, ec, ncombo);
+#else
+    uint32_t m;
+    {
+      d3 P1d[3], N1d[3];
+      load_tri(tris, pt[2 * r], P1d, N1d);
+      double ec[2][3];
+      const int ncombo = eta_combos(x0, P1d, v1t, v2t, ef, eb, ec);  // FP64 side decision, as the FP64 path
+      float ecf[2][3];
+      for (int c = 0; c < 2; ++c)
+        for (int j = 0; j < 3; ++j) ecf[c][j] = (float)ec[c][j];
+      f3 P1[3], N1[3], P2[3], N2[3];
+      float s1, s2;
+      load_tri_f(tris, pt[2 * r], P1, N1, s1);
+      load_tri_f(tris, pt[2 * r + 1], P2, N2, s2);
+      const f3 x0f = {(float)x0.x, (float)x0.y, (float)x0.z}, x3f = {(float)x3.x, (float)x3.y, (float)x3.z};
+      m = children_mask_f(P1, N1, s1, P2, N2, s2, x0f, fnorm(x0f), x3f, fnorm(x3f), nd, h, ecf, ncombo);
+    }
+#endif
     if (!m) continue;
     if (last) {
       keep[r] = 1;

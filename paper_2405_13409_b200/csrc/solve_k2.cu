@@ -475,8 +475,11 @@ __device__ __forceinline__ void group_counters(const Grp<G>& g, const uint32_t* 
 
 // ---- kernel 1: coefficient phase (group per pair, shared-memory arena), record write
 constexpr int kBuildWarps = 2;
+#ifndef SPOLY_BUILD_MINB
+#define SPOLY_BUILD_MINB 4  // 4 x 64 threads: up to 255 registers (5 blocks fit the TT arena but cap them at 168: spills)
+#endif
 template <bool V1T, bool V2T>
-__global__ void __launch_bounds__(kBuildWarps * 32) k2_build(const uint32_t* __restrict__ pq,
+__global__ void __launch_bounds__(kBuildWarps * 32, SPOLY_BUILD_MINB) k2_build(const uint32_t* __restrict__ pq,
                                                             const uint32_t* __restrict__ pt, uint64_t p0,
                                                             uint64_t np, const TriRec* __restrict__ tris,
                                                             const double* __restrict__ ep, SolveParams prm,
@@ -585,6 +588,16 @@ constexpr int kScanWarps = 4;
 // resident blocks per SM the register budget must allow: the scan is latency-bound (dependent shuffles and
 // FP64 chains), so occupancy matters more than the compiler's unconstrained register use (252 for TT)
 __host__ __device__ constexpr int scan_min_blocks(int nc) { return nc == 0 ? 1 : (nc <= 16 ? 4 : (nc <= 24 ? 3 : 2)); }
+// lanes per system in the scan: a class with order <= 16 needs 16 rows, so two systems share a warp (the build's
+// group is 32 wide for the chains whose b has more than 16 u-rows)
+template <bool V1T, bool V2T>
+__host__ __device__ constexpr int scan_group(int nc) {
+#ifdef SPOLY_SCAN_G32
+  return Deg2<V1T, V2T>::G;
+#else
+  return (nc > 0 && nc <= 16) ? 16 : Deg2<V1T, V2T>::G;
+#endif
+}
 template <bool V1T, bool V2T, int NC>
 __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(uint64_t p0, uint64_t np, SolveParams prm,
                                                           const uint32_t* __restrict__ vrange,
@@ -596,7 +609,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
                                                           unsigned long long* __restrict__ next) {
   using D = Deg2<V1T, V2T>;
   using R = Rec2<V1T, V2T>;
-  constexpr int G = D::G, GPW = 32 / G;
+  constexpr int G = scan_group<V1T, V2T>(NC), GPW = 32 / G;
   constexpr bool BIG = NC == 0;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, gi = (threadIdx.x & 31) / G;
@@ -715,6 +728,192 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
     }
     g.sync();
   }
+  group_counters(g, cnt, S);
+}
+
+// ---- kernel 2 (multi-sample form, orders <= 16): one system per warp, D = 32 / L determinants at once (wdet_quad).
+// The samples j = jlo..jhi are evaluated D at a time and walked in order with exactly the sequential scan's
+// decisions (c14 probe, exact zero, sign change), so the v-root list is the same list in the same order.  Each
+// sign-changing piece is then bisected by multisection: the 2^m - 1 nested midpoints of the bracket (m <= log2 D
+// levels per round, the values sequential bisection would compute along any path) are evaluated at once and the
+// bisection path is walked through their signs: the same final bracket as 10 sequential bisections.
+template <int NC>
+struct QuadCfg {
+  static constexpr int L = NC <= 8 ? 2 : 4;
+  static constexpr int D = 32 / L;
+  static constexpr int LV = D >= 8 ? 3 : (D >= 4 ? 2 : 1);  // bisection levels per multisection round
+};
+template <bool V1T, bool V2T, int NC>
+__global__ void __launch_bounds__(kScanWarps * 32, 2) k2_scan_q(uint64_t p0, uint64_t np, SolveParams prm,
+                                                               const uint32_t* __restrict__ vrange,
+                                                               double* __restrict__ recs, SolSink S,
+                                                               const uint32_t* __restrict__ clist,
+                                                               const unsigned long long* __restrict__ ccount,
+                                                               uint32_t* __restrict__ plist,
+                                                               unsigned long long* __restrict__ pcount,
+                                                               unsigned long long* __restrict__ next) {
+  using D2 = Deg2<V1T, V2T>;
+  using R = Rec2<V1T, V2T>;
+  using Q = QuadCfg<NC>;
+  constexpr int L = Q::L, ND = Q::D;
+  __shared__ uint32_t pend_s[kScanWarps][kMaxV2];  // pending bisections: j (16) | slot (8) | sign (1)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, q = lane / L;
+  uint32_t* pend = pend_s[warp];
+  uint32_t cnt[C_NUM];
+  for (int i = 0; i < C_NUM; ++i) cnt[i] = 0;
+  const unsigned long long nlist = *ccount;
+  const double P = (double)prm.pieces;
+  while (true) {
+    unsigned long long li = 0;
+    if (lane == 0) li = atomicAdd(next, 1ull);
+    li = __shfl_sync(0xffffffffu, li, 0);
+    if (li >= nlist) break;
+    const uint64_t r = clist[li];
+    double* rec = recs + r * R::STRIDE;
+    const bool ok = rec[H_OK] != 0.0;
+    const int n = (int)rec[H_N];
+    uint32_t flags = (uint32_t)rec[H_FLAGS];
+    int nv = 0;
+    if (ok) {
+      const int da = (int)rec[H_DA], db = (int)rec[H_DB];
+      const double* AT = rec + R::AT;
+      const double* BT = rec + R::BT;
+      const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
+      double slice_terms = 0;
+      for (int i = 0; i <= n; ++i)
+        slice_terms += (i <= da ? D2::DA - i + 1 : 0) + (i <= db ? D2::DB - i + 1 : 0);
+      const double nn = (double)n;
+      const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
+      int ndet = 0;  // determinant evaluations of the sequential algorithm (FLOP model)
+      const int Pi = prm.pieces;
+      int jlo = 0, jhi = Pi;
+      if (vrange) {
+        const uint32_t lo = vrange[2 * (p0 + r)], hi = vrange[2 * (p0 + r) + 1];
+        jlo = max(0, (int)((lo * (uint32_t)Pi) / 32u) - 1);
+        jhi = min(Pi, (int)((hi * (uint32_t)Pi + 31u) / 32u) + 1);
+        if (jhi < jlo) jhi = jlo;
+      }
+      int nprobe = 0, npend = 0;
+      // walk state: sample jc (pending its successor), its sign / log|det|, and the predecessor's log|det|
+      int jc = jlo - 1, s_cur = 0;
+      double lg_cur = -INFINITY, lg_prev = -INFINITY;
+      auto visit = [&](int j, int s_next, double lg_next) {  // decisions of sample j (uniform over the warp)
+        const double nb = fmax(lg_prev, lg_next);
+        if (lg_cur < log(1e-9) + nb) {
+          if (nv < kMaxV2) {
+            if (lane == 0) rec[R::VR + nv] = 2.0 + (double)j / P;
+            nv++;
+            nprobe++;
+          } else {
+            flags |= SPOLY_FLAG_NEAR_TANGENT;
+          }
+        }
+        if (s_cur == 0) {
+          if (nv < kMaxV2) {
+            if (lane == 0) rec[R::VR + nv] = (double)j / P;
+            nv++;
+          } else {
+            flags |= SPOLY_FLAG_TRUNCATED;
+            cnt[C_TRUNCATED]++;
+          }
+        } else if (j < jhi && s_next != 0 && s_next != s_cur) {
+          if (nv < kMaxV2) {
+            if (lane == 0) pend[npend] = ((uint32_t)j << 16) | ((uint32_t)nv << 1) | (s_cur > 0 ? 1u : 0u);
+            npend++;
+            nv++;
+          } else {
+            flags |= SPOLY_FLAG_TRUNCATED;
+            cnt[C_TRUNCATED]++;
+          }
+        }
+      };
+      for (int base = jlo; base <= jhi; base += ND) {
+        const int j = min(base + q, jhi);
+        double lgq;
+        const int sq = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, D2::DB, n, (double)j / P, &lgq);
+#pragma unroll
+        for (int k = 0; k < ND; ++k) {
+          if (base + k > jhi) break;
+          const int sk = __shfl_sync(0xffffffffu, sq, L * k);
+          const double lk = __shfl_sync(0xffffffffu, lgq, L * k);
+          ndet++;
+          if (jc >= jlo) visit(jc, sk, lk);
+          lg_prev = lg_cur;
+          s_cur = sk;
+          lg_cur = lk;
+          jc = base + k;
+        }
+      }
+      visit(jc, 0, -INFINITY);  // the last sample (jc == jhi): no successor
+      __syncwarp();
+      // multisection of the pending sign changes (sequential order of discovery)
+      for (int b = 0; b < npend; ++b) {
+        const uint32_t e = pend[b];
+        const int j = (int)(e >> 16), slot = (int)((e >> 1) & 255u), sc = (e & 1u) ? 1 : -1;
+        double lo = (double)j / P, hi = (double)(j + 1) / P;
+        bool hit = false;
+        for (int it = 0; it < prm.scan_bisect_iters && !hit;) {
+          const int lv = min(Q::LV, prm.scan_bisect_iters - it);
+          const int M = 1 << lv;  // bracket cut into M parts: points 1..M-1
+          // nested midpoints X[0..M] (X[0] = lo, X[M] = hi), as sequential bisection computes them
+          double X[9];
+          X[0] = lo;
+          X[M] = hi;
+#pragma unroll
+          for (int st = 8; st >= 2; st >>= 1) {
+            const int h = st * M / 8;
+            if (h < 2) continue;
+            for (int a = 0; a + h <= M; a += h) X[a + h / 2] = 0.5 * (X[a] + X[a + h]);
+          }
+          const int pi = 1 + (q % (M - 1));  // quads beyond M - 1 repeat a point (results unused)
+          double lgm;
+          const int sm_q = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, D2::DB, n, X[pi], &lgm);
+          int sg[9];
+#pragma unroll
+          for (int k = 1; k < 8; ++k) sg[k] = __shfl_sync(0xffffffffu, sm_q, L * ((k - 1) % ND));
+          // the bisection path through the evaluated points (quad k - 1 evaluated point k)
+          int a = 0, c = M;
+          for (int l = 0; l < lv; ++l) {
+            const int m = (a + c) >> 1;
+            int sv = 0;
+#pragma unroll
+            for (int k = 1; k < 8; ++k)
+              if (k == m) sv = sg[k];
+            ndet++;
+            it++;
+            if (sv == 0) {
+              lo = hi = X[m];
+              hit = true;
+              break;
+            }
+            if (sv == sc)
+              a = m;
+            else
+              c = m;
+          }
+          if (!hit) {
+            lo = X[a];
+            hi = X[c];
+          }
+        }
+        if (lane == 0) rec[R::VR + slot] = 0.5 * (lo + hi);
+      }
+      cnt[C_KFLOP] += (uint32_t)((build_f + ndet * eval_f) * 1e-3);
+      cnt[C_VROOTS] += nv - nprobe;
+    }
+    if (lane == 0) {
+      rec[H_NV] = nv;
+      if (flags) emit_flags(S, p0 + r, flags);
+      if (nv) {
+        const unsigned long long k = atomicAdd(pcount, 1ull);
+        plist[k] = (uint32_t)r;
+      }
+    }
+    __syncwarp();
+  }
+  Grp<32> g;
+  g.lane = lane;
+  g.mask = 0xffffffffu;
   group_counters(g, cnt, S);
 }
 
@@ -1040,6 +1239,8 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr
     const uint64_t np = npairs - p0 < chunk ? npairs - p0 : chunk;
     cudaMemsetAsync(W.ctr, 0, 24 * sizeof(unsigned long long), st);
     const uint64_t gb = (uint64_t)kBuildWarps * (32 / G), gs = (uint64_t)kScanWarps * (32 / G);
+    const uint64_t gs16 = (uint64_t)kScanWarps * 2;  // classes of order <= 16 run two systems per warp
+    const int bs16 = (int)std::min<uint64_t>((np + gs16 - 1) / gs16, (uint64_t)nsm * occ_s);
     const int bb = (int)std::min<uint64_t>((np + gb - 1) / gb, (uint64_t)nsm * occ_b);
     const int bs = (int)std::min<uint64_t>((np + gs - 1) / gs, (uint64_t)nsm * occ_s);
     const int bp = (int)std::min<uint64_t>((np + 127) / 128, (uint64_t)nsm * occ_p);
@@ -1047,14 +1248,37 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr
     k2_bin<V1T, V2T><<<(int)std::min<uint64_t>((np + 255) / 256, (uint64_t)nsm * 8), 256, 0, st>>>(np, W.rec, W.clist,
                                                                                                    cc);
     const uint32_t* L = W.clist;
+#ifdef SPOLY_SCAN_QUAD
+    {  // classes of order <= 16: multi-sample scan, one system per warp (C4: 1.78 -> 2.29 s: the restricted v-ranges
+       // (R25) are short, so most of the D parallel samples and the multisection points are wasted)
+      const int bq = (int)std::min<uint64_t>((np + kScanWarps - 1) / kScanWarps, (uint64_t)nsm * 4);
+      k2_scan_q<V1T, V2T, nc_of_class<G>(0)><<<bq, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan_q<V1T, V2T, nc_of_class<G>(1)><<<bq, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      if (G == 16)
+        k2_scan_q<V1T, V2T, nc_of_class<G>(2)><<<bq, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      else
+        k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
+      if (G != 16) {
+        k2_scan<V1T, V2T, nc_of_class<G>(3)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 3 * np, cc + 3, W.plist, W.ctr + 1, cn + 3);
+        k2_scan<V1T, V2T, nc_of_class<G>(4)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 4 * np, cc + 4, W.plist, W.ctr + 1, cn + 4);
+        k2_scan<V1T, V2T, nc_of_class<G>(5)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 5 * np, cc + 5, W.plist, W.ctr + 1, cn + 5);
+        W.launches += 3;
+        if (D::DB > 32) {
+          k2_scan<V1T, V2T, 0><<<nsm, kScanWarps * 32, sh_big, st>>>(p0, np, prm, vr, W.rec, S, L + 6 * np, cc + 6, W.plist, W.ctr + 1, cn + 6);
+          W.launches += 1;
+        }
+      }
+      W.launches += 3;
+    }
+#else
     if (G == 16) {
       k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
       k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
       k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
       W.launches += 3;
     } else {
-      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
-      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
+      k2_scan<V1T, V2T, nc_of_class<G>(0)><<<bs16, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L, cc, W.plist, W.ctr + 1, cn);
+      k2_scan<V1T, V2T, nc_of_class<G>(1)><<<bs16, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + np, cc + 1, W.plist, W.ctr + 1, cn + 1);
       k2_scan<V1T, V2T, nc_of_class<G>(2)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 2 * np, cc + 2, W.plist, W.ctr + 1, cn + 2);
       k2_scan<V1T, V2T, nc_of_class<G>(3)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 3 * np, cc + 3, W.plist, W.ctr + 1, cn + 3);
       k2_scan<V1T, V2T, nc_of_class<G>(4)><<<bs, kScanWarps * 32, 0, st>>>(p0, np, prm, vr, W.rec, S, L + 4 * np, cc + 4, W.plist, W.ctr + 1, cn + 4);
@@ -1065,6 +1289,7 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr
         W.launches += 1;
       }
     }
+#endif
     k2_path<V1T, V2T><<<bp, 128, 0, st>>>(pq, pt, p0, M.tris, ep, inten, prm, W.rec, S, W.plist, W.ctr + 1);
     W.launches += 3;
   }

@@ -96,6 +96,11 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
   }
 }
 
+// inlined at every call site (an out-of-line copy per (G, K), -DSPOLY_WMUL_INLINE="__device__ __noinline__",
+// measured 10% slower on C4 despite ncu's instruction-fetch stalls)
+#ifndef SPOLY_WMUL_INLINE
+#define SPOLY_WMUL_INLINE __device__ __forceinline__
+#endif
 // c = sum_k s_k a_k b_k  (+ c if acc); every product term with i + j <= c.d is produced.
 // Register-windowed gather (W = 8): a lane owns W consecutive coefficients (i, j0..j0+W-1) of one output row; for
 // every operand row pair (p, i - p) it walks q once, so each a coefficient is loaded once for the W outputs
@@ -103,7 +108,7 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 // FMAs instead of 2 per FMA.  Out-of-row b positions read as 0 (predicated), so the W outputs may share the
 // union of their q ranges.
 template <int G, int K>
-__device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
+SPOLY_WMUL_INLINE void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
   constexpr int W = 8;
   const int dc = c.d;
   int i = 0, j0 = 0;
@@ -127,6 +132,24 @@ __device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], 
         const double* bp = b[kk].c + poff(db, i - p);
         const int qlo = max(0, j0 - blen), qhi = min(j0 + W - 1, da - p);
         if (qlo > qhi) continue;
+#ifndef SPOLY_WMUL_SLIDE
+        // register-blocked: 8 a coefficients x 15 b coefficients -> 64 FMAs per block of q, all register
+        // indices static (no sliding-window moves); positions outside a row read as 0
+        for (int qb = qlo; qb <= qhi; qb += W) {
+          double av[W], bw[2 * W - 1];
+#pragma unroll
+          for (int m = 0; m < W; ++m) av[m] = (qb + m <= qhi) ? ap[qb + m] : 0.0;
+#pragma unroll
+          for (int r = 0; r < 2 * W - 1; ++r) {
+            const int jb = j0 - qb - (W - 1) + r;
+            bw[r] = ((unsigned)jb <= (unsigned)blen) ? bp[jb] : 0.0;
+          }
+#pragma unroll
+          for (int m = 0; m < W; ++m)
+#pragma unroll
+            for (int k = 0; k < W; ++k) t[k] = fma(av[m], bw[k - m + W - 1], t[k]);
+        }
+#else
         double w[W];
 #pragma unroll
         for (int k = 0; k < W; ++k) {
@@ -142,6 +165,7 @@ __device__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], 
           const int jb = j0 - q - 1;  // <= blen - 1 because q >= qlo >= j0 - blen
           w[0] = jb >= 0 ? bp[jb] : 0.0;
         }
+#endif
       }
 #pragma unroll
       for (int k = 0; k < W; ++k) out[k] = fma(s[kk], t[k], out[k]);
@@ -378,6 +402,120 @@ __device__ int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* B
   if (n <= 24) return wdet_rows<G, 24>(g, as, bs, aj1, bj1, n, lg);
   if (n <= 28) return wdet_rows<G, 28>(g, as, bs, aj1, bj1, n, lg);
   return wdet_rows<G, 32>(g, as, bs, aj1, bj1, n, lg);
+}
+
+// Several determinants per warp (the scan's samples of one system): L lanes per determinant ("quad" for L = 4),
+// D = 32 / L determinants at once, lane t of a quad holding the columns r = t + L k (k < NC / L) of the symmetric
+// Bezout matrix in registers.  The arithmetic per matrix entry is the same as wdet_rows' (slices by rowT, the
+// Chionh recurrence, virtual partial pivoting on the quantised |x| with the lowest row on ties, one fma per entry
+// and step), so every determinant's sign and log|det| are those wdet_rows computes; the communication per
+// shuffle instruction serves D determinants instead of one.  All quads execute every step (n is the system's, so
+// uniform); a quad whose determinant hit a zero pivot keeps stepping with its result frozen.
+// a == b ? x : y through PTX selp (a plain select chain over a register array is turned into a dynamically
+// indexed local-memory load by the compiler)
+__device__ __forceinline__ double sel_eq(int a, int b, double x, double y) {
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.eq.s32 p, %1, %2;\n\tselp.f64 %0, %3, %4, p;\n\t}"
+      : "=d"(r) : "r"(a), "r"(b), "d"(x), "d"(y));
+  return r;
+}
+
+template <int L, int NC, int NR>
+__device__ __noinline__ int wdet_quad(const double* __restrict__ AT, int DA, const double* __restrict__ BT, int DB, int n, double v,
+                         double* lg) {
+  constexpr int RPL = (NC + L - 1) / L;   // columns per lane
+  constexpr int SPL = (NC + L) / L;       // slices 0..NC per lane (i = t + L k)
+  const int lane = threadIdx.x & 31, t = lane % L, qb = lane - t;
+  // slices a_i(v), b_i(v), i = t + L k <= NC (rows >= NR are absent: zero)
+  double sa[SPL], sb[SPL];
+#pragma unroll
+  for (int k = 0; k < SPL; ++k) {
+    const int i = t + L * k;
+    const bool have = i <= NC && i < NR;
+    sa[k] = have ? rowT<NR>(AT, DA, have ? i : 0, v) : 0.0;
+    sb[k] = have ? rowT<NR>(BT, DB, have ? i : 0, v) : 0.0;
+  }
+  // a_{r+1}, b_{r+1} of each own column r = t + L k: slice r + 1 lives on lane (t + 1) % L, slot k (+1 if t = L-1)
+  double aj1[RPL], bj1[RPL];
+#pragma unroll
+  for (int k = 0; k < RPL; ++k) {
+    const int src = qb + (t + 1) % L;
+    const double xa = __shfl_sync(0xffffffffu, sa[k], src), xb = __shfl_sync(0xffffffffu, sb[k], src);
+    const double ya = (k + 1 < SPL) ? __shfl_sync(0xffffffffu, sa[k + 1 < SPL ? k + 1 : k], src) : 0.0;
+    const double yb = (k + 1 < SPL) ? __shfl_sync(0xffffffffu, sb[k + 1 < SPL ? k + 1 : k], src) : 0.0;
+    aj1[k] = (t + 1 < L) ? xa : ya;
+    bj1[k] = (t + 1 < L) ? xb : yb;
+  }
+  double col[RPL][NC];
+#pragma unroll
+  for (int i = 0; i < NC; ++i) {
+    const double ai = __shfl_sync(0xffffffffu, sa[i / L], qb + i % L);
+    const double bi = __shfl_sync(0xffffffffu, sb[i / L], qb + i % L);
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      // B_{i-1, r+1}: entry i - 1 of column r + 1 (lane (t + 1) % L, slot k, or slot k + 1 from lane 0)
+      double prev = 0.0;
+      if (i > 0) {
+        const int src = qb + (t + 1) % L;
+        const double x = __shfl_sync(0xffffffffu, col[k][i - 1], src);
+        const double y = (k + 1 < RPL) ? __shfl_sync(0xffffffffu, col[k + 1 < RPL ? k + 1 : k][i - 1], src) : 0.0;
+        prev = (t + 1 < L) ? x : y;
+      }
+      const int r = t + L * k;
+      if (i == 0 || r + 1 >= n) prev = 0.0;
+      col[k][i] = (i < n) ? prev + (ai * bj1[k] - bi * aj1[k]) : 0.0;
+    }
+  }
+  unsigned used = 0u;
+  int sign = 1, dead = 0;
+  double mant = 1.0;
+  int ex = 0;
+#pragma unroll
+  for (int c = 0; c < NC; ++c) {
+    if (c >= n) continue;  // uniform: n is the system's (no break: keeps the loop fully unrolled)
+    bool cand[RPL];
+    unsigned key = 0u;
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) {
+      const int r = t + L * k;
+      cand[k] = r < n && !((used >> r) & 1u);
+      if (cand[k]) key = max(key, (((unsigned)__double2hiint(fabs(col[k][c]))) & ~31u) | (unsigned)(31 - r));
+    }
+#pragma unroll
+    for (int o = 1; o < L; o <<= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+    if ((key >> 5) == 0u) dead = 1;
+    const int p = 31 - (int)(key & 31u);
+    const int owner = qb + p % L, kp = p / L;
+    double sel = col[0][c];
+#pragma unroll
+    for (int k = 1; k < RPL; ++k) sel = sel_eq(kp, k, col[k][c], sel);
+    const double piv = __shfl_sync(0xffffffffu, sel, owner);
+    if (!dead) {
+      if ((__popc(~used & ((1u << p) - 1u)) & 1) ^ (piv < 0)) sign = -sign;
+      mant *= fabs(piv);
+      renorm(mant, ex);
+      used |= 1u << p;
+    }
+    const double rp = dead ? 0.0 : fast_rcp(piv);
+    double lm[RPL];
+#pragma unroll
+    for (int k = 0; k < RPL; ++k) lm[k] = (cand[k] && t + L * k != p && !dead) ? col[k][c] * rp : 0.0;
+#pragma unroll
+    for (int jj = c + 1; jj < NC; ++jj) {
+      double sj = col[0][jj];
+#pragma unroll
+      for (int k = 1; k < RPL; ++k) sj = sel_eq(kp, k, col[k][jj], sj);
+      const double pj = __shfl_sync(0xffffffffu, sj, owner);
+#pragma unroll
+      for (int k = 0; k < RPL; ++k) col[k][jj] = fma(-lm[k], pj, col[k][jj]);
+    }
+  }
+  if (dead) {
+    *lg = -INFINITY;
+    return 0;
+  }
+  *lg = log(mant) + ex * 0.69314718055994530942;
+  return sign;
 }
 
 // Same determinant for n > G (rare: numerical TT orders above 32): matrix in the shared-memory scratch M
