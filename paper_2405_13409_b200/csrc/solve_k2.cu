@@ -69,6 +69,7 @@ struct Deg2 {
 struct Sys2w {
   WP a, b, U, V, K;
   double eta0, eta1, eta2;
+  int tb;  // b's effective total degree (reading R29)
   bool relabel;
   uint32_t flags;
   int da, db, n;
@@ -297,6 +298,20 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   S.da = g.imax(da);
   S.db = g.imax(db);
   S.n = max(S.da, S.db);
+#ifdef SPOLY_NO_TB
+  S.tb = S.b.d;
+#else
+  {
+    // reading R29: b's effective total degree T: its terms of total degree above T are bounded, on |u|, |v| <= 1.1,
+    // by 2^-56 of max |b_ij| (= 1 after the normalisation); the scan evaluates each row only up to T
+    double* mb = ar.raw(S.b.d + 1);
+    wmass(g, S.b, mb);
+    double tail;
+    S.tb = trunc_degree(mb, S.b.d, 0x1p-56, &tail);
+    g.sync();
+    ar.top = mark;
+  }
+#endif
   if (S.n == 0) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
@@ -444,7 +459,7 @@ struct Rec2 {
   static constexpr int K = V + tri_n(D::DU);
   static constexpr int STRIDE = (K + tri_n(D::DK) + 7) & ~7;
 };
-enum { H_ETA0 = 0, H_ETA1, H_ETA2, H_RELABEL, H_FLAGS, H_DA, H_DB, H_N, H_OK, H_NV };
+enum { H_ETA0 = 0, H_ETA1, H_ETA2, H_RELABEL, H_FLAGS, H_DA, H_DB, H_N, H_OK, H_NV, H_TB };
 constexpr int kMaxSol2 = 8;  // admissible chains kept per pair (more: SPOLY_FLAG_TRUNCATED)
 
 __device__ __forceinline__ void load_chain(const TriRec* __restrict__ tris, const uint32_t* __restrict__ pt,
@@ -475,6 +490,14 @@ __device__ __forceinline__ void group_counters(const Grp<G>& g, const uint32_t* 
 
 // ---- kernel 1: coefficient phase (group per pair, shared-memory arena), record write
 constexpr int kBuildWarps = 2;
+template <bool V1T, bool V2T>
+__host__ __device__ constexpr int build_group() {
+#ifdef SPOLY_BUILD_G16
+  return 16;
+#else
+  return Deg2<V1T, V2T>::G;
+#endif
+}
 #ifndef SPOLY_BUILD_MINB
 #define SPOLY_BUILD_MINB 4  // 4 x 64 threads: up to 255 registers (5 blocks fit the TT arena but cap them at 168: spills)
 #endif
@@ -487,7 +510,7 @@ __global__ void __launch_bounds__(kBuildWarps * 32, SPOLY_BUILD_MINB) k2_build(c
                                                             unsigned long long* __restrict__ next) {
   using D = Deg2<V1T, V2T>;
   using R = Rec2<V1T, V2T>;
-  constexpr int G = D::G, GPW = 32 / G;
+  constexpr int G = build_group<V1T, V2T>(), GPW = 32 / G;
   extern __shared__ double smem[];
   const int warp = threadIdx.x >> 5, gi = (threadIdx.x & 31) / G;
   Grp<G> g;
@@ -520,6 +543,7 @@ __global__ void __launch_bounds__(kBuildWarps * 32, SPOLY_BUILD_MINB) k2_build(c
       rec[H_N] = ok ? Sy.n : 0;
       rec[H_OK] = ok ? 1.0 : 0.0;
       rec[H_NV] = 0.0;
+      rec[H_TB] = ok ? Sy.tb : 0;
     }
     if (ok) {
       cnt[C_SYSTEMS]++;
@@ -640,16 +664,17 @@ __global__ void __launch_bounds__(kScanWarps * 32, scan_min_blocks(NC)) k2_scan(
       // RR 17k, RT 40k, TR 150k, TT 400k) + per determinant evaluation: slices 2 (sum of the
       // a_i, b_i lengths, i <= n) + Chionh 3 n^2 + GE (2/3) n^3
       const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
+      const int tb = (int)rec[H_TB];  // b's total degree after the cut (reading R29): row l has tb - l + 1 terms
       double slice_terms = 0;
       for (int i = 0; i <= n; ++i)
-        slice_terms += (i <= da ? D::DA - i + 1 : 0) + (i <= db ? D::DB - i + 1 : 0);
+        slice_terms += (i <= da ? D::DA - i + 1 : 0) + (i <= db && i <= tb ? tb - i + 1 : 0);
       const double nn = (double)n;
       const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
       double kflop_acc = build_f;
       auto det = [&](double v, double* lg) -> int {
         kflop_acc += eval_f;
-        if (BIG) return wdet_sign_smem<G, R::NR>(g, AT, D::DA, BT, D::DB, n, v, lg, scratch, scratch + 2 * (n + 2));
-        return wdet_T<G, R::NR, NC>(g, AT, D::DA, BT, D::DB, n, v, lg);
+        if (BIG) return wdet_sign_smem<G, R::NR>(g, AT, D::DA, BT, tb, n, v, lg, scratch, scratch + 2 * (n + 2));
+        return wdet_T<G, R::NR, NC>(g, AT, D::DA, BT, tb, n, v, lg);
       };
       const int P = prm.pieces;
       // reading R25: only the pieces that overlap the v-range of T_1's surviving cull cells, +1 piece each side
@@ -779,9 +804,10 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) k2_scan_q(uint64_t p0, uin
       const double* AT = rec + R::AT;
       const double* BT = rec + R::BT;
       const double build_f = (!V1T && !V2T) ? 17e3 : (!V1T ? 40e3 : (!V2T ? 150e3 : 400e3));
+      const int tb = (int)rec[H_TB];
       double slice_terms = 0;
       for (int i = 0; i <= n; ++i)
-        slice_terms += (i <= da ? D2::DA - i + 1 : 0) + (i <= db ? D2::DB - i + 1 : 0);
+        slice_terms += (i <= da ? D2::DA - i + 1 : 0) + (i <= db && i <= tb ? tb - i + 1 : 0);
       const double nn = (double)n;
       const double eval_f = 2.0 * slice_terms + 3.0 * nn * nn + (2.0 / 3.0) * nn * nn * nn;
       int ndet = 0;  // determinant evaluations of the sequential algorithm (FLOP model)
@@ -830,7 +856,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) k2_scan_q(uint64_t p0, uin
       for (int base = jlo; base <= jhi; base += ND) {
         const int j = min(base + q, jhi);
         double lgq;
-        const int sq = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, D2::DB, n, (double)j / P, &lgq);
+        const int sq = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, tb, n, (double)j / P, &lgq);
 #pragma unroll
         for (int k = 0; k < ND; ++k) {
           if (base + k > jhi) break;
@@ -867,7 +893,7 @@ __global__ void __launch_bounds__(kScanWarps * 32, 2) k2_scan_q(uint64_t p0, uin
           }
           const int pi = 1 + (q % (M - 1));  // quads beyond M - 1 repeat a point (results unused)
           double lgm;
-          const int sm_q = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, D2::DB, n, X[pi], &lgm);
+          const int sm_q = wdet_quad<L, NC, R::NR>(AT, D2::DA, BT, tb, n, X[pi], &lgm);
           int sg[9];
 #pragma unroll
           for (int k = 1; k < 8; ++k) sg[k] = __shfl_sync(0xffffffffu, sm_q, L * ((k - 1) % ND));
@@ -1218,7 +1244,7 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr
   using D = Deg2<V1T, V2T>;
   using R = Rec2<V1T, V2T>;
   constexpr int G = D::G;
-  const size_t sh_build = (size_t)kBuildWarps * (32 / G) * D::ARENA * sizeof(double);
+  const size_t sh_build = (size_t)kBuildWarps * (32 / build_group<V1T, V2T>()) * D::ARENA * sizeof(double);
   const size_t sh_big = (size_t)kScanWarps * (32 / G) * (2 * (R::NR + 2) + R::NR * R::NR) * sizeof(double);
   // the attribute is per device: set it on every launch (cheap; a process-wide "done" flag would skip it on a
   // second context's device, and is not thread-safe)
@@ -1238,7 +1264,7 @@ static void launch_k2(const uint32_t* pq, const uint32_t* pt, const uint32_t* vr
   for (uint64_t p0 = 0; p0 < npairs; p0 += chunk) {
     const uint64_t np = npairs - p0 < chunk ? npairs - p0 : chunk;
     cudaMemsetAsync(W.ctr, 0, 24 * sizeof(unsigned long long), st);
-    const uint64_t gb = (uint64_t)kBuildWarps * (32 / G), gs = (uint64_t)kScanWarps * (32 / G);
+    const uint64_t gb = (uint64_t)kBuildWarps * (32 / build_group<V1T, V2T>()), gs = (uint64_t)kScanWarps * (32 / G);
     const uint64_t gs16 = (uint64_t)kScanWarps * 2;  // classes of order <= 16 run two systems per warp
     const int bs16 = (int)std::min<uint64_t>((np + gs16 - 1) / gs16, (uint64_t)nsm * occ_s);
     const int bb = (int)std::min<uint64_t>((np + gb - 1) / gb, (uint64_t)nsm * occ_b);

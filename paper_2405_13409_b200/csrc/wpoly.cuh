@@ -119,7 +119,7 @@ SPOLY_WMUL_INLINE void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&
     double out[W];
 #pragma unroll
     for (int k = 0; k < W; ++k) out[k] = (acc && j0 + k < rowlen) ? cp[j0 + k] : 0.0;
-#pragma unroll
+#pragma unroll  // (rolled, the operand descriptors go to local memory: C4 build +8%)
     for (int kk = 0; kk < K; ++kk) {
       const int da = a[kk].d, db = b[kk].d;
       double t[W];
@@ -297,6 +297,45 @@ __device__ __forceinline__ double* wmovev(const Grp<G>& g, WV& V, double* dst) {
   return dst + tri_n(V.z.d);
 }
 
+// ------------------------------------------------------------------ total-degree mass bounds (reading R29)
+// m[s] = sum_{i+j=s} |c_ij|, s = 0..p.d (lane s; a sum of products obeys m_{ab}[s] <= sum m_a[s1] m_b[s - s1])
+template <int G>
+__device__ __forceinline__ void wmass(const Grp<G>& g, const WP& p, double* m) {
+  for (int s = g.lane; s <= p.d; s += G) {
+    double t = 0.0;
+    for (int i = 0; i <= s; ++i) t += fabs(p.c[poff(p.d, i) + s - i]);
+    m[s] = t;
+  }
+  g.sync();
+}
+// out[s] = sum_{s1} x[s1] y[s - s1], s = 0..nx + ny (upper bound of the product's masses)
+template <int G>
+__device__ __forceinline__ void mconv(const Grp<G>& g, double* out, const double* x, int nx, const double* y, int ny) {
+  for (int s = g.lane; s <= nx + ny; s += G) {
+    double t = 0.0;
+    for (int s1 = max(0, s - ny); s1 <= min(s, nx); ++s1) t = fma(x[s1], y[s - s1], t);
+    out[s] = t;
+  }
+  g.sync();
+}
+// smallest T with sum_{s > T} m[s] 1.1^s <= thr (the dropped terms' bound on |u|, |v| <= 1.1, the back-substitution
+// range); *tail receives that bound for T.  Uniform over the group (every lane scans m).
+__device__ __forceinline__ int trunc_degree(const double* m, int d, double thr, double* tail) {
+  double w = 1.0;
+  for (int s = 0; s < d; ++s) w *= 1.1;  // 1.1^d
+  double acc = 0.0;
+  int T = d;
+  for (int s = d; s >= 1; --s) {
+    const double nacc = acc + m[s] * w;
+    if (!(nacc <= thr)) break;
+    acc = nacc;
+    T = s - 1;
+    w *= 1.0 / 1.1;
+  }
+  *tail = acc;
+  return T;
+}
+
 // ------------------------------------------------------------------ scalar evaluation (one lane)
 __device__ __forceinline__ double wp_row(const WP& p, int i, double v) {  // sum_j c_ij v^j
   const double* r = p.c + poff(p.d, i);
@@ -371,9 +410,10 @@ __device__ int wdet_rows(const Grp<G>& g, double as, double bs, double aj1, doub
 
 // slice of row l at v from a transposed coefficient block AT[j * NR + l] (zero beyond the row)
 template <int NR>
+// D: the polynomial's total degree, so row l holds the terms j <= D - l (higher positions are structural zeros)
 __device__ __forceinline__ double rowT(const double* __restrict__ AT, int D, int l, double v) {
   double s = 0.0;
-  for (int j = D; j >= 0; --j) s = fma(s, v, __ldg(AT + j * NR + l));
+  for (int j = D - l; j >= 0; --j) s = fma(s, v, __ldg(AT + j * NR + l));
   return s;
 }
 
