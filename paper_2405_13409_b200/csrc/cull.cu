@@ -59,9 +59,8 @@ __device__ __forceinline__ bool test_cluster(f3 x0, f3 x2, const ClusterRec& C, 
 // product of two barycentric-linear functions, so its triangle-Bernstein control points are
 // A_ii (corners) and (A_ij + A_ji)/2 (edges) with A_ij = ((p_i - x0) x w) . n_j, w = x2 - x0.  A strict
 // common sign beyond 1e-3 sum|A| (FP32 errors are ~1e-6 relative) proves a != 0 on the triangle: no chain.
-__device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
-  const float4* r = tris[t].r;
-  const float4 a = __ldg(r), b = __ldg(r + 1), c = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+__device__ __forceinline__ bool coplanar_keep_r(const float4 a, const float4 b, const float4 c, const float4 d,
+                                                const float4 e, f3 x0, f3 x2) {
   const f3 w = x2 - x0;
   const f3 c0 = crossf(f3{a.x, a.y, a.z} - x0, w), c1 = crossf(f3{a.w, b.x, b.y} - x0, w),
            c2 = crossf(f3{b.z, b.w, c.x} - x0, w);
@@ -74,6 +73,10 @@ __device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, u
   const bool neg = a00 < -m && a11 < -m && a22 < -m && e01 < -m && e02 < -m && e12 < -m;
   return !(pos || neg);
 }
+__device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
+  const float4* r = tris[t].r;
+  return coplanar_keep_r(__ldg(r), __ldg(r + 1), __ldg(r + 2), __ldg(r + 3), __ldg(r + 4), x0, x2);
+}
 
 // Product-form sign test (exact condition, FP32 with margin; reading R21): every admissible
 // reflection zeroes b = (d0.n)(d1.t) + (d0.t)(d1.n) (Eq. 12) for ANY tangent field t perpendicular to n, here
@@ -83,9 +86,8 @@ __device__ __forceinline__ bool coplanar_keep(const TriRec* __restrict__ tris, u
 // rule of Bernstein polynomials.  A strict common sign beyond 1e-4 of the term-magnitude bound
 // M = max|d0| max|n| max|d1| max|t| + max|d0| max|t| max|d1| max|n| (FP32 errors are ~1e-6 M) proves b != 0
 // on the closed triangle: no reflection chain, the pair is dropped.
-__device__ __forceinline__ bool bprod_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
-  const float4* r = tris[t].r;
-  const float4 a = __ldg(r), b = __ldg(r + 1), c4 = __ldg(r + 2), d = __ldg(r + 3), e = __ldg(r + 4);
+__device__ __forceinline__ bool bprod_keep_r(const float4 a, const float4 b, const float4 c4, const float4 d,
+                                             const float4 e, f3 x0, f3 x2) {
   const f3 p[3] = {{a.x, a.y, a.z}, {a.w, b.x, b.y}, {b.z, b.w, c4.x}};
   const f3 n[3] = {{c4.y, c4.z, c4.w}, {d.x, d.y, d.z}, {d.w, e.x, e.y}};
   const f3 e1 = p[1] - p[0];
@@ -137,6 +139,10 @@ __device__ __forceinline__ bool bprod_keep(const TriRec* __restrict__ tris, uint
     neg = neg && c[k] < -m;
   }
   return !(pos || neg);
+}
+__device__ __forceinline__ bool bprod_keep(const TriRec* __restrict__ tris, uint32_t t, f3 x0, f3 x2) {
+  const float4* r = tris[t].r;
+  return bprod_keep_r(__ldg(r), __ldg(r + 1), __ldg(r + 2), __ldg(r + 3), __ldg(r + 4), x0, x2);
 }
 
 template <bool REFRACT>
@@ -422,6 +428,63 @@ __global__ void __launch_bounds__(256) k_query_cull(const double* __restrict__ e
   }
 }
 
+// Tile-major form of the same per-query cull (default; SPOLY_QC_QUERY_MAJOR builds the query-major one above): one
+// warp per tile of 32 Morton-sorted queries, lane = candidate triangle of the tile's list, its cull node and record
+// loaded once into registers and tested against every query of the tile (the query-major form loaded them once
+// per query).  Same predicate per (query, triangle), same mask layout and counts.
+template <bool REFRACT>
+__global__ void __launch_bounds__(256) k_tile_query_cull(const double* __restrict__ ep, uint32_t nq,
+                                                         const uint32_t* __restrict__ order,
+                                                         const TriCull* __restrict__ tc,
+                                                         const TriRec* __restrict__ tris, float ef, float eb,
+                                                         uint32_t cap, const uint32_t* __restrict__ tile_list,
+                                                         const uint32_t* __restrict__ tile_count, uint32_t* counts,
+                                                         uint32_t* __restrict__ masks) {
+  __shared__ float sx[8][32][6];
+  __shared__ uint32_t sq[8][32];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nw = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t words = (cap + 31) / 32;
+  const uint32_t ntiles = (nq + 31) / 32;
+  constexpr uint32_t S = 8;  // warps per tile: warp (t, sub) takes the tile's candidate blocks sub, sub + S, ...
+  for (uint32_t vw = gw; vw < ntiles * S; vw += nw) {
+    const uint32_t t = vw / S, sub = vw % S;
+    const uint32_t n = tile_count[t];
+    if (sub * 32 >= n) continue;  // warp-uniform
+    const int nqt = (int)min(32u, nq - t * 32);
+    __syncwarp();
+    if (lane < nqt) {
+      const uint32_t q = order[t * 32 + lane];
+      const double* e = ep + 6ull * q;
+#pragma unroll
+      for (int c = 0; c < 6; ++c) sx[wib][lane][c] = (float)e[c];
+      sq[wib][lane] = q;
+    }
+    __syncwarp();
+    const uint32_t* list = tile_list + (uint64_t)t * cap;
+    uint32_t cnt = 0;  // lane qi's query count (this warp's blocks)
+    for (uint32_t b = sub * 32; b < n; b += 32 * S) {
+      const uint32_t j = b + lane;
+      const bool have = j < n;
+      const uint32_t tri = have ? list[j] : list[0];
+      const TriCull C = tc[tri];
+      const float4* r = tris[tri].r;
+      const float4 r0 = __ldg(r), r1 = __ldg(r + 1), r2 = __ldg(r + 2), r3 = __ldg(r + 3), r4 = __ldg(r + 4);
+      for (int qi = 0; qi < nqt; ++qi) {
+        const f3 x0 = {sx[wib][qi][0], sx[wib][qi][1], sx[wib][qi][2]};
+        const f3 x2 = {sx[wib][qi][3], sx[wib][qi][4], sx[wib][qi][5]};
+        bool k = have && test_tri<REFRACT>(x0, x2, C, ef, eb) && coplanar_keep_r(r0, r1, r2, r3, r4, x0, x2);
+        if (!REFRACT && k) k = bprod_keep_r(r0, r1, r2, r3, r4, x0, x2);  // reading R21
+        const unsigned m = __ballot_sync(0xffffffffu, k);
+        if (lane == 0) masks[(uint64_t)sq[wib][qi] * words + b / 32] = m;
+        if (lane == qi) cnt += __popc(m);
+      }
+    }
+    if (lane < nqt && cnt) atomicAdd(counts + sq[wib][lane], cnt);
+  }
+}
+
 __global__ void __launch_bounds__(256) k_query_expand(uint32_t nq, const uint32_t* __restrict__ order, uint32_t cap,
                                                       const uint32_t* __restrict__ tile_list,
                                                       const uint32_t* __restrict__ tile_count,
@@ -462,9 +525,25 @@ void launch_query_cull(int pass, const double* ep, uint32_t nq, const uint32_t* 
 #endif
   uint64_t capb = (uint64_t)nsm * SPOLY_QC_GRID;
   const int blocks = (int)(want < capb ? want : capb);
-  if (pass == 1)
+  if (pass == 1) {
     k_query_expand<<<blocks, threads, 0, st>>>(nq, order, cap, tile_list, tile_count, masks, offsets, pq, pt);
-  else if (refract)
+    return;
+  }
+#ifndef SPOLY_QC_QUERY_MAJOR
+  {
+    const uint64_t wt = ((uint64_t)(nq + 31) / 32 * 8 * 32 + threads - 1) / threads, ct = (uint64_t)nsm * 32;
+    const int bt = (int)(wt < ct ? wt : ct);
+    cudaMemsetAsync(counts, 0, sizeof(uint32_t) * nq, st);
+    if (refract)
+      k_tile_query_cull<true><<<bt, threads, 0, st>>>(ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
+                                                       tile_list, tile_count, counts, masks);
+    else
+      k_tile_query_cull<false><<<bt, threads, 0, st>>>(ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
+                                                        tile_list, tile_count, counts, masks);
+    return;
+  }
+#endif
+  if (refract)
     k_query_cull<true><<<blocks, threads, 0, st>>>(ep, nq, order, M.tcull, M.tris, M.eta_front, M.eta_back, cap,
                                                     tile_list, tile_count, counts, masks);
   else
@@ -1264,13 +1343,14 @@ __device__ __forceinline__ SubBf sub_bound_f(const f3 P[3], const f3 N[3], float
     return B;
   }
   B.ax = rsqrtf(sl2) * s;
-  float sb = 0.f;
+  float sb2 = 0.f;
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     if (!(dotf(M[j], B.ax) > 2e-3f)) B.ok = false;
-    sb = fmaxf(sb, fnorm(crossf(M[j], B.ax)));
+    const f3 x = crossf(M[j], B.ax);
+    sb2 = fmaxf(sb2, dotf(x, x));
   }
-  B.sinb = fminf(1.f, sb + 4e-6f);
+  B.sinb = fminf(1.f, sqrtf(sb2) + 4e-6f);
   return B;
 }
 
@@ -1292,10 +1372,15 @@ __device__ __forceinline__ bool exact_cone_f(const f3 (&d)[M], const float (&S)[
   const float sl2 = dotf(s, s);
   if (!(sl2 > 1e-12f)) return false;
   axis = rsqrtf(sl2) * s;
-  float c = 0.f;
+  // max_j (|w_j - axis| + er_j) <= sqrt(max_j |w_j - axis|^2) + max_j er_j: one square root
+  float c2 = 0.f, em = 0.f;
 #pragma unroll
-  for (int j = 0; j < M; ++j) c = fmaxf(c, fnorm(w[j] - axis) + er[j]);
-  chord = c * (1.f + 1e-5f) + 2e-6f;
+  for (int j = 0; j < M; ++j) {
+    const f3 t = w[j] - axis;
+    c2 = fmaxf(c2, dotf(t, t));
+    em = fmaxf(em, er[j]);
+  }
+  chord = (sqrtf(c2) + em) * (1.f + 1e-5f) + 2e-6f;
   return true;
 }
 

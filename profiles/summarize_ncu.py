@@ -1,7 +1,8 @@
 import csv, json, sys, collections
 rep, launches, tag = sys.argv[1], sys.argv[2], sys.argv[3]
 import subprocess
-raw = subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], stderr=subprocess.DEVNULL).decode()
+raw = (open(rep).read() if rep.endswith(".csv") else  # a `--page raw --csv` export, or the .ncu-rep itself
+       subprocess.check_output(["ncu", "-i", rep, "--page", "raw", "--csv"], stderr=subprocess.DEVNULL).decode())
 rows = list(csv.reader(raw.splitlines())); h = rows[0]; u = rows[1]
 keys = ['gpu__time_duration.sum','dram__bytes_read.sum','dram__bytes_write.sum',
         'smsp__thread_inst_executed_per_inst_executed.ratio','sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active',
@@ -43,12 +44,13 @@ for k, v in sorted(agg.items(), key=lambda kv: -sum(kv[1])):
 print("\n".join(lines))
 return_json = sys.argv[4] if len(sys.argv) > 4 else None
 if return_json:
-    # bench.py reports the path phase (k1_cand + k1_path launches) under "k1_path<..>": its traffic is the sum
+    # bench.py reports the path phase (k1_path_fast + k1_path launches) under "k1_path<..>": its traffic is the sum
     for ch in ("R", "T"):
-        if "k1_cand" in out and f"k1_path<{ch}>" in out:
-            c, pth = out["k1_cand"], out[f"k1_path<{ch}>"]
-            out[f"k1_path<{ch}>"] = dict(pth, dram_bytes_per_launch=c["dram_bytes_per_launch"] + pth["dram_bytes_per_launch"],
-                                        duration_ms_ncu=c["duration_ms_ncu"] + pth["duration_ms_ncu"],
-                                        note="phase = k1_cand + k1_path launches")
+        fast = out.get(f"k1_path_fast<{ch}>")
+        if fast is not None:
+            pth = out.get(f"k1_path<{ch}>", {"dram_bytes_per_launch": 0.0, "duration_ms_ncu": 0.0})
+            out[f"k1_path<{ch}>"] = dict(fast, dram_bytes_per_launch=fast["dram_bytes_per_launch"] + pth["dram_bytes_per_launch"],
+                                        duration_ms_ncu=fast["duration_ms_ncu"] + pth["duration_ms_ncu"],
+                                        note="phase = k1_path_fast + k1_path launches")
     out["_note"] = "dram__bytes_read.sum + dram__bytes_write.sum per launch, one ncu --set full capture at the C2 bench config (" + tag + ")"
     json.dump(out, open(return_json, 'w'), indent=1)
