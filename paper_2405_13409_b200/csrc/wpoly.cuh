@@ -98,6 +98,9 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 
 // inlined at every call site (an out-of-line copy per (G, K), -DSPOLY_WMUL_INLINE="__device__ __noinline__",
 // measured 10% slower on C4 despite ncu's instruction-fetch stalls)
+#ifndef SPOLY_WMUL_W
+#define SPOLY_WMUL_W 8  // output coefficients per lane chunk (A/B: 4)
+#endif
 #ifndef SPOLY_WMUL_INLINE
 #define SPOLY_WMUL_INLINE __device__ __forceinline__
 #endif
@@ -109,7 +112,7 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 // union of their q ranges.
 template <int G, int K>
 SPOLY_WMUL_INLINE void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
-  constexpr int W = 8;
+  constexpr int W = SPOLY_WMUL_W;
   const int dc = c.d;
   int i = 0, j0 = 0;
   tadv<W>(dc, g.lane, i, j0);
