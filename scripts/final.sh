@@ -15,7 +15,7 @@ $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $T/l
   python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-e2e > $T/launches_C2.log 2>&1
 $NCU --metrics gpu__time_duration.sum --clock-control none --csv --log-file $T/launches_C4.csv \
   python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $T/launches_C4.log 2>&1
-$NCU --set full --clock-control none --import-source on -k regex:"k1_phase1|k1_path_fast|k_query_cull|k_tile_cull|k1_path<|k1_roots_deep" -c 12 \
+$NCU --set full --clock-control none --import-source on -k regex:"k1_phase1|k1_path_fast|k_tile_query_cull|k_tile_cull|k1_roots_deep" -c 12 \
   -o /tmp/k1f -f python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-e2e > $T/k1_full.log 2>&1
 $NCU -i /tmp/k1f.ncu-rep --page raw --csv > $T/k1_full.raw.csv 2>/dev/null
 $NCU -i /tmp/k1f.ncu-rep --page details > $T/k1_full.details.txt 2>/dev/null
