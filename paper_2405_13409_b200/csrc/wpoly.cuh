@@ -110,9 +110,9 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 // and the b operands slide through a W-register window (one new load per step): 2 shared-memory loads per W
 // FMAs instead of 2 per FMA.  Out-of-row b positions read as 0 (predicated), so the W outputs may share the
 // union of their q ranges.
-template <int G, int K>
-SPOLY_WMUL_INLINE void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K], bool acc) {
-  constexpr int W = SPOLY_WMUL_W;
+template <int G, int K, int W>
+SPOLY_WMUL_INLINE void wmul_w(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
+                              bool acc) {
   const int dc = c.d;
   int i = 0, j0 = 0;
   tadv<W>(dc, g.lane, i, j0);
@@ -179,6 +179,22 @@ SPOLY_WMUL_INLINE void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&
     tadv<W>(dc, G, i, j0);
   }
   g.sync();
+}
+// outputs with few coefficients use 4-wide chunks, so more lanes get one (the build's small products left most of
+// the group idle with 8-wide chunks); the large products keep 8-wide register blocks
+template <int G, int K>
+__device__ __forceinline__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
+                                     bool acc) {
+#ifndef SPOLY_WMUL_SMALL_DC
+#define SPOLY_WMUL_SMALL_DC 12  // A/B on C4: none 1.81 s, 12 1.73 s, 20 1.74 s (outputs bit-identical)
+#endif
+#if SPOLY_WMUL_SMALL_DC > 0
+  if (c.d < SPOLY_WMUL_SMALL_DC) {
+    wmul_w<G, K, 4>(g, c, a, b, s, acc);
+    return;
+  }
+#endif
+  wmul_w<G, K, SPOLY_WMUL_W>(g, c, a, b, s, acc);
 }
 template <int G>
 __device__ __forceinline__ void wmul1(const Grp<G>& g, WP c, WP a, WP b, double s, bool acc) {
