@@ -20,8 +20,23 @@
 #include "wpoly.cuh"
 
 #include <algorithm>
+#include <cstdio>
 
 namespace spoly {
+
+#ifdef SPOLY_PROF_BUILD  // section timing of the two-bounce build (clock64 per system, lane 0; diagnostic only)
+__device__ unsigned long long g_bprof[16];
+#define BPROF_INIT long long bprof_t = clock64();
+#define BPROF(k)                                                   \
+  do {                                                             \
+    const long long bprof_n = clock64();                           \
+    if (g.lane == 0) atomicAdd(&g_bprof[k], (unsigned long long)(bprof_n - bprof_t)); \
+    bprof_t = bprof_n;                                             \
+  } while (0)
+#else
+#define BPROF_INIT
+#define BPROF(k)
+#endif
 
 struct Tri2 {
   d3 p[3], n[3];
@@ -52,6 +67,11 @@ cudaError_t k2_sqrt_table(int from_device, double* out30) {
   return cudaSuccess;
 }
 
+#ifndef SPOLY_TT_ARENA
+// TT: room for P^2 and Q^2 side by side (one batched product, then b in one two-term pass); 2 x 27.2 KB per block,
+// 4 blocks per SM (the register budget's limit) still fit the 228 KB of shared memory
+#define SPOLY_TT_ARENA 3400
+#endif
 // polynomial degrees of the chain X1 X2 (X = R reflection / T refraction)
 template <bool V1T, bool V2T>
 struct Deg2 {
@@ -63,7 +83,7 @@ struct Deg2 {
   static constexpr int G = (DB <= 15) ? 16 : 32;                               // lanes per system
   // shared-memory arena per group (doubles): persistent a, b, U, V, K + the build temporaries (peak) +
   // the v-root list; the n > 32 determinant scratch reuses the temporaries (TT only)
-  static constexpr int ARENA = (!V1T && !V2T) ? 640 : (!V1T ? 768 : (!V2T ? 1984 : 2560));
+  static constexpr int ARENA = (!V1T && !V2T) ? 640 : (!V1T ? 768 : (!V2T ? 1984 : SPOLY_TT_ARENA));
 };
 
 struct Sys2w {
@@ -81,6 +101,7 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
                         const SolveParams& prm, Sys2w& S) {
   using D = Deg2<V1T, V2T>;
   constexpr int DK = D::DK, DU = D::DU;
+  BPROF_INIT
   S.flags = 0;
   const bool front0 = dot(x0 - T1.p[0], T1.g()) > 0;
   S.eta0 = front0 ? prm.eta_front : prm.eta_back;
@@ -124,12 +145,17 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   WP dn = ar.poly(2), nn = ar.poly(2);
   wdot(g, dn, D0, N1, 1.0, false);
   wdot(g, nn, N1, N1, 1.0, false);
+  BPROF(0);
   WV Dt = ar.vec(DK);
   if (!V1T) {
     // Eq. 17: d~ = -2 (d0 . n) n + d0 n^2
+#ifndef SPOLY_NO_BATCH
+    wmul2x3(g, Dt, wv_rep(dn), N1, -2.0, wv_rep(nn), D0, 1.0, false);
+#else
     wmul2(g, Dt.x, dn, N1.x, -2.0, nn, D0.x, 1.0, false);
     wmul2(g, Dt.y, dn, N1.y, -2.0, nn, D0.y, 1.0, false);
     wmul2(g, Dt.z, dn, N1.z, -2.0, nn, D0.z, 1.0, false);
+#endif
   } else {
     // Eqs. 18-20 with sqrt(beta) ~ sqrt(s) (c0 s + c1 beta) / (s + d1 beta), denominator cleared
     const double ep = S.eta0 / S.eta1;
@@ -157,14 +183,23 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
     wlin1(g, sq, beta, c_sqrt_tab[piece][3], false);
     wadd0(g, sq, c_sqrt_tab[piece][2] * s);
     WV tang = ar.vec(3);  // nn D0 - dn N1
+#ifndef SPOLY_NO_BATCH
+    wmul2x3(g, tang, wv_rep(nn), D0, 1.0, wv_rep(dn), N1, -1.0, false);
+#else
     wmul2(g, tang.x, nn, D0.x, 1.0, dn, N1.x, -1.0, false);
     wmul2(g, tang.y, nn, D0.y, 1.0, dn, N1.y, -1.0, false);
     wmul2(g, tang.z, nn, D0.z, 1.0, dn, N1.z, -1.0, false);
+#endif
     const double k2 = -sigma * sqrt(s);
+#ifndef SPOLY_NO_BATCH
+    wmul2x3(g, Dt, wv_rep(den), tang, ep, wv_rep(sq), N1, k2, false);
+#else
     wmul2(g, Dt.x, den, tang.x, ep, sq, N1.x, k2, false);
     wmul2(g, Dt.y, den, tang.y, ep, sq, N1.y, k2, false);
     wmul2(g, Dt.z, den, tang.z, ep, sq, N1.z, k2, false);
+#endif
   }
+  BPROF(1);
   // rational coordinate mapping onto T_2 (Eqs. 13-16)
   const d3 f1 = T2.e1(), f2 = T2.e2(), r0 = T2.n[0], g1 = T2.n[1] - T2.n[0], g2 = T2.n[2] - T2.n[0];
   const bool face2 = T2.n[1].x == r0.x && T2.n[1].y == r0.y && T2.n[1].z == r0.z && T2.n[2].x == r0.x &&
@@ -173,11 +208,21 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   wlinear3(g, Sv, T1.p[0] - T2.p[0], e1, e2);
   WV Dxf2 = ar.vec(DK);
   wcross_c(g, Dxf2, Dt, f2);
-  wdot(g, S.U, Dxf2, Sv, 1.0, false);                                 // u~ = (d~ x e22) . (x1 - p20)
   wlin3(g, S.K, Dxf2.x, f1.x, Dxf2.y, f1.y, Dxf2.z, f1.z, false);     // kappa = (d~ x e22) . e21
   WV Sxf1 = ar.vec(1);
   wcross_c(g, Sxf1, Sv, f1);
+#ifndef SPOLY_NO_BATCH
+  {  // u~ = (d~ x e22) . (x1 - p20), v~ = ((x1 - p20) x e21) . d~, side by side
+    const WP c[2] = {S.U, S.V};
+    const WP a[2][3] = {{Dxf2.x, Dxf2.y, Dxf2.z}, {Sxf1.x, Sxf1.y, Sxf1.z}};
+    const WP b[2][3] = {{Sv.x, Sv.y, Sv.z}, {Dt.x, Dt.y, Dt.z}};
+    const double sc[2][3] = {{1, 1, 1}, {1, 1, 1}};
+    wmul_batch<G, 3, 2>(g, c, a, b, sc, false);
+  }
+#else
+  wdot(g, S.U, Dxf2, Sv, 1.0, false);                                 // u~ = (d~ x e22) . (x1 - p20)
   wdot(g, S.V, Sxf1, Dt, 1.0, false);                                 // v~ = ((x1 - p20) x e21) . d~
+#endif
   // kappa x_2 and kappa n_2
   WV X2 = ar.vec(DU), N2 = ar.vec(DU);
   wlin3(g, X2.x, S.K, T2.p[0].x, S.U, f1.x, S.V, f2.x, false);
@@ -197,20 +242,33 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
     wlin3(g, N2.y, S.K, r0.y, S.U, g1.y, S.V, g2.y, false);
     wlin3(g, N2.z, S.K, r0.z, S.U, g1.z, S.V, g2.z, false);
   }
+  BPROF(2);
   // a = ((X2 - K X1) x (x3 - X1)) . N2   (Eq. 6 at x_2, Eq. 23 first line)
   {
     const int m2 = ar.top;
     WV W = ar.vec(DU);
+#ifndef SPOLY_NO_BATCH
+    wlin1(g, W.x, X2.x, 1.0, false);
+    wlin1(g, W.y, X2.y, 1.0, false);
+    wlin1(g, W.z, X2.z, 1.0, false);
+    wmul1x3(g, W, wv_rep(S.K), X1, -1.0, true);
+#else
     wlin1(g, W.x, X2.x, 1.0, false); wmul1(g, W.x, S.K, X1.x, -1.0, true);
     wlin1(g, W.y, X2.y, 1.0, false); wmul1(g, W.y, S.K, X1.y, -1.0, true);
     wlin1(g, W.z, X2.z, 1.0, false); wmul1(g, W.z, S.K, X1.z, -1.0, true);
+#endif
     WV Y = ar.vec(1);
     wlinear3(g, Y, x3 - T1.p[0], -1.0 * e1, -1.0 * e2);
     WV Cc = ar.vec(DU + 1);
+#ifndef SPOLY_NO_BATCH
+    wmul2x3(g, Cc, WV{W.y, W.z, W.x}, WV{Y.z, Y.x, Y.y}, 1.0, WV{W.z, W.x, W.y}, WV{Y.y, Y.z, Y.x}, -1.0, false);
+#else
     wcross(g, Cc, W, Y);
+#endif
     wdot(g, S.a, Cc, N2, 1.0, false);
     ar.top = m2;
   }
+  BPROF(3);
   // D2 = K x3 - X2 (kappa d_2)
   WV D2 = ar.vec(DU);
   wlin2(g, D2.x, S.K, x3.x, X2.x, -1.0, false);
@@ -229,20 +287,28 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
     WV Tt = ar.vec(DU);
     wcross_c(g, Tt, N2, f1);
     WP p1 = ar.poly(DK + DU), p2 = ar.poly(2 * DU), p3 = ar.poly(DK + DU), p4 = ar.poly(2 * DU);
+#ifndef SPOLY_NO_BATCH
+    wdot4(g, p1, Dt, N2, p2, D2, Tt, p3, Dt, Tt, p4, D2, N2);
+#else
     wdot(g, p1, Dt, N2, 1.0, false);
     wdot(g, p2, D2, Tt, 1.0, false);
     wdot(g, p3, Dt, Tt, 1.0, false);
     wdot(g, p4, D2, N2, 1.0, false);
+#endif
     wmul2(g, S.b, p1, p2, 1.0, p3, p4, 1.0, false);
   } else {
     // b = eta1^2 D2^2 ((d~ x N2).l)^2 - eta2^2 d~^2 ((D2 x N2).l)^2   (Eq. 9 at x_2); (A x N2).l = A.(N2 x l)
     WV Nl = ar.vec(DU);
     wcross_c(g, Nl, N2, ell);
     WP P = ar.poly(DK + DU), Q = ar.poly(2 * DU), d22 = ar.poly(2 * DU), dt2 = ar.poly(2 * DK);
+#ifndef SPOLY_NO_BATCH
+    wdot4(g, P, Dt, Nl, Q, D2, Nl, d22, D2, D2, dt2, Dt, Dt);
+#else
     wdot(g, P, Dt, Nl, 1.0, false);
     wdot(g, Q, D2, Nl, 1.0, false);
     wdot(g, d22, D2, D2, 1.0, false);
     wdot(g, dt2, Dt, Dt, 1.0, false);
+#endif
     {  // only P, Q, D2^2, d~^2 are live from here
       double* dst = S.K.c + tri_n(DK);
       wmove(g, P, dst);
@@ -255,13 +321,31 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
       dst += tri_n(dt2.d);
       ar.top = (int)(dst - ar.base);
     }
-    WP PQ2 = ar.poly(4 * DU);
-    WP P2{PQ2.c, 2 * (DK + DU)};
-    wmul1(g, P2, P, P, 1.0, false);
-    wmul1(g, S.b, d22, P2, S.eta1 * S.eta1, false);
-    wmul1(g, PQ2, Q, Q, 1.0, false);
-    wmul1(g, S.b, dt2, PQ2, -S.eta2 * S.eta2, true);
+    BPROF(4);
+#ifndef SPOLY_NO_BATCH
+    if (D::ARENA - ar.top >= tri_n(2 * (DK + DU)) + tri_n(4 * DU)) {
+      // P^2 and Q^2 side by side, then b = eta1^2 d22 P^2 - eta2^2 dt2 Q^2 in one two-term pass (the same fma
+      // sequence per coefficient as two passes)
+      WP P2 = ar.poly(2 * (DK + DU)), Q2 = ar.poly(4 * DU);
+      {
+        const WP c[2] = {P2, Q2};
+        const WP a[2][1] = {{P}, {Q}}, b[2][1] = {{P}, {Q}};
+        const double sc[2][1] = {{1.0}, {1.0}};
+        wmul_batch<G, 1, 2>(g, c, a, b, sc, false);
+      }
+      wmul2(g, S.b, d22, P2, S.eta1 * S.eta1, dt2, Q2, -S.eta2 * S.eta2, false);
+    } else
+#endif
+    {
+      WP PQ2 = ar.poly(4 * DU);
+      WP P2{PQ2.c, 2 * (DK + DU)};
+      wmul1(g, P2, P, P, 1.0, false);
+      wmul1(g, S.b, d22, P2, S.eta1 * S.eta1, false);
+      wmul1(g, PQ2, Q, Q, 1.0, false);
+      wmul1(g, S.b, dt2, PQ2, -S.eta2 * S.eta2, true);
+    }
   }
+  BPROF(5);
   ar.top = mark;
   if (ar.overflow) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
@@ -298,6 +382,7 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
   S.da = g.imax(da);
   S.db = g.imax(db);
   S.n = max(S.da, S.db);
+  BPROF(6);
 #ifdef SPOLY_NO_TB
   S.tb = S.b.d;
 #else
@@ -312,6 +397,7 @@ __device__ bool build_w(const Grp<G>& g, Arena& ar, d3 x0, d3 x3, const Tri2& T1
     ar.top = mark;
   }
 #endif
+  BPROF(7);
   if (S.n == 0) {
     S.flags |= SPOLY_FLAG_DEGENERATE;
     return false;
@@ -531,6 +617,7 @@ __global__ void __launch_bounds__(kBuildWarps * 32, SPOLY_BUILD_MINB) k2_build(c
     Arena ar{base, 0, D::ARENA, false};
     Sys2w Sy;
     const bool ok = build_w<V1T, V2T, G>(g, ar, C.x0, C.x3, C.T1, C.T2, prm, Sy);
+    BPROF_INIT
     double* rec = recs + r * R::STRIDE;
     if (g.lane == 0) {
       rec[H_ETA0] = Sy.eta0;
@@ -562,6 +649,7 @@ __global__ void __launch_bounds__(kBuildWarps * 32, SPOLY_BUILD_MINB) k2_build(c
       for (int idx = g.lane; idx < tri_n(D::DK); idx += G) rec[R::K + idx] = Sy.K.c[idx];
     }
     g.sync();
+    BPROF(8);
   }
   group_counters(g, cnt, S);
 }
@@ -1332,6 +1420,7 @@ void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, c
                      const DeviceMesh& M, const double* ep, const double* inten, const SolveParams& prm,
                      const SolSink& S, K2Scratch& W, int nsm, cudaStream_t st) {
   if (!npairs) return;
+
   if (v1t && v2t)
     launch_k2<true, true>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
   else if (v1t)
@@ -1340,6 +1429,15 @@ void launch_solve_k2(int v1t, int v2t, const uint32_t* pq, const uint32_t* pt, c
     launch_k2<false, true>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
   else
     launch_k2<false, false>(pq, pt, vr, npairs, M, ep, inten, prm, S, W, nsm, st);
+#ifdef SPOLY_PROF_BUILD
+  unsigned long long h[16];
+  cudaStreamSynchronize(st);
+  if (cudaMemcpyFromSymbol(h, g_bprof, sizeof(h)) == cudaSuccess) {
+    fprintf(stderr, "k2_build section clocks (cumulative, lane 0):");
+    for (int i = 0; i < 9; ++i) fprintf(stderr, " %d:%.3e", i, (double)h[i]);
+    fprintf(stderr, "\n");
+  }
+#endif
 }
 
 }  // namespace spoly

@@ -101,6 +101,9 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 #ifndef SPOLY_WMUL_W
 #define SPOLY_WMUL_W 8  // output coefficients per lane chunk (A/B: 4)
 #endif
+#ifndef SPOLY_WMUL_SMALL_DC
+#define SPOLY_WMUL_SMALL_DC 12  // 4-wide chunks below this output degree; A/B on C4: none 1.81 s, 12 1.73 s, 20 1.74 s
+#endif
 #ifndef SPOLY_WMUL_INLINE
 #define SPOLY_WMUL_INLINE __device__ __forceinline__
 #endif
@@ -110,12 +113,12 @@ __device__ __forceinline__ void tadv(int d, int step, int& i, int& j0) {
 // and the b operands slide through a W-register window (one new load per step): 2 shared-memory loads per W
 // FMAs instead of 2 per FMA.  Out-of-row b positions read as 0 (predicated), so the W outputs may share the
 // union of their q ranges.
-template <int G, int K, int W>
-SPOLY_WMUL_INLINE void wmul_w(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
-                              bool acc) {
+template <int K, int W>
+SPOLY_WMUL_INLINE void wmul_core(int lane, int stride, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
+                                 bool acc) {
   const int dc = c.d;
   int i = 0, j0 = 0;
-  tadv<W>(dc, g.lane, i, j0);
+  tadv<W>(dc, lane, i, j0);
   while (i <= dc) {
     const int rowlen = dc - i + 1;
     double* cp = c.c + poff(dc, i);
@@ -176,8 +179,13 @@ SPOLY_WMUL_INLINE void wmul_w(const Grp<G>& g, WP c, const WP (&a)[K], const WP 
 #pragma unroll
     for (int k = 0; k < W; ++k)
       if (j0 + k < rowlen) cp[j0 + k] = out[k];
-    tadv<W>(dc, G, i, j0);
+    tadv<W>(dc, stride, i, j0);
   }
+}
+template <int G, int K, int W>
+__device__ __forceinline__ void wmul_w(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
+                                       bool acc) {
+  wmul_core<K, W>(g.lane, G, c, a, b, s, acc);
   g.sync();
 }
 // outputs with few coefficients use 4-wide chunks, so more lanes get one (the build's small products left most of
@@ -185,9 +193,6 @@ SPOLY_WMUL_INLINE void wmul_w(const Grp<G>& g, WP c, const WP (&a)[K], const WP 
 template <int G, int K>
 __device__ __forceinline__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], const WP (&b)[K], const double (&s)[K],
                                      bool acc) {
-#ifndef SPOLY_WMUL_SMALL_DC
-#define SPOLY_WMUL_SMALL_DC 12  // A/B on C4: none 1.81 s, 12 1.73 s, 20 1.74 s (outputs bit-identical)
-#endif
 #if SPOLY_WMUL_SMALL_DC > 0
   if (c.d < SPOLY_WMUL_SMALL_DC) {
     wmul_w<G, K, 4>(g, c, a, b, s, acc);
@@ -196,6 +201,86 @@ __device__ __forceinline__ void wmul(const Grp<G>& g, WP c, const WP (&a)[K], co
 #endif
   wmul_w<G, K, SPOLY_WMUL_W>(g, c, a, b, s, acc);
 }
+// NB independent products at once, G / NB lanes each (lane l works on product l / (G / NB)): the build's medium
+// products have fewer 8-wide output chunks than lanes, and NB of them side by side fill the group with one sync.
+// A product with c.d < 0 is a placeholder (no chunks).  Each output chunk is still computed once by the same
+// arithmetic as wmul's.
+__device__ __forceinline__ WP sel_wp(bool p, WP x, WP y) {
+  WP r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %2, 0;\n\tselp.b64 %0, %3, %4, q;\n\tselp.b32 %1, %5, %6, q;\n\t}"
+      : "=l"(r.c), "=r"(r.d) : "r"((int)p), "l"(x.c), "l"(y.c), "r"(x.d), "r"(y.d));
+  return r;
+}
+__device__ __forceinline__ double sel_d(bool p, double x, double y) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.s32 q, %1, 0;\n\tselp.f64 %0, %2, %3, q;\n\t}" : "=d"(r) : "r"((int)p), "d"(x), "d"(y));
+  return r;
+}
+template <int G, int K, int NB>
+__device__ __forceinline__ void wmul_batch(const Grp<G>& g, const WP (&c)[NB], const WP (&a)[NB][K],
+                                           const WP (&b)[NB][K], const double (&s)[NB][K], bool acc) {
+  constexpr int SG = G / NB;
+  const int job = g.lane / SG;
+  WP cc = c[0], aa[K], bb[K];
+  double ss[K];
+#pragma unroll
+  for (int k = 0; k < K; ++k) {
+    aa[k] = a[0][k];
+    bb[k] = b[0][k];
+    ss[k] = s[0][k];
+  }
+#pragma unroll
+  for (int q = 1; q < NB; ++q) {
+    const bool m = job == q;
+    cc = sel_wp(m, c[q], cc);
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+      aa[k] = sel_wp(m, a[q][k], aa[k]);
+      bb[k] = sel_wp(m, b[q][k], bb[k]);
+      ss[k] = sel_d(m, s[q][k], ss[k]);
+    }
+  }
+#if SPOLY_WMUL_SMALL_DC > 0
+  if (c[0].d < SPOLY_WMUL_SMALL_DC)
+    wmul_core<K, 4>(g.lane % SG, SG, cc, aa, bb, ss, acc);
+  else
+#endif
+    wmul_core<K, SPOLY_WMUL_W>(g.lane % SG, SG, cc, aa, bb, ss, acc);
+  g.sync();
+}
+template <int G>
+__device__ __forceinline__ void wmul1x3(const Grp<G>& g, const WV& R, const WV& A, const WV& B, double s0, bool acc) {
+  const WP none{R.x.c, -1};
+  const WP c[4] = {R.x, R.y, R.z, none};
+  const WP a[4][1] = {{A.x}, {A.y}, {A.z}, {A.x}};
+  const WP b[4][1] = {{B.x}, {B.y}, {B.z}, {B.x}};
+  const double s[4][1] = {{s0}, {s0}, {s0}, {s0}};
+  wmul_batch<G, 1, 4>(g, c, a, b, s, acc);
+}
+// three (or four) dot products c_q = s_q A_q . B_q side by side
+template <int G>
+__device__ __forceinline__ void wdot4(const Grp<G>& g, WP c0, const WV& A0, const WV& B0, WP c1, const WV& A1, const WV& B1,
+                                      WP c2, const WV& A2, const WV& B2, WP c3, const WV& A3, const WV& B3) {
+  const WP c[4] = {c0, c1, c2, c3};
+  const WP a[4][3] = {{A0.x, A0.y, A0.z}, {A1.x, A1.y, A1.z}, {A2.x, A2.y, A2.z}, {A3.x, A3.y, A3.z}};
+  const WP b[4][3] = {{B0.x, B0.y, B0.z}, {B1.x, B1.y, B1.z}, {B2.x, B2.y, B2.z}, {B3.x, B3.y, B3.z}};
+  const double s[4][3] = {{1, 1, 1}, {1, 1, 1}, {1, 1, 1}, {1, 1, 1}};
+  wmul_batch<G, 3, 4>(g, c, a, b, s, false);
+}
+// the three components of sum_k s_k a_k(x) b_k(x) (x = x, y, z) side by side: R.x = s0 a0.x b0.x + s1 a1.x b1.x etc.
+// with per-component operands given as WVs (a WP repeated in all three for a scalar factor)
+template <int G>
+__device__ __forceinline__ void wmul2x3(const Grp<G>& g, const WV& R, const WV& A0, const WV& B0, double s0,
+                                        const WV& A1, const WV& B1, double s1, bool acc) {
+  const WP none{R.x.c, -1};
+  const WP c[4] = {R.x, R.y, R.z, none};
+  const WP a[4][2] = {{A0.x, A1.x}, {A0.y, A1.y}, {A0.z, A1.z}, {A0.x, A1.x}};
+  const WP b[4][2] = {{B0.x, B1.x}, {B0.y, B1.y}, {B0.z, B1.z}, {B0.x, B1.x}};
+  const double s[4][2] = {{s0, s1}, {s0, s1}, {s0, s1}, {s0, s1}};
+  wmul_batch<G, 2, 4>(g, c, a, b, s, acc);
+}
+__device__ __forceinline__ WV wv_rep(WP p) { return {p, p, p}; }
+
 template <int G>
 __device__ __forceinline__ void wmul1(const Grp<G>& g, WP c, WP a, WP b, double s, bool acc) {
   const WP A[1] = {a}, B[1] = {b};
@@ -436,9 +521,12 @@ __device__ __forceinline__ double rowT(const double* __restrict__ AT, int D, int
   return s;
 }
 
+#ifndef SPOLY_WDET_INLINE
+#define SPOLY_WDET_INLINE __device__
+#endif
 // det sign for n <= G from the transposed blocks (the group evaluates the slices, lane l row l)
 template <int G, int NR, int NCF = 0>
-__device__ int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* BT, int DB, int n, double v,
+SPOLY_WDET_INLINE int wdet_T(const Grp<G>& g, const double* AT, int DA, const double* BT, int DB, int n, double v,
                       double* lg) {
   const int l = g.lane;
   const double as = rowT<NR>(AT, DA, l, v), bs = rowT<NR>(BT, DB, l, v);
