@@ -522,7 +522,9 @@ __device__ __forceinline__ double rowT(const double* __restrict__ AT, int D, int
 }
 
 #ifndef SPOLY_WDET_INLINE
-#define SPOLY_WDET_INLINE __device__
+// one out-of-line copy per class: the scan calls it from three sites (first sample, next sample, bisection);
+// A/B: C5 solve 2.01 -> 1.85 s (instruction-cache misses of the 20-row class), C4 -0.5%, bit-identical
+#define SPOLY_WDET_INLINE __device__ __noinline__
 #endif
 // det sign for n <= G from the transposed blocks (the group evaluates the slices, lane l row l)
 template <int G, int NR, int NCF = 0>
