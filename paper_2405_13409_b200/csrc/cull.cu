@@ -1421,7 +1421,11 @@ __device__ uint32_t children_mask_f(const f3 P1[3], const f3 N1[3], float s1, co
     ok3[c] = exact_cone_f<3>(d3_, S3, a3[c], c3[c]);
   }
   uint32_t m = 0;
+#ifdef SPOLY_REFINE_ROLL
+#pragma unroll 1
+#else
 #pragma unroll
+#endif
   for (int ia = 0; ia < 4; ++ia)
 #pragma unroll 1
   for (int ib = 0; ib < 4; ++ib) {
