@@ -14,6 +14,8 @@
 #include "kernels.cuh"
 #include "solve_k1.cuh"
 
+#include <cstdio>
+
 namespace spoly {
 
 template <bool TC>
@@ -770,6 +772,19 @@ __global__ void SPOLY_PATH_BOUNDS k1_path(const uint32_t* __restrict__ pq, const
 #define SPOLY_FAST_MINB 4  // <= 128 registers (A/B: 222 unbounded -> 1.59, 128 -> 1.54 ms on C2)
 #endif
 #define SPOLY_FAST_BOUNDS __launch_bounds__(128, SPOLY_FAST_MINB)
+#ifdef SPOLY_PROF_FAST  // section clocks of k1_path_fast (lane 0 of each warp; diagnostic only)
+__device__ unsigned long long g_fprof[8];
+#define FPROF_INIT long long fprof_t = clock64();
+#define FPROF(k)                                                                          \
+  do {                                                                                    \
+    const long long fprof_n = clock64();                                                  \
+    if (lane == 0) atomicAdd(&g_fprof[k], (unsigned long long)(fprof_n - fprof_t));        \
+    fprof_t = fprof_n;                                                                    \
+  } while (0)
+#else
+#define FPROF_INIT
+#define FPROF(k)
+#endif
 template <bool TC>
 __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, const uint32_t* __restrict__ pt,
                                                     const TriRec* __restrict__ tris, const double* __restrict__ ep,
@@ -782,6 +797,7 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
   const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nw = ((uint64_t)gridDim.x * blockDim.x) >> 5;
   const int lane = threadIdx.x & 31;
+  FPROF_INIT
   for (uint64_t base = gw * 32; base < n; base += nw * 32) {
     const uint64_t i = base + lane;
     const bool active = i < n;
@@ -798,6 +814,7 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
       load_pair(pq, pt, tris, ep, pair, P, N, x0, x2, q);
       Sys1<TC> Sys;
       build_system<TC>(x0, x2, P, N, prm, Sys);  // bit-identical to phase 1 (known non-degenerate)
+      FPROF(0);
       cnt[C_REBUILDS]++;
       const double I = inten ? __ldg(inten + q) : 1.0;
       const d3 e1o = P[1] - P[0], e2o = P[2] - P[0];
@@ -813,8 +830,10 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
           continue;
         }
         cnt[C_REFINED]++;
+        FPROF(1);
         double fau, fav, fbu, fbv;
         refine_ab<TC>(Sys.A, Sys.B, ua[iu], vs, us, vv, fau, fav, fbu, fbv);
+        FPROF(2);
         const double ur = Sys.relabel ? vv : us, vr_ = Sys.relabel ? us : vv;  // original labeling
         const d3 x1 = P[0] + ur * e1o + vr_ * e2o;
         const d3 nx = N[0] + ur * (N[1] - N[0]) + vr_ * (N[2] - N[0]);
@@ -842,7 +861,9 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
           cnt[C_REJ_SIDE]++;
           continue;
         }
+        FPROF(3);
         const double J1 = jacobian_k1(TC, x0, x2, x1, e1o, e2o, N[1] - N[0], N[2] - N[0], nx, Sys.eta1, Sys.eta0);
+        FPROF(4);
         su[nsol] = ur;
         sv[nsol] = vr_;
         sc[nsol] = J1 > 0 ? I / J1 : 0.0;
@@ -852,6 +873,7 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
         cnt[C_ADMISSIBLE]++;
       }
     }
+    FPROF(5);
     emit_flag(active && flags != 0, flags, pair, S);
     uint32_t ex;
     const unsigned long long b = warp_alloc(S.count, (uint32_t)nsol, &ex);
@@ -866,6 +888,7 @@ __global__ void SPOLY_FAST_BOUNDS k1_path_fast(const uint32_t* __restrict__ pq, 
         S.resid[p] = sr[s2];
       }
     }
+    FPROF(6);
   }
   flush_counters(S, cnt);
 }
@@ -905,6 +928,15 @@ void launch_solve_k1(int phase, int refract, const uint32_t* pq, const uint32_t*
       k1_path_fast<false><<<nsm * SPOLY_FAST_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
       k1_path<false><<<nsm * SPOLY_PATH_GRID, threads, 0, st>>>(pq, pt, M.tris, ep, inten, prm, S, J);
     }
+#ifdef SPOLY_PROF_FAST
+    unsigned long long h[8];
+    cudaStreamSynchronize(st);
+    if (cudaMemcpyFromSymbol(h, g_fprof, sizeof(h)) == cudaSuccess) {
+      fprintf(stderr, "k1_path_fast section clocks (cumulative, lane 0):");
+      for (int k = 0; k < 7; ++k) fprintf(stderr, " %d:%.3e", k, (double)h[k]);
+      fprintf(stderr, "\n");
+    }
+#endif
   }
 }
 
