@@ -1504,7 +1504,10 @@ __device__ __forceinline__ void dec_node(uint64_t c, int& u, int& v, int& s) {
   s = ((c >> 10) & 1) ? 1 : -1;
 }
 
-__global__ void __launch_bounds__(128) k_refine_level(int level, int last, const uint32_t* __restrict__ pq,
+#ifndef SPOLY_REFINE_MINB
+#define SPOLY_REFINE_MINB 1
+#endif
+__global__ void __launch_bounds__(128, SPOLY_REFINE_MINB) k_refine_level(int level, int last, const uint32_t* __restrict__ pq,
                                                       const uint32_t* __restrict__ pt, uint64_t npairs,
                                                       const TriRec* __restrict__ tris, const double* __restrict__ ep,
                                                       int v1t, int v2t, float ef, float eb,
