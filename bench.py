@@ -278,11 +278,13 @@ def main():
     w = W.CONFIGS[args.config](**kw)
     nq_full = w.nqueries
     if world > 1:
-        # strong scaling of ONE frame: the frame's res x res query grid in 64 x 64 tiles, tile t ->
+        # strong scaling of ONE frame: the frame's res x res query grid in 64 x 64 tiles (halved while
+        # there are fewer than 4 tiles per rank), tile t ->
         # rank t mod world; every rank uploads the whole mesh and solves its tiles; no collective inside the solve
         from paper_2405_13409_b200 import dist as D
         side = int(round(nq_full ** 0.5))
-        shard_idx = (D.shard_grid_tiles(side, side, world, rank) if side * side == nq_full
+        shard_idx = (D.shard_grid_tiles(side, side, world, rank, D.grid_tile_side(side, side, world))
+                     if side * side == nq_full
                      else D.shard_tiles(nq_full, world, rank))
         w = w.subset(shard_idx)
     chain = w.chain
@@ -416,7 +418,8 @@ def main():
                    "queries_per_gpu": w.nqueries, "triangles": w.mesh.ntris, "chain": chain,
                    "queries_total": int(nq_full),
                    "l2": "flushed between timed steps (256 MB write)",
-                   "parallelism": ("one frame, 64x64 query tiles round-robin over %d ranks (strong scaling)" % world
+                   "parallelism": ("one frame, query tiles (64x64, halved for small frames) round-robin over %d ranks "
+                                   "(strong scaling)" % world
                                    if world > 1 else "single GPU")},
         "paths_per_step_per_gpu": reports[-1]["n_solutions"], "pairs_per_step_per_gpu": reports[-1]["n_pairs_in"],
         "counters": {k: reports[-1][k] for k in ("n_systems", "n_vroots", "n_candidates", "n_admissible", "n_flagged",

@@ -19,6 +19,14 @@ from __future__ import annotations
 import numpy as np
 
 
+def grid_tile_side(width: int, height: int, world: int, tile: int = 64, min_tile: int = 8) -> int:
+    """64, halved while the frame would give fewer than 4 tiles per rank (a 128 x 128 frame has only 4 tiles of 64:
+    over 8 ranks half of them would idle), down to `min_tile`."""
+    while tile > min_tile and ((width + tile - 1) // tile) * ((height + tile - 1) // tile) < 4 * world:
+        tile //= 2
+    return tile
+
+
 def shard_grid_tiles(width: int, height: int, world: int, rank: int, tile: int = 64) -> np.ndarray:
     """Query indices (row-major, q = y * width + x) owned by `rank`: tile (ty, tx) has index t = ty * ntx + tx
     and goes to rank t % world; within a tile, row-major.  Ragged edge tiles are kept whole."""

@@ -44,6 +44,19 @@ def test_shard_grid_tiles_partition():
                 assert y.max() - y.min() < 64 and x.max() - x.min() < 64  # first tile is a 64 x 64 block
 
 
+def test_grid_tile_side_keeps_ranks_busy():
+    """small frames get smaller tiles (at least 4 per rank, down to 8 x 8); large frames keep 64 x 64"""
+    assert D.grid_tile_side(1024, 1024, 8) == 64
+    assert D.grid_tile_side(256, 256, 8) == 32      # 16 tiles of 64 < 32 -> 64 tiles of 32
+    assert D.grid_tile_side(128, 128, 8) == 16      # C4: 256 tiles of 16 x 16
+    assert D.grid_tile_side(32, 32, 8) == 8
+    for w, world in [(128, 8), (256, 4), (100, 3)]:
+        t = D.grid_tile_side(w, w, world)
+        parts = [D.shard_grid_tiles(w, w, world, r, t) for r in range(world)]
+        assert np.array_equal(np.sort(np.concatenate(parts)), np.arange(w * w))
+        assert min(len(p) for p in parts) > 0
+
+
 def _worker(rank, world, port, ret):
     import torch
     import torch.distributed as dist
