@@ -36,12 +36,14 @@ def _solve(ctx, torch, chain, ep):
     return out
 
 
-@pytest.mark.parametrize("name,alpha,tol", [("C2", 0.1, 1e-5), ("C3", 0.05, 1e-5), ("C5RR", 0.03, 1e-4)])
+@pytest.mark.parametrize("name,alpha,tol", [("C2", 0.1, 1e-5), ("C3", 0.05, 1e-5), ("C5RR", 0.03, 1e-4),
+                                            ("C4", 0.02, 1e-4)])
 def test_glossy_solve_parity(sp, torch_cuda, orc, name, alpha, tol):
     # one offset sample on a one-bounce glint / caustic subset and on the two-bounce mirrors: the GPU solve after
     # spoly_set_normal_offsets equals the oracle's solve of the perturbed (de-indexed) surface
     w = {"C2": lambda: W.glints_c2(res=24), "C3": lambda: W.pool_c3(res=32),
-         "C5RR": lambda: W.mirrors_rr(res=16, quads=16).subset(np.arange(0, 256, 2))}[name]()
+         "C5RR": lambda: W.mirrors_rr(res=16, quads=16).subset(np.arange(0, 256, 2)),
+         "C4": lambda: W.sphere_c4(res=32).subset(np.arange(0, 1024, 32))}[name]()
     sl = W.beckmann_slopes(11, 1, w.mesh.ntris, alpha)[0]
     ctx = sp.Context(0)
     ctx.upload_mesh(w.mesh)
